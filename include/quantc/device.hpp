@@ -1,0 +1,47 @@
+// quantc/device.hpp — B200 extension: device context and errors.
+//
+// Not part of the reference API.  One process drives one GPU (the device is
+// picked from QUANTC_DEVICE, else LOCAL_RANK, else 0); all engine work is
+// issued on one stream of that device with stream-ordered allocation.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace quantc {
+
+class DeviceError : public std::runtime_error {
+ public:
+  explicit DeviceError(const std::string& what) : std::runtime_error(what) {}
+};
+
+namespace device {
+
+// Engine selection for sim-quant evaluation (CandidateEvaluator, predict_top1
+// with a binding).  kExact: FP64 exact-order conv/dense everywhere
+// (bit-identical to the reference).  kFast: int8 tcgen05 GEMMs wherever both
+// MAC operands are int8-grid simulated-quantize outputs (bit-identical when
+// thresholds are powers of two; documented tolerance otherwise).  kAuto: kFast
+// only where it is provably bit-identical, kExact elsewhere.
+enum class EngineMode { kExact = 0, kFast = 1, kAuto = 2 };
+
+void set_engine_mode(EngineMode m);
+EngineMode engine_mode();
+
+int current_device();
+void* stream();  // cudaStream_t of the engine
+void synchronize();
+size_t memory_budget_bytes();  // per-batch activation budget
+
+// Counters (for bench / profiling evidence).
+struct Counters {
+  int64_t kernel_launches = 0;
+  int64_t tcgen05_gemms = 0;
+  int64_t f64_convs = 0;
+};
+Counters& counters();
+
+}  // namespace device
+}  // namespace quantc

@@ -1,0 +1,80 @@
+/*
+ * quantc_cuda.h — the thin C-ABI between the quantc C++ host and the sm_100a
+ * kernels (north_star: "The host side stays C++ and calls CUDA through a thin
+ * C-ABI layer").  Plain device pointers, sizes and an explicit cudaStream_t
+ * (passed as void*, NULL = the engine stream); status codes as in
+ * quantc_capi.h, message via qc_last_error().
+ *
+ * Each entry point replaces one hot loop of the reference CPU implementation:
+ *   qcu_sim_quant        simulate.cpp:64-87     simulated_quantize over a tensor
+ *   qcu_minmax           calibration.cpp:70-79  per-edge exact extrema
+ *   qcu_histogram        calibration.cpp:97-105 |v| histogram against absmax
+ *   qcu_kl_sweep         calibration.cpp:161-206 KL threshold sweep, many edges
+ *   qcu_conv2d_f64acc    interpreter.cpp:210-236 fp32 conv/dense, double acc
+ *   qcu_conv2d_int       interpreter.cpp:238-264 integer conv/dense + clamp/trap
+ *   qcu_requantize       interpreter.cpp:464-482 fixed-point requantize
+ *   qcu_gemm_s8          int8 x int8 -> int32 on tcgen05 with the fused
+ *                        sim-quant conv epilogue (y = float(acc*scale+bias))
+ */
+#ifndef QUANTC_CUDA_H_
+#define QUANTC_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "quantc_capi.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* x, y: float32 device buffers of n elements (y may alias x). */
+int qcu_sim_quant(const float* x, float* y, int64_t n, const qc_qparams* p, void* stream);
+
+/* out_minmax: 2 doubles on the device (min, max) of the n values. */
+int qcu_minmax(const float* x, int64_t n, double* out_minmax, void* stream);
+
+/* counts: `bins` uint64 on the device, accumulated (+=) */
+int qcu_histogram(const float* x, int64_t n, double absmax, int bins, uint64_t* counts,
+                  void* stream);
+
+/* counts: [n_edges][bins] int64 on the device; best_i (int32) and best_kl
+ * (double) per edge on the device.  threshold = absmax * best_i / bins. */
+int qcu_kl_sweep(const int64_t* counts, int n_edges, int bins, int target_bit, int* best_i,
+                 double* best_kl, void* stream);
+
+/* NCHW x [N,C,H,W], OIHW w, bias [O] (may be NULL), y [N,O,OH,OW]; dense is
+ * H=W=KH=KW=1. */
+int qcu_conv2d_f64acc(const float* x, const float* w, const float* bias, float* y, int N, int C,
+                      int H, int W, int O, int KH, int KW, int sh, int sw, int ph, int pw,
+                      void* stream);
+
+/* int32-storage operands; acc_dtype QC_I16/QC_I32; trap != 0 reports the
+ * lowest overflowing flat index through *overflow_flat (-1 if none). */
+int qcu_conv2d_int(const int32_t* x, const int32_t* w, const int32_t* bias, int32_t* y, int N,
+                   int C, int H, int W, int O, int KH, int KW, int sh, int sw, int ph, int pw,
+                   int64_t zp0, int64_t zp1, int acc_dtype, int trap, int64_t* overflow_flat,
+                   void* stream);
+
+int qcu_requantize(const int32_t* x, int32_t* y, int64_t n, int64_t multiplier, int shift,
+                   int64_t in_zp, int64_t out_zp, int64_t qmin, int64_t qmax, void* stream);
+
+/* A [M][K], B [N][K] int8 row-major (K multiple of 128); y float NCHW with
+ * OHW pixels per image: y[(m/OHW)*N + n][m%OHW] = float(acc*scale + bias[n]). */
+int qcu_gemm_s8(const int8_t* A, const int8_t* B, int M, int N, int K, double scale,
+                const float* bias, float* y, int OHW, void* stream);
+
+int qcu_synchronize(void* stream);
+const char* qcu_last_error(void);
+/* 1 when the tcgen05 path can run on the current device */
+int qcu_tcgen05_available(void);
+/* engine mode for sim-quant evaluation: 0 exact, 1 fast, 2 auto */
+int qcu_set_engine_mode(int mode);
+/* counters since load: kernel launches issued by the engine, tcgen05 GEMMs */
+int qcu_counters(int64_t* steps, int64_t* tcgen05_gemms, int64_t* f64_convs);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QUANTC_CUDA_H_ */

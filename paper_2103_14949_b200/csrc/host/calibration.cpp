@@ -1,0 +1,288 @@
+// calibration.cpp — statistics collection and threshold estimation on the
+// GPU (reference calibration.cpp:14-234).
+//
+// collect_stats keeps the reference's two-pass structure (exact extrema, then
+// histograms against the final absmax) but runs each pass as batched GPU
+// forwards with the statistics kernels hooked onto the producing steps.  When
+// the target activations of the whole calibration set fit in the memory
+// budget, pass 1 keeps them resident and pass 2 reads them back instead of
+// recomputing the forward (the reference recomputes, calibration.cpp:95-96;
+// the values are identical either way).  Constant (weight) edges are reduced
+// once and their counts scaled by the sample count — the reference
+// re-histograms the same tensor for every sample, so the counts are equal.
+#include "quantc/calibration.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <unordered_map>
+
+#include "dataset.hpp"
+#include "engine.hpp"
+#include "quantc/device.hpp"
+
+namespace quantc {
+
+namespace {
+cudaStream_t S() { return static_cast<cudaStream_t>(device::stream()); }
+void ok(cudaError_t e) {
+  if (e != cudaSuccess) throw DeviceError(cudaGetErrorString(e));
+}
+}  // namespace
+
+int64_t EdgeStats::total_count() const {
+  int64_t n = 0;
+  for (int64_t c : counts) n += c;
+  return n;
+}
+
+double EdgeStats::bin_upper_edge(int i) const {
+  return absmax * (static_cast<double>(i + 1) / static_cast<double>(counts.size()));
+}
+
+CalibrationStats collect_stats(const Graph& g, const Dataset& dataset, int bins,
+                               const std::vector<int>& edge_indices, int workers) {
+  (void)workers;
+  if (dataset.empty()) throw CalibrationError("calibration dataset is empty");
+  if (bins < 2) throw CalibrationError("histogram needs at least 2 bins");
+  const std::vector<Edge> edges = edge_order(g);
+  std::vector<int> targets = edge_indices;
+  if (targets.empty()) {
+    for (size_t k = 0; k < edges.size(); ++k) targets.push_back(static_cast<int>(k));
+  }
+  for (int k : targets) {
+    if (k < 0 || k >= static_cast<int>(edges.size())) {
+      throw CalibrationError("edge index " + std::to_string(k) + " out of range");
+    }
+  }
+
+  engine::Plan plan(g);
+  gpu::DeviceDataset dd(g, dataset);
+  const int64_t N = dd.size();
+
+  // one statistics slot per distinct producer step
+  std::unordered_map<int, int> slot_of_step;
+  std::vector<int> slot_step;
+  std::vector<int> edge_slot(targets.size());
+  for (size_t t = 0; t < targets.size(); ++t) {
+    const int step = plan.step_of(edges[static_cast<size_t>(targets[t])].src.node);
+    auto it = slot_of_step.find(step);
+    if (it == slot_of_step.end()) {
+      it = slot_of_step.emplace(step, static_cast<int>(slot_step.size())).first;
+      slot_step.push_back(step);
+    }
+    edge_slot[t] = it->second;
+  }
+  const int n_slots = static_cast<int>(slot_step.size());
+
+  auto keys = engine::device_alloc(static_cast<size_t>(n_slots) * 16);
+  auto* k64 = static_cast<unsigned long long*>(keys.get());
+  kern::minmax_init(k64, n_slots, S());
+
+  // resident-activation cache for pass 2
+  int64_t per_sample_bytes = 0;
+  for (int st : slot_step) {
+    if (plan.batched(st)) per_sample_bytes += shape_numel(plan.shape(st)) * 4;
+  }
+  const bool cache = per_sample_bytes * N <= static_cast<int64_t>(device::memory_budget_bytes());
+  std::vector<std::vector<std::pair<int, engine::DevTensor>>> cached;  // per batch
+
+  const int batch = plan.batch_for(N);
+  using Hook = std::function<void(int step, const engine::DevTensor&, int b, int64_t bi)>;
+  auto forward = [&](const Hook& hook) {
+    int64_t bi = 0;
+    for (int64_t s0 = 0; s0 < N; s0 += batch, ++bi) {
+      const int b = static_cast<int>(std::min<int64_t>(batch, N - s0));
+      engine::RunSpec spec;
+      spec.batch = b;
+      for (size_t k = 0; k < dd.num_inputs(); ++k) spec.inputs.push_back(dd.input(k, s0));
+      spec.on_value = [&, b, bi](int step, const engine::DevTensor& v) {
+        if (slot_of_step.count(step)) hook(step, v, b, bi);
+      };
+      engine::run(plan, spec);
+    }
+  };
+  auto require_float = [](const engine::DevTensor& v) {
+    if (!v.dtype.is_float()) throw std::logic_error("floats() on " + v.dtype.name() + " tensor");
+  };
+
+  // pass 1: exact extrema (calibration.cpp:62-91)
+  std::vector<int> batch_size_of;
+  forward([&](int step, const engine::DevTensor& v, int b, int64_t bi) {
+    require_float(v);
+    const int slot = slot_of_step.at(step);
+    if (v.batched || bi == 0) kern::minmax_accumulate(v.f(), v.numel(b), k64 + 2 * slot, S());
+    if (cache) {
+      if (static_cast<int64_t>(cached.size()) <= bi) {
+        cached.resize(static_cast<size_t>(bi) + 1);
+        batch_size_of.resize(static_cast<size_t>(bi) + 1);
+      }
+      batch_size_of[static_cast<size_t>(bi)] = b;
+      if (v.batched || bi == 0) cached[static_cast<size_t>(bi)].push_back({step, v});
+    }
+  });
+  std::vector<double> mm(static_cast<size_t>(n_slots) * 2);
+  {
+    auto dmm = engine::device_alloc(mm.size() * 8);
+    kern::minmax_decode(k64, static_cast<double*>(dmm.get()), n_slots, S());
+    ok(cudaMemcpyAsync(mm.data(), dmm.get(), mm.size() * 8, cudaMemcpyDeviceToHost, S()));
+    device::synchronize();
+  }
+  std::vector<double> absmax(static_cast<size_t>(n_slots));
+  for (int s = 0; s < n_slots; ++s) {
+    absmax[static_cast<size_t>(s)] =
+        std::max(std::fabs(mm[2 * static_cast<size_t>(s)]), std::fabs(mm[2 * static_cast<size_t>(s) + 1]));
+  }
+
+  // pass 2: histograms against the final absmax (calibration.cpp:93-113)
+  auto counts = engine::device_alloc(static_cast<size_t>(n_slots) * bins * 8);
+  ok(cudaMemsetAsync(counts.get(), 0, static_cast<size_t>(n_slots) * bins * 8, S()));
+  auto* c64 = static_cast<unsigned long long*>(counts.get());
+  auto hist = [&](int step, const engine::DevTensor& v, int b, int64_t bi) {
+    const int slot = slot_of_step.at(step);
+    if (v.batched) {
+      kern::histogram_accumulate(v.f(), v.numel(b), absmax[static_cast<size_t>(slot)], bins,
+                                 c64 + static_cast<int64_t>(slot) * bins, 1ull, S());
+    } else if (bi == 0) {
+      kern::histogram_accumulate(v.f(), v.numel(b), absmax[static_cast<size_t>(slot)], bins,
+                                 c64 + static_cast<int64_t>(slot) * bins,
+                                 static_cast<unsigned long long>(N), S());
+    }
+  };
+  if (cache) {
+    for (size_t bi = 0; bi < cached.size(); ++bi) {
+      for (auto& [step, v] : cached[bi]) hist(step, v, batch_size_of[bi], static_cast<int64_t>(bi));
+      cached[bi].clear();
+    }
+  } else {
+    forward(hist);
+  }
+  std::vector<int64_t> hc(static_cast<size_t>(n_slots) * bins);
+  ok(cudaMemcpyAsync(hc.data(), counts.get(), hc.size() * 8, cudaMemcpyDeviceToHost, S()));
+  device::synchronize();
+
+  CalibrationStats stats;
+  for (size_t t = 0; t < targets.size(); ++t) {
+    const size_t s = static_cast<size_t>(edge_slot[t]);
+    EdgeStats e;
+    e.min = mm[2 * s];
+    e.max = mm[2 * s + 1];
+    e.absmax = absmax[s];
+    e.sample_count = N;
+    e.counts.assign(hc.begin() + static_cast<int64_t>(s) * bins,
+                    hc.begin() + static_cast<int64_t>(s + 1) * bins);
+    stats.per_edge[targets[t]] = std::move(e);
+  }
+  return stats;
+}
+
+double threshold_max(const EdgeStats& stats) {
+  return stats.absmax > 0.0 ? stats.absmax : kDegenerateThreshold;
+}
+
+double threshold_quantile(const EdgeStats& stats, double q) {
+  if (!(q > 0.0) || q > 1.0) throw CalibrationError("quantile must be in (0, 1]");
+  if (stats.absmax <= 0.0) return kDegenerateThreshold;
+  const int64_t total = stats.total_count();
+  if (total == 0) throw CalibrationError("histogram is empty");
+  int64_t cum = 0;
+  for (size_t b = 0; b < stats.counts.size(); ++b) {
+    cum += stats.counts[b];
+    if (static_cast<double>(cum) >= q * static_cast<double>(total)) {
+      return stats.bin_upper_edge(static_cast<int>(b));
+    }
+  }
+  return stats.absmax;
+}
+
+namespace {
+
+// Validation + degenerate handling of reference calibration.cpp:161-169.
+// Returns true when the edge needs the KL sweep.
+bool kl_precheck(const EdgeStats& s, int target_bit, double* degenerate) {
+  if (target_bit < 1 || target_bit > 16) throw CalibrationError("target_bit out of range");
+  const int bins = static_cast<int>(s.counts.size());
+  if (bins < (1 << target_bit)) {
+    throw CalibrationError("histogram has fewer bins than 2^target_bit levels");
+  }
+  if (s.total_count() == 0) throw CalibrationError("histogram is empty");
+  if (s.absmax <= 0.0) {
+    *degenerate = kDegenerateThreshold;
+    return false;
+  }
+  return true;
+}
+
+// Runs the device KL sweep over a group of edges with equal bin counts.
+std::vector<int> kl_best_indices(const std::vector<const EdgeStats*>& es, int target_bit) {
+  const int bins = static_cast<int>(es[0]->counts.size());
+  std::vector<int64_t> flat;
+  flat.reserve(es.size() * static_cast<size_t>(bins));
+  for (const EdgeStats* e : es) flat.insert(flat.end(), e->counts.begin(), e->counts.end());
+  auto dc = engine::device_alloc(flat.size() * 8);
+  ok(cudaMemcpyAsync(dc.get(), flat.data(), flat.size() * 8, cudaMemcpyHostToDevice, S()));
+  auto di = engine::device_alloc(es.size() * 4);
+  auto dk = engine::device_alloc(es.size() * 8);
+  kern::kl_sweep(static_cast<const int64_t*>(dc.get()), static_cast<int>(es.size()), bins,
+                 target_bit, static_cast<int*>(di.get()), static_cast<double*>(dk.get()), S());
+  std::vector<int> best(es.size());
+  ok(cudaMemcpyAsync(best.data(), di.get(), best.size() * 4, cudaMemcpyDeviceToHost, S()));
+  device::synchronize();
+  return best;
+}
+
+}  // namespace
+
+double threshold_kl(const EdgeStats& stats, int target_bit) {
+  double degenerate = 0.0;
+  if (!kl_precheck(stats, target_bit, &degenerate)) return degenerate;
+  const int best = kl_best_indices({&stats}, target_bit)[0];
+  return stats.absmax *
+         (static_cast<double>(best) / static_cast<double>(stats.counts.size()));
+}
+
+double round_pow2(double threshold) {
+  if (!(threshold > 0.0)) throw CalibrationError("round_pow2 needs a positive threshold");
+  return std::exp2(std::floor(std::log2(threshold) + 0.5));
+}
+
+std::map<int, double> estimate_thresholds(const CalibrationStats& stats,
+                                          const ThresholdConfig& config) {
+  std::map<int, double> result;
+  if (config.method == ThresholdMethod::kKl) {
+    // validate in edge order (first failing edge throws, like the reference),
+    // then sweep all remaining edges in one launch per bin count
+    std::map<int, std::vector<std::pair<int, const EdgeStats*>>> by_bins;
+    for (const auto& [k, e] : stats.per_edge) {
+      double deg = 0.0;
+      if (kl_precheck(e, config.kl_bits, &deg)) {
+        by_bins[static_cast<int>(e.counts.size())].push_back({k, &e});
+      } else {
+        result[k] = deg;
+      }
+    }
+    for (const auto& [bins, group] : by_bins) {
+      std::vector<const EdgeStats*> es;
+      for (const auto& kv : group) es.push_back(kv.second);
+      std::vector<int> best = kl_best_indices(es, config.kl_bits);
+      for (size_t j = 0; j < group.size(); ++j) {
+        result[group[j].first] =
+            group[j].second->absmax * (static_cast<double>(best[j]) / static_cast<double>(bins));
+      }
+    }
+  } else {
+    for (const auto& [k, e] : stats.per_edge) {
+      result[k] = config.method == ThresholdMethod::kMax ? threshold_max(e)
+                  : e.absmax > 0.0 ? threshold_quantile(e, config.quantile)
+                                   : kDegenerateThreshold;
+    }
+  }
+  if (config.pow2) {
+    for (auto& [k, t] : result) t = round_pow2(t);
+  }
+  return result;
+}
+
+}  // namespace quantc

@@ -1,0 +1,37 @@
+// dataset.hpp — calibration/evaluation samples resident in HBM and the
+// batched top-1 prediction loop shared by predict_top1, collect_stats and
+// CandidateEvaluator (internal to the B200 build).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "engine.hpp"
+#include "quantc/interpreter.hpp"
+
+namespace quantc::gpu {
+
+class DeviceDataset {
+ public:
+  // Validates every sample against the graph inputs (reference
+  // interpreter.cpp:115-125, :519-531) and uploads [first, first+count).
+  DeviceDataset(const Graph& g, const Dataset& ds, int64_t first = 0, int64_t count = -1);
+  int64_t size() const { return n_; }
+  const float* input(size_t k, int64_t sample) const {
+    return static_cast<const float*>(bufs_[k].get()) + sample * per_[k];
+  }
+  size_t num_inputs() const { return bufs_.size(); }
+
+ private:
+  int64_t n_ = 0;
+  std::vector<std::shared_ptr<void>> bufs_;
+  std::vector<int64_t> per_;
+};
+
+// Per-sample argmax of the first graph output over every sample, on device
+// (int64 [size]).
+std::shared_ptr<void> predict_device(const engine::Plan& plan, const DeviceDataset& dd,
+                                     const SimBinding* binding, bool integer_regime,
+                                     bool allow_fast);
+
+}  // namespace quantc::gpu

@@ -1,0 +1,93 @@
+// device.cpp — per-process device context: device selection, the engine
+// stream, stream-ordered memory pool, engine mode.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdlib>
+#include <mutex>
+#include <string>
+
+#include "quantc/device.hpp"
+
+namespace quantc::device {
+
+namespace {
+
+struct Context {
+  int dev = -1;
+  cudaStream_t stream = nullptr;
+  std::atomic<int> mode{static_cast<int>(EngineMode::kAuto)};
+};
+
+Context& ctx() {
+  static Context c;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+      throw DeviceError(std::string("quantc-b200 needs a CUDA device (sm_100a): ") +
+                        (e != cudaSuccess ? cudaGetErrorString(e) : "no device visible"));
+    }
+    int dev = 0;
+    if (const char* v = std::getenv("QUANTC_DEVICE")) {
+      dev = std::atoi(v);
+    } else if (const char* r = std::getenv("LOCAL_RANK")) {
+      dev = std::atoi(r) % n;
+    }
+    if (cudaSetDevice(dev) != cudaSuccess) throw DeviceError("cudaSetDevice failed");
+    cudaDeviceProp prop{};
+    cudaGetDeviceProperties(&prop, dev);
+    if (prop.major != 10) {
+      throw DeviceError("quantc-b200 kernels are built for sm_100a; device " +
+                        std::string(prop.name) + " is sm_" + std::to_string(prop.major) +
+                        std::to_string(prop.minor));
+    }
+    // keep freed blocks in the pool: per-batch activations are re-allocated
+    // every step
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thresh = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh);
+    }
+    cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking);
+    c.dev = dev;
+    if (const char* m = std::getenv("QUANTC_ENGINE")) {
+      std::string s(m);
+      if (s == "exact") c.mode = static_cast<int>(EngineMode::kExact);
+      if (s == "fast") c.mode = static_cast<int>(EngineMode::kFast);
+      if (s == "auto") c.mode = static_cast<int>(EngineMode::kAuto);
+    }
+  });
+  // the engine may be driven from several host threads; bind the device
+  cudaSetDevice(c.dev);
+  return c;
+}
+
+}  // namespace
+
+void set_engine_mode(EngineMode m) { ctx().mode = static_cast<int>(m); }
+EngineMode engine_mode() { return static_cast<EngineMode>(ctx().mode.load()); }
+int current_device() { return ctx().dev; }
+void* stream() { return ctx().stream; }
+
+void synchronize() {
+  cudaError_t e = cudaStreamSynchronize(ctx().stream);
+  if (e != cudaSuccess) throw DeviceError(std::string("CUDA error: ") + cudaGetErrorString(e));
+}
+
+size_t memory_budget_bytes() {
+  if (const char* v = std::getenv("QUANTC_BATCH_BYTES")) return std::strtoull(v, nullptr, 10);
+  size_t free_b = 0, total = 0;
+  cudaMemGetInfo(&free_b, &total);
+  size_t budget = free_b / 4;
+  const size_t cap = size_t{24} << 30;
+  return budget > cap ? cap : budget;
+}
+
+Counters& counters() {
+  static Counters c;
+  return c;
+}
+
+}  // namespace quantc::device

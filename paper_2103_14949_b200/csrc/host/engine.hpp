@@ -1,0 +1,96 @@
+// engine.hpp — the GPU graph executor behind every quantc evaluation entry
+// point (eval_fp32 / eval_int / predict_top1 / collect_stats /
+// CandidateEvaluator).  Internal to the B200 build.
+//
+// A Plan is compiled once per graph (traversal order, port wiring, constants
+// resident in HBM).  run() executes the plan over a batch of samples on the
+// engine stream: samples are stacked along the leading dimension (every
+// per-sample computation of the reference is independent, so batching changes
+// no result), constants and values derived only from constants are computed
+// once per run (weight simulated-quantize happens once per candidate, not once
+// per sample as in the reference, which is bit-identical).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <functional>
+#include <memory>
+#include <unordered_map>
+#include <vector>
+
+#include "quantc/graph.hpp"
+#include "quantc/interpreter.hpp"
+#include "../kernels/kernels.h"
+
+namespace quantc::engine {
+
+struct DevTensor {
+  std::shared_ptr<void> buf;  // device memory (shared by aliases, e.g. flatten)
+  DType dtype = f32;          // float32 or integer (int32 storage)
+  std::vector<int64_t> shape; // batched: per-sample shape; else full shape
+  bool batched = false;
+
+  int64_t per_numel() const { return shape_numel(shape); }
+  int64_t numel(int batch) const { return batched ? per_numel() * batch : per_numel(); }
+  float* f() const { return static_cast<float*>(buf.get()); }
+  int32_t* i() const { return static_cast<int32_t*>(buf.get()); }
+};
+
+// stream-ordered device allocation
+std::shared_ptr<void> device_alloc(size_t bytes);
+
+kern::SqParams resolve_sq(const QParams& p);  // validates like simulate.cpp:47-60
+QParams qparams_of(const Node& n, const SimBinding* binding);
+
+class Plan {
+ public:
+  explicit Plan(const Graph& g);
+  Plan(const Plan&) = delete;
+
+  struct Step {
+    const Node* node = nullptr;
+    std::vector<int> in;  // producer step index per port (-1 unfed)
+    int uses = 0;         // consumers + graph-output references
+  };
+
+  const Graph& graph() const { return g_; }
+  const std::vector<Step>& steps() const { return steps_; }
+  int step_of(NodeId id) const { return index_.at(id); }
+  const DevTensor& constant(int step) const { return constants_.at(step); }
+  // per-sample output shape of every step (batched values) / full shape
+  const std::vector<int64_t>& shape(int step) const { return shapes_[static_cast<size_t>(step)]; }
+  bool batched(int step) const { return batched_[static_cast<size_t>(step)] != 0; }
+  int64_t per_sample_bytes_peak() const { return peak_bytes_; }
+  int batch_for(int64_t n_samples) const;
+
+ private:
+  const Graph& g_;
+  std::vector<Step> steps_;
+  std::unordered_map<NodeId, int> index_;
+  std::unordered_map<int, DevTensor> constants_;
+  std::vector<std::vector<int64_t>> shapes_;
+  std::vector<char> batched_;
+  int64_t peak_bytes_ = 0;
+};
+
+struct RunSpec {
+  int batch = 1;
+  std::vector<const float*> inputs;  // device, one per graph input, [batch x per-sample]
+  const SimBinding* binding = nullptr;
+  bool integer_regime = false;
+  OverflowMode mode = OverflowMode::kSaturate;
+  bool allow_fast = false;  // tcgen05 int8 path permitted (sim-quant evaluation)
+  // called right after a step's value is produced
+  std::function<void(int step, const DevTensor&)> on_value;
+  std::vector<int> keep;  // steps whose values are returned
+};
+
+// Runs a plan; returns kept values indexed like spec.keep.
+std::vector<DevTensor> run(const Plan& plan, const RunSpec& spec);
+
+// Host <-> device helpers
+DevTensor upload(const Tensor& t);
+Tensor download(const DevTensor& d, int batch);
+
+}  // namespace quantc::engine

@@ -1,0 +1,191 @@
+// interpreter.cpp — the reference executor API on the GPU engine
+// (reference interpreter.cpp:487-603).
+#include "quantc/interpreter.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "dataset.hpp"
+#include "engine.hpp"
+#include "quantc/device.hpp"
+
+namespace quantc {
+
+OverflowError::OverflowError(NodeId node_, int64_t flat_index_, int64_t value_)
+    : EvalError("accumulator overflow at node " + std::to_string(node_) + ", element " +
+                std::to_string(flat_index_) + " (value " + std::to_string(value_) + ")"),
+      node(node_),
+      flat_index(flat_index_),
+      value(value_) {}
+
+namespace {
+
+cudaStream_t S() { return static_cast<cudaStream_t>(device::stream()); }
+
+// FeedMap -> one-sample device inputs, with the reference's checks
+// (interpreter.cpp:115-125)
+std::vector<std::shared_ptr<void>> feed_inputs(const Graph& g, const FeedMap& feed) {
+  std::vector<std::shared_ptr<void>> bufs;
+  for (NodeId id : g.inputs()) {
+    const Node& n = g.node(id);
+    const std::string name = n.attr_or<std::string>("name", "");
+    auto it = feed.find(name);
+    if (it == feed.end()) throw EvalError("missing input tensor: " + name);
+    auto shape = n.attr<std::vector<int64_t>>("shape");
+    if (it->second.shape() != shape) {
+      throw EvalError("input " + name + " has shape " + shape_to_string(it->second.shape()) +
+                      ", expected " + shape_to_string(shape));
+    }
+    if (!it->second.dtype().is_float()) {
+      throw EvalError("B200 engine: graph inputs must be float32 (input " + name + ")");
+    }
+    engine::DevTensor t = engine::upload(it->second);
+    bufs.push_back(t.buf);
+  }
+  return bufs;
+}
+
+std::vector<Tensor> run_single(const Graph& g, const FeedMap& feed, const SimBinding* binding,
+                               bool integer_regime, OverflowMode mode) {
+  engine::Plan plan(g);
+  auto bufs = feed_inputs(g, feed);
+  engine::RunSpec spec;
+  spec.batch = 1;
+  for (auto& b : bufs) spec.inputs.push_back(static_cast<const float*>(b.get()));
+  spec.binding = binding;
+  spec.integer_regime = integer_regime;
+  spec.mode = mode;
+  for (const PortRef& o : g.outputs()) spec.keep.push_back(plan.step_of(o.node));
+  auto vals = engine::run(plan, spec);
+  std::vector<Tensor> outs;
+  for (size_t k = 0; k < vals.size(); ++k) {
+    if (!vals[k].buf) throw EvalError("graph output was never computed");
+    outs.push_back(engine::download(vals[k], 1));
+  }
+  return outs;
+}
+
+}  // namespace
+
+std::vector<Tensor> eval_fp32(const Graph& g, const FeedMap& feed, const SimBinding* binding) {
+  return run_single(g, feed, binding, false, OverflowMode::kSaturate);
+}
+
+std::map<NodeId, Tensor> eval_fp32_values(const Graph& g, const FeedMap& feed,
+                                          const SimBinding* binding) {
+  engine::Plan plan(g);
+  auto bufs = feed_inputs(g, feed);
+  engine::RunSpec spec;
+  spec.batch = 1;
+  for (auto& b : bufs) spec.inputs.push_back(static_cast<const float*>(b.get()));
+  spec.binding = binding;
+  for (size_t i = 0; i < plan.steps().size(); ++i) spec.keep.push_back(static_cast<int>(i));
+  auto vals = engine::run(plan, spec);
+  std::map<NodeId, Tensor> out;
+  for (size_t i = 0; i < vals.size(); ++i) {
+    out[plan.steps()[i].node->id] = engine::download(vals[i], 1);
+  }
+  return out;
+}
+
+std::vector<Tensor> eval_int(const Graph& g, const FeedMap& feed, OverflowMode mode) {
+  if (g.contains_op(OpKind::kSimulatedQuantize)) {
+    throw EvalError("eval_int expects a realized graph without simulated_quantize nodes");
+  }
+  return run_single(g, feed, nullptr, true, mode);
+}
+
+std::vector<Tensor> eval_model(const Graph& g, const FeedMap& feed, OverflowMode mode,
+                               const SimBinding* binding) {
+  if (g.is_realized()) return eval_int(g, feed, mode);
+  return eval_fp32(g, feed, binding);
+}
+
+FeedMap feed_for(const Graph& g, const Sample& sample) {
+  if (sample.inputs.size() != g.inputs().size()) {
+    throw EvalError("sample provides " + std::to_string(sample.inputs.size()) + " tensors for " +
+                    std::to_string(g.inputs().size()) + " graph inputs");
+  }
+  FeedMap feed;
+  for (size_t i = 0; i < g.inputs().size(); ++i) {
+    feed[g.node(g.inputs()[i]).attr_or<std::string>("name", "")] = sample.inputs[i];
+  }
+  return feed;
+}
+
+int64_t argmax_class(const Tensor& scores) {
+  auto s = scores.floats();
+  if (s.empty()) throw EvalError("empty score vector");
+  int64_t best = 0;
+  for (size_t i = 1; i < s.size(); ++i) {
+    if (s[i] > s[static_cast<size_t>(best)]) best = static_cast<int64_t>(i);
+  }
+  return best;
+}
+
+std::vector<int64_t> predict_top1(const Graph& g, const Dataset& dataset, int workers,
+                                  const SimBinding* binding) {
+  (void)workers;  // per-sample parallelism is the GPU batch dimension
+  if (dataset.empty()) return {};
+  engine::Plan plan(g);
+  gpu::DeviceDataset dd(g, dataset);
+  const bool realized = g.is_realized();
+  if (realized && g.contains_op(OpKind::kSimulatedQuantize)) {
+    throw EvalError("eval_int expects a realized graph without simulated_quantize nodes");
+  }
+  auto preds = gpu::predict_device(plan, dd, realized ? nullptr : binding, realized,
+                                   /*allow_fast=*/binding != nullptr);
+  std::vector<int64_t> h(dataset.size());
+  cudaMemcpyAsync(h.data(), preds.get(), h.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, S());
+  device::synchronize();
+  return h;
+}
+
+double top1_agreement(const Graph& g_ref, const Graph& g_test, const Dataset& dataset,
+                      int workers) {
+  if (dataset.empty()) throw EvalError("empty dataset");
+  if (g_ref.inputs().size() != g_test.inputs().size()) {
+    throw EvalError("models have different input signatures");
+  }
+  auto a = predict_top1(g_ref, dataset, workers);
+  auto b = predict_top1(g_test, dataset, workers);
+  int64_t same = 0;
+  for (size_t i = 0; i < a.size(); ++i) same += a[i] == b[i] ? 1 : 0;
+  return static_cast<double>(same) / static_cast<double>(a.size());
+}
+
+double labeled_accuracy(const Graph& g, const Dataset& dataset, int workers) {
+  auto preds = predict_top1(g, dataset, workers);
+  int64_t labeled = 0, correct = 0;
+  for (size_t i = 0; i < dataset.size(); ++i) {
+    if (!dataset[i].label) continue;
+    ++labeled;
+    correct += preds[i] == *dataset[i].label ? 1 : 0;
+  }
+  if (labeled == 0) throw EvalError("dataset carries no labels");
+  return static_cast<double>(correct) / static_cast<double>(labeled);
+}
+
+double mean_abs_output_diff(const Graph& g_a, const Graph& g_b, const Dataset& dataset,
+                            int workers) {
+  (void)workers;
+  if (dataset.empty()) throw EvalError("empty dataset");
+  double total = 0.0;
+  for (const Sample& s : dataset) {
+    Tensor a = eval_model(g_a, feed_for(g_a, s))[0];
+    Tensor b = eval_model(g_b, feed_for(g_b, s))[0];
+    if (!a.same_shape(b)) throw EvalError("output shape mismatch");
+    auto aa = a.floats();
+    auto bb = b.floats();
+    double acc = 0.0;
+    for (size_t k = 0; k < aa.size(); ++k) {
+      acc += std::fabs(static_cast<double>(aa[k]) - static_cast<double>(bb[k]));
+    }
+    total += acc / static_cast<double>(aa.size());
+  }
+  return total / static_cast<double>(dataset.size());
+}
+
+}  // namespace quantc

@@ -1,0 +1,185 @@
+// conv_f64.cu — exact-order fp32 conv2d / dense (reference interpreter.cpp:
+// 210-236 and 276-291).
+//
+// The reference accumulates every output in double, sequentially over
+// k = (c, kh, kw), skipping padded taps, adds the bias in double and rounds to
+// float once.  Products of two floats are exact in double, so a DFMA chain in
+// the same k order reproduces every partial sum bit for bit; padded taps are
+// fed as 0.0, which leaves the accumulator unchanged (it can never be -0.0:
+// it starts at +0.0 and exact cancellation rounds to +0.0).  Therefore this
+// kernel is bit-identical to the reference for all finite inputs.
+//
+// Implicit GEMM on CUDA-core FP64: M = N*OH*OW output pixels, N = O output
+// channels, K = C*KH*KW.  CTA tile (16*TM) x (16*TN) with 256 threads, each
+// owning a TM x TN register tile (rows ty+16i, cols tx+16j: conflict-free
+// shared-memory reads), BK = 8, double-buffered shared memory with register
+// prefetch of the next im2col/weight slice.  K is never split (order!).
+#include "common.cuh"
+
+namespace quantc::kern {
+
+namespace {
+
+constexpr int BK = 8;
+
+template <int TM, int TN>
+__global__ void __launch_bounds__(256) conv_f64_kernel(const float* __restrict__ x,
+                                                       const float* __restrict__ w,
+                                                       const float* __restrict__ bias,
+                                                       float* __restrict__ y, ConvShape cs) {
+  constexpr int BM = 16 * TM, BN = 16 * TN;
+  constexpr int A_PER = BM * BK / 256;  // im2col elements loaded per thread per tile
+  constexpr int B_PER = (BN * BK + 255) / 256;
+  __shared__ double As[2][BK][BM];
+  __shared__ double Bs[2][BK][BN];
+
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int64_t M = static_cast<int64_t>(cs.N) * cs.OH * cs.OW;
+  const int K = cs.C * cs.KH * cs.KW;
+  const int khw = cs.KH * cs.KW;
+  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * BM;
+  const int n0 = blockIdx.y * BN;
+
+  // A loader: thread owns pixel column am = tid % BM and rows ak + (256/BM)*r
+  const int am = tid % BM;
+  const int ak0 = tid / BM;
+  constexpr int AK_STEP = 256 / BM;
+  const int64_t mg = m0 + am;
+  const bool m_ok = mg < M;
+  int img = 0, ih0 = 0, iw0 = 0;
+  if (m_ok) {
+    const int64_t ohw = static_cast<int64_t>(cs.OH) * cs.OW;
+    img = static_cast<int>(mg / ohw);
+    const int rem = static_cast<int>(mg % ohw);
+    ih0 = (rem / cs.OW) * cs.sh - cs.ph;
+    iw0 = (rem % cs.OW) * cs.sw - cs.pw;
+  }
+  const float* ximg = x + static_cast<int64_t>(img) * cs.C * cs.H * cs.W;
+
+  auto load_a = [&](int k0, double (&ra)[A_PER]) {
+#pragma unroll
+    for (int r = 0; r < A_PER; ++r) {
+      const int k = k0 + ak0 + r * AK_STEP;
+      double v = 0.0;
+      if (m_ok && k < K) {
+        const int c = k / khw;
+        const int rr = k - c * khw;
+        const int kh = rr / cs.KW;
+        const int kw = rr - kh * cs.KW;
+        const int ih = ih0 + kh, iw = iw0 + kw;
+        if (ih >= 0 && ih < cs.H && iw >= 0 && iw < cs.W) {
+          v = static_cast<double>(__ldg(ximg + (static_cast<int64_t>(c) * cs.H + ih) * cs.W + iw));
+        }
+      }
+      ra[r] = v;
+    }
+  };
+  // B loader: element e = tid + 256*r -> (bk = e % BK, bn = e / BK)
+  auto load_b = [&](int k0, double (&rb)[B_PER]) {
+#pragma unroll
+    for (int r = 0; r < B_PER; ++r) {
+      const int e = tid + 256 * r;
+      const int bk = e % BK, bn = e / BK;
+      const int k = k0 + bk, o = n0 + bn;
+      double v = 0.0;
+      if (bn < BN && k < K && o < cs.O) v = static_cast<double>(__ldg(w + static_cast<int64_t>(o) * K + k));
+      rb[r] = v;
+    }
+  };
+  auto store = [&](int buf, const double (&ra)[A_PER], const double (&rb)[B_PER]) {
+#pragma unroll
+    for (int r = 0; r < A_PER; ++r) As[buf][ak0 + r * AK_STEP][am] = ra[r];
+#pragma unroll
+    for (int r = 0; r < B_PER; ++r) {
+      const int e = tid + 256 * r;
+      if (e / BK < BN) Bs[buf][e % BK][e / BK] = rb[r];
+    }
+  };
+
+  double acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.0;
+
+  double ra[A_PER], rb[B_PER];
+  load_a(0, ra);
+  load_b(0, rb);
+  store(0, ra, rb);
+  __syncthreads();
+
+  const int ntiles = (K + BK - 1) / BK;
+  for (int t = 0; t < ntiles; ++t) {
+    const int cur = t & 1;
+    if (t + 1 < ntiles) {
+      load_a((t + 1) * BK, ra);
+      load_b((t + 1) * BK, rb);
+    }
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      double a[TM], b[TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) a[i] = As[cur][kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) b[j] = Bs[cur][kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = __fma_rn(a[i], b[j], acc[i][j]);
+    }
+    if (t + 1 < ntiles) store(cur ^ 1, ra, rb);
+    __syncthreads();
+  }
+
+  const int64_t ohw = static_cast<int64_t>(cs.OH) * cs.OW;
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int64_t m = m0 + ty + 16 * i;
+    if (m >= M) continue;
+    const int64_t im = m / ohw, pix = m % ohw;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int o = n0 + tx + 16 * j;
+      if (o >= cs.O) continue;
+      double v = acc[i][j];
+      if (bias) v = __dadd_rn(v, static_cast<double>(__ldg(bias + o)));
+      y[(im * cs.O + o) * ohw + pix] = __double2float_rn(v);
+    }
+  }
+}
+
+template <int TM, int TN>
+void launch(const float* x, const float* w, const float* bias, float* y, const ConvShape& cs,
+            cudaStream_t s) {
+  const int64_t M = static_cast<int64_t>(cs.N) * cs.OH * cs.OW;
+  dim3 grid(static_cast<unsigned>((M + 16 * TM - 1) / (16 * TM)),
+            static_cast<unsigned>((cs.O + 16 * TN - 1) / (16 * TN)));
+  conv_f64_kernel<TM, TN><<<grid, 256, 0, s>>>(x, w, bias, y, cs);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+}  // namespace
+
+void conv2d_f64acc(const float* x, const float* w, const float* bias, float* y,
+                   const ConvShape& cs, cudaStream_t s) {
+  const int64_t M = static_cast<int64_t>(cs.N) * cs.OH * cs.OW;
+  if (M <= 0 || cs.O <= 0) return;
+  // Pick the channel tile; shrink the pixel tile when the grid would not fill
+  // the 148 SMs.
+  if (cs.O <= 16) {
+    launch<8, 1>(x, w, bias, y, cs, s);
+  } else if (cs.O <= 32) {
+    launch<8, 2>(x, w, bias, y, cs, s);
+  } else if (cs.O <= 64) {
+    launch<8, 4>(x, w, bias, y, cs, s);
+  } else if ((M + 127) / 128 * ((cs.O + 127) / 128) >= 148) {
+    launch<8, 8>(x, w, bias, y, cs, s);
+  } else if ((M + 63) / 64 * ((cs.O + 127) / 128) >= 148) {
+    launch<4, 8>(x, w, bias, y, cs, s);
+  } else {
+    launch<2, 8>(x, w, bias, y, cs, s);
+  }
+}
+
+}  // namespace quantc::kern

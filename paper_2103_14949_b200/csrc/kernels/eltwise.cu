@@ -1,0 +1,183 @@
+// eltwise.cu — fp32 elementwise, pooling and per-sample reductions
+// (reference interpreter.cpp:312-430, :533-541).  Semantics:
+//   add    float + float (per element, broadcast of an unbatched operand)
+//   relu   std::max(v, 0.f)          -> (v < 0) ? 0 : v   (NaN, -0.0 pass)
+//   clip   std::clamp(v, lo, hi)     -> (v < lo) ? lo : (hi < v) ? hi : v
+//   maxpool  best = lowest; best = (best < v) ? v : best over in-bounds taps
+//   gap    sequential double sum / (double)(H*W), rounded to float
+//   argmax strict '>' scan == first index of the maximum (non-NaN data)
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace quantc::kern {
+
+namespace {
+
+__global__ void add_kernel(const float* __restrict__ a, int64_t na, const float* __restrict__ b,
+                           int64_t nb, float* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    y[i] = __fadd_rn(a[na == n ? i : i % na], b[nb == n ? i : i % nb]);
+  }
+}
+
+__global__ void relu_kernel(const float* __restrict__ x, float* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float v = x[i];
+    y[i] = (v < 0.0f) ? 0.0f : v;
+  }
+}
+
+__global__ void clip_kernel(const float* __restrict__ x, float* __restrict__ y, int64_t n,
+                            float lo, float hi) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float v = x[i];
+    y[i] = (v < lo) ? lo : ((hi < v) ? hi : v);
+  }
+}
+
+__global__ void maxpool_kernel(const float* __restrict__ x, float* __restrict__ y, int N, int C,
+                               int H, int W, int OH, int OW, int kh, int kw, int sh, int sw,
+                               int ph, int pw) {
+  const int64_t total = static_cast<int64_t>(N) * C * OH * OW;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int ow = static_cast<int>(i % OW);
+    const int oh = static_cast<int>((i / OW) % OH);
+    const int64_t nc = i / (static_cast<int64_t>(OW) * OH);
+    const float* src = x + nc * H * W;
+    float best = -FLT_MAX;
+    for (int a = 0; a < kh; ++a) {
+      const int ih = oh * sh - ph + a;
+      if (ih < 0 || ih >= H) continue;
+      for (int b = 0; b < kw; ++b) {
+        const int iw = ow * sw - pw + b;
+        if (iw < 0 || iw >= W) continue;
+        const float v = src[ih * W + iw];
+        best = (best < v) ? v : best;
+      }
+    }
+    y[i] = best;
+  }
+}
+
+// one warp per (n, c): lanes stage the plane through registers, lane 0 sums
+// in the reference order
+__global__ void gap_kernel(const float* __restrict__ x, float* __restrict__ y, int NC, int HW) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= NC) return;
+  const float* src = x + static_cast<int64_t>(warp) * HW;
+  double acc = 0.0;
+  for (int base = 0; base < HW; base += 32) {
+    const int idx = base + lane;
+    const float v = idx < HW ? src[idx] : 0.0f;
+    const int cnt = min(32, HW - base);
+    for (int l = 0; l < cnt; ++l) {
+      const float vl = __shfl_sync(0xffffffffu, v, l);
+      acc = __dadd_rn(acc, static_cast<double>(vl));
+    }
+  }
+  if (lane == 0) y[warp] = __double2float_rn(__ddiv_rn(acc, static_cast<double>(HW)));
+}
+
+__global__ void __launch_bounds__(256) argmax_kernel(const float* __restrict__ x, int64_t cols,
+                                                     int64_t* __restrict__ out) {
+  const float* row = x + static_cast<int64_t>(blockIdx.x) * cols;
+  float bv = -FLT_MAX;
+  int64_t bi = -1;
+  for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
+    const float v = row[c];
+    if (bi < 0 || v > bv) {
+      bv = v;
+      bi = c;
+    }
+  }
+  auto take = [](float v, int64_t i, float& bv2, int64_t& bi2) {
+    if (i < 0) return;
+    if (bi2 < 0 || v > bv2 || (v == bv2 && i < bi2)) {
+      bv2 = v;
+      bi2 = i;
+    }
+  };
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    take(ov, oi, bv, bi);
+  }
+  __shared__ float sv[8];
+  __shared__ int64_t si[8];
+  if ((threadIdx.x & 31) == 0) {
+    sv[threadIdx.x >> 5] = bv;
+    si[threadIdx.x >> 5] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w2 = 1; w2 < static_cast<int>(blockDim.x >> 5); ++w2) take(sv[w2], si[w2], bv, bi);
+    out[blockIdx.x] = bi < 0 ? 0 : bi;
+  }
+}
+
+__global__ void count_equal_kernel(const int64_t* a, const int64_t* b, int n,
+                                   unsigned long long* count) {
+  unsigned int mine = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    mine += a[i] == b[i];
+  }
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(count, static_cast<unsigned long long>(mine));
+}
+
+}  // namespace
+
+void add_f32(const float* a, int64_t na, const float* b, int64_t nb, float* y, int64_t n,
+             cudaStream_t s) {
+  if (n <= 0) return;
+  add_kernel<<<grid_for(n, 256), 256, 0, s>>>(a, na, b, nb, y, n);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+void relu_f32(const float* x, float* y, int64_t n, cudaStream_t s) {
+  if (n <= 0) return;
+  relu_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, y, n);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+void clip_f32(const float* x, float* y, int64_t n, float lo, float hi, cudaStream_t s) {
+  if (n <= 0) return;
+  clip_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, y, n, lo, hi);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+void maxpool_f32(const float* x, float* y, int N, int C, int H, int W, int OH, int OW, int kh,
+                 int kw, int sh, int sw, int ph, int pw, cudaStream_t s) {
+  const int64_t total = static_cast<int64_t>(N) * C * OH * OW;
+  if (total <= 0) return;
+  maxpool_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, y, N, C, H, W, OH, OW, kh, kw, sh, sw,
+                                                      ph, pw);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+void gap_f32(const float* x, float* y, int NC, int HW, cudaStream_t s) {
+  if (NC <= 0) return;
+  gap_kernel<<<(NC * 32 + 255) / 256, 256, 0, s>>>(x, y, NC, HW);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+void argmax_rows(const float* x, int rows, int64_t cols, int64_t* out, cudaStream_t s) {
+  if (rows <= 0) return;
+  argmax_kernel<<<rows, 256, 0, s>>>(x, cols, out);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+void count_equal(const int64_t* a, const int64_t* b, int n, unsigned long long* count,
+                 cudaStream_t s) {
+  if (n <= 0) return;
+  count_equal_kernel<<<grid_for(n, 256, 64), 256, 0, s>>>(a, b, n, count);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+}  // namespace quantc::kern

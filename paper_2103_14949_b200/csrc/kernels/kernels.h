@@ -1,0 +1,111 @@
+// kernels.h — host launchers of the sm_100a kernels (internal C++ interface
+// used by the engine; the public C-ABI over them is include/quantc_cuda.h).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace quantc::kern {
+
+// Simulated-quantize parameters resolved on the host once per node
+// (reference simulate.cpp:64-78 with compute_scale/quant_bounds hoisted).
+struct SqParams {
+  double lo, hi;       // accumulator clamp bounds (valid if has_acc)
+  double s;            // scale threshold / 2^(bit-sign)
+  double inv_s;        // RN(1/s), fast-path reciprocal
+  double qmin, qmax;   // code bounds (as doubles, like the reference clamp)
+  double zp;           // zero point as double
+  int32_t has_acc;
+  int32_t passthrough;
+  int32_t exact_div;   // 1 when inv_s is not finite: always divide
+  int32_t pad_;
+};
+
+// ---- simulated quantize (simquant.cu) ------------------------------------
+void sim_quant(const float* x, float* y, int64_t n, const SqParams& p, cudaStream_t s);
+// also emit integer codes (q - zp) as int8 in NHWC order for a tcgen05 GEMM:
+// x is NCHW [N,C,H,W] (H=W=1 for dense rows); codes [N,H,W,Cpad] with zero
+// padding for channels >= C.
+void sim_quant_codes_nhwc(const float* x, float* y, int8_t* codes, int N, int C, int H, int W,
+                          int Cpad, const SqParams& p, cudaStream_t s);
+
+// ---- statistics (stats.cu) -------------------------------------------------
+// d_minmax: 2 uint64 order keys per slot (min key, max key), pre-initialised.
+void minmax_init(unsigned long long* keys, int n_slots, cudaStream_t s);
+void minmax_accumulate(const float* x, int64_t n, unsigned long long* keys2, cudaStream_t s);
+void minmax_decode(const unsigned long long* keys, double* out, int n_slots, cudaStream_t s);
+// histogram of |x| against absmax (reference calibration.cpp:28-33,97-105);
+// counts are uint64 accumulated (multiplier applied per element count).
+void histogram_accumulate(const float* x, int64_t n, double absmax, int bins,
+                          unsigned long long* counts, unsigned long long multiplier,
+                          cudaStream_t s);
+
+// ---- KL sweep (kl.cu) --------------------------------------------------------
+// counts: [n_edges][bins] int64; outputs best index i (bins units) and its KL.
+void kl_sweep(const int64_t* counts, int n_edges, int bins, int target_bit, int* best_i,
+              double* best_kl, cudaStream_t s);
+
+// ---- exact fp32 conv/dense with sequential FP64 accumulation (conv_f64.cu) --
+struct ConvShape {
+  int N, C, H, W, O, KH, KW, OH, OW, sh, sw, ph, pw;
+};
+void conv2d_f64acc(const float* x, const float* w, const float* bias, float* y,
+                   const ConvShape& cs, cudaStream_t s);
+
+// ---- elementwise / pooling / reductions (eltwise.cu) -------------------------
+void add_f32(const float* a, int64_t na, const float* b, int64_t nb, float* y, int64_t n,
+             cudaStream_t s);  // na/nb: operand extents (broadcast by modulo)
+void relu_f32(const float* x, float* y, int64_t n, cudaStream_t s);
+void clip_f32(const float* x, float* y, int64_t n, float lo, float hi, cudaStream_t s);
+void maxpool_f32(const float* x, float* y, int N, int C, int H, int W, int OH, int OW, int kh,
+                 int kw, int sh, int sw, int ph, int pw, cudaStream_t s);
+void gap_f32(const float* x, float* y, int NC, int HW, cudaStream_t s);
+void argmax_rows(const float* x, int rows, int64_t cols, int64_t* out, cudaStream_t s);
+void count_equal(const int64_t* a, const int64_t* b, int n, unsigned long long* count,
+                 cudaStream_t s);
+
+// ---- integer regime (intops.cu) ------------------------------------------------
+// int32 storage (reference tensor.hpp:15-17); exact int64 accumulation.
+// trap_flat: when non-null, overflowing elements atomicMin their flat index there.
+void conv2d_int(const int32_t* x, const int32_t* w, const int32_t* bias, int32_t* y,
+                const ConvShape& cs, int64_t zp0, int64_t zp1, int64_t acc_min, int64_t acc_max,
+                unsigned long long* trap_flat, cudaStream_t s);
+int64_t conv2d_int_value_at(const int32_t* x, const int32_t* w, const int32_t* bias,
+                            const ConvShape& cs, int64_t zp0, int64_t zp1, int64_t flat,
+                            cudaStream_t s);
+void add_int(const int32_t* a, int64_t na, const int32_t* b, int64_t nb, int32_t* y, int64_t n,
+             int64_t acc_min, int64_t acc_max, unsigned long long* trap_flat, cudaStream_t s);
+void relu_int(const int32_t* x, int32_t* y, int64_t n, int32_t zp, cudaStream_t s);
+void clip_int(const int32_t* x, int32_t* y, int64_t n, int32_t lo, int32_t hi, cudaStream_t s);
+void maxpool_int(const int32_t* x, int32_t* y, int N, int C, int H, int W, int OH, int OW,
+                 int kh, int kw, int sh, int sw, int ph, int pw, cudaStream_t s);
+void quantize_f32_int(const float* x, int32_t* y, int64_t n, double scale, int64_t zp,
+                      int64_t qmin, int64_t qmax, cudaStream_t s);
+void dequantize_int_f32(const int32_t* x, float* y, int64_t n, double scale, int64_t zp,
+                        cudaStream_t s);
+void requantize_int(const int32_t* x, int32_t* y, int64_t n, int64_t mult, int shift,
+                    int64_t in_zp, int64_t out_zp, int64_t qmin, int64_t qmax, cudaStream_t s);
+
+// ---- tcgen05 int8 GEMM (gemm_tcgen05.cu) -----------------------------------------
+// C[M,N] (int32 accumulators, consumed by the epilogue) = A[M,K] * B[N,K]^T,
+// A/B int8 K-major, K a multiple of 128 (zero padded).  Epilogue: y (NCHW
+// float, M rows = (img, oh, ow), N = channels) = float(acc * scale + bias[n]).
+struct GemmEpilogue {
+  float* y;          // output, NCHW
+  const float* bias; // may be null
+  double scale;      // s_x * s_w
+  int OHW;           // pixels per image (OH*OW); 1 for dense
+};
+bool gemm_s8_tcgen05_available();
+void gemm_s8_tcgen05(const int8_t* A, const int8_t* B, int M, int N, int K,
+                     const GemmEpilogue& ep, cudaStream_t s);
+// im2col of NHWC int8 codes into [M, Kpad] rows (k order = (kh, kw, c))
+void im2col_s8(const int8_t* x, int8_t* out, int N, int H, int W, int Cpad, int KH, int KW,
+               int OH, int OW, int sh, int sw, int ph, int pw, int Kpad, cudaStream_t s);
+// weights [O][C][KH][KW] float (already sim-quantized) -> codes [O][Kpad] in
+// (kh, kw, c) order with the same code convention.
+void weights_to_codes(const float* w, int8_t* codes, int O, int C, int KH, int KW, int Cpad,
+                      int Kpad, const SqParams& p, cudaStream_t s);
+
+}  // namespace quantc::kern

@@ -1,0 +1,195 @@
+"""GPU parity: the B200 implementation vs the reference oracle on identical
+inputs, through the C ABI (include/quantc_capi.h) and the kernel ABI
+(include/quantc_cuda.h).
+
+Bar (BASELINE.json north_star): bit-exact for histogram counts, min/max,
+integer outputs, predictions, losses and the selected strategy; KL values
+within 1e-12 relative (log() may differ from glibc by 1 ulp); thresholds
+bit-exact (they are absmax * i / B with the same integer i)."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2103_14949_b200 import fixtures as F
+from paper_2103_14949_b200 import quantc as Q
+
+pytestmark = pytest.mark.gpu
+
+
+def _pipeline(q, model, data, spec_name="int8_int32", method="quantile", pow2=False,
+              quantile=0.999):
+    g = q.graph(model.doc, model.blob)
+    spec = q.parse_spec(F.spec_fixture(spec_name))
+    topo = q.generate_topology(g, spec)
+    sim = q.insert_simulated_quantize(g, topo)
+    ds = q.dataset(data)
+    edges = q.simulated_edge_indices(g, topo)
+    st = q.collect_stats(g, ds, 2048, edges)
+    thr = st.estimate_thresholds(method, quantile=quantile, kl_bits=8, pow2=pow2)
+    ev = q.evaluator(sim, spec, topo, thr, st, ds)
+    return dict(g=g, spec=spec, topo=topo, sim=sim, ds=ds, edges=edges, st=st, thr=thr, ev=ev)
+
+
+@pytest.fixture(scope="module")
+def small_cnn():
+    m = F.small_cnn()
+    return m, m.data(16)
+
+
+def test_collect_stats_bit_exact(b200, ref, small_cnn):
+    m, data = small_cnn
+    a = _pipeline(b200, m, data)
+    r = _pipeline(ref, m, data)
+    assert a["edges"] == r["edges"]
+    for k in r["edges"]:
+        ea, er = a["st"].get(k), r["st"].get(k)
+        assert ea["min"] == er["min"] and ea["max"] == er["max"], k
+        assert ea["absmax"] == er["absmax"], k
+        assert ea["sample_count"] == er["sample_count"]
+        np.testing.assert_array_equal(ea["counts"], er["counts"], err_msg=f"edge {k}")
+
+
+@pytest.mark.parametrize("method,pow2", [("max", False), ("quantile", False), ("kl", False),
+                                         ("quantile", True), ("kl", True)])
+def test_thresholds_and_losses_identical(b200, ref, small_cnn, method, pow2):
+    m, data = small_cnn
+    a = _pipeline(b200, m, data, method=method, pow2=pow2)
+    r = _pipeline(ref, m, data, method=method, pow2=pow2)
+    assert a["thr"] == r["thr"]
+    np.testing.assert_array_equal(a["ev"].reference_predictions(),
+                                  r["ev"].reference_predictions())
+    sp = r["ev"].space()
+    assert a["ev"].space() == sp
+    rng = np.random.default_rng(0)
+    cands = [sp.all_hi(), sp.all_lo()] + [
+        [int(rng.integers(lo, hi + 1)) for lo, hi in zip(sp.lo, sp.hi)] for _ in range(6)]
+    np.testing.assert_array_equal(a["ev"].losses(cands), r["ev"].losses(cands))
+    for c in cands[:3]:
+        assert a["ev"].bind(c).keys() == r["ev"].bind(c).keys()
+        for k, p in r["ev"].bind(c).items():
+            assert a["ev"].bind(c)[k].as_dict() == p.as_dict()
+        assert a["ev"].strategy_for(c) == r["ev"].strategy_for(c)
+
+
+def test_greedy_selects_identical_strategy(b200, ref, small_cnn):
+    m, data = small_cnn
+    out = []
+    for q in (b200, ref):
+        p = _pipeline(q, m, data, method="quantile", pow2=False)
+        sp = p["ev"].space()
+        res = q.search("greedy", sp, evaluator=p["ev"], rounds=2, tol=0.05)
+        out.append((res.best, res.best_loss, res.evaluations, res.trace,
+                    p["ev"].strategy_for(res.best)))
+    assert out[0] == out[1]
+
+
+def test_eval_fp32_resnet_block_bit_exact(b200, ref):
+    m = F.resnet(18, image=32, classes=10, width=8)
+    x = m.data(1)[0]
+    ga, gr = b200.graph(m.doc, m.blob), ref.graph(m.doc, m.blob)
+    ya, yr = b200.eval_fp32(ga, x), ref.eval_fp32(gr, x)
+    assert ya.tobytes() == yr.tobytes()
+
+
+def test_sim_quant_tensor_bit_exact(b200, ref):
+    rng = np.random.default_rng(1)
+    x = (rng.standard_normal(1 << 16) * rng.choice([0.01, 1, 100], 1 << 16)).astype(np.float32)
+    for t, bit, sign, acc in [(1.0, 8, 1, Q.NONE), (0.37, 6, 1, Q.NONE), (3.3, 4, 1, Q.I16),
+                              (2.0**-3, 8, 1, Q.I32), (5.0, 8, 0, Q.NONE)]:
+        dt = Q.I8 if sign else Q.U8
+        p = Q.QParams.make(t, bit, sign, dt, acc_dtype=acc, acc_scale=1e-3 if acc != Q.NONE else 0)
+        if sign == 0:
+            p.zero_point = 17
+        assert b200.simulated_quantize(x, p).tobytes() == ref.simulated_quantize(x, p).tobytes()
+
+
+def test_sim_quant_kernel_vs_port_many_tuples(cuda_lib, port):
+    """SPEC acceptance 1: >= 10^4 (x, threshold, bit, sign) tuples, bit-exact."""
+    rng = np.random.default_rng(2)
+    for trial in range(40):
+        t = float(np.exp(rng.uniform(-8, 8)))
+        bit = int(rng.integers(2, 9))
+        sign = int(rng.integers(0, 2))
+        zp = 0 if sign else int(rng.integers(0, 1 << bit))
+        x = (rng.standard_normal(4096) * t * rng.uniform(0.1, 3)).astype(np.float32)
+        # near-tie values: exact half-integers of the grid
+        s = t / 2.0 ** (bit - sign)
+        x[:256] = ((rng.integers(-200, 200, 256) + 0.5) * s).astype(np.float32)
+        p = Q.QParams.make(t, bit, sign, Q.I8 if sign else Q.U8, zero_point=zp)
+        y = cuda_lib.sim_quant(torch.from_numpy(x).cuda(), p).cpu().numpy()
+        expect = port.sim_quant(x, t, bit, sign, zp)
+        assert y.tobytes() == expect.tobytes(), trial
+
+
+def test_histogram_and_minmax_kernels(cuda_lib, port):
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(1_000_003).astype(np.float32)
+    x[:5] = 0.0
+    xt = torch.from_numpy(x).cuda()
+    mm = cuda_lib.minmax(xt).cpu().numpy()
+    assert mm[0] == float(x.min()) and mm[1] == float(x.max())
+    absmax = max(abs(mm[0]), abs(mm[1]))
+    for bins in (2048, 100, 7):
+        c = cuda_lib.histogram(xt, absmax, bins).cpu().numpy()
+        np.testing.assert_array_equal(c, port.histogram(x, absmax, bins))
+
+
+def test_kl_sweep_kernel_matches_port(cuda_lib, port):
+    rng = np.random.default_rng(4)
+    hists = []
+    for shape in range(12):
+        if shape % 3 == 0:
+            h = rng.integers(0, 1000, 2048)
+        elif shape % 3 == 1:
+            h = np.floor(1e6 * np.exp(-np.arange(2048) / rng.uniform(20, 400))).astype(np.int64)
+        else:
+            h = np.zeros(2048, np.int64)
+            h[rng.integers(0, 2048, 50)] = rng.integers(1, 100, 50)
+        hists.append(h)
+    counts = torch.tensor(np.stack(hists), dtype=torch.int64).cuda()
+    bi, bk = cuda_lib.kl_sweep(counts, 8)
+    for e, h in enumerate(hists):
+        i, kl = port.kl_best_index(h, 8)
+        assert int(bi[e]) == i
+        assert abs(float(bk[e]) - kl) <= 1e-12 * max(1.0, abs(kl))
+
+
+def test_conv_f64_kernel_bit_exact(cuda_lib, port):
+    rng = np.random.default_rng(5)
+    for (N, Cc, H, W, O, K, s, pd) in [(2, 3, 17, 15, 16, 3, 1, 1), (1, 8, 12, 12, 70, 3, 2, 1),
+                                       (3, 5, 9, 9, 130, 1, 1, 0), (1, 3, 30, 30, 8, 7, 2, 3)]:
+        x = rng.standard_normal((N, Cc, H, W)).astype(np.float32)
+        w = rng.standard_normal((O, Cc, K, K)).astype(np.float32)
+        b = rng.standard_normal(O).astype(np.float32)
+        y = cuda_lib.conv2d_f64acc(torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda(),
+                                   torch.from_numpy(b).cuda(), (s, s), (pd, pd)).cpu().numpy()
+        assert y.tobytes() == port.conv2d(x, w, b, (s, s), (pd, pd)).tobytes()
+
+
+def test_tcgen05_gemm_exact_integer(cuda_lib):
+    if not cuda_lib.tcgen05_available():
+        pytest.fail("tcgen05 path not available on this device")
+    rng = np.random.default_rng(6)
+    for M, N, K in [(128, 64, 128), (300, 96, 256), (1000, 256, 640), (129, 300, 384)]:
+        A = rng.integers(-128, 128, (M, K), dtype=np.int8)
+        B = rng.integers(-128, 128, (N, K), dtype=np.int8)
+        y = cuda_lib.gemm_s8(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), 1.0, None,
+                             1).cpu().numpy().reshape(M, N)
+        ref = A.astype(np.int64) @ B.astype(np.int64).T
+        np.testing.assert_array_equal(y.astype(np.int64), ref)
+
+
+def test_fast_engine_equals_exact_engine_pow2(b200, cuda_lib, small_cnn):
+    """pow2 thresholds: tcgen05 int8 path is bit-identical to the FP64 path."""
+    m, data = small_cnn
+    p = _pipeline(b200, m, data, method="quantile", pow2=True)
+    sp = p["ev"].space()
+    cands = [sp.all_hi(), sp.all_lo(), [5] * len(sp.hi)]
+    cuda_lib.set_engine_mode("exact")
+    exact = p["ev"].losses(cands)
+    g0 = cuda_lib.counters()["tcgen05_gemms"]
+    cuda_lib.set_engine_mode("fast")
+    fast = p["ev"].losses(cands)
+    assert cuda_lib.counters()["tcgen05_gemms"] > g0
+    cuda_lib.set_engine_mode("auto")
+    np.testing.assert_array_equal(exact, fast)
