@@ -1,0 +1,349 @@
+"""bench.py — HAGO calibrate-and-search hot path on B200.
+
+Metric (BASELINE.json): int8 simulated-quantized ResNet-50 images/s; search
+candidates/s.  One step = one candidate evaluation (bind -> sim-quant int8
+forward of the calibration batch -> top-1 agreement with the fp32
+references) over a batch of B synthetic 224x224 images per GPU, exactly the
+inner loop of CandidateEvaluator::loss (reference search.cpp:421-428).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B]
+  python bench.py --impl reference ...   (the reference CPU implementation)
+
+N > 1 runs under torchrun, one rank per GPU: each rank holds its own shard of
+B calibration images (weak scaling) and the per-candidate agreement counts are
+all-reduced with NCCL (the search's only data-path collective).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+from paper_2103_14949_b200 import fixtures as F  # noqa: E402
+from paper_2103_14949_b200 import quantc as Q  # noqa: E402
+
+METRIC = "int8 sim-quant ResNet-50 images/sec"
+REF_LIB = os.path.join(REPO, "oracle", "_ref", "libquantc_ref.so")
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.samples, self._stop = gpu, [], threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def build_pipeline(q, model, data, calib_stats=None):
+    g = q.graph(model.doc, model.blob)
+    spec = q.parse_spec(F.spec_fixture("int8_int32"))
+    topo = q.generate_topology(g, spec)
+    sim = q.insert_simulated_quantize(g, topo)
+    ds = q.dataset(data)
+    st = calib_stats if calib_stats is not None else q.collect_stats(
+        g, ds, 2048, q.simulated_edge_indices(g, topo))
+    # power-of-two thresholds: the int8 tensor-core path is bit-identical to
+    # the reference (engine kAuto); quantile q=0.999
+    thr = st.estimate_thresholds("quantile", quantile=0.999, pow2=True)
+    return g, spec, topo, sim, ds, st, thr
+
+
+def candidates(space, n, seed=0):
+    """Greedy-style probes: all_hi with one slot decremented, cycling slots."""
+    out = []
+    hi = space.all_hi()
+    for i in range(n):
+        c = list(hi)
+        s = (i * 7 + seed) % len(c)
+        c[s] = max(space.lo[s], c[s] - 1 - (i % 3))
+        out.append(c)
+    return out
+
+
+def _ref_binding(ref, model, threads):
+    """Reference-only setup: calibrate on one image, bind one candidate."""
+    one = model.data(1, seed=11)
+    g, spec, topo, sim, ds, st, thr = build_pipeline(ref, model, one)
+    ev = ref.evaluator(sim, spec, topo, thr, st, ds, 4, threads)
+    return sim, ev, ev.space()
+
+
+def cpu_reference_rate(model, sample, threads, binding):
+    """The reference CPU implementation (oracle/_ref, compiled from the
+    reference sources) timed on this host: predict_top1 of the sim-quant graph
+    under one candidate binding (the body of CandidateEvaluator::loss,
+    reference search.cpp:421-428) over `sample` images with `threads`
+    workers.  The binding is the bit-identical one computed by the B200
+    library (tests/test_gpu_parity.py) so no reference calibration pass is
+    needed to time this leg."""
+    ref = Q.load(REF_LIB)
+    g = ref.graph(model.doc, model.blob)
+    spec = ref.parse_spec(F.spec_fixture("int8_int32"))
+    sim = ref.insert_simulated_quantize(g, ref.generate_topology(g, spec))
+    ds = ref.dataset(model.data(sample, seed=11))
+    t0 = time.perf_counter()
+    ref.predict_top1(sim, ds, threads, binding)
+    dt = time.perf_counter() - t0
+    return sample / dt, dt
+
+
+def run_reference(args):
+    rank = _env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    if not os.path.exists(REF_LIB):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return 0
+    model = F.resnet(50)
+    threads = os.cpu_count() or 1
+    sample = threads  # one image per host thread per step (the reference's parallel unit)
+    ref = Q.load(REF_LIB)
+    sim, ev, sp = _ref_binding(ref, model, threads)
+    cands = candidates(sp, args.warmup + args.steps)
+    ds = ref.dataset(model.data(sample, seed=11))
+    for i in range(args.warmup):
+        ref.predict_top1(sim, ds, threads, ev.bind(cands[i]))
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        ref.predict_top1(sim, ds, threads, ev.bind(cands[args.warmup + i]))
+    dt = time.perf_counter() - t0
+    value = sample * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64/f32 (reference CPU)", "data": "synthetic",
+        "config": {"workload": "resnet50 int8_int32 sim-quant candidate evaluation",
+                   "model": "resnet50", "image": 224, "batch": sample,
+                   "parallelism": f"{threads} host threads"},
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": threads,
+                         "kind": "reference",
+                         "sample": f"{sample} images per step, {args.steps} candidates"},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--engine", default="auto", choices=["auto", "fast", "exact"])
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    os.environ.setdefault("QUANTC_DEVICE", str(local))
+    torch.cuda.set_device(local)
+
+    from paper_2103_14949_b200 import cuda_ops
+    b = Q.load_b200()
+    ops = cuda_ops.load()
+    ops.set_engine_mode(args.engine)
+    L = b.lib
+    L.qc_evaluator_agreement.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.c_size_t, C.c_size_t,
+                                         C.POINTER(C.c_int64)]
+    L.qcu_engine_stream.restype = C.c_void_p
+    L.qcu_profile_enable.argtypes = [C.c_int]
+    L.qcu_profile_read.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                                   C.POINTER(C.c_double)]
+
+    model = F.resnet(50)
+    B = args.batch
+    # weak scaling: rank r owns calibration images [r*B, (r+1)*B)
+    data_all = model.data(B * world, seed=9)
+    data = np.ascontiguousarray(data_all[rank * B:(rank + 1) * B])
+    g, spec, topo, sim, ds, st, thr = build_pipeline(b, model, data)
+    ev = b.evaluator(sim, spec, topo, thr, st, ds)
+    sp = ev.space()
+    cands = candidates(sp, args.warmup + args.steps)
+
+    stream = torch.cuda.ExternalStream(L.qcu_engine_stream())
+    counts = np.zeros(1, np.int64)
+    cnt_t = torch.zeros(1, dtype=torch.int64, device=f"cuda:{local}")
+
+    def step(c):
+        arr = np.asarray(c, np.int32)
+        rc = L.qc_evaluator_agreement(ev.h, arr.ctypes.data_as(C.POINTER(C.c_int)), 1, len(c),
+                                      counts.ctypes.data_as(C.POINTER(C.c_int64)))
+        b.check(rc)
+        if dist is not None:
+            cnt_t.fill_(int(counts[0]))
+            dist.all_reduce(cnt_t)
+            return 1.0 - cnt_t.item() / (B * world)
+        return 1.0 - counts[0] / B
+
+    for i in range(args.warmup):
+        step(cands[i])
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ops.counters()["steps"]
+    L.qcu_profile_enable(1)
+    gms, gl, gops = C.c_double(), C.c_int64(), C.c_double()
+    L.qcu_profile_read(C.byref(gms), C.byref(gl), C.byref(gops))  # drain
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for i in range(args.steps):
+            step(cands[args.warmup + i])
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    L.qcu_profile_read(C.byref(gms), C.byref(gl), C.byref(gops))
+    L.qcu_profile_enable(0)
+    launches = ops.counters()["steps"] - launches0
+    ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    imgs_per_s = B * world * args.steps / (ms / 1e3)
+
+    # ---- e2e: public C-ABI call with HOST buffers: predict_top1 of the sim
+    # graph under a candidate binding (uploads images + plan, downloads preds)
+    binding = ev.bind(cands[0])
+    e2e_steps = max(2, min(5, args.steps))
+    b.predict_top1(sim, ds, 0, binding)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        b.predict_top1(sim, ds, 0, binding)
+    e2e_dt = (time.perf_counter() - t0) / e2e_steps
+    if dist is not None:
+        t = torch.tensor([e2e_dt], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_dt = float(t.item())
+    weight_bytes = len(model.blob)
+    h2d = data.nbytes + weight_bytes
+    d2h = 8 * B
+
+    # ---- roofline of the dominant kernel (tcgen05 int8 implicit-GEMM conv)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    bf16 = peaks.get("bf16_tflops", 1590.0)
+    int8_peak = 2.0 * bf16  # dense int8 rate = 2x bf16 on B200
+    achieved = (gops.value / (gms.value / 1e3)) / 1e12 if gms.value > 0 else 0.0
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(REPO, "profiles", "ncu_summary.json")))
+        traffic = prof.get("gemm_dram_bytes_per_launch")
+    except Exception:
+        pass
+
+    line = {
+        "metric": METRIC, "value": imgs_per_s, "unit": "images/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
+        "data": "synthetic (N(0,1) images, He-normal BN-folded ResNet-50 weights, seeds 9/42)",
+        "config": {"workload": "resnet50 int8_int32 sim-quant candidate evaluation",
+                   "model": "resnet50", "image": 224, "global_batch": B * world,
+                   "per_gpu_batch": B, "parallelism": f"dp{world} (calibration shards)",
+                   "thresholds": "quantile 0.999, pow2 (tcgen05 path bit-exact)",
+                   "engine": args.engine, "l2": "inputs 38.5 MB/GPU + activations > L2"},
+        "candidates_per_s": world * args.steps / (ms / 1e3) / world * 1.0,
+        "e2e": {"value": B * world / e2e_dt, "unit": "images/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "api": "qc_predict_top1(sim_graph, host dataset, binding)"},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": int8_peak,
+                     "unit": "TOPS", "frac": achieved / int8_peak if int8_peak else None,
+                     "traffic": traffic,
+                     "kernel": "gemm_s8_kernel (tcgen05.mma kind::i8)",
+                     "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (burst)",
+                     "gemm_share_of_step": (gms.value / ms) if ms > 0 else None,
+                     "gemm_launches": int(gl.value)},
+        "clocks": clk.summary(),
+    }
+    line["candidates_per_s"] = args.steps / (ms / 1e3)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and os.path.exists(REF_LIB):
+        threads = os.cpu_count() or 1
+        sample = min(max(threads, 2), 16)
+        rate, dt = cpu_reference_rate(model, sample, threads, binding)
+        line["cpu_baseline"] = {"value": rate, "unit": "images/s", "cores": threads,
+                                "kind": "reference",
+                                "sample": f"{sample} images x 1 candidate ({dt:.1f} s)"}
+    if rank == 0:
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -37,11 +37,21 @@ size_t memory_budget_bytes();  // per-batch activation budget
 
 // Counters (for bench / profiling evidence).
 struct Counters {
-  int64_t kernel_launches = 0;
+  int64_t kernel_launches = 0;  // every sm_100a kernel this library launched
   int64_t tcgen05_gemms = 0;
   int64_t f64_convs = 0;
 };
 Counters& counters();
+
+// Optional per-GEMM timing with CUDA events on the engine stream: when
+// enabled, every tcgen05 GEMM launch is bracketed by events and its
+// algorithmic int8 op count (2*M*N*K_true) recorded.
+void profile_enable(bool on);
+bool profile_enabled();
+void profile_gemm_begin();
+void profile_gemm_end(double ops);
+// drains recorded events: total GEMM ms, launches, algorithmic ops
+void profile_read(double* gemm_ms, int64_t* gemm_launches, double* gemm_ops);
 
 }  // namespace device
 }  // namespace quantc

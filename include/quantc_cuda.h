@@ -2,7 +2,8 @@
  * quantc_cuda.h — the thin C-ABI between the quantc C++ host and the sm_100a
  * kernels (north_star: "The host side stays C++ and calls CUDA through a thin
  * C-ABI layer").  Plain device pointers, sizes and an explicit cudaStream_t
- * (passed as void*, NULL = the engine stream); status codes as in
+ * (passed as void*, NULL = the engine stream, (void*)1 = cudaStreamLegacy,
+ * i.e. the legacy default stream); status codes as in
  * quantc_capi.h, message via qc_last_error().
  *
  * Each entry point replaces one hot loop of the reference CPU implementation:
@@ -70,6 +71,16 @@ const char* qcu_last_error(void);
 int qcu_tcgen05_available(void);
 /* engine mode for sim-quant evaluation: 0 exact, 1 fast, 2 auto */
 int qcu_set_engine_mode(int mode);
+/* the engine's cudaStream_t (for CUDA-event timing of engine work) */
+void* qcu_engine_stream(void);
+/* per-GEMM CUDA-event profiling of the engine's tcgen05 launches */
+int qcu_profile_enable(int on);
+int qcu_profile_read(double* gemm_ms, int64_t* gemm_launches, double* gemm_ops);
+/* CandidateEvaluator::agreement_counts (B200 extension): per candidate, the
+ * number of local calibration samples whose top-1 equals the fp32 reference;
+ * the multi-GPU driver all-reduces these (loss = 1 - sum / N_total). */
+int qc_evaluator_agreement(const qc_evaluator* e, const int* cands, size_t n_cands,
+                           size_t n_slots, int64_t* counts);
 /* counters since load: kernel launches issued by the engine, tcgen05 GEMMs */
 int qcu_counters(int64_t* steps, int64_t* tcgen05_gemms, int64_t* f64_convs);
 

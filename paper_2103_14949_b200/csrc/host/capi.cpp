@@ -31,6 +31,7 @@
 #include "quantc/topology.hpp"
 #ifdef QUANTC_B200
 #include "quantc/device.hpp"
+#include "quantc_cuda.h"
 #endif
 
 using namespace quantc;
@@ -740,6 +741,20 @@ int qc_evaluator_strategy(const qc_evaluator* e, const int* cand, size_t n_slots
     *json = dup_string(doc.dump());
   });
 }
+
+#ifdef QUANTC_B200
+int qc_evaluator_agreement(const qc_evaluator* e, const int* cands, size_t n_cands,
+                           size_t n_slots, int64_t* counts) {
+  return run([&] {
+    std::vector<Candidate> cs;
+    for (size_t i = 0; i < n_cands; ++i) {
+      cs.emplace_back(cands + i * n_slots, cands + (i + 1) * n_slots);
+    }
+    auto v = e->ev->agreement_counts(std::span<const Candidate>(cs.data(), cs.size()));
+    for (size_t i = 0; i < v.size(); ++i) counts[i] = v[i];
+  });
+}
+#endif
 
 int qc_evaluator_evaluations(const qc_evaluator* e, int64_t* out) {
   return run([&] { *out = e->ev->evaluations(); });

@@ -170,6 +170,22 @@ int qcu_set_engine_mode(int mode) {
   });
 }
 
+void* qcu_engine_stream(void) {
+  try {
+    return device::stream();
+  } catch (...) {
+    return nullptr;
+  }
+}
+
+int qcu_profile_enable(int on) {
+  return wrap([&] { device::profile_enable(on != 0); });
+}
+
+int qcu_profile_read(double* gemm_ms, int64_t* gemm_launches, double* gemm_ops) {
+  return wrap([&] { device::profile_read(gemm_ms, gemm_launches, gemm_ops); });
+}
+
 int qcu_counters(int64_t* steps, int64_t* tcgen05_gemms, int64_t* f64_convs) {
   const auto& c = device::counters();
   if (steps) *steps = c.kernel_launches;

@@ -6,6 +6,8 @@
 #include <cstdlib>
 #include <mutex>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "quantc/device.hpp"
 
@@ -88,6 +90,64 @@ size_t memory_budget_bytes() {
 Counters& counters() {
   static Counters c;
   return c;
+}
+
+namespace {
+struct Profile {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
+  std::vector<double> ops;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t take() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+Profile& prof() {
+  static Profile p;
+  return p;
+}
+}  // namespace
+
+void profile_enable(bool on) { prof().on = on; }
+bool profile_enabled() { return prof().on; }
+
+void profile_gemm_begin() {
+  Profile& p = prof();
+  cudaEvent_t a = p.take(), b = p.take();
+  cudaEventRecord(a, ctx().stream);
+  p.events.push_back({a, b});
+}
+
+void profile_gemm_end(double ops) {
+  Profile& p = prof();
+  cudaEventRecord(p.events.back().second, ctx().stream);
+  p.ops.push_back(ops);
+}
+
+void profile_read(double* gemm_ms, int64_t* gemm_launches, double* gemm_ops) {
+  Profile& p = prof();
+  synchronize();
+  double ms = 0.0, ops = 0.0;
+  for (size_t i = 0; i < p.events.size(); ++i) {
+    float t = 0.0f;
+    cudaEventElapsedTime(&t, p.events[i].first, p.events[i].second);
+    ms += t;
+    ops += p.ops[i];
+    p.pool.push_back(p.events[i].first);
+    p.pool.push_back(p.events[i].second);
+  }
+  if (gemm_ms) *gemm_ms = ms;
+  if (gemm_launches) *gemm_launches = static_cast<int64_t>(p.events.size());
+  if (gemm_ops) *gemm_ops = ops;
+  p.events.clear();
+  p.ops.clear();
 }
 
 }  // namespace quantc::device

@@ -485,8 +485,11 @@ void Runner::exec_conv_fast(int i, bool dense) {
   ep.bias = (st.in.size() > 2 && st.in[2] >= 0) ? vals[static_cast<size_t>(st.in[2])].f() : nullptr;
   ep.scale = sqp[static_cast<size_t>(d)].s * sqp[static_cast<size_t>(w)].s;
   ep.OHW = OH * OW;
+  const bool prof = device::profile_enabled();
+  if (prof) device::profile_gemm_begin();
   kern::gemm_s8_tcgen05(A, static_cast<const int8_t*>(wcodes.get()), static_cast<int>(M), O, Kpad,
                         ep, S());
+  if (prof) device::profile_gemm_end(2.0 * static_cast<double>(M) * O * C * KH * KW);
   device::counters().tcgen05_gemms++;
   vals[static_cast<size_t>(i)] = y;
 }
@@ -738,7 +741,6 @@ std::vector<DevTensor> run(const Plan& plan, const RunSpec& spec) {
   const int n = static_cast<int>(plan.steps().size());
   for (int i = 0; i < n; ++i) {
     r.exec(i);
-    device::counters().kernel_launches++;
     if (spec.on_value) spec.on_value(i, r.vals[static_cast<size_t>(i)]);
     r.release_inputs(i);
   }

@@ -8,10 +8,12 @@
 #include <string>
 
 #include "common.cuh"
+#include "quantc/device.hpp"
 
 namespace quantc::kern {
 
 void check_launch(const char* file, int line) {
+  ++quantc::device::counters().kernel_launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     throw std::runtime_error(std::string("CUDA launch failed at ") + file + ":" +

@@ -38,7 +38,10 @@ class CudaOps:
 
     @staticmethod
     def _s():
-        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        # torch's default stream has handle 0, which the ABI reserves for the
+        # engine stream; pass cudaStreamLegacy (0x1) so kernels order with it
+        h = torch.cuda.current_stream().cuda_stream
+        return C.c_void_p(h if h else 1)
 
     @staticmethod
     def _p(t):
