@@ -65,11 +65,18 @@ namespace {
 thread_local std::string g_last_error;
 thread_local int64_t g_ovf[3] = {-1, -1, 0};
 
+struct BufferTooSmall : std::runtime_error {
+  BufferTooSmall() : std::runtime_error("caller buffer too small") {}
+};
+
 template <typename F>
 int guarded(F&& f) {
   try {
     f();
     return QC_OK;
+  } catch (const BufferTooSmall& e) {
+    g_last_error = e.what();
+    return QC_ERR_BUFFER;
   } catch (const OverflowError& e) {
     g_last_error = e.what();
     g_ovf[0] = e.node;
@@ -110,10 +117,6 @@ int guarded(F&& f) {
     return QC_ERR_INTERNAL;
   }
 }
-
-struct BufferTooSmall : std::runtime_error {
-  BufferTooSmall() : std::runtime_error("caller buffer too small") {}
-};
 
 int run(const std::function<void()>& f) {
   try {
