@@ -40,6 +40,7 @@ struct Counters {
   int64_t kernel_launches = 0;  // every sm_100a kernel this library launched
   int64_t tcgen05_gemms = 0;
   int64_t f64_convs = 0;
+  int64_t fused_batches = 0;  // batches evaluated by the fused int8 dataflow (engine v2)
 };
 Counters& counters();
 

@@ -82,7 +82,8 @@ int qcu_profile_read(double* gemm_ms, int64_t* gemm_launches, double* gemm_ops);
 int qc_evaluator_agreement(const qc_evaluator* e, const int* cands, size_t n_cands,
                            size_t n_slots, int64_t* counts);
 /* counters since load: kernel launches issued by the engine, tcgen05 GEMMs */
-int qcu_counters(int64_t* steps, int64_t* tcgen05_gemms, int64_t* f64_convs);
+int qcu_counters(int64_t* steps, int64_t* tcgen05_gemms, int64_t* f64_convs,
+                 int64_t* fused_batches);
 
 #ifdef __cplusplus
 }

@@ -186,7 +186,9 @@ int qcu_profile_read(double* gemm_ms, int64_t* gemm_launches, double* gemm_ops) 
   return wrap([&] { device::profile_read(gemm_ms, gemm_launches, gemm_ops); });
 }
 
-int qcu_counters(int64_t* steps, int64_t* tcgen05_gemms, int64_t* f64_convs) {
+int qcu_counters(int64_t* steps, int64_t* tcgen05_gemms, int64_t* f64_convs,
+                 int64_t* fused_batches) {
+  if (fused_batches) *fused_batches = device::counters().fused_batches;
   const auto& c = device::counters();
   if (steps) *steps = c.kernel_launches;
   if (tcgen05_gemms) *tcgen05_gemms = c.tcgen05_gemms;

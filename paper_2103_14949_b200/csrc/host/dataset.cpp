@@ -3,8 +3,11 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
+#include <string>
 
+#include "fastplan.hpp"
 #include "quantc/device.hpp"
 
 namespace quantc::gpu {
@@ -58,6 +61,29 @@ std::shared_ptr<void> predict_device(const engine::Plan& plan, const DeviceDatas
   if (g.outputs().empty()) throw EvalError("model has no outputs");
   const int out_step = plan.step_of(g.outputs()[0].node);
   auto preds = engine::device_alloc(static_cast<size_t>(std::max<int64_t>(1, dd.size())) * 8);
+  // engine v2: fused int8 dataflow, when the graph compiles and the binding is
+  // eligible (power-of-two scales in auto mode => bit-identical)
+  const auto mode = device::engine_mode();
+  const char* fused_env = std::getenv("QUANTC_FUSED");
+  const bool fused_on = !(fused_env && std::string(fused_env) == "0");
+  if (allow_fast && !integer_regime && fused_on && mode != device::EngineMode::kExact &&
+      kern::gemm_s8_tcgen05_available()) {
+    if (!plan.fused_tried) {
+      plan.fused_tried = true;
+      plan.fused = std::make_shared<fast::FastPlan>(plan);
+    }
+    if (plan.fused->ok() &&
+        plan.fused->eligible(binding, mode == device::EngineMode::kAuto)) {
+      const int fb = std::min<int64_t>(std::max<int64_t>(1, dd.size()), 256);
+      for (int64_t first = 0; first < dd.size(); first += fb) {
+        const int b = static_cast<int>(std::min<int64_t>(fb, dd.size() - first));
+        std::vector<const float*> ins;
+        for (size_t k = 0; k < dd.num_inputs(); ++k) ins.push_back(dd.input(k, first));
+        plan.fused->predict(b, ins, binding, static_cast<int64_t*>(preds.get()) + first);
+      }
+      return preds;
+    }
+  }
   const int batch = plan.batch_for(dd.size());
   for (int64_t first = 0; first < dd.size(); first += batch) {
     const int b = static_cast<int>(std::min<int64_t>(batch, dd.size() - first));

@@ -23,6 +23,10 @@
 #include "quantc/interpreter.hpp"
 #include "../kernels/kernels.h"
 
+namespace quantc::fast {
+class FastPlan;
+}
+
 namespace quantc::engine {
 
 struct DevTensor {
@@ -72,6 +76,11 @@ class Plan {
   std::vector<std::vector<int64_t>> shapes_;
   std::vector<char> batched_;
   int64_t peak_bytes_ = 0;
+
+ public:
+  // lazily compiled fused int8 dataflow (engine v2) for this graph
+  mutable std::shared_ptr<fast::FastPlan> fused;
+  mutable bool fused_tried = false;
 };
 
 struct RunSpec {

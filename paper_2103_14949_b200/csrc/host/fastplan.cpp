@@ -1,0 +1,767 @@
+// fastplan.cpp — compiler + executor of the fused int8 dataflow (engine v2).
+#include "fastplan.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <limits>
+#include <set>
+
+#include "quantc/device.hpp"
+#include "quantc/simulate.hpp"
+
+namespace quantc::fast {
+
+using kern::FSq;
+using kern::ProgArgs;
+using kern::ProgBuf;
+using kern::ProgInstr;
+
+namespace {
+cudaStream_t S() { return static_cast<cudaStream_t>(device::stream()); }
+void ok_cuda(cudaError_t e) {
+  if (e != cudaSuccess) throw DeviceError(std::string("fastplan: ") + cudaGetErrorString(e));
+}
+int r16(int c) { return (c + 15) / 16 * 16; }
+
+struct Attr2 {
+  int a, b;
+};
+Attr2 pair_of(const Node& n, const char* key, Attr2 d) {
+  if (!n.has_attr(key)) return d;
+  auto v = n.attr<std::vector<int64_t>>(key);
+  return {static_cast<int>(v[0]), static_cast<int>(v[1])};
+}
+
+bool is_pow2(double t) {
+  if (!(t > 0.0) || !std::isfinite(t)) return false;
+  int e = 0;
+  return std::frexp(t, &e) == 0.5;
+}
+}  // namespace
+
+struct FastPlan::Val {
+  int step = -1;        // node whose value is stored
+  int sq_step = -1;     // sq that produced the codes (kind 0)
+  int kind = 0;         // 0 int8 codes, 1 fp32
+  int64_t rows_ps = 0;  // rows per sample in the (m, n) space
+  int C = 0;
+  int hw = 1, cs = 0;
+  int64_t ld = 0;
+  bool zero_fill = false;
+  int64_t bytes_ps() const {
+    return (rows_ps / hw) * ld * (kind == 0 ? 1 : 4);
+  }
+};
+
+struct FastPlan::Stage {
+  enum Kind { kInput, kGemm, kMaxpool, kGap } kind = kInput;
+  int step = -1;
+  int code_off = 0, code_len = 0;
+  int in_val = -1;
+  // input
+  int input_k = 0, n0 = 1, C = 0, HW = 1;
+  // gemm
+  bool dense = false, gather = false;
+  int w_sq = -1, w_const = -1, bias_const = -1;
+  int O = 0, KH = 1, KW = 1, sh = 1, sw = 1, ph = 0, pw = 0, H = 1, W = 1, OH = 1, OW = 1;
+  int taps = 1, ldk = 0, Ktrue = 0, Kpad = 0;
+  int64_t rows_out_ps = 0;
+  // pool
+  int pkh = 1, pkw = 1;
+};
+
+namespace {
+
+// per-element program builder
+struct Builder {
+  const engine::Plan& plan;
+  std::vector<ProgInstr>& code;
+  std::map<int, int>& sq_index;
+  std::vector<int>& sq_steps;
+  std::vector<float>& clip_lo;
+  std::vector<float>& clip_hi;
+  std::vector<std::unique_ptr<FastPlan::Val>>& vals;
+  std::map<int, int>& val_of;  // materialised step -> val index
+  std::set<int>& absorbed;
+  std::function<void(const std::string&)> fail;
+  // current register value space
+  int64_t rows_ps = 0;
+  int C = 0;
+  int flat_hw = 1, flat_cs = 0;
+  int depth = 0;
+  int* out_val = nullptr;
+  int64_t* out_per_sample = nullptr;
+
+  const Graph& g() const { return plan.graph(); }
+  const Node& node(int step) const { return *plan.steps()[static_cast<size_t>(step)].node; }
+
+  std::vector<std::pair<int, int>> consumers(int step) const {
+    std::vector<std::pair<int, int>> out;
+    for (const Edge* e : g().out_edges(node(step).id)) {
+      out.push_back({plan.step_of(e->dst.node), e->dst.port});
+    }
+    return out;
+  }
+  bool is_output(int step) const {
+    for (const PortRef& o : g().outputs()) {
+      if (o.node == node(step).id) return true;
+    }
+    return false;
+  }
+  int sq_slot(int step) {
+    auto it = sq_index.find(step);
+    if (it != sq_index.end()) return it->second;
+    const int s = static_cast<int>(sq_steps.size());
+    sq_index[step] = s;
+    sq_steps.push_back(step);
+    return s;
+  }
+  void op(uint8_t k, int a = 0, int b = 0) {
+    code.push_back(ProgInstr{k, 0, static_cast<uint16_t>(a), static_cast<uint32_t>(b)});
+  }
+  int make_val(int step, int sq_step, int kind, int64_t ld, int hw, int cs, bool zero) {
+    auto v = std::make_unique<FastPlan::Val>();
+    v->step = step;
+    v->sq_step = sq_step;
+    v->kind = kind;
+    v->rows_ps = rows_ps;
+    v->C = C;
+    v->hw = hw;
+    v->cs = cs;
+    v->ld = ld;
+    v->zero_fill = zero;
+    vals.push_back(std::move(v));
+    const int id = static_cast<int>(vals.size()) - 1;
+    val_of[step] = id;
+    return id;
+  }
+
+  // layout for the codes of sq `x` consumed by step `y` at `port`
+  bool codes_for(int x, int y, int port) {
+    const Node& ny = node(y);
+    int64_t ld = r16(C);
+    int hw = 1, cs = 0;
+    bool zero = false;
+    switch (ny.op) {
+      case OpKind::kConv2d: {
+        if (port != 0) {
+          fail("conv2d weight is not a constant");
+          return false;
+        }
+        if (flat_hw != 1) {
+          fail("conv2d after flatten");
+          return false;
+        }
+        const auto& ws = plan.shape(plan.steps()[static_cast<size_t>(y)].in[1]);
+        Attr2 st = pair_of(ny, "strides", {1, 1}), pd = pair_of(ny, "padding", {0, 0});
+        const bool direct = ws[2] == 1 && ws[3] == 1 && st.a == 1 && st.b == 1 && pd.a == 0 &&
+                            pd.b == 0 && C % 16 == 0;
+        ld = direct ? C : r16(C);
+        zero = ld != C;
+        break;
+      }
+      case OpKind::kDense:
+        if (port != 0) {
+          fail("dense weight is not a constant");
+          return false;
+        }
+        if (flat_hw > 1) {
+          hw = flat_hw;
+          cs = flat_cs;
+          ld = static_cast<int64_t>(flat_hw) * flat_cs;
+        } else {
+          ld = C;
+        }
+        if (ld % 16 != 0) {
+          fail("dense reduction not a multiple of 16 bytes");
+          return false;
+        }
+        break;
+      case OpKind::kMaxPool2d:
+      case OpKind::kAdd:
+        if (flat_hw != 1) {
+          fail("pool/add after flatten");
+          return false;
+        }
+        break;
+      default:
+        fail("unsupported consumer of a quantized edge: " + op_name(ny.op));
+        return false;
+    }
+    op(kern::kPSqStore8, sq_slot(x), make_val(x, x, 0, ld, hw, cs, zero));
+    return true;
+  }
+
+  void store_f32(int step, bool output) {
+    if (flat_hw != 1 && !output) {
+      fail("fp32 materialisation after flatten");
+      return;
+    }
+    const int v = make_val(step, -1, 1, C, 1, 0, false);
+    op(kern::kPStoreF32, 0, v);
+    if (output) {
+      // argmax runs over the per-sample tensor in reference (NCHW) order:
+      // identical to NHWC only when there is one pixel per row
+      const auto& shp = plan.shape(step);
+      int64_t pix = 1;
+      for (size_t i = 2; i < shp.size(); ++i) pix *= shp[i];
+      if (pix != 1 && C != 1) fail("4-D graph output with H*W > 1");
+      *out_val = v;
+      *out_per_sample = rows_ps * C;
+    }
+  }
+
+  // u's value is in the register
+  void emit(int u) {
+    auto cons = consumers(u);
+    const bool out = is_output(u);
+    const size_t n = cons.size() + (out ? 1 : 0);
+    for (size_t i = 0; i < n; ++i) {
+      const bool branch = i + 1 < n;
+      if (branch) {
+        if (++depth > 3) {
+          fail("fan-out deeper than the program stack");
+          return;
+        }
+        op(kern::kPPush);
+      }
+      if (i < cons.size()) {
+        handle(u, cons[i].first, cons[i].second);
+      } else {
+        store_f32(u, true);
+      }
+      if (branch) {
+        op(kern::kPPop);
+        --depth;
+      }
+    }
+  }
+
+  // consumer x of the register value u
+  void handle(int u, int x, int port) {
+    (void)u;
+    const Node& nx = node(x);
+    switch (nx.op) {
+      case OpKind::kSimulatedQuantize: {
+        absorbed.insert(x);
+        auto cy = consumers(x);
+        if (cy.empty()) {
+          op(kern::kPSq, sq_slot(x));
+          if (is_output(x)) store_f32(x, true);
+          return;
+        }
+        if (cy.size() > 1 || is_output(x)) {
+          fail("simulated_quantize with several consumers");
+          return;
+        }
+        const int y = cy[0].first;
+        const Node& ny = node(y);
+        switch (ny.op) {
+          case OpKind::kRelu:
+          case OpKind::kClip:
+          case OpKind::kFlatten:
+            op(kern::kPSq, sq_slot(x));
+            handle(x, y, cy[0].second);
+            return;
+          case OpKind::kAdd: {
+            const auto& yin = plan.steps()[static_cast<size_t>(y)].in;
+            const int other = yin[static_cast<size_t>(1 - cy[0].second)];
+            auto it = val_of.find(other);
+            if (it != val_of.end()) {
+              op(kern::kPSq, sq_slot(x));
+              op(kern::kPAdd, 0, it->second);
+              absorbed.insert(y);
+              emit(y);
+            } else {
+              codes_for(x, y, cy[0].second);
+            }
+            return;
+          }
+          case OpKind::kGlobalAvgPool2d:
+            op(kern::kPSq, sq_slot(x));
+            store_f32(x, false);
+            return;
+          default:
+            codes_for(x, y, cy[0].second);
+            return;
+        }
+      }
+      case OpKind::kRelu:
+        absorbed.insert(x);
+        op(kern::kPRelu);
+        emit(x);
+        return;
+      case OpKind::kClip: {
+        absorbed.insert(x);
+        if (!nx.has_attr("a_min")) {
+          fail("integer clip in the fp32 graph");
+          return;
+        }
+        clip_lo.push_back(static_cast<float>(nx.attr<double>("a_min")));
+        clip_hi.push_back(static_cast<float>(nx.attr<double>("a_max")));
+        op(kern::kPClip, static_cast<int>(clip_lo.size()) - 1);
+        emit(x);
+        return;
+      }
+      case OpKind::kFlatten: {
+        absorbed.insert(x);
+        if (flat_hw != 1) {
+          fail("double flatten");
+          return;
+        }
+        const auto& in_shape = plan.shape(plan.steps()[static_cast<size_t>(x)].in[0]);
+        int64_t hw = 1;
+        for (size_t i = 2; i < in_shape.size(); ++i) hw *= in_shape[i];
+        flat_hw = static_cast<int>(hw);
+        flat_cs = C;
+        emit(x);
+        flat_hw = 1;
+        flat_cs = 0;
+        return;
+      }
+      default:
+        fail("operator " + op_name(nx.op) + " consumes an unquantized value (port " +
+             std::to_string(port) + ")");
+        return;
+    }
+  }
+};
+
+FSq make_fsq(const QParams& p) {
+  FSq f{};
+  f.passthrough = p.passthrough ? 1 : 0;
+  f.has_acc = p.acc_dtype.has_value() && p.acc_scale > 0.0;
+  double s = 1.0, qmin = 0, qmax = 0, zp = 0;
+  if (!p.passthrough) {
+    s = compute_scale(p.threshold, p.bit, p.sign);
+    QuantBounds b = quant_bounds(p.bit, p.sign);
+    qmin = static_cast<double>(b.qmin);
+    qmax = static_cast<double>(b.qmax);
+    zp = static_cast<double>(p.zero_point);
+  }
+  f.s = static_cast<float>(s);
+  f.inv_s = static_cast<float>(1.0 / s);
+  f.qmin = static_cast<float>(qmin);
+  f.qmax = static_cast<float>(qmax);
+  f.zp = static_cast<float>(zp);
+  if (f.has_acc) {
+    const double lo = static_cast<double>(p.acc_dtype->min_value()) * p.acc_scale;
+    const double hi = static_cast<double>(p.acc_dtype->max_value()) * p.acc_scale;
+    float lu = static_cast<float>(lo);
+    if (static_cast<double>(lu) < lo) lu = std::nextafter(lu, std::numeric_limits<float>::infinity());
+    float hd = static_cast<float>(hi);
+    if (static_cast<double>(hd) > hi) hd = std::nextafter(hd, -std::numeric_limits<float>::infinity());
+    f.lo_up = lu;
+    f.hi_dn = hd;
+    f.lo_rn = static_cast<float>(lo);
+    f.hi_rn = static_cast<float>(hi);
+    if (!p.passthrough) {
+      auto code = [&](double v) {
+        double q = std::round(v / s) + zp;
+        return static_cast<float>(std::clamp(q, qmin, qmax));
+      };
+      f.q_lo = code(lo);
+      f.q_hi = code(hi);
+    }
+  }
+  return f;
+}
+
+}  // namespace
+
+FastPlan::~FastPlan() = default;
+
+void FastPlan::fail(const std::string& why) {
+  if (ok_ || why_.empty()) why_ = why;
+  ok_ = false;
+}
+
+FastPlan::FastPlan(const engine::Plan& plan) : plan_(plan) {
+  ok_ = true;
+  try {
+    compile();
+  } catch (const std::exception& e) {
+    fail(std::string("compile: ") + e.what());
+  }
+}
+
+void FastPlan::compile() {
+  const auto& steps = plan_.steps();
+  std::vector<ProgInstr> code;
+  std::map<int, int> val_of;
+  std::set<int> absorbed;
+  Builder b{plan_, code, sq_index_, sq_steps_, clip_lo_, clip_hi_, vals_, val_of, absorbed,
+            [this](const std::string& w) { fail(w); }};
+  b.out_val = &out_val_;
+  b.out_per_sample = &out_per_sample_;
+  const Graph& g = plan_.graph();
+
+  for (size_t i = 0; i < steps.size() && ok_; ++i) {
+    const int step = static_cast<int>(i);
+    const Node& n = *steps[i].node;
+    if (absorbed.count(step)) continue;
+    auto st = std::make_unique<Stage>();
+    st->step = step;
+    st->code_off = static_cast<int>(code.size());
+    const auto& shp = plan_.shape(step);
+    switch (n.op) {
+      case OpKind::kConstant:
+        continue;  // weights / biases, consumed by GEMM stages
+      case OpKind::kSimulatedQuantize: {
+        // weight sq (constant input) belongs to its GEMM; anything else here
+        // was not reached by a program
+        const int src = steps[i].in[0];
+        if (src >= 0 && steps[static_cast<size_t>(src)].node->op == OpKind::kConstant) continue;
+        fail("simulated_quantize not reachable from a producing stage");
+        continue;
+      }
+      case OpKind::kInput: {
+        auto it = std::find(g.inputs().begin(), g.inputs().end(), n.id);
+        st->kind = Stage::kInput;
+        st->input_k = static_cast<int>(it - g.inputs().begin());
+        if (shp.size() == 4) {
+          st->n0 = static_cast<int>(shp[0]);
+          st->C = static_cast<int>(shp[1]);
+          st->HW = static_cast<int>(shp[2] * shp[3]);
+        } else if (shp.size() == 2) {
+          st->n0 = static_cast<int>(shp[0]);
+          st->C = static_cast<int>(shp[1]);
+          st->HW = 1;
+        } else {
+          fail("input rank");
+          continue;
+        }
+        b.rows_ps = static_cast<int64_t>(st->n0) * st->HW;
+        b.C = st->C;
+        break;
+      }
+      case OpKind::kConv2d:
+      case OpKind::kDense: {
+        st->kind = Stage::kGemm;
+        st->dense = n.op == OpKind::kDense;
+        const auto& in = steps[i].in;
+        if (in.size() < 2 || in[0] < 0 || in[1] < 0) {
+          fail("gemm inputs");
+          continue;
+        }
+        const Node& dsq = *steps[static_cast<size_t>(in[0])].node;
+        const Node& wsq = *steps[static_cast<size_t>(in[1])].node;
+        auto vit = val_of.find(in[0]);
+        if (dsq.op != OpKind::kSimulatedQuantize || vit == val_of.end() ||
+            vals_[static_cast<size_t>(vit->second)]->kind != 0) {
+          fail("conv/dense data input is not an int8 simulated_quantize");
+          continue;
+        }
+        if (wsq.op != OpKind::kSimulatedQuantize ||
+            steps[static_cast<size_t>(steps[static_cast<size_t>(in[1])].in[0])].node->op != OpKind::kConstant) {
+          fail("conv/dense weight is not a simulated-quantized constant");
+          continue;
+        }
+        st->in_val = vit->second;
+        st->w_sq = in[1];
+        st->w_const = steps[static_cast<size_t>(in[1])].in[0];
+        if (in.size() > 2 && in[2] >= 0) {
+          if (steps[static_cast<size_t>(in[2])].node->op != OpKind::kConstant ||
+              !steps[static_cast<size_t>(in[2])].node->payload->dtype().is_float()) {
+            fail("bias is not a float constant");
+            continue;
+          }
+          st->bias_const = in[2];
+        }
+        const Val& dv = *vals_[static_cast<size_t>(st->in_val)];
+        const auto& ws = plan_.shape(st->w_const);
+        st->O = static_cast<int>(ws[0]);
+        if (st->dense) {
+          st->Ktrue = static_cast<int>((dv.rows_ps / dv.hw) > 0 ? dv.ld : dv.ld);
+          st->Ktrue = static_cast<int>(dv.hw > 1 ? static_cast<int64_t>(dv.hw) * dv.cs : dv.C);
+          st->taps = dv.hw;
+          st->ldk = dv.hw > 1 ? dv.cs : dv.C;
+          st->gather = false;
+          st->rows_out_ps = dv.rows_ps / dv.hw;
+          b.rows_ps = st->rows_out_ps;
+        } else {
+          const auto& ds = plan_.shape(in[0]);
+          Attr2 strd = pair_of(n, "strides", {1, 1}), pad = pair_of(n, "padding", {0, 0});
+          st->H = static_cast<int>(ds[2]);
+          st->W = static_cast<int>(ds[3]);
+          st->KH = static_cast<int>(ws[2]);
+          st->KW = static_cast<int>(ws[3]);
+          st->sh = strd.a;
+          st->sw = strd.b;
+          st->ph = pad.a;
+          st->pw = pad.b;
+          st->OH = static_cast<int>(shp[2]);
+          st->OW = static_cast<int>(shp[3]);
+          st->n0 = static_cast<int>(ds[0]);
+          st->C = static_cast<int>(ds[1]);
+          st->taps = st->KH * st->KW;
+          st->gather = !(st->taps == 1 && st->sh == 1 && st->sw == 1 && st->ph == 0 &&
+                         st->pw == 0 && dv.ld == st->C);
+          st->ldk = st->gather ? static_cast<int>(dv.ld) : st->C;
+          st->Ktrue = st->gather ? st->taps * st->ldk : st->C;
+          st->rows_out_ps = static_cast<int64_t>(st->n0) * st->OH * st->OW;
+          b.rows_ps = st->rows_out_ps;
+        }
+        st->Kpad = (st->Ktrue + 127) / 128 * 128;
+        b.C = st->O;
+        absorbed.insert(in[1]);
+        break;
+      }
+      case OpKind::kMaxPool2d: {
+        st->kind = Stage::kMaxpool;
+        const int src = steps[i].in[0];
+        auto vit = val_of.find(src);
+        if (vit == val_of.end() || vals_[static_cast<size_t>(vit->second)]->kind != 0) {
+          fail("max_pool2d input is not int8 codes");
+          continue;
+        }
+        st->in_val = vit->second;
+        const auto& ds = plan_.shape(src);
+        auto k = n.attr<std::vector<int64_t>>("pool_size");
+        Attr2 strd = pair_of(n, "strides", {static_cast<int>(k[0]), static_cast<int>(k[1])});
+        Attr2 pad = pair_of(n, "padding", {0, 0});
+        st->n0 = static_cast<int>(ds[0]);
+        st->C = static_cast<int>(ds[1]);
+        st->H = static_cast<int>(ds[2]);
+        st->W = static_cast<int>(ds[3]);
+        st->OH = static_cast<int>(shp[2]);
+        st->OW = static_cast<int>(shp[3]);
+        st->pkh = static_cast<int>(k[0]);
+        st->pkw = static_cast<int>(k[1]);
+        st->sh = strd.a;
+        st->sw = strd.b;
+        st->ph = pad.a;
+        st->pw = pad.b;
+        b.rows_ps = static_cast<int64_t>(st->n0) * st->OH * st->OW;
+        b.C = st->C;
+        break;
+      }
+      case OpKind::kGlobalAvgPool2d: {
+        st->kind = Stage::kGap;
+        const int src = steps[i].in[0];
+        auto vit = val_of.find(src);
+        if (vit == val_of.end() || vals_[static_cast<size_t>(vit->second)]->kind != 1) {
+          fail("global_avg_pool2d input is not materialised fp32");
+          continue;
+        }
+        st->in_val = vit->second;
+        const auto& ds = plan_.shape(src);
+        st->n0 = static_cast<int>(ds[0]);
+        st->C = static_cast<int>(ds[1]);
+        st->HW = static_cast<int>(ds[2] * ds[3]);
+        b.rows_ps = st->n0;
+        b.C = st->C;
+        break;
+      }
+      default:
+        fail("operator " + op_name(n.op) + " (node " + std::to_string(n.id) +
+             ") outside the fused dataflow");
+        continue;
+    }
+    b.flat_hw = 1;
+    b.flat_cs = 0;
+    b.depth = 0;
+    b.emit(step);
+    st->code_len = static_cast<int>(code.size()) - st->code_off;
+    stages_.push_back(std::move(st));
+  }
+  if (ok_ && out_val_ < 0) fail("graph output not reached");
+  if (ok_ && sq_steps_.size() > 65535) fail("too many simulated_quantize nodes");
+  if (!ok_) return;
+  d_code_ = engine::device_alloc(std::max<size_t>(1, code.size()) * sizeof(ProgInstr));
+  ok_cuda(cudaMemcpyAsync(d_code_.get(), code.data(), code.size() * sizeof(ProgInstr),
+                          cudaMemcpyHostToDevice, S()));
+  device::synchronize();
+}
+
+bool FastPlan::eligible(const SimBinding* binding, bool exact, std::string* why) const {
+  if (!ok_) {
+    if (why) *why = why_;
+    return false;
+  }
+  std::set<int> coded;
+  for (const auto& v : vals_) {
+    if (v->kind == 0) coded.insert(v->sq_step);
+  }
+  for (const auto& st : stages_) {
+    if (st->kind == Stage::kGemm) coded.insert(st->w_sq);
+  }
+  auto check = [&](int step) -> bool {
+    const QParams p = engine::qparams_of(*plan_.steps()[static_cast<size_t>(step)].node, binding);
+    try {
+      engine::resolve_sq(p);
+    } catch (...) {
+      if (why) *why = "invalid QParams";
+      return false;
+    }
+    if (!p.passthrough) {
+      const double s = compute_scale(p.threshold, p.bit, p.sign);
+      if (exact && !is_pow2(s)) {
+        if (why) *why = "non power-of-two scale";
+        return false;
+      }
+      const float sf = static_cast<float>(s);
+      if (!(std::isfinite(sf) && sf > 0 && std::isfinite(1.0f / sf) && std::fpclassify(sf) == FP_NORMAL)) {
+        if (why) *why = "scale outside fp32 range";
+        return false;
+      }
+    }
+    if (p.acc_dtype.has_value() && p.acc_scale > 0.0) {
+      const double lo = static_cast<double>(p.acc_dtype->min_value()) * p.acc_scale;
+      if (!std::isfinite(static_cast<float>(lo))) {
+        if (why) *why = "accumulator bound outside fp32 range";
+        return false;
+      }
+    }
+    if (coded.count(step)) {
+      if (p.passthrough || p.sign != 1 || p.zero_point != 0 || p.bit > 8) {
+        if (why) *why = "materialised code is not int8";
+        return false;
+      }
+    }
+    return true;
+  };
+  for (int step : sq_steps_) {
+    if (!check(step)) return false;
+  }
+  for (const auto& st : stages_) {
+    if (st->kind == Stage::kGemm && !check(st->w_sq)) return false;
+  }
+  return true;
+}
+
+void FastPlan::ensure_arena(int batch) {
+  if (arena_batch_ == batch) return;
+  arena_.clear();
+  for (const auto& v : vals_) {
+    const size_t bytes = static_cast<size_t>(v->bytes_ps()) * batch;
+    auto buf = engine::device_alloc(bytes + 64);
+    if (v->zero_fill) ok_cuda(cudaMemsetAsync(buf.get(), 0, bytes + 64, S()));
+    arena_.push_back(buf);
+  }
+  d_bufs_ = engine::device_alloc(std::max<size_t>(1, vals_.size()) * sizeof(ProgBuf));
+  d_tables_ = engine::device_alloc((sq_steps_.size() + 1) * sizeof(FSq) +
+                                   (clip_lo_.size() + 1) * sizeof(float2));
+  arena_batch_ = batch;
+}
+
+void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
+                       const SimBinding* binding, int64_t* d_preds) {
+  ensure_arena(batch);
+  // ---- per-run tables: FSq per sq node, clip bounds, buffer descriptors
+  std::vector<FSq> fsq(sq_steps_.size());
+  std::vector<float> scale_of_sq_step;
+  std::map<int, float> scale_by_step;
+  for (size_t k = 0; k < sq_steps_.size(); ++k) {
+    const QParams p = engine::qparams_of(*plan_.steps()[static_cast<size_t>(sq_steps_[k])].node, binding);
+    fsq[k] = make_fsq(p);
+    scale_by_step[sq_steps_[k]] = fsq[k].s;
+  }
+  std::vector<float2> clips(clip_lo_.size());
+  for (size_t k = 0; k < clips.size(); ++k) clips[k] = make_float2(clip_lo_[k], clip_hi_[k]);
+  std::vector<ProgBuf> bufs(vals_.size());
+  for (size_t k = 0; k < vals_.size(); ++k) {
+    const Val& v = *vals_[k];
+    bufs[k] = ProgBuf{arena_[k].get(), v.ld, v.hw, v.cs, v.kind,
+                      v.kind == 0 ? scale_by_step.at(v.sq_step) : 1.0f};
+  }
+  const size_t fsq_bytes = fsq.size() * sizeof(FSq);
+  std::vector<uint8_t> tables(fsq_bytes + clips.size() * sizeof(float2) + 16);
+  std::memcpy(tables.data(), fsq.data(), fsq_bytes);
+  std::memcpy(tables.data() + fsq_bytes, clips.data(), clips.size() * sizeof(float2));
+  ok_cuda(cudaMemcpyAsync(d_tables_.get(), tables.data(), tables.size() - 16,
+                          cudaMemcpyHostToDevice, S()));
+  ok_cuda(cudaMemcpyAsync(d_bufs_.get(), bufs.data(), bufs.size() * sizeof(ProgBuf),
+                          cudaMemcpyHostToDevice, S()));
+  const auto* d_fsq = static_cast<const FSq*>(d_tables_.get());
+  const auto* d_clip = reinterpret_cast<const float2*>(static_cast<const uint8_t*>(d_tables_.get()) + fsq_bytes);
+  const auto* d_bufs = static_cast<const ProgBuf*>(d_bufs_.get());
+  const auto* d_code = static_cast<const ProgInstr*>(d_code_.get());
+
+  for (size_t si = 0; si < stages_.size(); ++si) {
+    const Stage& st = *stages_[si];
+    ProgArgs pa{d_code + st.code_off, st.code_len, 0, d_fsq, d_clip, d_bufs};
+    switch (st.kind) {
+      case Stage::kInput:
+        kern::stage_input(inputs.at(static_cast<size_t>(st.input_k)), batch * st.n0, st.C, st.HW,
+                          pa, S());
+        break;
+      case Stage::kMaxpool: {
+        const Val& v = *vals_[static_cast<size_t>(st.in_val)];
+        kern::stage_maxpool(static_cast<const int8_t*>(arena_[static_cast<size_t>(st.in_val)].get()),
+                            static_cast<int>(v.ld), scale_by_step.at(v.sq_step), batch * st.n0,
+                            st.C, st.H, st.W, st.OH, st.OW, st.pkh, st.pkw, st.sh, st.sw, st.ph,
+                            st.pw, pa, S());
+        break;
+      }
+      case Stage::kGap: {
+        const Val& v = *vals_[static_cast<size_t>(st.in_val)];
+        kern::stage_gap(static_cast<const float*>(arena_[static_cast<size_t>(st.in_val)].get()),
+                        v.ld, batch * st.n0, st.C, st.HW, pa, S());
+        break;
+      }
+      case Stage::kGemm: {
+        const Val& dv = *vals_[static_cast<size_t>(st.in_val)];
+        const int wslot = sq_index_.count(st.w_sq) ? sq_index_.at(st.w_sq) : -1;
+        const QParams wp = engine::qparams_of(*plan_.steps()[static_cast<size_t>(st.w_sq)].node, binding);
+        const FSq wf = wslot >= 0 ? fsq[static_cast<size_t>(wslot)] : make_fsq(wp);
+        std::string key(reinterpret_cast<const char*>(&wf), sizeof(FSq));
+        auto ck = std::make_pair(static_cast<int>(si), key);
+        auto it = wcache_.find(ck);
+        if (it == wcache_.end()) {
+          auto codes = engine::device_alloc(static_cast<size_t>(st.O) * st.Kpad);
+          kern::weight_codes_v2(plan_.constant(st.w_const).f(), static_cast<int8_t*>(codes.get()),
+                                st.O, st.dense ? (st.taps > 1 ? dv.cs : dv.C) : st.C, st.taps,
+                                st.ldk, st.Kpad, wf, S());
+          it = wcache_.emplace(ck, codes).first;
+        }
+        kern::TcConvSpec sp{};
+        sp.x = static_cast<const int8_t*>(arena_[static_cast<size_t>(st.in_val)].get());
+        sp.w = static_cast<const int8_t*>(it->second.get());
+        sp.M = st.rows_out_ps * batch;
+        sp.O = st.O;
+        sp.Kpad = st.Kpad;
+        sp.gather = st.gather ? 1 : 0;
+        sp.Ktrue = st.Ktrue;
+        sp.lda = static_cast<int>(st.dense ? dv.ld : dv.ld);
+        sp.Nimg = batch * st.n0;
+        sp.H = st.H;
+        sp.W = st.W;
+        sp.C = st.C;
+        sp.ld = static_cast<int>(dv.ld);
+        sp.KH = st.KH;
+        sp.KW = st.KW;
+        sp.sh = st.sh;
+        sp.sw = st.sw;
+        sp.ph = st.ph;
+        sp.pw = st.pw;
+        sp.OH = st.OH;
+        sp.OW = st.OW;
+        sp.bias = st.bias_const >= 0 ? plan_.constant(st.bias_const).f() : nullptr;
+        sp.scale = static_cast<double>(scale_by_step.count(dv.sq_step) ? scale_by_step.at(dv.sq_step) : 0.0f) *
+                   static_cast<double>(wf.s);
+        sp.prog = pa;
+        const bool prof = device::profile_enabled();
+        if (prof) device::profile_gemm_begin();
+        kern::tc_conv(sp, S());
+        if (prof) {
+          device::profile_gemm_end(2.0 * static_cast<double>(sp.M) * st.O *
+                                   (st.dense ? st.Ktrue : st.C * st.KH * st.KW));
+        }
+        device::counters().tcgen05_gemms++;
+        break;
+      }
+    }
+  }
+  const Val& ov = *vals_[static_cast<size_t>(out_val_)];
+  (void)ov;
+  device::counters().fused_batches++;
+  kern::argmax_rows(static_cast<const float*>(arena_[static_cast<size_t>(out_val_)].get()), batch,
+                    out_per_sample_, d_preds, S());
+}
+
+}  // namespace quantc::fast

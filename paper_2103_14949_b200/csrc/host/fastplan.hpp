@@ -1,0 +1,68 @@
+// fastplan.hpp — engine v2: the fused int8 dataflow for simulated-quantize
+// evaluation (internal to the B200 build).
+//
+// Compiles a simulated graph into stages, each = one producing operator
+// (graph input, tcgen05 conv/dense GEMM, max-pool on codes, GAP) + the
+// per-element program of everything elementwise hanging off it (consumer
+// simulated_quantize, relu, clip, residual add, flatten).  Values cross stage
+// boundaries as NHWC int8 codes (sq outputs) or fp32 rows (boundary values,
+// graph outputs).  See kernels/fused.h for the program ops and the exactness
+// argument (power-of-two scales).
+#pragma once
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "engine.hpp"
+
+namespace quantc::fast {
+
+class FastPlan {
+ public:
+  explicit FastPlan(const engine::Plan& plan);
+  ~FastPlan();
+  FastPlan(const FastPlan&) = delete;
+
+  bool ok() const { return ok_; }
+  const std::string& why_not() const { return why_; }
+
+  // Binding eligibility: every simulated_quantize resolvable to the fp32
+  // program form, every materialised code int8; `exact` additionally
+  // requires power-of-two scales (bit-identical to the reference).
+  bool eligible(const SimBinding* binding, bool exact, std::string* why = nullptr) const;
+
+  // Runs one batch; writes per-sample argmax of graph output 0 to preds.
+  void predict(int batch, const std::vector<const float*>& inputs, const SimBinding* binding,
+               int64_t* d_preds);
+
+  struct Val;
+  struct Stage;
+
+ private:
+  const engine::Plan& plan_;
+  bool ok_ = false;
+  std::string why_;
+  std::vector<std::unique_ptr<Val>> vals_;
+  std::vector<std::unique_ptr<Stage>> stages_;
+  std::map<int, int> sq_index_;  // sq step -> FSq table slot
+  std::vector<int> sq_steps_;
+  std::vector<float> clip_lo_, clip_hi_;
+  int out_val_ = -1;
+  int64_t out_per_sample_ = 0;
+  std::shared_ptr<void> d_code_;  // all programs, uploaded once
+  // per-batch arena
+  int arena_batch_ = -1;
+  std::vector<std::shared_ptr<void>> arena_;
+  std::shared_ptr<void> d_bufs_;
+  std::shared_ptr<void> d_tables_;  // FSq table + clip table
+  // weight code cache: (stage, FSq bytes) -> codes
+  std::map<std::pair<int, std::string>, std::shared_ptr<void>> wcache_;
+
+  void compile();
+  void fail(const std::string& why);
+  void ensure_arena(int batch);
+};
+
+}  // namespace quantc::fast

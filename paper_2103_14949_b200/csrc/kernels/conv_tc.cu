@@ -1,0 +1,398 @@
+// conv_tc.cu — engine v2 GEMM: persistent, warp-specialised tcgen05 int8
+// implicit-GEMM conv/dense with the fused per-element epilogue program.
+//
+//   D[m, n] = sum_k A[m, k] * B[n, k]          (int8 x int8 -> int32 in TMEM)
+//   v       = (float) RN53(D * s_x*s_w + bias[n])   (one DFMA: the reference's
+//             sequential double accumulator, exact for pow2 scales)
+//   program(v) -> consumer sq / relu / add / flatten -> int8 codes (NHWC)
+//
+// A comes either straight from an NHWC code tensor by TMA (1x1 stride-1
+// convs, dense; rows = pixels, K = channels) or is gathered per tap by the
+// producer warps with cp.async (implicit im2col for KxK / strided convs:
+// k = tap*ld + c, zero-fill for padding and c >= C) into the SWIZZLE_128B
+// K-major layout the UMMA descriptor expects.  B (weight codes [O, Kpad]) is
+// always TMA.
+//
+// CTA = 13 warps, persistent over output tiles (n fastest, so concurrent CTAs
+// share the A tile through L2):
+//   warps 0-7  epilogue (warp w reads TMEM lanes 32*(w%4).., column half w/4)
+//   warps 8-11 producers (cp.async gather; warp 8 lane 0 issues the TMAs)
+//   warp 12    TMEM allocator + single-thread tcgen05.mma issuer
+// Pipelines: S-stage smem ring (full/empty mbarriers) and a double-buffered
+// TMEM accumulator (tfull/tempty) so the epilogue of tile i overlaps the MMAs
+// of tile i+1.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <stdexcept>
+
+#include "fused.cuh"
+
+namespace quantc::kern {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 128;
+constexpr int UMMA_K = 32;
+constexpr int STAGES = 4;
+constexpr int EPI_WARPS = 8;
+constexpr int PROD_WARPS = 4;
+constexpr int MMA_WARP = EPI_WARPS + PROD_WARPS;
+constexpr int THREADS = (MMA_WARP + 1) * 32;
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t phase) {
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra W_%=;\n}\n" ::"r"(su32(b)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma2d(const CUtensorMap* m, uint64_t* bar, void* dst, int c0,
+                                      int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(su32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>(1) << 16) |
+         (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
+         (static_cast<uint64_t>(2) << 61);
+}
+__host__ __device__ constexpr uint32_t idesc(int m, int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(m >> 4) << 24);
+}
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t id,
+                                    uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void commit(uint64_t* b) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(b))
+      : "memory");
+}
+
+}  // namespace
+
+struct TcGeom {
+  const int8_t* x;  // gather source: NHWC codes [N*H*W, ld]
+  int N, H, W, C, ld, KH, KW, sh, sw, ph, pw, OH, OW;
+};
+
+struct TcArgs {
+  int M, N, K;   // GEMM dims (K multiple of 128)
+  int gather;
+  TcGeom g;
+  const float* bias;
+  double scale;
+  ProgArgs prog;
+  int m_tiles, n_tiles;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(THREADS, 1)
+    tc_conv_kernel(const __grid_constant__ CUtensorMap map_a,
+                   const __grid_constant__ CUtensorMap map_b, const TcArgs args) {
+  constexpr uint32_t A_BYTES = BM * BK;
+  constexpr uint32_t B_BYTES = BN * BK;
+  constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sa = smem;
+  uint8_t* sb = sa + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sb + STAGES * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nk = args.K / BK;
+  const int n_tiles_total = args.m_tiles * args.n_tiles;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      bar_init(&full[s], args.gather ? (PROD_WARPS * 32 + 1) : 1);
+      bar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      bar_init(&tfull[a], 1);
+      bar_init(&tempty[a], EPI_WARPS * 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == MMA_WARP) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     su32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp >= EPI_WARPS && warp < MMA_WARP) {
+    // ================= producers =================
+    const int p = threadIdx.x - EPI_WARPS * 32;  // 0..127 = tile row
+    if (!args.gather) {
+      if (p == 0) {
+        uint32_t it = 0;
+        for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+          const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
+          for (int kb = 0; kb < nk; ++kb, ++it) {
+            const int s = it % STAGES;
+            if (it >= STAGES) bar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+            bar_expect(&full[s], A_BYTES + B_BYTES);
+            tma2d(&map_a, &full[s], sa + s * A_BYTES, kb * BK, m0);
+            tma2d(&map_b, &full[s], sb + s * B_BYTES, kb * BK, n0);
+          }
+        }
+      }
+    } else {
+      const TcGeom& g = args.g;
+      const int taps = g.KH * g.KW;
+      uint32_t it = 0;
+      int pending = -1;  // stage whose copies are in flight but not yet arrived
+      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+        const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
+        const int64_t row = static_cast<int64_t>(m0) + p;
+        const bool row_ok = row < args.M;
+        int img = 0, ih0 = 0, iw0 = 0;
+        if (row_ok) {
+          const int ohw = g.OH * g.OW;
+          img = static_cast<int>(row / ohw);
+          const int rem = static_cast<int>(row % ohw);
+          ih0 = (rem / g.OW) * g.sh - g.ph;
+          iw0 = (rem % g.OW) * g.sw - g.pw;
+        }
+        const int8_t* ximg = g.x + static_cast<int64_t>(img) * g.H * g.W * g.ld;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES;
+          if (it >= STAGES) bar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+          if (p == 0) {
+            bar_expect(&full[s], B_BYTES);
+            tma2d(&map_b, &full[s], sb + s * B_BYTES, kb * BK, n0);
+          }
+          const uint32_t dst_row = su32(sa + s * A_BYTES) + p * 128;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int k = kb * BK + j * 16;
+            const int tap = k / g.ld;
+            const int c = k - tap * g.ld;
+            const int8_t* src = ximg;
+            uint32_t bytes = 0;
+            if (row_ok && tap < taps && c < g.C) {
+              const int kh = tap / g.KW, kw = tap - (tap / g.KW) * g.KW;
+              const int ih = ih0 + kh, iw = iw0 + kw;
+              if (ih >= 0 && ih < g.H && iw >= 0 && iw < g.W) {
+                src = ximg + (static_cast<int64_t>(ih) * g.W + iw) * g.ld + c;
+                bytes = 16;
+              }
+            }
+            const uint32_t dst = dst_row + ((j ^ (p & 7)) << 4);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                         "r"(bytes)
+                         : "memory");
+          }
+          asm volatile("cp.async.commit_group;" ::: "memory");
+          if (pending >= 0) {
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bar_arrive(&full[pending]);
+          }
+          pending = s;
+        }
+      }
+      if (pending >= 0) {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        bar_arrive(&full[pending]);
+      }
+    }
+  } else if (warp == MMA_WARP) {
+    // ================= MMA issuer =================
+    if (lane == 0) {
+      constexpr uint32_t id = idesc(BM, BN);
+      uint32_t it = 0, tl = 0;
+      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
+        const uint32_t acc = tl & 1;
+        if (tl >= 2) bar_wait(&tempty[acc], ((tl / 2) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES;
+          bar_wait(&full[s], (it / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t ab = su32(sa + s * A_BYTES), bb = su32(sb + s * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / UMMA_K; ++k) {
+            mma(d, desc_sw128(ab + k * UMMA_K), desc_sw128(bb + k * UMMA_K), id,
+                (kb | k) != 0 ? 1u : 0u);
+          }
+          commit(&empty[s]);
+        }
+        commit(&tfull[acc]);
+      }
+    }
+  } else {
+    // ================= epilogue =================
+    const int quarter = warp & 3;
+    const int half = warp >> 2;
+    const int r = quarter * 32 + lane;
+    uint32_t tl = 0;
+    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
+      const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
+      const uint32_t acc = tl & 1;
+      bar_wait(&tfull[acc], (tl / 2) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int64_t m = static_cast<int64_t>(m0) + r;
+      const uint32_t tbase = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 16) {
+        uint32_t d[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+            "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]),
+              "=r"(d[6]), "=r"(d[7]), "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]),
+              "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15])
+            : "r"(tbase + c0));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const int n = n0 + c0;
+        const int nvalid = args.N - n < 16 ? args.N - n : 16;
+        if (m < args.M && nvalid > 0) {
+          float v[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const double b = (args.bias && j < nvalid) ? static_cast<double>(__ldg(args.bias + n + j)) : 0.0;
+            v[j] = __double2float_rn(
+                __fma_rn(static_cast<double>(static_cast<int32_t>(d[j])), args.scale, b));
+          }
+          run_prog<16>(v, m, n, nvalid, args.prog);
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      bar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == MMA_WARP) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------------------------
+namespace {
+
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiled encoder() {
+  static EncodeTiled fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess || q != cudaDriverEntryPointSuccess) {
+      return static_cast<EncodeTiled>(nullptr);
+    }
+    return reinterpret_cast<EncodeTiled>(p);
+  }();
+  return fn;
+}
+
+// 2-D K-major map: rows x cols(K) bytes, row stride `stride` bytes
+CUtensorMap kmap(const void* base, int64_t rows, int64_t cols, int64_t stride, int box_rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(stride)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t es[2] = {1, 1};
+  if (encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box,
+                es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+    throw std::runtime_error("cuTensorMapEncodeTiled failed (conv_tc)");
+  }
+  return m;
+}
+
+int num_sms() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+template <int BN>
+void launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const TcArgs& a, cudaStream_t s) {
+  const size_t smem = 1024 + STAGES * (BM * BK + BN * BK) + 128;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    cudaFuncSetAttribute(tc_conv_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+  });
+  const int tiles = a.m_tiles * a.n_tiles;
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  tc_conv_kernel<BN><<<grid, THREADS, smem, s>>>(ma, mb, a);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+}  // namespace
+
+void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
+  TcArgs a{};
+  a.M = static_cast<int>(sp.M);
+  a.N = sp.O;
+  a.K = sp.Kpad;
+  a.gather = sp.gather;
+  a.g = TcGeom{sp.x, sp.Nimg, sp.H, sp.W, sp.C, sp.ld, sp.KH, sp.KW, sp.sh, sp.sw,
+               sp.ph, sp.pw, sp.OH, sp.OW};
+  a.bias = sp.bias;
+  a.scale = sp.scale;
+  a.prog = sp.prog;
+  const int BN = sp.O <= 64 ? 64 : (sp.O <= 128 ? 128 : 256);
+  a.m_tiles = static_cast<int>((sp.M + BM - 1) / BM);
+  a.n_tiles = (sp.O + BN - 1) / BN;
+  // A: direct 2-D map over the code rows (unused, but must be valid, when gathering)
+  const CUtensorMap ma = kmap(sp.x, sp.gather ? 1 : sp.M, sp.gather ? BK : sp.Ktrue,
+                              sp.gather ? BK : sp.lda, BM);
+  const CUtensorMap mb = kmap(sp.w, sp.O, sp.Kpad, sp.Kpad, BN);
+  if (BN == 64) {
+    launch_tc<64>(ma, mb, a, s);
+  } else if (BN == 128) {
+    launch_tc<128>(ma, mb, a, s);
+  } else {
+    launch_tc<256>(ma, mb, a, s);
+  }
+}
+
+}  // namespace quantc::kern

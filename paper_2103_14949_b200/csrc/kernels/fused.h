@@ -1,0 +1,86 @@
+// fused.h — the fused int8 dataflow (engine v2): per-element epilogue
+// programs and stage kernels.  Shared by host (fastplan.cpp) and device.
+//
+// A "program" is the chain of elementwise operators hanging off one
+// producing operator (conv/dense GEMM, max-pool, GAP, graph input), applied
+// per element in registers: the consumer-edge simulated_quantize nodes, relu
+// / clip, a residual add whose other operand is already materialised, and
+// identity reshapes (flatten).  Fan-out is expressed with PUSH/POP.  Values
+// leave the program as int8 codes (sq outputs feeding MAC/pool/add
+// consumers; NHWC rows) or fp32 (boundary values, graph outputs).
+//
+// Exactness: the fused engine only runs when every simulated_quantize of
+// the graph has a power-of-two scale (engine mode auto) — then
+// round(v/s) = roundf(v*2^-j), (q-zp)*s = q*2^j and the accumulator clamp
+// compares are exact in fp32 with host-rounded bounds (see FSq), so every
+// value equals the reference's double-precision result bit for bit.
+#pragma once
+
+#include <cstdint>
+
+#include <vector_types.h>
+
+namespace quantc::kern {
+
+enum ProgOpKind : uint8_t {
+  kPEnd = 0,
+  kPSq = 1,        // v = sq(v, sq[a])
+  kPSqStore8 = 2,  // v = sq(v, sq[a]); buf[b][m,n] = int8(q - zp)
+  kPRelu = 3,
+  kPClip = 4,      // v = clamp(v, clip[a].x, clip[a].y)
+  kPAdd = 5,       // v = v + value(buf[b][m,n])
+  kPStoreF32 = 6,  // buf[b][m,n] = v
+  kPPush = 7,
+  kPPop = 8,
+};
+
+struct ProgInstr {
+  uint8_t op;
+  uint8_t pad0;
+  uint16_t a;
+  uint32_t b;
+};
+
+// Simulated quantize in fp32 (pow2 scale).  Semantics of reference
+// simulate.cpp:64-78:
+//   v' = has_acc ? clamp((double)v, lo, hi) : v
+//   passthrough -> (float)v'
+//   q = clamp(round(v'/s) + zp, qmin, qmax);  out = (float)((q - zp) * s)
+// lo_up = smallest float >= lo, hi_dn = largest float <= hi, so
+// (double)v < lo  <=>  v < lo_up.  A clamped v' (possibly not a float) maps to
+// the host-computed codes q_lo / q_hi and floats lo_rn / hi_rn.
+struct FSq {
+  float lo_up, hi_dn;   // clamp tests
+  float lo_rn, hi_rn;   // (float)lo, (float)hi  (passthrough results)
+  float q_lo, q_hi;     // code of a clamped value
+  float inv_s, s;       // 2^-j, 2^j
+  float qmin, qmax, zp;
+  int32_t has_acc;
+  int32_t passthrough;
+  int32_t pad_[3];
+};
+
+// A materialised value: element (m, n) lives at
+//   base + (m / hw) * ld + (m % hw) * cs + n
+// (hw = 1, cs = 0 for plain NHWC rows; hw = H*W, cs = C for a flattened
+// [N, H*W*C] dense operand).  kind 0: int8 codes with value (code)*scale;
+// kind 1: fp32.
+struct ProgBuf {
+  void* ptr;
+  int64_t ld;
+  int32_t hw;
+  int32_t cs;
+  int32_t kind;
+  float scale;
+};
+
+struct ProgArgs {
+  const ProgInstr* code;
+  int32_t n_code;
+  int32_t pad_;
+  const FSq* sq;
+  const float2* clip;
+  const ProgBuf* bufs;
+};
+
+}  // namespace quantc::kern

@@ -108,4 +108,40 @@ void im2col_s8(const int8_t* x, int8_t* out, int N, int H, int W, int Cpad, int 
 void weights_to_codes(const float* w, int8_t* codes, int O, int C, int KH, int KW, int Cpad,
                       int Kpad, const SqParams& p, cudaStream_t s);
 
+// ---- engine v2: fused int8 dataflow (conv_tc.cu, stages.cu) ------------------
+}  // namespace quantc::kern
+#include "fused.h"
+namespace quantc::kern {
+
+struct TcConvSpec {
+  const int8_t* x;   // A source: NHWC codes (gather) or code rows (direct)
+  const int8_t* w;   // B: weight codes [O][Kpad]
+  int64_t M;         // output rows (pixels / samples)
+  int O;             // output channels
+  int Kpad;          // multiple of 128
+  int gather;        // 1: implicit im2col gather, 0: direct TMA rows
+  int Ktrue, lda;    // direct: valid K bytes per row, row stride
+  int Nimg, H, W, C, ld, KH, KW, sh, sw, ph, pw, OH, OW;  // gather geometry
+  const float* bias;
+  double scale;      // s_x * s_w
+  ProgArgs prog;
+};
+void tc_conv(const TcConvSpec& spec, cudaStream_t s);
+
+// weight codes [O][Kpad], k = tap*ldk + c, from OIHW float weights (taps =
+// KH*KW; a flattened dense is the taps = H*W case), fp32 sq (pow2 scale)
+void weight_codes_v2(const float* w, int8_t* codes, int O, int C, int taps, int ldk, int Kpad,
+                     const FSq& p, cudaStream_t s);
+// graph input NCHW fp32 -> program over (m = n*H*W + hw, c)
+void stage_input(const float* x, int N, int C, int HW, const ProgArgs& prog, cudaStream_t s);
+// max_pool2d over NHWC codes (value = code * scale) -> program
+void stage_maxpool(const int8_t* x, int ld, float scale, int N, int C, int H, int W, int OH,
+                   int OW, int kh, int kw, int sh, int sw, int ph, int pw, const ProgArgs& prog,
+                   cudaStream_t s);
+// global_avg_pool2d over NHWC values (fp32 rows, ld) -> program over (n, c)
+void stage_gap(const float* x, int64_t ld, int N, int C, int HW, const ProgArgs& prog,
+               cudaStream_t s);
+// generic elementwise stage over an (M, C) space: v = value(src) -> program
+void stage_ew(const ProgBuf& src, int64_t M, int C, const ProgArgs& prog, cudaStream_t s);
+
 }  // namespace quantc::kern

@@ -1,0 +1,187 @@
+// stages.cu — non-GEMM stages of the fused int8 dataflow (engine v2):
+// graph-input quantisation, max-pool on codes, global average pool, weight
+// codes.  Each evaluates the stage's epilogue program on its output.
+//
+// Semantics: max_pool2d on codes == max_pool2d on values because the value
+// map code -> code*s (s > 0) is monotone (reference interpreter.cpp:377-397,
+// padded taps skipped); GAP is the reference's sequential double sum over
+// h*W+w then / (H*W) (interpreter.cpp:412-417).
+#include <cfloat>
+
+#include "fused.cuh"
+
+namespace quantc::kern {
+
+namespace {
+
+// one thread per (m, 16-channel group); reads NCHW (strided by HW)
+__global__ void input_kernel(const float* __restrict__ x, int N, int C, int HW, ProgArgs prog) {
+  const int groups = (C + 15) / 16;
+  const int64_t total = static_cast<int64_t>(N) * HW * groups;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int grp = static_cast<int>(i % groups);
+    const int64_t m = i / groups;
+    const int64_t n = m / HW, hw = m % HW;
+    const int c0 = grp * 16;
+    const int nvalid = C - c0 < 16 ? C - c0 : 16;
+    float v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      v[j] = j < nvalid ? x[(n * C + c0 + j) * HW + hw] : 0.0f;
+    }
+    run_prog<16>(v, m, c0, nvalid, prog);
+  }
+}
+
+__global__ void maxpool_codes_kernel(const int8_t* __restrict__ x, int ld, float scale, int N,
+                                     int C, int H, int W, int OH, int OW, int kh, int kw, int sh,
+                                     int sw, int ph, int pw, ProgArgs prog) {
+  const int groups = (C + 15) / 16;
+  const int64_t total = static_cast<int64_t>(N) * OH * OW * groups;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int grp = static_cast<int>(i % groups);
+    const int64_t m = i / groups;
+    const int ow = static_cast<int>(m % OW);
+    const int oh = static_cast<int>((m / OW) % OH);
+    const int64_t n = m / (static_cast<int64_t>(OW) * OH);
+    const int c0 = grp * 16;
+    const int nvalid = C - c0 < 16 ? C - c0 : 16;
+    int best[16];
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) best[j] = -129;
+    for (int a = 0; a < kh; ++a) {
+      const int ih = oh * sh - ph + a;
+      if (ih < 0 || ih >= H) continue;
+      for (int b = 0; b < kw; ++b) {
+        const int iw = ow * sw - pw + b;
+        if (iw < 0 || iw >= W) continue;
+        any = true;
+        const int8_t* src = x + ((n * H + ih) * W + iw) * ld + c0;
+        if (nvalid == 16 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+          const int4 raw = *reinterpret_cast<const int4*>(src);
+          const int8_t* cc = reinterpret_cast<const int8_t*>(&raw);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) best[j] = max(best[j], static_cast<int>(cc[j]));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (j < nvalid) best[j] = max(best[j], static_cast<int>(src[j]));
+          }
+        }
+      }
+    }
+    float v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      v[j] = any ? __fmul_rn(static_cast<float>(best[j]), scale) : -FLT_MAX;
+    }
+    run_prog<16>(v, m, c0, nvalid, prog);
+  }
+}
+
+// one thread per (n, c): sequential double sum in h*W+w order
+__global__ void gap_rows_kernel(const float* __restrict__ x, int64_t ld, int N, int C, int HW,
+                                ProgArgs prog) {
+  const int groups = (C + 15) / 16;
+  const int64_t total = static_cast<int64_t>(N) * groups;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int grp = static_cast<int>(i % groups);
+    const int64_t n = i / groups;
+    const int c0 = grp * 16;
+    const int nvalid = C - c0 < 16 ? C - c0 : 16;
+    double acc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+    for (int hw = 0; hw < HW; ++hw) {
+      const float* row = x + (n * HW + hw) * ld + c0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j < nvalid) acc[j] = __dadd_rn(acc[j], static_cast<double>(row[j]));
+      }
+    }
+    float v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = __double2float_rn(__ddiv_rn(acc[j], static_cast<double>(HW)));
+    run_prog<16>(v, n, c0, nvalid, prog);
+  }
+}
+
+__global__ void ew_kernel(ProgBuf src, int64_t M, int C, ProgArgs prog) {
+  const int groups = (C + 15) / 16;
+  const int64_t total = M * groups;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int grp = static_cast<int>(i % groups);
+    const int64_t m = i / groups;
+    const int c0 = grp * 16;
+    const int nvalid = C - c0 < 16 ? C - c0 : 16;
+    float v[16];
+    load_values<16>(src, m, c0, nvalid, v);
+    run_prog<16>(v, m, c0, nvalid, prog);
+  }
+}
+
+__global__ void weight_codes_v2_kernel(const float* __restrict__ w, int8_t* __restrict__ codes,
+                                       int O, int C, int taps, int ldk, int Kpad, FSq p) {
+  const int64_t total = static_cast<int64_t>(O) * Kpad;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(i % Kpad);
+    const int o = static_cast<int>(i / Kpad);
+    const int tap = k / ldk, c = k - (k / ldk) * ldk;
+    int8_t code = 0;
+    if (tap < taps && c < C) {
+      const float v = w[(static_cast<int64_t>(o) * C + c) * taps + tap];
+      code = static_cast<int8_t>(static_cast<int>(__fsub_rn(fsq_code(v, p), p.zp)));
+    }
+    codes[i] = code;
+  }
+}
+
+}  // namespace
+
+void stage_input(const float* x, int N, int C, int HW, const ProgArgs& prog, cudaStream_t s) {
+  const int64_t total = static_cast<int64_t>(N) * HW * ((C + 15) / 16);
+  if (total <= 0) return;
+  input_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, N, C, HW, prog);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+void stage_maxpool(const int8_t* x, int ld, float scale, int N, int C, int H, int W, int OH,
+                   int OW, int kh, int kw, int sh, int sw, int ph, int pw, const ProgArgs& prog,
+                   cudaStream_t s) {
+  const int64_t total = static_cast<int64_t>(N) * OH * OW * ((C + 15) / 16);
+  if (total <= 0) return;
+  maxpool_codes_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, ld, scale, N, C, H, W, OH, OW, kh,
+                                                            kw, sh, sw, ph, pw, prog);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+void stage_gap(const float* x, int64_t ld, int N, int C, int HW, const ProgArgs& prog,
+               cudaStream_t s) {
+  const int64_t total = static_cast<int64_t>(N) * ((C + 15) / 16);
+  if (total <= 0) return;
+  gap_rows_kernel<<<grid_for(total, 128), 128, 0, s>>>(x, ld, N, C, HW, prog);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+void stage_ew(const ProgBuf& src, int64_t M, int C, const ProgArgs& prog, cudaStream_t s) {
+  const int64_t total = M * ((C + 15) / 16);
+  if (total <= 0) return;
+  ew_kernel<<<grid_for(total, 256), 256, 0, s>>>(src, M, C, prog);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+void weight_codes_v2(const float* w, int8_t* codes, int O, int C, int taps, int ldk, int Kpad,
+                     const FSq& p, cudaStream_t s) {
+  const int64_t total = static_cast<int64_t>(O) * Kpad;
+  if (total <= 0) return;
+  weight_codes_v2_kernel<<<grid_for(total, 256), 256, 0, s>>>(w, codes, O, C, taps, ldk, Kpad, p);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+}  // namespace quantc::kern

@@ -30,7 +30,7 @@ class CudaOps:
                                   _P]
         L.qcu_synchronize.argtypes = [_P]
         L.qcu_set_engine_mode.argtypes = [C.c_int]
-        L.qcu_counters.argtypes = [C.POINTER(C.c_int64)] * 3
+        L.qcu_counters.argtypes = [C.POINTER(C.c_int64)] * 4
 
     def _ok(self, rc):
         if rc != 0:
@@ -118,9 +118,10 @@ class CudaOps:
         self._ok(self.lib.qcu_set_engine_mode({"exact": 0, "fast": 1, "auto": 2}[mode]))
 
     def counters(self):
-        v = [C.c_int64() for _ in range(3)]
+        v = [C.c_int64() for _ in range(4)]
         self.lib.qcu_counters(*[C.byref(x) for x in v])
-        return {"steps": v[0].value, "tcgen05_gemms": v[1].value, "f64_convs": v[2].value}
+        return {"steps": v[0].value, "tcgen05_gemms": v[1].value, "f64_convs": v[2].value,
+                "fused_batches": v[3].value}
 
 
 _ops = None

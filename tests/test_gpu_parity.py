@@ -193,3 +193,30 @@ def test_fast_engine_equals_exact_engine_pow2(b200, cuda_lib, small_cnn):
     assert cuda_lib.counters()["tcgen05_gemms"] > g0
     cuda_lib.set_engine_mode("auto")
     np.testing.assert_array_equal(exact, fast)
+
+
+@pytest.mark.parametrize("name,n", [("small_cnn", 16), ("resnet18", 8), ("resnet50", 4)])
+def test_fused_engine_bit_exact_vs_exact_engine(b200, cuda_lib, name, n):
+    """Engine v2 (fused NHWC int8 dataflow, tcgen05 implicit GEMM, fp32
+    epilogue programs) must reproduce the FP64 exact engine bit for bit on
+    power-of-two bindings: identical per-sample predictions and losses."""
+    m = {"small_cnn": lambda: F.small_cnn(),
+         "resnet18": lambda: F.resnet(18, image=64, classes=100),
+         "resnet50": lambda: F.resnet(50, image=64, classes=100)}[name]()
+    data = m.data(n)
+    p = _pipeline(b200, m, data, method="quantile", pow2=True, quantile=0.99)
+    sp = p["ev"].space()
+    rng = np.random.default_rng(11)
+    cands = [sp.all_hi(), sp.all_lo()] + [
+        [int(rng.integers(lo, hi + 1)) for lo, hi in zip(sp.lo, sp.hi)] for _ in range(3)]
+    cuda_lib.set_engine_mode("exact")
+    exact = p["ev"].losses(cands)
+    preds_exact = [b200.predict_top1(p["sim"], p["ds"], 0, p["ev"].bind(c)) for c in cands[:2]]
+    cuda_lib.set_engine_mode("auto")
+    f0 = cuda_lib.counters()["fused_batches"]
+    fused = p["ev"].losses(cands)
+    assert cuda_lib.counters()["fused_batches"] > f0, "fused engine was not used"
+    preds_fused = [b200.predict_top1(p["sim"], p["ds"], 0, p["ev"].bind(c)) for c in cands[:2]]
+    np.testing.assert_array_equal(exact, fused)
+    for a, b in zip(preds_exact, preds_fused):
+        np.testing.assert_array_equal(a, b)
