@@ -72,6 +72,12 @@ struct FastPlan::Stage {
   int64_t rows_out_ps = 0;
   // pool
   int pkh = 1, pkw = 1;
+  // program with stage-local indices (see kern::StageTables)
+  std::vector<ProgInstr> code;
+  std::vector<int> sq_slots;  // local sq index -> global FSq slot
+  std::vector<int> buf_vals;  // local buf index -> Val id
+  std::vector<int> clips;     // local clip index -> global clip id
+  int depth = 0;
 };
 
 namespace {
@@ -93,6 +99,7 @@ struct Builder {
   int C = 0;
   int flat_hw = 1, flat_cs = 0;
   int depth = 0;
+  int max_depth = 0;
   int* out_val = nullptr;
   int64_t* out_per_sample = nullptr;
 
@@ -227,6 +234,7 @@ struct Builder {
           fail("fan-out deeper than the program stack");
           return;
         }
+        max_depth = std::max(max_depth, depth);
         op(kern::kPPush);
       }
       if (i < cons.size()) {
@@ -565,17 +573,52 @@ void FastPlan::compile() {
     b.flat_hw = 1;
     b.flat_cs = 0;
     b.depth = 0;
+    b.max_depth = 0;
     b.emit(step);
     st->code_len = static_cast<int>(code.size()) - st->code_off;
+    st->depth = b.max_depth;
+    // re-index the stage's program against its own compact tables
+    std::map<int, int> lsq, lbuf, lclip;
+    for (int pc = st->code_off; pc < st->code_off + st->code_len; ++pc) {
+      ProgInstr ins = code[static_cast<size_t>(pc)];
+      auto local = [](std::map<int, int>& m, std::vector<int>& v, int g) {
+        auto it = m.find(g);
+        if (it != m.end()) return it->second;
+        const int l = static_cast<int>(v.size());
+        m[g] = l;
+        v.push_back(g);
+        return l;
+      };
+      switch (ins.op) {
+        case kern::kPSq:
+          ins.a = static_cast<uint16_t>(local(lsq, st->sq_slots, ins.a));
+          break;
+        case kern::kPSqStore8:
+          ins.a = static_cast<uint16_t>(local(lsq, st->sq_slots, ins.a));
+          ins.b = static_cast<uint32_t>(local(lbuf, st->buf_vals, static_cast<int>(ins.b)));
+          break;
+        case kern::kPAdd:
+        case kern::kPStoreF32:
+          ins.b = static_cast<uint32_t>(local(lbuf, st->buf_vals, static_cast<int>(ins.b)));
+          break;
+        case kern::kPClip:
+          ins.a = static_cast<uint16_t>(local(lclip, st->clips, ins.a));
+          break;
+        default:
+          break;
+      }
+      st->code.push_back(ins);
+    }
+    if (st->code.size() > static_cast<size_t>(kern::kMaxCode) ||
+        st->sq_slots.size() > static_cast<size_t>(kern::kMaxSq) ||
+        st->buf_vals.size() > static_cast<size_t>(kern::kMaxBuf) ||
+        st->clips.size() > static_cast<size_t>(kern::kMaxClip)) {
+      fail("stage program exceeds the StageTables limits");
+    }
     stages_.push_back(std::move(st));
   }
   if (ok_ && out_val_ < 0) fail("graph output not reached");
   if (ok_ && sq_steps_.size() > 65535) fail("too many simulated_quantize nodes");
-  if (!ok_) return;
-  d_code_ = engine::device_alloc(std::max<size_t>(1, code.size()) * sizeof(ProgInstr));
-  ok_cuda(cudaMemcpyAsync(d_code_.get(), code.data(), code.size() * sizeof(ProgInstr),
-                          cudaMemcpyHostToDevice, S()));
-  device::synchronize();
 }
 
 bool FastPlan::eligible(const SimBinding* binding, bool exact, std::string* why) const {
@@ -643,9 +686,7 @@ void FastPlan::ensure_arena(int batch) {
     if (v->zero_fill) ok_cuda(cudaMemsetAsync(buf.get(), 0, bytes + 64, S()));
     arena_.push_back(buf);
   }
-  d_bufs_ = engine::device_alloc(std::max<size_t>(1, vals_.size()) * sizeof(ProgBuf));
-  d_tables_ = engine::device_alloc((sq_steps_.size() + 1) * sizeof(FSq) +
-                                   (clip_lo_.size() + 1) * sizeof(float2));
+  d_tables_ = engine::device_alloc(std::max<size_t>(1, stages_.size()) * sizeof(kern::StageTables));
   arena_batch_ = batch;
 }
 
@@ -661,30 +702,36 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
     fsq[k] = make_fsq(p);
     scale_by_step[sq_steps_[k]] = fsq[k].s;
   }
-  std::vector<float2> clips(clip_lo_.size());
-  for (size_t k = 0; k < clips.size(); ++k) clips[k] = make_float2(clip_lo_[k], clip_hi_[k]);
-  std::vector<ProgBuf> bufs(vals_.size());
-  for (size_t k = 0; k < vals_.size(); ++k) {
-    const Val& v = *vals_[k];
-    bufs[k] = ProgBuf{arena_[k].get(), v.ld, v.hw, v.cs, v.kind,
-                      v.kind == 0 ? scale_by_step.at(v.sq_step) : 1.0f};
+  // one compact table block per stage (instructions + referenced params)
+  std::vector<kern::StageTables> tabs(stages_.size());
+  for (size_t si = 0; si < stages_.size(); ++si) {
+    const Stage& st = *stages_[si];
+    kern::StageTables& t = tabs[si];
+    std::memset(&t, 0, sizeof(t));
+    t.n_code = static_cast<int32_t>(st.code.size());
+    t.n_sq = static_cast<int32_t>(st.sq_slots.size());
+    t.n_buf = static_cast<int32_t>(st.buf_vals.size());
+    t.n_clip = static_cast<int32_t>(st.clips.size());
+    std::copy(st.code.begin(), st.code.end(), t.code);
+    for (size_t k = 0; k < st.sq_slots.size(); ++k) t.sq[k] = fsq[static_cast<size_t>(st.sq_slots[k])];
+    for (size_t k = 0; k < st.buf_vals.size(); ++k) {
+      const int vid = st.buf_vals[k];
+      const Val& v = *vals_[static_cast<size_t>(vid)];
+      t.buf[k] = ProgBuf{arena_[static_cast<size_t>(vid)].get(), v.ld, v.hw, v.cs, v.kind,
+                         v.kind == 0 ? scale_by_step.at(v.sq_step) : 1.0f};
+    }
+    for (size_t k = 0; k < st.clips.size(); ++k) {
+      const int c = st.clips[k];
+      t.clip[k] = make_float2(clip_lo_[static_cast<size_t>(c)], clip_hi_[static_cast<size_t>(c)]);
+    }
   }
-  const size_t fsq_bytes = fsq.size() * sizeof(FSq);
-  std::vector<uint8_t> tables(fsq_bytes + clips.size() * sizeof(float2) + 16);
-  std::memcpy(tables.data(), fsq.data(), fsq_bytes);
-  std::memcpy(tables.data() + fsq_bytes, clips.data(), clips.size() * sizeof(float2));
-  ok_cuda(cudaMemcpyAsync(d_tables_.get(), tables.data(), tables.size() - 16,
+  ok_cuda(cudaMemcpyAsync(d_tables_.get(), tabs.data(), tabs.size() * sizeof(kern::StageTables),
                           cudaMemcpyHostToDevice, S()));
-  ok_cuda(cudaMemcpyAsync(d_bufs_.get(), bufs.data(), bufs.size() * sizeof(ProgBuf),
-                          cudaMemcpyHostToDevice, S()));
-  const auto* d_fsq = static_cast<const FSq*>(d_tables_.get());
-  const auto* d_clip = reinterpret_cast<const float2*>(static_cast<const uint8_t*>(d_tables_.get()) + fsq_bytes);
-  const auto* d_bufs = static_cast<const ProgBuf*>(d_bufs_.get());
-  const auto* d_code = static_cast<const ProgInstr*>(d_code_.get());
+  const auto* d_tabs = static_cast<const kern::StageTables*>(d_tables_.get());
 
   for (size_t si = 0; si < stages_.size(); ++si) {
     const Stage& st = *stages_[si];
-    ProgArgs pa{d_code + st.code_off, st.code_len, 0, d_fsq, d_clip, d_bufs};
+    ProgArgs pa{d_tabs + si, st.depth, 0};
     switch (st.kind) {
       case Stage::kInput:
         kern::stage_input(inputs.at(static_cast<size_t>(st.input_k)), batch * st.n0, st.C, st.HW,

@@ -110,7 +110,35 @@ struct TcArgs {
   int m_tiles, n_tiles;
 };
 
-template <int BN>
+template <int W>
+__device__ __forceinline__ void tmem_ld(uint32_t addr, uint32_t (&d)[W]);
+
+template <>
+__device__ __forceinline__ void tmem_ld<16>(uint32_t addr, uint32_t (&d)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]),
+        "=r"(d[7]), "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]),
+        "=r"(d[14]), "=r"(d[15])
+      : "r"(addr));
+}
+
+template <>
+__device__ __forceinline__ void tmem_ld<32>(uint32_t addr, uint32_t (&d)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]),
+        "=r"(d[7]), "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]),
+        "=r"(d[14]), "=r"(d[15]), "=r"(d[16]), "=r"(d[17]), "=r"(d[18]), "=r"(d[19]),
+        "=r"(d[20]), "=r"(d[21]), "=r"(d[22]), "=r"(d[23]), "=r"(d[24]), "=r"(d[25]),
+        "=r"(d[26]), "=r"(d[27]), "=r"(d[28]), "=r"(d[29]), "=r"(d[30]), "=r"(d[31])
+      : "r"(addr));
+}
+
+template <int BN, int EW, int DEPTH>
 __global__ void __launch_bounds__(THREADS, 1)
     tc_conv_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b, const TcArgs args) {
@@ -127,6 +155,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  StageTables* tabs = reinterpret_cast<StageTables*>(tmem_slot + 4);
+  load_tables(tabs, args.prog.tables);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -272,27 +302,21 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int64_t m = static_cast<int64_t>(m0) + r;
       const uint32_t tbase = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
 #pragma unroll 1
-      for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 16) {
-        uint32_t d[16];
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-            "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]),
-              "=r"(d[6]), "=r"(d[7]), "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]),
-              "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15])
-            : "r"(tbase + c0));
+      for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += EW) {
+        uint32_t d[EW];
+        tmem_ld<EW>(tbase + c0, d);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         const int n = n0 + c0;
-        const int nvalid = args.N - n < 16 ? args.N - n : 16;
+        const int nvalid = args.N - n < EW ? args.N - n : EW;
         if (m < args.M && nvalid > 0) {
-          float v[16];
+          float v[EW];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
+          for (int j = 0; j < EW; ++j) {
             const double b = (args.bias && j < nvalid) ? static_cast<double>(__ldg(args.bias + n + j)) : 0.0;
             v[j] = __double2float_rn(
                 __fma_rn(static_cast<double>(static_cast<int32_t>(d[j])), args.scale, b));
           }
-          run_prog<16>(v, m, n, nvalid, args.prog);
+          run_prog<EW, DEPTH>(v, m, n, nvalid, *tabs);
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -352,18 +376,27 @@ int num_sms() {
   return n;
 }
 
-template <int BN>
+template <int BN, int EW, int DEPTH>
 void launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const TcArgs& a, cudaStream_t s) {
-  const size_t smem = 1024 + STAGES * (BM * BK + BN * BK) + 128;
+  const size_t smem = 1024 + STAGES * (BM * BK + BN * BK) + 128 + sizeof(StageTables);
   static std::once_flag once;
   std::call_once(once, [&] {
-    cudaFuncSetAttribute(tc_conv_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
+    cudaFuncSetAttribute(tc_conv_kernel<BN, EW, DEPTH>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   });
   const int tiles = a.m_tiles * a.n_tiles;
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  tc_conv_kernel<BN><<<grid, THREADS, smem, s>>>(ma, mb, a);
+  tc_conv_kernel<BN, EW, DEPTH><<<grid, THREADS, smem, s>>>(ma, mb, a);
   QC_CUDA_CHECK_LAUNCH();
+}
+
+template <int BN>
+void launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const TcArgs& a, cudaStream_t s) {
+  if (a.prog.depth <= 1) {
+    launch_tc<BN, 16, 1>(ma, mb, a, s);
+  } else {
+    launch_tc<BN, 16, 3>(ma, mb, a, s);
+  }
 }
 
 }  // namespace
@@ -387,11 +420,11 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
                               sp.gather ? BK : sp.lda, BM);
   const CUtensorMap mb = kmap(sp.w, sp.O, sp.Kpad, sp.Kpad, BN);
   if (BN == 64) {
-    launch_tc<64>(ma, mb, a, s);
+    launch_bn<64>(ma, mb, a, s);
   } else if (BN == 128) {
-    launch_tc<128>(ma, mb, a, s);
+    launch_bn<128>(ma, mb, a, s);
   } else {
-    launch_tc<256>(ma, mb, a, s);
+    launch_bn<256>(ma, mb, a, s);
   }
 }
 

@@ -1,6 +1,9 @@
 // fused.cuh — device side of the per-element epilogue programs (fused.h).
 // A thread evaluates one row m over W consecutive columns n0..n0+W-1 at once
-// (SIMD-in-thread), so codes leave as one W-byte vector store.
+// (SIMD-in-thread): every program op is a W-wide unrolled loop whose
+// per-op flags are tested once, and codes leave as W-byte vector stores.
+// The program and its parameters are read from the stage's StageTables block
+// in shared memory.
 #pragma once
 
 #include "common.cuh"
@@ -8,51 +11,105 @@
 
 namespace quantc::kern {
 
-// fp32 simulated quantize with host-rounded bounds (exact for pow2 scales)
+__device__ __forceinline__ float clampf_ref(float v, float lo, float hi) {
+  return (v < lo) ? lo : ((hi < v) ? hi : v);
+}
+
+// copy a StageTables block from global to shared memory (all threads)
+__device__ __forceinline__ void load_tables(StageTables* dst, const StageTables* src) {
+  const int words = static_cast<int>(sizeof(StageTables) / 16);
+  const int4* s = reinterpret_cast<const int4*>(src);
+  int4* d = reinterpret_cast<int4*>(dst);
+  for (int i = threadIdx.x; i < words; i += blockDim.x) d[i] = s[i];
+}
+
+// scalar code q (clamp + round) of one value
 __device__ __forceinline__ float fsq_code(float v, const FSq& p) {
-  if (p.has_acc) {
-    if (v < p.lo_up) return p.q_lo;
-    if (v > p.hi_dn) return p.q_hi;
-  }
-  float q = __fadd_rn(roundf(__fmul_rn(v, p.inv_s)), p.zp);
-  q = (q < p.qmin) ? p.qmin : ((p.qmax < q) ? p.qmax : q);
+  float q = clampf_ref(__fadd_rn(roundf(__fmul_rn(v, p.inv_s)), p.zp), p.qmin, p.qmax);
+  if (p.has_acc) q = (v < p.lo_up) ? p.q_lo : ((v > p.hi_dn) ? p.q_hi : q);
   return q;
 }
 
-__device__ __forceinline__ float fsq_value(float v, const FSq& p) {
+template <int W>
+__device__ __forceinline__ void sq_values(float (&v)[W], const FSq& p) {
   if (p.passthrough) {
     if (p.has_acc) {
-      if (v < p.lo_up) return p.lo_rn;
-      if (v > p.hi_dn) return p.hi_rn;
+      const float lu = p.lo_up, hd = p.hi_dn, lr = p.lo_rn, hr = p.hi_rn;
+#pragma unroll
+      for (int j = 0; j < W; ++j) v[j] = (v[j] < lu) ? lr : ((v[j] > hd) ? hr : v[j]);
     }
-    return v;
+    return;
   }
-  return __fmul_rn(__fsub_rn(fsq_code(v, p), p.zp), p.s);
+  const float inv = p.inv_s, s = p.s, zp = p.zp, qmin = p.qmin, qmax = p.qmax;
+  if (p.has_acc) {
+    const float lu = p.lo_up, hd = p.hi_dn, ql = p.q_lo, qh = p.q_hi;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      float q = clampf_ref(__fadd_rn(roundf(__fmul_rn(v[j], inv)), zp), qmin, qmax);
+      q = (v[j] < lu) ? ql : ((v[j] > hd) ? qh : q);
+      v[j] = __fmul_rn(__fsub_rn(q, zp), s);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      const float q = clampf_ref(__fadd_rn(roundf(__fmul_rn(v[j], inv)), zp), qmin, qmax);
+      v[j] = __fmul_rn(__fsub_rn(q, zp), s);
+    }
+  }
+}
+
+// as sq_values, also returning the integer codes q - zp
+template <int W>
+__device__ __forceinline__ void sq_codes(float (&v)[W], float (&c)[W], const FSq& p) {
+  const float inv = p.inv_s, s = p.s, zp = p.zp, qmin = p.qmin, qmax = p.qmax;
+  if (p.has_acc) {
+    const float lu = p.lo_up, hd = p.hi_dn, ql = p.q_lo, qh = p.q_hi;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      float q = clampf_ref(__fadd_rn(roundf(__fmul_rn(v[j], inv)), zp), qmin, qmax);
+      q = (v[j] < lu) ? ql : ((v[j] > hd) ? qh : q);
+      c[j] = __fsub_rn(q, zp);
+      v[j] = __fmul_rn(c[j], s);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      const float q = clampf_ref(__fadd_rn(roundf(__fmul_rn(v[j], inv)), zp), qmin, qmax);
+      c[j] = __fsub_rn(q, zp);
+      v[j] = __fmul_rn(c[j], s);
+    }
+  }
 }
 
 __device__ __forceinline__ int64_t buf_off(const ProgBuf& b, int64_t m, int n) {
-  return (m / b.hw) * b.ld + (m % b.hw) * b.cs + n;
+  return b.hw == 1 ? m * b.ld + n : (m / b.hw) * b.ld + (m % b.hw) * b.cs + n;
+}
+
+__device__ __forceinline__ uint32_t pack4(float a, float b, float c, float d) {
+  return (static_cast<uint32_t>(static_cast<uint8_t>(static_cast<int8_t>(__float2int_rn(a))))) |
+         (static_cast<uint32_t>(static_cast<uint8_t>(static_cast<int8_t>(__float2int_rn(b)))) << 8) |
+         (static_cast<uint32_t>(static_cast<uint8_t>(static_cast<int8_t>(__float2int_rn(c)))) << 16) |
+         (static_cast<uint32_t>(static_cast<uint8_t>(static_cast<int8_t>(__float2int_rn(d)))) << 24);
 }
 
 template <int W>
 __device__ __forceinline__ void store_codes(const ProgBuf& b, int64_t m, int n0, int nvalid,
                                             const float (&q)[W]) {
   int8_t* dst = static_cast<int8_t*>(b.ptr) + buf_off(b, m, n0);
-  if (W == 16 && nvalid == 16 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-    uint32_t w[4];
+  if (nvalid == W && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      w[i] = (static_cast<uint32_t>(static_cast<uint8_t>(static_cast<int8_t>(static_cast<int>(q[4 * i])))) |
-              (static_cast<uint32_t>(static_cast<uint8_t>(static_cast<int8_t>(static_cast<int>(q[4 * i + 1])))) << 8) |
-              (static_cast<uint32_t>(static_cast<uint8_t>(static_cast<int8_t>(static_cast<int>(q[4 * i + 2])))) << 16) |
-              (static_cast<uint32_t>(static_cast<uint8_t>(static_cast<int8_t>(static_cast<int>(q[4 * i + 3])))) << 24));
+    for (int i = 0; i < W / 16; ++i) {
+      const int o = 16 * i;
+      *reinterpret_cast<int4*>(dst + o) =
+          make_int4(static_cast<int>(pack4(q[o], q[o + 1], q[o + 2], q[o + 3])),
+                    static_cast<int>(pack4(q[o + 4], q[o + 5], q[o + 6], q[o + 7])),
+                    static_cast<int>(pack4(q[o + 8], q[o + 9], q[o + 10], q[o + 11])),
+                    static_cast<int>(pack4(q[o + 12], q[o + 13], q[o + 14], q[o + 15])));
     }
-    *reinterpret_cast<int4*>(dst) = make_int4(static_cast<int>(w[0]), static_cast<int>(w[1]),
-                                              static_cast<int>(w[2]), static_cast<int>(w[3]));
   } else {
 #pragma unroll
     for (int j = 0; j < W; ++j) {
-      if (j < nvalid) dst[j] = static_cast<int8_t>(static_cast<int>(q[j]));
+      if (j < nvalid) dst[j] = static_cast<int8_t>(__float2int_rn(q[j]));
     }
   }
 }
@@ -62,14 +119,20 @@ __device__ __forceinline__ void load_values(const ProgBuf& b, int64_t m, int n0,
                                             float (&o)[W]) {
   if (b.kind == 0) {
     const int8_t* src = static_cast<const int8_t*>(b.ptr) + buf_off(b, m, n0);
-    if (W == 16 && nvalid == 16 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-      const int4 raw = *reinterpret_cast<const int4*>(src);
-      const int8_t* c = reinterpret_cast<const int8_t*>(&raw);
+    const float sc = b.scale;
+    if (nvalid == W && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
 #pragma unroll
-      for (int j = 0; j < W; ++j) o[j] = __fmul_rn(static_cast<float>(c[j]), b.scale);
+      for (int i = 0; i < W / 16; ++i) {
+        const int4 raw = *reinterpret_cast<const int4*>(src + 16 * i);
+        const int8_t* cc = reinterpret_cast<const int8_t*>(&raw);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) o[16 * i + j] = __fmul_rn(static_cast<float>(cc[j]), sc);
+      }
     } else {
 #pragma unroll
-      for (int j = 0; j < W; ++j) o[j] = j < nvalid ? __fmul_rn(static_cast<float>(src[j]), b.scale) : 0.0f;
+      for (int j = 0; j < W; ++j) {
+        o[j] = j < nvalid ? __fmul_rn(static_cast<float>(src[j]), sc) : 0.0f;
+      }
     }
   } else {
     const float* src = static_cast<const float*>(b.ptr) + buf_off(b, m, n0);
@@ -78,29 +141,26 @@ __device__ __forceinline__ void load_values(const ProgBuf& b, int64_t m, int n0,
   }
 }
 
-template <int W>
+// DEPTH: number of PUSH slots the program may use (host-checked)
+template <int W, int DEPTH>
 __device__ __forceinline__ void run_prog(float (&v)[W], int64_t m, int n0, int nvalid,
-                                         const ProgArgs& a) {
-  float s0[W], s1[W], s2[W];
+                                         const StageTables& t) {
+  float s0[W];
+  float s1[DEPTH > 1 ? W : 1];
+  float s2[DEPTH > 2 ? W : 1];
   int sp = 0;
-  for (int pc = 0; pc < a.n_code; ++pc) {
-    const ProgInstr ins = a.code[pc];
+  const int n_code = t.n_code;
+#pragma unroll 1
+  for (int pc = 0; pc < n_code; ++pc) {
+    const ProgInstr ins = t.code[pc];
     switch (ins.op) {
-      case kPSq: {
-        const FSq p = a.sq[ins.a];
-#pragma unroll
-        for (int j = 0; j < W; ++j) v[j] = fsq_value(v[j], p);
+      case kPSq:
+        sq_values<W>(v, t.sq[ins.a]);
         break;
-      }
       case kPSqStore8: {
-        const FSq p = a.sq[ins.a];
         float q[W];
-#pragma unroll
-        for (int j = 0; j < W; ++j) {
-          q[j] = __fsub_rn(fsq_code(v[j], p), p.zp);
-          v[j] = __fmul_rn(q[j], p.s);
-        }
-        store_codes<W>(a.bufs[ins.b], m, n0, nvalid, q);
+        sq_codes<W>(v, q, t.sq[ins.a]);
+        store_codes<W>(t.buf[ins.b], m, n0, nvalid, q);
         break;
       }
       case kPRelu:
@@ -108,20 +168,20 @@ __device__ __forceinline__ void run_prog(float (&v)[W], int64_t m, int n0, int n
         for (int j = 0; j < W; ++j) v[j] = (v[j] < 0.0f) ? 0.0f : v[j];
         break;
       case kPClip: {
-        const float2 c = a.clip[ins.a];
+        const float2 c = t.clip[ins.a];
 #pragma unroll
-        for (int j = 0; j < W; ++j) v[j] = (v[j] < c.x) ? c.x : ((c.y < v[j]) ? c.y : v[j]);
+        for (int j = 0; j < W; ++j) v[j] = clampf_ref(v[j], c.x, c.y);
         break;
       }
       case kPAdd: {
         float o[W];
-        load_values<W>(a.bufs[ins.b], m, n0, nvalid, o);
+        load_values<W>(t.buf[ins.b], m, n0, nvalid, o);
 #pragma unroll
         for (int j = 0; j < W; ++j) v[j] = __fadd_rn(v[j], o[j]);
         break;
       }
       case kPStoreF32: {
-        const ProgBuf& b = a.bufs[ins.b];
+        const ProgBuf& b = t.buf[ins.b];
         float* dst = static_cast<float*>(b.ptr) + buf_off(b, m, n0);
 #pragma unroll
         for (int j = 0; j < W; ++j) {
@@ -130,29 +190,29 @@ __device__ __forceinline__ void run_prog(float (&v)[W], int64_t m, int n0, int n
         break;
       }
       case kPPush:
-        if (sp == 0) {
+        if (DEPTH <= 1 || sp == 0) {
 #pragma unroll
           for (int j = 0; j < W; ++j) s0[j] = v[j];
-        } else if (sp == 1) {
+        } else if (DEPTH <= 2 || sp == 1) {
 #pragma unroll
-          for (int j = 0; j < W; ++j) s1[j] = v[j];
+          for (int j = 0; j < W; ++j) s1[DEPTH > 1 ? j : 0] = v[j];
         } else {
 #pragma unroll
-          for (int j = 0; j < W; ++j) s2[j] = v[j];
+          for (int j = 0; j < W; ++j) s2[DEPTH > 2 ? j : 0] = v[j];
         }
         ++sp;
         break;
       case kPPop:
         --sp;
-        if (sp == 0) {
+        if (DEPTH <= 1 || sp == 0) {
 #pragma unroll
           for (int j = 0; j < W; ++j) v[j] = s0[j];
-        } else if (sp == 1) {
+        } else if (DEPTH <= 2 || sp == 1) {
 #pragma unroll
-          for (int j = 0; j < W; ++j) v[j] = s1[j];
+          for (int j = 0; j < W; ++j) v[j] = s1[DEPTH > 1 ? j : 0];
         } else {
 #pragma unroll
-          for (int j = 0; j < W; ++j) v[j] = s2[j];
+          for (int j = 0; j < W; ++j) v[j] = s2[DEPTH > 2 ? j : 0];
         }
         break;
       default:

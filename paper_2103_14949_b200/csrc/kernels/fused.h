@@ -9,6 +9,10 @@
 // leave the program as int8 codes (sq outputs feeding MAC/pool/add
 // consumers; NHWC rows) or fp32 (boundary values, graph outputs).
 //
+// Each stage gets a compact StageTables block (its instructions plus only the
+// sq parameters / buffers / clip bounds it references, re-indexed locally);
+// kernels stage it in shared memory once.
+//
 // Exactness: the fused engine only runs when every simulated_quantize of
 // the graph has a power-of-two scale (engine mode auto) — then
 // round(v/s) = roundf(v*2^-j), (q-zp)*s = q*2^j and the accumulator clamp
@@ -74,13 +78,24 @@ struct ProgBuf {
   float scale;
 };
 
+constexpr int kMaxCode = 48;
+constexpr int kMaxSq = 12;
+constexpr int kMaxBuf = 8;
+constexpr int kMaxClip = 4;
+
+struct StageTables {
+  int32_t n_code, n_sq, n_buf, n_clip;
+  ProgInstr code[kMaxCode];
+  FSq sq[kMaxSq];
+  ProgBuf buf[kMaxBuf];
+  float2 clip[kMaxClip];
+};
+
+// kernels receive the stage's table block in global memory
 struct ProgArgs {
-  const ProgInstr* code;
-  int32_t n_code;
+  const StageTables* tables;
+  int32_t depth;  // PUSH depth of the program
   int32_t pad_;
-  const FSq* sq;
-  const float2* clip;
-  const ProgBuf* bufs;
 };
 
 }  // namespace quantc::kern

@@ -16,6 +16,9 @@ namespace {
 
 // one thread per (m, 16-channel group); reads NCHW (strided by HW)
 __global__ void input_kernel(const float* __restrict__ x, int N, int C, int HW, ProgArgs prog) {
+  __shared__ StageTables T;
+  load_tables(&T, prog.tables);
+  __syncthreads();
   const int groups = (C + 15) / 16;
   const int64_t total = static_cast<int64_t>(N) * HW * groups;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -30,13 +33,16 @@ __global__ void input_kernel(const float* __restrict__ x, int N, int C, int HW, 
     for (int j = 0; j < 16; ++j) {
       v[j] = j < nvalid ? x[(n * C + c0 + j) * HW + hw] : 0.0f;
     }
-    run_prog<16>(v, m, c0, nvalid, prog);
+    run_prog<16, 3>(v, m, c0, nvalid, T);
   }
 }
 
 __global__ void maxpool_codes_kernel(const int8_t* __restrict__ x, int ld, float scale, int N,
                                      int C, int H, int W, int OH, int OW, int kh, int kw, int sh,
                                      int sw, int ph, int pw, ProgArgs prog) {
+  __shared__ StageTables T;
+  load_tables(&T, prog.tables);
+  __syncthreads();
   const int groups = (C + 15) / 16;
   const int64_t total = static_cast<int64_t>(N) * OH * OW * groups;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -78,13 +84,16 @@ __global__ void maxpool_codes_kernel(const int8_t* __restrict__ x, int ld, float
     for (int j = 0; j < 16; ++j) {
       v[j] = any ? __fmul_rn(static_cast<float>(best[j]), scale) : -FLT_MAX;
     }
-    run_prog<16>(v, m, c0, nvalid, prog);
+    run_prog<16, 3>(v, m, c0, nvalid, T);
   }
 }
 
 // one thread per (n, c): sequential double sum in h*W+w order
 __global__ void gap_rows_kernel(const float* __restrict__ x, int64_t ld, int N, int C, int HW,
                                 ProgArgs prog) {
+  __shared__ StageTables T;
+  load_tables(&T, prog.tables);
+  __syncthreads();
   const int groups = (C + 15) / 16;
   const int64_t total = static_cast<int64_t>(N) * groups;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -106,11 +115,14 @@ __global__ void gap_rows_kernel(const float* __restrict__ x, int64_t ld, int N, 
     float v[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = __double2float_rn(__ddiv_rn(acc[j], static_cast<double>(HW)));
-    run_prog<16>(v, n, c0, nvalid, prog);
+    run_prog<16, 3>(v, n, c0, nvalid, T);
   }
 }
 
 __global__ void ew_kernel(ProgBuf src, int64_t M, int C, ProgArgs prog) {
+  __shared__ StageTables T;
+  load_tables(&T, prog.tables);
+  __syncthreads();
   const int groups = (C + 15) / 16;
   const int64_t total = M * groups;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -121,7 +133,7 @@ __global__ void ew_kernel(ProgBuf src, int64_t M, int C, ProgArgs prog) {
     const int nvalid = C - c0 < 16 ? C - c0 : 16;
     float v[16];
     load_values<16>(src, m, c0, nvalid, v);
-    run_prog<16>(v, m, c0, nvalid, prog);
+    run_prog<16, 3>(v, m, c0, nvalid, T);
   }
 }
 
