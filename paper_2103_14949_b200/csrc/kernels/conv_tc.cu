@@ -106,6 +106,7 @@ struct TcArgs {
   TcGeom g;
   const float* bias;
   double scale;
+  float scale_f;  // scale as fp32 when exactly representable (normal), else 0
   ProgArgs prog;
   int m_tiles, n_tiles;
 };
@@ -310,11 +311,31 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int nvalid = args.N - n < EW ? args.N - n : EW;
         if (m < args.M && nvalid > 0) {
           float v[EW];
+          float bias[EW];
+#pragma unroll
+          for (int j = 0; j < EW; ++j) bias[j] = (args.bias && j < nvalid) ? __ldg(args.bias + n + j) : 0.0f;
+          // |acc| < 2^24 for every column: acc*s is an exact float and
+          // RN24(RN53(acc*s + b)) == RN24(acc*s + b) (53 >= 2*24+2: double
+          // rounding is innocuous), so the reference's double accumulator
+          // rounds to the same float as one fp32 add
+          bool small = args.scale_f != 0.0f;
 #pragma unroll
           for (int j = 0; j < EW; ++j) {
-            const double b = (args.bias && j < nvalid) ? static_cast<double>(__ldg(args.bias + n + j)) : 0.0;
-            v[j] = __double2float_rn(
-                __fma_rn(static_cast<double>(static_cast<int32_t>(d[j])), args.scale, b));
+            const int32_t a = static_cast<int32_t>(d[j]);
+            small = small && a < (1 << 24) && a > -(1 << 24);
+          }
+          if (small) {
+#pragma unroll
+            for (int j = 0; j < EW; ++j) {
+              v[j] = __fadd_rn(__fmul_rn(static_cast<float>(static_cast<int32_t>(d[j])), args.scale_f),
+                               bias[j]);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < EW; ++j) {
+              v[j] = __double2float_rn(__fma_rn(static_cast<double>(static_cast<int32_t>(d[j])),
+                                                args.scale, static_cast<double>(bias[j])));
+            }
           }
           run_prog<EW, DEPTH>(v, m, n, nvalid, *tabs);
         }
@@ -411,6 +432,10 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
                sp.ph, sp.pw, sp.OH, sp.OW};
   a.bias = sp.bias;
   a.scale = sp.scale;
+  {
+    const float f = static_cast<float>(sp.scale);
+    a.scale_f = (static_cast<double>(f) == sp.scale && std::fpclassify(f) == FP_NORMAL) ? f : 0.0f;
+  }
   a.prog = sp.prog;
   const int BN = sp.O <= 64 ? 64 : (sp.O <= 128 ? 128 : 256);
   a.m_tiles = static_cast<int>((sp.M + BM - 1) / BM);

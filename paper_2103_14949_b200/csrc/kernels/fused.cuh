@@ -15,6 +15,12 @@ __device__ __forceinline__ float clampf_ref(float v, float lo, float hi) {
   return (v < lo) ? lo : ((hi < v) ? hi : v);
 }
 
+// code clamp: identical to the reference's std::clamp for every non-NaN q
+// (the fused engine requires finite activations; NaN would saturate here)
+__device__ __forceinline__ float clampq(float q, float lo, float hi) {
+  return fminf(fmaxf(q, lo), hi);
+}
+
 // copy a StageTables block from global to shared memory (all threads)
 __device__ __forceinline__ void load_tables(StageTables* dst, const StageTables* src) {
   const int words = static_cast<int>(sizeof(StageTables) / 16);
@@ -25,7 +31,7 @@ __device__ __forceinline__ void load_tables(StageTables* dst, const StageTables*
 
 // scalar code q (clamp + round) of one value
 __device__ __forceinline__ float fsq_code(float v, const FSq& p) {
-  float q = clampf_ref(__fadd_rn(roundf(__fmul_rn(v, p.inv_s)), p.zp), p.qmin, p.qmax);
+  float q = clampq(__fadd_rn(roundf(__fmul_rn(v, p.inv_s)), p.zp), p.qmin, p.qmax);
   if (p.has_acc) q = (v < p.lo_up) ? p.q_lo : ((v > p.hi_dn) ? p.q_hi : q);
   return q;
 }
@@ -45,14 +51,14 @@ __device__ __forceinline__ void sq_values(float (&v)[W], const FSq& p) {
     const float lu = p.lo_up, hd = p.hi_dn, ql = p.q_lo, qh = p.q_hi;
 #pragma unroll
     for (int j = 0; j < W; ++j) {
-      float q = clampf_ref(__fadd_rn(roundf(__fmul_rn(v[j], inv)), zp), qmin, qmax);
+      float q = clampq(__fadd_rn(roundf(__fmul_rn(v[j], inv)), zp), qmin, qmax);
       q = (v[j] < lu) ? ql : ((v[j] > hd) ? qh : q);
       v[j] = __fmul_rn(__fsub_rn(q, zp), s);
     }
   } else {
 #pragma unroll
     for (int j = 0; j < W; ++j) {
-      const float q = clampf_ref(__fadd_rn(roundf(__fmul_rn(v[j], inv)), zp), qmin, qmax);
+      const float q = clampq(__fadd_rn(roundf(__fmul_rn(v[j], inv)), zp), qmin, qmax);
       v[j] = __fmul_rn(__fsub_rn(q, zp), s);
     }
   }
@@ -66,7 +72,7 @@ __device__ __forceinline__ void sq_codes(float (&v)[W], float (&c)[W], const FSq
     const float lu = p.lo_up, hd = p.hi_dn, ql = p.q_lo, qh = p.q_hi;
 #pragma unroll
     for (int j = 0; j < W; ++j) {
-      float q = clampf_ref(__fadd_rn(roundf(__fmul_rn(v[j], inv)), zp), qmin, qmax);
+      float q = clampq(__fadd_rn(roundf(__fmul_rn(v[j], inv)), zp), qmin, qmax);
       q = (v[j] < lu) ? ql : ((v[j] > hd) ? qh : q);
       c[j] = __fsub_rn(q, zp);
       v[j] = __fmul_rn(c[j], s);
@@ -74,7 +80,7 @@ __device__ __forceinline__ void sq_codes(float (&v)[W], float (&c)[W], const FSq
   } else {
 #pragma unroll
     for (int j = 0; j < W; ++j) {
-      const float q = clampf_ref(__fadd_rn(roundf(__fmul_rn(v[j], inv)), zp), qmin, qmax);
+      const float q = clampq(__fadd_rn(roundf(__fmul_rn(v[j], inv)), zp), qmin, qmax);
       c[j] = __fsub_rn(q, zp);
       v[j] = __fmul_rn(c[j], s);
     }
