@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 namespace quantc {
 
@@ -55,4 +56,18 @@ void profile_gemm_end(double ops);
 void profile_read(double* gemm_ms, int64_t* gemm_launches, double* gemm_ops);
 
 }  // namespace device
+
+class Graph;
+struct Sample;
+
+// Two-pass calibration pieces for sharded (multi-GPU) statistics: pass 1
+// exact extrema of the listed canonical edges over this shard; pass 2
+// histograms against the GLOBAL absmax (after the extrema all-reduce).
+// collect_stats == pass1 + absmax + pass2 on one shard.
+void collect_extrema(const Graph& g, const std::vector<Sample>& shard, const std::vector<int>& edges,
+                     std::vector<double>* mins, std::vector<double>* maxs);
+void collect_histograms(const Graph& g, const std::vector<Sample>& shard,
+                        const std::vector<int>& edges, const std::vector<double>& absmax, int bins,
+                        std::vector<int64_t>* counts /* edges x bins */);
+
 }  // namespace quantc

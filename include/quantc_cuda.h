@@ -81,6 +81,15 @@ int qcu_profile_read(double* gemm_ms, int64_t* gemm_launches, double* gemm_ops);
  * the multi-GPU driver all-reduces these (loss = 1 - sum / N_total). */
 int qc_evaluator_agreement(const qc_evaluator* e, const int* cands, size_t n_cands,
                            size_t n_slots, int64_t* counts);
+/* Sharded calibration (B200 extension; quantc/device.hpp): pass 1 extrema of
+ * the listed canonical edges over this process's shard, pass 2 histograms
+ * against the GLOBAL absmax.  A multi-GPU driver all-reduces min/max between
+ * the passes and sums the int64 counts after (paper_2103_14949_b200/parallel.py).
+ * counts: n x bins. */
+int qc_collect_extrema(const qc_graph* g, const qc_dataset* d, const int* edges, size_t n,
+                       double* mins, double* maxs);
+int qc_collect_histograms(const qc_graph* g, const qc_dataset* d, const int* edges, size_t n,
+                          const double* absmax, int bins, int64_t* counts);
 /* counters since load: kernel launches issued by the engine, tcgen05 GEMMs */
 int qcu_counters(int64_t* steps, int64_t* tcgen05_gemms, int64_t* f64_convs,
                  int64_t* fused_batches);

@@ -178,6 +178,110 @@ CalibrationStats collect_stats(const Graph& g, const Dataset& dataset, int bins,
   return stats;
 }
 
+namespace {
+
+// Shared driver of the sharded passes: batched forwards over `ds` with
+// `hook(slot, value, batch, batch_index)` on every target producer step.
+struct ShardPasses {
+  engine::Plan plan;
+  gpu::DeviceDataset dd;
+  std::unordered_map<int, int> slot_of_step;
+  std::vector<int> edge_slot;
+  int n_slots = 0;
+
+  ShardPasses(const Graph& g, const Dataset& ds, const std::vector<int>& edges_idx)
+      : plan(g), dd(g, ds) {
+    const std::vector<Edge> edges = edge_order(g);
+    for (int k : edges_idx) {
+      if (k < 0 || k >= static_cast<int>(edges.size())) {
+        throw CalibrationError("edge index " + std::to_string(k) + " out of range");
+      }
+      const int step = plan.step_of(edges[static_cast<size_t>(k)].src.node);
+      auto it = slot_of_step.find(step);
+      if (it == slot_of_step.end()) it = slot_of_step.emplace(step, n_slots++).first;
+      edge_slot.push_back(it->second);
+    }
+  }
+
+  template <typename Hook>
+  void forward(Hook&& hook) {
+    const int64_t N = dd.size();
+    const int batch = plan.batch_for(N);
+    int64_t bi = 0;
+    for (int64_t s0 = 0; s0 < N; s0 += batch, ++bi) {
+      const int b = static_cast<int>(std::min<int64_t>(batch, N - s0));
+      engine::RunSpec spec;
+      spec.batch = b;
+      for (size_t k = 0; k < dd.num_inputs(); ++k) spec.inputs.push_back(dd.input(k, s0));
+      spec.on_value = [&, b, bi](int step, const engine::DevTensor& v) {
+        auto it = slot_of_step.find(step);
+        if (it == slot_of_step.end()) return;
+        if (!v.dtype.is_float()) throw std::logic_error("floats() on " + v.dtype.name() + " tensor");
+        hook(it->second, v, b, bi);
+      };
+      engine::run(plan, spec);
+    }
+  }
+};
+
+}  // namespace
+
+void collect_extrema(const Graph& g, const Dataset& shard, const std::vector<int>& edges,
+                     std::vector<double>* mins, std::vector<double>* maxs) {
+  if (shard.empty()) throw CalibrationError("calibration dataset is empty");
+  ShardPasses sp(g, shard, edges);
+  auto keys = engine::device_alloc(static_cast<size_t>(sp.n_slots) * 16 + 16);
+  auto* k64 = static_cast<unsigned long long*>(keys.get());
+  kern::minmax_init(k64, sp.n_slots, S());
+  sp.forward([&](int slot, const engine::DevTensor& v, int b, int64_t bi) {
+    if (v.batched || bi == 0) kern::minmax_accumulate(v.f(), v.numel(b), k64 + 2 * slot, S());
+  });
+  std::vector<double> mm(static_cast<size_t>(sp.n_slots) * 2);
+  auto dmm = engine::device_alloc(mm.size() * 8 + 16);
+  kern::minmax_decode(k64, static_cast<double*>(dmm.get()), sp.n_slots, S());
+  ok(cudaMemcpyAsync(mm.data(), dmm.get(), mm.size() * 8, cudaMemcpyDeviceToHost, S()));
+  device::synchronize();
+  mins->clear();
+  maxs->clear();
+  for (int s : sp.edge_slot) {
+    mins->push_back(mm[2 * static_cast<size_t>(s)]);
+    maxs->push_back(mm[2 * static_cast<size_t>(s) + 1]);
+  }
+}
+
+void collect_histograms(const Graph& g, const Dataset& shard, const std::vector<int>& edges,
+                        const std::vector<double>& absmax, int bins,
+                        std::vector<int64_t>* counts) {
+  if (shard.empty()) throw CalibrationError("calibration dataset is empty");
+  if (bins < 2) throw CalibrationError("histogram needs at least 2 bins");
+  if (absmax.size() != edges.size()) throw std::invalid_argument("absmax per edge required");
+  ShardPasses sp(g, shard, edges);
+  std::vector<double> slot_absmax(static_cast<size_t>(sp.n_slots), 0.0);
+  for (size_t t = 0; t < edges.size(); ++t) slot_absmax[static_cast<size_t>(sp.edge_slot[t])] = absmax[t];
+  const int64_t N = sp.dd.size();
+  auto dc = engine::device_alloc(static_cast<size_t>(sp.n_slots) * bins * 8 + 16);
+  ok(cudaMemsetAsync(dc.get(), 0, static_cast<size_t>(sp.n_slots) * bins * 8, S()));
+  auto* c64 = static_cast<unsigned long long*>(dc.get());
+  sp.forward([&](int slot, const engine::DevTensor& v, int b, int64_t bi) {
+    if (v.batched) {
+      kern::histogram_accumulate(v.f(), v.numel(b), slot_absmax[static_cast<size_t>(slot)], bins,
+                                 c64 + static_cast<int64_t>(slot) * bins, 1ull, S());
+    } else if (bi == 0) {
+      kern::histogram_accumulate(v.f(), v.numel(b), slot_absmax[static_cast<size_t>(slot)], bins,
+                                 c64 + static_cast<int64_t>(slot) * bins,
+                                 static_cast<unsigned long long>(N), S());
+    }
+  });
+  std::vector<int64_t> hc(static_cast<size_t>(sp.n_slots) * bins);
+  ok(cudaMemcpyAsync(hc.data(), dc.get(), hc.size() * 8, cudaMemcpyDeviceToHost, S()));
+  device::synchronize();
+  counts->clear();
+  for (int s : sp.edge_slot) {
+    counts->insert(counts->end(), hc.begin() + static_cast<int64_t>(s) * bins,
+                   hc.begin() + static_cast<int64_t>(s + 1) * bins);
+  }
+}
+
 double threshold_max(const EdgeStats& stats) {
   return stats.absmax > 0.0 ? stats.absmax : kDegenerateThreshold;
 }

@@ -746,6 +746,26 @@ int qc_evaluator_strategy(const qc_evaluator* e, const int* cand, size_t n_slots
 }
 
 #ifdef QUANTC_B200
+int qc_collect_extrema(const qc_graph* g, const qc_dataset* d, const int* edges, size_t n,
+                       double* mins, double* maxs) {
+  return run([&] {
+    std::vector<double> lo, hi;
+    collect_extrema(*g->g, *d->d, std::vector<int>(edges, edges + n), &lo, &hi);
+    std::copy(lo.begin(), lo.end(), mins);
+    std::copy(hi.begin(), hi.end(), maxs);
+  });
+}
+
+int qc_collect_histograms(const qc_graph* g, const qc_dataset* d, const int* edges, size_t n,
+                          const double* absmax, int bins, int64_t* counts) {
+  return run([&] {
+    std::vector<int64_t> c;
+    collect_histograms(*g->g, *d->d, std::vector<int>(edges, edges + n),
+                       std::vector<double>(absmax, absmax + n), bins, &c);
+    std::copy(c.begin(), c.end(), counts);
+  });
+}
+
 int qc_evaluator_agreement(const qc_evaluator* e, const int* cands, size_t n_cands,
                            size_t n_slots, int64_t* counts) {
   return run([&] {
