@@ -78,6 +78,11 @@ struct FastPlan::Stage {
   std::vector<int> buf_vals;  // local buf index -> Val id
   std::vector<int> clips;     // local clip index -> global clip id
   int depth = 0;
+  // GEMM epilogue smem slots (kern::ProgBuf::slot) per local buffer
+  std::vector<int> buf_slot;
+  int n_out = 0;
+  int out_vals[2] = {-1, -1};
+  int res_val = -1;
 };
 
 namespace {
@@ -609,6 +614,39 @@ void FastPlan::compile() {
       }
       st->code.push_back(ins);
     }
+    // GEMM stages: route plain-row int8 code outputs (<= 2) and one residual
+    // operand through shared-memory tile slots (TMA store / TMA prefetch)
+    st->buf_slot.assign(st->buf_vals.size(), -1);
+    if (st->kind == Stage::kGemm) {
+      auto slot_ok = [&](int vid) {
+        const Val& v = *vals_[static_cast<size_t>(vid)];
+        return v.kind == 0 && v.hw == 1 && v.ld % 16 == 0 && v.rows_ps == st->rows_out_ps &&
+               v.C == st->O;
+      };
+      std::vector<int> produced;
+      for (const ProgInstr& ins : st->code) {
+        if (ins.op != kern::kPSqStore8) continue;
+        const int lb = static_cast<int>(ins.b);
+        produced.push_back(lb);
+        if (st->buf_slot[static_cast<size_t>(lb)] < 0 && st->n_out < 2 &&
+            slot_ok(st->buf_vals[static_cast<size_t>(lb)])) {
+          st->buf_slot[static_cast<size_t>(lb)] = st->n_out;
+          st->out_vals[st->n_out++] = st->buf_vals[static_cast<size_t>(lb)];
+        }
+      }
+      for (const ProgInstr& ins : st->code) {
+        if (ins.op != kern::kPAdd) continue;
+        const int lb = static_cast<int>(ins.b);
+        const bool mine = std::find(produced.begin(), produced.end(), lb) != produced.end();
+        if (!mine && st->res_val < 0 && slot_ok(st->buf_vals[static_cast<size_t>(lb)])) {
+          st->res_val = st->buf_vals[static_cast<size_t>(lb)];
+          st->buf_slot[static_cast<size_t>(lb)] = 2;  // fixed below to n_out
+        }
+      }
+      for (size_t k = 0; k < st->buf_slot.size(); ++k) {
+        if (st->buf_slot[k] == 2 && st->buf_vals[k] == st->res_val) st->buf_slot[k] = st->n_out;
+      }
+    }
     if (st->code.size() > static_cast<size_t>(kern::kMaxCode) ||
         st->sq_slots.size() > static_cast<size_t>(kern::kMaxSq) ||
         st->buf_vals.size() > static_cast<size_t>(kern::kMaxBuf) ||
@@ -718,7 +756,8 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
       const int vid = st.buf_vals[k];
       const Val& v = *vals_[static_cast<size_t>(vid)];
       t.buf[k] = ProgBuf{arena_[static_cast<size_t>(vid)].get(), v.ld, v.hw, v.cs, v.kind,
-                         v.kind == 0 ? scale_by_step.at(v.sq_step) : 1.0f};
+                         v.kind == 0 ? scale_by_step.at(v.sq_step) : 1.0f,
+                         k < st.buf_slot.size() ? st.buf_slot[k] : -1, 0};
     }
     for (size_t k = 0; k < st.clips.size(); ++k) {
       const int c = st.clips[k];
@@ -792,6 +831,19 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
         sp.scale = static_cast<double>(scale_by_step.count(dv.sq_step) ? scale_by_step.at(dv.sq_step) : 0.0f) *
                    static_cast<double>(wf.s);
         sp.prog = pa;
+        sp.n_out = st.n_out;
+        for (int o = 0; o < st.n_out; ++o) {
+          const Val& ov = *vals_[static_cast<size_t>(st.out_vals[o])];
+          sp.out_ptr[o] = arena_[static_cast<size_t>(st.out_vals[o])].get();
+          sp.out_cols[o] = ov.C;
+          sp.out_ld[o] = ov.ld;
+        }
+        if (st.res_val >= 0) {
+          const Val& rv = *vals_[static_cast<size_t>(st.res_val)];
+          sp.res_ptr = arena_[static_cast<size_t>(st.res_val)].get();
+          sp.res_cols = rv.C;
+          sp.res_ld = rv.ld;
+        }
         const bool prof = device::profile_enabled();
         if (prof) device::profile_gemm_begin();
         kern::tc_conv(sp, S());

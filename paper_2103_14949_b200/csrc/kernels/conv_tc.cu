@@ -2,8 +2,8 @@
 // implicit-GEMM conv/dense with the fused per-element epilogue program.
 //
 //   D[m, n] = sum_k A[m, k] * B[n, k]          (int8 x int8 -> int32 in TMEM)
-//   v       = (float) RN53(D * s_x*s_w + bias[n])   (one DFMA: the reference's
-//             sequential double accumulator, exact for pow2 scales)
+//   v       = (float) RN53(D * s_x*s_w + bias[n])   (the reference's
+//             sequential double accumulator; exact for pow2 scales)
 //   program(v) -> consumer sq / relu / add / flatten -> int8 codes (NHWC)
 //
 // A comes either straight from an NHWC code tensor by TMA (1x1 stride-1
@@ -13,17 +13,23 @@
 // K-major layout the UMMA descriptor expects.  B (weight codes [O, Kpad]) is
 // always TMA.
 //
+// Epilogue I/O goes through shared memory: up to two int8 code outputs are
+// written into swizzled 128 x BN tile slots and leave with TMA bulk-tensor
+// stores (full-line writes, no per-lane row-strided stores), and a residual
+// (add) operand is TMA-prefetched into a slot one tile ahead.
+//
 // CTA = 13 warps, persistent over output tiles (n fastest, so concurrent CTAs
 // share the A tile through L2):
 //   warps 0-7  epilogue (warp w reads TMEM lanes 32*(w%4).., column half w/4)
 //   warps 8-11 producers (cp.async gather; warp 8 lane 0 issues the TMAs)
 //   warp 12    TMEM allocator + single-thread tcgen05.mma issuer
-// Pipelines: S-stage smem ring (full/empty mbarriers) and a double-buffered
-// TMEM accumulator (tfull/tempty) so the epilogue of tile i overlaps the MMAs
-// of tile i+1.
+// Pipelines: S-stage smem ring (full/empty mbarriers), double-buffered TMEM
+// accumulator (tfull/tempty) so the epilogue of tile i overlaps the MMAs of
+// tile i+1, and the residual prefetch barrier (rfull).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <mutex>
 #include <stdexcept>
 
@@ -36,11 +42,12 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 128;
 constexpr int UMMA_K = 32;
-constexpr int STAGES = 4;
+constexpr int MAX_STAGES = 8;
 constexpr int EPI_WARPS = 8;
 constexpr int PROD_WARPS = 4;
 constexpr int MMA_WARP = EPI_WARPS + PROD_WARPS;
 constexpr int THREADS = (MMA_WARP + 1) * 32;
+constexpr int SMEM_LIMIT = 227 * 1024;
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -70,6 +77,17 @@ __device__ __forceinline__ void tma2d(const CUtensorMap* m, uint64_t* bar, void*
       " [%0], [%1, {%3, %4}], [%2];" ::"r"(su32(dst)),
       "l"(reinterpret_cast<uint64_t>(m)), "r"(su32(bar)), "r"(c0), "r"(c1)
       : "memory");
+}
+__device__ __forceinline__ void tma_store2d(const CUtensorMap* m, const void* src, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(m)),
+      "r"(su32(src)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void epi_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32) : "memory");
 }
 __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
   return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>(1) << 16) |
@@ -103,6 +121,9 @@ struct TcGeom {
 struct TcArgs {
   int M, N, K;   // GEMM dims (K multiple of 128)
   int gather;
+  int stages;    // runtime pipeline depth (<= MAX_STAGES)
+  int n_out;     // smem-staged code outputs (TMA store), 0..2
+  int has_res;   // TMA-prefetched residual slot (index n_out)
   TcGeom g;
   const float* bias;
   double scale;
@@ -125,37 +146,33 @@ __device__ __forceinline__ void tmem_ld<16>(uint32_t addr, uint32_t (&d)[16]) {
       : "r"(addr));
 }
 
-template <>
-__device__ __forceinline__ void tmem_ld<32>(uint32_t addr, uint32_t (&d)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]),
-        "=r"(d[7]), "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]),
-        "=r"(d[14]), "=r"(d[15]), "=r"(d[16]), "=r"(d[17]), "=r"(d[18]), "=r"(d[19]),
-        "=r"(d[20]), "=r"(d[21]), "=r"(d[22]), "=r"(d[23]), "=r"(d[24]), "=r"(d[25]),
-        "=r"(d[26]), "=r"(d[27]), "=r"(d[28]), "=r"(d[29]), "=r"(d[30]), "=r"(d[31])
-      : "r"(addr));
-}
-
-template <int BN, int EW, int DEPTH>
+template <int BN, int DEPTH>
 __global__ void __launch_bounds__(THREADS, 1)
     tc_conv_kernel(const __grid_constant__ CUtensorMap map_a,
-                   const __grid_constant__ CUtensorMap map_b, const TcArgs args) {
+                   const __grid_constant__ CUtensorMap map_b,
+                   const __grid_constant__ CUtensorMap map_o0,
+                   const __grid_constant__ CUtensorMap map_o1,
+                   const __grid_constant__ CUtensorMap map_r, const TcArgs args) {
+  constexpr int EW = 16;
   constexpr uint32_t A_BYTES = BM * BK;
   constexpr uint32_t B_BYTES = BN * BK;
+  constexpr uint32_t SLOT_BYTES = BM * BN;
+  constexpr int SWZ = BN >= 128 ? 128 : 64;
   constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  const int stages = args.stages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sa = smem;
-  uint8_t* sb = sa + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sb + STAGES * B_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint8_t* sb = sa + stages * A_BYTES;
+  uint8_t* slots = sb + stages * B_BYTES;  // 1024-aligned (stage sizes are multiples of 1 KB)
+  const int n_slots = args.n_out + args.has_res;
+  uint64_t* full = reinterpret_cast<uint64_t*>(slots + n_slots * SLOT_BYTES);
+  uint64_t* empty = full + MAX_STAGES;
+  uint64_t* tfull = empty + MAX_STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rfull = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 2);
   StageTables* tabs = reinterpret_cast<StageTables*>(tmem_slot + 4);
   load_tables(tabs, args.prog.tables);
 
@@ -165,7 +182,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int n_tiles_total = args.m_tiles * args.n_tiles;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < stages; ++s) {
       bar_init(&full[s], args.gather ? (PROD_WARPS * 32 + 1) : 1);
       bar_init(&empty[s], 1);
     }
@@ -173,6 +190,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       bar_init(&tfull[a], 1);
       bar_init(&tempty[a], EPI_WARPS * 32);
     }
+    bar_init(rfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == MMA_WARP) {
@@ -195,8 +213,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
           const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
           for (int kb = 0; kb < nk; ++kb, ++it) {
-            const int s = it % STAGES;
-            if (it >= STAGES) bar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+            const int s = it % stages;
+            if (it >= static_cast<uint32_t>(stages)) bar_wait(&empty[s], ((it / stages) - 1) & 1);
             bar_expect(&full[s], A_BYTES + B_BYTES);
             tma2d(&map_a, &full[s], sa + s * A_BYTES, kb * BK, m0);
             tma2d(&map_b, &full[s], sb + s * B_BYTES, kb * BK, n0);
@@ -222,18 +240,18 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         const int8_t* ximg = g.x + static_cast<int64_t>(img) * g.H * g.W * g.ld;
         for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % STAGES;
-          if (it >= STAGES) bar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+          const int s = it % stages;
+          if (it >= static_cast<uint32_t>(stages)) bar_wait(&empty[s], ((it / stages) - 1) & 1);
           if (p == 0) {
             bar_expect(&full[s], B_BYTES);
             tma2d(&map_b, &full[s], sb + s * B_BYTES, kb * BK, n0);
           }
           const uint32_t dst_row = su32(sa + s * A_BYTES) + p * 128;
+          // (tap, c) of the first chunk of this K block; chunks advance by 16
+          int tap = (kb * BK) / g.ld;
+          int c = kb * BK - tap * g.ld;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            const int k = kb * BK + j * 16;
-            const int tap = k / g.ld;
-            const int c = k - tap * g.ld;
             const int8_t* src = ximg;
             uint32_t bytes = 0;
             if (row_ok && tap < taps && c < g.C) {
@@ -248,6 +266,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
                          "r"(bytes)
                          : "memory");
+            c += 16;
+            if (c >= g.ld) {
+              c -= g.ld;
+              ++tap;
+            }
           }
           asm volatile("cp.async.commit_group;" ::: "memory");
           if (pending >= 0) {
@@ -275,8 +298,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + acc * BN;
         for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % STAGES;
-          bar_wait(&full[s], (it / STAGES) & 1);
+          const int s = it % stages;
+          bar_wait(&full[s], (it / stages) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t ab = su32(sa + s * A_BYTES), bb = su32(sb + s * B_BYTES);
 #pragma unroll
@@ -294,12 +317,29 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int quarter = warp & 3;
     const int half = warp >> 2;
     const int r = quarter * 32 + lane;
+    const bool leader = threadIdx.x == 0;
+    TileIo io{slots, r, static_cast<int>(SLOT_BYTES), SWZ};
+    auto load_res = [&](int t) {
+      const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
+      uint8_t* dst = slots + args.n_out * SLOT_BYTES;
+      bar_expect(rfull, SLOT_BYTES);
+      for (int blk = 0; blk < BN / SWZ; ++blk) {
+        tma2d(&map_r, rfull, dst + blk * (BM * SWZ), n0 + blk * SWZ, m0);
+      }
+    };
+    if (args.has_res && leader && static_cast<int>(blockIdx.x) < n_tiles_total) load_res(blockIdx.x);
     uint32_t tl = 0;
     for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
       const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
       const uint32_t acc = tl & 1;
       bar_wait(&tfull[acc], (tl / 2) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (args.n_out > 0) {
+        // the previous tile's TMA stores must have finished reading the slots
+        if (leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        epi_sync();
+      }
+      if (args.has_res) bar_wait(rfull, tl & 1);
       const int64_t m = static_cast<int64_t>(m0) + r;
       const uint32_t tbase = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
 #pragma unroll 1
@@ -337,12 +377,30 @@ __global__ void __launch_bounds__(THREADS, 1)
                                                 args.scale, static_cast<double>(bias[j])));
             }
           }
-          run_prog<EW, DEPTH>(v, m, n, nvalid, *tabs);
+          run_prog<EW, DEPTH>(v, m, n, nvalid, *tabs, &io, c0);
         }
       }
+      // publish slot writes to the async proxy, release TMEM, store the tile
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       bar_arrive(&tempty[acc]);
+      if (args.n_out > 0 || args.has_res) epi_sync();
+      if (leader) {
+        if (args.n_out > 0) {
+          for (int blk = 0; blk < BN / SWZ; ++blk) {
+            tma_store2d(&map_o0, slots + blk * (BM * SWZ), n0 + blk * SWZ, m0);
+            if (args.n_out > 1) {
+              tma_store2d(&map_o1, slots + SLOT_BYTES + blk * (BM * SWZ), n0 + blk * SWZ, m0);
+            }
+          }
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        if (args.has_res && t + static_cast<int>(gridDim.x) < n_tiles_total) {
+          load_res(t + gridDim.x);
+        }
+      }
     }
+    if (leader && args.n_out > 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   __syncthreads();
   if (warp == MMA_WARP) {
@@ -371,16 +429,19 @@ EncodeTiled encoder() {
   return fn;
 }
 
-// 2-D K-major map: rows x cols(K) bytes, row stride `stride` bytes
-CUtensorMap kmap(const void* base, int64_t rows, int64_t cols, int64_t stride, int box_rows) {
+// 2-D byte map: rows x cols, row stride `stride` bytes, box {box_cols, box_rows}
+CUtensorMap bmap(const void* base, int64_t rows, int64_t cols, int64_t stride, int box_cols,
+                 int box_rows, int swz) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(stride)};
-  const cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
   const cuuint32_t es[2] = {1, 1};
+  const CUtensorMapSwizzle sw = swz == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : swz == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                            : CU_TENSOR_MAP_SWIZZLE_NONE;
   if (encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box,
-                es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
     throw std::runtime_error("cuTensorMapEncodeTiled failed (conv_tc)");
   }
@@ -397,30 +458,42 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int EW, int DEPTH>
-void launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const TcArgs& a, cudaStream_t s) {
-  const size_t smem = 1024 + STAGES * (BM * BK + BN * BK) + 128 + sizeof(StageTables);
+template <int BN, int DEPTH>
+void launch_tc(const CUtensorMap* maps, TcArgs a, cudaStream_t s) {
+  constexpr int stage_bytes = BM * BK + BN * BK;
+  const int fixed = 1024 + (a.n_out + a.has_res) * BM * BN + (2 * MAX_STAGES + 6) * 8 + 16 +
+                    static_cast<int>(sizeof(StageTables)) + 64;
+  int stages = (SMEM_LIMIT - fixed) / stage_bytes;
+  const int nk = a.K / BK;
+  stages = stages > MAX_STAGES ? MAX_STAGES : stages;
+  stages = stages > nk + 1 ? nk + 1 : stages;  // no deeper than the K loop needs
+  if (stages < 2) stages = 2;
+  a.stages = stages;
+  const size_t smem = static_cast<size_t>(fixed) + static_cast<size_t>(stages) * stage_bytes;
   static std::once_flag once;
   std::call_once(once, [&] {
-    cudaFuncSetAttribute(tc_conv_kernel<BN, EW, DEPTH>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(tc_conv_kernel<BN, DEPTH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         SMEM_LIMIT);
   });
   const int tiles = a.m_tiles * a.n_tiles;
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  tc_conv_kernel<BN, EW, DEPTH><<<grid, THREADS, smem, s>>>(ma, mb, a);
+  tc_conv_kernel<BN, DEPTH><<<grid, THREADS, smem, s>>>(maps[0], maps[1], maps[2], maps[3],
+                                                        maps[4], a);
   QC_CUDA_CHECK_LAUNCH();
 }
 
 template <int BN>
-void launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const TcArgs& a, cudaStream_t s) {
+void launch_bn(const CUtensorMap* maps, const TcArgs& a, cudaStream_t s) {
   if (a.prog.depth <= 1) {
-    launch_tc<BN, 16, 1>(ma, mb, a, s);
+    launch_tc<BN, 1>(maps, a, s);
   } else {
-    launch_tc<BN, 16, 3>(ma, mb, a, s);
+    launch_tc<BN, 3>(maps, a, s);
   }
 }
 
 }  // namespace
+
+int tc_conv_bn(int O) { return O <= 64 ? 64 : (O <= 128 ? 128 : 256); }
 
 void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
   TcArgs a{};
@@ -428,6 +501,8 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
   a.N = sp.O;
   a.K = sp.Kpad;
   a.gather = sp.gather;
+  a.n_out = sp.n_out;
+  a.has_res = sp.res_ptr != nullptr ? 1 : 0;
   a.g = TcGeom{sp.x, sp.Nimg, sp.H, sp.W, sp.C, sp.ld, sp.KH, sp.KW, sp.sh, sp.sw,
                sp.ph, sp.pw, sp.OH, sp.OW};
   a.bias = sp.bias;
@@ -437,19 +512,26 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
     a.scale_f = (static_cast<double>(f) == sp.scale && std::fpclassify(f) == FP_NORMAL) ? f : 0.0f;
   }
   a.prog = sp.prog;
-  const int BN = sp.O <= 64 ? 64 : (sp.O <= 128 ? 128 : 256);
+  const int BN = tc_conv_bn(sp.O);
+  const int swz = BN >= 128 ? 128 : 64;
   a.m_tiles = static_cast<int>((sp.M + BM - 1) / BM);
   a.n_tiles = (sp.O + BN - 1) / BN;
-  // A: direct 2-D map over the code rows (unused, but must be valid, when gathering)
-  const CUtensorMap ma = kmap(sp.x, sp.gather ? 1 : sp.M, sp.gather ? BK : sp.Ktrue,
-                              sp.gather ? BK : sp.lda, BM);
-  const CUtensorMap mb = kmap(sp.w, sp.O, sp.Kpad, sp.Kpad, BN);
+  CUtensorMap maps[5];
+  // A: direct 2-D map over the code rows (a valid dummy when gathering)
+  maps[0] = bmap(sp.x, sp.gather ? BM : sp.M, sp.gather ? BK : sp.Ktrue, sp.gather ? BK : sp.lda,
+                 BK, BM, 128);
+  maps[1] = bmap(sp.w, sp.O, sp.Kpad, sp.Kpad, BK, BN, 128);
+  for (int o = 0; o < 2; ++o) {
+    maps[2 + o] = o < sp.n_out ? bmap(sp.out_ptr[o], sp.M, sp.out_cols[o], sp.out_ld[o], swz, BM, swz)
+                               : maps[1];
+  }
+  maps[4] = a.has_res ? bmap(sp.res_ptr, sp.M, sp.res_cols, sp.res_ld, swz, BM, swz) : maps[1];
   if (BN == 64) {
-    launch_bn<64>(ma, mb, a, s);
+    launch_bn<64>(maps, a, s);
   } else if (BN == 128) {
-    launch_bn<128>(ma, mb, a, s);
+    launch_bn<128>(maps, a, s);
   } else {
-    launch_bn<256>(ma, mb, a, s);
+    launch_bn<256>(maps, a, s);
   }
 }
 

@@ -87,6 +87,22 @@ __device__ __forceinline__ void sq_codes(float (&v)[W], float (&c)[W], const FSq
   }
 }
 
+// tcgen05-epilogue tile I/O: the thread's row within the 128-row tile and the
+// shared-memory slot area (see ProgBuf::slot / slot_swizzle)
+struct TileIo {
+  uint8_t* base;
+  int rl;
+  int slot_bytes;
+  int swz;
+};
+
+__device__ __forceinline__ uint8_t* tile_ptr(const TileIo& io, int slot, int cl) {
+  const int S = io.swz;
+  const int blk = cl / S, within = cl - blk * S;
+  const int chunk = (within >> 4) ^ ((io.rl * S >> 7) & (S / 16 - 1));
+  return io.base + slot * io.slot_bytes + blk * (128 * S) + io.rl * S + (chunk << 4);
+}
+
 __device__ __forceinline__ int64_t buf_off(const ProgBuf& b, int64_t m, int n) {
   return b.hw == 1 ? m * b.ld + n : (m / b.hw) * b.ld + (m % b.hw) * b.cs + n;
 }
@@ -100,7 +116,16 @@ __device__ __forceinline__ uint32_t pack4(float a, float b, float c, float d) {
 
 template <int W>
 __device__ __forceinline__ void store_codes(const ProgBuf& b, int64_t m, int n0, int nvalid,
-                                            const float (&q)[W]) {
+                                            const float (&q)[W], const TileIo* io = nullptr,
+                                            int cl = 0) {
+  if (W == 16 && io != nullptr && b.slot >= 0) {
+    *reinterpret_cast<int4*>(tile_ptr(*io, b.slot, cl)) =
+        make_int4(static_cast<int>(pack4(q[0], q[1], q[2], q[3])),
+                  static_cast<int>(pack4(q[4], q[5], q[6], q[7])),
+                  static_cast<int>(pack4(q[8], q[9], q[10], q[11])),
+                  static_cast<int>(pack4(q[12], q[13], q[14], q[15])));
+    return;
+  }
   int8_t* dst = static_cast<int8_t*>(b.ptr) + buf_off(b, m, n0);
   if (nvalid == W && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
 #pragma unroll
@@ -122,7 +147,16 @@ __device__ __forceinline__ void store_codes(const ProgBuf& b, int64_t m, int n0,
 
 template <int W>
 __device__ __forceinline__ void load_values(const ProgBuf& b, int64_t m, int n0, int nvalid,
-                                            float (&o)[W]) {
+                                            float (&o)[W], const TileIo* io = nullptr,
+                                            int cl = 0) {
+  if (W == 16 && io != nullptr && b.slot >= 0) {
+    const int4 raw = *reinterpret_cast<const int4*>(tile_ptr(*io, b.slot, cl));
+    const int8_t* cc = reinterpret_cast<const int8_t*>(&raw);
+    const float sc = b.scale;
+#pragma unroll
+    for (int j = 0; j < W; ++j) o[j] = __fmul_rn(static_cast<float>(cc[j % 16]), sc);
+    return;
+  }
   if (b.kind == 0) {
     const int8_t* src = static_cast<const int8_t*>(b.ptr) + buf_off(b, m, n0);
     const float sc = b.scale;
@@ -150,7 +184,8 @@ __device__ __forceinline__ void load_values(const ProgBuf& b, int64_t m, int n0,
 // DEPTH: number of PUSH slots the program may use (host-checked)
 template <int W, int DEPTH>
 __device__ __forceinline__ void run_prog(float (&v)[W], int64_t m, int n0, int nvalid,
-                                         const StageTables& t) {
+                                         const StageTables& t, const TileIo* io = nullptr,
+                                         int cl = 0) {
   float s0[W];
   float s1[DEPTH > 1 ? W : 1];
   float s2[DEPTH > 2 ? W : 1];
@@ -166,7 +201,7 @@ __device__ __forceinline__ void run_prog(float (&v)[W], int64_t m, int n0, int n
       case kPSqStore8: {
         float q[W];
         sq_codes<W>(v, q, t.sq[ins.a]);
-        store_codes<W>(t.buf[ins.b], m, n0, nvalid, q);
+        store_codes<W>(t.buf[ins.b], m, n0, nvalid, q, io, cl);
         break;
       }
       case kPRelu:
@@ -181,7 +216,7 @@ __device__ __forceinline__ void run_prog(float (&v)[W], int64_t m, int n0, int n
       }
       case kPAdd: {
         float o[W];
-        load_values<W>(t.buf[ins.b], m, n0, nvalid, o);
+        load_values<W>(t.buf[ins.b], m, n0, nvalid, o, io, cl);
 #pragma unroll
         for (int j = 0; j < W; ++j) v[j] = __fadd_rn(v[j], o[j]);
         break;

@@ -76,7 +76,21 @@ struct ProgBuf {
   int32_t cs;
   int32_t kind;
   float scale;
+  // GEMM stages: >= 0 routes this buffer through shared-memory tile slot
+  // `slot` (TMA store for outputs, TMA-prefetched tile for an add operand)
+  int32_t slot;
+  int32_t pad_;
 };
+
+// shared-memory tile slot geometry of the tcgen05 epilogue: 128 rows x BN
+// bytes, stored as BN/S column blocks of S-byte swizzled rows (S = 128 for
+// BN >= 128, 64 for BN = 64) — the TMA SWIZZLE_S layout.
+#ifdef __CUDACC__
+#define QC_HD __host__ __device__
+#else
+#define QC_HD
+#endif
+QC_HD inline int slot_swizzle(int bn) { return bn >= 128 ? 128 : 64; }
 
 constexpr int kMaxCode = 48;
 constexpr int kMaxSq = 12;

@@ -125,8 +125,18 @@ struct TcConvSpec {
   const float* bias;
   double scale;      // s_x * s_w
   ProgArgs prog;
+  // smem-staged epilogue I/O (ProgBuf::slot): code outputs stored by TMA
+  // (slots 0..n_out-1) and one TMA-prefetched add operand (slot n_out)
+  int n_out;
+  void* out_ptr[2];
+  int out_cols[2];
+  int64_t out_ld[2];
+  const void* res_ptr;
+  int res_cols;
+  int64_t res_ld;
 };
 void tc_conv(const TcConvSpec& spec, cudaStream_t s);
+int tc_conv_bn(int O);  // output-channel tile the kernel uses for O channels
 
 // weight codes [O][Kpad], k = tap*ldk + c, from OIHW float weights (taps =
 // KH*KW; a flattened dense is the taps = H*W case), fp32 sq (pow2 scale)
