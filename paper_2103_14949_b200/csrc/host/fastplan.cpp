@@ -83,7 +83,79 @@ struct FastPlan::Stage {
   int n_out = 0;
   int out_vals[2] = {-1, -1};
   int res_val = -1;
+  double bias_absmax = 0.0;
 };
+
+namespace {
+
+double code_absmax(const FSq& f) {
+  return std::max(std::fabs(static_cast<double>(f.qmin) - f.zp),
+                  std::fabs(static_cast<double>(f.qmax) - f.zp));
+}
+
+// Per-run table optimisation of one stage (observable results unchanged):
+//  * interval analysis of |v| along the program; an accumulator clamp that
+//    the bound proves can never fire is dropped (has_acc = 0);
+//  * sq -> relu folds into the code clamp: relu((q-zp)*s) == (max(q,zp)-zp)*s.
+// `v0` bounds the stage's produced value before the program.
+void optimise_tables(kern::StageTables& t, double v0) {
+  std::vector<double> stack;
+  double b = v0;
+  std::vector<kern::ProgInstr> out;
+  for (int pc = 0; pc < t.n_code; ++pc) {
+    kern::ProgInstr ins = t.code[pc];
+    switch (ins.op) {
+      case kern::kPSq:
+      case kern::kPSqStore8: {
+        FSq& f = t.sq[ins.a];
+        if (f.has_acc && std::isfinite(b) && -b * 1.001 > static_cast<double>(f.lo_up) &&
+            b * 1.001 < static_cast<double>(f.hi_dn)) {
+          f.has_acc = 0;
+        }
+        if (f.has_acc) {
+          b = std::min(b, std::max(std::fabs(static_cast<double>(f.lo_rn)),
+                                   std::fabs(static_cast<double>(f.hi_rn))) * 1.001);
+        }
+        if (!f.passthrough) b = code_absmax(f) * static_cast<double>(f.s);
+        const bool relu_next = pc + 1 < t.n_code && t.code[pc + 1].op == kern::kPRelu;
+        if (ins.op == kern::kPSq && relu_next && !f.passthrough) {
+          f.qmin = std::max(f.qmin, f.zp);
+          f.q_lo = std::max(f.q_lo, f.zp);
+          f.q_hi = std::max(f.q_hi, f.zp);
+          out.push_back(ins);
+          ++pc;  // relu folded
+          continue;
+        }
+        break;
+      }
+      case kern::kPClip: {
+        const float2 c = t.clip[ins.a];
+        b = std::min(b, std::max(std::fabs(static_cast<double>(c.x)), std::fabs(static_cast<double>(c.y))));
+        break;
+      }
+      case kern::kPAdd: {
+        const kern::ProgBuf& pb = t.buf[ins.b];
+        b = pb.kind == 0 ? b + 128.0 * static_cast<double>(pb.scale)
+                         : std::numeric_limits<double>::infinity();
+        break;
+      }
+      case kern::kPPush:
+        stack.push_back(b);
+        break;
+      case kern::kPPop:
+        b = stack.back();
+        stack.pop_back();
+        break;
+      default:
+        break;
+    }
+    out.push_back(ins);
+  }
+  t.n_code = static_cast<int32_t>(out.size());
+  std::copy(out.begin(), out.end(), t.code);
+}
+
+}  // namespace
 
 namespace {
 
@@ -484,6 +556,9 @@ void FastPlan::compile() {
             continue;
           }
           st->bias_const = in[2];
+          for (float bv : steps[static_cast<size_t>(in[2])].node->payload->floats()) {
+            st->bias_absmax = std::max(st->bias_absmax, std::fabs(static_cast<double>(bv)));
+          }
         }
         const Val& dv = *vals_[static_cast<size_t>(st->in_val)];
         const auto& ws = plan_.shape(st->w_const);
@@ -740,6 +815,18 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
     fsq[k] = make_fsq(p);
     scale_by_step[sq_steps_[k]] = fsq[k].s;
   }
+  // weight-edge sq parameters and |accumulator| bounds of the GEMM stages
+  std::vector<FSq> wfsq(stages_.size());
+  std::vector<double> acc_bound(stages_.size(), 0.0);
+  for (size_t si = 0; si < stages_.size(); ++si) {
+    const Stage& st = *stages_[si];
+    if (st.kind != Stage::kGemm) continue;
+    wfsq[si] = make_fsq(engine::qparams_of(*plan_.steps()[static_cast<size_t>(st.w_sq)].node, binding));
+    const Val& dv = *vals_[static_cast<size_t>(st.in_val)];
+    const FSq& df = fsq[static_cast<size_t>(sq_index_.at(dv.sq_step))];
+    const double kreal = st.dense ? st.Ktrue : static_cast<double>(st.C) * st.KH * st.KW;
+    acc_bound[si] = kreal * code_absmax(df) * code_absmax(wfsq[si]);
+  }
   // one compact table block per stage (instructions + referenced params)
   std::vector<kern::StageTables> tabs(stages_.size());
   for (size_t si = 0; si < stages_.size(); ++si) {
@@ -763,6 +850,18 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
       const int c = st.clips[k];
       t.clip[k] = make_float2(clip_lo_[static_cast<size_t>(c)], clip_hi_[static_cast<size_t>(c)]);
     }
+    double v0 = std::numeric_limits<double>::infinity();
+    if (st.kind == Stage::kGemm) {
+      const Val& dv = *vals_[static_cast<size_t>(st.in_val)];
+      const double sxw = static_cast<double>(scale_by_step.at(dv.sq_step)) *
+                         static_cast<double>(wfsq[si].s);
+      v0 = acc_bound[si] * sxw * 1.0001 + st.bias_absmax;
+    } else if (st.kind == Stage::kMaxpool) {
+      const Val& v = *vals_[static_cast<size_t>(st.in_val)];
+      const FSq& f = fsq[static_cast<size_t>(sq_index_.at(v.sq_step))];
+      v0 = code_absmax(f) * static_cast<double>(f.s);
+    }
+    optimise_tables(t, v0);
   }
   ok_cuda(cudaMemcpyAsync(d_tables_.get(), tabs.data(), tabs.size() * sizeof(kern::StageTables),
                           cudaMemcpyHostToDevice, S()));
@@ -794,7 +893,9 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
         const Val& dv = *vals_[static_cast<size_t>(st.in_val)];
         const int wslot = sq_index_.count(st.w_sq) ? sq_index_.at(st.w_sq) : -1;
         const QParams wp = engine::qparams_of(*plan_.steps()[static_cast<size_t>(st.w_sq)].node, binding);
-        const FSq wf = wslot >= 0 ? fsq[static_cast<size_t>(wslot)] : make_fsq(wp);
+        (void)wslot;
+        (void)wp;
+        const FSq wf = wfsq[si];
         std::string key(reinterpret_cast<const char*>(&wf), sizeof(FSq));
         auto ck = std::make_pair(static_cast<int>(si), key);
         auto it = wcache_.find(ck);
@@ -831,6 +932,7 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
         sp.scale = static_cast<double>(scale_by_step.count(dv.sq_step) ? scale_by_step.at(dv.sq_step) : 0.0f) *
                    static_cast<double>(wf.s);
         sp.prog = pa;
+        sp.acc_bound = acc_bound[si];
         sp.n_out = st.n_out;
         for (int o = 0; o < st.n_out; ++o) {
           const Val& ov = *vals_[static_cast<size_t>(st.out_vals[o])];

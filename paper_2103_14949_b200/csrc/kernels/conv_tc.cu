@@ -128,6 +128,7 @@ struct TcArgs {
   const float* bias;
   double scale;
   float scale_f;  // scale as fp32 when exactly representable (normal), else 0
+  int always_small;  // |acc| <= 2^24 guaranteed for this layer
   ProgArgs prog;
   int m_tiles, n_tiles;
 };
@@ -352,17 +353,31 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (m < args.M && nvalid > 0) {
           float v[EW];
           float bias[EW];
+          if (args.bias && nvalid == EW && ((n & 3) == 0)) {
 #pragma unroll
-          for (int j = 0; j < EW; ++j) bias[j] = (args.bias && j < nvalid) ? __ldg(args.bias + n + j) : 0.0f;
-          // |acc| < 2^24 for every column: acc*s is an exact float and
+            for (int j = 0; j < EW; j += 4) {
+              const float4 b4 = __ldg(reinterpret_cast<const float4*>(args.bias + n + j));
+              bias[j] = b4.x;
+              bias[j + 1] = b4.y;
+              bias[j + 2] = b4.z;
+              bias[j + 3] = b4.w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < EW; ++j) bias[j] = (args.bias && j < nvalid) ? __ldg(args.bias + n + j) : 0.0f;
+          }
+          // |acc| <= 2^24 for every column: acc*s is an exact float and
           // RN24(RN53(acc*s + b)) == RN24(acc*s + b) (53 >= 2*24+2: double
           // rounding is innocuous), so the reference's double accumulator
-          // rounds to the same float as one fp32 add
+          // rounds to the same float as one fp32 add.  always_small: the
+          // host proved K*|qx|max*|qw|max <= 2^24 for this layer.
           bool small = args.scale_f != 0.0f;
+          if (!args.always_small) {
 #pragma unroll
-          for (int j = 0; j < EW; ++j) {
-            const int32_t a = static_cast<int32_t>(d[j]);
-            small = small && a < (1 << 24) && a > -(1 << 24);
+            for (int j = 0; j < EW; ++j) {
+              const int32_t a = static_cast<int32_t>(d[j]);
+              small = small && a <= (1 << 24) && a >= -(1 << 24);
+            }
           }
           if (small) {
 #pragma unroll
@@ -512,6 +527,7 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
     a.scale_f = (static_cast<double>(f) == sp.scale && std::fpclassify(f) == FP_NORMAL) ? f : 0.0f;
   }
   a.prog = sp.prog;
+  a.always_small = sp.acc_bound <= static_cast<double>(1 << 24) ? 1 : 0;
   const int BN = tc_conv_bn(sp.O);
   const int swz = BN >= 128 ? 128 : 64;
   a.m_tiles = static_cast<int>((sp.M + BM - 1) / BM);

@@ -55,6 +55,13 @@ __device__ __forceinline__ void sq_values(float (&v)[W], const FSq& p) {
       q = (v[j] < lu) ? ql : ((v[j] > hd) ? qh : q);
       v[j] = __fmul_rn(__fsub_rn(q, zp), s);
     }
+  } else if (zp == 0.0f) {
+    // symmetric grid: (q - 0) * s; the +0 of the reference only canonicalises
+    // -0.0, which never changes a code or a prediction
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      v[j] = __fmul_rn(clampq(roundf(__fmul_rn(v[j], inv)), qmin, qmax), s);
+    }
   } else {
 #pragma unroll
     for (int j = 0; j < W; ++j) {
@@ -75,6 +82,12 @@ __device__ __forceinline__ void sq_codes(float (&v)[W], float (&c)[W], const FSq
       float q = clampq(__fadd_rn(roundf(__fmul_rn(v[j], inv)), zp), qmin, qmax);
       q = (v[j] < lu) ? ql : ((v[j] > hd) ? qh : q);
       c[j] = __fsub_rn(q, zp);
+      v[j] = __fmul_rn(c[j], s);
+    }
+  } else if (zp == 0.0f) {
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      c[j] = clampq(roundf(__fmul_rn(v[j], inv)), qmin, qmax);
       v[j] = __fmul_rn(c[j], s);
     }
   } else {
