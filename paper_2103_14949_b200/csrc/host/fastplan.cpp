@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <limits>
@@ -456,6 +457,21 @@ FSq make_fsq(const QParams& p) {
   return f;
 }
 
+// straight-line epilogue shape of a GEMM stage program (fused.cuh kShape*)
+int classify_shape(const kern::StageTables& t) {
+  std::vector<uint8_t> ops;
+  for (int i = 0; i < t.n_code; ++i) ops.push_back(t.code[i].op);
+  using V = std::vector<uint8_t>;
+  if (ops == V{kern::kPSqStore8}) return 1;
+  if (ops == V{kern::kPSq, kern::kPSqStore8}) return 2;
+  if (ops == V{kern::kPSq, kern::kPAdd, kern::kPSq, kern::kPPush, kern::kPSqStore8, kern::kPPop,
+               kern::kPSqStore8}) {
+    return 3;
+  }
+  if (ops == V{kern::kPSq, kern::kPAdd, kern::kPSq, kern::kPSqStore8}) return 4;
+  return 0;
+}
+
 }  // namespace
 
 FastPlan::~FastPlan() = default;
@@ -869,7 +885,8 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
 
   for (size_t si = 0; si < stages_.size(); ++si) {
     const Stage& st = *stages_[si];
-    ProgArgs pa{d_tabs + si, st.depth, 0};
+    ProgArgs pa{d_tabs + si, st.depth,
+                st.kind == Stage::kGemm && !std::getenv("QUANTC_NO_SHAPES") ? classify_shape(tabs[si]) : 0};
     switch (st.kind) {
       case Stage::kInput:
         kern::stage_input(inputs.at(static_cast<size_t>(st.input_k)), batch * st.n0, st.C, st.HW,

@@ -70,6 +70,24 @@ __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+// single-thread waits (MMA issuer / TMA producer): back off between polls so
+// spinning lanes do not steal issue slots from the epilogue warps
+__device__ __forceinline__ void bar_wait_sleep(uint64_t* b, uint32_t phase) {
+  uint32_t ok = 0;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(su32(b)), "r"(phase)
+      : "memory");
+  while (!ok) {
+    __nanosleep(32);
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(su32(b)), "r"(phase)
+        : "memory");
+  }
+}
 __device__ __forceinline__ void tma2d(const CUtensorMap* m, uint64_t* bar, void* dst, int c0,
                                       int c1) {
   asm volatile(
@@ -147,7 +165,7 @@ __device__ __forceinline__ void tmem_ld<16>(uint32_t addr, uint32_t (&d)[16]) {
       : "r"(addr));
 }
 
-template <int BN, int DEPTH>
+template <int BN, int SHAPE>
 __global__ void __launch_bounds__(THREADS, 1)
     tc_conv_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b,
@@ -215,7 +233,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
           for (int kb = 0; kb < nk; ++kb, ++it) {
             const int s = it % stages;
-            if (it >= static_cast<uint32_t>(stages)) bar_wait(&empty[s], ((it / stages) - 1) & 1);
+            if (it >= static_cast<uint32_t>(stages)) bar_wait_sleep(&empty[s], ((it / stages) - 1) & 1);
             bar_expect(&full[s], A_BYTES + B_BYTES);
             tma2d(&map_a, &full[s], sa + s * A_BYTES, kb * BK, m0);
             tma2d(&map_b, &full[s], sb + s * B_BYTES, kb * BK, n0);
@@ -242,7 +260,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int8_t* ximg = g.x + static_cast<int64_t>(img) * g.H * g.W * g.ld;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % stages;
-          if (it >= static_cast<uint32_t>(stages)) bar_wait(&empty[s], ((it / stages) - 1) & 1);
+          if (it >= static_cast<uint32_t>(stages)) bar_wait_sleep(&empty[s], ((it / stages) - 1) & 1);
           if (p == 0) {
             bar_expect(&full[s], B_BYTES);
             tma2d(&map_b, &full[s], sb + s * B_BYTES, kb * BK, n0);
@@ -295,12 +313,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t it = 0, tl = 0;
       for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
         const uint32_t acc = tl & 1;
-        if (tl >= 2) bar_wait(&tempty[acc], ((tl / 2) - 1) & 1);
+        if (tl >= 2) bar_wait_sleep(&tempty[acc], ((tl / 2) - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + acc * BN;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % stages;
-          bar_wait(&full[s], (it / stages) & 1);
+          bar_wait_sleep(&full[s], (it / stages) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t ab = su32(sa + s * A_BYTES), bb = su32(sb + s * B_BYTES);
 #pragma unroll
@@ -392,7 +410,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                                                 args.scale, static_cast<double>(bias[j])));
             }
           }
-          run_prog<EW, DEPTH>(v, m, n, nvalid, *tabs, &io, c0);
+          if constexpr (SHAPE == kShapeGeneric) {
+            run_prog<EW, 3>(v, m, n, nvalid, *tabs, &io, c0);
+          } else {
+            run_shape<EW, SHAPE>(v, m, n, nvalid, *tabs, &io, c0);
+          }
         }
       }
       // publish slot writes to the async proxy, release TMEM, store the tile
@@ -473,7 +495,7 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int DEPTH>
+template <int BN, int SHAPE>
 void launch_tc(const CUtensorMap* maps, TcArgs a, cudaStream_t s) {
   constexpr int stage_bytes = BM * BK + BN * BK;
   const int fixed = 1024 + (a.n_out + a.has_res) * BM * BN + (2 * MAX_STAGES + 6) * 8 + 16 +
@@ -487,22 +509,34 @@ void launch_tc(const CUtensorMap* maps, TcArgs a, cudaStream_t s) {
   const size_t smem = static_cast<size_t>(fixed) + static_cast<size_t>(stages) * stage_bytes;
   static std::once_flag once;
   std::call_once(once, [&] {
-    cudaFuncSetAttribute(tc_conv_kernel<BN, DEPTH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(tc_conv_kernel<BN, SHAPE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          SMEM_LIMIT);
   });
   const int tiles = a.m_tiles * a.n_tiles;
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  tc_conv_kernel<BN, DEPTH><<<grid, THREADS, smem, s>>>(maps[0], maps[1], maps[2], maps[3],
+  tc_conv_kernel<BN, SHAPE><<<grid, THREADS, smem, s>>>(maps[0], maps[1], maps[2], maps[3],
                                                         maps[4], a);
   QC_CUDA_CHECK_LAUNCH();
 }
 
 template <int BN>
 void launch_bn(const CUtensorMap* maps, const TcArgs& a, cudaStream_t s) {
-  if (a.prog.depth <= 1) {
-    launch_tc<BN, 1>(maps, a, s);
-  } else {
-    launch_tc<BN, 3>(maps, a, s);
+  switch (a.prog.shape) {
+    case kShapeStore:
+      launch_tc<BN, kShapeStore>(maps, a, s);
+      break;
+    case kShapeSqStore:
+      launch_tc<BN, kShapeSqStore>(maps, a, s);
+      break;
+    case kShapeAddFork:
+      launch_tc<BN, kShapeAddFork>(maps, a, s);
+      break;
+    case kShapeAdd:
+      launch_tc<BN, kShapeAdd>(maps, a, s);
+      break;
+    default:
+      launch_tc<BN, kShapeGeneric>(maps, a, s);
+      break;
   }
 }
 

@@ -194,6 +194,53 @@ __device__ __forceinline__ void load_values(const ProgBuf& b, int64_t m, int n0,
   }
 }
 
+// Straight-line epilogues for the program shapes that dominate CNN graphs
+// (identified on the host after optimise_tables; operand indices are read
+// from the stage table).  SHAPE 0 is the generic interpreter below.
+//   1: SQ_STORE8
+//   2: SQ, SQ_STORE8                          (conv -> sq [-> relu] -> sq -> codes)
+//   3: SQ, ADD, SQ, PUSH, SQ_STORE8, POP, SQ_STORE8   (residual block end)
+//   4: SQ, ADD, SQ, SQ_STORE8
+enum : int { kShapeGeneric = 0, kShapeStore = 1, kShapeSqStore = 2, kShapeAddFork = 3,
+             kShapeAdd = 4 };
+
+template <int W>
+__device__ __forceinline__ void shape_sq_store(float (&v)[W], const FSq& p, const ProgBuf& b,
+                                               int64_t m, int n0, int nvalid,
+                                               const TileIo* io, int cl) {
+  float q[W];
+  sq_codes<W>(v, q, p);
+  store_codes<W>(b, m, n0, nvalid, q, io, cl);
+}
+
+template <int W, int SHAPE>
+__device__ __forceinline__ void run_shape(float (&v)[W], int64_t m, int n0, int nvalid,
+                                          const StageTables& t, const TileIo* io, int cl) {
+  const ProgInstr* c = t.code;
+  if (SHAPE == kShapeStore) {
+    shape_sq_store<W>(v, t.sq[c[0].a], t.buf[c[0].b], m, n0, nvalid, io, cl);
+  } else if (SHAPE == kShapeSqStore) {
+    sq_values<W>(v, t.sq[c[0].a]);
+    shape_sq_store<W>(v, t.sq[c[1].a], t.buf[c[1].b], m, n0, nvalid, io, cl);
+  } else if (SHAPE == kShapeAddFork || SHAPE == kShapeAdd) {
+    sq_values<W>(v, t.sq[c[0].a]);
+    float o[W];
+    load_values<W>(t.buf[c[1].b], m, n0, nvalid, o, io, cl);
+#pragma unroll
+    for (int j = 0; j < W; ++j) v[j] = __fadd_rn(v[j], o[j]);
+    sq_values<W>(v, t.sq[c[2].a]);
+    if (SHAPE == kShapeAddFork) {
+      float keep[W];
+#pragma unroll
+      for (int j = 0; j < W; ++j) keep[j] = v[j];
+      shape_sq_store<W>(v, t.sq[c[4].a], t.buf[c[4].b], m, n0, nvalid, io, cl);
+      shape_sq_store<W>(keep, t.sq[c[6].a], t.buf[c[6].b], m, n0, nvalid, io, cl);
+    } else {
+      shape_sq_store<W>(v, t.sq[c[3].a], t.buf[c[3].b], m, n0, nvalid, io, cl);
+    }
+  }
+}
+
 // DEPTH: number of PUSH slots the program may use (host-checked)
 template <int W, int DEPTH>
 __device__ __forceinline__ void run_prog(float (&v)[W], int64_t m, int n0, int nvalid,

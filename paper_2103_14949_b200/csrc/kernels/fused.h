@@ -109,7 +109,7 @@ struct StageTables {
 struct ProgArgs {
   const StageTables* tables;
   int32_t depth;  // PUSH depth of the program
-  int32_t pad_;
+  int32_t shape;  // straight-line epilogue shape (fused.cuh kShape*), 0 = interpreter
 };
 
 }  // namespace quantc::kern
