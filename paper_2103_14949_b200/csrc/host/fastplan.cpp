@@ -66,7 +66,7 @@ struct FastPlan::Stage {
   // input
   int input_k = 0, n0 = 1, C = 0, HW = 1;
   // gemm
-  bool dense = false, gather = false;
+  bool dense = false, gather = false, packed = false;
   int w_sq = -1, w_const = -1, bias_const = -1;
   int O = 0, KH = 1, KW = 1, sh = 1, sw = 1, ph = 0, pw = 0, H = 1, W = 1, OH = 1, OW = 1;
   int taps = 1, ldk = 0, Ktrue = 0, Kpad = 0;
@@ -607,6 +607,14 @@ void FastPlan::compile() {
                          st->pw == 0 && dv.ld == st->C);
           st->ldk = st->gather ? static_cast<int>(dv.ld) : st->C;
           st->Ktrue = st->gather ? st->taps * st->ldk : st->C;
+          // tiny-channel convs (e.g. the RGB stem, C=3 in 16-byte rows): pack
+          // dense im2col rows k = tap*C + c first, then run the GEMM direct
+          if (st->gather && st->C <= 8 && st->taps > 1) {
+            st->packed = true;
+            st->gather = false;
+            st->ldk = st->C;
+            st->Ktrue = st->taps * st->C;
+          }
           st->rows_out_ps = static_cast<int64_t>(st->n0) * st->OH * st->OW;
           b.rows_ps = st->rows_out_ps;
         }
@@ -925,13 +933,24 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
         }
         kern::TcConvSpec sp{};
         sp.x = static_cast<const int8_t*>(arena_[static_cast<size_t>(st.in_val)].get());
+        std::shared_ptr<void> packed;
+        if (st.packed) {
+          packed = engine::device_alloc(static_cast<size_t>(st.rows_out_ps * batch) * st.Kpad);
+          kern::pack_im2col(sp.x, static_cast<int8_t*>(packed.get()), batch * st.n0, st.H, st.W,
+                            st.C, static_cast<int>(dv.ld), st.KH, st.KW, st.sh, st.sw, st.ph,
+                            st.pw, st.OH, st.OW, st.Ktrue, st.Kpad, S());
+        }
         sp.w = static_cast<const int8_t*>(it->second.get());
         sp.M = st.rows_out_ps * batch;
         sp.O = st.O;
         sp.Kpad = st.Kpad;
         sp.gather = st.gather ? 1 : 0;
         sp.Ktrue = st.Ktrue;
-        sp.lda = static_cast<int>(st.dense ? dv.ld : dv.ld);
+        sp.lda = static_cast<int>(dv.ld);
+        if (st.packed) {
+          sp.x = static_cast<const int8_t*>(packed.get());
+          sp.lda = st.Kpad;
+        }
         sp.Nimg = batch * st.n0;
         sp.H = st.H;
         sp.W = st.W;

@@ -152,6 +152,11 @@ void stage_maxpool(const int8_t* x, int ld, float scale, int N, int C, int H, in
 // global_avg_pool2d over NHWC values (fp32 rows, ld) -> program over (n, c)
 void stage_gap(const float* x, int64_t ld, int N, int C, int HW, const ProgArgs& prog,
                cudaStream_t s);
+// dense im2col rows of NHWC codes for tiny-channel convs: out[m][k] with
+// k = (kh*KW + kw)*C + c for k < Ktrue, 0 up to Kpad
+void pack_im2col(const int8_t* x, int8_t* out, int N, int H, int W, int C, int ld, int KH, int KW,
+                 int sh, int sw, int ph, int pw, int OH, int OW, int Ktrue, int Kpad,
+                 cudaStream_t s);
 // generic elementwise stage over an (M, C) space: v = value(src) -> program
 void stage_ew(const ProgBuf& src, int64_t M, int C, const ProgArgs& prog, cudaStream_t s);
 
