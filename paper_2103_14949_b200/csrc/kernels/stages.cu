@@ -154,33 +154,42 @@ __global__ void weight_codes_v2_kernel(const float* __restrict__ w, int8_t* __re
   }
 }
 
-// 4 output bytes per thread
+// one thread per output row: walks (kh, kw, c) with incremental counters and
+// emits the row as 16-byte stores
 __global__ void pack_im2col_kernel(const int8_t* __restrict__ x, int8_t* __restrict__ out, int N,
                                    int H, int W, int C, int ld, int KH, int KW, int sh, int sw,
                                    int ph, int pw, int OH, int OW, int Ktrue, int Kpad) {
-  const int words = Kpad / 4;
-  const int64_t total = static_cast<int64_t>(N) * OH * OW * words;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int wd = static_cast<int>(i % words);
-    const int64_t m = i / words;
+  const int64_t rows = static_cast<int64_t>(N) * OH * OW;
+  for (int64_t m = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; m < rows;
+       m += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int ow = static_cast<int>(m % OW);
     const int oh = static_cast<int>((m / OW) % OH);
     const int64_t n = m / (static_cast<int64_t>(OW) * OH);
-    uint32_t word = 0;
+    const int8_t* img = x + n * H * W * ld;
+    const int ih0 = oh * sh - ph, iw0 = ow * sw - pw;
+    int c = 0, kw = 0, kh = 0, k = 0;
+    int4* dst = reinterpret_cast<int4*>(out + m * Kpad);
+    for (int chunk = 0; chunk < Kpad / 16; ++chunk) {
+      uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int k = wd * 4 + b;
-      int8_t v = 0;
-      if (k < Ktrue) {
-        const int tap = k / C, c = k - (k / C) * C;
-        const int kh = tap / KW, kw = tap - (tap / KW) * KW;
-        const int ih = oh * sh - ph + kh, iw = ow * sw - pw + kw;
-        if (ih >= 0 && ih < H && iw >= 0 && iw < W) v = x[((n * H + ih) * W + iw) * ld + c];
+      for (int b = 0; b < 16; ++b, ++k) {
+        if (k < Ktrue) {
+          const int ih = ih0 + kh, iw = iw0 + kw;
+          int8_t v = 0;
+          if (ih >= 0 && ih < H && iw >= 0 && iw < W) v = img[(ih * W + iw) * ld + c];
+          w[b >> 2] |= static_cast<uint32_t>(static_cast<uint8_t>(v)) << (8 * (b & 3));
+          if (++c == C) {
+            c = 0;
+            if (++kw == KW) {
+              kw = 0;
+              ++kh;
+            }
+          }
+        }
       }
-      word |= static_cast<uint32_t>(static_cast<uint8_t>(v)) << (8 * b);
+      dst[chunk] = make_int4(static_cast<int>(w[0]), static_cast<int>(w[1]),
+                             static_cast<int>(w[2]), static_cast<int>(w[3]));
     }
-    reinterpret_cast<uint32_t*>(out)[i] = word;
   }
 }
 
@@ -189,9 +198,9 @@ __global__ void pack_im2col_kernel(const int8_t* __restrict__ x, int8_t* __restr
 void pack_im2col(const int8_t* x, int8_t* out, int N, int H, int W, int C, int ld, int KH, int KW,
                  int sh, int sw, int ph, int pw, int OH, int OW, int Ktrue, int Kpad,
                  cudaStream_t s) {
-  const int64_t total = static_cast<int64_t>(N) * OH * OW * (Kpad / 4);
+  const int64_t total = static_cast<int64_t>(N) * OH * OW;
   if (total <= 0) return;
-  pack_im2col_kernel<<<grid_for(total, 256, 148 * 32), 256, 0, s>>>(x, out, N, H, W, C, ld, KH, KW,
+  pack_im2col_kernel<<<grid_for(total, 128, 148 * 32), 128, 0, s>>>(x, out, N, H, W, C, ld, KH, KW,
                                                                      sh, sw, ph, pw, OH, OW, Ktrue,
                                                                      Kpad);
   QC_CUDA_CHECK_LAUNCH();
