@@ -458,9 +458,25 @@ FSq make_fsq(const QParams& p) {
 }
 
 // straight-line epilogue shape of a GEMM stage program (fused.cuh kShape*)
-int classify_shape(const kern::StageTables& t) {
+// The shape kernels keep 4 sq parameters in registers and address all code
+// I/O through tile slots, so they require: symmetric grids (zp = 0), no live
+// accumulator clamp, no passthrough, slot-resident stores / add operand, and
+// O % 16 == 0 (whole 16-column chunks).  Anything else runs the interpreter.
+int classify_shape(const kern::StageTables& t, int O) {
+  if (O % 16 != 0) return 0;
   std::vector<uint8_t> ops;
-  for (int i = 0; i < t.n_code; ++i) ops.push_back(t.code[i].op);
+  for (int i = 0; i < t.n_code; ++i) {
+    const kern::ProgInstr& in = t.code[i];
+    ops.push_back(in.op);
+    if (in.op == kern::kPSq || in.op == kern::kPSqStore8) {
+      const kern::FSq& f = t.sq[in.a];
+      if (f.zp != 0.0f || f.has_acc || f.passthrough) return 0;
+    }
+    if ((in.op == kern::kPSqStore8 || in.op == kern::kPAdd) &&
+        (t.buf[in.b].slot < 0 || t.buf[in.b].kind != 0)) {
+      return 0;
+    }
+  }
   using V = std::vector<uint8_t>;
   if (ops == V{kern::kPSqStore8}) return 1;
   if (ops == V{kern::kPSq, kern::kPSqStore8}) return 2;
@@ -894,7 +910,7 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
   for (size_t si = 0; si < stages_.size(); ++si) {
     const Stage& st = *stages_[si];
     ProgArgs pa{d_tabs + si, st.depth,
-                st.kind == Stage::kGemm && !std::getenv("QUANTC_NO_SHAPES") ? classify_shape(tabs[si]) : 0};
+                st.kind == Stage::kGemm && !std::getenv("QUANTC_NO_SHAPES") ? classify_shape(tabs[si], st.O) : 0};
     switch (st.kind) {
       case Stage::kInput:
         kern::stage_input(inputs.at(static_cast<size_t>(st.input_k)), batch * st.n0, st.C, st.HW,

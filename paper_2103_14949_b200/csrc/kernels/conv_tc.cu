@@ -165,6 +165,17 @@ __device__ __forceinline__ void tmem_ld<16>(uint32_t addr, uint32_t (&d)[16]) {
       : "r"(addr));
 }
 
+// wait for this thread's outstanding tcgen05.ld; the destination registers are
+// tied to the wait so no consumer can be scheduled above it
+__device__ __forceinline__ void tmem_wait(uint32_t (&d)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3]), "+r"(d[4]), "+r"(d[5]),
+                 "+r"(d[6]), "+r"(d[7]), "+r"(d[8]), "+r"(d[9]), "+r"(d[10]), "+r"(d[11]),
+                 "+r"(d[12]), "+r"(d[13]), "+r"(d[14]), "+r"(d[15])
+               :
+               : "memory");
+}
+
 template <int BN, int SHAPE>
 __global__ void __launch_bounds__(THREADS, 1)
     tc_conv_kernel(const __grid_constant__ CUtensorMap map_a,
@@ -193,7 +204,22 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* rfull = tempty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 2);
   StageTables* tabs = reinterpret_cast<StageTables*>(tmem_slot + 4);
+  // gather K-chunk table: chunk q (16 bytes of K) = channel run c..c+15 of tap
+  // (kh, kw); x = byte offset from the row's (ih0, iw0) pixel, y = kh<<16|kw
+  // (kh = kw = 0x4000 for chunks past the taps or past C: always out of bounds)
+  int2* ktab = reinterpret_cast<int2*>(tabs + 1);
   load_tables(tabs, args.prog.tables);
+  if (args.gather) {
+    const TcGeom& g = args.g;
+    for (int q = threadIdx.x; q < args.K / 16; q += blockDim.x) {
+      const int k = q * 16;
+      const int tap = k / g.ld, c = k - tap * g.ld;
+      const int kh = tap / g.KW, kw = tap - kh * g.KW;
+      const bool ok = tap < g.KH * g.KW && c < g.C;
+      ktab[q] = ok ? make_int2((kh * g.W + kw) * g.ld + c, (kh << 16) | kw)
+                   : make_int2(0, (0x4000 << 16) | 0x4000);
+    }
+  }
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -242,22 +268,25 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     } else {
       const TcGeom& g = args.g;
-      const int taps = g.KH * g.KW;
       uint32_t it = 0;
       int pending = -1;  // stage whose copies are in flight but not yet arrived
+      // this thread's 8 swizzled 16-byte destinations within its A row
+      const uint32_t swz_row = static_cast<uint32_t>(p) * 128;
       for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
         const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
         const int64_t row = static_cast<int64_t>(m0) + p;
-        const bool row_ok = row < args.M;
-        int img = 0, ih0 = 0, iw0 = 0;
-        if (row_ok) {
+        // rows past M get an origin no tap can bring in bounds
+        int ih0 = -0x20000000, iw0 = -0x20000000;
+        const int8_t* rowbase = g.x;
+        if (row < args.M) {
           const int ohw = g.OH * g.OW;
-          img = static_cast<int>(row / ohw);
-          const int rem = static_cast<int>(row % ohw);
-          ih0 = (rem / g.OW) * g.sh - g.ph;
-          iw0 = (rem % g.OW) * g.sw - g.pw;
+          const int img = static_cast<int>(row / ohw);
+          const int rem = static_cast<int>(row - static_cast<int64_t>(img) * ohw);
+          const int oh = rem / g.OW;
+          ih0 = oh * g.sh - g.ph;
+          iw0 = (rem - oh * g.OW) * g.sw - g.pw;
+          rowbase = g.x + ((static_cast<int64_t>(img) * g.H + ih0) * g.W + iw0) * g.ld;
         }
-        const int8_t* ximg = g.x + static_cast<int64_t>(img) * g.H * g.W * g.ld;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % stages;
           if (it >= static_cast<uint32_t>(stages)) bar_wait_sleep(&empty[s], ((it / stages) - 1) & 1);
@@ -265,31 +294,19 @@ __global__ void __launch_bounds__(THREADS, 1)
             bar_expect(&full[s], B_BYTES);
             tma2d(&map_b, &full[s], sb + s * B_BYTES, kb * BK, n0);
           }
-          const uint32_t dst_row = su32(sa + s * A_BYTES) + p * 128;
-          // (tap, c) of the first chunk of this K block; chunks advance by 16
-          int tap = (kb * BK) / g.ld;
-          int c = kb * BK - tap * g.ld;
+          const uint32_t dst_row = su32(sa + s * A_BYTES) + swz_row;
+          const uint32_t kt = su32(ktab) + kb * 8 * sizeof(int2);
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            const int8_t* src = ximg;
-            uint32_t bytes = 0;
-            if (row_ok && tap < taps && c < g.C) {
-              const int kh = tap / g.KW, kw = tap - (tap / g.KW) * g.KW;
-              const int ih = ih0 + kh, iw = iw0 + kw;
-              if (ih >= 0 && ih < g.H && iw >= 0 && iw < g.W) {
-                src = ximg + (static_cast<int64_t>(ih) * g.W + iw) * g.ld + c;
-                bytes = 16;
-              }
-            }
+            int2 e;
+            asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(e.x), "=r"(e.y) : "r"(kt + j * 8));
+            const bool ok = static_cast<uint32_t>(ih0 + (e.y >> 16)) < static_cast<uint32_t>(g.H) &&
+                            static_cast<uint32_t>(iw0 + (e.y & 0xffff)) < static_cast<uint32_t>(g.W);
+            const int8_t* src = ok ? rowbase + e.x : g.x;
             const uint32_t dst = dst_row + ((j ^ (p & 7)) << 4);
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
-                         "r"(bytes)
+                         "r"(ok ? 16u : 0u)
                          : "memory");
-            c += 16;
-            if (c >= g.ld) {
-              c -= g.ld;
-              ++tap;
-            }
           }
           asm volatile("cp.async.commit_group;" ::: "memory");
           if (pending >= 0) {
@@ -337,7 +354,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int half = warp >> 2;
     const int r = quarter * 32 + lane;
     const bool leader = threadIdx.x == 0;
-    TileIo io{slots, r, static_cast<int>(SLOT_BYTES), SWZ};
+    TileIo io{su32(slots), r, static_cast<int>(SLOT_BYTES), SWZ};
+    const ShapeRegs sregs = load_shape_regs(*tabs, SHAPE);
     auto load_res = [&](int t) {
       const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
       uint8_t* dst = slots + args.n_out * SLOT_BYTES;
@@ -361,11 +379,68 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (args.has_res) bar_wait(rfull, tl & 1);
       const int64_t m = static_cast<int64_t>(m0) + r;
       const uint32_t tbase = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
+      if constexpr (SHAPE != kShapeGeneric) {
+        // straight-line shapes: host-checked preconditions (classify_shape)
+        // — O % 16 == 0, all I/O through slots (rows >= M and columns >= O
+        // are clipped by the TMA store), zp = 0, no live acc clamp.  TMEM
+        // loads run one chunk ahead of the math.
+        const int cbeg = half * (BN / 2), cend = cbeg + BN / 2;
+        uint32_t d[EW];
+        tmem_ld<EW>(tbase + cbeg, d);
+#pragma unroll 1
+        for (int c0 = cbeg; c0 < cend; c0 += EW) {
+          tmem_wait(d);
+          const int n = n0 + c0;
+          float v[EW];
+          bool small = args.scale_f != 0.0f;
+          if (!args.always_small) {
+#pragma unroll
+            for (int j = 0; j < EW; ++j) {
+              const int32_t a = static_cast<int32_t>(d[j]);
+              small = small && a <= (1 << 24) && a >= -(1 << 24);
+            }
+          }
+          uint32_t dn[EW];
+#pragma unroll
+          for (int j = 0; j < EW; ++j) dn[j] = d[j];
+          if (c0 + EW < cend) tmem_ld<EW>(tbase + c0 + EW, d);
+          if (n < args.N) {
+            float bias[EW];
+            if (args.bias) {
+#pragma unroll
+              for (int j = 0; j < EW; j += 4) {
+                const float4 b4 = __ldg(reinterpret_cast<const float4*>(args.bias + n + j));
+                bias[j] = b4.x;
+                bias[j + 1] = b4.y;
+                bias[j + 2] = b4.z;
+                bias[j + 3] = b4.w;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < EW; ++j) bias[j] = 0.0f;
+            }
+            if (small) {
+              // acc * s is exact (|acc| <= 2^24, pow2 s): fma == fadd(fmul)
+#pragma unroll
+              for (int j = 0; j < EW; ++j) {
+                v[j] = __fmaf_rn(static_cast<float>(static_cast<int32_t>(dn[j])), args.scale_f, bias[j]);
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < EW; ++j) {
+                v[j] = __double2float_rn(__fma_rn(static_cast<double>(static_cast<int32_t>(dn[j])),
+                                                  args.scale, static_cast<double>(bias[j])));
+              }
+            }
+            run_shape_regs<SHAPE>(v, sregs, io, c0);
+          }
+        }
+      } else
 #pragma unroll 1
       for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += EW) {
         uint32_t d[EW];
         tmem_ld<EW>(tbase + c0, d);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        tmem_wait(d);
         const int n = n0 + c0;
         const int nvalid = args.N - n < EW ? args.N - n : EW;
         if (m < args.M && nvalid > 0) {
@@ -410,11 +485,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                                                 args.scale, static_cast<double>(bias[j])));
             }
           }
-          if constexpr (SHAPE == kShapeGeneric) {
-            run_prog<EW, 3>(v, m, n, nvalid, *tabs, &io, c0);
-          } else {
-            run_shape<EW, SHAPE>(v, m, n, nvalid, *tabs, &io, c0);
-          }
+          run_prog<EW, 3>(v, m, n, nvalid, *tabs, &io, c0);
         }
       }
       // publish slot writes to the async proxy, release TMEM, store the tile
@@ -499,7 +570,8 @@ template <int BN, int SHAPE>
 void launch_tc(const CUtensorMap* maps, TcArgs a, cudaStream_t s) {
   constexpr int stage_bytes = BM * BK + BN * BK;
   const int fixed = 1024 + (a.n_out + a.has_res) * BM * BN + (2 * MAX_STAGES + 6) * 8 + 16 +
-                    static_cast<int>(sizeof(StageTables)) + 64;
+                    static_cast<int>(sizeof(StageTables)) + 64 +
+                    (a.gather ? a.K / 16 * static_cast<int>(sizeof(int2)) : 0);
   int stages = (SMEM_LIMIT - fixed) / stage_bytes;
   const int nk = a.K / BK;
   stages = stages > MAX_STAGES ? MAX_STAGES : stages;
@@ -562,9 +634,13 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
   }
   a.prog = sp.prog;
   a.always_small = sp.acc_bound <= static_cast<double>(1 << 24) ? 1 : 0;
-  const int BN = tc_conv_bn(sp.O);
-  const int swz = BN >= 128 ? 128 : 64;
   a.m_tiles = static_cast<int>((sp.M + BM - 1) / BM);
+  // narrower output tiles while that still fits the grid in one wave: a
+  // layer with few M tiles (late stages at small batch) would otherwise
+  // leave most SMs idle
+  int BN = tc_conv_bn(sp.O);
+  while (BN > 64 && 2 * a.m_tiles * ((sp.O + BN - 1) / BN) <= num_sms()) BN /= 2;
+  const int swz = BN >= 128 ? 128 : 64;
   a.n_tiles = (sp.O + BN - 1) / BN;
   CUtensorMap maps[5];
   // A: direct 2-D map over the code rows (a valid dummy when gathering)

@@ -103,17 +103,33 @@ __device__ __forceinline__ void sq_codes(float (&v)[W], float (&c)[W], const FSq
 // tcgen05-epilogue tile I/O: the thread's row within the 128-row tile and the
 // shared-memory slot area (see ProgBuf::slot / slot_swizzle)
 struct TileIo {
-  uint8_t* base;
+  uint32_t base;  // shared-window address of slot 0
   int rl;
   int slot_bytes;
   int swz;
 };
 
-__device__ __forceinline__ uint8_t* tile_ptr(const TileIo& io, int slot, int cl) {
+__device__ __forceinline__ uint32_t tile_addr(const TileIo& io, int slot, int cl) {
   const int S = io.swz;
   const int blk = cl / S, within = cl - blk * S;
   const int chunk = (within >> 4) ^ ((io.rl * S >> 7) & (S / 16 - 1));
-  return io.base + slot * io.slot_bytes + blk * (128 * S) + io.rl * S + (chunk << 4);
+  return io.base + static_cast<uint32_t>(slot * io.slot_bytes + blk * (128 * S) + io.rl * S +
+                                         (chunk << 4));
+}
+
+__device__ __forceinline__ int4 lds128(uint32_t a) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void sts128(uint32_t a, int4 v) {
+  asm volatile("st.shared.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
 }
 
 __device__ __forceinline__ int64_t buf_off(const ProgBuf& b, int64_t m, int n) {
@@ -132,11 +148,11 @@ __device__ __forceinline__ void store_codes(const ProgBuf& b, int64_t m, int n0,
                                             const float (&q)[W], const TileIo* io = nullptr,
                                             int cl = 0) {
   if (W == 16 && io != nullptr && b.slot >= 0) {
-    *reinterpret_cast<int4*>(tile_ptr(*io, b.slot, cl)) =
-        make_int4(static_cast<int>(pack4(q[0], q[1], q[2], q[3])),
-                  static_cast<int>(pack4(q[4], q[5], q[6], q[7])),
-                  static_cast<int>(pack4(q[8], q[9], q[10], q[11])),
-                  static_cast<int>(pack4(q[12], q[13], q[14], q[15])));
+    sts128(tile_addr(*io, b.slot, cl),
+           make_int4(static_cast<int>(pack4(q[0], q[1], q[2], q[3])),
+                     static_cast<int>(pack4(q[4], q[5], q[6], q[7])),
+                     static_cast<int>(pack4(q[8], q[9], q[10], q[11])),
+                     static_cast<int>(pack4(q[12], q[13], q[14], q[15]))));
     return;
   }
   int8_t* dst = static_cast<int8_t*>(b.ptr) + buf_off(b, m, n0);
@@ -163,7 +179,7 @@ __device__ __forceinline__ void load_values(const ProgBuf& b, int64_t m, int n0,
                                             float (&o)[W], const TileIo* io = nullptr,
                                             int cl = 0) {
   if (W == 16 && io != nullptr && b.slot >= 0) {
-    const int4 raw = *reinterpret_cast<const int4*>(tile_ptr(*io, b.slot, cl));
+    const int4 raw = lds128(tile_addr(*io, b.slot, cl));
     const int8_t* cc = reinterpret_cast<const int8_t*>(&raw);
     const float sc = b.scale;
 #pragma unroll
@@ -204,40 +220,93 @@ __device__ __forceinline__ void load_values(const ProgBuf& b, int64_t m, int n0,
 enum : int { kShapeGeneric = 0, kShapeStore = 1, kShapeSqStore = 2, kShapeAddFork = 3,
              kShapeAdd = 4 };
 
-template <int W>
-__device__ __forceinline__ void shape_sq_store(float (&v)[W], const FSq& p, const ProgBuf& b,
-                                               int64_t m, int n0, int nvalid,
-                                               const TileIo* io, int cl) {
-  float q[W];
-  sq_codes<W>(v, q, p);
-  store_codes<W>(b, m, n0, nvalid, q, io, cl);
+// ---- register-resident shape epilogues ------------------------------------------
+// For shapes 1-4 the host guarantees (classify_shape): every sq has zp = 0, no
+// live accumulator clamp (elided by interval analysis) and is not
+// passthrough; all code I/O is through tile slots.  The per-op parameters are
+// then 4 floats, loaded once per kernel.
+struct RegSq {
+  float inv, s, qmin, qmax;
+};
+
+struct ShapeRegs {
+  RegSq sq[4];
+  int slot[4];     // store slots / add source slot, in program order
+  float add_scale;
+};
+
+__device__ __forceinline__ ShapeRegs load_shape_regs(const StageTables& t, int shape) {
+  ShapeRegs r{};
+  const ProgInstr* c = t.code;
+  auto take = [&](int i, const ProgInstr& ins) {
+    const FSq& f = t.sq[ins.a];
+    r.sq[i] = RegSq{f.inv_s, f.s, f.qmin, f.qmax};
+  };
+  if (shape == kShapeStore) {
+    take(0, c[0]);
+    r.slot[0] = t.buf[c[0].b].slot;
+  } else if (shape == kShapeSqStore) {
+    take(0, c[0]);
+    take(1, c[1]);
+    r.slot[0] = t.buf[c[1].b].slot;
+  } else if (shape == kShapeAddFork) {
+    take(0, c[0]);
+    take(1, c[2]);
+    take(2, c[4]);
+    take(3, c[6]);
+    r.slot[0] = t.buf[c[4].b].slot;
+    r.slot[1] = t.buf[c[6].b].slot;
+    r.slot[2] = t.buf[c[1].b].slot;
+    r.add_scale = t.buf[c[1].b].scale;
+  } else if (shape == kShapeAdd) {
+    take(0, c[0]);
+    take(1, c[2]);
+    take(2, c[3]);
+    r.slot[0] = t.buf[c[3].b].slot;
+    r.slot[2] = t.buf[c[1].b].slot;
+    r.add_scale = t.buf[c[1].b].scale;
+  }
+  return r;
 }
 
-template <int W, int SHAPE>
-__device__ __forceinline__ void run_shape(float (&v)[W], int64_t m, int n0, int nvalid,
-                                          const StageTables& t, const TileIo* io, int cl) {
-  const ProgInstr* c = t.code;
+template <int W>
+__device__ __forceinline__ void rsq(float (&v)[W], const RegSq& p) {
+#pragma unroll
+  for (int j = 0; j < W; ++j) v[j] = __fmul_rn(clampq(roundf(__fmul_rn(v[j], p.inv)), p.qmin, p.qmax), p.s);
+}
+
+template <int W>
+__device__ __forceinline__ void rsq_store(const float (&v)[W], const RegSq& p, const TileIo& io,
+                                          int slot, int cl) {
+  float q[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) q[j] = clampq(roundf(__fmul_rn(v[j], p.inv)), p.qmin, p.qmax);
+  sts128(tile_addr(io, slot, cl),
+         make_int4(static_cast<int>(pack4(q[0], q[1], q[2], q[3])),
+                   static_cast<int>(pack4(q[4], q[5], q[6], q[7])),
+                   static_cast<int>(pack4(q[8], q[9], q[10], q[11])),
+                   static_cast<int>(pack4(q[12], q[13], q[14], q[15]))));
+}
+
+template <int SHAPE>
+__device__ __forceinline__ void run_shape_regs(float (&v)[16], const ShapeRegs& r,
+                                               const TileIo& io, int cl) {
   if (SHAPE == kShapeStore) {
-    shape_sq_store<W>(v, t.sq[c[0].a], t.buf[c[0].b], m, n0, nvalid, io, cl);
+    rsq_store<16>(v, r.sq[0], io, r.slot[0], cl);
   } else if (SHAPE == kShapeSqStore) {
-    sq_values<W>(v, t.sq[c[0].a]);
-    shape_sq_store<W>(v, t.sq[c[1].a], t.buf[c[1].b], m, n0, nvalid, io, cl);
-  } else if (SHAPE == kShapeAddFork || SHAPE == kShapeAdd) {
-    sq_values<W>(v, t.sq[c[0].a]);
-    float o[W];
-    load_values<W>(t.buf[c[1].b], m, n0, nvalid, o, io, cl);
+    rsq<16>(v, r.sq[0]);
+    rsq_store<16>(v, r.sq[1], io, r.slot[0], cl);
+  } else {
+    rsq<16>(v, r.sq[0]);
+    const int4 raw = lds128(tile_addr(io, r.slot[2], cl));
+    const int8_t* cc = reinterpret_cast<const int8_t*>(&raw);
+    // code * scale is exact (|code| <= 128, normal pow2 scale): one fma
+    // rounds like fadd(v, fmul(code, scale))
 #pragma unroll
-    for (int j = 0; j < W; ++j) v[j] = __fadd_rn(v[j], o[j]);
-    sq_values<W>(v, t.sq[c[2].a]);
-    if (SHAPE == kShapeAddFork) {
-      float keep[W];
-#pragma unroll
-      for (int j = 0; j < W; ++j) keep[j] = v[j];
-      shape_sq_store<W>(v, t.sq[c[4].a], t.buf[c[4].b], m, n0, nvalid, io, cl);
-      shape_sq_store<W>(keep, t.sq[c[6].a], t.buf[c[6].b], m, n0, nvalid, io, cl);
-    } else {
-      shape_sq_store<W>(v, t.sq[c[3].a], t.buf[c[3].b], m, n0, nvalid, io, cl);
-    }
+    for (int j = 0; j < 16; ++j) v[j] = __fmaf_rn(static_cast<float>(cc[j]), r.add_scale, v[j]);
+    rsq<16>(v, r.sq[1]);
+    rsq_store<16>(v, r.sq[2], io, r.slot[0], cl);
+    if (SHAPE == kShapeAddFork) rsq_store<16>(v, r.sq[3], io, r.slot[1], cl);
   }
 }
 
