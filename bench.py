@@ -287,20 +287,23 @@ def main():
 
     # ---- e2e: public C-ABI call with HOST buffers: predict_top1 of the sim
     # graph under a candidate binding (uploads images + plan, downloads preds)
-    binding = ev.bind(cands[0])
-    e2e_steps = max(2, min(5, args.steps))
-    b.predict_top1(sim, ds, 0, binding)
+    # The first call compiles the plan and uploads the weights (cold); later
+    # calls on the same graph reuse the resident plan (engine plan cache), so
+    # a step moves the images in and the predictions out.
+    e2e_steps = max(3, min(10, args.steps))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        b.predict_top1(sim, ds, 0, binding)
+    b.predict_top1(sim, ds, 0, ev.bind(cands[0]))
+    cold_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    for i in range(e2e_steps):
+        b.predict_top1(sim, ds, 0, ev.bind(cands[(i + 1) % len(cands)]))
     e2e_dt = (time.perf_counter() - t0) / e2e_steps
     if dist is not None:
         t = torch.tensor([e2e_dt], device=f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_dt = float(t.item())
-    weight_bytes = len(model.blob)
-    h2d = data.nbytes + weight_bytes
+    h2d = data.nbytes
     d2h = 8 * B
 
     # ---- roofline of the dominant kernel (tcgen05 int8 implicit-GEMM conv)
@@ -332,7 +335,9 @@ def main():
         "candidates_per_s": world * args.steps / (ms / 1e3) / world * 1.0,
         "e2e": {"value": B * world / e2e_dt, "unit": "images/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
-                "api": "qc_predict_top1(sim_graph, host dataset, binding)"},
+                "api": "qc_predict_top1(sim_graph, host dataset, binding) per step, new binding each",
+                "cold_first_call_s": cold_s,
+                "weights_bytes_uploaded_once": len(model.blob)},
         "gpu_launches": int(launches),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": int8_peak,
                      "unit": "TOPS", "frac": achieved / int8_peak if int8_peak else None,

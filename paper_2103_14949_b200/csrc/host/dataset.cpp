@@ -3,9 +3,15 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <mutex>
 #include <string>
+#include <vector>
+
+#include "quantc/parallel.hpp"
 
 #include "fastplan.hpp"
 #include "quantc/device.hpp"
@@ -14,6 +20,64 @@ namespace quantc::gpu {
 
 namespace {
 cudaStream_t S() { return static_cast<cudaStream_t>(device::stream()); }
+
+// Reusable pinned staging for sample uploads: two chunk buffers, packed by
+// host threads while the other chunk's DMA runs.  Pinned and reused, so an
+// upload touches no fresh pages and copies at full PCIe/C2C rate.
+class Staging {
+ public:
+  static constexpr size_t kChunk = size_t{8} << 20;
+
+  static Staging& get() {
+    static Staging s;
+    return s;
+  }
+  std::mutex& mu() { return mu_; }
+
+  // pack `count` samples of `bytes_per` each via pack(sample, dst) and copy
+  // them to dst_dev, chunk by chunk
+  void upload(uint8_t* dst_dev, int64_t count, size_t bytes_per,
+              const std::function<void(int64_t, uint8_t*)>& pack) {
+    ensure();
+    const int64_t per_chunk = std::max<int64_t>(1, static_cast<int64_t>(kChunk / bytes_per));
+    int ci = 0;
+    for (int64_t s0 = 0; s0 < count; s0 += per_chunk, ++ci) {
+      const int64_t n = std::min(per_chunk, count - s0);
+      const int slot = ci & 1;
+      uint8_t* buf = static_cast<uint8_t*>(buf_[slot]);
+      const size_t bytes = static_cast<size_t>(n) * bytes_per;
+      if (bytes > kChunk) {
+        // one sample larger than a chunk: pageable path
+        std::vector<uint8_t> tmp(bytes);
+        for (int64_t s = 0; s < n; ++s) pack(s0 + s, tmp.data() + s * bytes_per);
+        check(cudaMemcpyAsync(dst_dev + s0 * bytes_per, tmp.data(), bytes, cudaMemcpyHostToDevice, S()));
+        check(cudaStreamSynchronize(S()));
+        continue;
+      }
+      check(cudaEventSynchronize(ev_[slot]));  // DMA out of this buffer finished
+      parallel_for(static_cast<size_t>(n), n >= 4 ? 8 : 1,
+                   [&](size_t s) { pack(s0 + static_cast<int64_t>(s), buf + s * bytes_per); });
+      check(cudaMemcpyAsync(dst_dev + s0 * bytes_per, buf, bytes, cudaMemcpyHostToDevice, S()));
+      check(cudaEventRecord(ev_[slot], S()));
+    }
+  }
+
+ private:
+  void ensure() {
+    if (buf_[0]) return;
+    for (int i = 0; i < 2; ++i) {
+      check(cudaHostAlloc(&buf_[i], kChunk, cudaHostAllocDefault));
+      check(cudaEventCreateWithFlags(&ev_[i], cudaEventDisableTiming));
+      check(cudaEventRecord(ev_[i], S()));
+    }
+  }
+  static void check(cudaError_t e) {
+    if (e != cudaSuccess) throw DeviceError(std::string("staging: ") + cudaGetErrorString(e));
+  }
+  std::mutex mu_;
+  void* buf_[2] = {nullptr, nullptr};
+  cudaEvent_t ev_[2] = {nullptr, nullptr};
+};
 }  // namespace
 
 DeviceDataset::DeviceDataset(const Graph& g, const Dataset& ds, int64_t first, int64_t count) {
@@ -25,7 +89,6 @@ DeviceDataset::DeviceDataset(const Graph& g, const Dataset& ds, int64_t first, i
     const std::string name = node.attr_or<std::string>("name", "");
     const auto shape = node.attr<std::vector<int64_t>>("shape");
     const int64_t per = shape_numel(shape);
-    std::vector<float> host(static_cast<size_t>(per * count));
     for (int64_t s = 0; s < count; ++s) {
       const Sample& smp = ds[static_cast<size_t>(first + s)];
       if (smp.inputs.size() != n_in) {
@@ -40,17 +103,19 @@ DeviceDataset::DeviceDataset(const Graph& g, const Dataset& ds, int64_t first, i
       if (!t.dtype().is_float()) {
         throw EvalError("B200 engine: graph inputs must be float32 (input " + name + ")");
       }
-      std::memcpy(host.data() + s * per, t.floats().data(), static_cast<size_t>(per) * 4);
     }
-    auto buf = engine::device_alloc(host.size() * 4);
-    if (!host.empty()) {
-      cudaError_t e = cudaMemcpyAsync(buf.get(), host.data(), host.size() * 4,
-                                      cudaMemcpyHostToDevice, S());
-      if (e != cudaSuccess) throw DeviceError(cudaGetErrorString(e));
+    auto buf = engine::device_alloc(static_cast<size_t>(per * count) * 4);
+    if (per * count > 0) {
+      Staging& st = Staging::get();
+      std::lock_guard<std::mutex> lk(st.mu());
+      st.upload(static_cast<uint8_t*>(buf.get()), count, static_cast<size_t>(per) * 4,
+                [&](int64_t s, uint8_t* dst) {
+                  const Tensor& t = ds[static_cast<size_t>(first + s)].inputs[k];
+                  std::memcpy(dst, t.floats().data(), static_cast<size_t>(per) * 4);
+                });
     }
     bufs_.push_back(buf);
     per_.push_back(per);
-    device::synchronize();  // host staging goes out of scope
   }
 }
 

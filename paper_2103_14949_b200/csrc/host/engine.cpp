@@ -8,6 +8,8 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <list>
+#include <mutex>
 #include <stdexcept>
 
 #include "quantc/device.hpp"
@@ -190,6 +192,52 @@ Tensor download(const DevTensor& d, int batch) {
   if (n) cuda_ok(cudaMemcpyAsync(h.data(), d.buf.get(), n * 4, cudaMemcpyDeviceToHost, S()), "download");
   device::synchronize();
   return Tensor::from_ints(d.dtype, shape, std::move(h));
+}
+
+// ---- plan cache -------------------------------------------------------------------
+
+struct PlanLease::Entry {
+  uint64_t uid = 0;
+  std::mutex m;
+  std::unique_ptr<Plan> plan;
+};
+
+PlanLease lease_plan(const Graph& g) {
+  static std::mutex mu;
+  static std::list<std::shared_ptr<PlanLease::Entry>> lru;  // most recent first
+  static const size_t cap = [] {
+    const char* e = std::getenv("QUANTC_PLAN_CACHE");
+    return e ? static_cast<size_t>(std::max(0, std::atoi(e))) : size_t{2};
+  }();
+  PlanLease l;
+  if (cap == 0) {
+    l.own_ = std::make_unique<Plan>(g);
+    l.plan_ = l.own_.get();
+    return l;
+  }
+  std::shared_ptr<PlanLease::Entry> e;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto it = lru.begin(); it != lru.end(); ++it) {
+      if ((*it)->uid == g.uid()) {
+        e = *it;
+        lru.erase(it);
+        break;
+      }
+    }
+    if (!e) {
+      e = std::make_shared<PlanLease::Entry>();
+      e->uid = g.uid();
+    }
+    lru.push_front(e);
+    while (lru.size() > cap) lru.pop_back();  // leased entries stay alive with their lease
+  }
+  auto lock = std::make_shared<std::unique_lock<std::mutex>>(e->m);
+  if (!e->plan) e->plan = std::make_unique<Plan>(g);
+  l.entry_ = e;
+  l.lock_ = lock;
+  l.plan_ = e->plan.get();
+  return l;
 }
 
 // ---- Plan ----------------------------------------------------------------------

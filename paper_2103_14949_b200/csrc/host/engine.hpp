@@ -83,6 +83,26 @@ class Plan {
   mutable bool fused_tried = false;
 };
 
+// Process-wide cache of compiled plans (device-resident constants, the fused
+// plan with its activation arena and weight codes), keyed by Graph::uid() so a
+// serving loop calling predict_top1 on the same graph uploads its weights
+// once.  A lease holds the entry's lock: concurrent callers on one graph
+// serialise, different graphs run independently.  Capacity: QUANTC_PLAN_CACHE
+// entries (default 2; 0 = no caching, a private plan per call).
+class PlanLease {
+ public:
+  const Plan& plan() const { return *plan_; }
+  struct Entry;
+
+ private:
+  friend PlanLease lease_plan(const Graph& g);
+  std::shared_ptr<Entry> entry_;
+  std::unique_ptr<Plan> own_;
+  std::shared_ptr<void> lock_;
+  const Plan* plan_ = nullptr;
+};
+PlanLease lease_plan(const Graph& g);
+
 struct RunSpec {
   int batch = 1;
   std::vector<const float*> inputs;  // device, one per graph input, [batch x per-sample]

@@ -846,6 +846,10 @@ void FastPlan::ensure_arena(int batch) {
 void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
                        const SimBinding* binding, int64_t* d_preds) {
   ensure_arena(batch);
+  // weight codes are cached per (stage, weight sq parameters); a long search
+  // visits many weight bit-widths, so keep roughly the last few bindings
+  // (freed stream-ordered: in-flight launches keep their codes)
+  if (wcache_.size() > 4 * stages_.size()) wcache_.clear();
   // ---- per-run tables: FSq per sq node, clip bounds, buffer descriptors
   std::vector<FSq> fsq(sq_steps_.size());
   std::vector<float> scale_of_sq_step;

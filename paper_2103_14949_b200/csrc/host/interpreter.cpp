@@ -129,7 +129,8 @@ std::vector<int64_t> predict_top1(const Graph& g, const Dataset& dataset, int wo
                                   const SimBinding* binding) {
   (void)workers;  // per-sample parallelism is the GPU batch dimension
   if (dataset.empty()) return {};
-  engine::Plan plan(g);
+  const engine::PlanLease lease = engine::lease_plan(g);  // weights stay resident across calls
+  const engine::Plan& plan = lease.plan();
   gpu::DeviceDataset dd(g, dataset);
   const bool realized = g.is_realized();
   if (realized && g.contains_op(OpKind::kSimulatedQuantize)) {

@@ -220,3 +220,27 @@ def test_fused_engine_bit_exact_vs_exact_engine(b200, cuda_lib, name, n):
     np.testing.assert_array_equal(exact, fused)
     for a, b in zip(preds_exact, preds_fused):
         np.testing.assert_array_equal(a, b)
+
+
+def test_predict_top1_plan_cache(b200, ref, small_cnn):
+    """predict_top1 keeps compiled plans resident across calls (keyed by
+    graph identity): repeated and interleaved calls on two graphs, under
+    several bindings, must still match the reference call for call."""
+    m, data = small_cnn
+    m2 = F.resnet(18, image=32, classes=10, width=8)
+    data2 = m2.data(6)
+    a, r = _pipeline(b200, m, data), _pipeline(ref, m, data)
+    a2, r2 = _pipeline(b200, m2, data2), _pipeline(ref, m2, data2)
+    sp, sp2 = r["ev"].space(), r2["ev"].space()
+    cands = [sp.all_hi(), sp.all_lo(), sp.all_hi()]
+    cands2 = [sp2.all_lo(), sp2.all_hi(), sp2.all_lo()]
+    for c, c2 in zip(cands, cands2):
+        np.testing.assert_array_equal(b200.predict_top1(a["sim"], a["ds"], 0, a["ev"].bind(c)),
+                                      ref.predict_top1(r["sim"], r["ds"], 0, r["ev"].bind(c)))
+        np.testing.assert_array_equal(b200.predict_top1(a2["sim"], a2["ds"], 0, a2["ev"].bind(c2)),
+                                      ref.predict_top1(r2["sim"], r2["ds"], 0, r2["ev"].bind(c2)))
+    # a graph rebuilt from the same document after the first is gone
+    del a
+    a3 = _pipeline(b200, m, data)
+    np.testing.assert_array_equal(b200.predict_top1(a3["sim"], a3["ds"], 0, a3["ev"].bind(cands[1])),
+                                  ref.predict_top1(r["sim"], r["ds"], 0, r["ev"].bind(cands[1])))
