@@ -11,6 +11,8 @@
 #include <string>
 #include <vector>
 
+#include "quantc/interpreter.hpp"
+
 namespace quantc {
 
 class DeviceError : public std::runtime_error {
@@ -57,8 +59,6 @@ void profile_read(double* gemm_ms, int64_t* gemm_launches, double* gemm_ops);
 
 }  // namespace device
 
-class Graph;
-struct Sample;
 
 // Two-pass calibration pieces for sharded (multi-GPU) statistics: pass 1
 // exact extrema of the listed canonical edges over this shard; pass 2
@@ -69,5 +69,12 @@ void collect_extrema(const Graph& g, const std::vector<Sample>& shard, const std
 void collect_histograms(const Graph& g, const std::vector<Sample>& shard,
                         const std::vector<int>& edges, const std::vector<double>& absmax, int bins,
                         std::vector<int64_t>* counts /* edges x bins */);
+
+// predict_top1's fp32 score rows (first graph output, samples x per-sample
+// numel) under the active engine mode: the fused int8 engine in auto/fast
+// mode when eligible, the FP64 exact engine otherwise.  Lets tests compare
+// engines bit for bit below the argmax.
+std::vector<float> predict_scores(const Graph& g, const std::vector<Sample>& dataset,
+                                  const SimBinding* binding, int64_t* per_sample);
 
 }  // namespace quantc

@@ -90,6 +90,11 @@ int qc_collect_extrema(const qc_graph* g, const qc_dataset* d, const int* edges,
                        double* mins, double* maxs);
 int qc_collect_histograms(const qc_graph* g, const qc_dataset* d, const int* edges, size_t n,
                           const double* absmax, int bins, int64_t* counts);
+/* fp32 score rows of predict_top1 (samples x per-sample numel) under the
+ * active engine mode (B200 extension; quantc/device.hpp predict_scores). */
+int qc_predict_scores(const qc_graph* g, const qc_dataset* d, const int64_t* bind_nodes,
+                      const qc_qparams* bind_params, size_t n_bind, float* out, size_t cap,
+                      size_t* n_out, int64_t* per_sample);
 /* counters since load: kernel launches issued by the engine, tcgen05 GEMMs */
 int qcu_counters(int64_t* steps, int64_t* tcgen05_gemms, int64_t* f64_convs,
                  int64_t* fused_batches);

@@ -766,6 +766,15 @@ int qc_collect_histograms(const qc_graph* g, const qc_dataset* d, const int* edg
   });
 }
 
+int qc_predict_scores(const qc_graph* g, const qc_dataset* d, const int64_t* bind_nodes,
+                      const qc_qparams* bind_params, size_t n_bind, float* out, size_t cap,
+                      size_t* n_out, int64_t* per_sample) {
+  return run([&] {
+    SimBinding b = make_binding(bind_nodes, bind_params, n_bind);
+    emit(predict_scores(*g->g, *d->d, n_bind ? &b : nullptr, per_sample), out, cap, n_out);
+  });
+}
+
 int qc_evaluator_agreement(const qc_evaluator* e, const int* cands, size_t n_cands,
                            size_t n_slots, int64_t* counts) {
   return run([&] {

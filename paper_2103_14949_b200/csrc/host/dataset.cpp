@@ -121,7 +121,8 @@ DeviceDataset::DeviceDataset(const Graph& g, const Dataset& ds, int64_t first, i
 
 std::shared_ptr<void> predict_device(const engine::Plan& plan, const DeviceDataset& dd,
                                      const SimBinding* binding, bool integer_regime,
-                                     bool allow_fast) {
+                                     bool allow_fast, std::shared_ptr<void>* scores,
+                                     int64_t* per_sample) {
   const Graph& g = plan.graph();
   if (g.outputs().empty()) throw EvalError("model has no outputs");
   const int out_step = plan.step_of(g.outputs()[0].node);
@@ -140,11 +141,17 @@ std::shared_ptr<void> predict_device(const engine::Plan& plan, const DeviceDatas
     if (plan.fused->ok() &&
         plan.fused->eligible(binding, mode == device::EngineMode::kAuto)) {
       const int fb = std::min<int64_t>(std::max<int64_t>(1, dd.size()), 256);
+      const int64_t per = plan.fused->out_per_sample();
+      if (scores) {
+        *scores = engine::device_alloc(static_cast<size_t>(dd.size() * per) * 4);
+        *per_sample = per;
+      }
       for (int64_t first = 0; first < dd.size(); first += fb) {
         const int b = static_cast<int>(std::min<int64_t>(fb, dd.size() - first));
         std::vector<const float*> ins;
         for (size_t k = 0; k < dd.num_inputs(); ++k) ins.push_back(dd.input(k, first));
-        plan.fused->predict(b, ins, binding, static_cast<int64_t*>(preds.get()) + first);
+        plan.fused->predict(b, ins, binding, static_cast<int64_t*>(preds.get()) + first,
+                            scores ? static_cast<float*>(scores->get()) + first * per : nullptr);
       }
       return preds;
     }
@@ -166,6 +173,18 @@ std::shared_ptr<void> predict_device(const engine::Plan& plan, const DeviceDatas
     }
     int64_t* dst = static_cast<int64_t*>(preds.get()) + first;
     if (out.per_numel() == 0) throw EvalError("empty score vector");
+    if (scores) {
+      const int64_t per = out.per_numel();
+      if (!*scores) {
+        *scores = engine::device_alloc(static_cast<size_t>(dd.size() * per) * 4);
+        *per_sample = per;
+      }
+      float* sdst = static_cast<float*>(scores->get()) + first * per;
+      for (int s = 0; s < b; ++s) {
+        cudaMemcpyAsync(sdst + s * per, out.f() + (out.batched ? s * per : 0), per * 4,
+                        cudaMemcpyDeviceToDevice, S());
+      }
+    }
     if (out.batched) {
       kern::argmax_rows(out.f(), b, out.per_numel(), dst, S());
     } else {

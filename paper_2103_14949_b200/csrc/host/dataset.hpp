@@ -30,8 +30,10 @@ class DeviceDataset {
 
 // Per-sample argmax of the first graph output over every sample, on device
 // (int64 [size]).
+// scores (optional): also returns the output rows, [size x *per_sample] fp32.
 std::shared_ptr<void> predict_device(const engine::Plan& plan, const DeviceDataset& dd,
                                      const SimBinding* binding, bool integer_regime,
-                                     bool allow_fast);
+                                     bool allow_fast, std::shared_ptr<void>* scores = nullptr,
+                                     int64_t* per_sample = nullptr);
 
 }  // namespace quantc::gpu

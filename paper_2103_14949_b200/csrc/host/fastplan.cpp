@@ -488,6 +488,104 @@ int classify_shape(const kern::StageTables& t, int O) {
   return 0;
 }
 
+// v as an exactly representable normal float
+bool exact_float(double v, float& out) {
+  out = static_cast<float>(v);
+  return static_cast<double>(out) == v && (v == 0.0 || std::fpclassify(out) == FP_NORMAL);
+}
+
+// Fold the shape's sq chain into EpiConsts (fused.h).  Every factor is a
+// power of two, so each folded product / offset must be an exact float;
+// returns false (interpreter fallback) when one is not.
+bool make_epi(const kern::StageTables& t, int shape, double sxw, kern::EpiConsts& e) {
+  using kern::kEpiExact;
+  using kern::kEpiNonneg;
+  std::memset(&e, 0, sizeof(e));
+  const kern::ProgInstr* c = t.code;
+  std::vector<int> qs;  // local sq indices in program order
+  int res = -1, out0 = -1, out1 = -1;
+  switch (shape) {
+    case 1: qs = {c[0].a}; out0 = static_cast<int>(c[0].b); break;
+    case 2: qs = {c[0].a, c[1].a}; out0 = static_cast<int>(c[1].b); break;
+    case 3:
+      qs = {c[0].a, c[2].a, c[4].a, c[6].a};
+      res = static_cast<int>(c[1].b);
+      out0 = static_cast<int>(c[4].b);
+      out1 = static_cast<int>(c[6].b);
+      break;
+    case 4:
+      qs = {c[0].a, c[2].a, c[3].a};
+      res = static_cast<int>(c[1].b);
+      out0 = static_cast<int>(c[3].b);
+      break;
+    default: return false;
+  }
+  const double M = kern::kMagic;
+  auto round_bounds = [](const kern::FSq& f, kern::EpiSq& q) {
+    q.lo = std::nextafter(f.qmin - 0.5f, std::numeric_limits<float>::infinity());
+    q.hi = std::nextafter(f.qmax + 0.5f, -std::numeric_limits<float>::infinity());
+    return std::fabs(f.qmin) < 65536.0f && std::fabs(f.qmax) < 65536.0f;
+  };
+  // sq0 on the conv output: x0 = fma(a, s_x*s_w / s0, bias / s0)
+  const kern::FSq& f0 = t.sq[qs[0]];
+  kern::EpiSq& q0 = e.q[0];
+  if (!exact_float(sxw / f0.s, q0.k) || !exact_float(f0.inv_s, e.inv0) || !round_bounds(f0, q0)) {
+    return false;
+  }
+  // bias / s0 must stay exact: scaling by 2^j >= 1 never leaves the normal range downwards
+  if (!(f0.inv_s >= 1.0f)) return false;
+  q0.flags = f0.qmin >= 0.0f ? kEpiNonneg : 0;
+  bool prev_nonneg = (q0.flags & kEpiNonneg) != 0;
+  double prev_s = f0.s;
+  size_t next = 1;
+  if (res >= 0) {
+    // x1 = fma(r0, s0/s1, c * s_res/s1); rounding (the sum is not integral in general)
+    const kern::FSq& f1 = t.sq[qs[1]];
+    kern::EpiSq& q1 = e.q[1];
+    const double sres = t.buf[res].scale;
+    if (!exact_float(prev_s / f1.s, q1.k) || !exact_float(sres / f1.s, e.ka) ||
+        !exact_float(-(8388608.0 + 128.0) * (sres / f1.s), e.ka_off) || !round_bounds(f1, q1)) {
+      return false;
+    }
+    q1.flags = f1.qmin >= 0.0f ? kEpiNonneg : 0;
+    prev_nonneg = (q1.flags & kEpiNonneg) != 0;
+    prev_s = f1.s;
+    e.slot_res = t.buf[res].slot;
+    next = 2;
+  }
+  // the remaining sqs all read the previous rounded code R (a fork reads the same R)
+  const bool prev_T = prev_nonneg;
+  for (size_t i = next; i < qs.size(); ++i) {
+    const kern::FSq& f = t.sq[qs[i]];
+    kern::EpiSq& q = e.q[i];
+    const double k = prev_s / f.s;
+    if (!exact_float(k, q.k)) return false;
+    const bool nonneg = f.qmin >= 0.0f || prev_T;
+    q.flags = nonneg ? kEpiNonneg : 0;
+    double off = 0.0;
+    if (k >= 1.0) {
+      // r * 2^d is already an integer: clamp in the output domain only
+      q.flags |= kEpiExact;
+      if (nonneg) {
+        off = prev_T ? M - M * k : M;
+        q.lo = static_cast<float>(M + f.qmin);
+        q.hi = static_cast<float>(M + f.qmax);
+      } else {
+        off = 0.0;
+        q.lo = f.qmin;
+        q.hi = f.qmax;
+      }
+    } else {
+      off = prev_T ? -M * k : 0.0;
+      if (!round_bounds(f, q)) return false;
+    }
+    if (!exact_float(off, q.off)) return false;
+  }
+  e.slot_out[0] = out0 >= 0 ? t.buf[out0].slot : -1;
+  e.slot_out[1] = out1 >= 0 ? t.buf[out1].slot : -1;
+  return true;
+}
+
 }  // namespace
 
 FastPlan::~FastPlan() = default;
@@ -844,7 +942,7 @@ void FastPlan::ensure_arena(int batch) {
 }
 
 void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
-                       const SimBinding* binding, int64_t* d_preds) {
+                       const SimBinding* binding, int64_t* d_preds, float* d_scores) {
   ensure_arena(batch);
   // weight codes are cached per (stage, weight sq parameters); a long search
   // visits many weight bit-widths, so keep roughly the last few bindings
@@ -988,6 +1086,7 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
         sp.scale = static_cast<double>(scale_by_step.count(dv.sq_step) ? scale_by_step.at(dv.sq_step) : 0.0f) *
                    static_cast<double>(wf.s);
         sp.prog = pa;
+        if (pa.shape != 0 && !make_epi(tabs[si], pa.shape, sp.scale, sp.epi)) sp.prog.shape = 0;
         sp.acc_bound = acc_bound[si];
         sp.n_out = st.n_out;
         for (int o = 0; o < st.n_out; ++o) {
@@ -1014,11 +1113,13 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
       }
     }
   }
-  const Val& ov = *vals_[static_cast<size_t>(out_val_)];
-  (void)ov;
   device::counters().fused_batches++;
-  kern::argmax_rows(static_cast<const float*>(arena_[static_cast<size_t>(out_val_)].get()), batch,
-                    out_per_sample_, d_preds, S());
+  const float* out = static_cast<const float*>(arena_[static_cast<size_t>(out_val_)].get());
+  kern::argmax_rows(out, batch, out_per_sample_, d_preds, S());
+  if (d_scores) {
+    ok_cuda(cudaMemcpyAsync(d_scores, out, static_cast<size_t>(batch) * out_per_sample_ * 4,
+                            cudaMemcpyDeviceToDevice, S()));
+  }
 }
 
 }  // namespace quantc::fast

@@ -34,8 +34,10 @@ class FastPlan {
   bool eligible(const SimBinding* binding, bool exact, std::string* why = nullptr) const;
 
   // Runs one batch; writes per-sample argmax of graph output 0 to preds.
+  // d_scores (optional): the output rows themselves, [batch x out_per_sample()]
   void predict(int batch, const std::vector<const float*>& inputs, const SimBinding* binding,
-               int64_t* d_preds);
+               int64_t* d_preds, float* d_scores = nullptr);
+  int64_t out_per_sample() const { return out_per_sample_; }
 
   struct Val;
   struct Stage;

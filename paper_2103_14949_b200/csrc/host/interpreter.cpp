@@ -144,6 +144,23 @@ std::vector<int64_t> predict_top1(const Graph& g, const Dataset& dataset, int wo
   return h;
 }
 
+std::vector<float> predict_scores(const Graph& g, const Dataset& dataset,
+                                  const SimBinding* binding, int64_t* per_sample) {
+  *per_sample = 0;
+  if (dataset.empty()) return {};
+  const engine::PlanLease lease = engine::lease_plan(g);
+  const engine::Plan& plan = lease.plan();
+  gpu::DeviceDataset dd(g, dataset);
+  const bool realized = g.is_realized();
+  std::shared_ptr<void> scores;
+  gpu::predict_device(plan, dd, realized ? nullptr : binding, realized,
+                      /*allow_fast=*/binding != nullptr, &scores, per_sample);
+  std::vector<float> h(static_cast<size_t>(dataset.size() * *per_sample));
+  cudaMemcpyAsync(h.data(), scores.get(), h.size() * 4, cudaMemcpyDeviceToHost, S());
+  device::synchronize();
+  return h;
+}
+
 double top1_agreement(const Graph& g_ref, const Graph& g_test, const Dataset& dataset,
                       int workers) {
   if (dataset.empty()) throw EvalError("empty dataset");

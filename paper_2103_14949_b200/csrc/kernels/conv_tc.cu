@@ -149,6 +149,7 @@ struct TcArgs {
   int always_small;  // |acc| <= 2^24 guaranteed for this layer
   ProgArgs prog;
   int m_tiles, n_tiles;
+  EpiConsts epi;
 };
 
 template <int W>
@@ -208,7 +209,14 @@ __global__ void __launch_bounds__(THREADS, 1)
   // (kh, kw); x = byte offset from the row's (ih0, iw0) pixel, y = kh<<16|kw
   // (kh = kw = 0x4000 for chunks past the taps or past C: always out of bounds)
   int2* ktab = reinterpret_cast<int2*>(tabs + 1);
+  // shape kernels: bias pre-scaled into sq0's grid, btab[n] = bias[n] / s0
+  float* btab = reinterpret_cast<float*>(ktab + (args.gather ? args.K / 16 : 0));
   load_tables(tabs, args.prog.tables);
+  if (SHAPE != kShapeGeneric) {
+    for (int n = threadIdx.x; n < args.n_tiles * BN; n += blockDim.x) {
+      btab[n] = (args.bias && n < args.N) ? __fmul_rn(__ldg(args.bias + n), args.epi.inv0) : 0.0f;
+    }
+  }
   if (args.gather) {
     const TcGeom& g = args.g;
     for (int q = threadIdx.x; q < args.K / 16; q += blockDim.x) {
@@ -355,7 +363,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int r = quarter * 32 + lane;
     const bool leader = threadIdx.x == 0;
     TileIo io{su32(slots), r, static_cast<int>(SLOT_BYTES), SWZ};
-    const ShapeRegs sregs = load_shape_regs(*tabs, SHAPE);
     auto load_res = [&](int t) {
       const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
       uint8_t* dst = slots + args.n_out * SLOT_BYTES;
@@ -385,54 +392,51 @@ __global__ void __launch_bounds__(THREADS, 1)
         // are clipped by the TMA store), zp = 0, no live acc clamp.  TMEM
         // loads run one chunk ahead of the math.
         const int cbeg = half * (BN / 2), cend = cbeg + BN / 2;
+        const EpiConsts& e = args.epi;
         uint32_t d[EW];
         tmem_ld<EW>(tbase + cbeg, d);
 #pragma unroll 1
         for (int c0 = cbeg; c0 < cend; c0 += EW) {
           tmem_wait(d);
           const int n = n0 + c0;
-          float v[EW];
-          bool small = args.scale_f != 0.0f;
-          if (!args.always_small) {
+          // acc -> float without the conversion pipe: bits(0x4B400000 + a) is
+          // the float M + a for |a| < 2^22 (checked for the whole chunk)
+          uint32_t u[EW];
+          uint32_t chk = 0;
 #pragma unroll
-            for (int j = 0; j < EW; ++j) {
-              const int32_t a = static_cast<int32_t>(d[j]);
-              small = small && a <= (1 << 24) && a >= -(1 << 24);
-            }
+          for (int j = 0; j < EW; ++j) {
+            u[j] = d[j] + 0x4B400000u;
+            chk |= u[j] ^ 0x4B000000u;
           }
-          uint32_t dn[EW];
-#pragma unroll
-          for (int j = 0; j < EW; ++j) dn[j] = d[j];
           if (c0 + EW < cend) tmem_ld<EW>(tbase + c0 + EW, d);
           if (n < args.N) {
-            float bias[EW];
-            if (args.bias) {
+            float x[EW];
+            float bs[EW];
 #pragma unroll
-              for (int j = 0; j < EW; j += 4) {
-                const float4 b4 = __ldg(reinterpret_cast<const float4*>(args.bias + n + j));
-                bias[j] = b4.x;
-                bias[j + 1] = b4.y;
-                bias[j + 2] = b4.z;
-                bias[j + 3] = b4.w;
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < EW; ++j) bias[j] = 0.0f;
+            for (int j = 0; j < EW; j += 4) {
+              const int4 b4 = lds128(su32(btab + n + j));
+              bs[j] = __int_as_float(b4.x);
+              bs[j + 1] = __int_as_float(b4.y);
+              bs[j + 2] = __int_as_float(b4.z);
+              bs[j + 3] = __int_as_float(b4.w);
             }
-            if (small) {
-              // acc * s is exact (|acc| <= 2^24, pow2 s): fma == fadd(fmul)
+            if (chk < 0x800000u) {
+              // x0 = (a*s + b)/s0 = fma(a, s/s0, b/s0): a*s/s0 exact, one
+              // rounding == the reference's RN24(RN53(a*s + b)) scaled by 2^k
 #pragma unroll
               for (int j = 0; j < EW; ++j) {
-                v[j] = __fmaf_rn(static_cast<float>(static_cast<int32_t>(dn[j])), args.scale_f, bias[j]);
+                x[j] = __fmaf_rn(__fsub_rn(__uint_as_float(u[j]), kMagic), e.q[0].k, bs[j]);
               }
             } else {
 #pragma unroll
               for (int j = 0; j < EW; ++j) {
-                v[j] = __double2float_rn(__fma_rn(static_cast<double>(static_cast<int32_t>(dn[j])),
-                                                  args.scale, static_cast<double>(bias[j])));
+                const int32_t a = static_cast<int32_t>(u[j] - 0x4B400000u);
+                const double b = args.bias ? static_cast<double>(__ldg(args.bias + n + j)) : 0.0;
+                x[j] = __fmul_rn(__double2float_rn(__fma_rn(static_cast<double>(a), args.scale, b)),
+                                 e.inv0);
               }
             }
-            run_shape_regs<SHAPE>(v, sregs, io, c0);
+            run_shape_epi<SHAPE>(x, e, io, c0);
           }
         }
       } else
@@ -571,7 +575,8 @@ void launch_tc(const CUtensorMap* maps, TcArgs a, cudaStream_t s) {
   constexpr int stage_bytes = BM * BK + BN * BK;
   const int fixed = 1024 + (a.n_out + a.has_res) * BM * BN + (2 * MAX_STAGES + 6) * 8 + 16 +
                     static_cast<int>(sizeof(StageTables)) + 64 +
-                    (a.gather ? a.K / 16 * static_cast<int>(sizeof(int2)) : 0);
+                    (a.gather ? a.K / 16 * static_cast<int>(sizeof(int2)) : 0) +
+                    (SHAPE != kShapeGeneric ? a.n_tiles * BN * 4 : 0);
   int stages = (SMEM_LIMIT - fixed) / stage_bytes;
   const int nk = a.K / BK;
   stages = stages > MAX_STAGES ? MAX_STAGES : stages;
@@ -633,6 +638,7 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
     a.scale_f = (static_cast<double>(f) == sp.scale && std::fpclassify(f) == FP_NORMAL) ? f : 0.0f;
   }
   a.prog = sp.prog;
+  a.epi = sp.epi;
   a.always_small = sp.acc_bound <= static_cast<double>(1 << 24) ? 1 : 0;
   a.m_tiles = static_cast<int>((sp.M + BM - 1) / BM);
   // narrower output tiles while that still fits the grid in one wave: a

@@ -220,93 +220,90 @@ __device__ __forceinline__ void load_values(const ProgBuf& b, int64_t m, int n0,
 enum : int { kShapeGeneric = 0, kShapeStore = 1, kShapeSqStore = 2, kShapeAddFork = 3,
              kShapeAdd = 4 };
 
-// ---- register-resident shape epilogues ------------------------------------------
-// For shapes 1-4 the host guarantees (classify_shape): every sq has zp = 0, no
-// live accumulator clamp (elided by interval analysis) and is not
-// passthrough; all code I/O is through tile slots.  The per-op parameters are
-// then 4 floats, loaded once per kernel.
-struct RegSq {
-  float inv, s, qmin, qmax;
-};
-
-struct ShapeRegs {
-  RegSq sq[4];
-  int slot[4];     // store slots / add source slot, in program order
-  float add_scale;
-};
-
-__device__ __forceinline__ ShapeRegs load_shape_regs(const StageTables& t, int shape) {
-  ShapeRegs r{};
-  const ProgInstr* c = t.code;
-  auto take = [&](int i, const ProgInstr& ins) {
-    const FSq& f = t.sq[ins.a];
-    r.sq[i] = RegSq{f.inv_s, f.s, f.qmin, f.qmax};
-  };
-  if (shape == kShapeStore) {
-    take(0, c[0]);
-    r.slot[0] = t.buf[c[0].b].slot;
-  } else if (shape == kShapeSqStore) {
-    take(0, c[0]);
-    take(1, c[1]);
-    r.slot[0] = t.buf[c[1].b].slot;
-  } else if (shape == kShapeAddFork) {
-    take(0, c[0]);
-    take(1, c[2]);
-    take(2, c[4]);
-    take(3, c[6]);
-    r.slot[0] = t.buf[c[4].b].slot;
-    r.slot[1] = t.buf[c[6].b].slot;
-    r.slot[2] = t.buf[c[1].b].slot;
-    r.add_scale = t.buf[c[1].b].scale;
-  } else if (shape == kShapeAdd) {
-    take(0, c[0]);
-    take(1, c[2]);
-    take(2, c[3]);
-    r.slot[0] = t.buf[c[3].b].slot;
-    r.slot[2] = t.buf[c[1].b].slot;
-    r.add_scale = t.buf[c[1].b].scale;
-  }
-  return r;
-}
-
-template <int W>
-__device__ __forceinline__ void rsq(float (&v)[W], const RegSq& p) {
+// ---- straight-line shape epilogues (no conversion-pipe instructions) -------------
+// Host preconditions (fastplan classify_shape / make_epi): every sq of the
+// shape has zp = 0, no live accumulator clamp, is not passthrough; code I/O
+// goes through tile slots; every scale ratio folded into EpiConsts is an
+// exact power of two.  Domains and rounding: fused.h (EpiSq).
+// round 16 values into sq q's code domain; the (uniform) flag tests sit
+// outside the element loops so each variant is straight-line code
+__device__ __forceinline__ void epi_round(float (&x)[16], const EpiSq& q) {
 #pragma unroll
-  for (int j = 0; j < W; ++j) v[j] = __fmul_rn(clampq(roundf(__fmul_rn(v[j], p.inv)), p.qmin, p.qmax), p.s);
-}
-
-template <int W>
-__device__ __forceinline__ void rsq_store(const float (&v)[W], const RegSq& p, const TileIo& io,
-                                          int slot, int cl) {
-  float q[W];
+  for (int j = 0; j < 16; ++j) x[j] = fminf(fmaxf(x[j], q.lo), q.hi);
+  if (q.flags & kEpiExact) return;
+  if (q.flags & kEpiNonneg) {
 #pragma unroll
-  for (int j = 0; j < W; ++j) q[j] = clampq(roundf(__fmul_rn(v[j], p.inv)), p.qmin, p.qmax);
-  sts128(tile_addr(io, slot, cl),
-         make_int4(static_cast<int>(pack4(q[0], q[1], q[2], q[3])),
-                   static_cast<int>(pack4(q[4], q[5], q[6], q[7])),
-                   static_cast<int>(pack4(q[8], q[9], q[10], q[11])),
-                   static_cast<int>(pack4(q[12], q[13], q[14], q[15]))));
-}
-
-template <int SHAPE>
-__device__ __forceinline__ void run_shape_regs(float (&v)[16], const ShapeRegs& r,
-                                               const TileIo& io, int cl) {
-  if (SHAPE == kShapeStore) {
-    rsq_store<16>(v, r.sq[0], io, r.slot[0], cl);
-  } else if (SHAPE == kShapeSqStore) {
-    rsq<16>(v, r.sq[0]);
-    rsq_store<16>(v, r.sq[1], io, r.slot[0], cl);
+    for (int j = 0; j < 16; ++j) x[j] = __fadd_rz(__fadd_rz(x[j], 0.5f), kMagic);
   } else {
-    rsq<16>(v, r.sq[0]);
-    const int4 raw = lds128(tile_addr(io, r.slot[2], cl));
-    const int8_t* cc = reinterpret_cast<const int8_t*>(&raw);
-    // code * scale is exact (|code| <= 128, normal pow2 scale): one fma
-    // rounds like fadd(v, fmul(code, scale))
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = __fmaf_rn(static_cast<float>(cc[j]), r.add_scale, v[j]);
-    rsq<16>(v, r.sq[1]);
-    rsq_store<16>(v, r.sq[2], io, r.slot[0], cl);
-    if (SHAPE == kShapeAddFork) rsq_store<16>(v, r.sq[3], io, r.slot[1], cl);
+    for (int j = 0; j < 16; ++j) {
+      x[j] = copysignf(__fsub_rn(__fadd_rz(__fadd_rz(fabsf(x[j]), 0.5f), kMagic), kMagic), x[j]);
+    }
+  }
+}
+
+// y = fma(R, q.k, q.off), rounded into q's domain
+__device__ __forceinline__ void epi_next(const float (&R)[16], float (&y)[16], const EpiSq& q) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) y[j] = __fmaf_rn(R[j], q.k, q.off);
+  epi_round(y, q);
+}
+
+// 16 rounded codes -> 16 int8 bytes (low byte of the T-domain bits)
+__device__ __forceinline__ void epi_store(float (&R)[16], const EpiSq& q, const TileIo& io,
+                                          int slot, int cl) {
+  if (!(q.flags & kEpiNonneg)) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) R[j] = __fadd_rn(R[j], kMagic);
+  }
+  uint32_t w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t lo = __byte_perm(__float_as_uint(R[4 * i]), __float_as_uint(R[4 * i + 1]), 0x0040);
+    const uint32_t hi =
+        __byte_perm(__float_as_uint(R[4 * i + 2]), __float_as_uint(R[4 * i + 3]), 0x0040);
+    w[i] = __byte_perm(lo, hi, 0x5410);
+  }
+  sts128(tile_addr(io, slot, cl), make_int4(static_cast<int>(w[0]), static_cast<int>(w[1]),
+                                            static_cast<int>(w[2]), static_cast<int>(w[3])));
+}
+
+// x[16] = conv output scaled into sq0's grid (x0 = v / s0); runs the shape
+template <int SHAPE>
+__device__ __forceinline__ void run_shape_epi(float (&x)[16], const EpiConsts& e,
+                                              const TileIo& io, int cl) {
+  epi_round(x, e.q[0]);
+  if (SHAPE == kShapeStore) {
+    epi_store(x, e.q[0], io, e.slot_out[0], cl);
+    return;
+  }
+  float y[16];
+  if (SHAPE == kShapeSqStore) {
+    epi_next(x, y, e.q[1]);
+    epi_store(y, e.q[1], io, e.slot_out[0], cl);
+    return;
+  }
+  // residual add: x1 = (r0 * s0 + c * s_res) / s1 in one rounding
+  if (e.q[0].flags & kEpiNonneg) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) x[j] = __fsub_rn(x[j], kMagic);
+  }
+  const int4 raw = lds128(tile_addr(io, e.slot_res, cl));
+  const uint32_t wr[4] = {static_cast<uint32_t>(raw.x) ^ 0x80808080u,
+                          static_cast<uint32_t>(raw.y) ^ 0x80808080u,
+                          static_cast<uint32_t>(raw.z) ^ 0x80808080u,
+                          static_cast<uint32_t>(raw.w) ^ 0x80808080u};
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const float C = __uint_as_float(__byte_perm(wr[j >> 2], 0x4B000000u, 0x7650u + (j & 3)));
+    x[j] = __fmaf_rn(x[j], e.q[1].k, __fmaf_rn(C, e.ka, e.ka_off));
+  }
+  epi_round(x, e.q[1]);
+  epi_next(x, y, e.q[2]);
+  epi_store(y, e.q[2], io, e.slot_out[0], cl);
+  if (SHAPE == kShapeAddFork) {
+    epi_next(x, y, e.q[3]);
+    epi_store(y, e.q[3], io, e.slot_out[1], cl);
   }
 }
 

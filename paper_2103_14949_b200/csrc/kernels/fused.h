@@ -105,6 +105,41 @@ struct StageTables {
   float2 clip[kMaxClip];
 };
 
+// ---- straight-line shape epilogues: host-folded constants -----------------------
+// The shape kernels (fused.cuh kShape*) evaluate their sq chain without any
+// conversion-pipe instruction.  Codes are carried as floats in one of two
+// domains:
+//   r-domain: the signed integer code r as a float;
+//   T-domain: M + r with M = 1.5*2^23 (bits 0x4B400000 + r), used when r is
+//             known >= 0 — its low byte is the int8 code.
+// Rounding (reference std::round, half away from zero) of x clamped to
+// [qmin - 1/2, qmax + 1/2] (nearest floats inside):
+//   T-domain: RZ(RZ(x + 1/2) + M)             (x >= -1/2)
+//   r-domain: copysign(RZ(RZ(|x| + 1/2) + M) - M, x)
+// RZ(x + 1/2) keeps floor(x + 1/2) exact (integers are representable), and
+// RZ(t + M) truncates the fraction on the unit grid of [2^23, 2^24).
+constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+
+enum : int32_t { kEpiNonneg = 1, kEpiExact = 2 };
+
+struct EpiSq {
+  float k;    // x = fma(R_in, k, off): input scale ratio s_in / s (sq0: s_x*s_w / s)
+  float off;  // domain offset of the input (see fastplan make_epi)
+  float lo, hi;   // clamp of x: rounding bounds, or (exact) the output-domain bounds
+  int32_t flags;  // kEpiNonneg: output in T-domain; kEpiExact: x already integral
+  int32_t pad_;
+};
+
+struct EpiConsts {
+  EpiSq q[4];       // program-order sq ops of the shape
+  float inv0;       // 1 / s of sq0 (bias table and the wide-accumulator path)
+  float ka, ka_off; // residual code c (biased magic float C = 2^23 + c + 128):
+                    // c * s_res / s_1 = fma(C, ka, ka_off)
+  int32_t slot_out[2];
+  int32_t slot_res;
+  int32_t pad_;
+};
+
 // kernels receive the stage's table block in global memory
 struct ProgArgs {
   const StageTables* tables;

@@ -135,6 +135,7 @@ struct TcConvSpec {
   int res_cols;
   int64_t res_ld;
   double acc_bound;  // host bound on |sum_k a*b| (K * max|qa| * max|qb|)
+  EpiConsts epi;     // shape kernels (prog.shape != 0): host-folded constants
 };
 void tc_conv(const TcConvSpec& spec, cudaStream_t s);
 int tc_conv_bn(int O);  // output-channel tile the kernel uses for O channels

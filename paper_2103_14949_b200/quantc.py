@@ -412,6 +412,27 @@ class Quantc:
         return self._vec(self.lib.qc_predict_top1, (g.h, d.h, workers, idp, params, nb),
                          C.c_int64, first_cap=max(1, d.n))
 
+    def predict_scores(self, g: "Graph", d: "Dataset", binding=None) -> np.ndarray:
+        """B200 extension (quantc/device.hpp): the fp32 output rows behind
+        predict_top1 under the active engine mode, shape [samples, per]."""
+        fn = self.lib.qc_predict_scores
+        fn.restype = C.c_int
+        fn.argtypes = [_P, _P, _PI64, C.POINTER(QParams), _SZ, C.POINTER(C.c_float), _SZ, _PSZ,
+                       _PI64]
+        ids, params, nb, idp = self._binding(binding)
+        per = C.c_int64(0)
+        n = C.c_size_t(0)
+        cap = max(1, d.n) * 1024
+        while True:
+            buf = np.zeros(cap, np.float32)
+            rc = fn(g.h, d.h, idp, params, nb, buf.ctypes.data_as(C.POINTER(C.c_float)), cap,
+                    C.byref(n), C.byref(per))
+            if rc == 10 and n.value > cap:
+                cap = n.value
+                continue
+            self.check(rc)
+            return buf[: n.value].reshape(d.n, -1)
+
     # -- search (search.hpp) --------------------------------------------
     def evaluator(self, sim_g, spec, topo, thresholds: Dict[int, float], stats, calib,
                   min_bit=4, workers=0) -> "CandidateEvaluator":

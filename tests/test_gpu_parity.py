@@ -244,3 +244,31 @@ def test_predict_top1_plan_cache(b200, ref, small_cnn):
     a3 = _pipeline(b200, m, data)
     np.testing.assert_array_equal(b200.predict_top1(a3["sim"], a3["ds"], 0, a3["ev"].bind(cands[1])),
                                   ref.predict_top1(r["sim"], r["ds"], 0, r["ev"].bind(cands[1])))
+
+
+@pytest.mark.parametrize("name,n", [("small_cnn", 16), ("resnet18", 8), ("resnet50", 4)])
+def test_fused_scores_bit_exact_vs_exact_engine(b200, cuda_lib, name, n):
+    """Below the argmax: the fused engine's fp32 output rows (every class
+    score) equal the FP64 exact engine's byte for byte, over bindings that mix
+    bit-widths (so sq chains hit signed / non-negative / exact-ratio epilogue
+    variants and half-way ties)."""
+    m = {"small_cnn": lambda: F.small_cnn(),
+         "resnet18": lambda: F.resnet(18, image=64, classes=100),
+         "resnet50": lambda: F.resnet(50, image=64, classes=100)}[name]()
+    data = m.data(n)
+    p = _pipeline(b200, m, data, method="quantile", pow2=True, quantile=0.99)
+    sp = p["ev"].space()
+    rng = np.random.default_rng(21)
+    cands = [sp.all_hi(), sp.all_lo()] + [
+        [int(rng.integers(lo, hi + 1)) for lo, hi in zip(sp.lo, sp.hi)] for _ in range(4)]
+    for c in cands:
+        bnd = p["ev"].bind(c)
+        cuda_lib.set_engine_mode("exact")
+        exact = b200.predict_scores(p["sim"], p["ds"], bnd)
+        cuda_lib.set_engine_mode("auto")
+        f0 = cuda_lib.counters()["fused_batches"]
+        fused = b200.predict_scores(p["sim"], p["ds"], bnd)
+        assert cuda_lib.counters()["fused_batches"] > f0, "fused engine was not used"
+        assert exact.shape == fused.shape
+        assert exact.tobytes() == fused.tobytes(), (
+            name, int((exact != fused).sum()), float(np.abs(exact - fused).max()))
