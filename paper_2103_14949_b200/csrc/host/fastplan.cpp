@@ -729,6 +729,8 @@ void FastPlan::compile() {
             st->ldk = st->C;
             st->Ktrue = st->taps * st->C;
           }
+          // the gather producer tracks tap validity in a 64-bit mask
+          if (st->gather && st->taps > 63) fail("conv kernel with more than 63 taps");
           st->rows_out_ps = static_cast<int64_t>(st->n0) * st->OH * st->OW;
           b.rows_ps = st->rows_out_ps;
         }

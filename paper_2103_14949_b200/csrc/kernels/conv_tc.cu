@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 #include <stdexcept>
 
@@ -96,6 +97,19 @@ __device__ __forceinline__ void tma2d(const CUtensorMap* m, uint64_t* bar, void*
       "l"(reinterpret_cast<uint64_t>(m)), "r"(su32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// im2col TMA: 128 consecutive output pixels' window starts (w, h, n) walked
+// inside the map's bounding box, channels [c, c+128) of input pixel
+// (w + off_w, h + off_h, n); outside the tensor (padding, rows past the last
+// image) reads as zero
+__device__ __forceinline__ void tma_im2col(const CUtensorMap* m, uint64_t* bar, void* dst, int c,
+                                          int w, int h, int n, uint16_t off_w, uint16_t off_h) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(su32(bar)), "r"(c), "r"(w), "r"(h), "r"(n),
+      "h"(off_w), "h"(off_h)
+      : "memory");
+}
 __device__ __forceinline__ void tma_store2d(const CUtensorMap* m, const void* src, int c0,
                                             int c1) {
   asm volatile(
@@ -142,6 +156,7 @@ struct TcArgs {
   int stages;    // runtime pipeline depth (<= MAX_STAGES)
   int n_out;     // smem-staged code outputs (TMA store), 0..2
   int has_res;   // TMA-prefetched residual slot (index n_out)
+  int dbuf;      // 1: two slot sets, alternating by tile (stores / prefetch overlap)
   TcGeom g;
   const float* bias;
   double scale;
@@ -198,34 +213,34 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint8_t* sb = sa + stages * A_BYTES;
   uint8_t* slots = sb + stages * B_BYTES;  // 1024-aligned (stage sizes are multiples of 1 KB)
   const int n_slots = args.n_out + args.has_res;
-  uint64_t* full = reinterpret_cast<uint64_t*>(slots + n_slots * SLOT_BYTES);
+  const uint32_t SET_BYTES = n_slots * SLOT_BYTES;  // one slot set
+  uint64_t* full = reinterpret_cast<uint64_t*>(slots + (args.dbuf + 1) * SET_BYTES);
   uint64_t* empty = full + MAX_STAGES;
   uint64_t* tfull = empty + MAX_STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* rfull = tempty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 2);  // rfull[2]: one per slot set
   StageTables* tabs = reinterpret_cast<StageTables*>(tmem_slot + 4);
   // gather K-chunk table: chunk q (16 bytes of K) = channel run c..c+15 of tap
-  // (kh, kw); x = byte offset from the row's (ih0, iw0) pixel, y = kh<<16|kw
-  // (kh = kw = 0x4000 for chunks past the taps or past C: always out of bounds)
+  // (kh, kw); x = byte offset from the row's (ih0, iw0) pixel, y = tap index
+  // kh*KW + kw (63 for chunks past the taps or past C: never valid)
   int2* ktab = reinterpret_cast<int2*>(tabs + 1);
   // shape kernels: bias pre-scaled into sq0's grid, btab[n] = bias[n] / s0
-  float* btab = reinterpret_cast<float*>(ktab + (args.gather ? args.K / 16 : 0));
+  float* btab = reinterpret_cast<float*>(ktab + (args.gather == 1 ? args.K / 16 : 0));
   load_tables(tabs, args.prog.tables);
   if (SHAPE != kShapeGeneric) {
     for (int n = threadIdx.x; n < args.n_tiles * BN; n += blockDim.x) {
       btab[n] = (args.bias && n < args.N) ? __fmul_rn(__ldg(args.bias + n), args.epi.inv0) : 0.0f;
     }
   }
-  if (args.gather) {
+  if (args.gather == 1) {
     const TcGeom& g = args.g;
     for (int q = threadIdx.x; q < args.K / 16; q += blockDim.x) {
       const int k = q * 16;
       const int tap = k / g.ld, c = k - tap * g.ld;
       const int kh = tap / g.KW, kw = tap - kh * g.KW;
       const bool ok = tap < g.KH * g.KW && c < g.C;
-      ktab[q] = ok ? make_int2((kh * g.W + kw) * g.ld + c, (kh << 16) | kw)
-                   : make_int2(0, (0x4000 << 16) | 0x4000);
+      ktab[q] = ok ? make_int2((kh * g.W + kw) * g.ld + c, tap) : make_int2(0, 63);
     }
   }
 
@@ -236,14 +251,15 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
-      bar_init(&full[s], args.gather ? (PROD_WARPS * 32 + 1) : 1);
+      bar_init(&full[s], args.gather == 1 ? (PROD_WARPS * 32 + 1) : 1);
       bar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       bar_init(&tfull[a], 1);
       bar_init(&tempty[a], EPI_WARPS * 32);
     }
-    bar_init(rfull, 1);
+    bar_init(&rfull[0], 1);
+    bar_init(&rfull[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == MMA_WARP) {
@@ -260,90 +276,142 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp >= EPI_WARPS && warp < MMA_WARP) {
     // ================= producers =================
     const int p = threadIdx.x - EPI_WARPS * 32;  // 0..127 = tile row
-    if (!args.gather) {
+    if (args.gather == 2) {
+      // im2col TMA: K block kb = channels [c0, c0+128) of tap (kh, kw)
       if (p == 0) {
-        uint32_t it = 0;
+        const TcGeom& g = args.g;
+        const int ohw = g.OH * g.OW;
+        int s = 0;
+        uint32_t ph = 0;
+        bool wrapped = false;
         for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
           const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
-          for (int kb = 0; kb < nk; ++kb, ++it) {
-            const int s = it % stages;
-            if (it >= static_cast<uint32_t>(stages)) bar_wait_sleep(&empty[s], ((it / stages) - 1) & 1);
+          const int img = m0 / ohw, rem = m0 - img * ohw;
+          const int oh = rem / g.OW, ow = rem - oh * g.OW;
+          const int w0 = ow * g.sw - g.pw, h0 = oh * g.sh - g.ph;
+          for (int kb = 0; kb < nk; ++kb) {
+            const int tap = (kb * BK) / g.ld, c0 = kb * BK - tap * g.ld;
+            const int kh = tap / g.KW, kw = tap - kh * g.KW;
+            if (wrapped) bar_wait_sleep(&empty[s], ph ^ 1);
+            bar_expect(&full[s], A_BYTES + B_BYTES);
+            tma_im2col(&map_a, &full[s], sa + s * A_BYTES, c0, w0, h0, img,
+                       static_cast<uint16_t>(kw), static_cast<uint16_t>(kh));
+            tma2d(&map_b, &full[s], sb + s * B_BYTES, kb * BK, n0);
+            if (++s == stages) {
+              s = 0;
+              ph ^= 1;
+              wrapped = true;
+            }
+          }
+        }
+      }
+    } else if (!args.gather) {
+      if (p == 0) {
+        int s = 0;
+        uint32_t ph = 0;
+        bool wrapped = false;  // ring slots are reused from the second lap on
+        for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+          const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
+          for (int kb = 0; kb < nk; ++kb) {
+            if (wrapped) bar_wait_sleep(&empty[s], ph ^ 1);
             bar_expect(&full[s], A_BYTES + B_BYTES);
             tma2d(&map_a, &full[s], sa + s * A_BYTES, kb * BK, m0);
             tma2d(&map_b, &full[s], sb + s * B_BYTES, kb * BK, n0);
+            if (++s == stages) {
+              s = 0;
+              ph ^= 1;
+              wrapped = true;
+            }
           }
         }
       }
     } else {
       const TcGeom& g = args.g;
-      uint32_t it = 0;
-      int pending = -1;  // stage whose copies are in flight but not yet arrived
+      int s = 0;
+      uint32_t ph = 0;
+      bool wrapped = false;
       // this thread's 8 swizzled 16-byte destinations within its A row
       const uint32_t swz_row = static_cast<uint32_t>(p) * 128;
       for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
         const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
         const int64_t row = static_cast<int64_t>(m0) + p;
-        // rows past M get an origin no tap can bring in bounds
-        int ih0 = -0x20000000, iw0 = -0x20000000;
-        const int8_t* rowbase = g.x;
+        // tap validity of this row (bit kh*KW + kw); rows past M: none.
+        // rowoff: byte offset of the (ih0, iw0) pixel (may be negative; only
+        // valid taps are ever added to it)
+        uint64_t tapmask = 0;
+        int64_t rowoff = 0;
         if (row < args.M) {
           const int ohw = g.OH * g.OW;
           const int img = static_cast<int>(row / ohw);
           const int rem = static_cast<int>(row - static_cast<int64_t>(img) * ohw);
           const int oh = rem / g.OW;
-          ih0 = oh * g.sh - g.ph;
-          iw0 = (rem - oh * g.OW) * g.sw - g.pw;
-          rowbase = g.x + ((static_cast<int64_t>(img) * g.H + ih0) * g.W + iw0) * g.ld;
+          const int ih0 = oh * g.sh - g.ph;
+          const int iw0 = (rem - oh * g.OW) * g.sw - g.pw;
+          rowoff = ((static_cast<int64_t>(img) * g.H + ih0) * g.W + iw0) * g.ld;
+          uint64_t colmask = 0;
+          for (int kw = 0; kw < g.KW; ++kw) {
+            if (static_cast<uint32_t>(iw0 + kw) < static_cast<uint32_t>(g.W)) colmask |= 1ull << kw;
+          }
+          for (int kh = 0; kh < g.KH; ++kh) {
+            if (static_cast<uint32_t>(ih0 + kh) < static_cast<uint32_t>(g.H)) tapmask |= colmask << (kh * g.KW);
+          }
         }
-        for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % stages;
-          if (it >= static_cast<uint32_t>(stages)) bar_wait_sleep(&empty[s], ((it / stages) - 1) & 1);
+        for (int kb = 0; kb < nk; ++kb) {
+          if (wrapped) bar_wait_sleep(&empty[s], ph ^ 1);
           if (p == 0) {
             bar_expect(&full[s], B_BYTES);
             tma2d(&map_b, &full[s], sb + s * B_BYTES, kb * BK, n0);
           }
           const uint32_t dst_row = su32(sa + s * A_BYTES) + swz_row;
           const uint32_t kt = su32(ktab) + kb * 8 * sizeof(int2);
+          // the table is read-only after the start-up barrier: plain (non-volatile)
+          // loads, so all eight chunk addresses are computed independently
+          int e[16];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            asm("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                : "=r"(e[4 * j]), "=r"(e[4 * j + 1]), "=r"(e[4 * j + 2]), "=r"(e[4 * j + 3])
+                : "r"(kt + j * 16));
+          }
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            int2 e;
-            asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(e.x), "=r"(e.y) : "r"(kt + j * 8));
-            const bool ok = static_cast<uint32_t>(ih0 + (e.y >> 16)) < static_cast<uint32_t>(g.H) &&
-                            static_cast<uint32_t>(iw0 + (e.y & 0xffff)) < static_cast<uint32_t>(g.W);
-            const int8_t* src = ok ? rowbase + e.x : g.x;
+            const bool ok = (tapmask >> e[2 * j + 1]) & 1;
+            // select the offset, then one 64-bit add: the address lands in a
+            // register pair and the eight copies do not serialise on a shared one
+            const int8_t* src = g.x + (ok ? rowoff + e[2 * j] : int64_t{0});
             const uint32_t dst = dst_row + ((j ^ (p & 7)) << 4);
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
                          "r"(ok ? 16u : 0u)
                          : "memory");
           }
-          asm volatile("cp.async.commit_group;" ::: "memory");
-          if (pending >= 0) {
-            asm volatile("cp.async.wait_group 1;" ::: "memory");
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            bar_arrive(&full[pending]);
+          // arrive on full[s] when this thread's copies land — no blocking
+          // wait here, so the producers run ahead through the whole ring
+          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(su32(&full[s]))
+                       : "memory");
+          if (++s == stages) {
+            s = 0;
+            ph ^= 1;
+            wrapped = true;
           }
-          pending = s;
         }
-      }
-      if (pending >= 0) {
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        bar_arrive(&full[pending]);
       }
     }
   } else if (warp == MMA_WARP) {
     // ================= MMA issuer =================
     if (lane == 0) {
       constexpr uint32_t id = idesc(BM, BN);
-      uint32_t it = 0, tl = 0;
+      uint32_t tl = 0, ph = 0;
+      int s = 0;
       for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
         const uint32_t acc = tl & 1;
         if (tl >= 2) bar_wait_sleep(&tempty[acc], ((tl / 2) - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + acc * BN;
-        for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % stages;
-          bar_wait_sleep(&full[s], (it / stages) & 1);
+        for (int kb = 0; kb < nk; ++kb) {
+          bar_wait_sleep(&full[s], ph);
+          // gathered A was written by cp.async (generic proxy): make it
+          // visible to the tensor core's async-proxy reads
+          if (args.gather == 1) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t ab = su32(sa + s * A_BYTES), bb = su32(sb + s * B_BYTES);
 #pragma unroll
@@ -352,6 +420,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                 (kb | k) != 0 ? 1u : 0u);
           }
           commit(&empty[s]);
+          if (++s == stages) {
+            s = 0;
+            ph ^= 1;
+          }
         }
         commit(&tfull[acc]);
       }
@@ -362,28 +434,48 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int half = warp >> 2;
     const int r = quarter * 32 + lane;
     const bool leader = threadIdx.x == 0;
-    TileIo io{su32(slots), r, static_cast<int>(SLOT_BYTES), SWZ};
-    auto load_res = [&](int t) {
+    // slot set of the tile with local index tl
+    auto set_of = [&](uint32_t tl) -> uint8_t* { return slots + (args.dbuf ? (tl & 1) : 0) * SET_BYTES; };
+    auto load_res = [&](int t, uint32_t tl) {
       const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
-      uint8_t* dst = slots + args.n_out * SLOT_BYTES;
-      bar_expect(rfull, SLOT_BYTES);
+      uint8_t* dst = set_of(tl) + args.n_out * SLOT_BYTES;
+      uint64_t* bar = &rfull[args.dbuf ? (tl & 1) : 0];
+      bar_expect(bar, SLOT_BYTES);
       for (int blk = 0; blk < BN / SWZ; ++blk) {
-        tma2d(&map_r, rfull, dst + blk * (BM * SWZ), n0 + blk * SWZ, m0);
+        tma2d(&map_r, bar, dst + blk * (BM * SWZ), n0 + blk * SWZ, m0);
       }
     };
-    if (args.has_res && leader && static_cast<int>(blockIdx.x) < n_tiles_total) load_res(blockIdx.x);
+    if (args.has_res && leader && static_cast<int>(blockIdx.x) < n_tiles_total) load_res(blockIdx.x, 0);
     uint32_t tl = 0;
     for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
       const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
       const uint32_t acc = tl & 1;
+      TileIo io{su32(set_of(tl)), r, static_cast<int>(SLOT_BYTES), SWZ};
       bar_wait(&tfull[acc], (tl / 2) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (args.dbuf && args.has_res && leader && t + static_cast<int>(gridDim.x) < n_tiles_total) {
+        // next tile's residual into the other set (its last reader, tile tl-1, is done)
+        load_res(t + gridDim.x, tl + 1);
+      }
       if (args.n_out > 0) {
-        // the previous tile's TMA stores must have finished reading the slots
-        if (leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        // this set's previous TMA stores must have finished reading it: the
+        // latest tile's group may still run when the sets alternate
+        if (leader) {
+          if (args.dbuf) {
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          } else {
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          }
+        }
         epi_sync();
       }
-      if (args.has_res) bar_wait(rfull, tl & 1);
+      if (args.has_res) {
+        if (args.dbuf) {
+          bar_wait(&rfull[tl & 1], (tl >> 1) & 1);
+        } else {
+          bar_wait(&rfull[0], tl & 1);
+        }
+      }
       const int64_t m = static_cast<int64_t>(m0) + r;
       const uint32_t tbase = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
       if constexpr (SHAPE != kShapeGeneric) {
@@ -500,15 +592,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (leader) {
         if (args.n_out > 0) {
           for (int blk = 0; blk < BN / SWZ; ++blk) {
-            tma_store2d(&map_o0, slots + blk * (BM * SWZ), n0 + blk * SWZ, m0);
+            tma_store2d(&map_o0, set_of(tl) + blk * (BM * SWZ), n0 + blk * SWZ, m0);
             if (args.n_out > 1) {
-              tma_store2d(&map_o1, slots + SLOT_BYTES + blk * (BM * SWZ), n0 + blk * SWZ, m0);
+              tma_store2d(&map_o1, set_of(tl) + SLOT_BYTES + blk * (BM * SWZ), n0 + blk * SWZ, m0);
             }
           }
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
-        if (args.has_res && t + static_cast<int>(gridDim.x) < n_tiles_total) {
-          load_res(t + gridDim.x);
+        if (!args.dbuf && args.has_res && t + static_cast<int>(gridDim.x) < n_tiles_total) {
+          load_res(t + gridDim.x, tl + 1);
         }
       }
     }
@@ -560,6 +652,53 @@ CUtensorMap bmap(const void* base, int64_t rows, int64_t cols, int64_t stride, i
   return m;
 }
 
+using EncodeIm2col = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const int*, const int*,
+                                  cuuint32_t, cuuint32_t, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+EncodeIm2col im2col_encoder() {
+  static EncodeIm2col fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) !=
+            cudaSuccess || q != cudaDriverEntryPointSuccess) {
+      return static_cast<EncodeIm2col>(nullptr);
+    }
+    return reinterpret_cast<EncodeIm2col>(p);
+  }();
+  return fn;
+}
+
+// im2col map over NHWC int8 codes [N, H, W, ld]: boxes of 128 pixels x 128
+// channels, SWIZZLE_128B (the UMMA K-major layout); false when unsupported
+bool im2col_map(CUtensorMap* m, const TcConvSpec& sp) {
+  if (!im2col_encoder()) return false;
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(sp.ld), static_cast<cuuint64_t>(sp.W),
+                              static_cast<cuuint64_t>(sp.H), static_cast<cuuint64_t>(sp.Nimg)};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(sp.ld),
+                                 static_cast<cuuint64_t>(sp.ld) * sp.W,
+                                 static_cast<cuuint64_t>(sp.ld) * sp.W * sp.H};
+  // window-start range along each spatial dim: [-pad, size - 1 + pad - (k - 1)]
+  const int lower[2] = {-sp.pw, -sp.ph};
+  const int upper[2] = {sp.pw - (sp.KW - 1), sp.ph - (sp.KH - 1)};
+  const cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(sp.sw), static_cast<cuuint32_t>(sp.sh), 1};
+  return im2col_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(sp.x), dims,
+                          strides, lower, upper, BK, BM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// the im2col path: square windows with equal pads/strides (the corner and
+// offset arrays are then symmetric), whole 128-channel K blocks, and
+// bounding-box offsets inside the rank-4 encoding's [-128, 127]
+bool im2col_ok(const TcConvSpec& sp) {
+  static const bool off = std::getenv("QUANTC_NO_IM2COL") != nullptr;
+  return !off && sp.gather && sp.ld % BK == 0 && sp.KH == sp.KW && sp.ph == sp.pw &&
+         sp.sh == sp.sw && sp.sh <= 8 && sp.ph <= 127 && sp.KH - 1 - sp.ph <= 128 &&
+         sp.KH <= 65535;
+}
+
 int num_sms() {
   static int n = [] {
     int dev = 0, v = 148;
@@ -570,17 +709,36 @@ int num_sms() {
   return n;
 }
 
+// shared memory of one CTA: everything but the pipeline stages
+int smem_fixed(const TcArgs& a, int bn, int sets, bool shape) {
+  return 1024 + sets * (a.n_out + a.has_res) * BM * bn + (2 * MAX_STAGES + 6) * 8 + 16 +
+         static_cast<int>(sizeof(StageTables)) + 64 +
+         (a.gather == 1 ? a.K / 16 * static_cast<int>(sizeof(int2)) : 0) +
+         (shape ? ((a.N + bn - 1) / bn) * bn * 4 : 0);
+}
+
+// pipeline depth that fits next to `fixed` bytes (capped by what the K loop uses)
+int fit_stages(const TcArgs& a, int bn, int fixed) {
+  int stages = (SMEM_LIMIT - fixed) / (BM * BK + bn * BK);
+  const int nk = a.K / BK;
+  stages = stages > MAX_STAGES ? MAX_STAGES : stages;
+  return stages > nk + 1 ? nk + 1 : stages;
+}
+
+// double-buffered slot sets when they fit beside >= 2 pipeline stages
+bool dbuf_fits(const TcArgs& a, int bn, bool shape) {
+  static const bool off = std::getenv("QUANTC_NO_DBUF") != nullptr;
+  if (off || a.n_out + a.has_res == 0) return false;
+  return fit_stages(a, bn, smem_fixed(a, bn, 2, shape)) >= 2;
+}
+
 template <int BN, int SHAPE>
 void launch_tc(const CUtensorMap* maps, TcArgs a, cudaStream_t s) {
   constexpr int stage_bytes = BM * BK + BN * BK;
-  const int fixed = 1024 + (a.n_out + a.has_res) * BM * BN + (2 * MAX_STAGES + 6) * 8 + 16 +
-                    static_cast<int>(sizeof(StageTables)) + 64 +
-                    (a.gather ? a.K / 16 * static_cast<int>(sizeof(int2)) : 0) +
-                    (SHAPE != kShapeGeneric ? a.n_tiles * BN * 4 : 0);
-  int stages = (SMEM_LIMIT - fixed) / stage_bytes;
-  const int nk = a.K / BK;
-  stages = stages > MAX_STAGES ? MAX_STAGES : stages;
-  stages = stages > nk + 1 ? nk + 1 : stages;  // no deeper than the K loop needs
+  constexpr bool shape = SHAPE != kShapeGeneric;
+  a.dbuf = dbuf_fits(a, BN, shape) ? 1 : 0;
+  const int fixed = smem_fixed(a, BN, a.dbuf + 1, shape);
+  int stages = fit_stages(a, BN, fixed);
   if (stages < 2) stages = 2;
   a.stages = stages;
   const size_t smem = static_cast<size_t>(fixed) + static_cast<size_t>(stages) * stage_bytes;
@@ -626,7 +784,7 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
   a.M = static_cast<int>(sp.M);
   a.N = sp.O;
   a.K = sp.Kpad;
-  a.gather = sp.gather;
+  a.gather = sp.gather ? 1 : 0;
   a.n_out = sp.n_out;
   a.has_res = sp.res_ptr != nullptr ? 1 : 0;
   a.g = TcGeom{sp.x, sp.Nimg, sp.H, sp.W, sp.C, sp.ld, sp.KH, sp.KW, sp.sh, sp.sw,
@@ -646,12 +804,18 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
   // leave most SMs idle
   int BN = tc_conv_bn(sp.O);
   while (BN > 64 && 2 * a.m_tiles * ((sp.O + BN - 1) / BN) <= num_sms()) BN /= 2;
+  // a wide tile whose slot sets cannot be double-buffered: halve it when the
+  // narrower one can (per-tile store drains / residual loads then overlap)
+  if (BN == 256 && !dbuf_fits(a, 256, sp.prog.shape != 0) && dbuf_fits(a, 128, sp.prog.shape != 0)) {
+    BN = 128;
+  }
   const int swz = BN >= 128 ? 128 : 64;
   a.n_tiles = (sp.O + BN - 1) / BN;
   CUtensorMap maps[5];
   // A: direct 2-D map over the code rows (a valid dummy when gathering)
   maps[0] = bmap(sp.x, sp.gather ? BM : sp.M, sp.gather ? BK : sp.Ktrue, sp.gather ? BK : sp.lda,
                  BK, BM, 128);
+  if (im2col_ok(sp) && im2col_map(&maps[0], sp)) a.gather = 2;
   maps[1] = bmap(sp.w, sp.O, sp.Kpad, sp.Kpad, BK, BN, 128);
   for (int o = 0; o < 2; ++o) {
     maps[2 + o] = o < sp.n_out ? bmap(sp.out_ptr[o], sp.M, sp.out_cols[o], sp.out_ld[o], swz, BM, swz)
