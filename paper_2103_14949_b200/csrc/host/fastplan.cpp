@@ -53,6 +53,11 @@ struct FastPlan::Val {
   int hw = 1, cs = 0;
   int64_t ld = 0;
   bool zero_fill = false;
+  // space-to-depth layout of a tiny-channel graph input feeding a stride-2
+  // conv: pixel (h, w, c) of an [H, W, C] image lives at s2d pixel
+  // (h/2, w/2), channel ((h%2)*2 + w%2)*C + c, 16-byte rows
+  bool s2d = false;
+  int s2d_C = 0, s2d_H = 0, s2d_W = 0;
   int64_t bytes_ps() const {
     return (rows_ps / hw) * ld * (kind == 0 ? 1 : 4);
   }
@@ -85,6 +90,10 @@ struct FastPlan::Stage {
   int out_vals[2] = {-1, -1};
   int res_val = -1;
   double bias_absmax = 0.0;
+  // space-to-depth stem conv (see Val::s2d): original channels / kernel and
+  // the tap alignment shift
+  bool s2d = false;
+  int s2d_C = 0, s2d_KH = 0, s2d_KW = 0, s2d_dh = 0, s2d_dw = 0;
 };
 
 namespace {
@@ -180,6 +189,9 @@ struct Builder {
   int max_depth = 0;
   int* out_val = nullptr;
   int64_t* out_per_sample = nullptr;
+  // set by compile() for a graph-input stage: its step and image geometry
+  int input_step = -1;
+  int input_H = 0, input_W = 0;
 
   const Graph& g() const { return plan.graph(); }
   const Node& node(int step) const { return *plan.steps()[static_cast<size_t>(step)].node; }
@@ -247,6 +259,26 @@ struct Builder {
                             pd.b == 0 && C % 16 == 0;
         ld = direct ? C : r16(C);
         zero = ld != C;
+        // the RGB stem: a graph input quantized straight into a stride-2 KxK
+        // conv with <= 4 channels is stored space-to-depth, making the conv a
+        // stride-1 conv over 16-byte pixels (one gather chunk per tap)
+        if (input_step >= 0 && C <= 4 && st.a == 2 && st.b == 2 && ws[2] > 1 && ws[3] > 1 &&
+            consumers(input_step).size() == 1 && consumers(x).size() == 1 && rows_ps > 0 &&
+            !std::getenv("QUANTC_NO_S2D")) {
+          const int H2 = (input_H + 1) / 2, W2 = (input_W + 1) / 2;
+          const int64_t n0 = rows_ps / (static_cast<int64_t>(input_H) * input_W);
+          const int64_t keep_rows = rows_ps;
+          rows_ps = n0 * H2 * W2;
+          const int v = make_val(x, x, 0, 16, 1, 0, true);
+          rows_ps = keep_rows;
+          FastPlan::Val& val = *vals[static_cast<size_t>(v)];
+          val.s2d = true;
+          val.s2d_C = C;
+          val.s2d_H = input_H;
+          val.s2d_W = input_W;
+          op(kern::kPSqStore8, sq_slot(x), v);
+          return true;
+        }
         break;
       }
       case OpKind::kDense:
@@ -652,6 +684,11 @@ void FastPlan::compile() {
         }
         b.rows_ps = static_cast<int64_t>(st->n0) * st->HW;
         b.C = st->C;
+        if (shp.size() == 4) {
+          b.input_step = step;
+          b.input_H = static_cast<int>(shp[2]);
+          b.input_W = static_cast<int>(shp[3]);
+        }
         break;
       }
       case OpKind::kConv2d:
@@ -729,6 +766,31 @@ void FastPlan::compile() {
             st->ldk = st->C;
             st->Ktrue = st->taps * st->C;
           }
+          if (dv.s2d) {
+            // stride-2 KxK conv over the space-to-depth input: a stride-1
+            // ceil((K+d)/2)^2 conv, pad ceil(p/2), where d = 2*ceil(p/2) - p
+            // aligns original tap k = 2*ka + dy - d (fastplan weight_codes_s2d)
+            st->s2d = true;
+            st->s2d_C = dv.s2d_C;
+            st->s2d_KH = st->KH;
+            st->s2d_KW = st->KW;
+            const int ph2 = (st->ph + 1) / 2, pw2 = (st->pw + 1) / 2;
+            st->s2d_dh = 2 * ph2 - st->ph;
+            st->s2d_dw = 2 * pw2 - st->pw;
+            st->KH = (st->s2d_KH + st->s2d_dh + 1) / 2;
+            st->KW = (st->s2d_KW + st->s2d_dw + 1) / 2;
+            st->ph = ph2;
+            st->pw = pw2;
+            st->sh = st->sw = 1;
+            st->H = (dv.s2d_H + 1) / 2;
+            st->W = (dv.s2d_W + 1) / 2;
+            st->C = 4 * dv.s2d_C;
+            st->taps = st->KH * st->KW;
+            st->gather = true;
+            st->packed = false;
+            st->ldk = 16;
+            st->Ktrue = st->taps * 16;
+          }
           // the gather producer tracks tap validity in a 64-bit mask
           if (st->gather && st->taps > 63) fail("conv kernel with more than 63 taps");
           st->rows_out_ps = static_cast<int64_t>(st->n0) * st->OH * st->OW;
@@ -790,6 +852,7 @@ void FastPlan::compile() {
              ") outside the fused dataflow");
         continue;
     }
+    if (st->kind != Stage::kInput) b.input_step = -1;
     b.flat_hw = 1;
     b.flat_cs = 0;
     b.depth = 0;
@@ -1016,10 +1079,26 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
     ProgArgs pa{d_tabs + si, st.depth,
                 st.kind == Stage::kGemm && !std::getenv("QUANTC_NO_SHAPES") ? classify_shape(tabs[si], st.O) : 0};
     switch (st.kind) {
-      case Stage::kInput:
+      case Stage::kInput: {
+        const Val* sv = nullptr;
+        for (int vid : st.buf_vals) {
+          if (vals_[static_cast<size_t>(vid)]->s2d) sv = vals_[static_cast<size_t>(vid)].get();
+        }
+        if (sv) {
+          // compile guarantees the program is the single store into the s2d value
+          if (st.code.size() != 1 || st.code[0].op != kern::kPSqStore8) {
+            throw EvalError("fastplan: space-to-depth input stage with a compound program");
+          }
+          kern::stage_input_s2d(inputs.at(static_cast<size_t>(st.input_k)), batch * st.n0,
+                                sv->s2d_C, sv->s2d_H, sv->s2d_W, tabs[si].sq[st.code[0].a],
+                                static_cast<int8_t*>(arena_[static_cast<size_t>(st.buf_vals[0])].get()),
+                                S());
+          break;
+        }
         kern::stage_input(inputs.at(static_cast<size_t>(st.input_k)), batch * st.n0, st.C, st.HW,
                           pa, S());
         break;
+      }
       case Stage::kMaxpool: {
         const Val& v = *vals_[static_cast<size_t>(st.in_val)];
         kern::stage_maxpool(static_cast<const int8_t*>(arena_[static_cast<size_t>(st.in_val)].get()),
@@ -1046,9 +1125,16 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
         auto it = wcache_.find(ck);
         if (it == wcache_.end()) {
           auto codes = engine::device_alloc(static_cast<size_t>(st.O) * st.Kpad);
-          kern::weight_codes_v2(plan_.constant(st.w_const).f(), static_cast<int8_t*>(codes.get()),
-                                st.O, st.dense ? (st.taps > 1 ? dv.cs : dv.C) : st.C, st.taps,
-                                st.ldk, st.Kpad, wf, S());
+          if (st.s2d) {
+            kern::weight_codes_s2d(plan_.constant(st.w_const).f(), static_cast<int8_t*>(codes.get()),
+                                   st.O, st.s2d_C, st.s2d_KH, st.s2d_KW, st.KH, st.KW, st.s2d_dh,
+                                   st.s2d_dw, st.Kpad, wf, S());
+          } else {
+            kern::weight_codes_v2(plan_.constant(st.w_const).f(),
+                                  static_cast<int8_t*>(codes.get()), st.O,
+                                  st.dense ? (st.taps > 1 ? dv.cs : dv.C) : st.C, st.taps, st.ldk,
+                                  st.Kpad, wf, S());
+          }
           it = wcache_.emplace(ck, codes).first;
         }
         kern::TcConvSpec sp{};
@@ -1107,8 +1193,10 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
         if (prof) device::profile_gemm_begin();
         kern::tc_conv(sp, S());
         if (prof) {
-          device::profile_gemm_end(2.0 * static_cast<double>(sp.M) * st.O *
-                                   (st.dense ? st.Ktrue : st.C * st.KH * st.KW));
+          device::profile_gemm_end(
+              2.0 * static_cast<double>(sp.M) * st.O *
+              (st.dense ? st.Ktrue
+                        : (st.s2d ? st.s2d_C * st.s2d_KH * st.s2d_KW : st.C * st.KH * st.KW)));
         }
         device::counters().tcgen05_gemms++;
         break;

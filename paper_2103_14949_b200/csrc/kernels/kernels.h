@@ -144,6 +144,14 @@ int tc_conv_bn(int O);  // output-channel tile the kernel uses for O channels
 // KH*KW; a flattened dense is the taps = H*W case), fp32 sq (pow2 scale)
 void weight_codes_v2(const float* w, int8_t* codes, int O, int C, int taps, int ldk, int Kpad,
                      const FSq& p, cudaStream_t s);
+// graph input NCHW fp32 [N, C, H, W] -> space-to-depth int8 codes
+// [N, ceil(H/2), ceil(W/2), 16], channel ((h%2)*2 + w%2)*C + c (C <= 4)
+void stage_input_s2d(const float* x, int N, int C, int H, int W, const FSq& p, int8_t* out,
+                     cudaStream_t s);
+// weight codes [O][Kpad] of the space-to-depth form of a stride-2 KHxKW conv
+// (KH2 x KW2 taps of 16 channels; original tap = 2*ka + dy - dh, 2*kb + dx - dw)
+void weight_codes_s2d(const float* w, int8_t* codes, int O, int C, int KH, int KW, int KH2,
+                      int KW2, int dh, int dw, int Kpad, const FSq& p, cudaStream_t s);
 // graph input NCHW fp32 -> program over (m = n*H*W + hw, c)
 void stage_input(const float* x, int N, int C, int HW, const ProgArgs& prog, cudaStream_t s);
 // max_pool2d over NHWC codes (value = code * scale) -> program

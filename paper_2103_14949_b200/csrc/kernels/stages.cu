@@ -154,6 +154,67 @@ __global__ void weight_codes_v2_kernel(const float* __restrict__ w, int8_t* __re
   }
 }
 
+// graph input NCHW fp32 -> space-to-depth int8 codes (fastplan Val::s2d): one
+// thread per 2x2 pixel block, its 4*C codes (zero-padded to 16) as one store
+__global__ void input_s2d_kernel(const float* __restrict__ x, int N, int C, int H, int W, int H2,
+                                 int W2, FSq p, int8_t* __restrict__ out) {
+  const int64_t total = static_cast<int64_t>(N) * H2 * W2;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int w2 = static_cast<int>(i % W2);
+    const int64_t t = i / W2;
+    const int h2 = static_cast<int>(t % H2);
+    const int64_t n = t / H2;
+    uint32_t word[4] = {0, 0, 0, 0};
+    for (int c = 0; c < C; ++c) {
+      const float* plane = x + (n * C + c) * H * W;
+#pragma unroll
+      for (int dy = 0; dy < 2; ++dy) {
+        const int h = 2 * h2 + dy;
+#pragma unroll
+        for (int dx = 0; dx < 2; ++dx) {
+          const int w = 2 * w2 + dx;
+          if (h < H && w < W) {
+            const float q = __fsub_rn(fsq_code(plane[h * W + w], p), p.zp);
+            const int b = (dy * 2 + dx) * C + c;
+            word[b >> 2] |= static_cast<uint32_t>(static_cast<uint8_t>(static_cast<int8_t>(
+                                __float2int_rn(q))))
+                            << (8 * (b & 3));
+          }
+        }
+      }
+    }
+    *reinterpret_cast<int4*>(out + i * 16) =
+        make_int4(static_cast<int>(word[0]), static_cast<int>(word[1]), static_cast<int>(word[2]),
+                  static_cast<int>(word[3]));
+  }
+}
+
+// weight codes of the space-to-depth conv: k = tap*16 + ch, tap = ka*KW2 + kb,
+// ch = (dy*2 + dx)*C + c  <->  original tap (2*ka + dy - dh, 2*kb + dx - dw)
+__global__ void weight_codes_s2d_kernel(const float* __restrict__ w, int8_t* __restrict__ codes,
+                                        int O, int C, int KH, int KW, int KH2, int KW2, int dh,
+                                        int dw, int Kpad, FSq p) {
+  const int64_t total = static_cast<int64_t>(O) * Kpad;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(i % Kpad);
+    const int o = static_cast<int>(i / Kpad);
+    const int tap = k >> 4, ch = k & 15;
+    int8_t code = 0;
+    if (tap < KH2 * KW2 && ch < 4 * C) {
+      const int ka = tap / KW2, kb = tap - (tap / KW2) * KW2;
+      const int sub = ch / C, c = ch - sub * C;
+      const int kh = 2 * ka + (sub >> 1) - dh, kw = 2 * kb + (sub & 1) - dw;
+      if (kh >= 0 && kh < KH && kw >= 0 && kw < KW) {
+        const float v = w[((static_cast<int64_t>(o) * C + c) * KH + kh) * KW + kw];
+        code = static_cast<int8_t>(static_cast<int>(__fsub_rn(fsq_code(v, p), p.zp)));
+      }
+    }
+    codes[i] = code;
+  }
+}
+
 // one thread per output row: walks (kh, kw, c) with incremental counters and
 // emits the row as 16-byte stores
 __global__ void pack_im2col_kernel(const int8_t* __restrict__ x, int8_t* __restrict__ out, int N,
@@ -203,6 +264,24 @@ void pack_im2col(const int8_t* x, int8_t* out, int N, int H, int W, int C, int l
   pack_im2col_kernel<<<grid_for(total, 128, 148 * 32), 128, 0, s>>>(x, out, N, H, W, C, ld, KH, KW,
                                                                      sh, sw, ph, pw, OH, OW, Ktrue,
                                                                      Kpad);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+void stage_input_s2d(const float* x, int N, int C, int H, int W, const FSq& p, int8_t* out,
+                     cudaStream_t s) {
+  const int H2 = (H + 1) / 2, W2 = (W + 1) / 2;
+  const int64_t total = static_cast<int64_t>(N) * H2 * W2;
+  if (total <= 0) return;
+  input_s2d_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, N, C, H, W, H2, W2, p, out);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+void weight_codes_s2d(const float* w, int8_t* codes, int O, int C, int KH, int KW, int KH2,
+                      int KW2, int dh, int dw, int Kpad, const FSq& p, cudaStream_t s) {
+  const int64_t total = static_cast<int64_t>(O) * Kpad;
+  if (total <= 0) return;
+  weight_codes_s2d_kernel<<<grid_for(total, 256), 256, 0, s>>>(w, codes, O, C, KH, KW, KH2, KW2,
+                                                                dh, dw, Kpad, p);
   QC_CUDA_CHECK_LAUNCH();
 }
 
