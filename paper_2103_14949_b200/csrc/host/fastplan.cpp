@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -127,6 +128,8 @@ void optimise_tables(kern::StageTables& t, double v0) {
                                    std::fabs(static_cast<double>(f.hi_rn))) * 1.001);
         }
         if (!f.passthrough) b = code_absmax(f) * static_cast<double>(f.s);
+        // a passthrough sq without a live accumulator clamp is the identity
+        if (ins.op == kern::kPSq && f.passthrough && !f.has_acc) continue;
         const bool relu_next = pc + 1 < t.n_code && t.code[pc + 1].op == kern::kPRelu;
         if (ins.op == kern::kPSq && relu_next && !f.passthrough) {
           f.qmin = std::max(f.qmin, f.zp);
@@ -508,6 +511,7 @@ int classify_shape(const kern::StageTables& t, int O) {
         (t.buf[in.b].slot < 0 || t.buf[in.b].kind != 0)) {
       return 0;
     }
+    if (in.op == kern::kPStoreF32 && (t.buf[in.b].kind != 1 || t.buf[in.b].hw != 1)) return 0;
   }
   using V = std::vector<uint8_t>;
   if (ops == V{kern::kPSqStore8}) return 1;
@@ -517,6 +521,7 @@ int classify_shape(const kern::StageTables& t, int O) {
     return 3;
   }
   if (ops == V{kern::kPSq, kern::kPAdd, kern::kPSq, kern::kPSqStore8}) return 4;
+  if (ops == V{kern::kPSq, kern::kPAdd, kern::kPSq, kern::kPStoreF32}) return 5;
   return 0;
 }
 
@@ -524,6 +529,41 @@ int classify_shape(const kern::StageTables& t, int O) {
 bool exact_float(double v, float& out) {
   out = static_cast<float>(v);
   return static_cast<double>(out) == v && (v == 0.0 || std::fpclassify(out) == FP_NORMAL);
+}
+
+// rounding bounds of sq f: x clamped to the nearest floats inside
+// [qmin - 1/2, qmax + 1/2] rounds (half away) into [qmin, qmax]
+bool round_bounds(const kern::FSq& f, kern::EpiSq& q) {
+  q.lo = std::nextafter(f.qmin - 0.5f, std::numeric_limits<float>::infinity());
+  q.hi = std::nextafter(f.qmax + 0.5f, -std::numeric_limits<float>::infinity());
+  return std::fabs(f.qmin) < 65536.0f && std::fabs(f.qmax) < 65536.0f;
+}
+
+// sq f applied to a previous integer code R on grid prev_s (T-domain when
+// prev_T): x = fma(R, s_prev/s, off); k >= 1 needs no rounding (kEpiExact)
+bool epi_from_code(double prev_s, bool prev_T, const kern::FSq& f, kern::EpiSq& q) {
+  const double M = kern::kMagic;
+  const double k = prev_s / f.s;
+  if (!exact_float(k, q.k)) return false;
+  const bool nonneg = f.qmin >= 0.0f || prev_T;
+  q.flags = nonneg ? kern::kEpiNonneg : 0;
+  double off = 0.0;
+  if (k >= 1.0) {
+    // r * 2^d is already an integer: clamp in the output domain only
+    q.flags |= kern::kEpiExact;
+    if (nonneg) {
+      off = prev_T ? M - M * k : M;
+      q.lo = static_cast<float>(M + f.qmin);
+      q.hi = static_cast<float>(M + f.qmax);
+    } else {
+      q.lo = f.qmin;
+      q.hi = f.qmax;
+    }
+  } else {
+    off = prev_T ? -M * k : 0.0;
+    if (!round_bounds(f, q)) return false;
+  }
+  return exact_float(off, q.off);
 }
 
 // Fold the shape's sq chain into EpiConsts (fused.h).  Every factor is a
@@ -550,14 +590,13 @@ bool make_epi(const kern::StageTables& t, int shape, double sxw, kern::EpiConsts
       res = static_cast<int>(c[1].b);
       out0 = static_cast<int>(c[3].b);
       break;
+    case 5:
+      qs = {c[0].a, c[2].a};
+      res = static_cast<int>(c[1].b);
+      out0 = static_cast<int>(c[3].b);
+      break;
     default: return false;
   }
-  const double M = kern::kMagic;
-  auto round_bounds = [](const kern::FSq& f, kern::EpiSq& q) {
-    q.lo = std::nextafter(f.qmin - 0.5f, std::numeric_limits<float>::infinity());
-    q.hi = std::nextafter(f.qmax + 0.5f, -std::numeric_limits<float>::infinity());
-    return std::fabs(f.qmin) < 65536.0f && std::fabs(f.qmax) < 65536.0f;
-  };
   // sq0 on the conv output: x0 = fma(a, s_x*s_w / s0, bias / s0)
   const kern::FSq& f0 = t.sq[qs[0]];
   kern::EpiSq& q0 = e.q[0];
@@ -585,36 +624,54 @@ bool make_epi(const kern::StageTables& t, int shape, double sxw, kern::EpiConsts
     e.slot_res = t.buf[res].slot;
     next = 2;
   }
-  // the remaining sqs all read the previous rounded code R (a fork reads the same R)
-  const bool prev_T = prev_nonneg;
+  // the remaining sqs read the previous rounded code (a fork, shape 3, reads
+  // the same R1 twice)
   for (size_t i = next; i < qs.size(); ++i) {
-    const kern::FSq& f = t.sq[qs[i]];
-    kern::EpiSq& q = e.q[i];
-    const double k = prev_s / f.s;
-    if (!exact_float(k, q.k)) return false;
-    const bool nonneg = f.qmin >= 0.0f || prev_T;
-    q.flags = nonneg ? kEpiNonneg : 0;
-    double off = 0.0;
-    if (k >= 1.0) {
-      // r * 2^d is already an integer: clamp in the output domain only
-      q.flags |= kEpiExact;
-      if (nonneg) {
-        off = prev_T ? M - M * k : M;
-        q.lo = static_cast<float>(M + f.qmin);
-        q.hi = static_cast<float>(M + f.qmax);
-      } else {
-        off = 0.0;
-        q.lo = f.qmin;
-        q.hi = f.qmax;
-      }
-    } else {
-      off = prev_T ? -M * k : 0.0;
-      if (!round_bounds(f, q)) return false;
-    }
-    if (!exact_float(off, q.off)) return false;
+    if (!epi_from_code(prev_s, prev_nonneg, t.sq[qs[i]], e.q[i])) return false;
   }
-  e.slot_out[0] = out0 >= 0 ? t.buf[out0].slot : -1;
+  if (shape == 5) {
+    // fp32 output value v = r * s of the last sq (T-domain: fma(R, s, -M*s))
+    const double s_last = prev_s;
+    if (!exact_float(s_last, e.f32_s) ||
+        !exact_float(prev_nonneg ? -kern::kMagic * s_last : 0.0, e.f32_off)) {
+      return false;
+    }
+    const kern::ProgBuf& fb = t.buf[out0];
+    if (fb.kind != 1 || fb.hw != 1) return false;
+    e.f32_ptr = static_cast<float*>(fb.ptr);
+    e.f32_ld = fb.ld;
+  }
+  e.slot_out[0] = out0 >= 0 && shape != 5 ? t.buf[out0].slot : -1;
   e.slot_out[1] = out1 >= 0 ? t.buf[out1].slot : -1;
+  return true;
+}
+
+// A max-pool whose program only stores codes of the pooled value ([sq_store8]
+// or the fork [push, sq_store8, pop, sq_store8]) into plain NHWC rows runs the
+// stores-only kernel; every store folds to code -> code constants.
+bool pool_stores(const kern::StageTables& t, double s_in, kern::PoolStores& ps) {
+  std::memset(&ps, 0, sizeof(ps));
+  std::vector<int> stores;
+  if (t.n_code == 1 && t.code[0].op == kern::kPSqStore8) {
+    stores = {0};
+  } else if (t.n_code == 4 && t.code[0].op == kern::kPPush && t.code[1].op == kern::kPSqStore8 &&
+             t.code[2].op == kern::kPPop && t.code[3].op == kern::kPSqStore8) {
+    stores = {1, 3};
+  } else {
+    return false;
+  }
+  for (size_t i = 0; i < stores.size(); ++i) {
+    const kern::ProgInstr& in = t.code[stores[i]];
+    const kern::FSq& f = t.sq[in.a];
+    const kern::ProgBuf& b = t.buf[in.b];
+    if (f.zp != 0.0f || f.has_acc || f.passthrough || b.kind != 0 || b.hw != 1 || b.ld % 16 != 0) {
+      return false;
+    }
+    if (!epi_from_code(s_in, false, f, ps.q[i])) return false;
+    ps.out[i] = static_cast<int8_t*>(b.ptr);
+    ps.ld[i] = b.ld;
+  }
+  ps.n_out = static_cast<int>(stores.size());
   return true;
 }
 
@@ -934,6 +991,18 @@ void FastPlan::compile() {
     stages_.push_back(std::move(st));
   }
   if (ok_ && out_val_ < 0) fail("graph output not reached");
+  if (std::getenv("QUANTC_DUMP_PLAN")) {
+    static const char* kind[] = {"input", "gemm", "maxpool", "gap"};
+    static const char* opn[] = {"end", "sq", "sq_store8", "relu", "clip", "add", "store_f32",
+                                "push", "pop"};
+    for (const auto& st : stages_) {
+      std::fprintf(stderr, "stage %-7s step %4d C %4d O %4d K %4dx%-2d s%d gather %d s2d %d n_out %d res %d:",
+                   kind[st->kind], st->step, st->C, st->O, st->KH, st->KW, st->sh,
+                   st->gather ? 1 : 0, st->s2d ? 1 : 0, st->n_out, st->res_val >= 0 ? 1 : 0);
+      for (const ProgInstr& in : st->code) std::fprintf(stderr, " %s", opn[in.op]);
+      std::fprintf(stderr, "\n");
+    }
+  }
   if (ok_ && sq_steps_.size() > 65535) fail("too many simulated_quantize nodes");
 }
 
@@ -1101,6 +1170,14 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
       }
       case Stage::kMaxpool: {
         const Val& v = *vals_[static_cast<size_t>(st.in_val)];
+        kern::PoolStores ps;
+        if (st.C % 16 == 0 && v.ld % 16 == 0 && st.ph < st.pkh && st.pw < st.pkw &&
+            pool_stores(tabs[si], scale_by_step.at(v.sq_step), ps)) {
+          kern::stage_maxpool_stores(static_cast<const int8_t*>(arena_[static_cast<size_t>(st.in_val)].get()),
+                                     static_cast<int>(v.ld), batch * st.n0, st.C, st.H, st.W, st.OH,
+                                     st.OW, st.pkh, st.pkw, st.sh, st.sw, st.ph, st.pw, ps, S());
+          break;
+        }
         kern::stage_maxpool(static_cast<const int8_t*>(arena_[static_cast<size_t>(st.in_val)].get()),
                             static_cast<int>(v.ld), scale_by_step.at(v.sq_step), batch * st.n0,
                             st.C, st.H, st.W, st.OH, st.OW, st.pkh, st.pkw, st.sh, st.sw, st.ph,
@@ -1175,6 +1252,20 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
                    static_cast<double>(wf.s);
         sp.prog = pa;
         if (pa.shape != 0 && !make_epi(tabs[si], pa.shape, sp.scale, sp.epi)) sp.prog.shape = 0;
+        if (std::getenv("QUANTC_DUMP_PLAN")) {
+          std::fprintf(stderr, "run stage %zu step %d shape %d -> %d ops", si, st.step, pa.shape,
+                       sp.prog.shape);
+          for (int pc = 0; pc < tabs[si].n_code; ++pc) {
+            const kern::ProgInstr& in = tabs[si].code[pc];
+            std::fprintf(stderr, " %d", in.op);
+            if (in.op == kern::kPSq || in.op == kern::kPSqStore8) {
+              const FSq& f = tabs[si].sq[in.a];
+              std::fprintf(stderr, "[zp%g acc%d pt%d q%g..%g s%g]", f.zp, f.has_acc, f.passthrough,
+                           f.qmin, f.qmax, f.s);
+            }
+          }
+          std::fprintf(stderr, "\n");
+        }
         sp.acc_bound = acc_bound[si];
         sp.n_out = st.n_out;
         for (int o = 0; o < st.n_out; ++o) {

@@ -528,7 +528,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                                  e.inv0);
               }
             }
-            run_shape_epi<SHAPE>(x, e, io, c0);
+            run_shape_epi<SHAPE>(x, e, io, c0, m, n, m < args.M);
           }
         }
       } else
@@ -768,6 +768,9 @@ void launch_bn(const CUtensorMap* maps, const TcArgs& a, cudaStream_t s) {
       break;
     case kShapeAdd:
       launch_tc<BN, kShapeAdd>(maps, a, s);
+      break;
+    case kShapeAddF32:
+      launch_tc<BN, kShapeAddF32>(maps, a, s);
       break;
     default:
       launch_tc<BN, kShapeGeneric>(maps, a, s);

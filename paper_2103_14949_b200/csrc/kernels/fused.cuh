@@ -156,7 +156,7 @@ __device__ __forceinline__ void store_codes(const ProgBuf& b, int64_t m, int n0,
     return;
   }
   int8_t* dst = static_cast<int8_t*>(b.ptr) + buf_off(b, m, n0);
-  if (nvalid == W && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+  if (W % 16 == 0 && nvalid == W && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
 #pragma unroll
     for (int i = 0; i < W / 16; ++i) {
       const int o = 16 * i;
@@ -189,7 +189,7 @@ __device__ __forceinline__ void load_values(const ProgBuf& b, int64_t m, int n0,
   if (b.kind == 0) {
     const int8_t* src = static_cast<const int8_t*>(b.ptr) + buf_off(b, m, n0);
     const float sc = b.scale;
-    if (nvalid == W && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+    if (W % 16 == 0 && nvalid == W && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
 #pragma unroll
       for (int i = 0; i < W / 16; ++i) {
         const int4 raw = *reinterpret_cast<const int4*>(src + 16 * i);
@@ -217,8 +217,9 @@ __device__ __forceinline__ void load_values(const ProgBuf& b, int64_t m, int n0,
 //   2: SQ, SQ_STORE8                          (conv -> sq [-> relu] -> sq -> codes)
 //   3: SQ, ADD, SQ, PUSH, SQ_STORE8, POP, SQ_STORE8   (residual block end)
 //   4: SQ, ADD, SQ, SQ_STORE8
+//   5: SQ, ADD, SQ, STORE_F32                  (residual end -> fp32 for a pool)
 enum : int { kShapeGeneric = 0, kShapeStore = 1, kShapeSqStore = 2, kShapeAddFork = 3,
-             kShapeAdd = 4 };
+             kShapeAdd = 4, kShapeAddF32 = 5 };
 
 // ---- straight-line shape epilogues (no conversion-pipe instructions) -------------
 // Host preconditions (fastplan classify_shape / make_epi): every sq of the
@@ -250,8 +251,7 @@ __device__ __forceinline__ void epi_next(const float (&R)[16], float (&y)[16], c
 }
 
 // 16 rounded codes -> 16 int8 bytes (low byte of the T-domain bits)
-__device__ __forceinline__ void epi_store(float (&R)[16], const EpiSq& q, const TileIo& io,
-                                          int slot, int cl) {
+__device__ __forceinline__ int4 epi_pack(float (&R)[16], const EpiSq& q) {
   if (!(q.flags & kEpiNonneg)) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) R[j] = __fadd_rn(R[j], kMagic);
@@ -264,14 +264,30 @@ __device__ __forceinline__ void epi_store(float (&R)[16], const EpiSq& q, const 
         __byte_perm(__float_as_uint(R[4 * i + 2]), __float_as_uint(R[4 * i + 3]), 0x0040);
     w[i] = __byte_perm(lo, hi, 0x5410);
   }
-  sts128(tile_addr(io, slot, cl), make_int4(static_cast<int>(w[0]), static_cast<int>(w[1]),
-                                            static_cast<int>(w[2]), static_cast<int>(w[3])));
+  return make_int4(static_cast<int>(w[0]), static_cast<int>(w[1]), static_cast<int>(w[2]),
+                   static_cast<int>(w[3]));
+}
+
+__device__ __forceinline__ void epi_store(float (&R)[16], const EpiSq& q, const TileIo& io,
+                                          int slot, int cl) {
+  sts128(tile_addr(io, slot, cl), epi_pack(R, q));
+}
+
+// 16 int8 codes (4 packed words) -> floats, without the conversion pipe
+__device__ __forceinline__ void codes_to_floats(const uint32_t (&w)[4], float (&r)[16]) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const float C = __uint_as_float(__byte_perm(w[j >> 2] ^ 0x80808080u, 0x4B000000u, 0x7650u + (j & 3)));
+    r[j] = __fsub_rn(C, 8388736.0f);  // 2^23 + 128
+  }
 }
 
 // x[16] = conv output scaled into sq0's grid (x0 = v / s0); runs the shape
+// (m, n): the element coordinates of x[0] (shape 5 stores to global rows)
 template <int SHAPE>
 __device__ __forceinline__ void run_shape_epi(float (&x)[16], const EpiConsts& e,
-                                              const TileIo& io, int cl) {
+                                              const TileIo& io, int cl, int64_t m, int n,
+                                              bool row_ok) {
   epi_round(x, e.q[0]);
   if (SHAPE == kShapeStore) {
     epi_store(x, e.q[0], io, e.slot_out[0], cl);
@@ -299,6 +315,19 @@ __device__ __forceinline__ void run_shape_epi(float (&x)[16], const EpiConsts& e
     x[j] = __fmaf_rn(x[j], e.q[1].k, __fmaf_rn(C, e.ka, e.ka_off));
   }
   epi_round(x, e.q[1]);
+  if (SHAPE == kShapeAddF32) {
+    if (row_ok) {
+      float4* dst = reinterpret_cast<float4*>(e.f32_ptr + m * e.f32_ld + n);
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) {
+        dst[j / 4] = make_float4(__fmaf_rn(x[j], e.f32_s, e.f32_off),
+                                 __fmaf_rn(x[j + 1], e.f32_s, e.f32_off),
+                                 __fmaf_rn(x[j + 2], e.f32_s, e.f32_off),
+                                 __fmaf_rn(x[j + 3], e.f32_s, e.f32_off));
+      }
+    }
+    return;
+  }
   epi_next(x, y, e.q[2]);
   epi_store(y, e.q[2], io, e.slot_out[0], cl);
   if (SHAPE == kShapeAddFork) {

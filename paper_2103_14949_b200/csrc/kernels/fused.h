@@ -138,6 +138,11 @@ struct EpiConsts {
   int32_t slot_out[2];
   int32_t slot_res;
   int32_t pad_;
+  // shape 5: the fp32 value v = fma(R, f32_s, f32_off) of the last sq, stored
+  // to plain rows f32_ptr[m * f32_ld + n]
+  float f32_s, f32_off;
+  float* f32_ptr;
+  int64_t f32_ld;
 };
 
 // kernels receive the stage's table block in global memory

@@ -166,6 +166,18 @@ void stage_gap(const float* x, int64_t ld, int N, int C, int HW, const ProgArgs&
 void pack_im2col(const int8_t* x, int8_t* out, int N, int H, int W, int C, int ld, int KH, int KW,
                  int sh, int sw, int ph, int pw, int OH, int OW, int Ktrue, int Kpad,
                  cudaStream_t s);
+// max-pool whose program is only code stores (<= 2, e.g. a fork to two
+// convs): per store the host-folded EpiSq of code -> code and a plain NHWC
+// destination (fused.h EpiSq)
+struct PoolStores {
+  EpiSq q[2];
+  int8_t* out[2];
+  int64_t ld[2];
+  int n_out;
+};
+void stage_maxpool_stores(const int8_t* x, int ld, int N, int C, int H, int W, int OH, int OW,
+                          int kh, int kw, int sh, int sw, int ph, int pw, const PoolStores& e,
+                          cudaStream_t s);
 // generic elementwise stage over an (M, C) space: v = value(src) -> program
 void stage_ew(const ProgBuf& src, int64_t M, int C, const ProgArgs& prog, cudaStream_t s);
 

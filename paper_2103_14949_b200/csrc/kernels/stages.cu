@@ -88,34 +88,63 @@ __global__ void maxpool_codes_kernel(const int8_t* __restrict__ x, int ld, float
   }
 }
 
-// one thread per (n, c): sequential double sum in h*W+w order
+// one thread per (n, c): sequential double sum in h*W+w order (coalesced
+// across c), then the stage program on that one value
 __global__ void gap_rows_kernel(const float* __restrict__ x, int64_t ld, int N, int C, int HW,
                                 ProgArgs prog) {
   __shared__ StageTables T;
   load_tables(&T, prog.tables);
   __syncthreads();
-  const int groups = (C + 15) / 16;
-  const int64_t total = static_cast<int64_t>(N) * groups;
+  const int64_t total = static_cast<int64_t>(N) * C;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % C);
+    const int64_t n = i / C;
+    const float* col = x + n * HW * ld + c;
+    double acc = 0.0;
+    for (int hw = 0; hw < HW; ++hw) acc = __dadd_rn(acc, static_cast<double>(__ldg(col + hw * ld)));
+    float v[1] = {__double2float_rn(__ddiv_rn(acc, static_cast<double>(HW)))};
+    run_prog<1, 3>(v, n, c, 1, T);
+  }
+}
+
+// max-pool -> code stores: signed byte max over the window, then each store's
+// folded sq (codes are exact floats; no conversion-pipe instructions)
+template <int NOUT>
+__global__ void maxpool_stores_kernel(const int8_t* __restrict__ x, int ld, int N, int C, int H,
+                                      int W, int OH, int OW, int kh, int kw, int sh, int sw, int ph,
+                                      int pw, PoolStores e) {
+  const int groups = C / 16;
+  const int64_t total = static_cast<int64_t>(N) * OH * OW * groups;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int grp = static_cast<int>(i % groups);
-    const int64_t n = i / groups;
-    const int c0 = grp * 16;
-    const int nvalid = C - c0 < 16 ? C - c0 : 16;
-    double acc[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) acc[j] = 0.0;
-    for (int hw = 0; hw < HW; ++hw) {
-      const float* row = x + (n * HW + hw) * ld + c0;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        if (j < nvalid) acc[j] = __dadd_rn(acc[j], static_cast<double>(row[j]));
+    const int64_t m = i / groups;
+    const int ow = static_cast<int>(m % OW);
+    const int oh = static_cast<int>((m / OW) % OH);
+    const int64_t n = m / (static_cast<int64_t>(OW) * OH);
+    uint32_t best[4] = {0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u};
+    for (int a = 0; a < kh; ++a) {
+      const int ih = oh * sh - ph + a;
+      if (ih < 0 || ih >= H) continue;
+      for (int b = 0; b < kw; ++b) {
+        const int iw = ow * sw - pw + b;
+        if (iw < 0 || iw >= W) continue;
+        const int4 raw = __ldg(reinterpret_cast<const int4*>(x + ((n * H + ih) * W + iw) * ld + grp * 16));
+        best[0] = __vmaxs4(best[0], static_cast<uint32_t>(raw.x));
+        best[1] = __vmaxs4(best[1], static_cast<uint32_t>(raw.y));
+        best[2] = __vmaxs4(best[2], static_cast<uint32_t>(raw.z));
+        best[3] = __vmaxs4(best[3], static_cast<uint32_t>(raw.w));
       }
     }
-    float v[16];
+    float r[16];
+    codes_to_floats(best, r);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = __double2float_rn(__ddiv_rn(acc[j], static_cast<double>(HW)));
-    run_prog<16, 3>(v, n, c0, nvalid, T);
+    for (int o = 0; o < NOUT; ++o) {
+      float y[16];
+      epi_next(r, y, e.q[o]);
+      *reinterpret_cast<int4*>(e.out[o] + m * e.ld[o] + grp * 16) = epi_pack(y, e.q[o]);
+    }
   }
 }
 
@@ -304,9 +333,24 @@ void stage_maxpool(const int8_t* x, int ld, float scale, int N, int C, int H, in
 
 void stage_gap(const float* x, int64_t ld, int N, int C, int HW, const ProgArgs& prog,
                cudaStream_t s) {
-  const int64_t total = static_cast<int64_t>(N) * ((C + 15) / 16);
+  const int64_t total = static_cast<int64_t>(N) * C;
   if (total <= 0) return;
-  gap_rows_kernel<<<grid_for(total, 128), 128, 0, s>>>(x, ld, N, C, HW, prog);
+  gap_rows_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, ld, N, C, HW, prog);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+void stage_maxpool_stores(const int8_t* x, int ld, int N, int C, int H, int W, int OH, int OW,
+                          int kh, int kw, int sh, int sw, int ph, int pw, const PoolStores& e,
+                          cudaStream_t s) {
+  const int64_t total = static_cast<int64_t>(N) * OH * OW * (C / 16);
+  if (total <= 0) return;
+  if (e.n_out == 2) {
+    maxpool_stores_kernel<2><<<grid_for(total, 256), 256, 0, s>>>(x, ld, N, C, H, W, OH, OW, kh,
+                                                                  kw, sh, sw, ph, pw, e);
+  } else {
+    maxpool_stores_kernel<1><<<grid_for(total, 256), 256, 0, s>>>(x, ld, N, C, H, W, OH, OW, kh,
+                                                                  kw, sh, sw, ph, pw, e);
+  }
   QC_CUDA_CHECK_LAUNCH();
 }
 
