@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1077,6 +1078,11 @@ void FastPlan::ensure_arena(int batch) {
 
 void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
                        const SimBinding* binding, int64_t* d_preds, float* d_scores) {
+  static const bool hprof = std::getenv("QUANTC_HOST_PROF") != nullptr;
+  const auto t_start = std::chrono::steady_clock::now();
+  auto us_since = [&](std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+  };
   ensure_arena(batch);
   // weight codes are cached per (stage, weight sq parameters); a long search
   // visits many weight bit-widths, so keep roughly the last few bindings
@@ -1139,9 +1145,11 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
     }
     optimise_tables(t, v0);
   }
+  const double t_tables = hprof ? us_since(t_start) : 0.0;
   ok_cuda(cudaMemcpyAsync(d_tables_.get(), tabs.data(), tabs.size() * sizeof(kern::StageTables),
                           cudaMemcpyHostToDevice, S()));
   const auto* d_tabs = static_cast<const kern::StageTables*>(d_tables_.get());
+  const double t_upload = hprof ? us_since(t_start) : 0.0;
 
   for (size_t si = 0; si < stages_.size(); ++si) {
     const Stage& st = *stages_[si];
@@ -1297,6 +1305,10 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
   device::counters().fused_batches++;
   const float* out = static_cast<const float*>(arena_[static_cast<size_t>(out_val_)].get());
   kern::argmax_rows(out, batch, out_per_sample_, d_preds, S());
+  if (hprof) {
+    std::fprintf(stderr, "predict host us: tables %.1f upload %.1f launches %.1f total %.1f\n",
+                 t_tables, t_upload - t_tables, us_since(t_start) - t_upload, us_since(t_start));
+  }
   if (d_scores) {
     ok_cuda(cudaMemcpyAsync(d_scores, out, static_cast<size_t>(batch) * out_per_sample_ * 4,
                             cudaMemcpyDeviceToDevice, S()));

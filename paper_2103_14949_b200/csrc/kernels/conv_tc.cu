@@ -32,6 +32,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <mutex>
+#include <unordered_map>
 #include <stdexcept>
 
 #include "fused.cuh"
@@ -634,8 +635,8 @@ EncodeTiled encoder() {
 }
 
 // 2-D byte map: rows x cols, row stride `stride` bytes, box {box_cols, box_rows}
-CUtensorMap bmap(const void* base, int64_t rows, int64_t cols, int64_t stride, int box_cols,
-                 int box_rows, int swz) {
+CUtensorMap encode_bmap(const void* base, int64_t rows, int64_t cols, int64_t stride, int box_cols,
+                        int box_rows, int swz) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(stride)};
@@ -650,6 +651,33 @@ CUtensorMap bmap(const void* base, int64_t rows, int64_t cols, int64_t stride, i
     throw std::runtime_error("cuTensorMapEncodeTiled failed (conv_tc)");
   }
   return m;
+}
+
+// Encoded maps are cached by their encode inputs: a plan re-runs the same
+// layers on the same buffers every step, and encoding costs ~1 us each.
+struct MapKey {
+  const void* base;
+  int64_t a, b, c, d;
+  int e, f, g, kind;
+  bool operator==(const MapKey& o) const {
+    return base == o.base && a == o.a && b == o.b && c == o.c && d == o.d && e == o.e &&
+           f == o.f && g == o.g && kind == o.kind;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    size_t h = std::hash<const void*>()(k.base);
+    for (int64_t v : {k.a, k.b, k.c, k.d, static_cast<int64_t>(k.e), static_cast<int64_t>(k.f),
+                      static_cast<int64_t>(k.g), static_cast<int64_t>(k.kind)}) {
+      h = h * 1000003u ^ std::hash<int64_t>()(v);
+    }
+    return h;
+  }
+};
+std::mutex g_map_mu;
+std::unordered_map<MapKey, CUtensorMap, MapKeyHash>& map_cache() {
+  static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> c;
+  return c;
 }
 
 using EncodeIm2col = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -674,6 +702,16 @@ EncodeIm2col im2col_encoder() {
 // channels, SWIZZLE_128B (the UMMA K-major layout); false when unsupported
 bool im2col_map(CUtensorMap* m, const TcConvSpec& sp) {
   if (!im2col_encoder()) return false;
+  const MapKey key{sp.x, sp.ld, sp.W, sp.H, sp.Nimg,
+                   sp.KH * 4096 + sp.KW, sp.ph * 4096 + sp.pw, sp.sh * 4096 + sp.sw, 1};
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    auto it = map_cache().find(key);
+    if (it != map_cache().end()) {
+      *m = it->second;
+      return true;
+    }
+  }
   const cuuint64_t dims[4] = {static_cast<cuuint64_t>(sp.ld), static_cast<cuuint64_t>(sp.W),
                               static_cast<cuuint64_t>(sp.H), static_cast<cuuint64_t>(sp.Nimg)};
   const cuuint64_t strides[3] = {static_cast<cuuint64_t>(sp.ld),
@@ -683,10 +721,16 @@ bool im2col_map(CUtensorMap* m, const TcConvSpec& sp) {
   const int lower[2] = {-sp.pw, -sp.ph};
   const int upper[2] = {sp.pw - (sp.KW - 1), sp.ph - (sp.KH - 1)};
   const cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(sp.sw), static_cast<cuuint32_t>(sp.sh), 1};
-  return im2col_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(sp.x), dims,
-                          strides, lower, upper, BK, BM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  if (im2col_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(sp.x), dims,
+                       strides, lower, upper, BK, BM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+    return false;
+  }
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  if (map_cache().size() > 8192) map_cache().clear();
+  map_cache().emplace(key, *m);
+  return true;
 }
 
 // the im2col path: square windows with equal pads/strides (the corner and
@@ -697,6 +741,19 @@ bool im2col_ok(const TcConvSpec& sp) {
   return !off && sp.gather && sp.ld % BK == 0 && sp.KH == sp.KW && sp.ph == sp.pw &&
          sp.sh == sp.sw && sp.sh <= 8 && sp.ph <= 127 && sp.KH - 1 - sp.ph <= 128 &&
          sp.KH <= 65535;
+}
+
+CUtensorMap bmap(const void* base, int64_t rows, int64_t cols, int64_t stride, int box_cols,
+                 int box_rows, int swz) {
+  const MapKey k{base, rows, cols, stride, 0, box_cols, box_rows, swz, 0};
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  auto& c = map_cache();
+  auto it = c.find(k);
+  if (it != c.end()) return it->second;
+  if (c.size() > 8192) c.clear();  // buffers come and go over a long search
+  const CUtensorMap m = encode_bmap(base, rows, cols, stride, box_cols, box_rows, swz);
+  c.emplace(k, m);
+  return m;
 }
 
 int num_sms() {
