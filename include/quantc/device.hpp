@@ -53,9 +53,12 @@ Counters& counters();
 void profile_enable(bool on);
 bool profile_enabled();
 void profile_gemm_begin();
-void profile_gemm_end(double ops);
+// ops: algorithmic int8 ops (2*M*N*K_true); bytes: algorithmic HBM bytes of
+// the launch (each operand / result touched once)
+void profile_gemm_end(double ops, double bytes = 0.0);
 // drains recorded events: total GEMM ms, launches, algorithmic ops
-void profile_read(double* gemm_ms, int64_t* gemm_launches, double* gemm_ops);
+void profile_read(double* gemm_ms, int64_t* gemm_launches, double* gemm_ops,
+                  double* gemm_bytes = nullptr);
 
 }  // namespace device
 

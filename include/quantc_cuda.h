@@ -75,7 +75,8 @@ int qcu_set_engine_mode(int mode);
 void* qcu_engine_stream(void);
 /* per-GEMM CUDA-event profiling of the engine's tcgen05 launches */
 int qcu_profile_enable(int on);
-int qcu_profile_read(double* gemm_ms, int64_t* gemm_launches, double* gemm_ops);
+int qcu_profile_read(double* gemm_ms, int64_t* gemm_launches, double* gemm_ops,
+                     double* gemm_bytes);
 /* CandidateEvaluator::agreement_counts (B200 extension): per candidate, the
  * number of local calibration samples whose top-1 equals the fp32 reference;
  * the multi-GPU driver all-reduces these (loss = 1 - sum / N_total). */

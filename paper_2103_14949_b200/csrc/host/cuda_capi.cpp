@@ -182,8 +182,9 @@ int qcu_profile_enable(int on) {
   return wrap([&] { device::profile_enable(on != 0); });
 }
 
-int qcu_profile_read(double* gemm_ms, int64_t* gemm_launches, double* gemm_ops) {
-  return wrap([&] { device::profile_read(gemm_ms, gemm_launches, gemm_ops); });
+int qcu_profile_read(double* gemm_ms, int64_t* gemm_launches, double* gemm_ops,
+                     double* gemm_bytes) {
+  return wrap([&] { device::profile_read(gemm_ms, gemm_launches, gemm_ops, gemm_bytes); });
 }
 
 int qcu_counters(int64_t* steps, int64_t* tcgen05_gemms, int64_t* f64_convs,

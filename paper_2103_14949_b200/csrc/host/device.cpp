@@ -97,6 +97,7 @@ struct Profile {
   bool on = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
   std::vector<double> ops;
+  std::vector<double> bytes;
   std::vector<cudaEvent_t> pool;
   cudaEvent_t take() {
     if (!pool.empty()) {
@@ -125,29 +126,34 @@ void profile_gemm_begin() {
   p.events.push_back({a, b});
 }
 
-void profile_gemm_end(double ops) {
+void profile_gemm_end(double ops, double bytes) {
   Profile& p = prof();
   cudaEventRecord(p.events.back().second, ctx().stream);
   p.ops.push_back(ops);
+  p.bytes.push_back(bytes);
 }
 
-void profile_read(double* gemm_ms, int64_t* gemm_launches, double* gemm_ops) {
+void profile_read(double* gemm_ms, int64_t* gemm_launches, double* gemm_ops,
+                  double* gemm_bytes) {
   Profile& p = prof();
   synchronize();
-  double ms = 0.0, ops = 0.0;
+  double ms = 0.0, ops = 0.0, bytes = 0.0;
   for (size_t i = 0; i < p.events.size(); ++i) {
     float t = 0.0f;
     cudaEventElapsedTime(&t, p.events[i].first, p.events[i].second);
     ms += t;
     ops += p.ops[i];
+    bytes += p.bytes[i];
     p.pool.push_back(p.events[i].first);
     p.pool.push_back(p.events[i].second);
   }
   if (gemm_ms) *gemm_ms = ms;
   if (gemm_launches) *gemm_launches = static_cast<int64_t>(p.events.size());
   if (gemm_ops) *gemm_ops = ops;
+  if (gemm_bytes) *gemm_bytes = bytes;
   p.events.clear();
   p.ops.clear();
+  p.bytes.clear();
 }
 
 }  // namespace quantc::device

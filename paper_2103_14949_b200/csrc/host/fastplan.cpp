@@ -542,7 +542,8 @@ bool round_bounds(const kern::FSq& f, kern::EpiSq& q) {
 
 // sq f applied to a previous integer code R on grid prev_s (T-domain when
 // prev_T): x = fma(R, s_prev/s, off); k >= 1 needs no rounding (kEpiExact)
-bool epi_from_code(double prev_s, bool prev_T, const kern::FSq& f, kern::EpiSq& q) {
+bool epi_from_code(double prev_s, bool prev_T, const kern::FSq& f, kern::EpiSq& q,
+                   double in_lo, double in_hi) {
   const double M = kern::kMagic;
   const double k = prev_s / f.s;
   if (!exact_float(k, q.k)) return false;
@@ -560,6 +561,8 @@ bool epi_from_code(double prev_s, bool prev_T, const kern::FSq& f, kern::EpiSq& 
       q.lo = f.qmin;
       q.hi = f.qmax;
     }
+    // the input codes span [in_lo, in_hi]: scaled, they may already fit
+    if (k * in_lo >= f.qmin && k * in_hi <= f.qmax) q.flags |= kern::kEpiNoClamp;
   } else {
     off = prev_T ? -M * k : 0.0;
     if (!round_bounds(f, q)) return false;
@@ -628,7 +631,10 @@ bool make_epi(const kern::StageTables& t, int shape, double sxw, kern::EpiConsts
   // the remaining sqs read the previous rounded code (a fork, shape 3, reads
   // the same R1 twice)
   for (size_t i = next; i < qs.size(); ++i) {
-    if (!epi_from_code(prev_s, prev_nonneg, t.sq[qs[i]], e.q[i])) return false;
+    const kern::FSq& fp = t.sq[qs[next - 1]];  // the code R all of them read
+    if (!epi_from_code(prev_s, prev_nonneg, t.sq[qs[i]], e.q[i], fp.qmin, fp.qmax)) {
+      return false;
+    }
   }
   if (shape == 5) {
     // fp32 output value v = r * s of the last sq (T-domain: fma(R, s, -M*s))
@@ -668,7 +674,8 @@ bool pool_stores(const kern::StageTables& t, double s_in, kern::PoolStores& ps) 
     if (f.zp != 0.0f || f.has_acc || f.passthrough || b.kind != 0 || b.hw != 1 || b.ld % 16 != 0) {
       return false;
     }
-    if (!epi_from_code(s_in, false, f, ps.q[i])) return false;
+    // pooled codes span the input grid's int8 range at most
+    if (!epi_from_code(s_in, false, f, ps.q[i], -128.0, 127.0)) return false;
     ps.out[i] = static_cast<int8_t*>(b.ptr);
     ps.ld[i] = b.ld;
   }
@@ -1292,10 +1299,18 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
         if (prof) device::profile_gemm_begin();
         kern::tc_conv(sp, S());
         if (prof) {
+          // algorithmic bytes: input codes once (the NHWC tensor for implicit
+          // GEMM), weight codes, bias, code outputs / residual / fp32 outputs
+          const double M = static_cast<double>(sp.M);
+          const double a_bytes = st.gather ? static_cast<double>(sp.Nimg) * st.H * st.W * sp.ld
+                                           : M * st.Ktrue;
+          const double out_bytes = M * st.O * (st.n_out + (st.res_val >= 0 ? 1 : 0)) +
+                                   (pa.shape == 5 ? 4.0 * M * st.O : 0.0);
           device::profile_gemm_end(
-              2.0 * static_cast<double>(sp.M) * st.O *
-              (st.dense ? st.Ktrue
-                        : (st.s2d ? st.s2d_C * st.s2d_KH * st.s2d_KW : st.C * st.KH * st.KW)));
+              2.0 * M * st.O *
+                  (st.dense ? st.Ktrue
+                            : (st.s2d ? st.s2d_C * st.s2d_KH * st.s2d_KW : st.C * st.KH * st.KW)),
+              a_bytes + static_cast<double>(st.O) * st.Ktrue + 4.0 * st.O + out_bytes);
         }
         device::counters().tcgen05_gemms++;
         break;

@@ -81,8 +81,12 @@ __device__ __forceinline__ void bar_wait_sleep(uint64_t* b, uint32_t phase) {
       : "=r"(ok)
       : "r"(su32(b)), "r"(phase)
       : "memory");
+  uint32_t ns = 32;
   while (!ok) {
-    __nanosleep(32);
+    // exponential backoff: these waits are long (a whole tile of epilogue)
+    // and every poll costs an issue slot the epilogue warps could use
+    __nanosleep(ns);
+    ns = ns < 512 ? 2 * ns : ns;
     asm volatile(
         "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(ok)

@@ -229,6 +229,7 @@ enum : int { kShapeGeneric = 0, kShapeStore = 1, kShapeSqStore = 2, kShapeAddFor
 // round 16 values into sq q's code domain; the (uniform) flag tests sit
 // outside the element loops so each variant is straight-line code
 __device__ __forceinline__ void epi_round(float (&x)[16], const EpiSq& q) {
+  if (q.flags & kEpiNoClamp) return;
 #pragma unroll
   for (int j = 0; j < 16; ++j) x[j] = fminf(fmaxf(x[j], q.lo), q.hi);
   if (q.flags & kEpiExact) return;

@@ -120,7 +120,9 @@ struct StageTables {
 // RZ(t + M) truncates the fraction on the unit grid of [2^23, 2^24).
 constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
 
-enum : int32_t { kEpiNonneg = 1, kEpiExact = 2 };
+// kEpiNoClamp (with kEpiExact): the host proved k * [qmin_in, qmax_in] lies
+// inside [qmin, qmax], so the output-domain clamp is the identity
+enum : int32_t { kEpiNonneg = 1, kEpiExact = 2, kEpiNoClamp = 4 };
 
 struct EpiSq {
   float k;    // x = fma(R_in, k, off): input scale ratio s_in / s (sq0: s_x*s_w / s)
