@@ -26,7 +26,7 @@ def main():
         ("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "tensor pipe % (realtime)"),
         ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe % active"),
         ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "ALU pipe % active"),
-        ("SM_A.TriageCompute.sm__inst_executed_pipe_xu_realtime.avg.pct_of_peak_sustained_elapsed", "XU pipe % (realtime)"),
+        ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "XU (conversion) pipe % active"),
         ("sm__inst_executed.avg.per_cycle_active", "IPC per SM"),
         ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
         ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
