@@ -96,6 +96,10 @@ int qc_collect_histograms(const qc_graph* g, const qc_dataset* d, const int* edg
 int qc_predict_scores(const qc_graph* g, const qc_dataset* d, const int64_t* bind_nodes,
                       const qc_qparams* bind_params, size_t n_bind, float* out, size_t cap,
                       size_t* n_out, int64_t* per_sample);
+/* host worker pool self-test (no GPU): sum of i over [0, n) through
+ * quantc::parallel_for with `workers`; throw_at >= 0 makes that index throw
+ * (the call then reports QC_ERR_INTERNAL with the lowest throwing index). */
+int qcu_parallel_selftest(size_t n, int workers, int64_t throw_at, int64_t* sum);
 /* counters since load: kernel launches issued by the engine, tcgen05 GEMMs */
 int qcu_counters(int64_t* steps, int64_t* tcgen05_gemms, int64_t* f64_convs,
                  int64_t* fused_batches);

@@ -4,13 +4,17 @@
 // parallel.cpp:15-56 (ranges, error messages' meaning, first-by-index
 // exception rethrow).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <exception>
+#include <functional>
 #include <mutex>
+#include <condition_variable>
 #include <stdexcept>
 #include <thread>
+#include <vector>
 
 #include "quantc/bigint.hpp"
 #include "quantc/dtype.hpp"
@@ -255,36 +259,118 @@ int resolve_workers(int requested) {
   return hw > 0 ? static_cast<int>(hw) : 1;
 }
 
+namespace {
+
+// Persistent workers for parallel_for: spawning threads per call costs tens of
+// microseconds each, which dominated short host loops (e.g. packing a batch
+// of samples into pinned staging).  A call hands out indices through an
+// atomic counter; the caller participates; nested calls run serially.
+class Pool {
+ public:
+  // Never destroyed: at process exit the workers are still blocked on cv_,
+  // and destroying a condition variable with waiters blocks in glibc.
+  static Pool& get() {
+    static Pool* p = new Pool;
+    return *p;
+  }
+
+  void run(size_t n, size_t w, const std::function<void(size_t)>& fn) {
+    std::unique_lock<std::mutex> call(call_mu_);  // one parallel_for at a time
+    ensure(w - 1);
+    Job job;
+    job.n = n;
+    job.fn = &fn;
+    job.first_idx = n;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = &job;
+      active_ = w - 1;
+      limit_ = w - 1;  // workers 0..w-2 join this call
+      ++gen_;
+    }
+    cv_.notify_all();
+    work(job);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return active_ == 0; });
+    job_ = nullptr;
+    lk.unlock();
+    if (job.first_err) std::rethrow_exception(job.first_err);
+  }
+
+  static bool in_worker() { return tl_worker_; }
+
+ private:
+  struct Job {
+    size_t n = 0;
+    const std::function<void(size_t)>* fn = nullptr;
+    std::atomic<size_t> next{0};
+    std::mutex err_mu;
+    size_t first_idx = 0;
+    std::exception_ptr first_err;
+  };
+
+  static void work(Job& job) {
+    for (;;) {
+      const size_t i = job.next.fetch_add(1);
+      if (i >= job.n) return;
+      try {
+        (*job.fn)(i);
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(job.err_mu);
+        if (i < job.first_idx) {
+          job.first_idx = i;
+          job.first_err = std::current_exception();
+        }
+      }
+    }
+  }
+
+  void ensure(size_t k) {
+    while (threads_.size() < k) {
+      const size_t id = threads_.size();
+      threads_.emplace_back([this, id] { loop(id); });
+      threads_.back().detach();
+    }
+  }
+
+  void loop(size_t id) {
+    tl_worker_ = true;
+    uint64_t seen = 0;
+    for (;;) {
+      Job* job = nullptr;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (job_ == nullptr || id >= limit_) continue;
+        job = job_;
+      }
+      work(*job);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--active_ == 0) done_cv_.notify_all();
+    }
+  }
+
+  std::mutex call_mu_, mu_;
+  std::condition_variable cv_, done_cv_;
+  std::vector<std::thread> threads_;
+  Job* job_ = nullptr;
+  size_t active_ = 0, limit_ = 0;
+  uint64_t gen_ = 0;
+  static thread_local bool tl_worker_;
+};
+thread_local bool Pool::tl_worker_ = false;
+
+}  // namespace
+
 void parallel_for(size_t n, int workers, const std::function<void(size_t)>& fn) {
   if (n == 0) return;
   const size_t w = std::min<size_t>(static_cast<size_t>(resolve_workers(workers)), n);
-  if (w <= 1) {
+  if (w <= 1 || Pool::in_worker()) {
     for (size_t i = 0; i < n; ++i) fn(i);
     return;
   }
-  std::vector<std::exception_ptr> first(w);
-  std::vector<size_t> first_idx(w, n);
-  std::vector<std::thread> pool;
-  for (size_t t = 0; t < w; ++t) {
-    pool.emplace_back([&, t] {
-      for (size_t i = t; i < n; i += w) {
-        try {
-          fn(i);
-        } catch (...) {
-          if (i < first_idx[t]) {
-            first_idx[t] = i;
-            first[t] = std::current_exception();
-          }
-        }
-      }
-    });
-  }
-  for (auto& th : pool) th.join();
-  size_t best = 0;
-  for (size_t t = 1; t < w; ++t) {
-    if (first_idx[t] < first_idx[best]) best = t;
-  }
-  if (first[best]) std::rethrow_exception(first[best]);
+  Pool::get().run(n, w, fn);
 }
 
 }  // namespace quantc

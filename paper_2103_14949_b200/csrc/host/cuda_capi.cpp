@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -10,6 +11,7 @@
 #include "../kernels/kernels.h"
 #include "engine.hpp"
 #include "quantc/device.hpp"
+#include "quantc/parallel.hpp"
 
 using namespace quantc;
 
@@ -180,6 +182,24 @@ void* qcu_engine_stream(void) {
 
 int qcu_profile_enable(int on) {
   return wrap([&] { device::profile_enable(on != 0); });
+}
+
+int qcu_parallel_selftest(size_t n, int workers, int64_t throw_at, int64_t* sum) {
+  // host-only: no device context
+  try {
+    std::atomic<int64_t> acc{0};
+    parallel_for(n, workers, [&](size_t i) {
+      if (throw_at >= 0 && static_cast<int64_t>(i) >= throw_at) {
+        throw std::runtime_error("selftest index " + std::to_string(i));
+      }
+      acc.fetch_add(static_cast<int64_t>(i));
+    });
+    *sum = acc.load();
+    return QC_OK;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return QC_ERR_INTERNAL;
+  }
 }
 
 int qcu_profile_read(double* gemm_ms, int64_t* gemm_launches, double* gemm_ops,

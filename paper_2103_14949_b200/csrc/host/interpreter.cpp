@@ -5,7 +5,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "dataset.hpp"
 #include "engine.hpp"
@@ -129,18 +132,31 @@ std::vector<int64_t> predict_top1(const Graph& g, const Dataset& dataset, int wo
                                   const SimBinding* binding) {
   (void)workers;  // per-sample parallelism is the GPU batch dimension
   if (dataset.empty()) return {};
+  static const bool hprof = std::getenv("QUANTC_HOST_PROF") != nullptr;
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
   const engine::PlanLease lease = engine::lease_plan(g);  // weights stay resident across calls
   const engine::Plan& plan = lease.plan();
+  const auto t1 = clk::now();
   gpu::DeviceDataset dd(g, dataset);
+  const auto t2 = clk::now();
   const bool realized = g.is_realized();
   if (realized && g.contains_op(OpKind::kSimulatedQuantize)) {
     throw EvalError("eval_int expects a realized graph without simulated_quantize nodes");
   }
   auto preds = gpu::predict_device(plan, dd, realized ? nullptr : binding, realized,
                                    /*allow_fast=*/binding != nullptr);
+  const auto t3 = clk::now();
   std::vector<int64_t> h(dataset.size());
   cudaMemcpyAsync(h.data(), preds.get(), h.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, S());
   device::synchronize();
+  if (hprof) {
+    auto us = [](clk::time_point a, clk::time_point b) {
+      return std::chrono::duration<double, std::micro>(b - a).count();
+    };
+    std::fprintf(stderr, "predict_top1 us: lease %.1f dataset %.1f predict(host) %.1f sync %.1f total %.1f\n",
+                 us(t0, t1), us(t1, t2), us(t2, t3), us(t3, clk::now()), us(t0, clk::now()));
+  }
   return h;
 }
 

@@ -73,3 +73,34 @@ def test_host_scalar_helpers_match_reference(b200, ref):
             ref.compute_scale(bad, 8, 1)
     with pytest.raises(Q.CalibrationError):
         b200.threshold_quantile(counts, 3.0, 1.5)
+
+
+def test_host_worker_pool_selftest_and_clean_exit(tmp_path):
+    """quantc::parallel_for runs on persistent workers: sums are exact for any
+    worker count, the lowest failing index's exception is reported, and a
+    process that used the pool exits promptly (the workers never block exit)."""
+    import pathlib
+    import subprocess
+    import sys
+    repo = str(pathlib.Path(__file__).resolve().parents[1])
+    code = r'''
+import ctypes as C, sys
+sys.path.insert(0, %r)
+from paper_2103_14949_b200 import quantc as Q
+L = Q.load_b200().lib
+f = L.qcu_parallel_selftest
+f.argtypes = [C.c_size_t, C.c_int, C.c_int64, C.POINTER(C.c_int64)]
+s = C.c_int64()
+for n in (0, 1, 7, 1000, 100003):
+    for w in (1, 2, 8, 33):
+        assert f(n, w, -1, C.byref(s)) == 0
+        assert s.value == n * (n - 1) // 2, (n, w, s.value)
+rc = f(1000, 8, 500, C.byref(s))
+assert rc != 0
+L.qcu_last_error.restype = C.c_char_p
+assert b"selftest index 500" in L.qcu_last_error(), L.qcu_last_error()
+print("ok")
+''' % (repo,)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    assert out.stdout.strip().endswith("ok")
