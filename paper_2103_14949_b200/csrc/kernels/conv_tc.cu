@@ -45,10 +45,17 @@ constexpr int BM = 128;
 constexpr int BK = 128;
 constexpr int UMMA_K = 32;
 constexpr int MAX_STAGES = 8;
-constexpr int EPI_WARPS = 8;
-constexpr int PROD_WARPS = 4;
-constexpr int MMA_WARP = EPI_WARPS + PROD_WARPS;
-constexpr int THREADS = (MMA_WARP + 1) * 32;
+// warp layout, by epilogue width EPIW: EPIW epilogue warps (EPIW/4 per TMEM
+// lane quarter), then the producer warps (4 for the cp.async gather, whose
+// 128 threads own one A row each; 1 for the TMA producers), then the MMA warp
+template <int EPIW>
+struct Layout {
+  static constexpr int EPI_WARPS = EPIW;
+  static constexpr int PROD_WARPS = EPIW == 8 ? 4 : 1;
+  static constexpr int MMA_WARP = EPI_WARPS + PROD_WARPS;
+  static constexpr int THREADS = (MMA_WARP + 1) * 32;
+  static constexpr int PARTS = EPIW / 4;  // column parts per lane quarter
+};
 constexpr int SMEM_LIMIT = 227 * 1024;
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -123,8 +130,9 @@ __device__ __forceinline__ void tma_store2d(const CUtensorMap* m, const void* sr
       "r"(su32(src)), "r"(c0), "r"(c1)
       : "memory");
 }
+template <int EPIW>
 __device__ __forceinline__ void epi_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"n"(EPIW * 32) : "memory");
 }
 __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
   return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>(1) << 16) |
@@ -197,8 +205,8 @@ __device__ __forceinline__ void tmem_wait(uint32_t (&d)[16]) {
                : "memory");
 }
 
-template <int BN, int SHAPE>
-__global__ void __launch_bounds__(THREADS, 1)
+template <int BN, int SHAPE, int EPIW>
+__global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
     tc_conv_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_o0,
@@ -210,6 +218,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   constexpr uint32_t SLOT_BYTES = BM * BN;
   constexpr int SWZ = BN >= 128 ? 128 : 64;
   constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  constexpr int EPI_WARPS = Layout<EPIW>::EPI_WARPS;
+  constexpr int PROD_WARPS = Layout<EPIW>::PROD_WARPS;
+  constexpr int MMA_WARP = Layout<EPIW>::MMA_WARP;
+  constexpr int PARTS = Layout<EPIW>::PARTS;
+  constexpr int NCHUNK = BN / 16;
   const int stages = args.stages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -330,7 +343,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
       }
-    } else {
+    } else if constexpr (PROD_WARPS == 4) {
       const TcGeom& g = args.g;
       int s = 0;
       uint32_t ph = 0;
@@ -436,7 +449,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else {
     // ================= epilogue =================
     const int quarter = warp & 3;
-    const int half = warp >> 2;
+    const int part = warp >> 2;  // this warp's chunks: part, part + PARTS, ...
     const int r = quarter * 32 + lane;
     const bool leader = threadIdx.x == 0;
     // slot set of the tile with local index tl
@@ -472,7 +485,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           }
         }
-        epi_sync();
+        epi_sync<EPIW>();
       }
       if (args.has_res) {
         if (args.dbuf) {
@@ -488,12 +501,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         // — O % 16 == 0, all I/O through slots (rows >= M and columns >= O
         // are clipped by the TMA store), zp = 0, no live acc clamp.  TMEM
         // loads run one chunk ahead of the math.
-        const int cbeg = half * (BN / 2), cend = cbeg + BN / 2;
         const EpiConsts& e = args.epi;
         uint32_t d[EW];
-        tmem_ld<EW>(tbase + cbeg, d);
+        if (part < NCHUNK) tmem_ld<EW>(tbase + part * EW, d);
 #pragma unroll 1
-        for (int c0 = cbeg; c0 < cend; c0 += EW) {
+        for (int c = part; c < NCHUNK; c += PARTS) {
+          const int c0 = c * EW;
           tmem_wait(d);
           const int n = n0 + c0;
           // acc -> float without the conversion pipe: bits(0x4B400000 + a) is
@@ -505,7 +518,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             u[j] = d[j] + 0x4B400000u;
             chk |= u[j] ^ 0x4B000000u;
           }
-          if (c0 + EW < cend) tmem_ld<EW>(tbase + c0 + EW, d);
+          if (c + PARTS < NCHUNK) tmem_ld<EW>(tbase + (c + PARTS) * EW, d);
           if (n < args.N) {
             float x[EW];
             float bs[EW];
@@ -538,7 +551,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       } else
 #pragma unroll 1
-      for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += EW) {
+      for (int c0 = part * EW; c0 < BN; c0 += PARTS * EW) {
         uint32_t d[EW];
         tmem_ld<EW>(tbase + c0, d);
         tmem_wait(d);
@@ -593,7 +606,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       bar_arrive(&tempty[acc]);
-      if (args.n_out > 0 || args.has_res) epi_sync();
+      if (args.n_out > 0 || args.has_res) epi_sync<EPIW>();
       if (leader) {
         if (args.n_out > 0) {
           for (int blk = 0; blk < BN / SWZ; ++blk) {
@@ -803,15 +816,28 @@ void launch_tc(const CUtensorMap* maps, TcArgs a, cudaStream_t s) {
   if (stages < 2) stages = 2;
   a.stages = stages;
   const size_t smem = static_cast<size_t>(fixed) + static_cast<size_t>(stages) * stage_bytes;
-  static std::once_flag once;
-  std::call_once(once, [&] {
-    cudaFuncSetAttribute(tc_conv_kernel<BN, SHAPE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         SMEM_LIMIT);
-  });
   const int tiles = a.m_tiles * a.n_tiles;
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  tc_conv_kernel<BN, SHAPE><<<grid, THREADS, smem, s>>>(maps[0], maps[1], maps[2], maps[3],
-                                                        maps[4], a);
+  // the cp.async gather needs 4 producer warps (one thread per A row); TMA
+  // producers need one thread, which leaves room for 12 epilogue warps
+  static const bool epi8 = std::getenv("QUANTC_EPI8") != nullptr;
+  if (a.gather == 1 || epi8) {
+    static std::once_flag once;
+    std::call_once(once, [&] {
+      cudaFuncSetAttribute(tc_conv_kernel<BN, SHAPE, 8>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
+    });
+    tc_conv_kernel<BN, SHAPE, 8><<<grid, Layout<8>::THREADS, smem, s>>>(
+        maps[0], maps[1], maps[2], maps[3], maps[4], a);
+  } else {
+    static std::once_flag once;
+    std::call_once(once, [&] {
+      cudaFuncSetAttribute(tc_conv_kernel<BN, SHAPE, 12>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
+    });
+    tc_conv_kernel<BN, SHAPE, 12><<<grid, Layout<12>::THREADS, smem, s>>>(
+        maps[0], maps[1], maps[2], maps[3], maps[4], a);
+  }
   QC_CUDA_CHECK_LAUNCH();
 }
 
