@@ -57,6 +57,10 @@ struct Layout {
   static constexpr int PARTS = EPIW / 4;  // column parts per lane quarter
 };
 constexpr int SMEM_LIMIT = 227 * 1024;
+#ifndef QC_EPIW_TMA
+#define QC_EPIW_TMA 16
+#endif
+constexpr int EPIW_TMA = QC_EPIW_TMA;  // epilogue warps of TMA-fed launches
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -832,10 +836,10 @@ void launch_tc(const CUtensorMap* maps, TcArgs a, cudaStream_t s) {
   } else {
     static std::once_flag once;
     std::call_once(once, [&] {
-      cudaFuncSetAttribute(tc_conv_kernel<BN, SHAPE, 12>,
+      cudaFuncSetAttribute(tc_conv_kernel<BN, SHAPE, EPIW_TMA>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
     });
-    tc_conv_kernel<BN, SHAPE, 12><<<grid, Layout<12>::THREADS, smem, s>>>(
+    tc_conv_kernel<BN, SHAPE, EPIW_TMA><<<grid, Layout<EPIW_TMA>::THREADS, smem, s>>>(
         maps[0], maps[1], maps[2], maps[3], maps[4], a);
   }
   QC_CUDA_CHECK_LAUNCH();
