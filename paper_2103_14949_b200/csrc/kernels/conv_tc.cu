@@ -138,6 +138,13 @@ template <int EPIW>
 __device__ __forceinline__ void epi_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(EPIW * 32) : "memory");
 }
+// K-major smem operand descriptor, rows of `sw` bytes swizzled in 8-row atoms:
+// sw = 128 -> layout SWIZZLE_128B (2), sw = 64 -> SWIZZLE_64B (4); SBO = 8 rows
+__device__ __forceinline__ uint64_t desc_sw(uint32_t saddr, uint32_t sw) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>(1) << 16) |
+         (static_cast<uint64_t>((8 * sw) >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
+         (static_cast<uint64_t>(sw == 128 ? 2 : 4) << 61);
+}
 __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
   return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>(1) << 16) |
          (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
@@ -171,6 +178,7 @@ struct TcArgs {
   int M, N, K;   // GEMM dims (K multiple of 128)
   int gather;
   int stages;    // runtime pipeline depth (<= MAX_STAGES)
+  int bkb;       // K-block bytes: 128 (SWIZZLE_128B tiles) or 64 (SWIZZLE_64B, 64-channel im2col)
   int n_out;     // smem-staged code outputs (TMA store), 0..2
   int has_res;   // TMA-prefetched residual slot (index n_out)
   int dbuf;      // 1: two slot sets, alternating by tile (stores / prefetch overlap)
@@ -217,8 +225,8 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
                    const __grid_constant__ CUtensorMap map_o1,
                    const __grid_constant__ CUtensorMap map_r, const TcArgs args) {
   constexpr int EW = 16;
-  constexpr uint32_t A_BYTES = BM * BK;
-  constexpr uint32_t B_BYTES = BN * BK;
+  const uint32_t A_BYTES = BM * args.bkb;
+  const uint32_t B_BYTES = BN * args.bkb;
   constexpr uint32_t SLOT_BYTES = BM * BN;
   constexpr int SWZ = BN >= 128 ? 128 : 64;
   constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
@@ -268,7 +276,7 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int nk = args.K / BK;
+  const int nk = args.K / args.bkb;
   const int n_tiles_total = args.m_tiles * args.n_tiles;
 
   if (threadIdx.x == 0) {
@@ -312,13 +320,13 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
           const int oh = rem / g.OW, ow = rem - oh * g.OW;
           const int w0 = ow * g.sw - g.pw, h0 = oh * g.sh - g.ph;
           for (int kb = 0; kb < nk; ++kb) {
-            const int tap = (kb * BK) / g.ld, c0 = kb * BK - tap * g.ld;
+            const int tap = (kb * args.bkb) / g.ld, c0 = kb * args.bkb - tap * g.ld;
             const int kh = tap / g.KW, kw = tap - kh * g.KW;
             if (wrapped) bar_wait_sleep(&empty[s], ph ^ 1);
             bar_expect(&full[s], A_BYTES + B_BYTES);
             tma_im2col(&map_a, &full[s], sa + s * A_BYTES, c0, w0, h0, img,
                        static_cast<uint16_t>(kw), static_cast<uint16_t>(kh));
-            tma2d(&map_b, &full[s], sb + s * B_BYTES, kb * BK, n0);
+            tma2d(&map_b, &full[s], sb + s * B_BYTES, kb * args.bkb, n0);
             if (++s == stages) {
               s = 0;
               ph ^= 1;
@@ -436,10 +444,18 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
           if (args.gather == 1) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t ab = su32(sa + s * A_BYTES), bb = su32(sb + s * B_BYTES);
+          if (args.bkb == 128) {
 #pragma unroll
-          for (int k = 0; k < BK / UMMA_K; ++k) {
-            mma(d, desc_sw128(ab + k * UMMA_K), desc_sw128(bb + k * UMMA_K), id,
-                (kb | k) != 0 ? 1u : 0u);
+            for (int k = 0; k < 128 / UMMA_K; ++k) {
+              mma(d, desc_sw128(ab + k * UMMA_K), desc_sw128(bb + k * UMMA_K), id,
+                  (kb | k) != 0 ? 1u : 0u);
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 64 / UMMA_K; ++k) {
+              mma(d, desc_sw(ab + k * UMMA_K, 64), desc_sw(bb + k * UMMA_K, 64), id,
+                  (kb | k) != 0 ? 1u : 0u);
+            }
           }
           commit(&empty[s]);
           if (++s == stages) {
@@ -721,10 +737,10 @@ EncodeIm2col im2col_encoder() {
 
 // im2col map over NHWC int8 codes [N, H, W, ld]: boxes of 128 pixels x 128
 // channels, SWIZZLE_128B (the UMMA K-major layout); false when unsupported
-bool im2col_map(CUtensorMap* m, const TcConvSpec& sp) {
+bool im2col_map(CUtensorMap* m, const TcConvSpec& sp, int cbox) {
   if (!im2col_encoder()) return false;
   const MapKey key{sp.x, sp.ld, sp.W, sp.H, sp.Nimg,
-                   sp.KH * 4096 + sp.KW, sp.ph * 4096 + sp.pw, sp.sh * 4096 + sp.sw, 1};
+                   sp.KH * 4096 + sp.KW, sp.ph * 4096 + sp.pw, sp.sh * 4096 + sp.sw, 1 + cbox};
   {
     std::lock_guard<std::mutex> lk(g_map_mu);
     auto it = map_cache().find(key);
@@ -743,8 +759,9 @@ bool im2col_map(CUtensorMap* m, const TcConvSpec& sp) {
   const int upper[2] = {sp.pw - (sp.KW - 1), sp.ph - (sp.KH - 1)};
   const cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(sp.sw), static_cast<cuuint32_t>(sp.sh), 1};
   if (im2col_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(sp.x), dims,
-                       strides, lower, upper, BK, BM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       strides, lower, upper, cbox, BM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       cbox == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
     return false;
   }
@@ -759,7 +776,7 @@ bool im2col_map(CUtensorMap* m, const TcConvSpec& sp) {
 // bounding-box offsets inside the rank-4 encoding's [-128, 127]
 bool im2col_ok(const TcConvSpec& sp) {
   static const bool off = std::getenv("QUANTC_NO_IM2COL") != nullptr;
-  return !off && sp.gather && sp.ld % BK == 0 && sp.KH == sp.KW && sp.ph == sp.pw &&
+  return !off && sp.gather && (sp.ld % BK == 0 || sp.ld == 64) && sp.KH == sp.KW && sp.ph == sp.pw &&
          sp.sh == sp.sw && sp.sh <= 8 && sp.ph <= 127 && sp.KH - 1 - sp.ph <= 128 &&
          sp.KH <= 65535;
 }
@@ -797,8 +814,8 @@ int smem_fixed(const TcArgs& a, int bn, int sets, bool shape) {
 
 // pipeline depth that fits next to `fixed` bytes (capped by what the K loop uses)
 int fit_stages(const TcArgs& a, int bn, int fixed) {
-  int stages = (SMEM_LIMIT - fixed) / (BM * BK + bn * BK);
-  const int nk = a.K / BK;
+  int stages = (SMEM_LIMIT - fixed) / (BM * a.bkb + bn * a.bkb);
+  const int nk = a.K / a.bkb;
   stages = stages > MAX_STAGES ? MAX_STAGES : stages;
   return stages > nk + 1 ? nk + 1 : stages;
 }
@@ -812,7 +829,7 @@ bool dbuf_fits(const TcArgs& a, int bn, bool shape) {
 
 template <int BN, int SHAPE>
 void launch_tc(const CUtensorMap* maps, TcArgs a, cudaStream_t s) {
-  constexpr int stage_bytes = BM * BK + BN * BK;
+  const int stage_bytes = BM * a.bkb + BN * a.bkb;
   constexpr bool shape = SHAPE != kShapeGeneric;
   a.dbuf = dbuf_fits(a, BN, shape) ? 1 : 0;
   const int fixed = smem_fixed(a, BN, a.dbuf + 1, shape);
@@ -893,6 +910,22 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
   a.epi = sp.epi;
   a.always_small = sp.acc_bound <= static_cast<double>(1 << 24) ? 1 : 0;
   a.m_tiles = static_cast<int>((sp.M + BM - 1) / BM);
+  a.bkb = BK;
+  CUtensorMap maps[5];
+  // A: direct 2-D map over the code rows (a valid dummy when gathering);
+  // im2col TMA replaces the cp.async gather where the geometry allows: 128-
+  // channel K blocks (SWIZZLE_128B) or, for 64-channel layers, 64-byte K
+  // blocks (SWIZZLE_64B); K then stops at the last real tap
+  maps[0] = bmap(sp.x, sp.gather ? BM : sp.M, sp.gather ? BK : sp.Ktrue, sp.gather ? BK : sp.lda,
+                 BK, BM, 128);
+  if (im2col_ok(sp)) {
+    const int cbox = sp.ld % BK == 0 ? BK : 64;
+    if (im2col_map(&maps[0], sp, cbox)) {
+      a.gather = 2;
+      a.bkb = cbox;
+      a.K = sp.KH * sp.KW * sp.ld;
+    }
+  }
   // narrower output tiles while that still fits the grid in one wave: a
   // layer with few M tiles (late stages at small batch) would otherwise
   // leave most SMs idle
@@ -905,12 +938,7 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
   }
   const int swz = BN >= 128 ? 128 : 64;
   a.n_tiles = (sp.O + BN - 1) / BN;
-  CUtensorMap maps[5];
-  // A: direct 2-D map over the code rows (a valid dummy when gathering)
-  maps[0] = bmap(sp.x, sp.gather ? BM : sp.M, sp.gather ? BK : sp.Ktrue, sp.gather ? BK : sp.lda,
-                 BK, BM, 128);
-  if (im2col_ok(sp) && im2col_map(&maps[0], sp)) a.gather = 2;
-  maps[1] = bmap(sp.w, sp.O, sp.Kpad, sp.Kpad, BK, BN, 128);
+  maps[1] = bmap(sp.w, sp.O, sp.Kpad, sp.Kpad, a.bkb, BN, a.bkb);
   for (int o = 0; o < 2; ++o) {
     maps[2 + o] = o < sp.n_out ? bmap(sp.out_ptr[o], sp.M, sp.out_cols[o], sp.out_ld[o], swz, BM, swz)
                                : maps[1];
