@@ -75,36 +75,18 @@ __device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
                : "memory");
 }
+// Waits park the thread in hardware until the phase completes (try_wait with
+// a suspend-time hint): no polling loop, so waiting threads spend no issue
+// slots that the epilogue warps could use.
 __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t phase) {
   asm volatile(
       "{\n.reg .pred p;\nW_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       "@!p bra W_%=;\n}\n" ::"r"(su32(b)),
-      "r"(phase)
+      "r"(phase), "r"(0x100000)
       : "memory");
 }
-// single-thread waits (MMA issuer / TMA producer): back off between polls so
-// spinning lanes do not steal issue slots from the epilogue warps
-__device__ __forceinline__ void bar_wait_sleep(uint64_t* b, uint32_t phase) {
-  uint32_t ok = 0;
-  asm volatile(
-      "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(ok)
-      : "r"(su32(b)), "r"(phase)
-      : "memory");
-  uint32_t ns = 32;
-  while (!ok) {
-    // exponential backoff: these waits are long (a whole tile of epilogue)
-    // and every poll costs an issue slot the epilogue warps could use
-    __nanosleep(ns);
-    ns = ns < 512 ? 2 * ns : ns;
-    asm volatile(
-        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(su32(b)), "r"(phase)
-        : "memory");
-  }
-}
+__device__ __forceinline__ void bar_wait_sleep(uint64_t* b, uint32_t phase) { bar_wait(b, phase); }
 __device__ __forceinline__ void tma2d(const CUtensorMap* m, uint64_t* bar, void* dst, int c0,
                                       int c1) {
   asm volatile(
@@ -522,11 +504,11 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
         // are clipped by the TMA store), zp = 0, no live acc clamp.  TMEM
         // loads run one chunk ahead of the math.
         const EpiConsts& e = args.epi;
-        uint32_t d[EW];
-        if (part < NCHUNK) tmem_ld<EW>(tbase + part * EW, d);
 #pragma unroll 1
         for (int c = part; c < NCHUNK; c += PARTS) {
           const int c0 = c * EW;
+          uint32_t d[EW];
+          tmem_ld<EW>(tbase + c0, d);
           tmem_wait(d);
           const int n = n0 + c0;
           // acc -> float without the conversion pipe: bits(0x4B400000 + a) is
@@ -538,7 +520,6 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
             u[j] = d[j] + 0x4B400000u;
             chk |= u[j] ^ 0x4B000000u;
           }
-          if (c + PARTS < NCHUNK) tmem_ld<EW>(tbase + (c + PARTS) * EW, d);
           if (n < args.N) {
             float x[EW];
             float bs[EW];
