@@ -1267,9 +1267,25 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
                    static_cast<double>(wf.s);
         sp.prog = pa;
         if (pa.shape != 0 && !make_epi(tabs[si], pa.shape, sp.scale, sp.epi)) sp.prog.shape = 0;
+        // flag-specialised kernels for the common constant profiles (fused.cuh)
+        if (!std::getenv("QUANTC_NO_SPECIAL")) {
+          auto identity = [](const kern::EpiSq& q) {
+            return q.flags == (kern::kEpiNonneg | kern::kEpiExact | kern::kEpiNoClamp) &&
+                   q.k == 1.0f && q.off == 0.0f;
+          };
+          const kern::EpiConsts& e = sp.epi;
+          if (sp.prog.shape == kern::kShapeSqStore && e.q[0].flags == kern::kEpiNonneg &&
+              identity(e.q[1])) {
+            sp.prog.shape = kern::kShapeSqStoreId;
+          } else if (sp.prog.shape == kern::kShapeAddFork && e.q[0].flags == 0 &&
+                     e.q[1].flags == kern::kEpiNonneg && identity(e.q[2]) && identity(e.q[3])) {
+            sp.prog.shape = kern::kShapeAddForkId;
+          }
+        }
         if (std::getenv("QUANTC_DUMP_PLAN")) {
-          std::fprintf(stderr, "run stage %zu step %d shape %d -> %d ops", si, st.step, pa.shape,
-                       sp.prog.shape);
+          std::fprintf(stderr, "run stage %zu step %d shape %d -> %d flags %d %d %d %d ops", si,
+                       st.step, pa.shape, sp.prog.shape, sp.epi.q[0].flags, sp.epi.q[1].flags,
+                       sp.epi.q[2].flags, sp.epi.q[3].flags);
           for (int pc = 0; pc < tabs[si].n_code; ++pc) {
             const kern::ProgInstr& in = tabs[si].code[pc];
             std::fprintf(stderr, " %d", in.op);

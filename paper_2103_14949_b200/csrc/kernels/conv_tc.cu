@@ -861,6 +861,12 @@ void launch_bn(const CUtensorMap* maps, const TcArgs& a, cudaStream_t s) {
     case kShapeAddF32:
       launch_tc<BN, kShapeAddF32>(maps, a, s);
       break;
+    case kShapeSqStoreId:
+      launch_tc<BN, kShapeSqStoreId>(maps, a, s);
+      break;
+    case kShapeAddForkId:
+      launch_tc<BN, kShapeAddForkId>(maps, a, s);
+      break;
     default:
       launch_tc<BN, kShapeGeneric>(maps, a, s);
       break;

@@ -210,16 +210,7 @@ __device__ __forceinline__ void load_values(const ProgBuf& b, int64_t m, int n0,
   }
 }
 
-// Straight-line epilogues for the program shapes that dominate CNN graphs
-// (identified on the host after optimise_tables; operand indices are read
-// from the stage table).  SHAPE 0 is the generic interpreter below.
-//   1: SQ_STORE8
-//   2: SQ, SQ_STORE8                          (conv -> sq [-> relu] -> sq -> codes)
-//   3: SQ, ADD, SQ, PUSH, SQ_STORE8, POP, SQ_STORE8   (residual block end)
-//   4: SQ, ADD, SQ, SQ_STORE8
-//   5: SQ, ADD, SQ, STORE_F32                  (residual end -> fp32 for a pool)
-enum : int { kShapeGeneric = 0, kShapeStore = 1, kShapeSqStore = 2, kShapeAddFork = 3,
-             kShapeAdd = 4, kShapeAddF32 = 5 };
+// (shape ids: fused.h kShape*)
 
 // ---- straight-line shape epilogues (no conversion-pipe instructions) -------------
 // Host preconditions (fastplan classify_shape / make_epi): every sq of the
@@ -249,6 +240,23 @@ __device__ __forceinline__ void epi_next(const float (&R)[16], float (&y)[16], c
 #pragma unroll
   for (int j = 0; j < 16; ++j) y[j] = __fmaf_rn(R[j], q.k, q.off);
   epi_round(y, q);
+}
+
+// compile-time-flag rounding (the specialised shapes): same arithmetic as
+// epi_round with the branches resolved at compile time
+template <bool NONNEG>
+__device__ __forceinline__ void epi_round_ct(float (&x)[16], const EpiSq& q) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) x[j] = fminf(fmaxf(x[j], q.lo), q.hi);
+  if constexpr (NONNEG) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) x[j] = __fadd_rz(__fadd_rz(x[j], 0.5f), kMagic);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      x[j] = copysignf(__fsub_rn(__fadd_rz(__fadd_rz(fabsf(x[j]), 0.5f), kMagic), kMagic), x[j]);
+    }
+  }
 }
 
 // 16 rounded codes -> 16 int8 bytes (low byte of the T-domain bits)
@@ -289,6 +297,29 @@ template <int SHAPE>
 __device__ __forceinline__ void run_shape_epi(float (&x)[16], const EpiConsts& e,
                                               const TileIo& io, int cl, int64_t m, int n,
                                               bool row_ok) {
+  if constexpr (SHAPE == kShapeSqStoreId) {
+    epi_round_ct<true>(x, e.q[0]);
+    sts128(tile_addr(io, e.slot_out[0], cl), epi_pack(x, e.q[1]));  // T-domain: bits as is
+    return;
+  }
+  if constexpr (SHAPE == kShapeAddForkId) {
+    epi_round_ct<false>(x, e.q[0]);
+    const int4 raw = lds128(tile_addr(io, e.slot_res, cl));
+    const uint32_t wr[4] = {static_cast<uint32_t>(raw.x) ^ 0x80808080u,
+                            static_cast<uint32_t>(raw.y) ^ 0x80808080u,
+                            static_cast<uint32_t>(raw.z) ^ 0x80808080u,
+                            static_cast<uint32_t>(raw.w) ^ 0x80808080u};
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float C = __uint_as_float(__byte_perm(wr[j >> 2], 0x4B000000u, 0x7650u + (j & 3)));
+      x[j] = __fmaf_rn(x[j], e.q[1].k, __fmaf_rn(C, e.ka, e.ka_off));
+    }
+    epi_round_ct<true>(x, e.q[1]);
+    const int4 packed = epi_pack(x, e.q[2]);  // q2 == q3 == identity on T-domain R1
+    sts128(tile_addr(io, e.slot_out[0], cl), packed);
+    sts128(tile_addr(io, e.slot_out[1], cl), packed);
+    return;
+  }
   epi_round(x, e.q[0]);
   if (SHAPE == kShapeStore) {
     epi_store(x, e.q[0], io, e.slot_out[0], cl);

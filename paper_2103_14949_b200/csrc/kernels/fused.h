@@ -147,6 +147,23 @@ struct EpiConsts {
   int64_t f32_ld;
 };
 
+// Straight-line epilogues for the program shapes that dominate CNN graphs
+// (identified on the host after optimise_tables; operand indices are read
+// from the stage table).  SHAPE 0 is the generic interpreter below.
+//   1: SQ_STORE8
+//   2: SQ, SQ_STORE8                          (conv -> sq [-> relu] -> sq -> codes)
+//   3: SQ, ADD, SQ, PUSH, SQ_STORE8, POP, SQ_STORE8   (residual block end)
+//   4: SQ, ADD, SQ, SQ_STORE8
+//   5: SQ, ADD, SQ, STORE_F32                  (residual end -> fp32 for a pool)
+// and two flag-specialised forms of the most common constant profiles (host
+// checks the folded constants, fastplan make_epi / specialise):
+//   6: shape 2 with sq0 non-negative rounding and an identity store (k = 1,
+//      exact, no clamp): the T-domain code of sq0 is the stored byte
+//   7: shape 3 with sq0 signed rounding, sq1 non-negative rounding and both
+//      fork stores identities: one packed code, stored to both slots
+enum : int { kShapeGeneric = 0, kShapeStore = 1, kShapeSqStore = 2, kShapeAddFork = 3,
+             kShapeAdd = 4, kShapeAddF32 = 5, kShapeSqStoreId = 6, kShapeAddForkId = 7 };
+
 // kernels receive the stage's table block in global memory
 struct ProgArgs {
   const StageTables* tables;
