@@ -1269,16 +1269,21 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
         if (pa.shape != 0 && !make_epi(tabs[si], pa.shape, sp.scale, sp.epi)) sp.prog.shape = 0;
         // flag-specialised kernels for the common constant profiles (fused.cuh)
         if (!std::getenv("QUANTC_NO_SPECIAL")) {
+          // a k = 1 store of a T-domain code: exact, at most a clamp
           auto identity = [](const kern::EpiSq& q) {
-            return q.flags == (kern::kEpiNonneg | kern::kEpiExact | kern::kEpiNoClamp) &&
+            return (q.flags & ~kern::kEpiNoClamp) == (kern::kEpiNonneg | kern::kEpiExact) &&
                    q.k == 1.0f && q.off == 0.0f;
+          };
+          auto same = [](const kern::EpiSq& a, const kern::EpiSq& b) {
+            return a.flags == b.flags && a.lo == b.lo && a.hi == b.hi;
           };
           const kern::EpiConsts& e = sp.epi;
           if (sp.prog.shape == kern::kShapeSqStore && e.q[0].flags == kern::kEpiNonneg &&
               identity(e.q[1])) {
             sp.prog.shape = kern::kShapeSqStoreId;
           } else if (sp.prog.shape == kern::kShapeAddFork && e.q[0].flags == 0 &&
-                     e.q[1].flags == kern::kEpiNonneg && identity(e.q[2]) && identity(e.q[3])) {
+                     e.q[1].flags == kern::kEpiNonneg && identity(e.q[2]) && identity(e.q[3]) &&
+                     same(e.q[2], e.q[3])) {
             sp.prog.shape = kern::kShapeAddForkId;
           }
         }

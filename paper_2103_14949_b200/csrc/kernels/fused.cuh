@@ -299,7 +299,8 @@ __device__ __forceinline__ void run_shape_epi(float (&x)[16], const EpiConsts& e
                                               bool row_ok) {
   if constexpr (SHAPE == kShapeSqStoreId) {
     epi_round_ct<true>(x, e.q[0]);
-    sts128(tile_addr(io, e.slot_out[0], cl), epi_pack(x, e.q[1]));  // T-domain: bits as is
+    epi_round(x, e.q[1]);  // k = 1 store: at most a clamp in the T-domain
+    sts128(tile_addr(io, e.slot_out[0], cl), epi_pack(x, e.q[1]));
     return;
   }
   if constexpr (SHAPE == kShapeAddForkId) {
@@ -315,7 +316,8 @@ __device__ __forceinline__ void run_shape_epi(float (&x)[16], const EpiConsts& e
       x[j] = __fmaf_rn(x[j], e.q[1].k, __fmaf_rn(C, e.ka, e.ka_off));
     }
     epi_round_ct<true>(x, e.q[1]);
-    const int4 packed = epi_pack(x, e.q[2]);  // q2 == q3 == identity on T-domain R1
+    epi_round(x, e.q[2]);                     // k = 1 store (q2 == q3): at most a clamp
+    const int4 packed = epi_pack(x, e.q[2]);
     sts128(tile_addr(io, e.slot_out[0], cl), packed);
     sts128(tile_addr(io, e.slot_out[1], cl), packed);
     return;
