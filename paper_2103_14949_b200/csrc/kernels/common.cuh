@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #include "kernels.h"
 
@@ -13,6 +14,33 @@ namespace quantc::kern {
 
 #define QC_CUDA_CHECK_LAUNCH() ::quantc::kern::check_launch(__FILE__, __LINE__)
 void check_launch(const char* file, int line);
+
+// ---- programmatic dependent launch (PDL) -----------------------------------
+// Engine kernels are launched with programmatic stream serialisation: a
+// kernel may start (prologue: barriers, TMEM, tables) while its predecessor's
+// last CTAs drain.  Every PDL kernel calls pdl_wait() before touching data a
+// predecessor produced and before it can complete, so completion stays
+// transitive along the stream.  QUANTC_NO_PDL=1 launches them plainly.
+bool pdl_enabled();
+
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 inline int grid_for(int64_t n, int block, int max_blocks = 148 * 16) {
   int64_t g = (n + block - 1) / block;

@@ -284,6 +284,10 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // prologue done (it read only constants: tables, bias, weights' geometry):
+  // let the next kernel start its own, then wait for our predecessor's data
+  pdl_trigger();
+  pdl_wait();
 
   if (warp >= EPI_WARPS && warp < MMA_WARP) {
     // ================= producers =================
@@ -829,16 +833,16 @@ void launch_tc(const CUtensorMap* maps, TcArgs a, cudaStream_t s) {
       cudaFuncSetAttribute(tc_conv_kernel<BN, SHAPE, 8>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
     });
-    tc_conv_kernel<BN, SHAPE, 8><<<grid, Layout<8>::THREADS, smem, s>>>(
-        maps[0], maps[1], maps[2], maps[3], maps[4], a);
+    launch_pdl(tc_conv_kernel<BN, SHAPE, 8>, dim3(grid), dim3(Layout<8>::THREADS), smem, s,
+               maps[0], maps[1], maps[2], maps[3], maps[4], a);
   } else {
     static std::once_flag once;
     std::call_once(once, [&] {
       cudaFuncSetAttribute(tc_conv_kernel<BN, SHAPE, EPIW_TMA>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
     });
-    tc_conv_kernel<BN, SHAPE, EPIW_TMA><<<grid, Layout<EPIW_TMA>::THREADS, smem, s>>>(
-        maps[0], maps[1], maps[2], maps[3], maps[4], a);
+    launch_pdl(tc_conv_kernel<BN, SHAPE, EPIW_TMA>, dim3(grid), dim3(Layout<EPIW_TMA>::THREADS),
+               smem, s, maps[0], maps[1], maps[2], maps[3], maps[4], a);
   }
   QC_CUDA_CHECK_LAUNCH();
 }

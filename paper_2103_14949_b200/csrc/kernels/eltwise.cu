@@ -86,6 +86,8 @@ __global__ void gap_kernel(const float* __restrict__ x, float* __restrict__ y, i
 
 __global__ void __launch_bounds__(256) argmax_kernel(const float* __restrict__ x, int64_t cols,
                                                      int64_t* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const float* row = x + static_cast<int64_t>(blockIdx.x) * cols;
   float bv = -FLT_MAX;
   int64_t bi = -1;
@@ -123,6 +125,8 @@ __global__ void __launch_bounds__(256) argmax_kernel(const float* __restrict__ x
 
 __global__ void count_equal_kernel(const int64_t* a, const int64_t* b, int n,
                                    unsigned long long* count) {
+  pdl_trigger();
+  pdl_wait();
   unsigned int mine = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     mine += a[i] == b[i];
@@ -169,14 +173,14 @@ void gap_f32(const float* x, float* y, int NC, int HW, cudaStream_t s) {
 
 void argmax_rows(const float* x, int rows, int64_t cols, int64_t* out, cudaStream_t s) {
   if (rows <= 0) return;
-  argmax_kernel<<<rows, 256, 0, s>>>(x, cols, out);
+  launch_pdl(argmax_kernel, dim3(rows), dim3(256), 0, s, x, cols, out);
   QC_CUDA_CHECK_LAUNCH();
 }
 
 void count_equal(const int64_t* a, const int64_t* b, int n, unsigned long long* count,
                  cudaStream_t s) {
   if (n <= 0) return;
-  count_equal_kernel<<<grid_for(n, 256, 64), 256, 0, s>>>(a, b, n, count);
+  launch_pdl(count_equal_kernel, dim3(grid_for(n, 256, 64)), dim3(256), 0, s, a, b, n, count);
   QC_CUDA_CHECK_LAUNCH();
 }
 

@@ -4,6 +4,7 @@
 // vector loads/stores, grid sized as a multiple of the 148 SMs, grid-stride.
 // Math is IEEE-double exactly as the reference (see sq_value in common.cuh).
 #include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -11,6 +12,11 @@
 #include "quantc/device.hpp"
 
 namespace quantc::kern {
+
+bool pdl_enabled() {
+  static const bool on = std::getenv("QUANTC_NO_PDL") == nullptr;
+  return on;
+}
 
 void check_launch(const char* file, int line) {
   ++quantc::device::counters().kernel_launches;

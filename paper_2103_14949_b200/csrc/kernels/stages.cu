@@ -16,6 +16,8 @@ namespace {
 
 // one thread per (m, 16-channel group); reads NCHW (strided by HW)
 __global__ void input_kernel(const float* __restrict__ x, int N, int C, int HW, ProgArgs prog) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ StageTables T;
   load_tables(&T, prog.tables);
   __syncthreads();
@@ -40,6 +42,8 @@ __global__ void input_kernel(const float* __restrict__ x, int N, int C, int HW, 
 __global__ void maxpool_codes_kernel(const int8_t* __restrict__ x, int ld, float scale, int N,
                                      int C, int H, int W, int OH, int OW, int kh, int kw, int sh,
                                      int sw, int ph, int pw, ProgArgs prog) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ StageTables T;
   load_tables(&T, prog.tables);
   __syncthreads();
@@ -92,6 +96,8 @@ __global__ void maxpool_codes_kernel(const int8_t* __restrict__ x, int ld, float
 // across c), then the stage program on that one value
 __global__ void gap_rows_kernel(const float* __restrict__ x, int64_t ld, int N, int C, int HW,
                                 ProgArgs prog) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ StageTables T;
   load_tables(&T, prog.tables);
   __syncthreads();
@@ -114,6 +120,8 @@ template <int NOUT>
 __global__ void maxpool_stores_kernel(const int8_t* __restrict__ x, int ld, int N, int C, int H,
                                       int W, int OH, int OW, int kh, int kw, int sh, int sw, int ph,
                                       int pw, PoolStores e) {
+  pdl_trigger();
+  pdl_wait();
   const int groups = C / 16;
   const int64_t total = static_cast<int64_t>(N) * OH * OW * groups;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -149,6 +157,8 @@ __global__ void maxpool_stores_kernel(const int8_t* __restrict__ x, int ld, int 
 }
 
 __global__ void ew_kernel(ProgBuf src, int64_t M, int C, ProgArgs prog) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ StageTables T;
   load_tables(&T, prog.tables);
   __syncthreads();
@@ -168,6 +178,8 @@ __global__ void ew_kernel(ProgBuf src, int64_t M, int C, ProgArgs prog) {
 
 __global__ void weight_codes_v2_kernel(const float* __restrict__ w, int8_t* __restrict__ codes,
                                        int O, int C, int taps, int ldk, int Kpad, FSq p) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t total = static_cast<int64_t>(O) * Kpad;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -187,6 +199,8 @@ __global__ void weight_codes_v2_kernel(const float* __restrict__ w, int8_t* __re
 // thread per 2x2 pixel block, its 4*C codes (zero-padded to 16) as one store
 __global__ void input_s2d_kernel(const float* __restrict__ x, int N, int C, int H, int W, int H2,
                                  int W2, FSq p, int8_t* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t total = static_cast<int64_t>(N) * H2 * W2;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -224,6 +238,8 @@ __global__ void input_s2d_kernel(const float* __restrict__ x, int N, int C, int 
 __global__ void weight_codes_s2d_kernel(const float* __restrict__ w, int8_t* __restrict__ codes,
                                         int O, int C, int KH, int KW, int KH2, int KW2, int dh,
                                         int dw, int Kpad, FSq p) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t total = static_cast<int64_t>(O) * Kpad;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -249,6 +265,8 @@ __global__ void weight_codes_s2d_kernel(const float* __restrict__ w, int8_t* __r
 __global__ void pack_im2col_kernel(const int8_t* __restrict__ x, int8_t* __restrict__ out, int N,
                                    int H, int W, int C, int ld, int KH, int KW, int sh, int sw,
                                    int ph, int pw, int OH, int OW, int Ktrue, int Kpad) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t rows = static_cast<int64_t>(N) * OH * OW;
   for (int64_t m = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; m < rows;
        m += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -290,7 +308,7 @@ void pack_im2col(const int8_t* x, int8_t* out, int N, int H, int W, int C, int l
                  cudaStream_t s) {
   const int64_t total = static_cast<int64_t>(N) * OH * OW;
   if (total <= 0) return;
-  pack_im2col_kernel<<<grid_for(total, 128, 148 * 32), 128, 0, s>>>(x, out, N, H, W, C, ld, KH, KW,
+  launch_pdl(pack_im2col_kernel, dim3(grid_for(total, 128, 148 * 32)), dim3(128), 0, s, x, out, N, H, W, C, ld, KH, KW,
                                                                      sh, sw, ph, pw, OH, OW, Ktrue,
                                                                      Kpad);
   QC_CUDA_CHECK_LAUNCH();
@@ -301,7 +319,7 @@ void stage_input_s2d(const float* x, int N, int C, int H, int W, const FSq& p, i
   const int H2 = (H + 1) / 2, W2 = (W + 1) / 2;
   const int64_t total = static_cast<int64_t>(N) * H2 * W2;
   if (total <= 0) return;
-  input_s2d_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, N, C, H, W, H2, W2, p, out);
+  launch_pdl(input_s2d_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, x, N, C, H, W, H2, W2, p, out);
   QC_CUDA_CHECK_LAUNCH();
 }
 
@@ -309,7 +327,7 @@ void weight_codes_s2d(const float* w, int8_t* codes, int O, int C, int KH, int K
                       int KW2, int dh, int dw, int Kpad, const FSq& p, cudaStream_t s) {
   const int64_t total = static_cast<int64_t>(O) * Kpad;
   if (total <= 0) return;
-  weight_codes_s2d_kernel<<<grid_for(total, 256), 256, 0, s>>>(w, codes, O, C, KH, KW, KH2, KW2,
+  launch_pdl(weight_codes_s2d_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, w, codes, O, C, KH, KW, KH2, KW2,
                                                                 dh, dw, Kpad, p);
   QC_CUDA_CHECK_LAUNCH();
 }
@@ -317,7 +335,7 @@ void weight_codes_s2d(const float* w, int8_t* codes, int O, int C, int KH, int K
 void stage_input(const float* x, int N, int C, int HW, const ProgArgs& prog, cudaStream_t s) {
   const int64_t total = static_cast<int64_t>(N) * HW * ((C + 15) / 16);
   if (total <= 0) return;
-  input_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, N, C, HW, prog);
+  launch_pdl(input_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, x, N, C, HW, prog);
   QC_CUDA_CHECK_LAUNCH();
 }
 
@@ -326,7 +344,7 @@ void stage_maxpool(const int8_t* x, int ld, float scale, int N, int C, int H, in
                    cudaStream_t s) {
   const int64_t total = static_cast<int64_t>(N) * OH * OW * ((C + 15) / 16);
   if (total <= 0) return;
-  maxpool_codes_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, ld, scale, N, C, H, W, OH, OW, kh,
+  launch_pdl(maxpool_codes_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, x, ld, scale, N, C, H, W, OH, OW, kh,
                                                             kw, sh, sw, ph, pw, prog);
   QC_CUDA_CHECK_LAUNCH();
 }
@@ -335,7 +353,7 @@ void stage_gap(const float* x, int64_t ld, int N, int C, int HW, const ProgArgs&
                cudaStream_t s) {
   const int64_t total = static_cast<int64_t>(N) * C;
   if (total <= 0) return;
-  gap_rows_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, ld, N, C, HW, prog);
+  launch_pdl(gap_rows_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, x, ld, N, C, HW, prog);
   QC_CUDA_CHECK_LAUNCH();
 }
 
@@ -345,10 +363,10 @@ void stage_maxpool_stores(const int8_t* x, int ld, int N, int C, int H, int W, i
   const int64_t total = static_cast<int64_t>(N) * OH * OW * (C / 16);
   if (total <= 0) return;
   if (e.n_out == 2) {
-    maxpool_stores_kernel<2><<<grid_for(total, 256), 256, 0, s>>>(x, ld, N, C, H, W, OH, OW, kh,
+    launch_pdl(maxpool_stores_kernel<2>, dim3(grid_for(total, 256)), dim3(256), 0, s, x, ld, N, C, H, W, OH, OW, kh,
                                                                   kw, sh, sw, ph, pw, e);
   } else {
-    maxpool_stores_kernel<1><<<grid_for(total, 256), 256, 0, s>>>(x, ld, N, C, H, W, OH, OW, kh,
+    launch_pdl(maxpool_stores_kernel<1>, dim3(grid_for(total, 256)), dim3(256), 0, s, x, ld, N, C, H, W, OH, OW, kh,
                                                                   kw, sh, sw, ph, pw, e);
   }
   QC_CUDA_CHECK_LAUNCH();
@@ -357,7 +375,7 @@ void stage_maxpool_stores(const int8_t* x, int ld, int N, int C, int H, int W, i
 void stage_ew(const ProgBuf& src, int64_t M, int C, const ProgArgs& prog, cudaStream_t s) {
   const int64_t total = M * ((C + 15) / 16);
   if (total <= 0) return;
-  ew_kernel<<<grid_for(total, 256), 256, 0, s>>>(src, M, C, prog);
+  launch_pdl(ew_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, src, M, C, prog);
   QC_CUDA_CHECK_LAUNCH();
 }
 
@@ -365,7 +383,7 @@ void weight_codes_v2(const float* w, int8_t* codes, int O, int C, int taps, int 
                      const FSq& p, cudaStream_t s) {
   const int64_t total = static_cast<int64_t>(O) * Kpad;
   if (total <= 0) return;
-  weight_codes_v2_kernel<<<grid_for(total, 256), 256, 0, s>>>(w, codes, O, C, taps, ldk, Kpad, p);
+  launch_pdl(weight_codes_v2_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, w, codes, O, C, taps, ldk, Kpad, p);
   QC_CUDA_CHECK_LAUNCH();
 }
 
