@@ -1216,7 +1216,9 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
         auto ck = std::make_pair(static_cast<int>(si), key);
         auto it = wcache_.find(ck);
         if (it == wcache_.end()) {
-          auto codes = engine::device_alloc(static_cast<size_t>(st.O) * st.Kpad);
+          // codes [O][Kpad], then one int: max_o sum_k |code| (the accumulator bound)
+          const size_t cbytes = static_cast<size_t>(st.O) * st.Kpad;
+          auto codes = engine::device_alloc(cbytes + 16);
           if (st.s2d) {
             kern::weight_codes_s2d(plan_.constant(st.w_const).f(), static_cast<int8_t*>(codes.get()),
                                    st.O, st.s2d_C, st.s2d_KH, st.s2d_KW, st.KH, st.KW, st.s2d_dh,
@@ -1227,6 +1229,9 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
                                   st.dense ? (st.taps > 1 ? dv.cs : dv.C) : st.C, st.taps, st.ldk,
                                   st.Kpad, wf, S());
           }
+          int* l1 = reinterpret_cast<int*>(static_cast<int8_t*>(codes.get()) + cbytes);
+          ok_cuda(cudaMemsetAsync(l1, 0, sizeof(int), S()));
+          kern::weight_l1_max(static_cast<const int8_t*>(codes.get()), st.O, st.Kpad, l1, S());
           it = wcache_.emplace(ck, codes).first;
         }
         kern::TcConvSpec sp{};
@@ -1239,6 +1244,9 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
                             st.pw, st.OH, st.OW, st.Ktrue, st.Kpad, S());
         }
         sp.w = static_cast<const int8_t*>(it->second.get());
+        sp.w_l1 = reinterpret_cast<const int*>(sp.w + static_cast<size_t>(st.O) * st.Kpad);
+        sp.x_absmax = static_cast<int>(
+            code_absmax(fsq[static_cast<size_t>(sq_index_.at(dv.sq_step))]));
         sp.M = st.rows_out_ps * batch;
         sp.O = st.O;
         sp.Kpad = st.Kpad;

@@ -169,6 +169,8 @@ struct TcArgs {
   double scale;
   float scale_f;  // scale as fp32 when exactly representable (normal), else 0
   int always_small;  // |acc| <= 2^24 guaranteed for this layer
+  const int* w_l1;   // device bound on the weights' row L1 norm (may be null)
+  int x_absmax;      // max |input code|
   ProgArgs prog;
   int m_tiles, n_tiles;
   EpiConsts epi;
@@ -288,6 +290,9 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
   // let the next kernel start its own, then wait for our predecessor's data
   pdl_trigger();
   pdl_wait();
+  // |acc| <= L1(w) * max|x| <= 2^24: I2F is exact and the conversion pipe is idle
+  const bool acc_small = args.w_l1 != nullptr &&
+                         static_cast<int64_t>(__ldg(args.w_l1)) * args.x_absmax <= (1 << 24);
 
   if (warp >= EPI_WARPS && warp < MMA_WARP) {
     // ================= producers =================
@@ -515,14 +520,17 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
           tmem_ld<EW>(tbase + c0, d);
           tmem_wait(d);
           const int n = n0 + c0;
-          // acc -> float without the conversion pipe: bits(0x4B400000 + a) is
-          // the float M + a for |a| < 2^22 (checked for the whole chunk)
+          // acc -> float: I2F when the layer's bound proves |acc| <= 2^24;
+          // otherwise bits(0x4B400000 + a) = the float M + a for |a| < 2^22
+          // (checked for the whole chunk) and a double path beyond
           uint32_t u[EW];
           uint32_t chk = 0;
+          if (!acc_small) {
 #pragma unroll
-          for (int j = 0; j < EW; ++j) {
-            u[j] = d[j] + 0x4B400000u;
-            chk |= u[j] ^ 0x4B000000u;
+            for (int j = 0; j < EW; ++j) {
+              u[j] = d[j] + 0x4B400000u;
+              chk |= u[j] ^ 0x4B000000u;
+            }
           }
           if (n < args.N) {
             float x[EW];
@@ -535,7 +543,12 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
               bs[j + 2] = __int_as_float(b4.z);
               bs[j + 3] = __int_as_float(b4.w);
             }
-            if (chk < 0x800000u) {
+            if (acc_small) {
+#pragma unroll
+              for (int j = 0; j < EW; ++j) {
+                x[j] = __fmaf_rn(static_cast<float>(static_cast<int32_t>(d[j])), e.q[0].k, bs[j]);
+              }
+            } else if (chk < 0x800000u) {
               // x0 = (a*s + b)/s0 = fma(a, s/s0, b/s0): a*s/s0 exact, one
               // rounding == the reference's RN24(RN53(a*s + b)) scaled by 2^k
 #pragma unroll
@@ -900,6 +913,8 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
   a.prog = sp.prog;
   a.epi = sp.epi;
   a.always_small = sp.acc_bound <= static_cast<double>(1 << 24) ? 1 : 0;
+  a.w_l1 = sp.w_l1;
+  a.x_absmax = sp.x_absmax;
   a.m_tiles = static_cast<int>((sp.M + BM - 1) / BM);
   a.bkb = BK;
   CUtensorMap maps[5];

@@ -135,6 +135,10 @@ struct TcConvSpec {
   int res_cols;
   int64_t res_ld;
   double acc_bound;  // host bound on |sum_k a*b| (K * max|qa| * max|qb|)
+  // device bound on |sum_k a*b|: max_o sum_k |w_code[o][k]| (weight_l1_max),
+  // times the input codes' max |q|; <= 2^24 lets the epilogue convert with I2F
+  const int* w_l1;
+  int x_absmax;
   EpiConsts epi;     // shape kernels (prog.shape != 0): host-folded constants
 };
 void tc_conv(const TcConvSpec& spec, cudaStream_t s);
@@ -152,6 +156,8 @@ void stage_input_s2d(const float* x, int N, int C, int H, int W, const FSq& p, i
 // (KH2 x KW2 taps of 16 channels; original tap = 2*ka + dy - dh, 2*kb + dx - dw)
 void weight_codes_s2d(const float* w, int8_t* codes, int O, int C, int KH, int KW, int KH2,
                       int KW2, int dh, int dw, int Kpad, const FSq& p, cudaStream_t s);
+// out = max over rows of sum_k |codes[o][k]| (out zeroed by the caller)
+void weight_l1_max(const int8_t* codes, int O, int Kpad, int* out, cudaStream_t s);
 // graph input NCHW fp32 -> program over (m = n*H*W + hw, c)
 void stage_input(const float* x, int N, int C, int HW, const ProgArgs& prog, cudaStream_t s);
 // max_pool2d over NHWC codes (value = code * scale) -> program

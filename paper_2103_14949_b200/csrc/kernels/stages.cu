@@ -260,6 +260,23 @@ __global__ void weight_codes_s2d_kernel(const float* __restrict__ w, int8_t* __r
   }
 }
 
+// one warp per weight row: sum |code| with byte SIMD, max over rows
+__global__ void weight_l1_kernel(const int8_t* __restrict__ codes, int O, int Kpad,
+                                 int* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int o = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; o < O; o += warps) {
+    const uint32_t* row = reinterpret_cast<const uint32_t*>(codes + static_cast<int64_t>(o) * Kpad);
+    uint32_t acc = 0;
+    for (int i = lane; i < Kpad / 4; i += 32) acc += __vsadu4(__vabsss4(row[i]), 0u);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+    if (lane == 0) atomicMax(out, static_cast<int>(acc));
+  }
+}
+
 // one thread per output row: walks (kh, kw, c) with incremental counters and
 // emits the row as 16-byte stores
 __global__ void pack_im2col_kernel(const int8_t* __restrict__ x, int8_t* __restrict__ out, int N,
@@ -311,6 +328,12 @@ void pack_im2col(const int8_t* x, int8_t* out, int N, int H, int W, int C, int l
   launch_pdl(pack_im2col_kernel, dim3(grid_for(total, 128, 148 * 32)), dim3(128), 0, s, x, out, N, H, W, C, ld, KH, KW,
                                                                      sh, sw, ph, pw, OH, OW, Ktrue,
                                                                      Kpad);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+void weight_l1_max(const int8_t* codes, int O, int Kpad, int* out, cudaStream_t s) {
+  if (O <= 0) return;
+  launch_pdl(weight_l1_kernel, dim3((O + 7) / 8), dim3(256), 0, s, codes, O, Kpad, out);
   QC_CUDA_CHECK_LAUNCH();
 }
 
