@@ -51,7 +51,7 @@ constexpr int MAX_STAGES = 8;
 template <int EPIW>
 struct Layout {
   static constexpr int EPI_WARPS = EPIW;
-  static constexpr int PROD_WARPS = EPIW == 8 ? 4 : 1;
+  static constexpr int PROD_WARPS = EPIW == 16 ? 1 : 4;
   static constexpr int MMA_WARP = EPI_WARPS + PROD_WARPS;
   static constexpr int THREADS = (MMA_WARP + 1) * 32;
   static constexpr int PARTS = EPIW / 4;  // column parts per lane quarter
@@ -61,6 +61,7 @@ constexpr int SMEM_LIMIT = 227 * 1024;
 #define QC_EPIW_TMA 16
 #endif
 constexpr int EPIW_TMA = QC_EPIW_TMA;  // epilogue warps of TMA-fed launches
+constexpr int EPIW_GATHER = 12;        // ... and of cp.async-gather launches (+4 producer warps)
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -839,14 +840,14 @@ void launch_tc(const CUtensorMap* maps, TcArgs a, cudaStream_t s) {
   const int grid = tiles < num_sms() ? tiles : num_sms();
   // the cp.async gather needs 4 producer warps (one thread per A row); TMA
   // producers need one thread, which leaves room for 12 epilogue warps
-  static const bool epi8 = std::getenv("QUANTC_EPI8") != nullptr;
-  if (a.gather == 1 || epi8) {
+  static const bool all_gather_layout = std::getenv("QUANTC_GATHER_LAYOUT") != nullptr;
+  if (a.gather == 1 || all_gather_layout) {
     static std::once_flag once;
     std::call_once(once, [&] {
-      cudaFuncSetAttribute(tc_conv_kernel<BN, SHAPE, 8>,
+      cudaFuncSetAttribute(tc_conv_kernel<BN, SHAPE, EPIW_GATHER>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
     });
-    launch_pdl(tc_conv_kernel<BN, SHAPE, 8>, dim3(grid), dim3(Layout<8>::THREADS), smem, s,
+    launch_pdl(tc_conv_kernel<BN, SHAPE, EPIW_GATHER>, dim3(grid), dim3(Layout<EPIW_GATHER>::THREADS), smem, s,
                maps[0], maps[1], maps[2], maps[3], maps[4], a);
   } else {
     static std::once_flag once;
