@@ -53,7 +53,8 @@ struct Layout {
   static constexpr int EPI_WARPS = EPIW;
   static constexpr int PROD_WARPS = EPIW == 16 ? 1 : 4;
   static constexpr int MMA_WARP = EPI_WARPS + PROD_WARPS;
-  static constexpr int THREADS = (MMA_WARP + 1) * 32;
+  static constexpr int STORE_WARP = MMA_WARP + 1;  // TMA stores / residual loads / drains
+  static constexpr int THREADS = (STORE_WARP + 1) * 32;
   static constexpr int PARTS = EPIW / 4;  // column parts per lane quarter
 };
 constexpr int SMEM_LIMIT = 227 * 1024;
@@ -116,10 +117,6 @@ __device__ __forceinline__ void tma_store2d(const CUtensorMap* m, const void* sr
           reinterpret_cast<uint64_t>(m)),
       "r"(su32(src)), "r"(c0), "r"(c1)
       : "memory");
-}
-template <int EPIW>
-__device__ __forceinline__ void epi_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(EPIW * 32) : "memory");
 }
 // K-major smem operand descriptor, rows of `sw` bytes swizzled in 8-row atoms:
 // sw = 128 -> layout SWIZZLE_128B (2), sw = 64 -> SWIZZLE_64B (4); SBO = 8 rows
@@ -218,6 +215,7 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
   constexpr int EPI_WARPS = Layout<EPIW>::EPI_WARPS;
   constexpr int PROD_WARPS = Layout<EPIW>::PROD_WARPS;
   constexpr int MMA_WARP = Layout<EPIW>::MMA_WARP;
+  constexpr int STORE_WARP = Layout<EPIW>::STORE_WARP;
   constexpr int PARTS = Layout<EPIW>::PARTS;
   constexpr int NCHUNK = BN / 16;
   const int stages = args.stages;
@@ -233,8 +231,10 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
   uint64_t* empty = full + MAX_STAGES;
   uint64_t* tfull = empty + MAX_STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* rfull = tempty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 2);  // rfull[2]: one per slot set
+  uint64_t* rfull = tempty + 2;   // [2] residual of a slot set landed
+  uint64_t* sfull = rfull + 2;    // [2] epilogue warps wrote a slot set
+  uint64_t* sfree = sfull + 2;    // [2] a slot set's stores drained (reusable)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfree + 2);
   StageTables* tabs = reinterpret_cast<StageTables*>(tmem_slot + 4);
   // gather K-chunk table: chunk q (16 bytes of K) = channel run c..c+15 of tap
   // (kh, kw); x = byte offset from the row's (ih0, iw0) pixel, y = tap index
@@ -273,8 +273,11 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
       bar_init(&tfull[a], 1);
       bar_init(&tempty[a], EPI_WARPS * 32);
     }
-    bar_init(&rfull[0], 1);
-    bar_init(&rfull[1], 1);
+    for (int a = 0; a < 2; ++a) {
+      bar_init(&rfull[a], 1);
+      bar_init(&sfull[a], EPI_WARPS);  // one arrival per epilogue warp
+      bar_init(&sfree[a], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == MMA_WARP) {
@@ -458,47 +461,68 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
         commit(&tfull[acc]);
       }
     }
+  } else if (warp == STORE_WARP) {
+    // ================= stores / residual prefetch =================
+    // per tile: wait for the epilogue warps' slot writes, TMA-store the code
+    // outputs, prefetch the residual of the tile that will reuse this set,
+    // drain the stores' smem reads and free the set
+    if (lane == 0 && (args.n_out > 0 || args.has_res)) {
+      const int nsets = args.dbuf ? 2 : 1;
+      auto load_res = [&](int t, int set) {
+        const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
+        uint8_t* dst = slots + set * SET_BYTES + args.n_out * SLOT_BYTES;
+        bar_expect(&rfull[set], SLOT_BYTES);
+        for (int blk = 0; blk < BN / SWZ; ++blk) {
+          tma2d(&map_r, &rfull[set], dst + blk * (BM * SWZ), n0 + blk * SWZ, m0);
+        }
+      };
+      if (args.has_res) {
+        for (int k = 0; k < nsets; ++k) {
+          const int t = static_cast<int>(blockIdx.x) + k * static_cast<int>(gridDim.x);
+          if (t < n_tiles_total) load_res(t, k);
+        }
+      }
+      uint32_t tl = 0;
+      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
+        const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
+        const int set = args.dbuf ? static_cast<int>(tl & 1) : 0;
+        const uint32_t use = args.dbuf ? (tl >> 1) : tl;
+        bar_wait(&sfull[set], use & 1);
+        uint8_t* base = slots + set * SET_BYTES;
+        if (args.n_out > 0) {
+          for (int blk = 0; blk < BN / SWZ; ++blk) {
+            tma_store2d(&map_o0, base + blk * (BM * SWZ), n0 + blk * SWZ, m0);
+            if (args.n_out > 1) {
+              tma_store2d(&map_o1, base + SLOT_BYTES + blk * (BM * SWZ), n0 + blk * SWZ, m0);
+            }
+          }
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        if (args.has_res) {
+          const int t2 = t + nsets * static_cast<int>(gridDim.x);
+          if (t2 < n_tiles_total) load_res(t2, set);
+        }
+        if (args.n_out > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        bar_arrive(&sfree[set]);
+      }
+      if (args.n_out > 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
   } else {
     // ================= epilogue =================
     const int quarter = warp & 3;
     const int part = warp >> 2;  // this warp's chunks: part, part + PARTS, ...
     const int r = quarter * 32 + lane;
-    const bool leader = threadIdx.x == 0;
-    // slot set of the tile with local index tl
-    auto set_of = [&](uint32_t tl) -> uint8_t* { return slots + (args.dbuf ? (tl & 1) : 0) * SET_BYTES; };
-    auto load_res = [&](int t, uint32_t tl) {
-      const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
-      uint8_t* dst = set_of(tl) + args.n_out * SLOT_BYTES;
-      uint64_t* bar = &rfull[args.dbuf ? (tl & 1) : 0];
-      bar_expect(bar, SLOT_BYTES);
-      for (int blk = 0; blk < BN / SWZ; ++blk) {
-        tma2d(&map_r, bar, dst + blk * (BM * SWZ), n0 + blk * SWZ, m0);
-      }
-    };
-    if (args.has_res && leader && static_cast<int>(blockIdx.x) < n_tiles_total) load_res(blockIdx.x, 0);
     uint32_t tl = 0;
     for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
       const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
       const uint32_t acc = tl & 1;
-      TileIo io{su32(set_of(tl)), r, static_cast<int>(SLOT_BYTES), SWZ};
+      const int set = args.dbuf ? static_cast<int>(tl & 1) : 0;
+      const uint32_t use = args.dbuf ? (tl >> 1) : tl;  // k-th use of this slot set
+      TileIo io{su32(slots + set * SET_BYTES), r, static_cast<int>(SLOT_BYTES), SWZ};
       bar_wait(&tfull[acc], (tl / 2) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (args.dbuf && args.has_res && leader && t + static_cast<int>(gridDim.x) < n_tiles_total) {
-        // next tile's residual into the other set (its last reader, tile tl-1, is done)
-        load_res(t + gridDim.x, tl + 1);
-      }
-      if (args.n_out > 0) {
-        // this set's previous TMA stores must have finished reading it: the
-        // latest tile's group may still run when the sets alternate
-        if (leader) {
-          if (args.dbuf) {
-            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          } else {
-            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-          }
-        }
-        epi_sync<EPIW>();
-      }
+      // this set's previous TMA stores must have finished reading it
+      if (args.n_out > 0 && use >= 1) bar_wait(&sfree[set], (use - 1) & 1);
       if (args.has_res) {
         if (args.dbuf) {
           bar_wait(&rfull[tl & 1], (tl >> 1) & 1);
@@ -621,27 +645,16 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
           run_prog<EW, 3>(v, m, n, nvalid, *tabs, &io, c0);
         }
       }
-      // publish slot writes to the async proxy, release TMEM, store the tile
+      // publish slot writes to the async proxy, release TMEM, hand the set to
+      // the store warp (no CTA-wide barrier: one arrival per warp)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       bar_arrive(&tempty[acc]);
-      if (args.n_out > 0 || args.has_res) epi_sync<EPIW>();
-      if (leader) {
-        if (args.n_out > 0) {
-          for (int blk = 0; blk < BN / SWZ; ++blk) {
-            tma_store2d(&map_o0, set_of(tl) + blk * (BM * SWZ), n0 + blk * SWZ, m0);
-            if (args.n_out > 1) {
-              tma_store2d(&map_o1, set_of(tl) + SLOT_BYTES + blk * (BM * SWZ), n0 + blk * SWZ, m0);
-            }
-          }
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
-        if (!args.dbuf && args.has_res && t + static_cast<int>(gridDim.x) < n_tiles_total) {
-          load_res(t + gridDim.x, tl + 1);
-        }
+      if (args.n_out > 0 || args.has_res) {
+        __syncwarp();
+        if (lane == 0) bar_arrive(&sfull[set]);
       }
     }
-    if (leader && args.n_out > 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   __syncthreads();
   if (warp == MMA_WARP) {
@@ -805,7 +818,7 @@ int num_sms() {
 
 // shared memory of one CTA: everything but the pipeline stages
 int smem_fixed(const TcArgs& a, int bn, int sets, bool shape) {
-  return 1024 + sets * (a.n_out + a.has_res) * BM * bn + (2 * MAX_STAGES + 6) * 8 + 16 +
+  return 1024 + sets * (a.n_out + a.has_res) * BM * bn + (2 * MAX_STAGES + 10) * 8 + 16 +
          static_cast<int>(sizeof(StageTables)) + 64 +
          (a.gather == 1 ? a.K / 16 * static_cast<int>(sizeof(int2)) : 0) +
          (shape ? ((a.N + bn - 1) / bn) * bn * 4 : 0);
