@@ -950,7 +950,17 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
   // layer with few M tiles (late stages at small batch) would otherwise
   // leave most SMs idle
   int BN = tc_conv_bn(sp.O);
-  while (BN > 64 && 2 * a.m_tiles * ((sp.O + BN - 1) / BN) <= num_sms()) BN /= 2;
+  {
+    // at least `per_sm` tiles per SM where possible: with one tile per CTA the
+    // operand loads, MMAs and epilogue of that tile run in series; several
+    // tiles per CTA overlap them through the double-buffered accumulator
+    static const int per_sm = [] {
+      const char* e = std::getenv("QUANTC_TILES_PER_SM");
+      return e ? std::atoi(e) : 1;
+    }();
+    const int want = per_sm > 1 ? per_sm * num_sms() : num_sms() / 2;
+    while (BN > 64 && a.m_tiles * ((sp.O + BN - 1) / BN) < want) BN /= 2;
+  }
   // a wide tile whose slot sets cannot be double-buffered: halve it when the
   // narrower one can (per-tile store drains / residual loads then overlap)
   if (BN == 256 && !dbuf_fits(a, 256, sp.prog.shape != 0) && dbuf_fits(a, 128, sp.prog.shape != 0)) {
