@@ -93,6 +93,27 @@ __device__ __forceinline__ int bin_of(float v, double absmax, double bins_over_a
   return idx < 0 ? 0 : (idx > bins - 1 ? bins - 1 : idx);
 }
 
+// Same bin with an fp32 fast path: t_f = |v| * RN32(B/absmax) is within a few
+// ulp (relative 2^-21) of the reference's double t; when t_f is farther than
+// that from every integer, floor(t_f) = floor(t) and t is not an integer, so
+// the bin ceil(t) - 1 = floor(t_f).  floor(t_f) (t_f < 2^22) is the integer
+// bits of RZ(t_f + 1.5*2^23).  Near an integer (or for zeros / huge t) the
+// exact double bin_of decides.
+__device__ __forceinline__ int bin_of_fast(float v, float r_f, double absmax,
+                                           double bins_over_absmax, int bins) {
+  const float a = fabsf(v);
+  const float t = __fmul_rn(a, r_f);
+  const float T = __fadd_rz(t, 12582912.0f);
+  const float fl = __fsub_rn(T, 12582912.0f);
+  const float fr = __fsub_rn(t, fl);
+  const float margin = t * 0x1p-19f;
+  if (a > 0.0f && t < 4194304.0f && fr > margin && fr < 1.0f - margin) {
+    const int idx = __float_as_int(T) - 0x4B400000;
+    return idx > bins - 1 ? bins - 1 : idx;
+  }
+  return bin_of(v, absmax, bins_over_absmax, bins);
+}
+
 __global__ void __launch_bounds__(512) hist_kernel(const float* __restrict__ x, int64_t n,
                                                    double absmax, double bins_over_absmax,
                                                    int bins, unsigned long long* counts,
@@ -103,15 +124,16 @@ __global__ void __launch_bounds__(512) hist_kernel(const float* __restrict__ x, 
   const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   if (absmax > 0.0) {
+    const float r_f = static_cast<float>(bins_over_absmax);
     if ((reinterpret_cast<uintptr_t>(x) & 15) == 0) {
       const int64_t n4 = n >> 2;
       const float4* x4 = reinterpret_cast<const float4*>(x);
       for (int64_t i = tid; i < n4; i += stride) {
         float4 v = __ldg(x4 + i);
-        atomicAdd(&sh[bin_of(v.x, absmax, bins_over_absmax, bins)], 1u);
-        atomicAdd(&sh[bin_of(v.y, absmax, bins_over_absmax, bins)], 1u);
-        atomicAdd(&sh[bin_of(v.z, absmax, bins_over_absmax, bins)], 1u);
-        atomicAdd(&sh[bin_of(v.w, absmax, bins_over_absmax, bins)], 1u);
+        atomicAdd(&sh[bin_of_fast(v.x, r_f, absmax, bins_over_absmax, bins)], 1u);
+        atomicAdd(&sh[bin_of_fast(v.y, r_f, absmax, bins_over_absmax, bins)], 1u);
+        atomicAdd(&sh[bin_of_fast(v.z, r_f, absmax, bins_over_absmax, bins)], 1u);
+        atomicAdd(&sh[bin_of_fast(v.w, r_f, absmax, bins_over_absmax, bins)], 1u);
       }
       for (int64_t i = (n4 << 2) + tid; i < n; i += stride) {
         atomicAdd(&sh[bin_of(x[i], absmax, bins_over_absmax, bins)], 1u);

@@ -272,3 +272,19 @@ def test_fused_scores_bit_exact_vs_exact_engine(b200, cuda_lib, name, n):
         assert exact.shape == fused.shape
         assert exact.tobytes() == fused.tobytes(), (
             name, int((exact != fused).sum()), float(np.abs(exact - fused).max()))
+
+
+def test_histogram_bin_edges_exact(cuda_lib, port):
+    """Values on and one ulp around bin edges (the fp32 fast path defers
+    these to the exact double binning): counts equal the restatement's."""
+    rng = np.random.default_rng(31)
+    for absmax, bins in [(6.0, 2048), (3.7, 2048), (1.0, 100), (0.001, 7)]:
+        k = rng.integers(1, bins + 1, 20000)
+        edge = (k * (absmax / bins)).astype(np.float32)
+        x = np.concatenate([edge, np.nextafter(edge, np.float32(0)),
+                            np.nextafter(edge, np.float32(np.inf)), -edge,
+                            np.zeros(7, np.float32),
+                            rng.uniform(-absmax, absmax, 50000).astype(np.float32)])
+        x = np.clip(x, -absmax, absmax).astype(np.float32)
+        c = cuda_lib.histogram(torch.from_numpy(x).cuda(), float(absmax), bins).cpu().numpy()
+        np.testing.assert_array_equal(c, port.histogram(x, float(absmax), bins))
