@@ -37,7 +37,7 @@ class Staging {
   // pack `count` samples of `bytes_per` each via pack(sample, dst) and copy
   // them to dst_dev, chunk by chunk
   void upload(uint8_t* dst_dev, int64_t count, size_t bytes_per,
-              const std::function<void(int64_t, uint8_t*)>& pack) {
+              const std::function<void(int64_t, uint8_t*)>& pack, cudaStream_t us) {
     ensure();
     const int64_t per_chunk = std::max<int64_t>(1, static_cast<int64_t>(kChunk / bytes_per));
     int ci = 0;
@@ -50,15 +50,15 @@ class Staging {
         // one sample larger than a chunk: pageable path
         std::vector<uint8_t> tmp(bytes);
         for (int64_t s = 0; s < n; ++s) pack(s0 + s, tmp.data() + s * bytes_per);
-        check(cudaMemcpyAsync(dst_dev + s0 * bytes_per, tmp.data(), bytes, cudaMemcpyHostToDevice, S()));
-        check(cudaStreamSynchronize(S()));
+        check(cudaMemcpyAsync(dst_dev + s0 * bytes_per, tmp.data(), bytes, cudaMemcpyHostToDevice, us));
+        check(cudaStreamSynchronize(us));
         continue;
       }
       check(cudaEventSynchronize(ev_[slot]));  // DMA out of this buffer finished
       parallel_for(static_cast<size_t>(n), n >= 4 ? 8 : 1,
                    [&](size_t s) { pack(s0 + static_cast<int64_t>(s), buf + s * bytes_per); });
-      check(cudaMemcpyAsync(dst_dev + s0 * bytes_per, buf, bytes, cudaMemcpyHostToDevice, S()));
-      check(cudaEventRecord(ev_[slot], S()));
+      check(cudaMemcpyAsync(dst_dev + s0 * bytes_per, buf, bytes, cudaMemcpyHostToDevice, us));
+      check(cudaEventRecord(ev_[slot], us));
     }
   }
 
@@ -80,7 +80,9 @@ class Staging {
 };
 }  // namespace
 
-DeviceDataset::DeviceDataset(const Graph& g, const Dataset& ds, int64_t first, int64_t count) {
+DeviceDataset::DeviceDataset(const Graph& g, const Dataset& ds, int64_t first, int64_t count,
+                             void* upload) {
+  const cudaStream_t us = upload ? static_cast<cudaStream_t>(upload) : S();
   if (count < 0) count = static_cast<int64_t>(ds.size()) - first;
   n_ = count;
   const size_t n_in = g.inputs().size();
@@ -105,6 +107,14 @@ DeviceDataset::DeviceDataset(const Graph& g, const Dataset& ds, int64_t first, i
       }
     }
     auto buf = engine::device_alloc(static_cast<size_t>(per * count) * 4);
+    if (us != S()) {
+      // the buffer comes from the engine stream's pool: order the copies after it
+      cudaEvent_t alloc_done;
+      cudaEventCreateWithFlags(&alloc_done, cudaEventDisableTiming);
+      cudaEventRecord(alloc_done, S());
+      cudaStreamWaitEvent(us, alloc_done, 0);
+      cudaEventDestroy(alloc_done);
+    }
     if (per * count > 0) {
       Staging& st = Staging::get();
       std::lock_guard<std::mutex> lk(st.mu());
@@ -112,11 +122,85 @@ DeviceDataset::DeviceDataset(const Graph& g, const Dataset& ds, int64_t first, i
                 [&](int64_t s, uint8_t* dst) {
                   const Tensor& t = ds[static_cast<size_t>(first + s)].inputs[k];
                   std::memcpy(dst, t.floats().data(), static_cast<size_t>(per) * 4);
-                });
+                },
+                us);
     }
     bufs_.push_back(buf);
     per_.push_back(per);
   }
+  if (us != S()) {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    cudaEventRecord(e, us);
+    ready_ = e;
+  }
+}
+
+DeviceDataset::~DeviceDataset() {
+  if (ready_) {
+    // the buffers are freed on the engine stream; the copies must be done
+    cudaStreamWaitEvent(S(), static_cast<cudaEvent_t>(ready_), 0);
+    cudaEventDestroy(static_cast<cudaEvent_t>(ready_));
+  }
+}
+
+void DeviceDataset::wait_ready() const {
+  if (ready_) cudaStreamWaitEvent(S(), static_cast<cudaEvent_t>(ready_), 0);
+}
+
+namespace {
+// the fused int8 engine applies: the plan compiles and the binding is
+// eligible (power-of-two scales in auto mode => bit-identical)
+bool fused_ready(const engine::Plan& plan, const SimBinding* binding, bool integer_regime,
+                 bool allow_fast) {
+  const auto mode = device::engine_mode();
+  const char* fused_env = std::getenv("QUANTC_FUSED");
+  const bool fused_on = !(fused_env && std::string(fused_env) == "0");
+  if (!(allow_fast && !integer_regime && fused_on && mode != device::EngineMode::kExact &&
+        kern::gemm_s8_tcgen05_available())) {
+    return false;
+  }
+  if (!plan.fused_tried) {
+    plan.fused_tried = true;
+    plan.fused = std::make_shared<fast::FastPlan>(plan);
+  }
+  return plan.fused->ok() && plan.fused->eligible(binding, mode == device::EngineMode::kAuto);
+}
+}  // namespace
+
+std::shared_ptr<void> predict_streamed(const engine::Plan& plan, const Graph& g,
+                                       const Dataset& ds, const SimBinding* binding) {
+  static const int parts_env = [] {
+    const char* e = std::getenv("QUANTC_E2E_PARTS");
+    return e ? std::max(1, std::atoi(e)) : 0;
+  }();
+  const int64_t n = static_cast<int64_t>(ds.size());
+  if (!fused_ready(plan, binding, false, binding != nullptr)) {
+    DeviceDataset dd(g, ds);
+    return predict_device(plan, dd, binding, false, binding != nullptr);
+  }
+  // QUANTC_E2E_PARTS > 1 splits the call so part k+1's packing and DMA overlap
+  // the forward of part k.  Default 1: host packing into pinned staging is the
+  // bottleneck of this path, and each extra part repeats the per-launch host
+  // work (measured on B200: 2 parts -28%, 4 parts -55% at 64 images)
+  const int parts = parts_env ? parts_env : 1;
+  auto preds = engine::device_alloc(static_cast<size_t>(std::max<int64_t>(1, n)) * 8);
+  std::vector<std::unique_ptr<DeviceDataset>> dds;
+  const int64_t per = (n + parts - 1) / parts;
+  for (int64_t first = 0; first < n; first += per) {
+    const int64_t cnt = std::min(per, n - first);
+    dds.push_back(std::make_unique<DeviceDataset>(g, ds, first, cnt, device::copy_stream()));
+    const DeviceDataset& dd = *dds.back();
+    dd.wait_ready();
+    const int fb = static_cast<int>(std::min<int64_t>(cnt, 256));
+    for (int64_t f = 0; f < cnt; f += fb) {
+      const int b = static_cast<int>(std::min<int64_t>(fb, cnt - f));
+      std::vector<const float*> ins;
+      for (size_t k = 0; k < dd.num_inputs(); ++k) ins.push_back(dd.input(k, f));
+      plan.fused->predict(b, ins, binding, static_cast<int64_t*>(preds.get()) + first + f);
+    }
+  }
+  return preds;
 }
 
 std::shared_ptr<void> predict_device(const engine::Plan& plan, const DeviceDataset& dd,
@@ -129,17 +213,8 @@ std::shared_ptr<void> predict_device(const engine::Plan& plan, const DeviceDatas
   auto preds = engine::device_alloc(static_cast<size_t>(std::max<int64_t>(1, dd.size())) * 8);
   // engine v2: fused int8 dataflow, when the graph compiles and the binding is
   // eligible (power-of-two scales in auto mode => bit-identical)
-  const auto mode = device::engine_mode();
-  const char* fused_env = std::getenv("QUANTC_FUSED");
-  const bool fused_on = !(fused_env && std::string(fused_env) == "0");
-  if (allow_fast && !integer_regime && fused_on && mode != device::EngineMode::kExact &&
-      kern::gemm_s8_tcgen05_available()) {
-    if (!plan.fused_tried) {
-      plan.fused_tried = true;
-      plan.fused = std::make_shared<fast::FastPlan>(plan);
-    }
-    if (plan.fused->ok() &&
-        plan.fused->eligible(binding, mode == device::EngineMode::kAuto)) {
+  {
+    if (fused_ready(plan, binding, integer_regime, allow_fast)) {
       const int fb = std::min<int64_t>(std::max<int64_t>(1, dd.size()), 256);
       const int64_t per = plan.fused->out_per_sample();
       if (scores) {

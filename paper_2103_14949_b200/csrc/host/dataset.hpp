@@ -15,7 +15,14 @@ class DeviceDataset {
  public:
   // Validates every sample against the graph inputs (reference
   // interpreter.cpp:115-125, :519-531) and uploads [first, first+count).
-  DeviceDataset(const Graph& g, const Dataset& ds, int64_t first = 0, int64_t count = -1);
+  // upload: the stream the copies are issued on (default: the engine
+  // stream).  On another stream, ready() is an event the engine waits on.
+  DeviceDataset(const Graph& g, const Dataset& ds, int64_t first = 0, int64_t count = -1,
+                void* upload = nullptr);
+  ~DeviceDataset();
+  DeviceDataset(const DeviceDataset&) = delete;
+  // make the engine stream wait for this dataset's upload
+  void wait_ready() const;
   int64_t size() const { return n_; }
   const float* input(size_t k, int64_t sample) const {
     return static_cast<const float*>(bufs_[k].get()) + sample * per_[k];
@@ -24,12 +31,18 @@ class DeviceDataset {
 
  private:
   int64_t n_ = 0;
+  void* ready_ = nullptr;  // cudaEvent_t recorded after the upload (other-stream uploads)
   std::vector<std::shared_ptr<void>> bufs_;
   std::vector<int64_t> per_;
 };
 
 // Per-sample argmax of the first graph output over every sample, on device
 // (int64 [size]).
+// predict_top1's device part over a HOST dataset: uploads overlap the fused
+// forward (chunked on the copy stream); other engines upload, then run.
+std::shared_ptr<void> predict_streamed(const engine::Plan& plan, const Graph& g,
+                                       const Dataset& ds, const SimBinding* binding);
+
 // scores (optional): also returns the output rows, [size x *per_sample] fp32.
 std::shared_ptr<void> predict_device(const engine::Plan& plan, const DeviceDataset& dd,
                                      const SimBinding* binding, bool integer_regime,

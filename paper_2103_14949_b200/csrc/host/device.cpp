@@ -18,6 +18,7 @@ namespace {
 struct Context {
   int dev = -1;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // host->device uploads overlapping engine work
   std::atomic<int> mode{static_cast<int>(EngineMode::kAuto)};
 };
 
@@ -53,6 +54,7 @@ Context& ctx() {
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh);
     }
     cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking);
     c.dev = dev;
     if (const char* m = std::getenv("QUANTC_ENGINE")) {
       std::string s(m);
@@ -72,6 +74,7 @@ void set_engine_mode(EngineMode m) { ctx().mode = static_cast<int>(m); }
 EngineMode engine_mode() { return static_cast<EngineMode>(ctx().mode.load()); }
 int current_device() { return ctx().dev; }
 void* stream() { return ctx().stream; }
+void* copy_stream() { return ctx().copy_stream; }
 
 void synchronize() {
   cudaError_t e = cudaStreamSynchronize(ctx().stream);

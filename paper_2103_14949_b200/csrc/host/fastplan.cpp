@@ -1071,7 +1071,8 @@ bool FastPlan::eligible(const SimBinding* binding, bool exact, std::string* why)
 }
 
 void FastPlan::ensure_arena(int batch) {
-  if (arena_batch_ == batch) return;
+  // buffers are batch-major rows: a smaller batch runs on a prefix
+  if (arena_batch_ >= batch) return;
   arena_.clear();
   for (const auto& v : vals_) {
     const size_t bytes = static_cast<size_t>(v->bytes_ps()) * batch;
