@@ -55,7 +55,11 @@ class Staging {
         continue;
       }
       check(cudaEventSynchronize(ev_[slot]));  // DMA out of this buffer finished
-      parallel_for(static_cast<size_t>(n), n >= 4 ? 8 : 1,
+      static const int workers = [] {
+        const char* e = std::getenv("QUANTC_PACK_WORKERS");
+        return e ? std::max(1, std::atoi(e)) : 3;  // memcpy-bound; more threads only contend (B200 box, 16 cores)
+      }();
+      parallel_for(static_cast<size_t>(n), n >= 4 ? workers : 1,
                    [&](size_t s) { pack(s0 + static_cast<int64_t>(s), buf + s * bytes_per); });
       check(cudaMemcpyAsync(dst_dev + s0 * bytes_per, buf, bytes, cudaMemcpyHostToDevice, us));
       check(cudaEventRecord(ev_[slot], us));
