@@ -34,7 +34,8 @@ void set_engine_mode(EngineMode m);
 EngineMode engine_mode();
 
 int current_device();
-void* stream();  // cudaStream_t of the engine
+void* stream();       // cudaStream_t of the engine
+void* copy_stream();  // cudaStream_t for uploads that overlap engine work
 void synchronize();
 size_t memory_budget_bytes();  // per-batch activation budget
 

@@ -88,6 +88,10 @@ void qc_free(void* p);
 int qc_graph_from_json(const char* json, const void* blob, size_t blob_len, qc_graph** out);
 /* structure + attrs only (payload shapes/dtypes, no bytes) */
 int qc_graph_to_json(const qc_graph* g, char** json_out);
+/* the payload bytes the offsets of qc_graph_to_json refer to (int32/fp32
+ * little-endian, in node order): with the JSON, qc_graph_from_json rebuilds
+ * the graph in any library exporting this ABI */
+int qc_graph_blob(const qc_graph* g, void* out, size_t cap, size_t* n);
 void qc_graph_free(qc_graph* g);
 int qc_graph_num_nodes(const qc_graph* g, size_t* n);
 /* validate_graph (graph.hpp:131): JSON array of {"node","message"} */

@@ -91,6 +91,11 @@ int qc_collect_extrema(const qc_graph* g, const qc_dataset* d, const int* edges,
                        double* mins, double* maxs);
 int qc_collect_histograms(const qc_graph* g, const qc_dataset* d, const int* edges, size_t n,
                           const double* absmax, int bins, int64_t* counts);
+/* realize (SPEC.md realize module; the reference declares it without an
+ * implementation): the simulated graph lowered under a strategy (the JSON of
+ * qc_evaluator_strategy) into an integer graph for qc_eval_int. */
+int qc_realize(const qc_graph* sim_g, const char* strategy_json, const qc_spec* spec,
+               qc_graph** out);
 /* fp32 score rows of predict_top1 (samples x per-sample numel) under the
  * active engine mode (B200 extension; quantc/device.hpp predict_scores). */
 int qc_predict_scores(const qc_graph* g, const qc_dataset* d, const int64_t* bind_nodes,

@@ -241,7 +241,7 @@ int qc_graph_from_json(const char* json, const void* blob, size_t blob_len, qc_g
       Node n;
       n.id = jn.at("id").get<NodeId>();
       n.op = parse_op(jn.at("op").get<std::string>());
-      if (jn.contains("attrs")) n.attrs = jn.at("attrs");
+      if (jn.contains("attrs") && jn.at("attrs").is_object()) n.attrs = jn.at("attrs");
       if (jn.contains("payload")) {
         const Json& pl = jn.at("payload");
         DType dt = parse_dtype(pl.at("dtype").get<std::string>());
@@ -303,6 +303,26 @@ int qc_graph_to_json(const qc_graph* g, char** json_out) {
     for (const PortRef& p : g->g->outputs()) outs.push_back({p.node, p.port});
     Json doc = {{"nodes", nodes}, {"edges", edges}, {"inputs", g->g->inputs()}, {"outputs", outs}};
     *json_out = dup_string(doc.dump());
+  });
+}
+
+int qc_graph_blob(const qc_graph* g, void* out, size_t cap, size_t* n) {
+  return run([&] {
+    size_t total = 0;
+    for (const Node& nd : g->g->nodes()) {
+      if (nd.payload.has_value()) total += static_cast<size_t>(nd.payload->numel()) * 4;
+    }
+    *n = total;
+    if (total > cap) throw BufferTooSmall();
+    auto* dst = static_cast<uint8_t*>(out);
+    for (const Node& nd : g->g->nodes()) {
+      if (!nd.payload.has_value()) continue;
+      const Tensor& t = *nd.payload;
+      const void* src = t.dtype().is_float() ? static_cast<const void*>(t.floats().data())
+                                             : static_cast<const void*>(t.ints().data());
+      std::memcpy(dst, src, static_cast<size_t>(t.numel()) * 4);
+      dst += static_cast<size_t>(t.numel()) * 4;
+    }
   });
 }
 
@@ -746,6 +766,26 @@ int qc_evaluator_strategy(const qc_evaluator* e, const int* cand, size_t n_slots
 }
 
 #ifdef QUANTC_B200
+int qc_realize(const qc_graph* sim_g, const char* strategy_json, const qc_spec* spec,
+               qc_graph** out) {
+  return run([&] {
+    Strategy st;
+    const Json doc = Json::parse(strategy_json);  // items() must not outlive it
+    for (const auto& kv : doc.items()) {
+      EdgeDecision d;
+      d.bit = kv.value().at("bit").get<int>();
+      d.threshold = kv.value().at("threshold").get<double>();
+      d.sign = kv.value().at("sign").get<int>();
+      d.zero_point = kv.value().at("zero_point").get<int64_t>();
+      d.storage_dtype = parse_dtype(kv.value().at("storage_dtype").get<std::string>());
+      st.edges[std::stoi(kv.key())] = d;
+    }
+    auto h = std::make_unique<qc_graph>();
+    h->g = std::make_shared<Graph>(realize(*sim_g->g, st, *spec->s));
+    *out = h.release();
+  });
+}
+
 int qc_collect_extrema(const qc_graph* g, const qc_dataset* d, const int* edges, size_t n,
                        double* mins, double* maxs) {
   return run([&] {

@@ -433,6 +433,17 @@ class Quantc:
             self.check(rc)
             return buf[: n.value].reshape(d.n, -1)
 
+    def realize(self, sim_g: "Graph", strategy: dict, spec) -> "Graph":
+        """B200 extension: realize() (SPEC.md realize module) of sim_g under a
+        strategy (CandidateEvaluator.strategy_for's dict)."""
+        fn = self.lib.qc_realize
+        fn.restype = C.c_int
+        fn.argtypes = [_P, C.c_char_p, _P, C.POINTER(_P)]
+        h = _P()
+        doc = json.dumps({str(k): v for k, v in strategy.items()}).encode()
+        self.check(fn(sim_g.h, doc, spec.h, C.byref(h)))
+        return Graph(self, h)
+
     # -- search (search.hpp) --------------------------------------------
     def evaluator(self, sim_g, spec, topo, thresholds: Dict[int, float], stats, calib,
                   min_bit=4, workers=0) -> "CandidateEvaluator":
@@ -510,6 +521,24 @@ class Graph(_Handle):
         s = C.c_void_p()
         self.q.check(self.q.lib.qc_graph_to_json(self.h, C.byref(s)))
         return json.loads(self.q._take_string(s))
+
+    def blob(self) -> bytes:
+        """Payload bytes matching to_json()'s offsets (qc_graph_blob)."""
+        fn = self.q.lib.qc_graph_blob
+        fn.restype = C.c_int
+        fn.argtypes = [_P, C.c_void_p, _SZ, _PSZ]
+        n = C.c_size_t()
+        rc = fn(self.h, None, 0, C.byref(n))
+        if rc not in (0, 10):
+            self.q.check(rc)
+        buf = C.create_string_buffer(max(1, n.value))
+        self.q.check(fn(self.h, buf, n.value, C.byref(n)))
+        return buf.raw[: n.value]
+
+    def copy_to(self, q: "Quantc") -> "Graph":
+        """The same graph inside another library exporting this ABI (JSON +
+        blob round trip), e.g. a realized graph handed to the reference."""
+        return q.graph(self.to_json(), self.blob())
 
     def num_nodes(self) -> int:
         n = C.c_size_t()
