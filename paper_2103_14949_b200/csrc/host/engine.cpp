@@ -328,10 +328,12 @@ struct Runner {
   std::vector<kern::SqParams> sqp;
   std::vector<QParams> qp;
   std::shared_ptr<void> trap;
+  std::vector<char> done;  // computed by a fused producer (requantize after an int conv)
 
   Runner(const Plan& p, const RunSpec& s) : plan(p), spec(s) {
     const size_t n = p.steps().size();
     vals.resize(n);
+    done.assign(n, 0);
     remaining.resize(n);
     keep.assign(n, 0);
     fast_conv.assign(n, 0);
@@ -444,10 +446,136 @@ struct Runner {
 
   void exec(int i);
   void exec_conv(int i, bool dense);
+  bool exec_conv_int_tc(int i, bool dense, const kern::ConvShape& cs, const DevTensor& d,
+                        const DevTensor& w, const DevTensor* b, DType acc,
+                        const std::vector<int64_t>& zps);
   void exec_conv_fast(int i, bool dense);
   void exec_sq(int i);
   void exec_sq_codes(int i);
 };
+
+// Realized-graph int8 x int8 conv/dense on tcgen05 (SURVEY §8(a) a7/a8 with
+// the a9 requantize fused): codes packed NHWC, weights packed K-major with
+// zp1 folded (when w - zp1 fits int8), the exact int32 tensor-core sum,
+// and the IntEpi epilogue (zp0 correction, bias, accumulator clamp / trap,
+// requantize of a sole requantize consumer).  Returns false when the layer
+// does not qualify (the int64 CUDA-core kernel then runs).
+bool Runner::exec_conv_int_tc(int i, bool dense, const kern::ConvShape& cs, const DevTensor& d,
+                              const DevTensor& w, const DevTensor* b, DType acc,
+                              const std::vector<int64_t>& zps) {
+  static const bool off = [] {
+    const char* e = std::getenv("QUANTC_INT_TC");
+    return e && std::string(e) == "0";
+  }();
+  if (off || !kern::gemm_s8_tcgen05_available()) return false;
+  // 8-bit (or narrower) data codes; the weights' range is checked on device
+  if (!d.dtype.is_integer() || d.dtype.width() > 8 || !w.dtype.is_integer()) return false;
+  if (acc.width() > 32) return false;
+
+  const auto& steps = plan.steps();
+  const Node& n = *steps[static_cast<size_t>(i)].node;
+  const int taps = cs.KH * cs.KW;
+  const int ld = (cs.C + 15) / 16 * 16;
+  const bool direct = dense || (taps == 1 && cs.sh == 1 && cs.sw == 1 && cs.ph == 0 &&
+                                cs.pw == 0 && ld == cs.C);
+  if (!direct && taps > 63) return false;
+  const int Ktrue = direct ? ld : taps * ld;
+  const int Kpad = (Ktrue + 127) / 128 * 128;
+  if (static_cast<int64_t>(Ktrue) * 255 * 128 >= (int64_t{1} << 31)) return false;  // int32 TMEM sum
+  // weights: w - zp1 as int8 codes [O][Kpad] and their per-row sums
+  auto wcodes = device_alloc(static_cast<size_t>(cs.O) * Kpad + 16);
+  auto wsum = device_alloc(static_cast<size_t>(cs.O) * 4 + 16);
+  int* bad = reinterpret_cast<int*>(static_cast<int8_t*>(wsum.get()) + static_cast<size_t>(cs.O) * 4);
+  cuda_ok(cudaMemsetAsync(wsum.get(), 0, static_cast<size_t>(cs.O) * 4 + 16, S()), "wsum");
+  kern::pack_i32_weights(w.i(), static_cast<int8_t*>(wcodes.get()), static_cast<int32_t*>(wsum.get()),
+                         bad, cs.O, cs.C, taps, ld, Kpad, zps.at(1), S());
+  int hbad = 0;
+  cuda_ok(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, S()), "pack flag");
+  device::synchronize();
+  if (hbad) return false;
+  // data codes NHWC.  The reference skips padded taps, i.e. they add
+  // (zp0 - zp0) * w = 0; with zp0 != 0 the border is materialised as zp0 so
+  // that acc - zp0 * wsum stays exact, otherwise the gather's zero fill is.
+  const bool pad_fill = zps.at(0) != 0 && (cs.ph != 0 || cs.pw != 0);
+  const int pph = pad_fill ? cs.ph : 0, ppw = pad_fill ? cs.pw : 0;
+  const int HP = cs.H + 2 * pph, WP = cs.W + 2 * ppw;
+  auto xcodes = device_alloc(static_cast<size_t>(cs.N) * HP * WP * ld + 64);
+  kern::pack_i32_nhwc(d.i(), static_cast<uint8_t*>(xcodes.get()), cs.N, cs.C, cs.H, cs.W, pph,
+                      ppw, ld, static_cast<int32_t>(zps.at(0)), S());
+  // a sole requantize consumer is fused into the epilogue
+  int rq = -1;
+  if (steps[static_cast<size_t>(i)].uses == 1 && !keep[static_cast<size_t>(i)]) {
+    for (size_t j = static_cast<size_t>(i) + 1; j < steps.size(); ++j) {
+      const auto& sj = steps[j];
+      if (std::find(sj.in.begin(), sj.in.end(), i) == sj.in.end()) continue;
+      if (sj.node->op == OpKind::kRequantize && spec.integer_regime) rq = static_cast<int>(j);
+      break;
+    }
+  }
+  DevTensor y = out_like(rq >= 0 ? rq : i, rq >= 0
+                                               ? parse_dtype(steps[static_cast<size_t>(rq)].node->attr<std::string>("out_dtype"))
+                                               : acc);
+  kern::TcConvSpec sp{};
+  sp.x = static_cast<const int8_t*>(xcodes.get());
+  sp.w = static_cast<const int8_t*>(wcodes.get());
+  sp.M = static_cast<int64_t>(cs.N) * cs.OH * cs.OW;
+  sp.O = cs.O;
+  sp.Kpad = Kpad;
+  sp.gather = direct ? 0 : 1;
+  sp.Ktrue = Ktrue;
+  sp.lda = ld;
+  sp.Nimg = cs.N;
+  sp.H = HP;
+  sp.W = WP;
+  sp.C = cs.C;
+  sp.ld = ld;
+  sp.KH = cs.KH;
+  sp.KW = cs.KW;
+  sp.sh = cs.sh;
+  sp.sw = cs.sw;
+  sp.ph = cs.ph - pph;
+  sp.pw = cs.pw - ppw;
+  sp.OH = cs.OH;
+  sp.OW = cs.OW;
+  sp.prog = kern::ProgArgs{nullptr, 0, kern::kShapeInt};
+  kern::IntEpi& ie = sp.iepi;
+  ie.y = y.i();
+  ie.bias = b ? b->i() : nullptr;
+  ie.zp0 = zps.at(0);
+  ie.wsum = ie.zp0 != 0 ? static_cast<const int32_t*>(wsum.get()) : nullptr;
+  ie.trap = trap_ptr();
+  ie.acc_min = acc.min_value();
+  ie.acc_max = acc.max_value();
+  ie.OHW = cs.OH * cs.OW;
+  ie.a_unsigned = d.dtype.is_signed() ? 0 : 1;
+  if (rq >= 0) {
+    const Node& r = *steps[static_cast<size_t>(rq)].node;
+    ie.rq = 1;
+    ie.mult = r.attr<int64_t>("multiplier");
+    ie.shift = r.attr<int>("shift");
+    ie.in_zp = r.attr_or<int64_t>("in_zero_point", 0);
+    ie.out_zp = r.attr_or<int64_t>("zero_point", 0);
+    ie.q_min = r.attr<int64_t>("q_min");
+    ie.q_max = r.attr<int64_t>("q_max");
+  }
+  kern::tc_conv(sp, S());
+  device::counters().tcgen05_gemms++;
+  if (ie.trap) {
+    const int64_t flat = trapped();
+    if (flat >= 0) {
+      const int64_t v = kern::conv2d_int_value_at(d.i(), w.i(), b ? b->i() : nullptr, cs, zps[0],
+                                                  zps[1], flat, S());
+      throw OverflowError(n.id, flat, v);
+    }
+  }
+  if (rq >= 0) {
+    vals[static_cast<size_t>(rq)] = y;
+    done[static_cast<size_t>(rq)] = 1;
+  } else {
+    vals[static_cast<size_t>(i)] = y;
+  }
+  return true;
+}
 
 void Runner::exec_sq(int i) {
   const Node& n = *plan.steps()[static_cast<size_t>(i)].node;
@@ -590,6 +718,7 @@ void Runner::exec_conv(int i, bool dense) {
   }
   DType acc = acc_dtype_of(n);
   auto zps = n.attr_or<std::vector<int64_t>>("in_zero_points", {0, 0});
+  if (exec_conv_int_tc(i, dense, cs, d, w, b, acc, zps)) return;
   DevTensor y = out_like(i, acc);
   unsigned long long* trap = trap_ptr();
   kern::conv2d_int(d.i(), w.i(), b ? b->i() : nullptr, y.i(), cs, zps[0], zps[1],
@@ -606,6 +735,7 @@ void Runner::exec_conv(int i, bool dense) {
 }
 
 void Runner::exec(int i) {
+  if (done[static_cast<size_t>(i)]) return;  // produced by a fused producer
   const auto& st = plan.steps()[static_cast<size_t>(i)];
   const Node& n = *st.node;
   switch (n.op) {

@@ -172,6 +172,7 @@ struct TcArgs {
   ProgArgs prog;
   int m_tiles, n_tiles;
   EpiConsts epi;
+  IntEpi iepi;
 };
 
 template <int W>
@@ -242,8 +243,8 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
   int2* ktab = reinterpret_cast<int2*>(tabs + 1);
   // shape kernels: bias pre-scaled into sq0's grid, btab[n] = bias[n] / s0
   float* btab = reinterpret_cast<float*>(ktab + (args.gather == 1 ? args.K / 16 : 0));
-  load_tables(tabs, args.prog.tables);
-  if (SHAPE != kShapeGeneric) {
+  if (args.prog.tables) load_tables(tabs, args.prog.tables);
+  if (SHAPE != kShapeGeneric && SHAPE != kShapeInt) {
     for (int n = threadIdx.x; n < args.n_tiles * BN; n += blockDim.x) {
       btab[n] = (args.bias && n < args.N) ? __fmul_rn(__ldg(args.bias + n), args.epi.inv0) : 0.0f;
     }
@@ -424,7 +425,8 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
   } else if (warp == MMA_WARP) {
     // ================= MMA issuer =================
     if (lane == 0) {
-      constexpr uint32_t id = idesc(BM, BN);
+      // uint8 A (realized graphs with unsigned activations): clear a_signed
+      const uint32_t id = idesc(BM, BN) & ~(args.iepi.a_unsigned ? (1u << 7) : 0u);
       uint32_t tl = 0, ph = 0;
       int s = 0;
       for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
@@ -532,7 +534,47 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
       }
       const int64_t m = static_cast<int64_t>(m0) + r;
       const uint32_t tbase = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
-      if constexpr (SHAPE != kShapeGeneric) {
+      if constexpr (SHAPE == kShapeInt) {
+        // realized-graph integer conv/dense: exact int64 epilogue (IntEpi)
+        const IntEpi& ie = args.iepi;
+        const bool row_ok = m < args.M;
+        const int64_t img = row_ok ? m / ie.OHW : 0;
+        const int64_t hw = row_ok ? m - img * ie.OHW : 0;
+#pragma unroll 1
+        for (int c = part; c < NCHUNK; c += PARTS) {
+          const int c0 = c * EW;
+          uint32_t d[EW];
+          tmem_ld<EW>(tbase + c0, d);
+          tmem_wait(d);
+          const int n = n0 + c0;
+          if (!row_ok) continue;
+#pragma unroll 4
+          for (int j = 0; j < EW; ++j) {
+            const int o = n + j;
+            if (o >= args.N) break;
+            int64_t v = static_cast<int32_t>(d[j]);
+            if (ie.wsum) v -= ie.zp0 * static_cast<int64_t>(__ldg(ie.wsum + o));
+            if (ie.bias) v += __ldg(ie.bias + o);
+            const int64_t flat = (img * args.N + o) * ie.OHW + hw;
+            if (v < ie.acc_min || v > ie.acc_max) {
+              if (ie.trap) atomicMin(ie.trap, static_cast<unsigned long long>(flat));
+              v = v < ie.acc_min ? ie.acc_min : ie.acc_max;
+            }
+            if (ie.rq) {
+              // fixed_point_rescale, round half away (reference interpreter.cpp:32-37)
+              const int64_t p = (v - ie.in_zp) * ie.mult;
+              int64_t q = p;
+              if (ie.shift > 0) {
+                const int64_t nudge = int64_t{1} << (ie.shift - 1);
+                q = p >= 0 ? (p + nudge) >> ie.shift : -((-p + nudge) >> ie.shift);
+              }
+              q += ie.out_zp;
+              v = q < ie.q_min ? ie.q_min : (q > ie.q_max ? ie.q_max : q);
+            }
+            ie.y[flat] = static_cast<int32_t>(v);
+          }
+        }
+      } else if constexpr (SHAPE != kShapeGeneric) {
         // straight-line shapes: host-checked preconditions (classify_shape)
         // — O % 16 == 0, all I/O through slots (rows >= M and columns >= O
         // are clipped by the TMA store), zp = 0, no live acc clamp.  TMEM
@@ -842,7 +884,7 @@ bool dbuf_fits(const TcArgs& a, int bn, bool shape) {
 template <int BN, int SHAPE>
 void launch_tc(const CUtensorMap* maps, TcArgs a, cudaStream_t s) {
   const int stage_bytes = BM * a.bkb + BN * a.bkb;
-  constexpr bool shape = SHAPE != kShapeGeneric;
+  constexpr bool shape = SHAPE != kShapeGeneric && SHAPE != kShapeInt;  // btab in smem
   a.dbuf = dbuf_fits(a, BN, shape) ? 1 : 0;
   const int fixed = smem_fixed(a, BN, a.dbuf + 1, shape);
   int stages = fit_stages(a, BN, fixed);
@@ -898,6 +940,9 @@ void launch_bn(const CUtensorMap* maps, const TcArgs& a, cudaStream_t s) {
     case kShapeAddForkId:
       launch_tc<BN, kShapeAddForkId>(maps, a, s);
       break;
+    case kShapeInt:
+      launch_tc<BN, kShapeInt>(maps, a, s);
+      break;
     default:
       launch_tc<BN, kShapeGeneric>(maps, a, s);
       break;
@@ -926,6 +971,7 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
   }
   a.prog = sp.prog;
   a.epi = sp.epi;
+  a.iepi = sp.iepi;
   a.always_small = sp.acc_bound <= static_cast<double>(1 << 24) ? 1 : 0;
   a.w_l1 = sp.w_l1;
   a.x_absmax = sp.x_absmax;

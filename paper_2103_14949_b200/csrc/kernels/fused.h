@@ -161,8 +161,29 @@ struct EpiConsts {
 //      exact, no clamp): the T-domain code of sq0 is the stored byte
 //   7: shape 3 with sq0 signed rounding, sq1 non-negative rounding and both
 //      fork stores identities: one packed code, stored to both slots
+//   8: integer conv/dense of a realized graph (IntEpi): exact int64 epilogue,
+//      accumulator-dtype clamp / trap, optional fused requantize, int32 NCHW out
 enum : int { kShapeGeneric = 0, kShapeStore = 1, kShapeSqStore = 2, kShapeAddFork = 3,
-             kShapeAdd = 4, kShapeAddF32 = 5, kShapeSqStoreId = 6, kShapeAddForkId = 7 };
+             kShapeAdd = 4, kShapeAddF32 = 5, kShapeSqStoreId = 6, kShapeAddForkId = 7,
+             kShapeInt = 8 };
+
+// Integer epilogue (reference interpreter.cpp:238-309 then :464-482):
+//   v = acc - zp0 * wsum[o] + bias[o]          (acc = sum_k x'*w', w' = w - zp1)
+//   v outside [acc_min, acc_max] -> trap (lowest flat index) or saturate
+//   requantize (optional): q = clamp(rescale(v - in_zp) + out_zp, q_min, q_max)
+//   y[((img*O + o)*OH + oh)*OW + ow] = v or q   (int32, NCHW like Tensor)
+struct IntEpi {
+  int32_t* y;
+  const int32_t* bias;  // may be null
+  const int32_t* wsum;  // sum_k w'[o][k]; may be null when zp0 == 0
+  unsigned long long* trap;  // may be null (saturate)
+  int64_t zp0, acc_min, acc_max;
+  int32_t rq;  // 1: fused requantize
+  int32_t shift;
+  int64_t mult, in_zp, out_zp, q_min, q_max;
+  int32_t OHW;  // output pixels per image (1 for dense)
+  int32_t a_unsigned;  // A codes are uint8 (tcgen05 unsigned A)
+};
 
 // kernels receive the stage's table block in global memory
 struct ProgArgs {

@@ -140,6 +140,7 @@ struct TcConvSpec {
   const int* w_l1;
   int x_absmax;
   EpiConsts epi;     // shape kernels (prog.shape != 0): host-folded constants
+  IntEpi iepi;       // prog.shape == kShapeInt: integer epilogue
 };
 void tc_conv(const TcConvSpec& spec, cudaStream_t s);
 int tc_conv_bn(int O);  // output-channel tile the kernel uses for O channels
@@ -158,6 +159,15 @@ void weight_codes_s2d(const float* w, int8_t* codes, int O, int C, int KH, int K
                       int KW2, int dh, int dw, int Kpad, const FSq& p, cudaStream_t s);
 // out = max over rows of sum_k |codes[o][k]| (out zeroed by the caller)
 void weight_l1_max(const int8_t* codes, int O, int Kpad, int* out, cudaStream_t s);
+// realized-graph integer path: int32 NCHW values (int8 / uint8 range) -> 8-bit
+// NHWC rows [N][H+2ph][W+2pw][ld] (channels >= C zero, the ph/pw border
+// `fill`); dense: H = W = 1
+void pack_i32_nhwc(const int32_t* x, uint8_t* out, int N, int C, int H, int W, int ph, int pw,
+                   int ld, int32_t fill, cudaStream_t s);
+// int32 OIHW weights -> int8 [O][Kpad] (k = tap*ld + c) of w - zp1, and
+// wsum[o] = sum of those codes; *bad != 0 when some w - zp1 leaves int8
+void pack_i32_weights(const int32_t* w, int8_t* codes, int32_t* wsum, int* bad, int O, int C,
+                      int taps, int ld, int Kpad, int64_t zp1, cudaStream_t s);
 // graph input NCHW fp32 -> program over (m = n*H*W + hw, c)
 void stage_input(const float* x, int N, int C, int HW, const ProgArgs& prog, cudaStream_t s);
 // max_pool2d over NHWC codes (value = code * scale) -> program

@@ -277,6 +277,63 @@ __global__ void weight_l1_kernel(const int8_t* __restrict__ codes, int O, int Kp
   }
 }
 
+// int32 NCHW (8-bit value range) -> 8-bit NHWC rows: one thread per (pixel,
+// 16-channel group), coalesced over pixels, one 16-byte store
+__global__ void pack_i32_nhwc_kernel(const int32_t* __restrict__ x, uint8_t* __restrict__ out,
+                                     int64_t pixels, int C, int H, int W, int ph, int pw,
+                                     int ld, uint32_t fill) {
+  pdl_trigger();
+  pdl_wait();
+  const int groups = ld / 16;
+  const int64_t total = pixels * groups;
+  const int HP = H + 2 * ph, WP = W + 2 * pw;
+  const uint32_t fill4 = (fill & 0xFFu) * 0x01010101u;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t pix = i % pixels;  // (padded) pixel fastest: coalesced reads per channel
+    const int g = static_cast<int>(i / pixels);
+    const int64_t n = pix / (static_cast<int64_t>(HP) * WP);
+    const int r = static_cast<int>(pix - n * HP * WP);
+    const int h = r / WP - ph, w = r % WP - pw;
+    uint32_t v[4] = {0, 0, 0, 0};
+    if (h < 0 || h >= H || w < 0 || w >= W) {
+      v[0] = v[1] = v[2] = v[3] = fill4;  // the padding value the zp0 correction assumes
+    } else {
+      const int64_t base = n * C * H * W + static_cast<int64_t>(h) * W + w;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int c = g * 16 + j;
+        if (c < C) v[j >> 2] |= (static_cast<uint32_t>(x[base + static_cast<int64_t>(c) * H * W]) & 0xFFu) << (8 * (j & 3));
+      }
+    }
+    *reinterpret_cast<int4*>(out + pix * ld + g * 16) =
+        make_int4(static_cast<int>(v[0]), static_cast<int>(v[1]), static_cast<int>(v[2]),
+                  static_cast<int>(v[3]));
+  }
+}
+
+__global__ void pack_i32_weights_kernel(const int32_t* __restrict__ w, int8_t* __restrict__ codes,
+                                        int32_t* __restrict__ wsum, int* __restrict__ bad, int O,
+                                        int C, int taps, int ld, int Kpad, int64_t zp1) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t total = static_cast<int64_t>(O) * Kpad;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(i % Kpad);
+    const int o = static_cast<int>(i / Kpad);
+    const int tap = k / ld, c = k - tap * ld;
+    int8_t code = 0;
+    if (tap < taps && c < C) {
+      const int64_t v = static_cast<int64_t>(w[(static_cast<int64_t>(o) * C + c) * taps + tap]) - zp1;
+      if (v < -128 || v > 127) atomicOr(bad, 1);
+      code = static_cast<int8_t>(v);
+      if (v != 0) atomicAdd(wsum + o, static_cast<int32_t>(v));
+    }
+    codes[i] = code;
+  }
+}
+
 // one thread per output row: walks (kh, kw, c) with incremental counters and
 // emits the row as 16-byte stores
 __global__ void pack_im2col_kernel(const int8_t* __restrict__ x, int8_t* __restrict__ out, int N,
@@ -328,6 +385,25 @@ void pack_im2col(const int8_t* x, int8_t* out, int N, int H, int W, int C, int l
   launch_pdl(pack_im2col_kernel, dim3(grid_for(total, 128, 148 * 32)), dim3(128), 0, s, x, out, N, H, W, C, ld, KH, KW,
                                                                      sh, sw, ph, pw, OH, OW, Ktrue,
                                                                      Kpad);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+void pack_i32_nhwc(const int32_t* x, uint8_t* out, int N, int C, int H, int W, int ph, int pw,
+                   int ld, int32_t fill, cudaStream_t s) {
+  const int64_t pixels = static_cast<int64_t>(N) * (H + 2 * ph) * (W + 2 * pw);
+  const int64_t total = pixels * (ld / 16);
+  if (total <= 0) return;
+  launch_pdl(pack_i32_nhwc_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, x, out, pixels,
+             C, H, W, ph, pw, ld, static_cast<uint32_t>(fill));
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+void pack_i32_weights(const int32_t* w, int8_t* codes, int32_t* wsum, int* bad, int O, int C,
+                      int taps, int ld, int Kpad, int64_t zp1, cudaStream_t s) {
+  const int64_t total = static_cast<int64_t>(O) * Kpad;
+  if (total <= 0) return;
+  launch_pdl(pack_i32_weights_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, w, codes,
+             wsum, bad, O, C, taps, ld, Kpad, zp1);
   QC_CUDA_CHECK_LAUNCH();
 }
 

@@ -298,3 +298,40 @@ def overflow_dense(k: int = 256, value: int = 127, acc: str = "int16") -> Tuple[
     d = gb.op("dense", [q, w], acc_dtype=acc)
     gb.output(d)
     return gb.build()
+
+
+def int_conv_probe(n=2, c=16, h=12, w=12, o=24, k=3, stride=1, pad=1, dtype="int8",
+                   zp0=0, zp1=0, acc="int32", requant=None, dense=False, seed=0,
+                   wlo=None, whi=None) -> Tuple[dict, bytes]:
+    """Realized-graph integer conv2d/dense probe (SPEC.md realize output
+    shapes): quantize(x) -> conv2d / dense(int weights, int32 bias, zero
+    points, acc dtype) [-> requantize(multiplier, shift, zero points)].
+    Exercises every IntEpi path of the tcgen05 integer kernel: signed /
+    unsigned data, nonzero zp0 with padding, zp1 folding, accumulator
+    saturation (int16 acc), and a fused requantize."""
+    rng = np.random.default_rng(seed)
+    lo, hi = (-128, 127) if dtype == "int8" else (0, 255)
+    # default weight range: int8 values whose w - zp1 also fits int8
+    wlo = max(-128, -128 + zp1) if wlo is None else wlo
+    whi = min(127, 127 + zp1) if whi is None else whi
+    gb = GraphBuilder()
+    shape = [n, c] if dense else [n, c, h, w]
+    x = gb.input("data", shape)
+    q = gb.op("quantize", [x], scale=1.0 / 32, zero_point=zp0, q_min=lo, q_max=hi,
+              out_dtype=dtype)
+    if dense:
+        wt = gb.constant(rng.integers(wlo, whi + 1, (o, c)), dtype="int8")
+    else:
+        wt = gb.constant(rng.integers(wlo, whi + 1, (o, c, k, k)), dtype="int8")
+    b = gb.constant(rng.integers(-5000, 5000, (o,)), dtype="int32")
+    attrs = dict(acc_dtype=acc, in_zero_points=[zp0, zp1])
+    if dense:
+        y = gb.op("dense", [q, wt, b], **attrs)
+    else:
+        y = gb.op("conv2d", [q, wt, b], strides=[stride, stride], padding=[pad, pad], **attrs)
+    if requant is not None:
+        mult, shift, in_zp, out_zp = requant
+        y = gb.op("requantize", [y], multiplier=mult, shift=shift, in_zero_point=in_zp,
+                  zero_point=out_zp, q_min=-128, q_max=127, out_dtype="int8")
+    gb.output(y)
+    return gb.build()

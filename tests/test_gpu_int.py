@@ -1,0 +1,99 @@
+"""GPU parity of the realized-graph integer path (SURVEY §8(a) conv2d/dense
+int branches + requantize, reference interpreter.cpp:230-300 and :460-482):
+the B200 eval_int — int8 x int8 -> int32 on tcgen05 with the zero-point /
+bias / accumulator-clamp / requantize epilogue fused — against the
+reference's own eval_int on the same graph, bit-exact, including the trap
+mode's node / lowest flat index / value."""
+import numpy as np
+import pytest
+
+from paper_2103_14949_b200 import fixtures as F
+from paper_2103_14949_b200 import quantc as Q
+
+pytestmark = pytest.mark.gpu
+
+RQ = (1 << 30, 41, 7, -3)  # multiplier 2^30, shift 41, in_zp 7, out_zp -3
+
+CASES = {
+    "3x3_pad": dict(),
+    "3x3_zp0_pad": dict(zp0=3, zp1=-2),
+    "3x3_rq": dict(requant=RQ),
+    "3x3_zp_rq": dict(zp0=-4, zp1=1, requant=RQ),
+    "u8_zp0_pad": dict(dtype="uint8", zp0=100, requant=RQ),
+    "1x1": dict(k=1, pad=0, c=64, o=40),
+    "1x1_s2": dict(k=1, pad=0, stride=2, c=32, o=48, requant=RQ),
+    "3x3_s2": dict(stride=2, c=24, o=20, h=15, w=15),
+    "7x7_s2": dict(k=7, stride=2, pad=3, c=3, o=16, h=20, w=20),
+    "5x5_c200": dict(k=5, pad=2, c=200, o=130, h=9, w=9, zp0=5, requant=RQ),
+    "acc_int16_saturate": dict(acc="int16", dtype="uint8", zp0=100),
+    "dense": dict(dense=True, c=300, o=70, n=5, requant=RQ),
+    "dense_zp_int16": dict(dense=True, c=256, o=10, n=3, zp0=9, zp1=4, acc="int16"),
+    "w_zp1_out_of_int8": dict(zp1=-10, wlo=-128, whi=127),  # w - zp1 leaves int8: generic kernel
+}
+
+
+def _x(case, cfg, seed=1):
+    n = cfg.get("n", 2)
+    c = cfg.get("c", 16)
+    shape = (n, c) if cfg.get("dense") else (n, c, cfg.get("h", 12), cfg.get("w", 12))
+    x = np.random.default_rng(seed).normal(0, 2, shape).astype(np.float32)
+    return np.abs(x) if cfg.get("dtype") == "uint8" else x
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_int_conv_bit_exact_vs_reference(b200, ref, cuda_lib, case):
+    cfg = CASES[case]
+    doc, blob = F.int_conv_probe(**cfg)
+    x = _x(case, cfg)
+    yr, dtr = ref.eval_int(ref.graph(doc, blob), x)
+    before = cuda_lib.counters()["tcgen05_gemms"]
+    yb, dtb = b200.eval_int(b200.graph(doc, blob), x)
+    used = cuda_lib.counters()["tcgen05_gemms"] - before
+    assert dtb == dtr
+    np.testing.assert_array_equal(yb, yr)
+    if case != "w_zp1_out_of_int8" and cuda_lib.tcgen05_available():
+        assert used >= 1, "integer conv did not run on tcgen05"
+
+
+@pytest.mark.parametrize("case", ["acc_int16_saturate", "dense_zp_int16"])
+def test_int_conv_trap_matches_reference(b200, ref, case):
+    cfg = CASES[case]
+    doc, blob = F.int_conv_probe(**cfg)
+    x = _x(case, cfg)
+    with pytest.raises(Q.OverflowError_) as er:
+        ref.eval_int(ref.graph(doc, blob), x, trap=True)
+    with pytest.raises(Q.OverflowError_) as eb:
+        b200.eval_int(b200.graph(doc, blob), x, trap=True)
+    assert (eb.value.node, eb.value.flat_index, eb.value.value) == (
+        er.value.node, er.value.flat_index, er.value.value)
+
+
+def _realized(ref, b200, model, spec_name, n):
+    data = model.data(n)
+    g = ref.graph(model.doc, model.blob)
+    spec = ref.parse_spec(F.spec_fixture(spec_name))
+    topo = ref.generate_topology(g, spec)
+    sim = ref.insert_simulated_quantize(g, topo)
+    ds = ref.dataset(data)
+    st = ref.collect_stats(g, ds, 2048, ref.simulated_edge_indices(g, topo))
+    thr = st.estimate_thresholds("quantile", quantile=0.999, pow2=True)
+    ev = ref.evaluator(sim, spec, topo, thr, st, ds)
+    strat = ev.strategy_for(ev.space().all_hi())
+    R = b200.realize(sim.copy_to(b200), strat, b200.parse_spec(F.spec_fixture(spec_name)))
+    return R, data
+
+
+@pytest.mark.parametrize("name,spec_name", [
+    ("small_cnn", "int8_int32"), ("small_cnn", "x86_vnni_like"),
+    ("small_cnn", "arm_vmlal_like"), ("resnet18", "int8_int32"),
+])
+def test_realized_model_eval_int_bit_exact(b200, ref, name, spec_name):
+    model = F.small_cnn() if name == "small_cnn" else F.resnet(18, image=32, classes=10,
+                                                                 width=8)
+    R, data = _realized(ref, b200, model, spec_name, 3)
+    Rr = R.copy_to(ref)
+    for x in data:
+        yr, dtr = ref.eval_int(Rr, x)
+        yb, dtb = b200.eval_int(R, x)
+        assert dtb == dtr
+        np.testing.assert_array_equal(yb, yr)
