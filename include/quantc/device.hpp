@@ -45,6 +45,7 @@ struct Counters {
   int64_t tcgen05_gemms = 0;
   int64_t f64_convs = 0;
   int64_t fused_batches = 0;  // batches evaluated by the fused int8 dataflow (engine v2)
+  int64_t simt_int_convs = 0;  // realized int conv/dense on the CUDA-core backend
 };
 Counters& counters();
 

@@ -108,6 +108,9 @@ int qcu_parallel_selftest(size_t n, int workers, int64_t throw_at, int64_t* sum)
 /* counters since load: kernel launches issued by the engine, tcgen05 GEMMs */
 int qcu_counters(int64_t* steps, int64_t* tcgen05_gemms, int64_t* f64_convs,
                  int64_t* fused_batches);
+/* realized-graph integer conv/dense layers run on the CUDA-core backend
+ * (int16 codes / int16 accumulator; kernels/conv_simt.cu) since load */
+int qcu_simt_int_convs(int64_t* n);
 
 #ifdef __cplusplus
 }

@@ -217,4 +217,9 @@ int qcu_counters(int64_t* steps, int64_t* tcgen05_gemms, int64_t* f64_convs,
   return QC_OK;
 }
 
+int qcu_simt_int_convs(int64_t* n) {
+  if (n) *n = device::counters().simt_int_convs;
+  return QC_OK;
+}
+
 }  // extern "C"

@@ -449,6 +449,13 @@ struct Runner {
   bool exec_conv_int_tc(int i, bool dense, const kern::ConvShape& cs, const DevTensor& d,
                         const DevTensor& w, const DevTensor* b, DType acc,
                         const std::vector<int64_t>& zps);
+  bool exec_conv_int_simt(int i, const kern::ConvShape& cs, const DevTensor& d,
+                          const DevTensor& w, const DevTensor* b, DType acc,
+                          const std::vector<int64_t>& zps);
+  int fused_requantize(int i) const;
+  void finish_int(int i, int rq, const DevTensor& y, const kern::ConvShape& cs,
+                  const DevTensor& d, const DevTensor& w, const DevTensor* b,
+                  const std::vector<int64_t>& zps);
   void exec_conv_fast(int i, bool dense);
   void exec_sq(int i);
   void exec_sq_codes(int i);
@@ -471,9 +478,15 @@ bool Runner::exec_conv_int_tc(int i, bool dense, const kern::ConvShape& cs, cons
   // 8-bit (or narrower) data codes; the weights' range is checked on device
   if (!d.dtype.is_integer() || d.dtype.width() > 8 || !w.dtype.is_integer()) return false;
   if (acc.width() > 32) return false;
+  // the int16-accumulator signature is the CUDA-core backend's
+  // (exec_conv_int_simt) unless QUANTC_INT16_ON_TC=1
+  static const bool i16_on_tc = [] {
+    const char* e = std::getenv("QUANTC_INT16_ON_TC");
+    return e && std::string(e) == "1";
+  }();
+  if (acc.width() <= 16 && !i16_on_tc) return false;
 
   const auto& steps = plan.steps();
-  const Node& n = *steps[static_cast<size_t>(i)].node;
   const int taps = cs.KH * cs.KW;
   const int ld = (cs.C + 15) / 16 * 16;
   const bool direct = dense || (taps == 1 && cs.sh == 1 && cs.sw == 1 && cs.ph == 0 &&
@@ -502,16 +515,7 @@ bool Runner::exec_conv_int_tc(int i, bool dense, const kern::ConvShape& cs, cons
   auto xcodes = device_alloc(static_cast<size_t>(cs.N) * HP * WP * ld + 64);
   kern::pack_i32_nhwc(d.i(), static_cast<uint8_t*>(xcodes.get()), cs.N, cs.C, cs.H, cs.W, pph,
                       ppw, ld, static_cast<int32_t>(zps.at(0)), S());
-  // a sole requantize consumer is fused into the epilogue
-  int rq = -1;
-  if (steps[static_cast<size_t>(i)].uses == 1 && !keep[static_cast<size_t>(i)]) {
-    for (size_t j = static_cast<size_t>(i) + 1; j < steps.size(); ++j) {
-      const auto& sj = steps[j];
-      if (std::find(sj.in.begin(), sj.in.end(), i) == sj.in.end()) continue;
-      if (sj.node->op == OpKind::kRequantize && spec.integer_regime) rq = static_cast<int>(j);
-      break;
-    }
-  }
+  const int rq = fused_requantize(i);
   DevTensor y = out_like(rq >= 0 ? rq : i, rq >= 0
                                                ? parse_dtype(steps[static_cast<size_t>(rq)].node->attr<std::string>("out_dtype"))
                                                : acc);
@@ -560,9 +564,35 @@ bool Runner::exec_conv_int_tc(int i, bool dense, const kern::ConvShape& cs, cons
   }
   kern::tc_conv(sp, S());
   device::counters().tcgen05_gemms++;
-  if (ie.trap) {
+  finish_int(i, rq, y, cs, d, w, b, zps);
+  return true;
+}
+
+// the step of a sole requantize consumer of step i (fused into i's
+// epilogue), or -1
+int Runner::fused_requantize(int i) const {
+  const auto& steps = plan.steps();
+  if (!spec.integer_regime || steps[static_cast<size_t>(i)].uses != 1 ||
+      keep[static_cast<size_t>(i)]) {
+    return -1;
+  }
+  for (size_t j = static_cast<size_t>(i) + 1; j < steps.size(); ++j) {
+    const auto& sj = steps[j];
+    if (std::find(sj.in.begin(), sj.in.end(), i) == sj.in.end()) continue;
+    return sj.node->op == OpKind::kRequantize ? static_cast<int>(j) : -1;
+  }
+  return -1;
+}
+
+// trap check (OverflowError at the lowest flat index, value recomputed
+// exactly) and publication of the integer conv's (or fused requantize's) value
+void Runner::finish_int(int i, int rq, const DevTensor& y, const kern::ConvShape& cs,
+                        const DevTensor& d, const DevTensor& w, const DevTensor* b,
+                        const std::vector<int64_t>& zps) {
+  if (trap) {
     const int64_t flat = trapped();
     if (flat >= 0) {
+      const Node& n = *plan.steps()[static_cast<size_t>(i)].node;
       const int64_t v = kern::conv2d_int_value_at(d.i(), w.i(), b ? b->i() : nullptr, cs, zps[0],
                                                   zps[1], flat, S());
       throw OverflowError(n.id, flat, v);
@@ -574,6 +604,89 @@ bool Runner::exec_conv_int_tc(int i, bool dense, const kern::ConvShape& cs, cons
   } else {
     vals[static_cast<size_t>(i)] = y;
   }
+}
+
+static kern::IntEpi int_epi(const DevTensor& y, const DevTensor* b, const void* wsum,
+                            unsigned long long* trap, DType acc, const kern::ConvShape& cs,
+                            const std::vector<int64_t>& zps, const Node* rqn) {
+  kern::IntEpi ie{};
+  ie.y = y.i();
+  ie.bias = b ? b->i() : nullptr;
+  ie.zp0 = zps.at(0);
+  ie.wsum = ie.zp0 != 0 ? static_cast<const int32_t*>(wsum) : nullptr;
+  ie.trap = trap;
+  ie.acc_min = acc.min_value();
+  ie.acc_max = acc.max_value();
+  ie.OHW = cs.OH * cs.OW;
+  if (rqn) {
+    ie.rq = 1;
+    ie.mult = rqn->attr<int64_t>("multiplier");
+    ie.shift = rqn->attr<int>("shift");
+    ie.in_zp = rqn->attr_or<int64_t>("in_zero_point", 0);
+    ie.out_zp = rqn->attr_or<int64_t>("zero_point", 0);
+    ie.q_min = rqn->attr<int64_t>("q_min");
+    ie.q_max = rqn->attr<int64_t>("q_max");
+  }
+  return ie;
+}
+
+// CUDA-core backend (conv_simt.cu): int16 codes, or the int16 accumulator
+bool Runner::exec_conv_int_simt(int i, const kern::ConvShape& cs, const DevTensor& d,
+                                const DevTensor& w, const DevTensor* b, DType acc,
+                                const std::vector<int64_t>& zps) {
+  static const bool off = [] {
+    const char* e = std::getenv("QUANTC_INT_SIMT");
+    return e && std::string(e) == "0";
+  }();
+  if (off || !d.dtype.is_integer() || !w.dtype.is_integer()) return false;
+  if (d.dtype.width() > 16 || acc.width() > 32) return false;
+  const bool i16 = d.dtype.width() > 8;
+  const bool u8 = !i16 && !d.dtype.is_signed();
+  const int per = i16 ? 2 : 4;
+  const int Cw = (cs.C + per - 1) / per;
+  const int taps = cs.KH * cs.KW;
+  const int64_t K = static_cast<int64_t>(taps) * Cw;
+  if (!i16 && K * 4 * 255 * 128 >= (int64_t{1} << 31)) return false;  // dp4a int32 sum
+  const auto& steps = plan.steps();
+  auto wwords = device_alloc(static_cast<size_t>(K) * cs.O * 4);
+  auto wsum = device_alloc(static_cast<size_t>(cs.O) * 4 + 16);
+  int* bad = reinterpret_cast<int*>(static_cast<int8_t*>(wsum.get()) + static_cast<size_t>(cs.O) * 4);
+  cuda_ok(cudaMemsetAsync(wsum.get(), 0, static_cast<size_t>(cs.O) * 4 + 16, S()), "wsum");
+  kern::pack_weight_words(w.i(), static_cast<uint32_t*>(wwords.get()),
+                          static_cast<int32_t*>(wsum.get()), bad, cs.O, cs.C, taps, Cw, i16,
+                          zps.at(1), S());
+  int hbad = 0;
+  cuda_ok(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, S()), "pack flag");
+  device::synchronize();
+  if (hbad) return false;
+  const int HP = cs.H + 2 * cs.ph, WP = cs.W + 2 * cs.pw;
+  auto xwords = device_alloc(static_cast<size_t>(cs.N) * HP * WP * Cw * 4 + 16);
+  kern::pack_words(d.i(), static_cast<uint32_t*>(xwords.get()), cs.N, cs.C, cs.H, cs.W, cs.ph,
+                   cs.pw, Cw, i16, static_cast<int32_t>(zps.at(0)), S());
+  const int rq = fused_requantize(i);
+  const Node* rqn = rq >= 0 ? steps[static_cast<size_t>(rq)].node : nullptr;
+  DevTensor y = out_like(rq >= 0 ? rq : i,
+                         rqn ? parse_dtype(rqn->attr<std::string>("out_dtype")) : acc);
+  kern::SimtConvSpec sp{};
+  sp.x = static_cast<const uint32_t*>(xwords.get());
+  sp.w = static_cast<const uint32_t*>(wwords.get());
+  sp.N = cs.N;
+  sp.HP = HP;
+  sp.WP = WP;
+  sp.Cw = Cw;
+  sp.O = cs.O;
+  sp.KH = cs.KH;
+  sp.KW = cs.KW;
+  sp.sh = cs.sh;
+  sp.sw = cs.sw;
+  sp.OH = cs.OH;
+  sp.OW = cs.OW;
+  sp.i16 = i16;
+  sp.u8 = u8;
+  sp.ie = int_epi(y, b, wsum.get(), trap_ptr(), acc, cs, zps, rqn);
+  kern::conv_int_simt(sp, S());
+  device::counters().simt_int_convs++;
+  finish_int(i, rq, y, cs, d, w, b, zps);
   return true;
 }
 
@@ -719,6 +832,7 @@ void Runner::exec_conv(int i, bool dense) {
   DType acc = acc_dtype_of(n);
   auto zps = n.attr_or<std::vector<int64_t>>("in_zero_points", {0, 0});
   if (exec_conv_int_tc(i, dense, cs, d, w, b, acc, zps)) return;
+  if (exec_conv_int_simt(i, cs, d, w, b, acc, zps)) return;
   DevTensor y = out_like(i, acc);
   unsigned long long* trap = trap_ptr();
   kern::conv2d_int(d.i(), w.i(), b ? b->i() : nullptr, y.i(), cs, zps[0], zps[1],

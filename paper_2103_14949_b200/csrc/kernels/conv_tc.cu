@@ -552,26 +552,8 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
           for (int j = 0; j < EW; ++j) {
             const int o = n + j;
             if (o >= args.N) break;
-            int64_t v = static_cast<int32_t>(d[j]);
-            if (ie.wsum) v -= ie.zp0 * static_cast<int64_t>(__ldg(ie.wsum + o));
-            if (ie.bias) v += __ldg(ie.bias + o);
             const int64_t flat = (img * args.N + o) * ie.OHW + hw;
-            if (v < ie.acc_min || v > ie.acc_max) {
-              if (ie.trap) atomicMin(ie.trap, static_cast<unsigned long long>(flat));
-              v = v < ie.acc_min ? ie.acc_min : ie.acc_max;
-            }
-            if (ie.rq) {
-              // fixed_point_rescale, round half away (reference interpreter.cpp:32-37)
-              const int64_t p = (v - ie.in_zp) * ie.mult;
-              int64_t q = p;
-              if (ie.shift > 0) {
-                const int64_t nudge = int64_t{1} << (ie.shift - 1);
-                q = p >= 0 ? (p + nudge) >> ie.shift : -((-p + nudge) >> ie.shift);
-              }
-              q += ie.out_zp;
-              v = q < ie.q_min ? ie.q_min : (q > ie.q_max ? ie.q_max : q);
-            }
-            ie.y[flat] = static_cast<int32_t>(v);
+            ie.y[flat] = int_epi_value(ie, static_cast<int32_t>(d[j]), o, flat);
           }
         }
       } else if constexpr (SHAPE != kShapeGeneric) {

@@ -451,4 +451,32 @@ __device__ __forceinline__ void run_prog(float (&v)[W], int64_t m, int n0, int n
   }
 }
 
+// Integer epilogue of a realized conv/dense output element (IntEpi, fused.h):
+// exact int64 zero-point correction + bias, ONE clamp to the accumulator
+// dtype (or a trap at the lowest flat index), then the optional fused
+// requantize (reference interpreter.cpp:25-37, :238-264, :464-482).  Shared
+// by the tcgen05 kernel and the CUDA-core backend.
+__device__ __forceinline__ int32_t int_epi_value(const IntEpi& ie, int64_t acc, int o,
+                                                 int64_t flat) {
+  int64_t v = acc;
+  if (ie.wsum) v -= ie.zp0 * static_cast<int64_t>(__ldg(ie.wsum + o));
+  if (ie.bias) v += __ldg(ie.bias + o);
+  if (v < ie.acc_min || v > ie.acc_max) {
+    if (ie.trap) atomicMin(ie.trap, static_cast<unsigned long long>(flat));
+    v = v < ie.acc_min ? ie.acc_min : ie.acc_max;
+  }
+  if (ie.rq) {
+    // fixed_point_rescale, round half away from zero
+    const int64_t p = (v - ie.in_zp) * ie.mult;
+    int64_t q = p;
+    if (ie.shift > 0) {
+      const int64_t nudge = int64_t{1} << (ie.shift - 1);
+      q = p >= 0 ? (p + nudge) >> ie.shift : -((-p + nudge) >> ie.shift);
+    }
+    q += ie.out_zp;
+    v = q < ie.q_min ? ie.q_min : (q > ie.q_max ? ie.q_max : q);
+  }
+  return static_cast<int32_t>(v);
+}
+
 }  // namespace quantc::kern

@@ -143,6 +143,25 @@ struct TcConvSpec {
   IntEpi iepi;       // prog.shape == kShapeInt: integer epilogue
 };
 void tc_conv(const TcConvSpec& spec, cudaStream_t s);
+
+// CUDA-core integer conv/dense backend (conv_simt.cu): int16 codes or the
+// int16-accumulator signature; dp4a / 16-bit products, fused IntEpi epilogue
+struct SimtConvSpec {
+  const uint32_t* x;  // [N][HP][WP][Cw] words (pack_words)
+  const uint32_t* w;  // [KH*KW*Cw][O] words (pack_weight_words)
+  int N, HP, WP, Cw, O, KH, KW, sh, sw, OH, OW;
+  bool i16, u8;
+  IntEpi ie;
+};
+void conv_int_simt(const SimtConvSpec& spec, cudaStream_t s);
+// int32 NCHW values -> NHWC words (4 x 8-bit or 2 x 16-bit channels), the
+// ph/pw border filled with `fill`
+void pack_words(const int32_t* x, uint32_t* out, int N, int C, int H, int W, int ph, int pw,
+                int Cw, bool i16, int32_t fill, cudaStream_t s);
+// OIHW int32 weights -> words [taps*Cw][O] of w - zp1, wsum[o] += sum w';
+// *bad != 0 when some w - zp1 leaves the 8/16-bit range
+void pack_weight_words(const int32_t* w, uint32_t* out, int32_t* wsum, int* bad, int O, int C,
+                       int taps, int Cw, bool i16, int64_t zp1, cudaStream_t s);
 int tc_conv_bn(int O);  // output-channel tile the kernel uses for O channels
 
 // weight codes [O][Kpad], k = tap*ldk + c, from OIHW float weights (taps =

@@ -31,6 +31,7 @@ class CudaOps:
         L.qcu_synchronize.argtypes = [_P]
         L.qcu_set_engine_mode.argtypes = [C.c_int]
         L.qcu_counters.argtypes = [C.POINTER(C.c_int64)] * 4
+        L.qcu_simt_int_convs.argtypes = [C.POINTER(C.c_int64)]
 
     def _ok(self, rc):
         if rc != 0:
@@ -120,8 +121,10 @@ class CudaOps:
     def counters(self):
         v = [C.c_int64() for _ in range(4)]
         self.lib.qcu_counters(*[C.byref(x) for x in v])
+        s = C.c_int64()
+        self.lib.qcu_simt_int_convs(C.byref(s))
         return {"steps": v[0].value, "tcgen05_gemms": v[1].value, "f64_convs": v[2].value,
-                "fused_batches": v[3].value}
+                "fused_batches": v[3].value, "simt_int_convs": s.value}
 
 
 _ops = None

@@ -310,19 +310,21 @@ def int_conv_probe(n=2, c=16, h=12, w=12, o=24, k=3, stride=1, pad=1, dtype="int
     unsigned data, nonzero zp0 with padding, zp1 folding, accumulator
     saturation (int16 acc), and a fused requantize."""
     rng = np.random.default_rng(seed)
-    lo, hi = (-128, 127) if dtype == "int8" else (0, 255)
-    # default weight range: int8 values whose w - zp1 also fits int8
-    wlo = max(-128, -128 + zp1) if wlo is None else wlo
-    whi = min(127, 127 + zp1) if whi is None else whi
+    lo, hi = {"int8": (-128, 127), "uint8": (0, 255), "int16": (-32768, 32767)}[dtype]
+    # default weight range: values of the data's width whose w - zp1 fits it
+    wl, wh = (-32768, 32767) if dtype == "int16" else (-128, 127)
+    wlo = max(wl, wl + zp1) if wlo is None else wlo
+    whi = min(wh, wh + zp1) if whi is None else whi
+    wdt = "int16" if dtype == "int16" else "int8"
     gb = GraphBuilder()
     shape = [n, c] if dense else [n, c, h, w]
     x = gb.input("data", shape)
-    q = gb.op("quantize", [x], scale=1.0 / 32, zero_point=zp0, q_min=lo, q_max=hi,
-              out_dtype=dtype)
+    q = gb.op("quantize", [x], scale=1.0 / (4096 if dtype == "int16" else 32), zero_point=zp0,
+              q_min=lo, q_max=hi, out_dtype=dtype)
     if dense:
-        wt = gb.constant(rng.integers(wlo, whi + 1, (o, c)), dtype="int8")
+        wt = gb.constant(rng.integers(wlo, whi + 1, (o, c)), dtype=wdt)
     else:
-        wt = gb.constant(rng.integers(wlo, whi + 1, (o, c, k, k)), dtype="int8")
+        wt = gb.constant(rng.integers(wlo, whi + 1, (o, c, k, k)), dtype=wdt)
     b = gb.constant(rng.integers(-5000, 5000, (o,)), dtype="int32")
     attrs = dict(acc_dtype=acc, in_zero_points=[zp0, zp1])
     if dense:

@@ -14,21 +14,32 @@ pytestmark = pytest.mark.gpu
 
 RQ = (1 << 30, 41, 7, -3)  # multiplier 2^30, shift 41, in_zp 7, out_zp -3
 
+# case -> (probe config, backend that must run it: tc = tcgen05 kernel,
+# simt = CUDA-core backend, generic = the int64 reference-order kernel)
 CASES = {
-    "3x3_pad": dict(),
-    "3x3_zp0_pad": dict(zp0=3, zp1=-2),
-    "3x3_rq": dict(requant=RQ),
-    "3x3_zp_rq": dict(zp0=-4, zp1=1, requant=RQ),
-    "u8_zp0_pad": dict(dtype="uint8", zp0=100, requant=RQ),
-    "1x1": dict(k=1, pad=0, c=64, o=40),
-    "1x1_s2": dict(k=1, pad=0, stride=2, c=32, o=48, requant=RQ),
-    "3x3_s2": dict(stride=2, c=24, o=20, h=15, w=15),
-    "7x7_s2": dict(k=7, stride=2, pad=3, c=3, o=16, h=20, w=20),
-    "5x5_c200": dict(k=5, pad=2, c=200, o=130, h=9, w=9, zp0=5, requant=RQ),
-    "acc_int16_saturate": dict(acc="int16", dtype="uint8", zp0=100),
-    "dense": dict(dense=True, c=300, o=70, n=5, requant=RQ),
-    "dense_zp_int16": dict(dense=True, c=256, o=10, n=3, zp0=9, zp1=4, acc="int16"),
-    "w_zp1_out_of_int8": dict(zp1=-10, wlo=-128, whi=127),  # w - zp1 leaves int8: generic kernel
+    "3x3_pad": (dict(), "tc"),
+    "3x3_zp0_pad": (dict(zp0=3, zp1=-2), "tc"),
+    "3x3_rq": (dict(requant=RQ), "tc"),
+    "3x3_zp_rq": (dict(zp0=-4, zp1=1, requant=RQ), "tc"),
+    "u8_zp0_pad": (dict(dtype="uint8", zp0=100, requant=RQ), "tc"),
+    "1x1": (dict(k=1, pad=0, c=64, o=40), "tc"),
+    "1x1_s2": (dict(k=1, pad=0, stride=2, c=32, o=48, requant=RQ), "tc"),
+    "3x3_s2": (dict(stride=2, c=24, o=20, h=15, w=15), "tc"),
+    "7x7_s2": (dict(k=7, stride=2, pad=3, c=3, o=16, h=20, w=20), "tc"),
+    "5x5_c200": (dict(k=5, pad=2, c=200, o=130, h=9, w=9, zp0=5, requant=RQ), "tc"),
+    "dense": (dict(dense=True, c=300, o=70, n=5, requant=RQ), "tc"),
+    "w_zp1_out_of_int8": (dict(zp1=-10, wlo=-128, whi=127), "generic"),
+    # int16-accumulator backend ((i8, i8) -> i16) on CUDA cores
+    "acc_int16_saturate": (dict(acc="int16", dtype="uint8", zp0=100), "simt"),
+    "acc_int16_rq": (dict(acc="int16", zp0=-3, zp1=2, requant=RQ, c=40, o=70), "simt"),
+    "dense_zp_int16": (dict(dense=True, c=256, o=10, n=3, zp0=9, zp1=4, acc="int16"), "simt"),
+    "dense_int16_acc_big": (dict(dense=True, c=1000, o=37, n=40, acc="int16"), "simt"),
+    # int16 codes ((i16, i16) -> i32) on CUDA cores
+    "i16_3x3": (dict(dtype="int16", c=20, o=33), "simt"),
+    "i16_zp_rq_s2": (dict(dtype="int16", zp0=-700, zp1=5, stride=2, requant=(1 << 30, 50, 0, 1)),
+                     "simt"),
+    "i16_dense": (dict(dtype="int16", dense=True, c=77, o=12, n=2, zp0=40), "simt"),
+    "i16_w_out_of_range": (dict(dtype="int16", zp1=-10, wlo=-32768, whi=32767), "generic"),
 }
 
 
@@ -40,24 +51,32 @@ def _x(case, cfg, seed=1):
     return np.abs(x) if cfg.get("dtype") == "uint8" else x
 
 
+def _backend_counts(cuda_lib):
+    c = cuda_lib.counters()
+    return c["tcgen05_gemms"], c["simt_int_convs"]
+
+
 @pytest.mark.parametrize("case", list(CASES))
 def test_int_conv_bit_exact_vs_reference(b200, ref, cuda_lib, case):
-    cfg = CASES[case]
+    cfg, backend = CASES[case]
     doc, blob = F.int_conv_probe(**cfg)
     x = _x(case, cfg)
     yr, dtr = ref.eval_int(ref.graph(doc, blob), x)
-    before = cuda_lib.counters()["tcgen05_gemms"]
+    t0, s0 = _backend_counts(cuda_lib)
     yb, dtb = b200.eval_int(b200.graph(doc, blob), x)
-    used = cuda_lib.counters()["tcgen05_gemms"] - before
+    t1, s1 = _backend_counts(cuda_lib)
     assert dtb == dtr
     np.testing.assert_array_equal(yb, yr)
-    if case != "w_zp1_out_of_int8" and cuda_lib.tcgen05_available():
-        assert used >= 1, "integer conv did not run on tcgen05"
+    ran = {"tc": t1 - t0, "simt": s1 - s0}
+    if backend == "generic":
+        assert ran == {"tc": 0, "simt": 0}
+    else:
+        assert ran[backend] == 1 and sum(ran.values()) == 1, ran
 
 
-@pytest.mark.parametrize("case", ["acc_int16_saturate", "dense_zp_int16"])
+@pytest.mark.parametrize("case", ["acc_int16_saturate", "dense_zp_int16", "i16_3x3"])
 def test_int_conv_trap_matches_reference(b200, ref, case):
-    cfg = CASES[case]
+    cfg = CASES[case][0]
     doc, blob = F.int_conv_probe(**cfg)
     x = _x(case, cfg)
     with pytest.raises(Q.OverflowError_) as er:
