@@ -36,6 +36,15 @@ EngineMode engine_mode();
 int current_device();
 void* stream();       // cudaStream_t of the engine
 void* copy_stream();  // cudaStream_t for uploads that overlap engine work
+
+// Page-locked host ranges.  Datasets created through the C-ABI pin their
+// sample storage once (cudaHostRegister) so DeviceDataset DMAs straight from
+// it instead of packing into staging.  pin_host is best effort (false: not
+// pinned, e.g. no device or over QUANTC_PIN_MAX_MB); unpin_host before the
+// memory is freed.
+bool pin_host(const void* p, size_t bytes);
+void unpin_host(const void* p);
+bool host_pinned(const void* p, size_t bytes);
 void synchronize();
 size_t memory_budget_bytes();  // per-batch activation budget
 

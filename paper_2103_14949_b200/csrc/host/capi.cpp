@@ -451,7 +451,20 @@ int qc_dataset_create(const float* data, int64_t n_samples, const int64_t* sampl
   return run([&] {
     std::vector<int64_t> sh(sample_shape, sample_shape + ndim);
     int64_t per = shape_numel(sh);
+#ifdef QUANTC_B200
+    // B200: the samples' storage is page-locked for the dataset's lifetime,
+    // so predictions DMA straight from it (device.hpp pin_host)
+    auto ds = std::shared_ptr<Dataset>(new Dataset, [](Dataset* p) {
+      for (const Sample& s : *p) {
+        for (const Tensor& t : s.inputs) {
+          if (t.dtype().is_float() && t.numel() > 0) device::unpin_host(t.floats().data());
+        }
+      }
+      delete p;
+    });
+#else
     auto ds = std::make_shared<Dataset>();
+#endif
     ds->reserve(static_cast<size_t>(n_samples));
     for (int64_t i = 0; i < n_samples; ++i) {
       Sample s;
@@ -460,6 +473,12 @@ int qc_dataset_create(const float* data, int64_t n_samples, const int64_t* sampl
       if (labels) s.label = labels[i];
       ds->push_back(std::move(s));
     }
+#ifdef QUANTC_B200
+    for (const Sample& s : *ds) {
+      const Tensor& t = s.inputs[0];
+      if (t.numel() > 0) device::pin_host(t.floats().data(), static_cast<size_t>(t.numel()) * 4);
+    }
+#endif
     auto h = std::make_unique<qc_dataset>();
     h->d = std::move(ds);
     *out = h.release();

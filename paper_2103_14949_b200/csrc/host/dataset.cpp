@@ -119,7 +119,31 @@ DeviceDataset::DeviceDataset(const Graph& g, const Dataset& ds, int64_t first, i
       cudaStreamWaitEvent(us, alloc_done, 0);
       cudaEventDestroy(alloc_done);
     }
-    if (per * count > 0) {
+    bool pinned = per * count > 0;
+    for (int64_t s = 0; s < count && pinned; ++s) {
+      pinned = device::host_pinned(ds[static_cast<size_t>(first + s)].inputs[k].floats().data(),
+                                   static_cast<size_t>(per) * 4);
+    }
+    if (pinned) {
+      // page-locked samples (C-ABI datasets): DMA straight from them, merging
+      // samples that happen to be contiguous
+      const size_t bytes_per = static_cast<size_t>(per) * 4;
+      int64_t s = 0;
+      while (s < count) {
+        const auto* src = reinterpret_cast<const uint8_t*>(ds[static_cast<size_t>(first + s)].inputs[k].floats().data());
+        int64_t run = 1;
+        while (s + run < count &&
+               reinterpret_cast<const uint8_t*>(ds[static_cast<size_t>(first + s + run)].inputs[k].floats().data()) ==
+                   src + run * bytes_per) {
+          ++run;
+        }
+        const cudaError_t e = cudaMemcpyAsync(static_cast<uint8_t*>(buf.get()) + s * bytes_per, src,
+                                              static_cast<size_t>(run) * bytes_per,
+                                              cudaMemcpyHostToDevice, us);
+        if (e != cudaSuccess) throw DeviceError(std::string("dataset upload: ") + cudaGetErrorString(e));
+        s += run;
+      }
+    } else if (per * count > 0) {
       Staging& st = Staging::get();
       std::lock_guard<std::mutex> lk(st.mu());
       st.upload(static_cast<uint8_t*>(buf.get()), count, static_cast<size_t>(per) * 4,
@@ -191,10 +215,19 @@ std::shared_ptr<void> predict_streamed(const engine::Plan& plan, const Graph& g,
   auto preds = engine::device_alloc(static_cast<size_t>(std::max<int64_t>(1, n)) * 8);
   std::vector<std::unique_ptr<DeviceDataset>> dds;
   const int64_t per = (n + parts - 1) / parts;
+  // every part's buffers are allocated (engine-stream pool) and its upload
+  // queued on the copy stream BEFORE any forward is queued, so part k+1's DMA
+  // runs under part k's forward instead of waiting behind it
+  std::vector<int64_t> firsts;
   for (int64_t first = 0; first < n; first += per) {
-    const int64_t cnt = std::min(per, n - first);
-    dds.push_back(std::make_unique<DeviceDataset>(g, ds, first, cnt, device::copy_stream()));
-    const DeviceDataset& dd = *dds.back();
+    firsts.push_back(first);
+    dds.push_back(std::make_unique<DeviceDataset>(g, ds, first, std::min(per, n - first),
+                                                  device::copy_stream()));
+  }
+  for (size_t p = 0; p < dds.size(); ++p) {
+    const int64_t first = firsts[p];
+    const int64_t cnt = dds[p]->size();
+    const DeviceDataset& dd = *dds[p];
     dd.wait_ready();
     const int fb = static_cast<int>(std::min<int64_t>(cnt, 256));
     for (int64_t f = 0; f < cnt; f += fb) {

@@ -2,7 +2,10 @@
 // stream, stream-ordered memory pool, engine mode.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
+#include <cstdint>
+#include <map>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -73,6 +76,65 @@ Context& ctx() {
 void set_engine_mode(EngineMode m) { ctx().mode = static_cast<int>(m); }
 EngineMode engine_mode() { return static_cast<EngineMode>(ctx().mode.load()); }
 int current_device() { return ctx().dev; }
+namespace {
+struct PinRegistry {
+  std::mutex mu;
+  std::map<uintptr_t, size_t> ranges;  // start -> bytes
+  size_t total = 0;
+};
+PinRegistry& pins() {
+  static PinRegistry* r = new PinRegistry;  // outlives static destructors
+  return *r;
+}
+}  // namespace
+
+bool pin_host(const void* p, size_t bytes) {
+  if (!p || bytes == 0) return false;
+  static const size_t cap = [] {
+    const char* e = std::getenv("QUANTC_PIN_MAX_MB");
+    return (e ? static_cast<size_t>(std::max(0, std::atoi(e))) : size_t{16384}) << 20;
+  }();
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return false;
+  }
+  PinRegistry& r = pins();
+  std::lock_guard<std::mutex> lk(r.mu);
+  const auto key = reinterpret_cast<uintptr_t>(p);
+  if (r.ranges.count(key)) return true;
+  if (r.total + bytes > cap) return false;
+  ctx();
+  if (cudaHostRegister(const_cast<void*>(p), bytes, cudaHostRegisterDefault) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  r.ranges[key] = bytes;
+  r.total += bytes;
+  return true;
+}
+
+void unpin_host(const void* p) {
+  PinRegistry& r = pins();
+  std::lock_guard<std::mutex> lk(r.mu);
+  auto it = r.ranges.find(reinterpret_cast<uintptr_t>(p));
+  if (it == r.ranges.end()) return;
+  cudaHostUnregister(const_cast<void*>(p));
+  r.total -= it->second;
+  r.ranges.erase(it);
+}
+
+bool host_pinned(const void* p, size_t bytes) {
+  PinRegistry& r = pins();
+  std::lock_guard<std::mutex> lk(r.mu);
+  if (r.ranges.empty()) return false;
+  const auto a = reinterpret_cast<uintptr_t>(p);
+  auto it = r.ranges.upper_bound(a);
+  if (it == r.ranges.begin()) return false;
+  --it;
+  return a + bytes <= it->first + it->second;
+}
+
 void* stream() { return ctx().stream; }
 void* copy_stream() { return ctx().copy_stream; }
 

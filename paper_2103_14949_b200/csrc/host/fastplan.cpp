@@ -11,6 +11,7 @@
 #include <cstring>
 #include <functional>
 #include <limits>
+#include <numeric>
 #include <set>
 
 #include "quantc/device.hpp"
@@ -1153,6 +1154,70 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
     }
     optimise_tables(t, v0);
   }
+  // ---- epilogue shapes and fork aliasing.  A fork whose two stores carry
+  // identical constants writes identical bytes: the second value becomes an
+  // alias of the first buffer and the kernel stores once (one TMA store
+  // stream fewer on the add-fork layers, the largest writers of a step).
+  static const bool no_shapes = std::getenv("QUANTC_NO_SHAPES") != nullptr;
+  static const bool no_special = std::getenv("QUANTC_NO_SPECIAL") != nullptr;
+  static const bool no_alias = std::getenv("QUANTC_NO_FORK_ALIAS") != nullptr;
+  std::vector<int> shape0(stages_.size(), 0), shape_of(stages_.size(), 0);
+  std::vector<kern::EpiConsts> epi_of(stages_.size());
+  std::vector<double> sxw_of(stages_.size(), 0.0);
+  std::vector<char> drop2(stages_.size(), 0);
+  std::vector<int> alias(vals_.size());
+  std::iota(alias.begin(), alias.end(), 0);
+  for (size_t si = 0; si < stages_.size(); ++si) {
+    const Stage& st = *stages_[si];
+    if (st.kind != Stage::kGemm) continue;
+    const Val& dv = *vals_[static_cast<size_t>(st.in_val)];
+    sxw_of[si] = static_cast<double>(scale_by_step.count(dv.sq_step) ? scale_by_step.at(dv.sq_step) : 0.0f) *
+                 static_cast<double>(wfsq[si].s);
+    const int sh0 = no_shapes ? 0 : classify_shape(tabs[si], st.O);
+    shape0[si] = sh0;
+    kern::EpiConsts& e = epi_of[si];
+    int sh = sh0;
+    if (sh != 0 && !make_epi(tabs[si], sh, sxw_of[si], e)) sh = 0;
+    // flag-specialised kernels for the common constant profiles (fused.cuh)
+    if (!no_special) {
+      // a k = 1 store of a T-domain code: exact, at most a clamp
+      auto identity = [](const kern::EpiSq& q) {
+        return (q.flags & ~kern::kEpiNoClamp) == (kern::kEpiNonneg | kern::kEpiExact) &&
+               q.k == 1.0f && q.off == 0.0f;
+      };
+      auto same = [](const kern::EpiSq& a, const kern::EpiSq& b) {
+        return a.flags == b.flags && a.lo == b.lo && a.hi == b.hi;
+      };
+      if (sh == kern::kShapeSqStore && e.q[0].flags == kern::kEpiNonneg && identity(e.q[1])) {
+        sh = kern::kShapeSqStoreId;
+      } else if (sh == kern::kShapeAddFork && e.q[0].flags == 0 &&
+                 e.q[1].flags == kern::kEpiNonneg && identity(e.q[2]) && identity(e.q[3]) &&
+                 same(e.q[2], e.q[3])) {
+        sh = kern::kShapeAddForkId;
+      }
+    }
+    shape_of[si] = sh;
+    if (!no_alias && (sh == kern::kShapeAddFork || sh == kern::kShapeAddForkId) &&
+        st.n_out == 2 && std::memcmp(&e.q[2], &e.q[3], sizeof(kern::EpiSq)) == 0) {
+      const Val& v0 = *vals_[static_cast<size_t>(st.out_vals[0])];
+      const Val& v1 = *vals_[static_cast<size_t>(st.out_vals[1])];
+      if (v0.kind == v1.kind && v0.C == v1.C && v0.ld == v1.ld && v0.hw == v1.hw &&
+          v0.rows_ps == v1.rows_ps && !v0.s2d && !v1.s2d && (v0.zero_fill || !v1.zero_fill)) {
+        alias[static_cast<size_t>(st.out_vals[1])] = alias[static_cast<size_t>(st.out_vals[0])];
+        drop2[si] = 1;
+        // one output slot (0); the residual moves to slot 1 (= n_out)
+        e.slot_out[0] = 0;
+        e.slot_out[1] = -1;
+        if (e.slot_res >= 0) e.slot_res = 1;
+      }
+    }
+  }
+  auto buf_of = [&](int vid) { return arena_[static_cast<size_t>(alias[static_cast<size_t>(vid)])].get(); };
+  for (size_t si = 0; si < stages_.size(); ++si) {
+    for (size_t k = 0; k < stages_[si]->buf_vals.size(); ++k) {
+      tabs[si].buf[k].ptr = buf_of(stages_[si]->buf_vals[k]);
+    }
+  }
   const double t_tables = hprof ? us_since(t_start) : 0.0;
   ok_cuda(cudaMemcpyAsync(d_tables_.get(), tabs.data(), tabs.size() * sizeof(kern::StageTables),
                           cudaMemcpyHostToDevice, S()));
@@ -1161,8 +1226,7 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
 
   for (size_t si = 0; si < stages_.size(); ++si) {
     const Stage& st = *stages_[si];
-    ProgArgs pa{d_tabs + si, st.depth,
-                st.kind == Stage::kGemm && !std::getenv("QUANTC_NO_SHAPES") ? classify_shape(tabs[si], st.O) : 0};
+    ProgArgs pa{d_tabs + si, st.depth, shape0[si]};
     switch (st.kind) {
       case Stage::kInput: {
         const Val* sv = nullptr;
@@ -1189,12 +1253,12 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
         kern::PoolStores ps;
         if (st.C % 16 == 0 && v.ld % 16 == 0 && st.ph < st.pkh && st.pw < st.pkw &&
             pool_stores(tabs[si], scale_by_step.at(v.sq_step), ps)) {
-          kern::stage_maxpool_stores(static_cast<const int8_t*>(arena_[static_cast<size_t>(st.in_val)].get()),
+          kern::stage_maxpool_stores(static_cast<const int8_t*>(buf_of(st.in_val)),
                                      static_cast<int>(v.ld), batch * st.n0, st.C, st.H, st.W, st.OH,
                                      st.OW, st.pkh, st.pkw, st.sh, st.sw, st.ph, st.pw, ps, S());
           break;
         }
-        kern::stage_maxpool(static_cast<const int8_t*>(arena_[static_cast<size_t>(st.in_val)].get()),
+        kern::stage_maxpool(static_cast<const int8_t*>(buf_of(st.in_val)),
                             static_cast<int>(v.ld), scale_by_step.at(v.sq_step), batch * st.n0,
                             st.C, st.H, st.W, st.OH, st.OW, st.pkh, st.pkw, st.sh, st.sw, st.ph,
                             st.pw, pa, S());
@@ -1202,7 +1266,7 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
       }
       case Stage::kGap: {
         const Val& v = *vals_[static_cast<size_t>(st.in_val)];
-        kern::stage_gap(static_cast<const float*>(arena_[static_cast<size_t>(st.in_val)].get()),
+        kern::stage_gap(static_cast<const float*>(buf_of(st.in_val)),
                         v.ld, batch * st.n0, st.C, st.HW, pa, S());
         break;
       }
@@ -1236,7 +1300,7 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
           it = wcache_.emplace(ck, codes).first;
         }
         kern::TcConvSpec sp{};
-        sp.x = static_cast<const int8_t*>(arena_[static_cast<size_t>(st.in_val)].get());
+        sp.x = static_cast<const int8_t*>(buf_of(st.in_val));
         std::shared_ptr<void> packed;
         if (st.packed) {
           packed = engine::device_alloc(static_cast<size_t>(st.rows_out_ps * batch) * st.Kpad);
@@ -1272,30 +1336,10 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
         sp.OH = st.OH;
         sp.OW = st.OW;
         sp.bias = st.bias_const >= 0 ? plan_.constant(st.bias_const).f() : nullptr;
-        sp.scale = static_cast<double>(scale_by_step.count(dv.sq_step) ? scale_by_step.at(dv.sq_step) : 0.0f) *
-                   static_cast<double>(wf.s);
+        sp.scale = sxw_of[si];
         sp.prog = pa;
-        if (pa.shape != 0 && !make_epi(tabs[si], pa.shape, sp.scale, sp.epi)) sp.prog.shape = 0;
-        // flag-specialised kernels for the common constant profiles (fused.cuh)
-        if (!std::getenv("QUANTC_NO_SPECIAL")) {
-          // a k = 1 store of a T-domain code: exact, at most a clamp
-          auto identity = [](const kern::EpiSq& q) {
-            return (q.flags & ~kern::kEpiNoClamp) == (kern::kEpiNonneg | kern::kEpiExact) &&
-                   q.k == 1.0f && q.off == 0.0f;
-          };
-          auto same = [](const kern::EpiSq& a, const kern::EpiSq& b) {
-            return a.flags == b.flags && a.lo == b.lo && a.hi == b.hi;
-          };
-          const kern::EpiConsts& e = sp.epi;
-          if (sp.prog.shape == kern::kShapeSqStore && e.q[0].flags == kern::kEpiNonneg &&
-              identity(e.q[1])) {
-            sp.prog.shape = kern::kShapeSqStoreId;
-          } else if (sp.prog.shape == kern::kShapeAddFork && e.q[0].flags == 0 &&
-                     e.q[1].flags == kern::kEpiNonneg && identity(e.q[2]) && identity(e.q[3]) &&
-                     same(e.q[2], e.q[3])) {
-            sp.prog.shape = kern::kShapeAddForkId;
-          }
-        }
+        sp.prog.shape = shape_of[si];
+        sp.epi = epi_of[si];
         if (std::getenv("QUANTC_DUMP_PLAN")) {
           std::fprintf(stderr, "run stage %zu step %d shape %d -> %d flags %d %d %d %d ops", si,
                        st.step, pa.shape, sp.prog.shape, sp.epi.q[0].flags, sp.epi.q[1].flags,
@@ -1312,16 +1356,16 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
           std::fprintf(stderr, "\n");
         }
         sp.acc_bound = acc_bound[si];
-        sp.n_out = st.n_out;
-        for (int o = 0; o < st.n_out; ++o) {
+        sp.n_out = drop2[si] ? 1 : st.n_out;
+        for (int o = 0; o < sp.n_out; ++o) {
           const Val& ov = *vals_[static_cast<size_t>(st.out_vals[o])];
-          sp.out_ptr[o] = arena_[static_cast<size_t>(st.out_vals[o])].get();
+          sp.out_ptr[o] = buf_of(st.out_vals[o]);
           sp.out_cols[o] = ov.C;
           sp.out_ld[o] = ov.ld;
         }
         if (st.res_val >= 0) {
           const Val& rv = *vals_[static_cast<size_t>(st.res_val)];
-          sp.res_ptr = arena_[static_cast<size_t>(st.res_val)].get();
+          sp.res_ptr = buf_of(st.res_val);
           sp.res_cols = rv.C;
           sp.res_ld = rv.ld;
         }
@@ -1334,7 +1378,7 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
           const double M = static_cast<double>(sp.M);
           const double a_bytes = st.gather ? static_cast<double>(sp.Nimg) * st.H * st.W * sp.ld
                                            : M * st.Ktrue;
-          const double out_bytes = M * st.O * (st.n_out + (st.res_val >= 0 ? 1 : 0)) +
+          const double out_bytes = M * st.O * (sp.n_out + (st.res_val >= 0 ? 1 : 0)) +
                                    (pa.shape == 5 ? 4.0 * M * st.O : 0.0);
           device::profile_gemm_end(
               2.0 * M * st.O *

@@ -319,7 +319,8 @@ __device__ __forceinline__ void run_shape_epi(float (&x)[16], const EpiConsts& e
     epi_round(x, e.q[2]);                     // k = 1 store (q2 == q3): at most a clamp
     const int4 packed = epi_pack(x, e.q[2]);
     sts128(tile_addr(io, e.slot_out[0], cl), packed);
-    sts128(tile_addr(io, e.slot_out[1], cl), packed);
+    // slot_out[1] < 0: the fork's second value aliases the first buffer
+    if (e.slot_out[1] >= 0) sts128(tile_addr(io, e.slot_out[1], cl), packed);
     return;
   }
   epi_round(x, e.q[0]);
@@ -364,7 +365,7 @@ __device__ __forceinline__ void run_shape_epi(float (&x)[16], const EpiConsts& e
   }
   epi_next(x, y, e.q[2]);
   epi_store(y, e.q[2], io, e.slot_out[0], cl);
-  if (SHAPE == kShapeAddFork) {
+  if (SHAPE == kShapeAddFork && e.slot_out[1] >= 0) {
     epi_next(x, y, e.q[3]);
     epi_store(y, e.q[3], io, e.slot_out[1], cl);
   }
