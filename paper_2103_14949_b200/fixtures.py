@@ -286,6 +286,155 @@ def resnet(depth: int = 50, seed: int = 42, image: int = 224, classes: int = 100
     return Model(f"resnet{depth}", doc, blob, [1, 3, image, image], gb)
 
 
+# ---- exact rewrites of ops outside the reference op set --------
+#
+# The reference has no grouped/depthwise conv, concat or avg_pool2d
+# (graph.cpp:17-35).  Configs C3 (MobileNetV2) and C5 (Inception-v3) are built
+# from exact rewrites so the unmodified reference runs them:
+#   depthwise KxK      -> conv2d with block-diagonal weights (off-diagonal
+#                         taps are 0: x*0 adds a signed zero to a nonzero or
+#                         +0 double accumulator, so the sum is unchanged)
+#   concat(a, b, ...)  -> sum of 1x1 "placement" convs (identity blocks),
+#                         one nonzero term per output channel
+#   avg_pool KxK       -> depthwise conv with constant 1/(K*K) weights
+#                         (count_include_pad semantics)
+#   relu6              -> clip(0, 6)
+
+def _depthwise(gb, wts, x, k, stride=1, pad=None, gain=1.0, bias=True):
+    c = gb.shapes[x][1]
+    pad = k // 2 if pad is None else pad
+    w = np.zeros((c, c, k, k), np.float32)
+    dw = wts.rng.standard_normal((c, k, k), dtype=np.float32) * np.float32(gain * np.sqrt(2.0 / (k * k)))
+    for i in range(c):
+        w[i, i] = dw[i]
+    ins = [x, gb.constant(w)]
+    if bias:
+        ins.append(gb.constant(wts.bias(c)))
+    return gb.op("conv2d", ins, strides=[stride, stride], padding=[pad, pad])
+
+
+def _avg_pool(gb, x, k=3, stride=1, pad=1):
+    c = gb.shapes[x][1]
+    w = np.zeros((c, c, k, k), np.float32)
+    for i in range(c):
+        w[i, i] = np.float32(1.0 / (k * k))
+    return gb.op("conv2d", [x, gb.constant(w)], strides=[stride, stride], padding=[pad, pad])
+
+
+def _concat(gb, xs):
+    total = sum(gb.shapes[x][1] for x in xs)
+    out, off = None, 0
+    for x in xs:
+        c = gb.shapes[x][1]
+        p = np.zeros((total, c, 1, 1), np.float32)
+        for i in range(c):
+            p[off + i, i, 0, 0] = 1.0
+        y = gb.op("conv2d", [x, gb.constant(p)], strides=[1, 1], padding=[0, 0])
+        out = y if out is None else gb.op("add", [out, y])
+        off += c
+    return out
+
+
+def _relu6(gb, x):
+    return gb.op("clip", [x], a_min=0.0, a_max=6.0)
+
+
+def mobilenet_v2(seed: int = 11, image: int = 32, classes: int = 10, width: float = 0.25,
+                 blocks=None) -> Model:
+    """BASELINE config C3: MobileNetV2 (inverted residuals, relu6, linear
+    bottlenecks) with depthwise convs rewritten exactly (see above), for the
+    arm_vmlal_like int16-accumulation spec.  `blocks` = (t, c, n, s) rows;
+    the default is the paper's table at width `width`."""
+    cfg = blocks or [(1, 16, 1, 1), (6, 24, 2, 2), (6, 32, 3, 2), (6, 64, 4, 2),
+                     (6, 96, 3, 1), (6, 160, 3, 2), (6, 320, 1, 1)]
+
+    def ch(c):
+        return max(8, int(round(c * width / 8)) * 8)
+
+    gb = GraphBuilder()
+    wts = _Weights(seed)
+    x = gb.input("data", [1, 3, image, image])
+    h = _relu6(gb, _conv(gb, wts, x, ch(32), 3, stride=2, pad=1))
+    in_c = ch(32)
+    for t, c, n, s in cfg:
+        out_c = ch(c)
+        for i in range(n):
+            stride = s if i == 0 else 1
+            y = h
+            if t != 1:
+                y = _relu6(gb, _conv(gb, wts, y, in_c * t, 1))
+            y = _relu6(gb, _depthwise(gb, wts, y, 3, stride))
+            y = _conv(gb, wts, y, out_c, 1, gain=0.5)  # linear bottleneck
+            h = gb.op("add", [h, y]) if (stride == 1 and in_c == out_c) else y
+            in_c = out_c
+    h = _relu6(gb, _conv(gb, wts, h, max(ch(1280), 64), 1))
+    p = gb.op("global_avg_pool2d", [h])
+    f = gb.op("flatten", [p])
+    y = gb.op("dense", [f, gb.constant(wts.dense(classes, gb.shapes[f][1])),
+                        gb.constant(wts.bias(classes))])
+    gb.output(y)
+    doc, blob = gb.build()
+    return Model("mobilenet_v2", doc, blob, [1, 3, image, image], gb)
+
+
+def inception_v3(seed: int = 13, image: int = 35, classes: int = 10, width: int = 8,
+                 modules: int = 2, head: str = "flatten") -> Model:
+    """BASELINE config C5: an Inception-v3-style network (stem, Inception-A
+    modules with 1x1 / 1x1-3x3 / 1x1-3x3-3x3 / avgpool-1x1 branches, a
+    grid-reduction module, Inception-C-style 1x3/3x1 factorised branches) with
+    concat and avg_pool rewritten exactly (see above).  head "gap" is the
+    paper's global-average-pool classifier; "flatten" (default) keeps the
+    spatial map so random inputs give varied top-1 predictions, which the
+    search's agreement loss needs."""
+    gb = GraphBuilder()
+    wts = _Weights(seed)
+
+    def cbr(x, o, kh, kw=None, stride=1, ph=None, pw=None):
+        kw = kh if kw is None else kw
+        c = gb.shapes[x][1]
+        w = gb.constant(wts.conv(o, c, kh, kw))
+        ph = kh // 2 if ph is None else ph
+        pw = kw // 2 if pw is None else pw
+        y = gb.op("conv2d", [x, w, gb.constant(wts.bias(o))], strides=[stride, stride],
+                  padding=[ph, pw])
+        return gb.op("relu", [y])
+
+    x = gb.input("data", [1, 3, image, image])
+    h = cbr(x, 2 * width, 3, stride=2, ph=0, pw=0)
+    h = cbr(h, 2 * width, 3)
+    h = cbr(h, 4 * width, 3)
+    for _ in range(modules):  # Inception-A
+        b1 = cbr(h, 4 * width, 1)
+        b2 = cbr(cbr(h, 3 * width, 1), 4 * width, 3)
+        b3 = cbr(cbr(cbr(h, 4 * width, 1), 6 * width, 3), 6 * width, 3)
+        b4 = cbr(_avg_pool(gb, h), 2 * width, 1)
+        h = _concat(gb, [b1, b2, b3, b4])
+    # grid reduction: 3x3 stride 2 | 1x1-3x3-3x3 stride 2 | max pool
+    r1 = cbr(h, 8 * width, 3, stride=2, ph=0, pw=0)
+    r2 = cbr(cbr(h, 4 * width, 1), 6 * width, 3, stride=2, ph=0, pw=0)
+    r3 = gb.op("max_pool2d", [h], pool_size=[3, 3], strides=[2, 2], padding=[0, 0])
+    h = _concat(gb, [r1, r2, r3])
+    # Inception-C-style: 1x1 | 1x1 -> (1x3, 3x1)
+    c1 = cbr(h, 8 * width, 1)
+    c2 = cbr(h, 6 * width, 1)
+    c2 = _concat(gb, [cbr(c2, 4 * width, 1, 3), cbr(c2, 4 * width, 3, 1)])
+    h = _concat(gb, [c1, c2])
+    if head == "gap":
+        f = gb.op("flatten", [gb.op("global_avg_pool2d", [h])])
+    else:
+        # a linear 1x1 projection with zero-sum rows removes the relu
+        # features' common mode
+        w = wts.conv(2 * width, gb.shapes[h][1], 1, 1)
+        w -= w.mean(axis=1, keepdims=True)
+        f = gb.op("flatten", [gb.op("conv2d", [h, gb.constant(w)], strides=[1, 1],
+                                    padding=[0, 0])])
+    y = gb.op("dense", [f, gb.constant(wts.dense(classes, gb.shapes[f][1])),
+                        gb.constant(wts.bias(classes))])
+    gb.output(y)
+    doc, blob = gb.build()
+    return Model("inception_v3", doc, blob, [1, 3, image, image], gb)
+
+
 def overflow_dense(k: int = 256, value: int = 127, acc: str = "int16") -> Tuple[dict, bytes]:
     """Realized int8 dense probe from SPEC.md interpreter examples: quantize ->
     dense(int8, weights all `value`) with `acc` accumulator. 127*127*256 exceeds
