@@ -42,7 +42,13 @@ def _device(group) -> torch.device:
     return torch.device("cpu")
 
 
+def _single() -> bool:
+    return not (dist.is_available() and dist.is_initialized())
+
+
 def allreduce_extrema(mins: Sequence[float], maxs: Sequence[float], group=None):
+    if _single():  # one process: the local extrema are the global ones
+        return np.asarray(mins, np.float64), np.asarray(maxs, np.float64)
     dev = _device(group)
     lo = torch.tensor(list(mins), dtype=torch.float64, device=dev)
     hi = torch.tensor(list(maxs), dtype=torch.float64, device=dev)
@@ -52,6 +58,8 @@ def allreduce_extrema(mins: Sequence[float], maxs: Sequence[float], group=None):
 
 
 def allreduce_counts(counts: np.ndarray, group=None) -> np.ndarray:
+    if _single():
+        return np.ascontiguousarray(counts, np.int64)
     dev = _device(group)
     t = torch.from_numpy(np.ascontiguousarray(counts, np.int64)).to(dev)
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
