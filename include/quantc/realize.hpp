@@ -4,7 +4,8 @@
 // reference declares these but ships no implementation;
 // EdgeDecision/Strategy are the search output.  requantize_params,
 // choose_storage_dtype and rewrite_clip are implemented from SPEC.md
-// realize module (:593-672); realize() itself is §8(f) "next" work.
+// realize module (:593-672); realize() is implemented from that restatement
+// (host/realize.cpp), the reference only declares it.
 #pragma once
 
 #include <cstdint>
