@@ -93,6 +93,7 @@ struct FastPlan::Stage {
   int out_vals[2] = {-1, -1};
   int res_val = -1;
   double bias_absmax = 0.0;
+  double bias_absmin = std::numeric_limits<double>::infinity();  // smallest nonzero |bias|
   // space-to-depth stem conv (see Val::s2d): original channels / kernel and
   // the tap alignment shift
   bool s2d = false;
@@ -571,6 +572,54 @@ bool epi_from_code(double prev_s, bool prev_T, const kern::FSq& f, kern::EpiSq& 
   return exact_float(off, q.off);
 }
 
+// Saturating form of shapes 6/7 (fused.cuh run_shape_epi): sq i's input is
+// pre-scaled by 1/P_i (P_i a power of two, code range [-P_i, P_i - 1] for a
+// signed sq0 of shape 7, [0, P_i - 1] otherwise), so that add.rz.sat clamps
+// the low side and one min caps the high side.  Scaling by a power of two
+// commutes with RN / RZ rounding for normal floats, so every folded constant
+// must stay an exact normal float, and so must the smallest nonzero bias
+// term bias / s0 / P0.  Returns false when the shape must fall back.
+bool fold_saturating(int shape, double bias_absmin, kern::EpiConsts& e) {
+  auto code_range = [](const kern::EpiSq& q, double& lo, double& hi) {
+    lo = std::nearbyint(static_cast<double>(q.lo) + 0.5);
+    hi = std::nearbyint(static_cast<double>(q.hi) - 0.5);
+  };
+  auto pow2 = [](double v) { return v >= 1.0 && std::exp2(std::round(std::log2(v))) == v; };
+  auto scaled = [](float& v, double p) {
+    float out;
+    if (!exact_float(static_cast<double>(v) / p, out)) return false;
+    v = out;
+    return true;
+  };
+  const double M = kern::kMagic;
+  kern::EpiConsts f = e;
+  double lo0, hi0;
+  code_range(f.q[0], lo0, hi0);
+  const bool signed0 = shape == kern::kShapeAddForkId;
+  const double P0 = signed0 ? -lo0 : hi0 + 1.0;
+  if (!pow2(P0) || hi0 != P0 - 1.0 || lo0 != (signed0 ? -P0 : 0.0)) return false;
+  if (!scaled(f.q[0].k, P0) || !scaled(f.inv0, P0)) return false;
+  // the bias table entries bias * inv0 / P0 must stay normal floats
+  if (std::isfinite(bias_absmin) && bias_absmin * static_cast<double>(f.inv0) < 0x1p-125) {
+    return false;
+  }
+  f.sat_half[0] = static_cast<float>(0.5 / P0);
+  f.sat_p[0] = static_cast<float>(P0);
+  f.sat_top[0] = static_cast<float>(signed0 ? P0 - 1.0 : M + hi0);
+  if (signed0) {
+    double lo1, hi1;
+    code_range(f.q[1], lo1, hi1);
+    const double P1 = hi1 + 1.0;
+    if (lo1 != 0.0 || !pow2(P1)) return false;
+    if (!scaled(f.q[1].k, P1) || !scaled(f.ka, P1) || !scaled(f.ka_off, P1)) return false;
+    f.sat_half[1] = static_cast<float>(0.5 / P1);
+    f.sat_p[1] = static_cast<float>(P1);
+    f.sat_top[1] = static_cast<float>(M + hi1);
+  }
+  e = f;
+  return true;
+}
+
 // Fold the shape's sq chain into EpiConsts (fused.h).  Every factor is a
 // power of two, so each folded product / offset must be an exact float;
 // returns false (interpreter fallback) when one is not.
@@ -791,6 +840,7 @@ void FastPlan::compile() {
           st->bias_const = in[2];
           for (float bv : steps[static_cast<size_t>(in[2])].node->payload->floats()) {
             st->bias_absmax = std::max(st->bias_absmax, std::fabs(static_cast<double>(bv)));
+            if (bv != 0.0f) st->bias_absmin = std::min(st->bias_absmin, std::fabs(static_cast<double>(bv)));
           }
         }
         const Val& dv = *vals_[static_cast<size_t>(st->in_val)];
@@ -1188,11 +1238,12 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
       auto same = [](const kern::EpiSq& a, const kern::EpiSq& b) {
         return a.flags == b.flags && a.lo == b.lo && a.hi == b.hi;
       };
-      if (sh == kern::kShapeSqStore && e.q[0].flags == kern::kEpiNonneg && identity(e.q[1])) {
+      if (sh == kern::kShapeSqStore && e.q[0].flags == kern::kEpiNonneg && identity(e.q[1]) &&
+          fold_saturating(kern::kShapeSqStoreId, st.bias_absmin, e)) {
         sh = kern::kShapeSqStoreId;
       } else if (sh == kern::kShapeAddFork && e.q[0].flags == 0 &&
                  e.q[1].flags == kern::kEpiNonneg && identity(e.q[2]) && identity(e.q[3]) &&
-                 same(e.q[2], e.q[3])) {
+                 same(e.q[2], e.q[3]) && fold_saturating(kern::kShapeAddForkId, st.bias_absmin, e)) {
         sh = kern::kShapeAddForkId;
       }
     }

@@ -242,23 +242,6 @@ __device__ __forceinline__ void epi_next(const float (&R)[16], float (&y)[16], c
   epi_round(y, q);
 }
 
-// compile-time-flag rounding (the specialised shapes): same arithmetic as
-// epi_round with the branches resolved at compile time
-template <bool NONNEG>
-__device__ __forceinline__ void epi_round_ct(float (&x)[16], const EpiSq& q) {
-#pragma unroll
-  for (int j = 0; j < 16; ++j) x[j] = fminf(fmaxf(x[j], q.lo), q.hi);
-  if constexpr (NONNEG) {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) x[j] = __fadd_rz(__fadd_rz(x[j], 0.5f), kMagic);
-  } else {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      x[j] = copysignf(__fsub_rn(__fadd_rz(__fadd_rz(fabsf(x[j]), 0.5f), kMagic), kMagic), x[j]);
-    }
-  }
-}
-
 // 16 rounded codes -> 16 int8 bytes (low byte of the T-domain bits)
 __device__ __forceinline__ int4 epi_pack(float (&R)[16], const EpiSq& q) {
   if (!(q.flags & kEpiNonneg)) {
@@ -291,6 +274,13 @@ __device__ __forceinline__ void codes_to_floats(const uint32_t (&w)[4], float (&
   }
 }
 
+// RZ(a + b) clamped to [0, 1] on the FMA pipe (PTX add.rz.sat: NaN -> +0)
+__device__ __forceinline__ float add_rz_sat(float a, float b) {
+  float r;
+  asm("add.rz.sat.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
 // x[16] = conv output scaled into sq0's grid (x0 = v / s0); runs the shape
 // (m, n): the element coordinates of x[0] (shape 5 stores to global rows)
 template <int SHAPE>
@@ -298,13 +288,17 @@ __device__ __forceinline__ void run_shape_epi(float (&x)[16], const EpiConsts& e
                                               const TileIo& io, int cl, int64_t m, int n,
                                               bool row_ok) {
   if constexpr (SHAPE == kShapeSqStoreId) {
-    epi_round_ct<true>(x, e.q[0]);
+    // sq0 (codes [0, P0 - 1]) on x0 / P0: T = M + min(floor(max(RZ(x0 + 1/2), 0)), P0 - 1)
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float u = add_rz_sat(x[j], e.sat_half[0]);
+      x[j] = fminf(__fmaf_rz(u, e.sat_p[0], kMagic), e.sat_top[0]);
+    }
     epi_round(x, e.q[1]);  // k = 1 store: at most a clamp in the T-domain
     sts128(tile_addr(io, e.slot_out[0], cl), epi_pack(x, e.q[1]));
     return;
   }
   if constexpr (SHAPE == kShapeAddForkId) {
-    epi_round_ct<false>(x, e.q[0]);
     const int4 raw = lds128(tile_addr(io, e.slot_res, cl));
     const uint32_t wr[4] = {static_cast<uint32_t>(raw.x) ^ 0x80808080u,
                             static_cast<uint32_t>(raw.y) ^ 0x80808080u,
@@ -312,10 +306,18 @@ __device__ __forceinline__ void run_shape_epi(float (&x)[16], const EpiConsts& e
                             static_cast<uint32_t>(raw.w) ^ 0x80808080u};
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
+      // sq0, signed codes [-P0, P0 - 1], on x0 / P0: half-away rounding of
+      // |x0| saturated at P0, sign restored, positive side capped at P0 - 1
+      const float u0 = add_rz_sat(fabsf(x[j]), e.sat_half[0]);
+      const float t0 = __fsub_rn(__fmaf_rz(u0, e.sat_p[0], kMagic), kMagic);
+      const float r0 = fminf(copysignf(t0, x[j]), e.sat_top[0]);
+      // residual add (k1, ka, ka_off pre-scaled by 1/P1), then sq1 (codes
+      // [0, P1 - 1]) into the T-domain
       const float C = __uint_as_float(__byte_perm(wr[j >> 2], 0x4B000000u, 0x7650u + (j & 3)));
-      x[j] = __fmaf_rn(x[j], e.q[1].k, __fmaf_rn(C, e.ka, e.ka_off));
+      const float x1 = __fmaf_rn(r0, e.q[1].k, __fmaf_rn(C, e.ka, e.ka_off));
+      const float u1 = add_rz_sat(x1, e.sat_half[1]);
+      x[j] = fminf(__fmaf_rz(u1, e.sat_p[1], kMagic), e.sat_top[1]);
     }
-    epi_round_ct<true>(x, e.q[1]);
     epi_round(x, e.q[2]);                     // k = 1 store (q2 == q3): at most a clamp
     const int4 packed = epi_pack(x, e.q[2]);
     sts128(tile_addr(io, e.slot_out[0], cl), packed);

@@ -145,6 +145,13 @@ struct EpiConsts {
   float f32_s, f32_off;
   float* f32_ptr;
   int64_t f32_ld;
+  // shapes 6/7 (saturating rounding, fastplan fold_saturating): sq i's
+  // input arrives pre-scaled by 1/P_i (P_i = 2^p: the code range is
+  // [-P_i, P_i - 1] or [0, P_i - 1]) so add.rz.sat clamps the low side on the
+  // FMA pipe; sat_top caps the high side (one min instead of a clamp pair)
+  float sat_half[2];  // 0.5 / P_i
+  float sat_p[2];     // P_i
+  float sat_top[2];   // highest code (r-domain) or M + highest code (T-domain)
 };
 
 // Straight-line epilogues for the program shapes that dominate CNN graphs
