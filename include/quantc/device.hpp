@@ -36,6 +36,7 @@ EngineMode engine_mode();
 int current_device();
 void* stream();       // cudaStream_t of the engine
 void* copy_stream();  // cudaStream_t for uploads that overlap engine work
+void* aux_stream(int i);  // i-th auxiliary compute stream (created on first use)
 
 // Page-locked host ranges.  Datasets created through the C-ABI pin their
 // sample storage once (cudaHostRegister) so DeviceDataset DMAs straight from

@@ -138,6 +138,19 @@ bool host_pinned(const void* p, size_t bytes) {
 void* stream() { return ctx().stream; }
 void* copy_stream() { return ctx().copy_stream; }
 
+void* aux_stream(int i) {
+  static std::mutex mu;
+  static std::vector<cudaStream_t>* streams = new std::vector<cudaStream_t>;  // never destroyed
+  ctx();
+  std::lock_guard<std::mutex> lk(mu);
+  while (static_cast<int>(streams->size()) <= i) {
+    cudaStream_t s = nullptr;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    streams->push_back(s);
+  }
+  return (*streams)[static_cast<size_t>(i)];
+}
+
 void synchronize() {
   cudaError_t e = cudaStreamSynchronize(ctx().stream);
   if (e != cudaSuccess) throw DeviceError(std::string("CUDA error: ") + cudaGetErrorString(e));

@@ -101,9 +101,11 @@ std::vector<int64_t> infer_shape(const Node& n, const std::vector<const std::vec
 
 }  // namespace
 
-std::shared_ptr<void> device_alloc(size_t bytes) {
+std::shared_ptr<void> device_alloc(size_t bytes) { return device_alloc_on(S(), bytes); }
+
+std::shared_ptr<void> device_alloc_on(void* stream, size_t bytes) {
   void* p = nullptr;
-  cudaStream_t s = S();
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (bytes == 0) bytes = 16;
   cuda_ok(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync");
   return std::shared_ptr<void>(p, [s](void* q) { cudaFreeAsync(q, s); });

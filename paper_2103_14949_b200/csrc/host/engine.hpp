@@ -43,6 +43,8 @@ struct DevTensor {
 
 // stream-ordered device allocation
 std::shared_ptr<void> device_alloc(size_t bytes);
+// stream-ordered allocation (and free) on `stream` (a cudaStream_t)
+std::shared_ptr<void> device_alloc_on(void* stream, size_t bytes);
 
 kern::SqParams resolve_sq(const QParams& p);  // validates like simulate.cpp:47-60
 QParams qparams_of(const Node& n, const SimBinding* binding);
@@ -81,6 +83,10 @@ class Plan {
   // lazily compiled fused int8 dataflow (engine v2) for this graph
   mutable std::shared_ptr<fast::FastPlan> fused;
   mutable bool fused_tried = false;
+  // extra instances of the fused plan, one per auxiliary stream: a batch is
+  // split across the streams so one forward's per-layer fill/drain latency
+  // overlaps another's work (dataset.cpp fused_predict)
+  mutable std::vector<std::shared_ptr<fast::FastPlan>> fused_aux;
 };
 
 // Process-wide cache of compiled plans (device-resident constants, the fused

@@ -26,6 +26,8 @@ using kern::ProgInstr;
 
 namespace {
 cudaStream_t S() { return static_cast<cudaStream_t>(device::stream()); }
+// inside FastPlan members: the instance's stream
+#define ST() static_cast<cudaStream_t>(stream_ ? stream_ : device::stream())
 void ok_cuda(cudaError_t e) {
   if (e != cudaSuccess) throw DeviceError(std::string("fastplan: ") + cudaGetErrorString(e));
 }
@@ -1127,11 +1129,11 @@ void FastPlan::ensure_arena(int batch) {
   arena_.clear();
   for (const auto& v : vals_) {
     const size_t bytes = static_cast<size_t>(v->bytes_ps()) * batch;
-    auto buf = engine::device_alloc(bytes + 64);
-    if (v->zero_fill) ok_cuda(cudaMemsetAsync(buf.get(), 0, bytes + 64, S()));
+    auto buf = engine::device_alloc_on(ST(), bytes + 64);
+    if (v->zero_fill) ok_cuda(cudaMemsetAsync(buf.get(), 0, bytes + 64, ST()));
     arena_.push_back(buf);
   }
-  d_tables_ = engine::device_alloc(std::max<size_t>(1, stages_.size()) * sizeof(kern::StageTables));
+  d_tables_ = engine::device_alloc_on(ST(), std::max<size_t>(1, stages_.size()) * sizeof(kern::StageTables));
   arena_batch_ = batch;
 }
 
@@ -1271,7 +1273,7 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
   }
   const double t_tables = hprof ? us_since(t_start) : 0.0;
   ok_cuda(cudaMemcpyAsync(d_tables_.get(), tabs.data(), tabs.size() * sizeof(kern::StageTables),
-                          cudaMemcpyHostToDevice, S()));
+                          cudaMemcpyHostToDevice, ST()));
   const auto* d_tabs = static_cast<const kern::StageTables*>(d_tables_.get());
   const double t_upload = hprof ? us_since(t_start) : 0.0;
 
@@ -1292,11 +1294,11 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
           kern::stage_input_s2d(inputs.at(static_cast<size_t>(st.input_k)), batch * st.n0,
                                 sv->s2d_C, sv->s2d_H, sv->s2d_W, tabs[si].sq[st.code[0].a],
                                 static_cast<int8_t*>(arena_[static_cast<size_t>(st.buf_vals[0])].get()),
-                                S());
+                                ST());
           break;
         }
         kern::stage_input(inputs.at(static_cast<size_t>(st.input_k)), batch * st.n0, st.C, st.HW,
-                          pa, S());
+                          pa, ST());
         break;
       }
       case Stage::kMaxpool: {
@@ -1306,19 +1308,19 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
             pool_stores(tabs[si], scale_by_step.at(v.sq_step), ps)) {
           kern::stage_maxpool_stores(static_cast<const int8_t*>(buf_of(st.in_val)),
                                      static_cast<int>(v.ld), batch * st.n0, st.C, st.H, st.W, st.OH,
-                                     st.OW, st.pkh, st.pkw, st.sh, st.sw, st.ph, st.pw, ps, S());
+                                     st.OW, st.pkh, st.pkw, st.sh, st.sw, st.ph, st.pw, ps, ST());
           break;
         }
         kern::stage_maxpool(static_cast<const int8_t*>(buf_of(st.in_val)),
                             static_cast<int>(v.ld), scale_by_step.at(v.sq_step), batch * st.n0,
                             st.C, st.H, st.W, st.OH, st.OW, st.pkh, st.pkw, st.sh, st.sw, st.ph,
-                            st.pw, pa, S());
+                            st.pw, pa, ST());
         break;
       }
       case Stage::kGap: {
         const Val& v = *vals_[static_cast<size_t>(st.in_val)];
         kern::stage_gap(static_cast<const float*>(buf_of(st.in_val)),
-                        v.ld, batch * st.n0, st.C, st.HW, pa, S());
+                        v.ld, batch * st.n0, st.C, st.HW, pa, ST());
         break;
       }
       case Stage::kGemm: {
@@ -1334,30 +1336,30 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
         if (it == wcache_.end()) {
           // codes [O][Kpad], then one int: max_o sum_k |code| (the accumulator bound)
           const size_t cbytes = static_cast<size_t>(st.O) * st.Kpad;
-          auto codes = engine::device_alloc(cbytes + 16);
+          auto codes = engine::device_alloc_on(ST(), cbytes + 16);
           if (st.s2d) {
             kern::weight_codes_s2d(plan_.constant(st.w_const).f(), static_cast<int8_t*>(codes.get()),
                                    st.O, st.s2d_C, st.s2d_KH, st.s2d_KW, st.KH, st.KW, st.s2d_dh,
-                                   st.s2d_dw, st.Kpad, wf, S());
+                                   st.s2d_dw, st.Kpad, wf, ST());
           } else {
             kern::weight_codes_v2(plan_.constant(st.w_const).f(),
                                   static_cast<int8_t*>(codes.get()), st.O,
                                   st.dense ? (st.taps > 1 ? dv.cs : dv.C) : st.C, st.taps, st.ldk,
-                                  st.Kpad, wf, S());
+                                  st.Kpad, wf, ST());
           }
           int* l1 = reinterpret_cast<int*>(static_cast<int8_t*>(codes.get()) + cbytes);
-          ok_cuda(cudaMemsetAsync(l1, 0, sizeof(int), S()));
-          kern::weight_l1_max(static_cast<const int8_t*>(codes.get()), st.O, st.Kpad, l1, S());
+          ok_cuda(cudaMemsetAsync(l1, 0, sizeof(int), ST()));
+          kern::weight_l1_max(static_cast<const int8_t*>(codes.get()), st.O, st.Kpad, l1, ST());
           it = wcache_.emplace(ck, codes).first;
         }
         kern::TcConvSpec sp{};
         sp.x = static_cast<const int8_t*>(buf_of(st.in_val));
         std::shared_ptr<void> packed;
         if (st.packed) {
-          packed = engine::device_alloc(static_cast<size_t>(st.rows_out_ps * batch) * st.Kpad);
+          packed = engine::device_alloc_on(ST(), static_cast<size_t>(st.rows_out_ps * batch) * st.Kpad);
           kern::pack_im2col(sp.x, static_cast<int8_t*>(packed.get()), batch * st.n0, st.H, st.W,
                             st.C, static_cast<int>(dv.ld), st.KH, st.KW, st.sh, st.sw, st.ph,
-                            st.pw, st.OH, st.OW, st.Ktrue, st.Kpad, S());
+                            st.pw, st.OH, st.OW, st.Ktrue, st.Kpad, ST());
         }
         sp.w = static_cast<const int8_t*>(it->second.get());
         sp.w_l1 = reinterpret_cast<const int*>(sp.w + static_cast<size_t>(st.O) * st.Kpad);
@@ -1422,7 +1424,7 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
         }
         const bool prof = device::profile_enabled();
         if (prof) device::profile_gemm_begin();
-        kern::tc_conv(sp, S());
+        kern::tc_conv(sp, ST());
         if (prof) {
           // algorithmic bytes: input codes once (the NHWC tensor for implicit
           // GEMM), weight codes, bias, code outputs / residual / fp32 outputs
@@ -1444,14 +1446,14 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
   }
   device::counters().fused_batches++;
   const float* out = static_cast<const float*>(arena_[static_cast<size_t>(out_val_)].get());
-  kern::argmax_rows(out, batch, out_per_sample_, d_preds, S());
+  kern::argmax_rows(out, batch, out_per_sample_, d_preds, ST());
   if (hprof) {
     std::fprintf(stderr, "predict host us: tables %.1f upload %.1f launches %.1f total %.1f\n",
                  t_tables, t_upload - t_tables, us_since(t_start) - t_upload, us_since(t_start));
   }
   if (d_scores) {
     ok_cuda(cudaMemcpyAsync(d_scores, out, static_cast<size_t>(batch) * out_per_sample_ * 4,
-                            cudaMemcpyDeviceToDevice, S()));
+                            cudaMemcpyDeviceToDevice, ST()));
   }
 }
 

@@ -38,12 +38,16 @@ class FastPlan {
   void predict(int batch, const std::vector<const float*>& inputs, const SimBinding* binding,
                int64_t* d_preds, float* d_scores = nullptr);
   int64_t out_per_sample() const { return out_per_sample_; }
+  // stream this instance enqueues on (nullptr: the engine stream); every
+  // buffer, table upload and launch of the instance is ordered on it
+  void set_stream(void* s) { stream_ = s; }
 
   struct Val;
   struct Stage;
 
  private:
   const engine::Plan& plan_;
+  void* stream_ = nullptr;
   bool ok_ = false;
   std::string why_;
   std::vector<std::unique_ptr<Val>> vals_;
