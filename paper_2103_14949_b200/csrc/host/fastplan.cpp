@@ -1123,44 +1123,61 @@ bool FastPlan::eligible(const SimBinding* binding, bool exact, std::string* why)
   return true;
 }
 
-void FastPlan::ensure_arena(int batch) {
+void FastPlan::ensure_arena(int batch, int group) {
   // buffers are batch-major rows: a smaller batch runs on a prefix
-  if (arena_batch_ >= batch) return;
-  arena_.clear();
+  Arena& ar = arenas_[static_cast<size_t>(group)];
+  if (ar.batch >= batch) return;
+  ar.bufs.clear();
   for (const auto& v : vals_) {
     const size_t bytes = static_cast<size_t>(v->bytes_ps()) * batch;
     auto buf = engine::device_alloc_on(ST(), bytes + 64);
     if (v->zero_fill) ok_cuda(cudaMemsetAsync(buf.get(), 0, bytes + 64, ST()));
-    arena_.push_back(buf);
+    ar.bufs.push_back(buf);
   }
-  d_tables_ = engine::device_alloc_on(ST(), std::max<size_t>(1, stages_.size()) * sizeof(kern::StageTables));
-  arena_batch_ = batch;
+  ar.tables = engine::device_alloc_on(ST(), std::max<size_t>(1, stages_.size()) * sizeof(kern::StageTables));
+  ar.batch = batch;
 }
 
-void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
-                       const SimBinding* binding, int64_t* d_preds, float* d_scores) {
-  static const bool hprof = std::getenv("QUANTC_HOST_PROF") != nullptr;
-  const auto t_start = std::chrono::steady_clock::now();
-  auto us_since = [&](std::chrono::steady_clock::time_point t0) {
-    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
-  };
-  ensure_arena(batch);
-  // weight codes are cached per (stage, weight sq parameters); a long search
-  // visits many weight bit-widths, so keep roughly the last few bindings
-  // (freed stream-ordered: in-flight launches keep their codes)
-  if (wcache_.size() > 4 * stages_.size()) wcache_.clear();
-  // ---- per-run tables: FSq per sq node, clip bounds, buffer descriptors
-  std::vector<FSq> fsq(sq_steps_.size());
-  std::vector<float> scale_of_sq_step;
+// Per-binding state of one forward: the host-built tables, epilogue shapes /
+// constants, fork aliases, and the arena (group) it runs in.
+struct FastPlan::Run {
+  int group = 0;
+  int batch = 0;
+  std::vector<const float*> inputs;
+  const SimBinding* binding = nullptr;
+  int64_t* d_preds = nullptr;
+  float* d_scores = nullptr;
+  std::vector<FSq> fsq, wfsq;
   std::map<int, float> scale_by_step;
+  std::vector<double> acc_bound;
+  std::vector<kern::StageTables> tabs;
+  std::vector<int> shape0, shape_of;
+  std::vector<kern::EpiConsts> epi_of;
+  std::vector<double> sxw_of;
+  std::vector<char> drop2;
+  std::vector<int> alias;
+  const kern::StageTables* d_tabs = nullptr;
+  std::vector<std::shared_ptr<void>> keep;  // per-run temporaries (stream-ordered frees)
+};
+
+void FastPlan::prepare(Run& r) {
+  ensure_arena(r.batch, r.group);
+  const SimBinding* binding = r.binding;
+  auto& fsq = r.fsq;
+  auto& scale_by_step = r.scale_by_step;
+  auto& wfsq = r.wfsq;
+  auto& acc_bound = r.acc_bound;
+  auto& tabs = r.tabs;
+  // ---- per-run tables: FSq per sq node, clip bounds, buffer descriptors
+  fsq.assign(sq_steps_.size(), FSq{});
   for (size_t k = 0; k < sq_steps_.size(); ++k) {
     const QParams p = engine::qparams_of(*plan_.steps()[static_cast<size_t>(sq_steps_[k])].node, binding);
     fsq[k] = make_fsq(p);
     scale_by_step[sq_steps_[k]] = fsq[k].s;
   }
   // weight-edge sq parameters and |accumulator| bounds of the GEMM stages
-  std::vector<FSq> wfsq(stages_.size());
-  std::vector<double> acc_bound(stages_.size(), 0.0);
+  wfsq.assign(stages_.size(), FSq{});
+  acc_bound.assign(stages_.size(), 0.0);
   for (size_t si = 0; si < stages_.size(); ++si) {
     const Stage& st = *stages_[si];
     if (st.kind != Stage::kGemm) continue;
@@ -1171,7 +1188,7 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
     acc_bound[si] = kreal * code_absmax(df) * code_absmax(wfsq[si]);
   }
   // one compact table block per stage (instructions + referenced params)
-  std::vector<kern::StageTables> tabs(stages_.size());
+  tabs.assign(stages_.size(), kern::StageTables{});
   for (size_t si = 0; si < stages_.size(); ++si) {
     const Stage& st = *stages_[si];
     kern::StageTables& t = tabs[si];
@@ -1185,7 +1202,10 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
     for (size_t k = 0; k < st.buf_vals.size(); ++k) {
       const int vid = st.buf_vals[k];
       const Val& v = *vals_[static_cast<size_t>(vid)];
-      t.buf[k] = ProgBuf{arena_[static_cast<size_t>(vid)].get(), v.ld, v.hw, v.cs, v.kind,
+      // the value's own buffer (shape 5 folds it into f32_ptr); re-pointed
+      // below once fork aliases are known
+      t.buf[k] = ProgBuf{arenas_[static_cast<size_t>(r.group)].bufs[static_cast<size_t>(vid)].get(),
+                         v.ld, v.hw, v.cs, v.kind,
                          v.kind == 0 ? scale_by_step.at(v.sq_step) : 1.0f,
                          k < st.buf_slot.size() ? st.buf_slot[k] : -1, 0};
     }
@@ -1213,11 +1233,18 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
   static const bool no_shapes = std::getenv("QUANTC_NO_SHAPES") != nullptr;
   static const bool no_special = std::getenv("QUANTC_NO_SPECIAL") != nullptr;
   static const bool no_alias = std::getenv("QUANTC_NO_FORK_ALIAS") != nullptr;
-  std::vector<int> shape0(stages_.size(), 0), shape_of(stages_.size(), 0);
-  std::vector<kern::EpiConsts> epi_of(stages_.size());
-  std::vector<double> sxw_of(stages_.size(), 0.0);
-  std::vector<char> drop2(stages_.size(), 0);
-  std::vector<int> alias(vals_.size());
+  auto& shape0 = r.shape0;
+  auto& shape_of = r.shape_of;
+  auto& epi_of = r.epi_of;
+  auto& sxw_of = r.sxw_of;
+  auto& drop2 = r.drop2;
+  auto& alias = r.alias;
+  shape0.assign(stages_.size(), 0);
+  shape_of.assign(stages_.size(), 0);
+  epi_of.assign(stages_.size(), kern::EpiConsts{});
+  sxw_of.assign(stages_.size(), 0.0);
+  drop2.assign(stages_.size(), 0);
+  alias.resize(vals_.size());
   std::iota(alias.begin(), alias.end(), 0);
   for (size_t si = 0; si < stages_.size(); ++si) {
     const Stage& st = *stages_[si];
@@ -1250,6 +1277,8 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
       }
     }
     shape_of[si] = sh;
+    static const bool epi_nop = std::getenv("QUANTC_EXPERIMENT_EPI_NOP") != nullptr;
+    if (epi_nop) e.pad_ = 0x5A5A;  // wrong results: timing experiments only
     if (!no_alias && (sh == kern::kShapeAddFork || sh == kern::kShapeAddForkId) &&
         st.n_out == 2 && std::memcmp(&e.q[2], &e.q[3], sizeof(kern::EpiSq)) == 0) {
       const Val& v0 = *vals_[static_cast<size_t>(st.out_vals[0])];
@@ -1265,196 +1294,287 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
       }
     }
   }
-  auto buf_of = [&](int vid) { return arena_[static_cast<size_t>(alias[static_cast<size_t>(vid)])].get(); };
   for (size_t si = 0; si < stages_.size(); ++si) {
     for (size_t k = 0; k < stages_[si]->buf_vals.size(); ++k) {
-      tabs[si].buf[k].ptr = buf_of(stages_[si]->buf_vals[k]);
+      tabs[si].buf[k].ptr = buf(r, stages_[si]->buf_vals[k]);
     }
   }
-  const double t_tables = hprof ? us_since(t_start) : 0.0;
-  ok_cuda(cudaMemcpyAsync(d_tables_.get(), tabs.data(), tabs.size() * sizeof(kern::StageTables),
+  Arena& ar = arenas_[static_cast<size_t>(r.group)];
+  ok_cuda(cudaMemcpyAsync(ar.tables.get(), tabs.data(), tabs.size() * sizeof(kern::StageTables),
                           cudaMemcpyHostToDevice, ST()));
-  const auto* d_tabs = static_cast<const kern::StageTables*>(d_tables_.get());
-  const double t_upload = hprof ? us_since(t_start) : 0.0;
+  r.d_tabs = static_cast<const kern::StageTables*>(ar.tables.get());
+}
 
-  for (size_t si = 0; si < stages_.size(); ++si) {
-    const Stage& st = *stages_[si];
-    ProgArgs pa{d_tabs + si, st.depth, shape0[si]};
-    switch (st.kind) {
-      case Stage::kInput: {
-        const Val* sv = nullptr;
-        for (int vid : st.buf_vals) {
-          if (vals_[static_cast<size_t>(vid)]->s2d) sv = vals_[static_cast<size_t>(vid)].get();
-        }
-        if (sv) {
-          // compile guarantees the program is the single store into the s2d value
-          if (st.code.size() != 1 || st.code[0].op != kern::kPSqStore8) {
-            throw EvalError("fastplan: space-to-depth input stage with a compound program");
-          }
-          kern::stage_input_s2d(inputs.at(static_cast<size_t>(st.input_k)), batch * st.n0,
-                                sv->s2d_C, sv->s2d_H, sv->s2d_W, tabs[si].sq[st.code[0].a],
-                                static_cast<int8_t*>(arena_[static_cast<size_t>(st.buf_vals[0])].get()),
-                                ST());
-          break;
-        }
-        kern::stage_input(inputs.at(static_cast<size_t>(st.input_k)), batch * st.n0, st.C, st.HW,
-                          pa, ST());
-        break;
-      }
-      case Stage::kMaxpool: {
-        const Val& v = *vals_[static_cast<size_t>(st.in_val)];
-        kern::PoolStores ps;
-        if (st.C % 16 == 0 && v.ld % 16 == 0 && st.ph < st.pkh && st.pw < st.pkw &&
-            pool_stores(tabs[si], scale_by_step.at(v.sq_step), ps)) {
-          kern::stage_maxpool_stores(static_cast<const int8_t*>(buf_of(st.in_val)),
-                                     static_cast<int>(v.ld), batch * st.n0, st.C, st.H, st.W, st.OH,
-                                     st.OW, st.pkh, st.pkw, st.sh, st.sw, st.ph, st.pw, ps, ST());
-          break;
-        }
-        kern::stage_maxpool(static_cast<const int8_t*>(buf_of(st.in_val)),
-                            static_cast<int>(v.ld), scale_by_step.at(v.sq_step), batch * st.n0,
-                            st.C, st.H, st.W, st.OH, st.OW, st.pkh, st.pkw, st.sh, st.sw, st.ph,
-                            st.pw, pa, ST());
-        break;
-      }
-      case Stage::kGap: {
-        const Val& v = *vals_[static_cast<size_t>(st.in_val)];
-        kern::stage_gap(static_cast<const float*>(buf_of(st.in_val)),
-                        v.ld, batch * st.n0, st.C, st.HW, pa, ST());
-        break;
-      }
-      case Stage::kGemm: {
-        const Val& dv = *vals_[static_cast<size_t>(st.in_val)];
-        const int wslot = sq_index_.count(st.w_sq) ? sq_index_.at(st.w_sq) : -1;
-        const QParams wp = engine::qparams_of(*plan_.steps()[static_cast<size_t>(st.w_sq)].node, binding);
-        (void)wslot;
-        (void)wp;
-        const FSq wf = wfsq[si];
-        std::string key(reinterpret_cast<const char*>(&wf), sizeof(FSq));
-        auto ck = std::make_pair(static_cast<int>(si), key);
-        auto it = wcache_.find(ck);
-        if (it == wcache_.end()) {
-          // codes [O][Kpad], then one int: max_o sum_k |code| (the accumulator bound)
-          const size_t cbytes = static_cast<size_t>(st.O) * st.Kpad;
-          auto codes = engine::device_alloc_on(ST(), cbytes + 16);
-          if (st.s2d) {
-            kern::weight_codes_s2d(plan_.constant(st.w_const).f(), static_cast<int8_t*>(codes.get()),
-                                   st.O, st.s2d_C, st.s2d_KH, st.s2d_KW, st.KH, st.KW, st.s2d_dh,
-                                   st.s2d_dw, st.Kpad, wf, ST());
-          } else {
-            kern::weight_codes_v2(plan_.constant(st.w_const).f(),
-                                  static_cast<int8_t*>(codes.get()), st.O,
-                                  st.dense ? (st.taps > 1 ? dv.cs : dv.C) : st.C, st.taps, st.ldk,
-                                  st.Kpad, wf, ST());
-          }
-          int* l1 = reinterpret_cast<int*>(static_cast<int8_t*>(codes.get()) + cbytes);
-          ok_cuda(cudaMemsetAsync(l1, 0, sizeof(int), ST()));
-          kern::weight_l1_max(static_cast<const int8_t*>(codes.get()), st.O, st.Kpad, l1, ST());
-          it = wcache_.emplace(ck, codes).first;
-        }
-        kern::TcConvSpec sp{};
-        sp.x = static_cast<const int8_t*>(buf_of(st.in_val));
-        std::shared_ptr<void> packed;
-        if (st.packed) {
-          packed = engine::device_alloc_on(ST(), static_cast<size_t>(st.rows_out_ps * batch) * st.Kpad);
-          kern::pack_im2col(sp.x, static_cast<int8_t*>(packed.get()), batch * st.n0, st.H, st.W,
-                            st.C, static_cast<int>(dv.ld), st.KH, st.KW, st.sh, st.sw, st.ph,
-                            st.pw, st.OH, st.OW, st.Ktrue, st.Kpad, ST());
-        }
-        sp.w = static_cast<const int8_t*>(it->second.get());
-        sp.w_l1 = reinterpret_cast<const int*>(sp.w + static_cast<size_t>(st.O) * st.Kpad);
-        sp.x_absmax = static_cast<int>(
-            code_absmax(fsq[static_cast<size_t>(sq_index_.at(dv.sq_step))]));
-        sp.M = st.rows_out_ps * batch;
-        sp.O = st.O;
-        sp.Kpad = st.Kpad;
-        sp.gather = st.gather ? 1 : 0;
-        sp.Ktrue = st.Ktrue;
-        sp.lda = static_cast<int>(dv.ld);
-        if (st.packed) {
-          sp.x = static_cast<const int8_t*>(packed.get());
-          sp.lda = st.Kpad;
-        }
-        sp.Nimg = batch * st.n0;
-        sp.H = st.H;
-        sp.W = st.W;
-        sp.C = st.C;
-        sp.ld = static_cast<int>(dv.ld);
-        sp.KH = st.KH;
-        sp.KW = st.KW;
-        sp.sh = st.sh;
-        sp.sw = st.sw;
-        sp.ph = st.ph;
-        sp.pw = st.pw;
-        sp.OH = st.OH;
-        sp.OW = st.OW;
-        sp.bias = st.bias_const >= 0 ? plan_.constant(st.bias_const).f() : nullptr;
-        sp.scale = sxw_of[si];
-        sp.prog = pa;
-        sp.prog.shape = shape_of[si];
-        sp.epi = epi_of[si];
-        if (std::getenv("QUANTC_DUMP_PLAN")) {
-          std::fprintf(stderr, "run stage %zu step %d shape %d -> %d flags %d %d %d %d ops", si,
-                       st.step, pa.shape, sp.prog.shape, sp.epi.q[0].flags, sp.epi.q[1].flags,
-                       sp.epi.q[2].flags, sp.epi.q[3].flags);
-          for (int pc = 0; pc < tabs[si].n_code; ++pc) {
-            const kern::ProgInstr& in = tabs[si].code[pc];
-            std::fprintf(stderr, " %d", in.op);
-            if (in.op == kern::kPSq || in.op == kern::kPSqStore8) {
-              const FSq& f = tabs[si].sq[in.a];
-              std::fprintf(stderr, "[zp%g acc%d pt%d q%g..%g s%g]", f.zp, f.has_acc, f.passthrough,
-                           f.qmin, f.qmax, f.s);
-            }
-          }
-          std::fprintf(stderr, "\n");
-        }
-        sp.acc_bound = acc_bound[si];
-        sp.n_out = drop2[si] ? 1 : st.n_out;
-        for (int o = 0; o < sp.n_out; ++o) {
-          const Val& ov = *vals_[static_cast<size_t>(st.out_vals[o])];
-          sp.out_ptr[o] = buf_of(st.out_vals[o]);
-          sp.out_cols[o] = ov.C;
-          sp.out_ld[o] = ov.ld;
-        }
-        if (st.res_val >= 0) {
-          const Val& rv = *vals_[static_cast<size_t>(st.res_val)];
-          sp.res_ptr = buf_of(st.res_val);
-          sp.res_cols = rv.C;
-          sp.res_ld = rv.ld;
-        }
-        const bool prof = device::profile_enabled();
-        if (prof) device::profile_gemm_begin();
-        kern::tc_conv(sp, ST());
-        if (prof) {
-          // algorithmic bytes: input codes once (the NHWC tensor for implicit
-          // GEMM), weight codes, bias, code outputs / residual / fp32 outputs
-          const double M = static_cast<double>(sp.M);
-          const double a_bytes = st.gather ? static_cast<double>(sp.Nimg) * st.H * st.W * sp.ld
-                                           : M * st.Ktrue;
-          const double out_bytes = M * st.O * (sp.n_out + (st.res_val >= 0 ? 1 : 0)) +
-                                   (pa.shape == 5 ? 4.0 * M * st.O : 0.0);
-          device::profile_gemm_end(
-              2.0 * M * st.O *
-                  (st.dense ? st.Ktrue
-                            : (st.s2d ? st.s2d_C * st.s2d_KH * st.s2d_KW : st.C * st.KH * st.KW)),
-              a_bytes + static_cast<double>(st.O) * st.Ktrue + 4.0 * st.O + out_bytes);
-        }
-        device::counters().tcgen05_gemms++;
-        break;
+void* FastPlan::buf(const Run& r, int vid) const {
+  const int root = r.alias.empty() ? vid : r.alias[static_cast<size_t>(vid)];
+  return arenas_[static_cast<size_t>(r.group)].bufs[static_cast<size_t>(root)].get();
+}
+
+// weight codes of stage si under the run's binding (cached per FSq), and the
+// tcgen05 launch spec of the stage for run r
+void FastPlan::gemm_spec(Run& r, size_t si, kern::TcConvSpec& sp) {
+  const Stage& st = *stages_[si];
+  const Val& dv = *vals_[static_cast<size_t>(st.in_val)];
+  const FSq wf = r.wfsq[si];
+  std::string key(reinterpret_cast<const char*>(&wf), sizeof(FSq));
+  auto ck = std::make_pair(static_cast<int>(si), key);
+  auto it = wcache_.find(ck);
+  if (it == wcache_.end()) {
+    // codes [O][Kpad], then one int: max_o sum_k |code| (the accumulator bound)
+    const size_t cbytes = static_cast<size_t>(st.O) * st.Kpad;
+    auto codes = engine::device_alloc_on(ST(), cbytes + 16);
+    if (st.s2d) {
+      kern::weight_codes_s2d(plan_.constant(st.w_const).f(), static_cast<int8_t*>(codes.get()),
+                             st.O, st.s2d_C, st.s2d_KH, st.s2d_KW, st.KH, st.KW, st.s2d_dh,
+                             st.s2d_dw, st.Kpad, wf, ST());
+    } else {
+      kern::weight_codes_v2(plan_.constant(st.w_const).f(),
+                            static_cast<int8_t*>(codes.get()), st.O,
+                            st.dense ? (st.taps > 1 ? dv.cs : dv.C) : st.C, st.taps, st.ldk,
+                            st.Kpad, wf, ST());
+    }
+    int* l1 = reinterpret_cast<int*>(static_cast<int8_t*>(codes.get()) + cbytes);
+    ok_cuda(cudaMemsetAsync(l1, 0, sizeof(int), ST()));
+    kern::weight_l1_max(static_cast<const int8_t*>(codes.get()), st.O, st.Kpad, l1, ST());
+    it = wcache_.emplace(ck, codes).first;
+  }
+  r.keep.push_back(it->second);  // a cache clear must not free codes this run uses
+  sp = kern::TcConvSpec{};
+  sp.x = static_cast<const int8_t*>(buf(r, st.in_val));
+  sp.lda = static_cast<int>(dv.ld);
+  if (st.packed) {
+    auto packed = engine::device_alloc_on(ST(), static_cast<size_t>(st.rows_out_ps * r.batch) * st.Kpad);
+    kern::pack_im2col(sp.x, static_cast<int8_t*>(packed.get()), r.batch * st.n0, st.H, st.W,
+                      st.C, static_cast<int>(dv.ld), st.KH, st.KW, st.sh, st.sw, st.ph,
+                      st.pw, st.OH, st.OW, st.Ktrue, st.Kpad, ST());
+    sp.x = static_cast<const int8_t*>(packed.get());
+    sp.lda = st.Kpad;
+    r.keep.push_back(packed);
+  }
+  sp.w = static_cast<const int8_t*>(it->second.get());
+  sp.w_l1 = reinterpret_cast<const int*>(sp.w + static_cast<size_t>(st.O) * st.Kpad);
+  sp.x_absmax = static_cast<int>(code_absmax(r.fsq[static_cast<size_t>(sq_index_.at(dv.sq_step))]));
+  sp.M = st.rows_out_ps * r.batch;
+  sp.O = st.O;
+  sp.Kpad = st.Kpad;
+  sp.gather = st.gather ? 1 : 0;
+  sp.Ktrue = st.Ktrue;
+  sp.Nimg = r.batch * st.n0;
+  sp.H = st.H;
+  sp.W = st.W;
+  sp.C = st.C;
+  sp.ld = static_cast<int>(dv.ld);
+  sp.KH = st.KH;
+  sp.KW = st.KW;
+  sp.sh = st.sh;
+  sp.sw = st.sw;
+  sp.ph = st.ph;
+  sp.pw = st.pw;
+  sp.OH = st.OH;
+  sp.OW = st.OW;
+  sp.bias = st.bias_const >= 0 ? plan_.constant(st.bias_const).f() : nullptr;
+  sp.scale = r.sxw_of[si];
+  sp.prog = ProgArgs{r.d_tabs + si, st.depth, r.shape_of[si]};
+  sp.epi = r.epi_of[si];
+  if (std::getenv("QUANTC_DUMP_PLAN")) {
+    std::fprintf(stderr, "run stage %zu step %d shape %d -> %d flags %d %d %d %d ops", si,
+                 st.step, r.shape0[si], sp.prog.shape, sp.epi.q[0].flags, sp.epi.q[1].flags,
+                 sp.epi.q[2].flags, sp.epi.q[3].flags);
+    for (int pc = 0; pc < r.tabs[si].n_code; ++pc) {
+      const kern::ProgInstr& in = r.tabs[si].code[pc];
+      std::fprintf(stderr, " %d", in.op);
+      if (in.op == kern::kPSq || in.op == kern::kPSqStore8) {
+        const FSq& f = r.tabs[si].sq[in.a];
+        std::fprintf(stderr, "[zp%g acc%d pt%d q%g..%g s%g]", f.zp, f.has_acc, f.passthrough,
+                     f.qmin, f.qmax, f.s);
       }
     }
+    std::fprintf(stderr, "\n");
   }
-  device::counters().fused_batches++;
-  const float* out = static_cast<const float*>(arena_[static_cast<size_t>(out_val_)].get());
-  kern::argmax_rows(out, batch, out_per_sample_, d_preds, ST());
-  if (hprof) {
-    std::fprintf(stderr, "predict host us: tables %.1f upload %.1f launches %.1f total %.1f\n",
-                 t_tables, t_upload - t_tables, us_since(t_start) - t_upload, us_since(t_start));
+  sp.acc_bound = r.acc_bound[si];
+  sp.n_out = r.drop2[si] ? 1 : st.n_out;
+  for (int o = 0; o < sp.n_out; ++o) {
+    const Val& ov = *vals_[static_cast<size_t>(st.out_vals[o])];
+    sp.out_ptr[o] = buf(r, st.out_vals[o]);
+    sp.out_cols[o] = ov.C;
+    sp.out_ld[o] = ov.ld;
   }
-  if (d_scores) {
-    ok_cuda(cudaMemcpyAsync(d_scores, out, static_cast<size_t>(batch) * out_per_sample_ * 4,
+  if (st.res_val >= 0) {
+    const Val& rv = *vals_[static_cast<size_t>(st.res_val)];
+    sp.res_ptr = buf(r, st.res_val);
+    sp.res_cols = rv.C;
+    sp.res_ld = rv.ld;
+  }
+  sp.groups = 1;
+}
+
+void FastPlan::launch_gemm(size_t si, const kern::TcConvSpec& sp) {
+  const Stage& st = *stages_[si];
+  const bool prof = device::profile_enabled();
+  if (prof) device::profile_gemm_begin();
+  kern::tc_conv(sp, ST());
+  if (prof) {
+    // algorithmic bytes: input codes once (the NHWC tensor for implicit
+    // GEMM), weight codes, bias, code outputs / residual / fp32 outputs
+    const double M = static_cast<double>(sp.M) * sp.groups;
+    const double a_bytes = st.gather ? static_cast<double>(sp.Nimg) * sp.groups * st.H * st.W * sp.ld
+                                     : M * st.Ktrue;
+    const double out_bytes = M * st.O * (sp.n_out + (st.res_val >= 0 ? 1 : 0)) +
+                             (sp.prog.shape == kern::kShapeAddF32 ? 4.0 * M * st.O : 0.0);
+    device::profile_gemm_end(
+        2.0 * M * st.O *
+            (st.dense ? st.Ktrue
+                      : (st.s2d ? st.s2d_C * st.s2d_KH * st.s2d_KW : st.C * st.KH * st.KW)),
+        a_bytes + static_cast<double>(st.O) * st.Ktrue * sp.groups + 4.0 * st.O + out_bytes);
+  }
+  device::counters().tcgen05_gemms++;
+}
+
+void FastPlan::run_stage(Run& r, size_t si) {
+  const Stage& st = *stages_[si];
+  ProgArgs pa{r.d_tabs + si, st.depth, r.shape0[si]};
+  const int batch = r.batch;
+  switch (st.kind) {
+    case Stage::kInput: {
+      const Val* sv = nullptr;
+      for (int vid : st.buf_vals) {
+        if (vals_[static_cast<size_t>(vid)]->s2d) sv = vals_[static_cast<size_t>(vid)].get();
+      }
+      if (sv) {
+        // compile guarantees the program is the single store into the s2d value
+        if (st.code.size() != 1 || st.code[0].op != kern::kPSqStore8) {
+          throw EvalError("fastplan: space-to-depth input stage with a compound program");
+        }
+        kern::stage_input_s2d(r.inputs.at(static_cast<size_t>(st.input_k)), batch * st.n0,
+                              sv->s2d_C, sv->s2d_H, sv->s2d_W, r.tabs[si].sq[st.code[0].a],
+                              static_cast<int8_t*>(buf(r, st.buf_vals[0])), ST());
+        break;
+      }
+      kern::stage_input(r.inputs.at(static_cast<size_t>(st.input_k)), batch * st.n0, st.C, st.HW,
+                        pa, ST());
+      break;
+    }
+    case Stage::kMaxpool: {
+      const Val& v = *vals_[static_cast<size_t>(st.in_val)];
+      kern::PoolStores ps;
+      if (st.C % 16 == 0 && v.ld % 16 == 0 && st.ph < st.pkh && st.pw < st.pkw &&
+          pool_stores(r.tabs[si], r.scale_by_step.at(v.sq_step), ps)) {
+        kern::stage_maxpool_stores(static_cast<const int8_t*>(buf(r, st.in_val)),
+                                   static_cast<int>(v.ld), batch * st.n0, st.C, st.H, st.W, st.OH,
+                                   st.OW, st.pkh, st.pkw, st.sh, st.sw, st.ph, st.pw, ps, ST());
+        break;
+      }
+      kern::stage_maxpool(static_cast<const int8_t*>(buf(r, st.in_val)),
+                          static_cast<int>(v.ld), r.scale_by_step.at(v.sq_step), batch * st.n0,
+                          st.C, st.H, st.W, st.OH, st.OW, st.pkh, st.pkw, st.sh, st.sw, st.ph,
+                          st.pw, pa, ST());
+      break;
+    }
+    case Stage::kGap: {
+      const Val& v = *vals_[static_cast<size_t>(st.in_val)];
+      kern::stage_gap(static_cast<const float*>(buf(r, st.in_val)), v.ld, batch * st.n0, st.C,
+                      st.HW, pa, ST());
+      break;
+    }
+    case Stage::kGemm: {
+      kern::TcConvSpec sp;
+      gemm_spec(r, si, sp);
+      launch_gemm(si, sp);
+      break;
+    }
+  }
+}
+
+void FastPlan::finish(Run& r) {
+  const float* out = static_cast<const float*>(buf(r, out_val_));
+  kern::argmax_rows(out, r.batch, out_per_sample_, r.d_preds, ST());
+  if (r.d_scores) {
+    ok_cuda(cudaMemcpyAsync(r.d_scores, out, static_cast<size_t>(r.batch) * out_per_sample_ * 4,
                             cudaMemcpyDeviceToDevice, ST()));
   }
+  device::counters().fused_batches++;
+}
+
+void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
+                       const SimBinding* binding, int64_t* d_preds, float* d_scores) {
+  static const bool hprof = std::getenv("QUANTC_HOST_PROF") != nullptr;
+  const auto t_start = std::chrono::steady_clock::now();
+  // weight codes are cached per (stage, weight sq parameters); a long search
+  // visits many weight bit-widths, so keep roughly the last few bindings
+  // (freed stream-ordered: in-flight launches keep their codes)
+  if (wcache_.size() > 4 * stages_.size()) wcache_.clear();
+  Run r;
+  r.group = 0;
+  r.batch = batch;
+  r.inputs = inputs;
+  r.binding = binding;
+  r.d_preds = d_preds;
+  r.d_scores = d_scores;
+  prepare(r);
+  const auto t_prep = std::chrono::steady_clock::now();
+  for (size_t si = 0; si < stages_.size(); ++si) run_stage(r, si);
+  finish(r);
+  if (hprof) {
+    auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+    std::fprintf(stderr, "predict host us: tables+upload %.1f launches %.1f\\n", us(t_start, t_prep),
+                 us(t_prep, std::chrono::steady_clock::now()));
+  }
+}
+
+// Two bindings over the same batch of samples in one pass: every GEMM stage
+// whose two specs are launch-compatible runs as ONE grouped tcgen05 launch
+// (twice the tiles: the per-layer pipeline fill / drain and launch latency are
+// paid once for both); other stages run per binding.  Each binding has its
+// own arena, tables and outputs, so results equal two predict() calls.
+void FastPlan::predict_pair(int batch, const std::vector<const float*>& inputs,
+                            const SimBinding* b0, const SimBinding* b1, int64_t* preds0,
+                            int64_t* preds1) {
+  if (wcache_.size() > 4 * stages_.size()) wcache_.clear();
+  Run r[2];
+  const SimBinding* bs[2] = {b0, b1};
+  int64_t* ps[2] = {preds0, preds1};
+  for (int g = 0; g < 2; ++g) {
+    r[g].group = g;
+    r[g].batch = batch;
+    r[g].inputs = inputs;
+    r[g].binding = bs[g];
+    r[g].d_preds = ps[g];
+    prepare(r[g]);
+  }
+  static const bool no_group = std::getenv("QUANTC_NO_GROUPED") != nullptr;
+  for (size_t si = 0; si < stages_.size(); ++si) {
+    if (stages_[si]->kind != Stage::kGemm) {
+      run_stage(r[0], si);
+      run_stage(r[1], si);
+      continue;
+    }
+    kern::TcConvSpec s0, s1;
+    gemm_spec(r[0], si, s0);
+    gemm_spec(r[1], si, s1);
+    const int sh = s0.prog.shape;
+    const bool shape_kernel = sh != kern::kShapeGeneric && sh != kern::kShapeInt;
+    if (!no_group && shape_kernel && s1.prog.shape == sh && s0.n_out == s1.n_out &&
+        (s0.res_ptr != nullptr) == (s1.res_ptr != nullptr) && s0.lda == s1.lda) {
+      s0.groups = 2;
+      s0.x1 = s1.x;
+      s0.w1 = s1.w;
+      s0.w_l1_1 = s1.w_l1;
+      s0.x_absmax1 = s1.x_absmax;
+      s0.scale1 = s1.scale;
+      s0.out_ptr1[0] = s1.out_ptr[0];
+      s0.out_ptr1[1] = s1.out_ptr[1];
+      s0.res_ptr1 = s1.res_ptr;
+      s0.epi1 = s1.epi;
+      // the wider of the two accumulator bounds decides the generic path
+      s0.acc_bound = std::max(s0.acc_bound, s1.acc_bound);
+      launch_gemm(si, s0);
+    } else {
+      launch_gemm(si, s0);
+      launch_gemm(si, s1);
+    }
+  }
+  finish(r[0]);
+  finish(r[1]);
 }
 
 }  // namespace quantc::fast

@@ -37,6 +37,10 @@ class FastPlan {
   // d_scores (optional): the output rows themselves, [batch x out_per_sample()]
   void predict(int batch, const std::vector<const float*>& inputs, const SimBinding* binding,
                int64_t* d_preds, float* d_scores = nullptr);
+  // two bindings over the same samples; compatible GEMM stages run as one
+  // grouped tcgen05 launch (fastplan.cpp)
+  void predict_pair(int batch, const std::vector<const float*>& inputs, const SimBinding* b0,
+                    const SimBinding* b1, int64_t* preds0, int64_t* preds1);
   int64_t out_per_sample() const { return out_per_sample_; }
   // stream this instance enqueues on (nullptr: the engine stream); every
   // buffer, table upload and launch of the instance is ordered on it
@@ -58,17 +62,27 @@ class FastPlan {
   int out_val_ = -1;
   int64_t out_per_sample_ = 0;
   std::shared_ptr<void> d_code_;  // all programs, uploaded once
-  // per-batch arena
-  int arena_batch_ = -1;
-  std::vector<std::shared_ptr<void>> arena_;
-  std::shared_ptr<void> d_bufs_;
-  std::shared_ptr<void> d_tables_;  // FSq table + clip table
+  // per-batch arenas (one per concurrently prepared binding): a buffer per
+  // materialised value and the stage-table block
+  struct Arena {
+    int batch = -1;
+    std::vector<std::shared_ptr<void>> bufs;
+    std::shared_ptr<void> tables;
+  };
+  Arena arenas_[2];
   // weight code cache: (stage, FSq bytes) -> codes
   std::map<std::pair<int, std::string>, std::shared_ptr<void>> wcache_;
 
+  struct Run;
   void compile();
   void fail(const std::string& why);
-  void ensure_arena(int batch);
+  void ensure_arena(int batch, int group);
+  void prepare(Run& r);
+  void* buf(const Run& r, int vid) const;
+  void gemm_spec(Run& r, size_t si, kern::TcConvSpec& sp);
+  void launch_gemm(size_t si, const kern::TcConvSpec& sp);
+  void run_stage(Run& r, size_t si);
+  void finish(Run& r);
 };
 
 }  // namespace quantc::fast

@@ -44,7 +44,7 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 128;
 constexpr int UMMA_K = 32;
-constexpr int MAX_STAGES = 8;
+constexpr int MAX_STAGES = 16;
 // warp layout, by epilogue width EPIW: EPIW epilogue warps (EPIW/4 per TMEM
 // lane quarter), then the producer warps (4 for the cp.async gather, whose
 // 128 threads own one A row each; 1 for the TMA producers), then the MMA warp
@@ -173,6 +173,16 @@ struct TcArgs {
   int m_tiles, n_tiles;
   EpiConsts epi;
   IntEpi iepi;
+  // grouped launch (shape kernels only): a second problem of the same layer
+  // (same geometry, template and slot layout) with its own operands (maps
+  // *_1), gather source, accumulator bound and epilogue constants; its tiles
+  // follow the first problem's tiles in the persistent schedule
+  int groups;        // 1 or 2
+  const int8_t* gx1;
+  const int* w_l1_1;
+  int x_absmax1;
+  double scale1;
+  EpiConsts epi1;
 };
 
 template <int W>
@@ -206,7 +216,12 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
                    const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_o0,
                    const __grid_constant__ CUtensorMap map_o1,
-                   const __grid_constant__ CUtensorMap map_r, const TcArgs args) {
+                   const __grid_constant__ CUtensorMap map_r,
+                   const __grid_constant__ CUtensorMap map_a1,
+                   const __grid_constant__ CUtensorMap map_b1,
+                   const __grid_constant__ CUtensorMap map_o01,
+                   const __grid_constant__ CUtensorMap map_o11,
+                   const __grid_constant__ CUtensorMap map_r1, const TcArgs args) {
   constexpr int EW = 16;
   const uint32_t A_BYTES = BM * args.bkb;
   const uint32_t B_BYTES = BN * args.bkb;
@@ -244,9 +259,13 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
   // shape kernels: bias pre-scaled into sq0's grid, btab[n] = bias[n] / s0
   float* btab = reinterpret_cast<float*>(ktab + (args.gather == 1 ? args.K / 16 : 0));
   if (args.prog.tables) load_tables(tabs, args.prog.tables);
+  const int btab_n = args.n_tiles * BN;  // per group
   if (SHAPE != kShapeGeneric && SHAPE != kShapeInt) {
-    for (int n = threadIdx.x; n < args.n_tiles * BN; n += blockDim.x) {
-      btab[n] = (args.bias && n < args.N) ? __fmul_rn(__ldg(args.bias + n), args.epi.inv0) : 0.0f;
+    for (int i = threadIdx.x; i < args.groups * btab_n; i += blockDim.x) {
+      const int grp = i >= btab_n ? 1 : 0;
+      const int n = i - grp * btab_n;
+      const float inv0 = grp ? args.epi1.inv0 : args.epi.inv0;
+      btab[i] = (args.bias && n < args.N) ? __fmul_rn(__ldg(args.bias + n), inv0) : 0.0f;
     }
   }
   if (args.gather == 1) {
@@ -263,7 +282,15 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nk = args.K / args.bkb;
-  const int n_tiles_total = args.m_tiles * args.n_tiles;
+  const int tiles_g = args.m_tiles * args.n_tiles;  // tiles of one group
+  const int n_tiles_total = tiles_g * args.groups;
+  // persistent tile t -> (group, row and column origin)
+  auto tile_at = [&](int t, int& grp, int& m0, int& n0) {
+    grp = t >= tiles_g ? 1 : 0;
+    const int lt = t - grp * tiles_g;
+    m0 = (lt / args.n_tiles) * BM;
+    n0 = (lt % args.n_tiles) * BN;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -298,6 +325,8 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
   // |acc| <= L1(w) * max|x| <= 2^24: I2F is exact and the conversion pipe is idle
   const bool acc_small = args.w_l1 != nullptr &&
                          static_cast<int64_t>(__ldg(args.w_l1)) * args.x_absmax <= (1 << 24);
+  const bool acc_small1 = args.groups > 1 && args.w_l1_1 != nullptr &&
+                          static_cast<int64_t>(__ldg(args.w_l1_1)) * args.x_absmax1 <= (1 << 24);
 
   if (warp >= EPI_WARPS && warp < MMA_WARP) {
     // ================= producers =================
@@ -311,7 +340,10 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
         uint32_t ph = 0;
         bool wrapped = false;
         for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
-          const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
+          int grp, m0, n0;
+          tile_at(t, grp, m0, n0);
+          const CUtensorMap* ma = grp ? &map_a1 : &map_a;
+          const CUtensorMap* mb = grp ? &map_b1 : &map_b;
           const int img = m0 / ohw, rem = m0 - img * ohw;
           const int oh = rem / g.OW, ow = rem - oh * g.OW;
           const int w0 = ow * g.sw - g.pw, h0 = oh * g.sh - g.ph;
@@ -320,9 +352,9 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
             const int kh = tap / g.KW, kw = tap - kh * g.KW;
             if (wrapped) bar_wait_sleep(&empty[s], ph ^ 1);
             bar_expect(&full[s], A_BYTES + B_BYTES);
-            tma_im2col(&map_a, &full[s], sa + s * A_BYTES, c0, w0, h0, img,
+            tma_im2col(ma, &full[s], sa + s * A_BYTES, c0, w0, h0, img,
                        static_cast<uint16_t>(kw), static_cast<uint16_t>(kh));
-            tma2d(&map_b, &full[s], sb + s * B_BYTES, kb * args.bkb, n0);
+            tma2d(mb, &full[s], sb + s * B_BYTES, kb * args.bkb, n0);
             if (++s == stages) {
               s = 0;
               ph ^= 1;
@@ -337,12 +369,15 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
         uint32_t ph = 0;
         bool wrapped = false;  // ring slots are reused from the second lap on
         for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
-          const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
+          int grp, m0, n0;
+          tile_at(t, grp, m0, n0);
+          const CUtensorMap* ma = grp ? &map_a1 : &map_a;
+          const CUtensorMap* mb = grp ? &map_b1 : &map_b;
           for (int kb = 0; kb < nk; ++kb) {
             if (wrapped) bar_wait_sleep(&empty[s], ph ^ 1);
             bar_expect(&full[s], A_BYTES + B_BYTES);
-            tma2d(&map_a, &full[s], sa + s * A_BYTES, kb * BK, m0);
-            tma2d(&map_b, &full[s], sb + s * B_BYTES, kb * BK, n0);
+            tma2d(ma, &full[s], sa + s * A_BYTES, kb * BK, m0);
+            tma2d(mb, &full[s], sb + s * B_BYTES, kb * BK, n0);
             if (++s == stages) {
               s = 0;
               ph ^= 1;
@@ -359,7 +394,10 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
       // this thread's 8 swizzled 16-byte destinations within its A row
       const uint32_t swz_row = static_cast<uint32_t>(p) * 128;
       for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
-        const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
+        int grp, m0, n0;
+        tile_at(t, grp, m0, n0);
+        const CUtensorMap* mb = grp ? &map_b1 : &map_b;
+        const int8_t* gsrc = grp ? args.gx1 : g.x;
         const int64_t row = static_cast<int64_t>(m0) + p;
         // tap validity of this row (bit kh*KW + kw); rows past M: none.
         // rowoff: byte offset of the (ih0, iw0) pixel (may be negative; only
@@ -386,7 +424,7 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
           if (wrapped) bar_wait_sleep(&empty[s], ph ^ 1);
           if (p == 0) {
             bar_expect(&full[s], B_BYTES);
-            tma2d(&map_b, &full[s], sb + s * B_BYTES, kb * BK, n0);
+            tma2d(mb, &full[s], sb + s * B_BYTES, kb * BK, n0);
           }
           const uint32_t dst_row = su32(sa + s * A_BYTES) + swz_row;
           const uint32_t kt = su32(ktab) + kb * 8 * sizeof(int2);
@@ -404,7 +442,7 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
             const bool ok = (tapmask >> e[2 * j + 1]) & 1;
             // select the offset, then one 64-bit add: the address lands in a
             // register pair and the eight copies do not serialise on a shared one
-            const int8_t* src = g.x + (ok ? rowoff + e[2 * j] : int64_t{0});
+            const int8_t* src = gsrc + (ok ? rowoff + e[2 * j] : int64_t{0});
             const uint32_t dst = dst_row + ((j ^ (p & 7)) << 4);
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
                          "r"(ok ? 16u : 0u)
@@ -471,11 +509,13 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
     if (lane == 0 && (args.n_out > 0 || args.has_res)) {
       const int nsets = args.dbuf ? 2 : 1;
       auto load_res = [&](int t, int set) {
-        const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
+        int grp, m0, n0;
+        tile_at(t, grp, m0, n0);
+        const CUtensorMap* mr = grp ? &map_r1 : &map_r;
         uint8_t* dst = slots + set * SET_BYTES + args.n_out * SLOT_BYTES;
         bar_expect(&rfull[set], SLOT_BYTES);
         for (int blk = 0; blk < BN / SWZ; ++blk) {
-          tma2d(&map_r, &rfull[set], dst + blk * (BM * SWZ), n0 + blk * SWZ, m0);
+          tma2d(mr, &rfull[set], dst + blk * (BM * SWZ), n0 + blk * SWZ, m0);
         }
       };
       if (args.has_res) {
@@ -486,16 +526,19 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
       }
       uint32_t tl = 0;
       for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
-        const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
+        int grp, m0, n0;
+        tile_at(t, grp, m0, n0);
+        const CUtensorMap* mo0 = grp ? &map_o01 : &map_o0;
+        const CUtensorMap* mo1 = grp ? &map_o11 : &map_o1;
         const int set = args.dbuf ? static_cast<int>(tl & 1) : 0;
         const uint32_t use = args.dbuf ? (tl >> 1) : tl;
         bar_wait(&sfull[set], use & 1);
         uint8_t* base = slots + set * SET_BYTES;
         if (args.n_out > 0) {
           for (int blk = 0; blk < BN / SWZ; ++blk) {
-            tma_store2d(&map_o0, base + blk * (BM * SWZ), n0 + blk * SWZ, m0);
+            tma_store2d(mo0, base + blk * (BM * SWZ), n0 + blk * SWZ, m0);
             if (args.n_out > 1) {
-              tma_store2d(&map_o1, base + SLOT_BYTES + blk * (BM * SWZ), n0 + blk * SWZ, m0);
+              tma_store2d(mo1, base + SLOT_BYTES + blk * (BM * SWZ), n0 + blk * SWZ, m0);
             }
           }
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -516,7 +559,8 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
     const int r = quarter * 32 + lane;
     uint32_t tl = 0;
     for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
-      const int m0 = (t / args.n_tiles) * BM, n0 = (t % args.n_tiles) * BN;
+      int grp, m0, n0;
+      tile_at(t, grp, m0, n0);
       const uint32_t acc = tl & 1;
       const int set = args.dbuf ? static_cast<int>(tl & 1) : 0;
       const uint32_t use = args.dbuf ? (tl >> 1) : tl;  // k-th use of this slot set
@@ -561,7 +605,10 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
         // — O % 16 == 0, all I/O through slots (rows >= M and columns >= O
         // are clipped by the TMA store), zp = 0, no live acc clamp.  TMEM
         // loads run one chunk ahead of the math.
-        const EpiConsts& e = args.epi;
+        const EpiConsts& e = grp ? args.epi1 : args.epi;
+        const bool small = grp ? acc_small1 : acc_small;
+        const float* btg = btab + grp * btab_n;
+        const double scale_g = grp ? args.scale1 : args.scale;
 #pragma unroll 1
         for (int c = part; c < NCHUNK; c += PARTS) {
           const int c0 = c * EW;
@@ -574,7 +621,7 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
           // (checked for the whole chunk) and a double path beyond
           uint32_t u[EW];
           uint32_t chk = 0;
-          if (!acc_small) {
+          if (!small) {
 #pragma unroll
             for (int j = 0; j < EW; ++j) {
               u[j] = d[j] + 0x4B400000u;
@@ -586,13 +633,13 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
             float bs[EW];
 #pragma unroll
             for (int j = 0; j < EW; j += 4) {
-              const int4 b4 = lds128(su32(btab + n + j));
+              const int4 b4 = lds128(su32(btg + n + j));
               bs[j] = __int_as_float(b4.x);
               bs[j + 1] = __int_as_float(b4.y);
               bs[j + 2] = __int_as_float(b4.z);
               bs[j + 3] = __int_as_float(b4.w);
             }
-            if (acc_small) {
+            if (small) {
 #pragma unroll
               for (int j = 0; j < EW; ++j) {
                 x[j] = __fmaf_rn(static_cast<float>(static_cast<int32_t>(d[j])), e.q[0].k, bs[j]);
@@ -609,7 +656,7 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
               for (int j = 0; j < EW; ++j) {
                 const int32_t a = static_cast<int32_t>(u[j] - 0x4B400000u);
                 const double b = args.bias ? static_cast<double>(__ldg(args.bias + n + j)) : 0.0;
-                x[j] = __fmul_rn(__double2float_rn(__fma_rn(static_cast<double>(a), args.scale, b)),
+                x[j] = __fmul_rn(__double2float_rn(__fma_rn(static_cast<double>(a), scale_g, b)),
                                  e.inv0);
               }
             }
@@ -845,7 +892,7 @@ int smem_fixed(const TcArgs& a, int bn, int sets, bool shape) {
   return 1024 + sets * (a.n_out + a.has_res) * BM * bn + (2 * MAX_STAGES + 10) * 8 + 16 +
          static_cast<int>(sizeof(StageTables)) + 64 +
          (a.gather == 1 ? a.K / 16 * static_cast<int>(sizeof(int2)) : 0) +
-         (shape ? ((a.N + bn - 1) / bn) * bn * 4 : 0);
+         (shape ? ((a.N + bn - 1) / bn) * bn * 4 * a.groups : 0);
 }
 
 // pipeline depth that fits next to `fixed` bytes (capped by what the K loop uses)
@@ -873,7 +920,7 @@ void launch_tc(const CUtensorMap* maps, TcArgs a, cudaStream_t s) {
   if (stages < 2) stages = 2;
   a.stages = stages;
   const size_t smem = static_cast<size_t>(fixed) + static_cast<size_t>(stages) * stage_bytes;
-  const int tiles = a.m_tiles * a.n_tiles;
+  const int tiles = a.m_tiles * a.n_tiles * a.groups;
   const int grid = tiles < num_sms() ? tiles : num_sms();
   // the cp.async gather needs 4 producer warps (one thread per A row); TMA
   // producers need one thread, which leaves room for 12 epilogue warps
@@ -885,7 +932,8 @@ void launch_tc(const CUtensorMap* maps, TcArgs a, cudaStream_t s) {
                            cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
     });
     launch_pdl(tc_conv_kernel<BN, SHAPE, EPIW_GATHER>, dim3(grid), dim3(Layout<EPIW_GATHER>::THREADS), smem, s,
-               maps[0], maps[1], maps[2], maps[3], maps[4], a);
+               maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], maps[7], maps[8],
+               maps[9], a);
   } else {
     static std::once_flag once;
     std::call_once(once, [&] {
@@ -893,7 +941,8 @@ void launch_tc(const CUtensorMap* maps, TcArgs a, cudaStream_t s) {
                            cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
     });
     launch_pdl(tc_conv_kernel<BN, SHAPE, EPIW_TMA>, dim3(grid), dim3(Layout<EPIW_TMA>::THREADS),
-               smem, s, maps[0], maps[1], maps[2], maps[3], maps[4], a);
+               smem, s, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], maps[7],
+               maps[8], maps[9], a);
   }
   QC_CUDA_CHECK_LAUNCH();
 }
@@ -959,16 +1008,31 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
   a.x_absmax = sp.x_absmax;
   a.m_tiles = static_cast<int>((sp.M + BM - 1) / BM);
   a.bkb = BK;
-  CUtensorMap maps[5];
+  // grouped launch: shape kernels only (the interpreter's tables and the
+  // integer epilogue are per problem)
+  a.groups = (sp.groups == 2 && sp.prog.shape != kShapeGeneric && sp.prog.shape != kShapeInt) ? 2 : 1;
+  if (a.groups == 2) {
+    a.gx1 = sp.x1;
+    a.w_l1_1 = sp.w_l1_1;
+    a.x_absmax1 = sp.x_absmax1;
+    a.scale1 = sp.scale1;
+    a.epi1 = sp.epi1;
+  }
+  CUtensorMap maps[10];
   // A: direct 2-D map over the code rows (a valid dummy when gathering);
   // im2col TMA replaces the cp.async gather where the geometry allows: 128-
   // channel K blocks (SWIZZLE_128B) or, for 64-channel layers, 64-byte K
   // blocks (SWIZZLE_64B); K then stops at the last real tap
   maps[0] = bmap(sp.x, sp.gather ? BM : sp.M, sp.gather ? BK : sp.Ktrue, sp.gather ? BK : sp.lda,
                  BK, BM, 128);
+  maps[5] = a.groups == 2 ? bmap(sp.x1, sp.gather ? BM : sp.M, sp.gather ? BK : sp.Ktrue,
+                                 sp.gather ? BK : sp.lda, BK, BM, 128)
+                          : maps[0];
   if (im2col_ok(sp)) {
     const int cbox = sp.ld % BK == 0 ? BK : 64;
-    if (im2col_map(&maps[0], sp, cbox)) {
+    TcConvSpec s1 = sp;
+    s1.x = sp.x1;
+    if (im2col_map(&maps[0], sp, cbox) && (a.groups == 1 || im2col_map(&maps[5], s1, cbox))) {
       a.gather = 2;
       a.bkb = cbox;
       a.K = sp.KH * sp.KW * sp.ld;
@@ -987,7 +1051,7 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
       return e ? std::atoi(e) : 1;
     }();
     const int want = per_sm > 1 ? per_sm * num_sms() : num_sms() / 2;
-    while (BN > 64 && a.m_tiles * ((sp.O + BN - 1) / BN) < want) BN /= 2;
+    while (BN > 64 && a.m_tiles * ((sp.O + BN - 1) / BN) * a.groups < want) BN /= 2;
   }
   // a wide tile whose slot sets cannot be double-buffered: halve it when the
   // narrower one can (per-tile store drains / residual loads then overlap)
@@ -1002,6 +1066,16 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
                                : maps[1];
   }
   maps[4] = a.has_res ? bmap(sp.res_ptr, sp.M, sp.res_cols, sp.res_ld, swz, BM, swz) : maps[1];
+  if (a.groups == 2) {
+    maps[6] = bmap(sp.w1, sp.O, sp.Kpad, sp.Kpad, a.bkb, BN, a.bkb);
+    for (int o = 0; o < 2; ++o) {
+      maps[7 + o] = o < sp.n_out ? bmap(sp.out_ptr1[o], sp.M, sp.out_cols[o], sp.out_ld[o], swz, BM, swz)
+                                 : maps[6];
+    }
+    maps[9] = a.has_res ? bmap(sp.res_ptr1, sp.M, sp.res_cols, sp.res_ld, swz, BM, swz) : maps[6];
+  } else {
+    for (int k = 6; k < 10; ++k) maps[k] = maps[k - 5];
+  }
   if (BN == 64) {
     launch_bn<64>(maps, a, s);
   } else if (BN == 128) {

@@ -141,6 +141,18 @@ struct TcConvSpec {
   int x_absmax;
   EpiConsts epi;     // shape kernels (prog.shape != 0): host-folded constants
   IntEpi iepi;       // prog.shape == kShapeInt: integer epilogue
+  // groups == 2: a second problem of the same layer in the same launch (shape
+  // kernels; same geometry, shape and output layout, its own operands and
+  // constants); its tiles run after the first problem's in the schedule
+  int groups;
+  const int8_t* x1;
+  const int8_t* w1;
+  const int* w_l1_1;
+  int x_absmax1;
+  double scale1;
+  void* out_ptr1[2];
+  const void* res_ptr1;
+  EpiConsts epi1;
 };
 void tc_conv(const TcConvSpec& spec, cudaStream_t s);
 

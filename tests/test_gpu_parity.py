@@ -288,3 +288,20 @@ def test_histogram_bin_edges_exact(cuda_lib, port):
         x = np.clip(x, -absmax, absmax).astype(np.float32)
         c = cuda_lib.histogram(torch.from_numpy(x).cuda(), float(absmax), bins).cpu().numpy()
         np.testing.assert_array_equal(c, port.histogram(x, float(absmax), bins))
+
+
+@pytest.mark.parametrize("name", ["small_cnn", "resnet18"])
+def test_candidate_pairs_grouped_equal_single_calls(b200, cuda_lib, name):
+    """losses(span) evaluates candidates two at a time through grouped tcgen05
+    launches (FastPlan::predict_pair); every count must equal the one-
+    candidate-per-call path."""
+    model = F.small_cnn() if name == "small_cnn" else F.resnet(18, image=64, classes=10, width=16)
+    p = _pipeline(b200, model, model.data(12), pow2=True)
+    ev = p["ev"]
+    sp = ev.space()
+    rng = np.random.default_rng(11)
+    cands = [sp.all_hi(), sp.all_lo()] + [
+        [int(rng.integers(lo, hi + 1)) for lo, hi in zip(sp.lo, sp.hi)] for _ in range(7)]
+    batched = ev.losses(cands).tolist()
+    single = [ev.loss(c) for c in cands]
+    assert batched == single
