@@ -294,25 +294,24 @@ std::shared_ptr<void> predict_streamed(const engine::Plan& plan, const Graph& g,
   return preds;
 }
 
-std::shared_ptr<void> predict_device_pair(const engine::Plan& plan, const DeviceDataset& dd,
-                                          const SimBinding* b0, const SimBinding* b1) {
-  static const bool off = [] {
-    const char* e = std::getenv("QUANTC_PAIR");
-    return e && std::string(e) == "0";
-  }();
-  if (off || device::profile_enabled() || !fused_ready(plan, b0, false, true) ||
-      !fused_ready(plan, b1, false, true)) {
-    return nullptr;
+std::shared_ptr<void> predict_device_group(const engine::Plan& plan, const DeviceDataset& dd,
+                                           const std::vector<const SimBinding*>& bindings) {
+  const int G = static_cast<int>(bindings.size());
+  if (G < 2 || device::profile_enabled()) return nullptr;
+  for (const SimBinding* b : bindings) {
+    if (!fused_ready(plan, b, false, true)) return nullptr;
   }
   const int64_t n = dd.size();
-  auto preds = engine::device_alloc(static_cast<size_t>(std::max<int64_t>(1, 2 * n)) * 8);
+  auto preds = engine::device_alloc(static_cast<size_t>(std::max<int64_t>(1, G * n)) * 8);
   auto* p = static_cast<int64_t*>(preds.get());
   const int fb = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, n), 256));
   for (int64_t first = 0; first < n; first += fb) {
     const int b = static_cast<int>(std::min<int64_t>(fb, n - first));
     std::vector<const float*> ins;
     for (size_t k = 0; k < dd.num_inputs(); ++k) ins.push_back(dd.input(k, first));
-    plan.fused->predict_pair(b, ins, b0, b1, p + first, p + n + first);
+    std::vector<int64_t*> outs;
+    for (int g = 0; g < G; ++g) outs.push_back(p + g * n + first);
+    plan.fused->predict_group(b, ins, bindings, outs);
   }
   return preds;
 }

@@ -49,11 +49,12 @@ std::shared_ptr<void> predict_device(const engine::Plan& plan, const DeviceDatas
                                      bool allow_fast, std::shared_ptr<void>* scores = nullptr,
                                      int64_t* per_sample = nullptr);
 
-// Two bindings over the same device samples (the candidate-batch path of the
-// search): when the fused int8 engine applies to both, every compatible GEMM
-// stage runs as one grouped tcgen05 launch.  Returns [2 x N] predictions
-// (binding 0's rows first), or nullptr when the pair path does not apply.
-std::shared_ptr<void> predict_device_pair(const engine::Plan& plan, const DeviceDataset& dd,
-                                          const SimBinding* b0, const SimBinding* b1);
+// Several bindings (2..4) over the same device samples (the candidate-batch
+// path of the search): when the fused int8 engine applies to all of them,
+// every compatible GEMM stage runs as one grouped tcgen05 launch.  Returns
+// [G x N] predictions (binding g's rows at g*N), or nullptr when the grouped
+// path does not apply.
+std::shared_ptr<void> predict_device_group(const engine::Plan& plan, const DeviceDataset& dd,
+                                           const std::vector<const SimBinding*>& bindings);
 
 }  // namespace quantc::gpu

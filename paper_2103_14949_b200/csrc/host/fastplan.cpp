@@ -1521,60 +1521,67 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
   }
 }
 
-// Two bindings over the same batch of samples in one pass: every GEMM stage
-// whose two specs are launch-compatible runs as ONE grouped tcgen05 launch
-// (twice the tiles: the per-layer pipeline fill / drain and launch latency are
-// paid once for both); other stages run per binding.  Each binding has its
-// own arena, tables and outputs, so results equal two predict() calls.
-void FastPlan::predict_pair(int batch, const std::vector<const float*>& inputs,
-                            const SimBinding* b0, const SimBinding* b1, int64_t* preds0,
-                            int64_t* preds1) {
-  if (wcache_.size() > 4 * stages_.size()) wcache_.clear();
-  Run r[2];
-  const SimBinding* bs[2] = {b0, b1};
-  int64_t* ps[2] = {preds0, preds1};
-  for (int g = 0; g < 2; ++g) {
+// Several bindings (<= kern::kMaxGroups) over the same batch of samples in
+// one pass: every GEMM stage whose specs are launch-compatible across the
+// bindings runs as ONE grouped tcgen05 launch (G times the tiles: the
+// per-layer pipeline fill / drain and launch latency are paid once); other
+// stages run per binding.  Each binding has its own arena, tables and
+// outputs, so results equal separate predict() calls.
+void FastPlan::predict_group(int batch, const std::vector<const float*>& inputs,
+                             const std::vector<const SimBinding*>& bindings,
+                             const std::vector<int64_t*>& preds) {
+  const int G = static_cast<int>(bindings.size());
+  if (G < 1 || G > kern::kMaxGroups) throw std::logic_error("predict_group: 1..4 bindings");
+  if (wcache_.size() > 4 * stages_.size() * static_cast<size_t>(G)) wcache_.clear();
+  std::vector<Run> r(static_cast<size_t>(G));
+  for (int g = 0; g < G; ++g) {
     r[g].group = g;
     r[g].batch = batch;
     r[g].inputs = inputs;
-    r[g].binding = bs[g];
-    r[g].d_preds = ps[g];
+    r[g].binding = bindings[g];
+    r[g].d_preds = preds[g];
     prepare(r[g]);
   }
   static const bool no_group = std::getenv("QUANTC_NO_GROUPED") != nullptr;
+  std::vector<kern::TcConvSpec> sp(static_cast<size_t>(G));
   for (size_t si = 0; si < stages_.size(); ++si) {
     if (stages_[si]->kind != Stage::kGemm) {
-      run_stage(r[0], si);
-      run_stage(r[1], si);
+      for (int g = 0; g < G; ++g) run_stage(r[g], si);
       continue;
     }
-    kern::TcConvSpec s0, s1;
-    gemm_spec(r[0], si, s0);
-    gemm_spec(r[1], si, s1);
-    const int sh = s0.prog.shape;
-    const bool shape_kernel = sh != kern::kShapeGeneric && sh != kern::kShapeInt;
-    if (!no_group && shape_kernel && s1.prog.shape == sh && s0.n_out == s1.n_out &&
-        (s0.res_ptr != nullptr) == (s1.res_ptr != nullptr) && s0.lda == s1.lda) {
-      s0.groups = 2;
-      s0.x1 = s1.x;
-      s0.w1 = s1.w;
-      s0.w_l1_1 = s1.w_l1;
-      s0.x_absmax1 = s1.x_absmax;
-      s0.scale1 = s1.scale;
-      s0.out_ptr1[0] = s1.out_ptr[0];
-      s0.out_ptr1[1] = s1.out_ptr[1];
-      s0.res_ptr1 = s1.res_ptr;
-      s0.epi1 = s1.epi;
-      // the wider of the two accumulator bounds decides the generic path
-      s0.acc_bound = std::max(s0.acc_bound, s1.acc_bound);
-      launch_gemm(si, s0);
-    } else {
-      launch_gemm(si, s0);
-      launch_gemm(si, s1);
+    for (int g = 0; g < G; ++g) gemm_spec(r[g], si, sp[g]);
+    // maximal runs of consecutive compatible bindings share a launch
+    int g0 = 0;
+    while (g0 < G) {
+      kern::TcConvSpec& head = sp[g0];
+      const int sh = head.prog.shape;
+      const bool shape_kernel = sh != kern::kShapeGeneric && sh != kern::kShapeInt;
+      int g1 = g0 + 1;
+      while (!no_group && shape_kernel && g1 < G && sp[g1].prog.shape == sh &&
+             sp[g1].n_out == head.n_out && (sp[g1].res_ptr != nullptr) == (head.res_ptr != nullptr) &&
+             sp[g1].lda == head.lda) {
+        ++g1;
+      }
+      head.groups = g1 - g0;
+      for (int g = g0 + 1; g < g1; ++g) {
+        const kern::TcConvSpec& o = sp[g];
+        const int k = g - g0 - 1;
+        head.xg[k] = o.x;
+        head.wg[k] = o.w;
+        head.w_l1g[k] = o.w_l1;
+        head.x_absmaxg[k] = o.x_absmax;
+        head.scaleg[k] = o.scale;
+        head.out_ptrg[k][0] = o.out_ptr[0];
+        head.out_ptrg[k][1] = o.out_ptr[1];
+        head.res_ptrg[k] = o.res_ptr;
+        head.epig[k] = o.epi;
+        head.acc_bound = std::max(head.acc_bound, o.acc_bound);
+      }
+      launch_gemm(si, head);
+      g0 = g1;
     }
   }
-  finish(r[0]);
-  finish(r[1]);
+  for (int g = 0; g < G; ++g) finish(r[g]);
 }
 
 }  // namespace quantc::fast

@@ -37,10 +37,11 @@ class FastPlan {
   // d_scores (optional): the output rows themselves, [batch x out_per_sample()]
   void predict(int batch, const std::vector<const float*>& inputs, const SimBinding* binding,
                int64_t* d_preds, float* d_scores = nullptr);
-  // two bindings over the same samples; compatible GEMM stages run as one
-  // grouped tcgen05 launch (fastplan.cpp)
-  void predict_pair(int batch, const std::vector<const float*>& inputs, const SimBinding* b0,
-                    const SimBinding* b1, int64_t* preds0, int64_t* preds1);
+  // several bindings (<= 4) over the same samples; compatible GEMM stages
+  // run as one grouped tcgen05 launch (fastplan.cpp)
+  void predict_group(int batch, const std::vector<const float*>& inputs,
+                     const std::vector<const SimBinding*>& bindings,
+                     const std::vector<int64_t*>& preds);
   int64_t out_per_sample() const { return out_per_sample_; }
   // stream this instance enqueues on (nullptr: the engine stream); every
   // buffer, table upload and launch of the instance is ordered on it
@@ -69,7 +70,7 @@ class FastPlan {
     std::vector<std::shared_ptr<void>> bufs;
     std::shared_ptr<void> tables;
   };
-  Arena arenas_[2];
+  Arena arenas_[4];
   // weight code cache: (stage, FSq bytes) -> codes
   std::map<std::pair<int, std::string>, std::shared_ptr<void>> wcache_;
 

@@ -173,16 +173,33 @@ struct TcArgs {
   int m_tiles, n_tiles;
   EpiConsts epi;
   IntEpi iepi;
-  // grouped launch (shape kernels only): a second problem of the same layer
-  // (same geometry, template and slot layout) with its own operands (maps
-  // *_1), gather source, accumulator bound and epilogue constants; its tiles
-  // follow the first problem's tiles in the persistent schedule
-  int groups;        // 1 or 2
-  const int8_t* gx1;
-  const int* w_l1_1;
-  int x_absmax1;
-  double scale1;
-  EpiConsts epi1;
+  // grouped launch (shape kernels only): up to kMaxGroups problems of the
+  // same layer (same geometry, template and slot layout); group g's tiles
+  // follow group g-1's in the persistent schedule.  Group 0 uses the fields
+  // above, groups 1.. their TcGroupsT entries.
+  int groups;
+};
+
+// the tensor maps of NG groups: A, B, code outputs 0/1, residual
+template <int NG>
+struct TcMapsT {
+  CUtensorMap m[NG][5];
+};
+
+// per-group operands of groups 1..NG-1: gather source, accumulator bound,
+// wide-path scale and epilogue constants (a separate kernel parameter so the
+// ungrouped kernels carry none of it)
+template <int NG>
+struct TcGroupsT {
+  const int8_t* gx[NG - 1];
+  const int* w_l1[NG - 1];
+  int x_absmax[NG - 1];
+  double scale[NG - 1];
+  EpiConsts epi[NG - 1];
+};
+template <>
+struct TcGroupsT<1> {
+  int unused;
 };
 
 template <int W>
@@ -210,18 +227,10 @@ __device__ __forceinline__ void tmem_wait(uint32_t (&d)[16]) {
                : "memory");
 }
 
-template <int BN, int SHAPE, int EPIW>
+template <int BN, int SHAPE, int EPIW, int NG>
 __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
-    tc_conv_kernel(const __grid_constant__ CUtensorMap map_a,
-                   const __grid_constant__ CUtensorMap map_b,
-                   const __grid_constant__ CUtensorMap map_o0,
-                   const __grid_constant__ CUtensorMap map_o1,
-                   const __grid_constant__ CUtensorMap map_r,
-                   const __grid_constant__ CUtensorMap map_a1,
-                   const __grid_constant__ CUtensorMap map_b1,
-                   const __grid_constant__ CUtensorMap map_o01,
-                   const __grid_constant__ CUtensorMap map_o11,
-                   const __grid_constant__ CUtensorMap map_r1, const TcArgs args) {
+    tc_conv_kernel(const __grid_constant__ TcMapsT<NG> maps, const TcArgs args,
+                   const __grid_constant__ TcGroupsT<NG> gr) {
   constexpr int EW = 16;
   const uint32_t A_BYTES = BM * args.bkb;
   const uint32_t B_BYTES = BN * args.bkb;
@@ -262,9 +271,12 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
   const int btab_n = args.n_tiles * BN;  // per group
   if (SHAPE != kShapeGeneric && SHAPE != kShapeInt) {
     for (int i = threadIdx.x; i < args.groups * btab_n; i += blockDim.x) {
-      const int grp = i >= btab_n ? 1 : 0;
+      const int grp = i / btab_n;
       const int n = i - grp * btab_n;
-      const float inv0 = grp ? args.epi1.inv0 : args.epi.inv0;
+      float inv0 = args.epi.inv0;
+      if constexpr (NG > 1) {
+        if (grp) inv0 = gr.epi[grp - 1].inv0;
+      }
       btab[i] = (args.bias && n < args.N) ? __fmul_rn(__ldg(args.bias + n), inv0) : 0.0f;
     }
   }
@@ -286,7 +298,7 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
   const int n_tiles_total = tiles_g * args.groups;
   // persistent tile t -> (group, row and column origin)
   auto tile_at = [&](int t, int& grp, int& m0, int& n0) {
-    grp = t >= tiles_g ? 1 : 0;
+    grp = NG > 1 ? t / tiles_g : 0;
     const int lt = t - grp * tiles_g;
     m0 = (lt / args.n_tiles) * BM;
     n0 = (lt % args.n_tiles) * BN;
@@ -325,8 +337,15 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
   // |acc| <= L1(w) * max|x| <= 2^24: I2F is exact and the conversion pipe is idle
   const bool acc_small = args.w_l1 != nullptr &&
                          static_cast<int64_t>(__ldg(args.w_l1)) * args.x_absmax <= (1 << 24);
-  const bool acc_small1 = args.groups > 1 && args.w_l1_1 != nullptr &&
-                          static_cast<int64_t>(__ldg(args.w_l1_1)) * args.x_absmax1 <= (1 << 24);
+  uint32_t small_mask = acc_small ? 1u : 0u;  // bit g: group g's |acc| <= 2^24
+  if constexpr (NG > 1) {
+    for (int g = 1; g < args.groups; ++g) {
+      if (gr.w_l1[g - 1] != nullptr &&
+          static_cast<int64_t>(__ldg(gr.w_l1[g - 1])) * gr.x_absmax[g - 1] <= (1 << 24)) {
+        small_mask |= 1u << g;
+      }
+    }
+  }
 
   if (warp >= EPI_WARPS && warp < MMA_WARP) {
     // ================= producers =================
@@ -342,8 +361,8 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
         for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
           int grp, m0, n0;
           tile_at(t, grp, m0, n0);
-          const CUtensorMap* ma = grp ? &map_a1 : &map_a;
-          const CUtensorMap* mb = grp ? &map_b1 : &map_b;
+          const CUtensorMap* ma = &maps.m[grp][0];
+          const CUtensorMap* mb = &maps.m[grp][1];
           const int img = m0 / ohw, rem = m0 - img * ohw;
           const int oh = rem / g.OW, ow = rem - oh * g.OW;
           const int w0 = ow * g.sw - g.pw, h0 = oh * g.sh - g.ph;
@@ -371,8 +390,8 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
         for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
           int grp, m0, n0;
           tile_at(t, grp, m0, n0);
-          const CUtensorMap* ma = grp ? &map_a1 : &map_a;
-          const CUtensorMap* mb = grp ? &map_b1 : &map_b;
+          const CUtensorMap* ma = &maps.m[grp][0];
+          const CUtensorMap* mb = &maps.m[grp][1];
           for (int kb = 0; kb < nk; ++kb) {
             if (wrapped) bar_wait_sleep(&empty[s], ph ^ 1);
             bar_expect(&full[s], A_BYTES + B_BYTES);
@@ -396,8 +415,11 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
       for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
         int grp, m0, n0;
         tile_at(t, grp, m0, n0);
-        const CUtensorMap* mb = grp ? &map_b1 : &map_b;
-        const int8_t* gsrc = grp ? args.gx1 : g.x;
+        const CUtensorMap* mb = &maps.m[grp][1];
+        const int8_t* gsrc = g.x;
+        if constexpr (NG > 1) {
+          if (grp) gsrc = gr.gx[grp - 1];
+        }
         const int64_t row = static_cast<int64_t>(m0) + p;
         // tap validity of this row (bit kh*KW + kw); rows past M: none.
         // rowoff: byte offset of the (ih0, iw0) pixel (may be negative; only
@@ -511,7 +533,7 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
       auto load_res = [&](int t, int set) {
         int grp, m0, n0;
         tile_at(t, grp, m0, n0);
-        const CUtensorMap* mr = grp ? &map_r1 : &map_r;
+        const CUtensorMap* mr = &maps.m[grp][4];
         uint8_t* dst = slots + set * SET_BYTES + args.n_out * SLOT_BYTES;
         bar_expect(&rfull[set], SLOT_BYTES);
         for (int blk = 0; blk < BN / SWZ; ++blk) {
@@ -528,8 +550,8 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
       for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
         int grp, m0, n0;
         tile_at(t, grp, m0, n0);
-        const CUtensorMap* mo0 = grp ? &map_o01 : &map_o0;
-        const CUtensorMap* mo1 = grp ? &map_o11 : &map_o1;
+        const CUtensorMap* mo0 = &maps.m[grp][2];
+        const CUtensorMap* mo1 = &maps.m[grp][3];
         const int set = args.dbuf ? static_cast<int>(tl & 1) : 0;
         const uint32_t use = args.dbuf ? (tl >> 1) : tl;
         bar_wait(&sfull[set], use & 1);
@@ -605,10 +627,17 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
         // — O % 16 == 0, all I/O through slots (rows >= M and columns >= O
         // are clipped by the TMA store), zp = 0, no live acc clamp.  TMEM
         // loads run one chunk ahead of the math.
-        const EpiConsts& e = grp ? args.epi1 : args.epi;
-        const bool small = grp ? acc_small1 : acc_small;
+        const EpiConsts* ep = &args.epi;
+        double scale_g = args.scale;
+        if constexpr (NG > 1) {
+          if (grp) {
+            ep = &gr.epi[grp - 1];
+            scale_g = gr.scale[grp - 1];
+          }
+        }
+        const EpiConsts& e = *ep;
+        const bool small = (small_mask >> grp) & 1u;
         const float* btg = btab + grp * btab_n;
-        const double scale_g = grp ? args.scale1 : args.scale;
 #pragma unroll 1
         for (int c = part; c < NCHUNK; c += PARTS) {
           const int c0 = c * EW;
@@ -910,8 +939,35 @@ bool dbuf_fits(const TcArgs& a, int bn, bool shape) {
   return fit_stages(a, bn, smem_fixed(a, bn, 2, shape)) >= 2;
 }
 
+template <int BN, int SHAPE, int EPIW, int NG>
+void launch_kernel(const TcMapsT<kMaxGroups>& all, const TcGroupsT<kMaxGroups>& grp_all, const TcArgs& a,
+                   int grid, size_t smem, cudaStream_t s) {
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    cudaFuncSetAttribute(tc_conv_kernel<BN, SHAPE, EPIW, NG>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
+  });
+  TcMapsT<NG> maps;
+  for (int g = 0; g < NG; ++g) {
+    for (int k = 0; k < 5; ++k) maps.m[g][k] = all.m[g][k];
+  }
+  TcGroupsT<NG> gr{};
+  if constexpr (NG > 1) {
+    for (int g = 0; g < NG - 1; ++g) {
+      gr.gx[g] = grp_all.gx[g];
+      gr.w_l1[g] = grp_all.w_l1[g];
+      gr.x_absmax[g] = grp_all.x_absmax[g];
+      gr.scale[g] = grp_all.scale[g];
+      gr.epi[g] = grp_all.epi[g];
+    }
+  }
+  launch_pdl(tc_conv_kernel<BN, SHAPE, EPIW, NG>, dim3(grid), dim3(Layout<EPIW>::THREADS), smem, s,
+             maps, a, gr);
+}
+
 template <int BN, int SHAPE>
-void launch_tc(const CUtensorMap* maps, TcArgs a, cudaStream_t s) {
+void launch_tc(const TcMapsT<kMaxGroups>* maps, const TcGroupsT<kMaxGroups>* grp, TcArgs a,
+               cudaStream_t s) {
   const int stage_bytes = BM * a.bkb + BN * a.bkb;
   constexpr bool shape = SHAPE != kShapeGeneric && SHAPE != kShapeInt;  // btab in smem
   a.dbuf = dbuf_fits(a, BN, shape) ? 1 : 0;
@@ -925,57 +981,54 @@ void launch_tc(const CUtensorMap* maps, TcArgs a, cudaStream_t s) {
   // the cp.async gather needs 4 producer warps (one thread per A row); TMA
   // producers need one thread, which leaves room for 12 epilogue warps
   static const bool all_gather_layout = std::getenv("QUANTC_GATHER_LAYOUT") != nullptr;
-  if (a.gather == 1 || all_gather_layout) {
-    static std::once_flag once;
-    std::call_once(once, [&] {
-      cudaFuncSetAttribute(tc_conv_kernel<BN, SHAPE, EPIW_GATHER>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
-    });
-    launch_pdl(tc_conv_kernel<BN, SHAPE, EPIW_GATHER>, dim3(grid), dim3(Layout<EPIW_GATHER>::THREADS), smem, s,
-               maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], maps[7], maps[8],
-               maps[9], a);
+  constexpr bool groupable = SHAPE != kShapeGeneric && SHAPE != kShapeInt;
+  const bool gather_layout = a.gather == 1 || all_gather_layout;
+  if (groupable && a.groups > 1) {
+    if constexpr (groupable) {
+      if (gather_layout) {
+        launch_kernel<BN, SHAPE, EPIW_GATHER, kMaxGroups>(*maps, *grp, a, grid, smem, s);
+      } else {
+        launch_kernel<BN, SHAPE, EPIW_TMA, kMaxGroups>(*maps, *grp, a, grid, smem, s);
+      }
+    }
+  } else if (gather_layout) {
+    launch_kernel<BN, SHAPE, EPIW_GATHER, 1>(*maps, *grp, a, grid, smem, s);
   } else {
-    static std::once_flag once;
-    std::call_once(once, [&] {
-      cudaFuncSetAttribute(tc_conv_kernel<BN, SHAPE, EPIW_TMA>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
-    });
-    launch_pdl(tc_conv_kernel<BN, SHAPE, EPIW_TMA>, dim3(grid), dim3(Layout<EPIW_TMA>::THREADS),
-               smem, s, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], maps[7],
-               maps[8], maps[9], a);
+    launch_kernel<BN, SHAPE, EPIW_TMA, 1>(*maps, *grp, a, grid, smem, s);
   }
   QC_CUDA_CHECK_LAUNCH();
 }
 
 template <int BN>
-void launch_bn(const CUtensorMap* maps, const TcArgs& a, cudaStream_t s) {
+void launch_bn(const TcMapsT<kMaxGroups>* maps, const TcGroupsT<kMaxGroups>* grp, const TcArgs& a,
+               cudaStream_t s) {
   switch (a.prog.shape) {
     case kShapeStore:
-      launch_tc<BN, kShapeStore>(maps, a, s);
+      launch_tc<BN, kShapeStore>(maps, grp, a, s);
       break;
     case kShapeSqStore:
-      launch_tc<BN, kShapeSqStore>(maps, a, s);
+      launch_tc<BN, kShapeSqStore>(maps, grp, a, s);
       break;
     case kShapeAddFork:
-      launch_tc<BN, kShapeAddFork>(maps, a, s);
+      launch_tc<BN, kShapeAddFork>(maps, grp, a, s);
       break;
     case kShapeAdd:
-      launch_tc<BN, kShapeAdd>(maps, a, s);
+      launch_tc<BN, kShapeAdd>(maps, grp, a, s);
       break;
     case kShapeAddF32:
-      launch_tc<BN, kShapeAddF32>(maps, a, s);
+      launch_tc<BN, kShapeAddF32>(maps, grp, a, s);
       break;
     case kShapeSqStoreId:
-      launch_tc<BN, kShapeSqStoreId>(maps, a, s);
+      launch_tc<BN, kShapeSqStoreId>(maps, grp, a, s);
       break;
     case kShapeAddForkId:
-      launch_tc<BN, kShapeAddForkId>(maps, a, s);
+      launch_tc<BN, kShapeAddForkId>(maps, grp, a, s);
       break;
     case kShapeInt:
-      launch_tc<BN, kShapeInt>(maps, a, s);
+      launch_tc<BN, kShapeInt>(maps, grp, a, s);
       break;
     default:
-      launch_tc<BN, kShapeGeneric>(maps, a, s);
+      launch_tc<BN, kShapeGeneric>(maps, grp, a, s);
       break;
   }
 }
@@ -1010,29 +1063,35 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
   a.bkb = BK;
   // grouped launch: shape kernels only (the interpreter's tables and the
   // integer epilogue are per problem)
-  a.groups = (sp.groups == 2 && sp.prog.shape != kShapeGeneric && sp.prog.shape != kShapeInt) ? 2 : 1;
-  if (a.groups == 2) {
-    a.gx1 = sp.x1;
-    a.w_l1_1 = sp.w_l1_1;
-    a.x_absmax1 = sp.x_absmax1;
-    a.scale1 = sp.scale1;
-    a.epi1 = sp.epi1;
+  const bool shape_kernel = sp.prog.shape != kShapeGeneric && sp.prog.shape != kShapeInt;
+  a.groups = shape_kernel ? std::max(1, std::min(sp.groups, kMaxGroups)) : 1;
+  static TcGroupsT<kMaxGroups> grp;  // host staging (launches are serial per thread)
+  for (int g = 1; g < a.groups; ++g) {
+    grp.gx[g - 1] = sp.xg[g - 1];
+    grp.w_l1[g - 1] = sp.w_l1g[g - 1];
+    grp.x_absmax[g - 1] = sp.x_absmaxg[g - 1];
+    grp.scale[g - 1] = sp.scaleg[g - 1];
+    grp.epi[g - 1] = sp.epig[g - 1];
   }
-  CUtensorMap maps[10];
+  auto x_of = [&](int g) { return g == 0 ? sp.x : sp.xg[g - 1]; };
+  static TcMapsT<kMaxGroups> maps;  // host staging of the kernel parameter
   // A: direct 2-D map over the code rows (a valid dummy when gathering);
   // im2col TMA replaces the cp.async gather where the geometry allows: 128-
   // channel K blocks (SWIZZLE_128B) or, for 64-channel layers, 64-byte K
   // blocks (SWIZZLE_64B); K then stops at the last real tap
-  maps[0] = bmap(sp.x, sp.gather ? BM : sp.M, sp.gather ? BK : sp.Ktrue, sp.gather ? BK : sp.lda,
-                 BK, BM, 128);
-  maps[5] = a.groups == 2 ? bmap(sp.x1, sp.gather ? BM : sp.M, sp.gather ? BK : sp.Ktrue,
-                                 sp.gather ? BK : sp.lda, BK, BM, 128)
-                          : maps[0];
+  for (int g = 0; g < a.groups; ++g) {
+    maps.m[g][0] = bmap(x_of(g), sp.gather ? BM : sp.M, sp.gather ? BK : sp.Ktrue,
+                        sp.gather ? BK : sp.lda, BK, BM, 128);
+  }
   if (im2col_ok(sp)) {
     const int cbox = sp.ld % BK == 0 ? BK : 64;
-    TcConvSpec s1 = sp;
-    s1.x = sp.x1;
-    if (im2col_map(&maps[0], sp, cbox) && (a.groups == 1 || im2col_map(&maps[5], s1, cbox))) {
+    bool ok = true;
+    for (int g = 0; g < a.groups && ok; ++g) {
+      TcConvSpec sg = sp;
+      sg.x = x_of(g);
+      ok = im2col_map(&maps.m[g][0], sg, cbox);
+    }
+    if (ok) {
       a.gather = 2;
       a.bkb = cbox;
       a.K = sp.KH * sp.KW * sp.ld;
@@ -1060,28 +1119,58 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
   }
   const int swz = BN >= 128 ? 128 : 64;
   a.n_tiles = (sp.O + BN - 1) / BN;
-  maps[1] = bmap(sp.w, sp.O, sp.Kpad, sp.Kpad, a.bkb, BN, a.bkb);
-  for (int o = 0; o < 2; ++o) {
-    maps[2 + o] = o < sp.n_out ? bmap(sp.out_ptr[o], sp.M, sp.out_cols[o], sp.out_ld[o], swz, BM, swz)
-                               : maps[1];
-  }
-  maps[4] = a.has_res ? bmap(sp.res_ptr, sp.M, sp.res_cols, sp.res_ld, swz, BM, swz) : maps[1];
-  if (a.groups == 2) {
-    maps[6] = bmap(sp.w1, sp.O, sp.Kpad, sp.Kpad, a.bkb, BN, a.bkb);
-    for (int o = 0; o < 2; ++o) {
-      maps[7 + o] = o < sp.n_out ? bmap(sp.out_ptr1[o], sp.M, sp.out_cols[o], sp.out_ld[o], swz, BM, swz)
-                                 : maps[6];
+  if (a.groups > 1 &&
+      smem_fixed(a, BN, 1, true) + 2 * (BM + BN) * a.bkb > SMEM_LIMIT) {
+    // the groups' bias tables do not fit beside two pipeline stages: split
+    const int h = a.groups / 2;
+    TcConvSpec lo = sp, hi = sp;
+    lo.groups = h;
+    hi.groups = a.groups - h;
+    hi.x = sp.xg[h - 1];
+    hi.w = sp.wg[h - 1];
+    hi.w_l1 = sp.w_l1g[h - 1];
+    hi.x_absmax = sp.x_absmaxg[h - 1];
+    hi.scale = sp.scaleg[h - 1];
+    hi.out_ptr[0] = sp.out_ptrg[h - 1][0];
+    hi.out_ptr[1] = sp.out_ptrg[h - 1][1];
+    hi.res_ptr = sp.res_ptrg[h - 1];
+    hi.epi = sp.epig[h - 1];
+    for (int g = 1; g < hi.groups; ++g) {
+      hi.xg[g - 1] = sp.xg[h + g - 1];
+      hi.wg[g - 1] = sp.wg[h + g - 1];
+      hi.w_l1g[g - 1] = sp.w_l1g[h + g - 1];
+      hi.x_absmaxg[g - 1] = sp.x_absmaxg[h + g - 1];
+      hi.scaleg[g - 1] = sp.scaleg[h + g - 1];
+      hi.out_ptrg[g - 1][0] = sp.out_ptrg[h + g - 1][0];
+      hi.out_ptrg[g - 1][1] = sp.out_ptrg[h + g - 1][1];
+      hi.res_ptrg[g - 1] = sp.res_ptrg[h + g - 1];
+      hi.epig[g - 1] = sp.epig[h + g - 1];
     }
-    maps[9] = a.has_res ? bmap(sp.res_ptr1, sp.M, sp.res_cols, sp.res_ld, swz, BM, swz) : maps[6];
-  } else {
-    for (int k = 6; k < 10; ++k) maps[k] = maps[k - 5];
+    tc_conv(lo, s);
+    tc_conv(hi, s);
+    return;
   }
+  for (int g = 0; g < a.groups; ++g) {
+    const int8_t* w = g == 0 ? sp.w : sp.wg[g - 1];
+    maps.m[g][1] = bmap(w, sp.O, sp.Kpad, sp.Kpad, a.bkb, BN, a.bkb);
+    for (int o = 0; o < 2; ++o) {
+      void* out = g == 0 ? sp.out_ptr[o] : sp.out_ptrg[g - 1][o];
+      maps.m[g][2 + o] = o < sp.n_out ? bmap(out, sp.M, sp.out_cols[o], sp.out_ld[o], swz, BM, swz)
+                                      : maps.m[g][1];
+    }
+    const void* res = g == 0 ? sp.res_ptr : sp.res_ptrg[g - 1];
+    maps.m[g][4] = a.has_res ? bmap(res, sp.M, sp.res_cols, sp.res_ld, swz, BM, swz) : maps.m[g][1];
+  }
+  for (int g = a.groups; g < kMaxGroups; ++g) {
+    for (int k = 0; k < 5; ++k) maps.m[g][k] = maps.m[0][k];
+  }
+  const TcMapsT<kMaxGroups>* mp = &maps;
   if (BN == 64) {
-    launch_bn<64>(maps, a, s);
+    launch_bn<64>(mp, &grp, a, s);
   } else if (BN == 128) {
-    launch_bn<128>(maps, a, s);
+    launch_bn<128>(mp, &grp, a, s);
   } else {
-    launch_bn<256>(maps, a, s);
+    launch_bn<256>(mp, &grp, a, s);
   }
 }
 

@@ -113,6 +113,9 @@ void weights_to_codes(const float* w, int8_t* codes, int O, int C, int KH, int K
 #include "fused.h"
 namespace quantc::kern {
 
+// problems of one layer a grouped tcgen05 launch can carry (TcConvSpec.groups)
+constexpr int kMaxGroups = 4;
+
 struct TcConvSpec {
   const int8_t* x;   // A source: NHWC codes (gather) or code rows (direct)
   const int8_t* w;   // B: weight codes [O][Kpad]
@@ -141,18 +144,19 @@ struct TcConvSpec {
   int x_absmax;
   EpiConsts epi;     // shape kernels (prog.shape != 0): host-folded constants
   IntEpi iepi;       // prog.shape == kShapeInt: integer epilogue
-  // groups == 2: a second problem of the same layer in the same launch (shape
-  // kernels; same geometry, shape and output layout, its own operands and
-  // constants); its tiles run after the first problem's in the schedule
+  // groups > 1: further problems of the same layer in the same launch (shape
+  // kernels; same geometry, shape and output layout, their own operands and
+  // constants), group g's tiles after group g-1's in the schedule.  Entry
+  // [g-1] of the arrays below is group g.
   int groups;
-  const int8_t* x1;
-  const int8_t* w1;
-  const int* w_l1_1;
-  int x_absmax1;
-  double scale1;
-  void* out_ptr1[2];
-  const void* res_ptr1;
-  EpiConsts epi1;
+  const int8_t* xg[kMaxGroups - 1];
+  const int8_t* wg[kMaxGroups - 1];
+  const int* w_l1g[kMaxGroups - 1];
+  int x_absmaxg[kMaxGroups - 1];
+  double scaleg[kMaxGroups - 1];
+  void* out_ptrg[kMaxGroups - 1][2];
+  const void* res_ptrg[kMaxGroups - 1];
+  EpiConsts epig[kMaxGroups - 1];
 };
 void tc_conv(const TcConvSpec& spec, cudaStream_t s);
 
