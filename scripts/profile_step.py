@@ -18,12 +18,17 @@ model = F.resnet(int(os.environ.get("DEPTH", "50")))
 data = model.data(batch, seed=9)
 g, spec, topo, sim, ds, st, thr = bench.build_pipeline(b, model, data)
 ev = b.evaluator(sim, spec, topo, thr, st, ds)
-cands = bench.candidates(ev.space(), 4)
+group = int(os.environ.get("GROUP", "1"))  # >1: one losses() call over GROUP candidates
+cands = bench.candidates(ev.space(), 3 + group)
 for c in cands[:3]:
     ev.loss(c)
+ev.losses(cands[:group])
 torch.cuda.synchronize()
 torch.cuda.profiler.start()
-ev.loss(cands[3])
+if group > 1:
+    ev.losses(cands[3:3 + group])
+else:
+    ev.loss(cands[3])
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
-print("profiled one step")
+print("profiled", group, "candidate(s)")
