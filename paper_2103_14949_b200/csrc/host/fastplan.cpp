@@ -1550,22 +1550,24 @@ void FastPlan::predict_group(int batch, const std::vector<const float*>& inputs,
       continue;
     }
     for (int g = 0; g < G; ++g) gemm_spec(r[g], si, sp[g]);
-    // maximal runs of consecutive compatible bindings share a launch
-    int g0 = 0;
-    while (g0 < G) {
+    // bindings whose specs are launch-compatible (same epilogue shape, output
+    // count, residual and A layout) share one launch
+    std::vector<char> launched(static_cast<size_t>(G), 0);
+    for (int g0 = 0; g0 < G; ++g0) {
+      if (launched[g0]) continue;
       kern::TcConvSpec& head = sp[g0];
+      launched[g0] = 1;
       const int sh = head.prog.shape;
       const bool shape_kernel = sh != kern::kShapeGeneric && sh != kern::kShapeInt;
-      int g1 = g0 + 1;
-      while (!no_group && shape_kernel && g1 < G && sp[g1].prog.shape == sh &&
-             sp[g1].n_out == head.n_out && (sp[g1].res_ptr != nullptr) == (head.res_ptr != nullptr) &&
-             sp[g1].lda == head.lda) {
-        ++g1;
-      }
-      head.groups = g1 - g0;
-      for (int g = g0 + 1; g < g1; ++g) {
+      head.groups = 1;
+      for (int g = g0 + 1; g < G && !no_group && shape_kernel; ++g) {
         const kern::TcConvSpec& o = sp[g];
-        const int k = g - g0 - 1;
+        if (launched[g] || o.prog.shape != sh || o.n_out != head.n_out ||
+            (o.res_ptr != nullptr) != (head.res_ptr != nullptr) || o.lda != head.lda) {
+          continue;
+        }
+        launched[g] = 1;
+        const int k = head.groups - 1;
         head.xg[k] = o.x;
         head.wg[k] = o.w;
         head.w_l1g[k] = o.w_l1;
@@ -1576,9 +1578,9 @@ void FastPlan::predict_group(int batch, const std::vector<const float*>& inputs,
         head.res_ptrg[k] = o.res_ptr;
         head.epig[k] = o.epi;
         head.acc_bound = std::max(head.acc_bound, o.acc_bound);
+        ++head.groups;
       }
       launch_gemm(si, head);
-      g0 = g1;
     }
   }
   for (int g = 0; g < G; ++g) finish(r[g]);

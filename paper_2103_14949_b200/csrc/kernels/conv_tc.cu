@@ -888,7 +888,8 @@ bool im2col_map(CUtensorMap* m, const TcConvSpec& sp, int cbox) {
 // bounding-box offsets inside the rank-4 encoding's [-128, 127]
 bool im2col_ok(const TcConvSpec& sp) {
   static const bool off = std::getenv("QUANTC_NO_IM2COL") != nullptr;
-  return !off && sp.gather && (sp.ld % BK == 0 || sp.ld == 64) && sp.KH == sp.KW && sp.ph == sp.pw &&
+  static const bool off64 = std::getenv("QUANTC_NO_IM2COL64") != nullptr;
+  return !off && sp.gather && (sp.ld % BK == 0 || (sp.ld == 64 && !off64)) && sp.KH == sp.KW && sp.ph == sp.pw &&
          sp.sh == sp.sw && sp.sh <= 8 && sp.ph <= 127 && sp.KH - 1 - sp.ph <= 128 &&
          sp.KH <= 65535;
 }
