@@ -241,11 +241,64 @@ def main():
     data_all = model.data(B * world, seed=9)
     data = np.ascontiguousarray(data_all[rank * B:(rank + 1) * B])
     g, spec, topo, sim, ds, st, thr = build_pipeline(b, model, data)
+    stream = torch.cuda.ExternalStream(L.qcu_engine_stream())
+    # ---- C4 leg (runs first, on a fresh allocator pool): ResNet-50 KL
+    # calibration, images sharded over ranks,
+    # extrema and int64 histograms all-reduced (parallel.sharded_collect_stats),
+    # KL thresholds for every edge; device-timed on the engine stream, max
+    # over ranks
+    calib = None
+    if args.calib_images > 0:
+        from paper_2103_14949_b200 import parallel as P
+        cn = args.calib_images
+        cal = np.ascontiguousarray(model.data(cn * world, seed=17)[rank * cn:(rank + 1) * cn])
+        cal_ds = b.dataset(cal)
+        cal_local = P.B200Local(b, g, cal_ds)
+        cal_edges = b.simulated_edge_indices(g, topo)
+        # one untimed pass over the same shard (allocator pool growth, plan
+        # upload), like the main leg's warm-up steps
+        P.sharded_collect_stats(cal_edges, cn * world, 2048, cal_local.extrema,
+                                cal_local.histograms)
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        # three timed passes (the stream-ordered allocator reaches its steady
+        # state after a pass or two); report the median
+        runs = []
+        for _ in range(3):
+            if dist is not None:
+                dist.barrier()
+            torch.cuda.synchronize()
+            c0 = torch.cuda.Event(enable_timing=True)
+            c1 = torch.cuda.Event(enable_timing=True)
+            c2 = torch.cuda.Event(enable_timing=True)
+            c0.record(stream)
+            per_edge = P.sharded_collect_stats(cal_edges, cn * world, 2048, cal_local.extrema,
+                                               cal_local.histograms)
+            c1.record(stream)
+            cal_thr = P.stats_handle(b, per_edge).estimate_thresholds("kl", kl_bits=8)
+            c2.record(stream)
+            torch.cuda.synchronize()
+            cms, kms = c0.elapsed_time(c1), c1.elapsed_time(c2)
+            if dist is not None:
+                t = torch.tensor([cms, kms], device=f"cuda:{local}")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                cms, kms = float(t[0]), float(t[1])
+            runs.append((cms + kms, cms, kms))
+        runs.sort()
+        _, cms, kms = runs[1]
+        calib = {"workload": "resnet50 KL calibration (BASELINE config C4)",
+                 "images": cn * world, "images_per_gpu": cn, "edges": len(cal_edges),
+                 "bins": 2048, "collect_stats_ms": cms, "kl_thresholds_ms": kms,
+                 "images_per_s": cn * world / ((cms + kms) / 1e3),
+                 "passes_ms": [round(r[0], 1) for r in runs], "reported": "median of 3 passes",
+                 "thresholds": len(cal_thr),
+                 "merge": "all_reduce MIN/MAX extrema + SUM int64 histograms" if world > 1
+                 else "single GPU"}
     ev = b.evaluator(sim, spec, topo, thr, st, ds)
     sp = ev.space()
     cands = candidates(sp, args.warmup + args.steps)
 
-    stream = torch.cuda.ExternalStream(L.qcu_engine_stream())
     counts = np.zeros(1, np.int64)
     cnt_t = torch.zeros(1, dtype=torch.int64, device=f"cuda:{local}")
 
@@ -353,45 +406,6 @@ def main():
     h2d = data.nbytes
     d2h = 8 * B
 
-    # ---- C4 leg: ResNet-50 KL calibration, images sharded over ranks,
-    # extrema and int64 histograms all-reduced (parallel.sharded_collect_stats),
-    # KL thresholds for every edge; device-timed on the engine stream, max
-    # over ranks
-    calib = None
-    if args.calib_images > 0:
-        from paper_2103_14949_b200 import parallel as P
-        cn = args.calib_images
-        cal = np.ascontiguousarray(model.data(cn * world, seed=17)[rank * cn:(rank + 1) * cn])
-        cal_ds = b.dataset(cal)
-        cal_local = P.B200Local(b, g, cal_ds)
-        cal_edges = b.simulated_edge_indices(g, topo)
-        warm_ds = b.dataset(cal[:2])
-        P.B200Local(b, g, warm_ds).extrema(cal_edges)
-        if dist is not None:
-            dist.barrier()
-        torch.cuda.synchronize()
-        c0 = torch.cuda.Event(enable_timing=True)
-        c1 = torch.cuda.Event(enable_timing=True)
-        c2 = torch.cuda.Event(enable_timing=True)
-        c0.record(stream)
-        per_edge = P.sharded_collect_stats(cal_edges, cn * world, 2048, cal_local.extrema,
-                                           cal_local.histograms)
-        c1.record(stream)
-        cal_thr = P.stats_handle(b, per_edge).estimate_thresholds("kl", kl_bits=8)
-        c2.record(stream)
-        torch.cuda.synchronize()
-        cms, kms = c0.elapsed_time(c1), c1.elapsed_time(c2)
-        if dist is not None:
-            t = torch.tensor([cms, kms], device=f"cuda:{local}")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            cms, kms = float(t[0]), float(t[1])
-        calib = {"workload": "resnet50 KL calibration (BASELINE config C4)",
-                 "images": cn * world, "images_per_gpu": cn, "edges": len(cal_edges),
-                 "bins": 2048, "collect_stats_ms": cms, "kl_thresholds_ms": kms,
-                 "images_per_s": cn * world / ((cms + kms) / 1e3),
-                 "thresholds": len(cal_thr),
-                 "merge": "all_reduce MIN/MAX extrema + SUM int64 histograms" if world > 1
-                 else "single GPU"}
 
     # ---- roofline of the dominant kernel: tc_conv_kernel, the fused tcgen05
     # implicit-GEMM conv + sq/add epilogue (every conv/dense launch of a step).

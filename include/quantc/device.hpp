@@ -48,6 +48,9 @@ void unpin_host(const void* p);
 bool host_pinned(const void* p, size_t bytes);
 void synchronize();
 size_t memory_budget_bytes();  // per-batch activation budget
+// make sure the engine stream's allocator pool holds at least `bytes` (one
+// allocate/free pair; the pool keeps released memory)
+void pool_reserve(size_t bytes);
 
 // Counters (for bench / profiling evidence).
 struct Counters {

@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <limits>
 #include <memory>
@@ -219,6 +221,11 @@ struct ShardPasses {
   void forward(Hook&& hook) {
     const int64_t N = dd.size();
     const int batch = plan.batch_for(N);
+    static const bool hprof = std::getenv("QUANTC_HOST_PROF") != nullptr;
+    if (hprof) {
+      std::fprintf(stderr, "ShardPasses::forward N %lld batch %d budget %zu\n",
+                   static_cast<long long>(N), batch, device::memory_budget_bytes());
+    }
     int64_t bi = 0;
     for (int64_t s0 = 0; s0 < N; s0 += batch, ++bi) {
       const int b = static_cast<int>(std::min<int64_t>(batch, N - s0));
@@ -231,7 +238,14 @@ struct ShardPasses {
         if (!v.dtype.is_float()) throw std::logic_error("floats() on " + v.dtype.name() + " tensor");
         hook(it->second, v, b, bi);
       };
+      const auto tr = std::chrono::steady_clock::now();
       engine::run(plan, spec);
+      if (hprof) {
+        const double host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tr).count();
+        device::synchronize();
+        std::fprintf(stderr, "  run batch %d: host %.1f ms, +sync %.1f ms\n", b, host_ms,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tr).count());
+      }
     }
   }
 };
@@ -267,7 +281,14 @@ const void* first_sample_ptr(const Dataset& ds) {
 void collect_extrema(const Graph& g, const Dataset& shard, const std::vector<int>& edges,
                      std::vector<double>* mins, std::vector<double>* maxs) {
   if (shard.empty()) throw CalibrationError("calibration dataset is empty");
+  static const bool hprof = std::getenv("QUANTC_HOST_PROF") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   ShardPasses sp(g, shard, edges);
+  if (hprof) {
+    device::synchronize();
+    std::fprintf(stderr, "collect_extrema: plan lease + upload %.1f ms\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
   auto keys = engine::device_alloc(static_cast<size_t>(sp.n_slots) * 16 + 16);
   auto* k64 = static_cast<unsigned long long*>(keys.get());
   kern::minmax_init(k64, sp.n_slots, S());
@@ -277,6 +298,10 @@ void collect_extrema(const Graph& g, const Dataset& shard, const std::vector<int
   }
   std::unique_ptr<Handoff> h;
   if (sp.resident_bytes() <= static_cast<int64_t>(device::memory_budget_bytes())) {
+    // grow the stream-ordered pool once for the retained activations (plus a
+    // batch's transient working set) instead of in many small mappings
+    // during the forward
+    device::pool_reserve(static_cast<size_t>(sp.resident_bytes()) * 5 / 4);
     h = std::make_unique<Handoff>();
     h->graph_uid = g.uid();
     h->shard = &shard;

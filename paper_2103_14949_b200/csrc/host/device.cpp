@@ -156,6 +156,19 @@ void synchronize() {
   if (e != cudaSuccess) throw DeviceError(std::string("CUDA error: ") + cudaGetErrorString(e));
 }
 
+void pool_reserve(size_t bytes) {
+  static size_t reserved = 0;
+  if (bytes <= reserved) return;
+  cudaStream_t s = static_cast<cudaStream_t>(stream());
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, bytes, s) == cudaSuccess) {
+    cudaFreeAsync(p, s);
+    reserved = bytes;
+  } else {
+    cudaGetLastError();
+  }
+}
+
 size_t memory_budget_bytes() {
   if (const char* v = std::getenv("QUANTC_BATCH_BYTES")) return std::strtoull(v, nullptr, 10);
   size_t free_b = 0, total = 0;

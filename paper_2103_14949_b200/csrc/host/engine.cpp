@@ -5,6 +5,8 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -1030,13 +1032,31 @@ void Runner::exec(int i) {
 }  // namespace
 
 std::vector<DevTensor> run(const Plan& plan, const RunSpec& spec) {
+  static const bool sprof = std::getenv("QUANTC_STEP_PROF") != nullptr;
   Runner r(plan, spec);
   r.plan_fast();
   const int n = static_cast<int>(plan.steps().size());
   for (int i = 0; i < n; ++i) {
+    if (!sprof) {
+      r.exec(i);
+      if (spec.on_value) spec.on_value(i, r.vals[static_cast<size_t>(i)]);
+      r.release_inputs(i);
+      continue;
+    }
+    // QUANTC_STEP_PROF: report steps whose host-side work exceeds 5 ms
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    const auto t0 = std::chrono::steady_clock::now();
     r.exec(i);
+    const auto t1 = std::chrono::steady_clock::now();
     if (spec.on_value) spec.on_value(i, r.vals[static_cast<size_t>(i)]);
+    const auto t2 = std::chrono::steady_clock::now();
     r.release_inputs(i);
+    const auto t3 = std::chrono::steady_clock::now();
+    if (ms(t0, t3) > 5.0) {
+      std::fprintf(stderr, "  step %d op %s: exec %.1f hook %.1f release %.1f ms\n", i,
+                   op_name(plan.steps()[static_cast<size_t>(i)].node->op).c_str(), ms(t0, t1),
+                   ms(t1, t2), ms(t2, t3));
+    }
   }
   std::vector<DevTensor> out;
   for (int k : spec.keep) out.push_back(r.vals[static_cast<size_t>(k)]);
