@@ -1277,8 +1277,6 @@ void FastPlan::prepare(Run& r) {
       }
     }
     shape_of[si] = sh;
-    static const bool epi_nop = std::getenv("QUANTC_EXPERIMENT_EPI_NOP") != nullptr;
-    if (epi_nop) e.pad_ = 0x5A5A;  // wrong results: timing experiments only
     if (!no_alias && (sh == kern::kShapeAddFork || sh == kern::kShapeAddForkId) &&
         st.n_out == 2 && std::memcmp(&e.q[2], &e.q[3], sizeof(kern::EpiSq)) == 0) {
       const Val& v0 = *vals_[static_cast<size_t>(st.out_vals[0])];

@@ -287,12 +287,6 @@ template <int SHAPE>
 __device__ __forceinline__ void run_shape_epi(float (&x)[16], const EpiConsts& e,
                                               const TileIo& io, int cl, int64_t m, int n,
                                               bool row_ok) {
-  if ((SHAPE == kShapeSqStoreId || SHAPE == kShapeAddForkId) && e.pad_ == 0x5A5A) {
-    // timing experiment only (QUANTC_EXPERIMENT_EPI_NOP): skip the math
-    const int4 z = make_int4(__float_as_int(x[0]), 0, 0, 0);
-    sts128(tile_addr(io, e.slot_out[0], cl), z);
-    return;
-  }
   if constexpr (SHAPE == kShapeSqStoreId) {
     // sq0 (codes [0, P0 - 1]) on x0 / P0: T = M + min(floor(max(RZ(x0 + 1/2), 0)), P0 - 1)
 #pragma unroll
