@@ -669,9 +669,13 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
               bs[j + 3] = __int_as_float(b4.w);
             }
             if (small) {
+              const f2 k2 = f2_pack(e.q[0].k, e.q[0].k);
 #pragma unroll
-              for (int j = 0; j < EW; ++j) {
-                x[j] = __fmaf_rn(static_cast<float>(static_cast<int32_t>(d[j])), e.q[0].k, bs[j]);
+              for (int j = 0; j < EW; j += 2) {
+                f2_unpack(f2_fma_rn(f2_pack(static_cast<float>(static_cast<int32_t>(d[j])),
+                                            static_cast<float>(static_cast<int32_t>(d[j + 1]))),
+                                    k2, f2_pack(bs[j], bs[j + 1])),
+                          x[j], x[j + 1]);
               }
             } else if (chk < 0x800000u) {
               // x0 = (a*s + b)/s0 = fma(a, s/s0, b/s0): a*s/s0 exact, one

@@ -274,6 +274,46 @@ __device__ __forceinline__ void codes_to_floats(const uint32_t (&w)[4], float (&
   }
 }
 
+// Packed fp32 pairs (sm_100 FFMA2 / FADD2: two IEEE fp32 operations per
+// instruction, same per-lane rounding as FFMA / FADD)
+using f2 = unsigned long long;
+__device__ __forceinline__ f2 f2_pack(float a, float b) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(f2 v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ f2 f2_fma_rn(f2 a, f2 b, f2 c) {
+  f2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f2 f2_fma_rz(f2 a, f2 b, f2 c) {
+  f2 r;
+  asm("fma.rz.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f2 f2_add_rn(f2 a, f2 b) {
+  f2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// byte permute with an immediate selector (keeps the selector out of registers)
+template <uint32_t SEL>
+__device__ __forceinline__ uint32_t prmt_imm(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "n"(SEL));
+  return r;
+}
+// residual code byte k of w as the biased magic float 2^23 + byte
+template <int K>
+__device__ __forceinline__ float code_float(uint32_t w) {
+  return __uint_as_float(prmt_imm<0x7650u + K>(w, 0x4B000000u));
+}
+
 // RZ(a + b) clamped to [0, 1] on the FMA pipe (PTX add.rz.sat: NaN -> +0)
 __device__ __forceinline__ float add_rz_sat(float a, float b) {
   float r;
@@ -289,10 +329,16 @@ __device__ __forceinline__ void run_shape_epi(float (&x)[16], const EpiConsts& e
                                               bool row_ok) {
   if constexpr (SHAPE == kShapeSqStoreId) {
     // sq0 (codes [0, P0 - 1]) on x0 / P0: T = M + min(floor(max(RZ(x0 + 1/2), 0)), P0 - 1)
+    const f2 p2 = f2_pack(e.sat_p[0], e.sat_p[0]);
+    const f2 m2 = f2_pack(kMagic, kMagic);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const float u = add_rz_sat(x[j], e.sat_half[0]);
-      x[j] = fminf(__fmaf_rz(u, e.sat_p[0], kMagic), e.sat_top[0]);
+    for (int j = 0; j < 16; j += 2) {
+      const f2 t = f2_fma_rz(f2_pack(add_rz_sat(x[j], e.sat_half[0]), add_rz_sat(x[j + 1], e.sat_half[0])),
+                             p2, m2);
+      float a, b;
+      f2_unpack(t, a, b);
+      x[j] = fminf(a, e.sat_top[0]);
+      x[j + 1] = fminf(b, e.sat_top[0]);
     }
     epi_round(x, e.q[1]);  // k = 1 store: at most a clamp in the T-domain
     sts128(tile_addr(io, e.slot_out[0], cl), epi_pack(x, e.q[1]));
@@ -304,19 +350,34 @@ __device__ __forceinline__ void run_shape_epi(float (&x)[16], const EpiConsts& e
                             static_cast<uint32_t>(raw.y) ^ 0x80808080u,
                             static_cast<uint32_t>(raw.z) ^ 0x80808080u,
                             static_cast<uint32_t>(raw.w) ^ 0x80808080u};
+    const f2 p0 = f2_pack(e.sat_p[0], e.sat_p[0]);
+    const f2 p1 = f2_pack(e.sat_p[1], e.sat_p[1]);
+    const f2 m2 = f2_pack(kMagic, kMagic);
+    const f2 nm2 = f2_pack(-kMagic, -kMagic);
+    const f2 k1 = f2_pack(e.q[1].k, e.q[1].k);
+    const f2 ka = f2_pack(e.ka, e.ka);
+    const f2 kofs = f2_pack(e.ka_off, e.ka_off);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < 16; j += 2) {
       // sq0, signed codes [-P0, P0 - 1], on x0 / P0: half-away rounding of
       // |x0| saturated at P0, sign restored, positive side capped at P0 - 1
-      const float u0 = add_rz_sat(fabsf(x[j]), e.sat_half[0]);
-      const float t0 = __fsub_rn(__fmaf_rz(u0, e.sat_p[0], kMagic), kMagic);
-      const float r0 = fminf(copysignf(t0, x[j]), e.sat_top[0]);
+      const f2 u0 = f2_pack(add_rz_sat(fabsf(x[j]), e.sat_half[0]),
+                            add_rz_sat(fabsf(x[j + 1]), e.sat_half[0]));
+      float ta, tb;
+      f2_unpack(f2_add_rn(f2_fma_rz(u0, p0, m2), nm2), ta, tb);
+      const float ra = fminf(copysignf(ta, x[j]), e.sat_top[0]);
+      const float rb = fminf(copysignf(tb, x[j + 1]), e.sat_top[0]);
       // residual add (k1, ka, ka_off pre-scaled by 1/P1), then sq1 (codes
       // [0, P1 - 1]) into the T-domain
-      const float C = __uint_as_float(__byte_perm(wr[j >> 2], 0x4B000000u, 0x7650u + (j & 3)));
-      const float x1 = __fmaf_rn(r0, e.q[1].k, __fmaf_rn(C, e.ka, e.ka_off));
-      const float u1 = add_rz_sat(x1, e.sat_half[1]);
-      x[j] = fminf(__fmaf_rz(u1, e.sat_p[1], kMagic), e.sat_top[1]);
+      const float Ca = (j & 3) == 0 ? code_float<0>(wr[j >> 2]) : code_float<2>(wr[j >> 2]);
+      const float Cb = (j & 3) == 0 ? code_float<1>(wr[j >> 2]) : code_float<3>(wr[j >> 2]);
+      float xa, xb;
+      f2_unpack(f2_fma_rn(f2_pack(ra, rb), k1, f2_fma_rn(f2_pack(Ca, Cb), ka, kofs)), xa, xb);
+      float ta1, tb1;
+      f2_unpack(f2_fma_rz(f2_pack(add_rz_sat(xa, e.sat_half[1]), add_rz_sat(xb, e.sat_half[1])), p1, m2),
+                ta1, tb1);
+      x[j] = fminf(ta1, e.sat_top[1]);
+      x[j + 1] = fminf(tb1, e.sat_top[1]);
     }
     epi_round(x, e.q[2]);                     // k = 1 store (q2 == q3): at most a clamp
     const int4 packed = epi_pack(x, e.q[2]);
