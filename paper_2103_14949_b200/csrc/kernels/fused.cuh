@@ -212,6 +212,38 @@ __device__ __forceinline__ void load_values(const ProgBuf& b, int64_t m, int n0,
 
 // (shape ids: fused.h kShape*)
 
+// Packed fp32 pairs (sm_100 FFMA2 / FADD2: two IEEE fp32 operations per
+// instruction, same per-lane rounding as FFMA / FADD)
+using f2 = unsigned long long;
+__device__ __forceinline__ f2 f2_pack(float a, float b) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(f2 v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ f2 f2_fma_rn(f2 a, f2 b, f2 c) {
+  f2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f2 f2_fma_rz(f2 a, f2 b, f2 c) {
+  f2 r;
+  asm("fma.rz.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f2 f2_add_rz(f2 a, f2 b) {
+  f2 r;
+  asm("add.rz.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2 f2_add_rn(f2 a, f2 b) {
+  f2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
 // ---- straight-line shape epilogues (no conversion-pipe instructions) -------------
 // Host preconditions (fastplan classify_shape / make_epi): every sq of the
 // shape has zp = 0, no live accumulator clamp, is not passthrough; code I/O
@@ -224,29 +256,42 @@ __device__ __forceinline__ void epi_round(float (&x)[16], const EpiSq& q) {
 #pragma unroll
   for (int j = 0; j < 16; ++j) x[j] = fminf(fmaxf(x[j], q.lo), q.hi);
   if (q.flags & kEpiExact) return;
+  // half-away rounding, two lanes per FADD2 (same per-lane RZ rounding)
+  const f2 half = f2_pack(0.5f, 0.5f);
+  const f2 m2 = f2_pack(kMagic, kMagic);
   if (q.flags & kEpiNonneg) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) x[j] = __fadd_rz(__fadd_rz(x[j], 0.5f), kMagic);
+    for (int j = 0; j < 16; j += 2) {
+      f2_unpack(f2_add_rz(f2_add_rz(f2_pack(x[j], x[j + 1]), half), m2), x[j], x[j + 1]);
+    }
   } else {
+    const f2 nm2 = f2_pack(-kMagic, -kMagic);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      x[j] = copysignf(__fsub_rn(__fadd_rz(__fadd_rz(fabsf(x[j]), 0.5f), kMagic), kMagic), x[j]);
+    for (int j = 0; j < 16; j += 2) {
+      float a, b;
+      f2_unpack(f2_add_rn(f2_add_rz(f2_add_rz(f2_pack(fabsf(x[j]), fabsf(x[j + 1])), half), m2), nm2),
+                a, b);
+      x[j] = copysignf(a, x[j]);
+      x[j + 1] = copysignf(b, x[j + 1]);
     }
   }
 }
 
 // y = fma(R, q.k, q.off), rounded into q's domain
 __device__ __forceinline__ void epi_next(const float (&R)[16], float (&y)[16], const EpiSq& q) {
+  const f2 k2 = f2_pack(q.k, q.k);
+  const f2 o2 = f2_pack(q.off, q.off);
 #pragma unroll
-  for (int j = 0; j < 16; ++j) y[j] = __fmaf_rn(R[j], q.k, q.off);
+  for (int j = 0; j < 16; j += 2) f2_unpack(f2_fma_rn(f2_pack(R[j], R[j + 1]), k2, o2), y[j], y[j + 1]);
   epi_round(y, q);
 }
 
 // 16 rounded codes -> 16 int8 bytes (low byte of the T-domain bits)
 __device__ __forceinline__ int4 epi_pack(float (&R)[16], const EpiSq& q) {
   if (!(q.flags & kEpiNonneg)) {
+    const f2 m2 = f2_pack(kMagic, kMagic);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) R[j] = __fadd_rn(R[j], kMagic);
+    for (int j = 0; j < 16; j += 2) f2_unpack(f2_add_rn(f2_pack(R[j], R[j + 1]), m2), R[j], R[j + 1]);
   }
   uint32_t w[4];
 #pragma unroll
@@ -272,33 +317,6 @@ __device__ __forceinline__ void codes_to_floats(const uint32_t (&w)[4], float (&
     const float C = __uint_as_float(__byte_perm(w[j >> 2] ^ 0x80808080u, 0x4B000000u, 0x7650u + (j & 3)));
     r[j] = __fsub_rn(C, 8388736.0f);  // 2^23 + 128
   }
-}
-
-// Packed fp32 pairs (sm_100 FFMA2 / FADD2: two IEEE fp32 operations per
-// instruction, same per-lane rounding as FFMA / FADD)
-using f2 = unsigned long long;
-__device__ __forceinline__ f2 f2_pack(float a, float b) {
-  f2 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ void f2_unpack(f2 v, float& a, float& b) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-}
-__device__ __forceinline__ f2 f2_fma_rn(f2 a, f2 b, f2 c) {
-  f2 r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-  return r;
-}
-__device__ __forceinline__ f2 f2_fma_rz(f2 a, f2 b, f2 c) {
-  f2 r;
-  asm("fma.rz.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-  return r;
-}
-__device__ __forceinline__ f2 f2_add_rn(f2 a, f2 b) {
-  f2 r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
 }
 
 // byte permute with an immediate selector (keeps the selector out of registers)
@@ -399,18 +417,26 @@ __device__ __forceinline__ void run_shape_epi(float (&x)[16], const EpiConsts& e
   }
   // residual add: x1 = (r0 * s0 + c * s_res) / s1 in one rounding
   if (e.q[0].flags & kEpiNonneg) {
+    const f2 nm2 = f2_pack(-kMagic, -kMagic);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) x[j] = __fsub_rn(x[j], kMagic);
+    for (int j = 0; j < 16; j += 2) f2_unpack(f2_add_rn(f2_pack(x[j], x[j + 1]), nm2), x[j], x[j + 1]);
   }
   const int4 raw = lds128(tile_addr(io, e.slot_res, cl));
   const uint32_t wr[4] = {static_cast<uint32_t>(raw.x) ^ 0x80808080u,
                           static_cast<uint32_t>(raw.y) ^ 0x80808080u,
                           static_cast<uint32_t>(raw.z) ^ 0x80808080u,
                           static_cast<uint32_t>(raw.w) ^ 0x80808080u};
+  {
+    const f2 k1 = f2_pack(e.q[1].k, e.q[1].k);
+    const f2 ka = f2_pack(e.ka, e.ka);
+    const f2 kofs = f2_pack(e.ka_off, e.ka_off);
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const float C = __uint_as_float(__byte_perm(wr[j >> 2], 0x4B000000u, 0x7650u + (j & 3)));
-    x[j] = __fmaf_rn(x[j], e.q[1].k, __fmaf_rn(C, e.ka, e.ka_off));
+    for (int j = 0; j < 16; j += 2) {
+      const float Ca = (j & 3) == 0 ? code_float<0>(wr[j >> 2]) : code_float<2>(wr[j >> 2]);
+      const float Cb = (j & 3) == 0 ? code_float<1>(wr[j >> 2]) : code_float<3>(wr[j >> 2]);
+      f2_unpack(f2_fma_rn(f2_pack(x[j], x[j + 1]), k1, f2_fma_rn(f2_pack(Ca, Cb), ka, kofs)), x[j],
+                x[j + 1]);
+    }
   }
   epi_round(x, e.q[1]);
   if (SHAPE == kShapeAddF32) {
