@@ -1155,6 +1155,7 @@ struct FastPlan::Run {
   std::vector<kern::EpiConsts> epi_of;
   std::vector<double> sxw_of;
   std::vector<char> drop2;
+  std::vector<char> pool_drop2;  // max-pool stage stores once (aliased outputs)
   std::vector<int> alias;
   const kern::StageTables* d_tabs = nullptr;
   std::vector<std::shared_ptr<void>> keep;  // per-run temporaries (stream-ordered frees)
@@ -1290,6 +1291,31 @@ void FastPlan::prepare(Run& r) {
         e.slot_out[1] = -1;
         if (e.slot_res >= 0) e.slot_res = 1;
       }
+    }
+  }
+  // a max-pool forking into two code stores with identical constants (the
+  // pooled value quantized the same way for the first block's conv and its
+  // shortcut): one store, the second value aliases the first buffer
+  r.pool_drop2.assign(stages_.size(), 0);
+  for (size_t si = 0; si < stages_.size() && !no_alias; ++si) {
+    const Stage& st = *stages_[si];
+    if (st.kind != Stage::kMaxpool) continue;
+    const Val& v = *vals_[static_cast<size_t>(st.in_val)];
+    kern::PoolStores ps;
+    const kern::StageTables& t = tabs[si];
+    if (!(st.C % 16 == 0 && v.ld % 16 == 0 && st.ph < st.pkh && st.pw < st.pkw &&
+          pool_stores(t, scale_by_step.at(v.sq_step), ps)) ||
+        ps.n_out != 2 || std::memcmp(&ps.q[0], &ps.q[1], sizeof(kern::EpiSq)) != 0) {
+      continue;
+    }
+    const int v0 = st.buf_vals[static_cast<size_t>(t.code[1].b)];
+    const int v1 = st.buf_vals[static_cast<size_t>(t.code[3].b)];
+    const Val& a = *vals_[static_cast<size_t>(v0)];
+    const Val& b = *vals_[static_cast<size_t>(v1)];
+    if (a.kind == b.kind && a.C == b.C && a.ld == b.ld && a.hw == b.hw && a.rows_ps == b.rows_ps &&
+        !a.s2d && !b.s2d && (a.zero_fill || !b.zero_fill)) {
+      alias[static_cast<size_t>(v1)] = alias[static_cast<size_t>(v0)];
+      r.pool_drop2[si] = 1;
     }
   }
   for (size_t si = 0; si < stages_.size(); ++si) {
@@ -1457,6 +1483,7 @@ void FastPlan::run_stage(Run& r, size_t si) {
       kern::PoolStores ps;
       if (st.C % 16 == 0 && v.ld % 16 == 0 && st.ph < st.pkh && st.pw < st.pkw &&
           pool_stores(r.tabs[si], r.scale_by_step.at(v.sq_step), ps)) {
+        if (!r.pool_drop2.empty() && r.pool_drop2[si]) ps.n_out = 1;
         kern::stage_maxpool_stores(static_cast<const int8_t*>(buf(r, st.in_val)),
                                    static_cast<int>(v.ld), batch * st.n0, st.C, st.H, st.W, st.OH,
                                    st.OW, st.pkh, st.pkw, st.sh, st.sw, st.ph, st.pw, ps, ST());
