@@ -503,7 +503,6 @@ FSq make_fsq(const QParams& p) {
 // accumulator clamp, no passthrough, slot-resident stores / add operand, and
 // O % 16 == 0 (whole 16-column chunks).  Anything else runs the interpreter.
 int classify_shape(const kern::StageTables& t, int O) {
-  if (O % 16 != 0) return 0;
   std::vector<uint8_t> ops;
   for (int i = 0; i < t.n_code; ++i) {
     const kern::ProgInstr& in = t.code[i];
@@ -519,6 +518,9 @@ int classify_shape(const kern::StageTables& t, int O) {
     if (in.op == kern::kPStoreF32 && (t.buf[in.b].kind != 1 || t.buf[in.b].hw != 1)) return 0;
   }
   using V = std::vector<uint8_t>;
+  // fp32 scores (masked tail chunk): any O
+  if (ops == V{kern::kPSq, kern::kPStoreF32} && O % 4 == 0) return kern::kShapeSqF32;
+  if (O % 16 != 0) return 0;
   if (ops == V{kern::kPSqStore8}) return 1;
   if (ops == V{kern::kPSq, kern::kPSqStore8}) return 2;
   if (ops == V{kern::kPSq, kern::kPAdd, kern::kPSq, kern::kPPush, kern::kPSqStore8, kern::kPPop,
@@ -651,6 +653,10 @@ bool make_epi(const kern::StageTables& t, int shape, double sxw, kern::EpiConsts
       res = static_cast<int>(c[1].b);
       out0 = static_cast<int>(c[3].b);
       break;
+    case kern::kShapeSqF32:
+      qs = {c[0].a};
+      out0 = static_cast<int>(c[1].b);
+      break;
     default: return false;
   }
   // sq0 on the conv output: x0 = fma(a, s_x*s_w / s0, bias / s0)
@@ -688,7 +694,7 @@ bool make_epi(const kern::StageTables& t, int shape, double sxw, kern::EpiConsts
       return false;
     }
   }
-  if (shape == 5) {
+  if (shape == 5 || shape == kern::kShapeSqF32) {
     // fp32 output value v = r * s of the last sq (T-domain: fma(R, s, -M*s))
     const double s_last = prev_s;
     if (!exact_float(s_last, e.f32_s) ||
@@ -700,7 +706,7 @@ bool make_epi(const kern::StageTables& t, int shape, double sxw, kern::EpiConsts
     e.f32_ptr = static_cast<float*>(fb.ptr);
     e.f32_ld = fb.ld;
   }
-  e.slot_out[0] = out0 >= 0 && shape != 5 ? t.buf[out0].slot : -1;
+  e.slot_out[0] = out0 >= 0 && shape != 5 && shape != kern::kShapeSqF32 ? t.buf[out0].slot : -1;
   e.slot_out[1] = out1 >= 0 ? t.buf[out1].slot : -1;
   return true;
 }
@@ -1258,6 +1264,7 @@ void FastPlan::prepare(Run& r) {
     kern::EpiConsts& e = epi_of[si];
     int sh = sh0;
     if (sh != 0 && !make_epi(tabs[si], sh, sxw_of[si], e)) sh = 0;
+    if (sh == kern::kShapeSqF32) e.f32_cols = st.O;
     // flag-specialised kernels for the common constant profiles (fused.cuh)
     if (!no_special) {
       // a k = 1 store of a T-domain code: exact, at most a clamp
@@ -1444,7 +1451,9 @@ void FastPlan::launch_gemm(size_t si, const kern::TcConvSpec& sp) {
     const double a_bytes = st.gather ? static_cast<double>(sp.Nimg) * sp.groups * st.H * st.W * sp.ld
                                      : M * st.Ktrue;
     const double out_bytes = M * st.O * (sp.n_out + (st.res_val >= 0 ? 1 : 0)) +
-                             (sp.prog.shape == kern::kShapeAddF32 ? 4.0 * M * st.O : 0.0);
+                             (sp.prog.shape == kern::kShapeAddF32 || sp.prog.shape == kern::kShapeSqF32
+                                  ? 4.0 * M * st.O
+                                  : 0.0);
     device::profile_gemm_end(
         2.0 * M * st.O *
             (st.dense ? st.Ktrue

@@ -1029,6 +1029,9 @@ void launch_bn(const TcMapsT<kMaxGroups>* maps, const TcGroupsT<kMaxGroups>* grp
     case kShapeAddForkId:
       launch_tc<BN, kShapeAddForkId>(maps, grp, a, s);
       break;
+    case kShapeSqF32:
+      launch_tc<BN, kShapeSqF32>(maps, grp, a, s);
+      break;
     case kShapeInt:
       launch_tc<BN, kShapeInt>(maps, grp, a, s);
       break;

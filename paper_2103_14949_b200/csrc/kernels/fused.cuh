@@ -405,6 +405,26 @@ __device__ __forceinline__ void run_shape_epi(float (&x)[16], const EpiConsts& e
     return;
   }
   epi_round(x, e.q[0]);
+  if constexpr (SHAPE == kShapeSqF32) {
+    // fp32 value of the code: v = fma(R, s, off) (T-domain offset folded)
+    if (!row_ok) return;
+    float* dst = e.f32_ptr + m * e.f32_ld + n;
+    const int nv = e.f32_cols - n;
+    if (nv >= 16) {
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) {
+        *reinterpret_cast<float4*>(dst + j) = make_float4(
+            __fmaf_rn(x[j], e.f32_s, e.f32_off), __fmaf_rn(x[j + 1], e.f32_s, e.f32_off),
+            __fmaf_rn(x[j + 2], e.f32_s, e.f32_off), __fmaf_rn(x[j + 3], e.f32_s, e.f32_off));
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j < nv) dst[j] = __fmaf_rn(x[j], e.f32_s, e.f32_off);
+      }
+    }
+    return;
+  }
   if (SHAPE == kShapeStore) {
     epi_store(x, e.q[0], io, e.slot_out[0], cl);
     return;

@@ -145,6 +145,8 @@ struct EpiConsts {
   float f32_s, f32_off;
   float* f32_ptr;
   int64_t f32_ld;
+  int32_t f32_cols;  // shape 9: valid output columns (O)
+  int32_t pad2_;
   // shapes 6/7 (saturating rounding, fastplan fold_saturating): sq i's
   // input arrives pre-scaled by 1/P_i (P_i = 2^p: the code range is
   // [-P_i, P_i - 1] or [0, P_i - 1]) so add.rz.sat clamps the low side on the
@@ -168,11 +170,13 @@ struct EpiConsts {
 //      exact, no clamp): the T-domain code of sq0 is the stored byte
 //   7: shape 3 with sq0 signed rounding, sq1 non-negative rounding and both
 //      fork stores identities: one packed code, stored to both slots
+//   9: SQ, STORE_F32 (a classifier's dense -> fp32 scores; any O, the last
+//      chunk's columns past O are masked)
 //   8: integer conv/dense of a realized graph (IntEpi): exact int64 epilogue,
 //      accumulator-dtype clamp / trap, optional fused requantize, int32 NCHW out
 enum : int { kShapeGeneric = 0, kShapeStore = 1, kShapeSqStore = 2, kShapeAddFork = 3,
              kShapeAdd = 4, kShapeAddF32 = 5, kShapeSqStoreId = 6, kShapeAddForkId = 7,
-             kShapeInt = 8 };
+             kShapeInt = 8, kShapeSqF32 = 9 };
 
 // Integer epilogue (reference interpreter.cpp:238-309 then :464-482):
 //   v = acc - zp0 * wsum[o] + bias[o]          (acc = sum_k x'*w', w' = w - zp1)
