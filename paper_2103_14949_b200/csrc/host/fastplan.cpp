@@ -519,7 +519,9 @@ int classify_shape(const kern::StageTables& t, int O) {
   }
   using V = std::vector<uint8_t>;
   // fp32 scores (masked tail chunk): any O
-  if (ops == V{kern::kPSq, kern::kPStoreF32} && O % 4 == 0) return kern::kShapeSqF32;
+  if ((ops == V{kern::kPSq, kern::kPStoreF32} || ops == V{kern::kPStoreF32}) && O % 4 == 0) {
+    return kern::kShapeSqF32;
+  }
   if (O % 16 != 0) return 0;
   if (ops == V{kern::kPSqStore8}) return 1;
   if (ops == V{kern::kPSq, kern::kPSqStore8}) return 2;
@@ -654,6 +656,21 @@ bool make_epi(const kern::StageTables& t, int shape, double sxw, kern::EpiConsts
       out0 = static_cast<int>(c[3].b);
       break;
     case kern::kShapeSqF32:
+      if (t.n_code == 1) {
+        // bare fp32 store of the conv output: x0 = fma(a, s_x*s_w, bias), one
+        // rounding (the reference's float conv value), no sq
+        if (!exact_float(sxw, e.q[0].k)) return false;
+        e.q[0].flags = kern::kEpiNoClamp;
+        e.inv0 = 1.0f;
+        e.f32_s = 1.0f;
+        e.f32_off = 0.0f;
+        const kern::ProgBuf& fb = t.buf[c[0].b];
+        if (fb.kind != 1 || fb.hw != 1) return false;
+        e.f32_ptr = static_cast<float*>(fb.ptr);
+        e.f32_ld = fb.ld;
+        e.slot_out[0] = e.slot_out[1] = -1;
+        return true;
+      }
       qs = {c[0].a};
       out0 = static_cast<int>(c[1].b);
       break;
