@@ -116,7 +116,7 @@ __global__ void gap_rows_kernel(const float* __restrict__ x, int64_t ld, int N, 
 
 // max-pool -> code stores: signed byte max over the window, then each store's
 // folded sq (codes are exact floats; no conversion-pipe instructions)
-template <int NOUT>
+template <int NOUT, bool K3>
 __global__ void maxpool_stores_kernel(const int8_t* __restrict__ x, int ld, int N, int C, int H,
                                       int W, int OH, int OW, int kh, int kw, int sh, int sw, int ph,
                                       int pw, PoolStores e) {
@@ -132,17 +132,42 @@ __global__ void maxpool_stores_kernel(const int8_t* __restrict__ x, int ld, int 
     const int oh = static_cast<int>((m / OW) % OH);
     const int64_t n = m / (static_cast<int64_t>(OW) * OH);
     uint32_t best[4] = {0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u};
-    for (int a = 0; a < kh; ++a) {
-      const int ih = oh * sh - ph + a;
-      if (ih < 0 || ih >= H) continue;
-      for (int b = 0; b < kw; ++b) {
-        const int iw = ow * sw - pw + b;
-        if (iw < 0 || iw >= W) continue;
-        const int4 raw = __ldg(reinterpret_cast<const int4*>(x + ((n * H + ih) * W + iw) * ld + grp * 16));
-        best[0] = __vmaxs4(best[0], static_cast<uint32_t>(raw.x));
-        best[1] = __vmaxs4(best[1], static_cast<uint32_t>(raw.y));
-        best[2] = __vmaxs4(best[2], static_cast<uint32_t>(raw.z));
-        best[3] = __vmaxs4(best[3], static_cast<uint32_t>(raw.w));
+    if constexpr (K3) {
+      // 3x3 window: the nine (masked) 16-byte loads are issued together
+      int4 raw[9];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const int ih = oh * sh - ph + a;
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          const int iw = ow * sw - pw + b;
+          const bool ok = ih >= 0 && ih < H && iw >= 0 && iw < W;
+          raw[a * 3 + b] = ok ? __ldg(reinterpret_cast<const int4*>(
+                                    x + ((n * H + ih) * W + iw) * ld + grp * 16))
+                              : make_int4(static_cast<int>(0x80808080u), static_cast<int>(0x80808080u),
+                                          static_cast<int>(0x80808080u), static_cast<int>(0x80808080u));
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        best[0] = __vmaxs4(best[0], static_cast<uint32_t>(raw[k].x));
+        best[1] = __vmaxs4(best[1], static_cast<uint32_t>(raw[k].y));
+        best[2] = __vmaxs4(best[2], static_cast<uint32_t>(raw[k].z));
+        best[3] = __vmaxs4(best[3], static_cast<uint32_t>(raw[k].w));
+      }
+    } else {
+      for (int a = 0; a < kh; ++a) {
+        const int ih = oh * sh - ph + a;
+        if (ih < 0 || ih >= H) continue;
+        for (int b = 0; b < kw; ++b) {
+          const int iw = ow * sw - pw + b;
+          if (iw < 0 || iw >= W) continue;
+          const int4 raw = __ldg(reinterpret_cast<const int4*>(x + ((n * H + ih) * W + iw) * ld + grp * 16));
+          best[0] = __vmaxs4(best[0], static_cast<uint32_t>(raw.x));
+          best[1] = __vmaxs4(best[1], static_cast<uint32_t>(raw.y));
+          best[2] = __vmaxs4(best[2], static_cast<uint32_t>(raw.z));
+          best[3] = __vmaxs4(best[3], static_cast<uint32_t>(raw.w));
+        }
       }
     }
     float r[16];
@@ -209,16 +234,27 @@ __global__ void input_s2d_kernel(const float* __restrict__ x, int N, int C, int 
     const int h2 = static_cast<int>(t % H2);
     const int64_t n = t / H2;
     uint32_t word[4] = {0, 0, 0, 0};
+    const bool pair = (W & 1) == 0;  // the two pixels of a row are one 8-byte load
     for (int c = 0; c < C; ++c) {
       const float* plane = x + (n * C + c) * H * W;
 #pragma unroll
       for (int dy = 0; dy < 2; ++dy) {
         const int h = 2 * h2 + dy;
+        if (h >= H) continue;
+        float v[2];
+        if (pair) {
+          const float2 v2 = __ldg(reinterpret_cast<const float2*>(plane + h * W + 2 * w2));
+          v[0] = v2.x;
+          v[1] = v2.y;
+        } else {
+          v[0] = plane[h * W + 2 * w2];
+          v[1] = 2 * w2 + 1 < W ? plane[h * W + 2 * w2 + 1] : 0.0f;
+        }
 #pragma unroll
         for (int dx = 0; dx < 2; ++dx) {
           const int w = 2 * w2 + dx;
-          if (h < H && w < W) {
-            const float q = __fsub_rn(fsq_code(plane[h * W + w], p), p.zp);
+          if (w < W) {
+            const float q = __fsub_rn(fsq_code(v[dx], p), p.zp);
             const int b = (dy * 2 + dx) * C + c;
             word[b >> 2] |= static_cast<uint32_t>(static_cast<uint8_t>(static_cast<int8_t>(
                                 __float2int_rn(q))))
@@ -418,7 +454,8 @@ void stage_input_s2d(const float* x, int N, int C, int H, int W, const FSq& p, i
   const int H2 = (H + 1) / 2, W2 = (W + 1) / 2;
   const int64_t total = static_cast<int64_t>(N) * H2 * W2;
   if (total <= 0) return;
-  launch_pdl(input_s2d_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, x, N, C, H, W, H2, W2, p, out);
+  launch_pdl(input_s2d_kernel, dim3(static_cast<unsigned>((total + 255) / 256)), dim3(256), 0, s, x,
+             N, C, H, W, H2, W2, p, out);
   QC_CUDA_CHECK_LAUNCH();
 }
 
@@ -461,13 +498,17 @@ void stage_maxpool_stores(const int8_t* x, int ld, int N, int C, int H, int W, i
                           cudaStream_t s) {
   const int64_t total = static_cast<int64_t>(N) * OH * OW * (C / 16);
   if (total <= 0) return;
+  const dim3 grid(static_cast<unsigned>((total + 255) / 256));  // one item per thread
+  const bool k3 = kh == 3 && kw == 3;
+#define QC_POOL(NO, K3)                                                                       \
+  launch_pdl(maxpool_stores_kernel<NO, K3>, grid, dim3(256), 0, s, x, ld, N, C, H, W, OH, OW, \
+             kh, kw, sh, sw, ph, pw, e)
   if (e.n_out == 2) {
-    launch_pdl(maxpool_stores_kernel<2>, dim3(grid_for(total, 256)), dim3(256), 0, s, x, ld, N, C, H, W, OH, OW, kh,
-                                                                  kw, sh, sw, ph, pw, e);
+    if (k3) QC_POOL(2, true); else QC_POOL(2, false);
   } else {
-    launch_pdl(maxpool_stores_kernel<1>, dim3(grid_for(total, 256)), dim3(256), 0, s, x, ld, N, C, H, W, OH, OW, kh,
-                                                                  kw, sh, sw, ph, pw, e);
+    if (k3) QC_POOL(1, true); else QC_POOL(1, false);
   }
+#undef QC_POOL
   QC_CUDA_CHECK_LAUNCH();
 }
 
