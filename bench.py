@@ -171,12 +171,24 @@ def run_reference(args):
     sim, ev, sp = _ref_binding(ref, model, threads)
     cands = candidates(sp, args.warmup + args.steps)
     ds = ref.dataset(model.data(sample, seed=11))
+    # one step (one image per host thread) takes ~10 s here: keep the whole
+    # run within a few minutes by timing at most ~150 s worth of the K steps
+    # (the warm-up step sizes it); `steps` reports what was timed
+    est = 0.0
     for i in range(args.warmup):
+        t0 = time.perf_counter()
         ref.predict_top1(sim, ds, threads, ev.bind(cands[i]))
+        est = time.perf_counter() - t0
+    if args.warmup == 0:
+        t0 = time.perf_counter()
+        ref.predict_top1(sim, ds, threads, ev.bind(cands[0]))
+        est = time.perf_counter() - t0
+    steps = max(1, min(args.steps, int(150.0 / max(est, 1e-3))))
     t0 = time.perf_counter()
-    for i in range(args.steps):
+    for i in range(steps):
         ref.predict_top1(sim, ds, threads, ev.bind(cands[args.warmup + i]))
     dt = time.perf_counter() - t0
+    args.steps = steps
     value = sample * args.steps / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s",
