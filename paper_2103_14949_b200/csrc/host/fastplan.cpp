@@ -1582,7 +1582,7 @@ void FastPlan::predict_group(int batch, const std::vector<const float*>& inputs,
                              const std::vector<const SimBinding*>& bindings,
                              const std::vector<int64_t*>& preds) {
   const int G = static_cast<int>(bindings.size());
-  if (G < 1 || G > kern::kMaxGroups) throw std::logic_error("predict_group: 1..4 bindings");
+  if (G < 1 || G > kern::kMaxGroups) throw std::logic_error("predict_group: 1..kMaxGroups bindings");
   if (wcache_.size() > 4 * stages_.size() * static_cast<size_t>(G)) wcache_.clear();
   std::vector<Run> r(static_cast<size_t>(G));
   for (int g = 0; g < G; ++g) {

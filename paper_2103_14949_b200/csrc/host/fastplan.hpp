@@ -70,7 +70,7 @@ class FastPlan {
     std::vector<std::shared_ptr<void>> bufs;
     std::shared_ptr<void> tables;
   };
-  Arena arenas_[4];
+  Arena arenas_[kern::kMaxGroups];
   // weight code cache: (stage, FSq bytes) -> codes
   std::map<std::pair<int, std::string>, std::shared_ptr<void>> wcache_;
 
