@@ -473,7 +473,11 @@ def main():
                      "tensor": {"achieved": tops, "peak": int8_peak, "unit": "TOPS",
                                 "frac": tops / int8_peak if int8_peak else None,
                                 "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (burst)"},
-                     "kernel_share_of_step": (gms.value / prof_steps / ms_step) if ms_step > 0 else None,
+                     # the profiling pass runs one candidate per call: its
+                     # share is of the per_call step (grouped steps interleave
+                     # four candidates' launches)
+                     "kernel_share_of_step": (gms.value / prof_steps / per_call["ms_per_step"])
+                     if per_call["ms_per_step"] > 0 else None,
                      "launches_per_step": int(gl.value) // prof_steps},
         "clocks": clk.summary(),
     }
