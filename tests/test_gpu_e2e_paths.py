@@ -1,6 +1,7 @@
 """predict_top1 through the C-ABI with the dataset page-locked (default: DMA
 straight from the samples) and not (QUANTC_PIN_MAX_MB=0: packed through the
-pinned staging buffers) gives identical predictions, equal to the reference's."""
+pinned staging buffers) gives identical predictions (reference equality of
+predict_top1 is covered by test_gpu_parity.py)."""
 import json
 import os
 import subprocess
