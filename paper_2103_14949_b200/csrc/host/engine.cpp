@@ -500,16 +500,26 @@ bool Runner::exec_conv_int_tc(int i, bool dense, const kern::ConvShape& cs, cons
   const int Kpad = (Ktrue + 127) / 128 * 128;
   if (static_cast<int64_t>(Ktrue) * 255 * 128 >= (int64_t{1} << 31)) return false;  // int32 TMEM sum
   // weights: w - zp1 as int8 codes [O][Kpad] and their per-row sums
-  auto wcodes = device_alloc(static_cast<size_t>(cs.O) * Kpad + 16);
-  auto wsum = device_alloc(static_cast<size_t>(cs.O) * 4 + 16);
-  int* bad = reinterpret_cast<int*>(static_cast<int8_t*>(wsum.get()) + static_cast<size_t>(cs.O) * 4);
-  cuda_ok(cudaMemsetAsync(wsum.get(), 0, static_cast<size_t>(cs.O) * 4 + 16, S()), "wsum");
-  kern::pack_i32_weights(w.i(), static_cast<int8_t*>(wcodes.get()), static_cast<int32_t*>(wsum.get()),
-                         bad, cs.O, cs.C, taps, ld, Kpad, zps.at(1), S());
-  int hbad = 0;
-  cuda_ok(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, S()), "pack flag");
-  device::synchronize();
-  if (hbad) return false;
+  // packed weights: once per plan and layer (the range check reads one flag)
+  auto key = std::make_pair(i, 0);
+  auto wit = plan.int_weights.find(key);
+  if (wit == plan.int_weights.end()) {
+    Plan::IntWeights iw;
+    iw.codes = device_alloc(static_cast<size_t>(cs.O) * Kpad + 16);
+    iw.wsum = device_alloc(static_cast<size_t>(cs.O) * 4 + 16);
+    int* bad = reinterpret_cast<int*>(static_cast<int8_t*>(iw.wsum.get()) + static_cast<size_t>(cs.O) * 4);
+    cuda_ok(cudaMemsetAsync(iw.wsum.get(), 0, static_cast<size_t>(cs.O) * 4 + 16, S()), "wsum");
+    kern::pack_i32_weights(w.i(), static_cast<int8_t*>(iw.codes.get()), static_cast<int32_t*>(iw.wsum.get()),
+                           bad, cs.O, cs.C, taps, ld, Kpad, zps.at(1), S());
+    int hbad = 0;
+    cuda_ok(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, S()), "pack flag");
+    device::synchronize();
+    iw.ok = hbad == 0;
+    wit = plan.int_weights.emplace(key, iw).first;
+  }
+  if (!wit->second.ok) return false;
+  const std::shared_ptr<void>& wcodes = wit->second.codes;
+  const std::shared_ptr<void>& wsum = wit->second.wsum;
   // data codes NHWC.  The reference skips padded taps, i.e. they add
   // (zp0 - zp0) * w = 0; with zp0 != 0 the border is materialised as zp0 so
   // that acc - zp0 * wsum stays exact, otherwise the gather's zero fill is.
@@ -652,17 +662,26 @@ bool Runner::exec_conv_int_simt(int i, const kern::ConvShape& cs, const DevTenso
   const int64_t K = static_cast<int64_t>(taps) * Cw;
   if (!i16 && K * 4 * 255 * 128 >= (int64_t{1} << 31)) return false;  // dp4a int32 sum
   const auto& steps = plan.steps();
-  auto wwords = device_alloc(static_cast<size_t>(K) * cs.O * 4);
-  auto wsum = device_alloc(static_cast<size_t>(cs.O) * 4 + 16);
-  int* bad = reinterpret_cast<int*>(static_cast<int8_t*>(wsum.get()) + static_cast<size_t>(cs.O) * 4);
-  cuda_ok(cudaMemsetAsync(wsum.get(), 0, static_cast<size_t>(cs.O) * 4 + 16, S()), "wsum");
-  kern::pack_weight_words(w.i(), static_cast<uint32_t*>(wwords.get()),
-                          static_cast<int32_t*>(wsum.get()), bad, cs.O, cs.C, taps, Cw, i16,
-                          zps.at(1), S());
-  int hbad = 0;
-  cuda_ok(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, S()), "pack flag");
-  device::synchronize();
-  if (hbad) return false;
+  auto key = std::make_pair(i, 1);
+  auto wit = plan.int_weights.find(key);
+  if (wit == plan.int_weights.end()) {
+    Plan::IntWeights iw;
+    iw.codes = device_alloc(static_cast<size_t>(K) * cs.O * 4);
+    iw.wsum = device_alloc(static_cast<size_t>(cs.O) * 4 + 16);
+    int* bad = reinterpret_cast<int*>(static_cast<int8_t*>(iw.wsum.get()) + static_cast<size_t>(cs.O) * 4);
+    cuda_ok(cudaMemsetAsync(iw.wsum.get(), 0, static_cast<size_t>(cs.O) * 4 + 16, S()), "wsum");
+    kern::pack_weight_words(w.i(), static_cast<uint32_t*>(iw.codes.get()),
+                            static_cast<int32_t*>(iw.wsum.get()), bad, cs.O, cs.C, taps, Cw, i16,
+                            zps.at(1), S());
+    int hbad = 0;
+    cuda_ok(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, S()), "pack flag");
+    device::synchronize();
+    iw.ok = hbad == 0;
+    wit = plan.int_weights.emplace(key, iw).first;
+  }
+  if (!wit->second.ok) return false;
+  const std::shared_ptr<void>& wwords = wit->second.codes;
+  const std::shared_ptr<void>& wsum = wit->second.wsum;
   const int HP = cs.H + 2 * cs.ph, WP = cs.W + 2 * cs.pw;
   auto xwords = device_alloc(static_cast<size_t>(cs.N) * HP * WP * Cw * 4 + 16);
   kern::pack_words(d.i(), static_cast<uint32_t*>(xwords.get()), cs.N, cs.C, cs.H, cs.W, cs.ph,

@@ -87,6 +87,14 @@ class Plan {
   // split across the streams so one forward's per-layer fill/drain latency
   // overlaps another's work (dataset.cpp fused_predict)
   mutable std::vector<std::shared_ptr<fast::FastPlan>> fused_aux;
+  // realized-graph integer convs: packed weights (w - zp1) and row sums per
+  // (step, backend), built once per plan; ok = false when w - zp1 leaves
+  // the backend's range (the layer then runs on the int64 kernel)
+  struct IntWeights {
+    std::shared_ptr<void> codes, wsum;
+    bool ok = false;
+  };
+  mutable std::map<std::pair<int, int>, IntWeights> int_weights;
 };
 
 // Process-wide cache of compiled plans (device-resident constants, the fused

@@ -52,7 +52,12 @@ std::vector<std::shared_ptr<void>> feed_inputs(const Graph& g, const FeedMap& fe
 
 std::vector<Tensor> run_single(const Graph& g, const FeedMap& feed, const SimBinding* binding,
                                bool integer_regime, OverflowMode mode) {
-  engine::Plan plan(g);
+  // weights stay resident across calls on the same graph (plan cache)
+  const engine::PlanLease lease = engine::lease_plan(g);
+  const engine::Plan& plan = lease.plan();
+  // grow the allocator pool once for the run's activations (many growth
+  // steps during the run stall the host for up to seconds)
+  device::pool_reserve(static_cast<size_t>(plan.per_sample_bytes_peak()) * 2);
   auto bufs = feed_inputs(g, feed);
   engine::RunSpec spec;
   spec.batch = 1;

@@ -245,17 +245,19 @@ def deep_chain(searchable_edges: int, seed: int = 3, width: int = 8) -> Model:
 
 
 def resnet(depth: int = 50, seed: int = 42, image: int = 224, classes: int = 1000,
-           width: int = 64, residual_gain: float = 0.3) -> Model:
+           width: int = 64, residual_gain: float = 0.3, batch: int = 1) -> Model:
     """BN-folded ResNet-18/34/50/101 (torchvision topology) built from the closed
     op set: conv2d(+bias) / relu / max_pool2d / add / global_avg_pool2d /
     flatten / dense.  `residual_gain` scales the last conv of every residual
-    branch (a folded BN gamma < 1) so activations stay O(1) with depth."""
+    branch (a folded BN gamma < 1) so activations stay O(1) with depth.
+    `batch` > 1 declares a batched input [batch, 3, image, image] (one eval_int
+    call over many images; predict_top1 samples stay [1, 3, H, W])."""
     cfg = {18: ("basic", [2, 2, 2, 2]), 34: ("basic", [3, 4, 6, 3]),
            50: ("bottleneck", [3, 4, 6, 3]), 101: ("bottleneck", [3, 4, 23, 3])}
     kind, blocks = cfg[depth]
     gb = GraphBuilder()
     wts = _Weights(seed)
-    x = gb.input("data", [1, 3, image, image])
+    x = gb.input("data", [batch, 3, image, image])
     h = gb.op("relu", [_conv(gb, wts, x, width, 7, stride=2, pad=3)])
     h = gb.op("max_pool2d", [h], pool_size=[3, 3], strides=[2, 2], padding=[1, 1])
     expansion = 4 if kind == "bottleneck" else 1
@@ -283,7 +285,7 @@ def resnet(depth: int = 50, seed: int = 42, image: int = 224, classes: int = 100
     y = gb.op("dense", [f, gb.constant(wts.dense(classes, in_c)), gb.constant(wts.bias(classes))])
     gb.output(y)
     doc, blob = gb.build()
-    return Model(f"resnet{depth}", doc, blob, [1, 3, image, image], gb)
+    return Model(f"resnet{depth}", doc, blob, [batch, 3, image, image], gb)
 
 
 # ---- exact rewrites of ops outside the reference op set --------
