@@ -456,8 +456,10 @@ struct Runner {
   bool exec_conv_int_simt(int i, const kern::ConvShape& cs, const DevTensor& d,
                           const DevTensor& w, const DevTensor* b, DType acc,
                           const std::vector<int64_t>& zps);
-  int fused_requantize(int i) const;
-  void finish_int(int i, int rq, const DevTensor& y, const kern::ConvShape& cs,
+  std::vector<int> fused_chain(int i) const;
+  DType chain_dtype(const std::vector<int>& chain, DType acc) const;
+  void fill_posts(kern::IntEpi& ie, const std::vector<int>& chain) const;
+  void finish_int(int i, const std::vector<int>& chain, const DevTensor& y, const kern::ConvShape& cs,
                   const DevTensor& d, const DevTensor& w, const DevTensor* b,
                   const std::vector<int64_t>& zps);
   void exec_conv_fast(int i, bool dense);
@@ -490,7 +492,6 @@ bool Runner::exec_conv_int_tc(int i, bool dense, const kern::ConvShape& cs, cons
   }();
   if (acc.width() <= 16 && !i16_on_tc) return false;
 
-  const auto& steps = plan.steps();
   const int taps = cs.KH * cs.KW;
   const int ld = (cs.C + 15) / 16 * 16;
   const bool direct = dense || (taps == 1 && cs.sh == 1 && cs.sw == 1 && cs.ph == 0 &&
@@ -529,10 +530,8 @@ bool Runner::exec_conv_int_tc(int i, bool dense, const kern::ConvShape& cs, cons
   auto xcodes = device_alloc(static_cast<size_t>(cs.N) * HP * WP * ld + 64);
   kern::pack_i32_nhwc(d.i(), static_cast<uint8_t*>(xcodes.get()), cs.N, cs.C, cs.H, cs.W, pph,
                       ppw, ld, static_cast<int32_t>(zps.at(0)), S());
-  const int rq = fused_requantize(i);
-  DevTensor y = out_like(rq >= 0 ? rq : i, rq >= 0
-                                               ? parse_dtype(steps[static_cast<size_t>(rq)].node->attr<std::string>("out_dtype"))
-                                               : acc);
+  const std::vector<int> chain = fused_chain(i);
+  DevTensor y = out_like(chain.empty() ? i : chain.back(), chain_dtype(chain, acc));
   kern::TcConvSpec sp{};
   sp.x = static_cast<const int8_t*>(xcodes.get());
   sp.w = static_cast<const int8_t*>(wcodes.get());
@@ -566,41 +565,76 @@ bool Runner::exec_conv_int_tc(int i, bool dense, const kern::ConvShape& cs, cons
   ie.acc_max = acc.max_value();
   ie.OHW = cs.OH * cs.OW;
   ie.a_unsigned = d.dtype.is_signed() ? 0 : 1;
-  if (rq >= 0) {
-    const Node& r = *steps[static_cast<size_t>(rq)].node;
-    ie.rq = 1;
-    ie.mult = r.attr<int64_t>("multiplier");
-    ie.shift = r.attr<int>("shift");
-    ie.in_zp = r.attr_or<int64_t>("in_zero_point", 0);
-    ie.out_zp = r.attr_or<int64_t>("zero_point", 0);
-    ie.q_min = r.attr<int64_t>("q_min");
-    ie.q_max = r.attr<int64_t>("q_max");
-  }
+  fill_posts(ie, chain);
   kern::tc_conv(sp, S());
   device::counters().tcgen05_gemms++;
-  finish_int(i, rq, y, cs, d, w, b, zps);
+  finish_int(i, chain, y, cs, d, w, b, zps);
   return true;
 }
 
-// the step of a sole requantize consumer of step i (fused into i's
-// epilogue), or -1
-int Runner::fused_requantize(int i) const {
+// the sole-consumer chain after integer conv/dense step i that the
+// epilogue absorbs: up to three requantize / relu steps, each the only
+// consumer of the previous value and not a kept (output) value
+std::vector<int> Runner::fused_chain(int i) const {
+  std::vector<int> chain;
+  if (!spec.integer_regime) return chain;
   const auto& steps = plan.steps();
-  if (!spec.integer_regime || steps[static_cast<size_t>(i)].uses != 1 ||
-      keep[static_cast<size_t>(i)]) {
-    return -1;
+  int cur = i;
+  while (chain.size() < 3) {
+    if (steps[static_cast<size_t>(cur)].uses != 1 || keep[static_cast<size_t>(cur)]) break;
+    int next = -1;
+    for (size_t j = static_cast<size_t>(cur) + 1; j < steps.size(); ++j) {
+      const auto& sj = steps[j];
+      if (std::find(sj.in.begin(), sj.in.end(), cur) != sj.in.end()) {
+        next = static_cast<int>(j);
+        break;
+      }
+    }
+    if (next < 0) break;
+    const auto& sn = steps[static_cast<size_t>(next)];
+    const OpKind op = sn.node->op;
+    if (op != OpKind::kRequantize && op != OpKind::kRelu) break;
+    if (sn.in.size() != 1) break;
+    chain.push_back(next);
+    cur = next;
   }
-  for (size_t j = static_cast<size_t>(i) + 1; j < steps.size(); ++j) {
-    const auto& sj = steps[j];
-    if (std::find(sj.in.begin(), sj.in.end(), i) == sj.in.end()) continue;
-    return sj.node->op == OpKind::kRequantize ? static_cast<int>(j) : -1;
+  return chain;
+}
+
+// dtype of the chain's last value (requantize: out_dtype; relu: its input's)
+DType Runner::chain_dtype(const std::vector<int>& chain, DType acc) const {
+  DType dt = acc;
+  for (int j : chain) {
+    const Node& n = *plan.steps()[static_cast<size_t>(j)].node;
+    if (n.op == OpKind::kRequantize) dt = parse_dtype(n.attr<std::string>("out_dtype"));
   }
-  return -1;
+  return dt;
+}
+
+void Runner::fill_posts(kern::IntEpi& ie, const std::vector<int>& chain) const {
+  ie.n_post = 0;
+  for (int j : chain) {
+    const Node& n = *plan.steps()[static_cast<size_t>(j)].node;
+    kern::IntEpi::Post& p = ie.post[ie.n_post++];
+    p = kern::IntEpi::Post{};
+    if (n.op == OpKind::kRelu) {
+      p.kind = kern::kPostRelu;
+      p.out_zp = n.attr_or<int64_t>("zero_point", 0);
+    } else {
+      p.kind = kern::kPostRequantize;
+      p.mult = n.attr<int64_t>("multiplier");
+      p.shift = n.attr<int>("shift");
+      p.in_zp = n.attr_or<int64_t>("in_zero_point", 0);
+      p.out_zp = n.attr_or<int64_t>("zero_point", 0);
+      p.q_min = n.attr<int64_t>("q_min");
+      p.q_max = n.attr<int64_t>("q_max");
+    }
+  }
 }
 
 // trap check (OverflowError at the lowest flat index, value recomputed
 // exactly) and publication of the integer conv's (or fused requantize's) value
-void Runner::finish_int(int i, int rq, const DevTensor& y, const kern::ConvShape& cs,
+void Runner::finish_int(int i, const std::vector<int>& chain, const DevTensor& y, const kern::ConvShape& cs,
                         const DevTensor& d, const DevTensor& w, const DevTensor* b,
                         const std::vector<int64_t>& zps) {
   if (trap) {
@@ -612,17 +646,13 @@ void Runner::finish_int(int i, int rq, const DevTensor& y, const kern::ConvShape
       throw OverflowError(n.id, flat, v);
     }
   }
-  if (rq >= 0) {
-    vals[static_cast<size_t>(rq)] = y;
-    done[static_cast<size_t>(rq)] = 1;
-  } else {
-    vals[static_cast<size_t>(i)] = y;
-  }
+  for (int j : chain) done[static_cast<size_t>(j)] = 1;
+  vals[static_cast<size_t>(chain.empty() ? i : chain.back())] = y;
 }
 
 static kern::IntEpi int_epi(const DevTensor& y, const DevTensor* b, const void* wsum,
                             unsigned long long* trap, DType acc, const kern::ConvShape& cs,
-                            const std::vector<int64_t>& zps, const Node* rqn) {
+                            const std::vector<int64_t>& zps) {
   kern::IntEpi ie{};
   ie.y = y.i();
   ie.bias = b ? b->i() : nullptr;
@@ -632,15 +662,6 @@ static kern::IntEpi int_epi(const DevTensor& y, const DevTensor* b, const void* 
   ie.acc_min = acc.min_value();
   ie.acc_max = acc.max_value();
   ie.OHW = cs.OH * cs.OW;
-  if (rqn) {
-    ie.rq = 1;
-    ie.mult = rqn->attr<int64_t>("multiplier");
-    ie.shift = rqn->attr<int>("shift");
-    ie.in_zp = rqn->attr_or<int64_t>("in_zero_point", 0);
-    ie.out_zp = rqn->attr_or<int64_t>("zero_point", 0);
-    ie.q_min = rqn->attr<int64_t>("q_min");
-    ie.q_max = rqn->attr<int64_t>("q_max");
-  }
   return ie;
 }
 
@@ -661,7 +682,6 @@ bool Runner::exec_conv_int_simt(int i, const kern::ConvShape& cs, const DevTenso
   const int taps = cs.KH * cs.KW;
   const int64_t K = static_cast<int64_t>(taps) * Cw;
   if (!i16 && K * 4 * 255 * 128 >= (int64_t{1} << 31)) return false;  // dp4a int32 sum
-  const auto& steps = plan.steps();
   auto key = std::make_pair(i, 1);
   auto wit = plan.int_weights.find(key);
   if (wit == plan.int_weights.end()) {
@@ -686,10 +706,8 @@ bool Runner::exec_conv_int_simt(int i, const kern::ConvShape& cs, const DevTenso
   auto xwords = device_alloc(static_cast<size_t>(cs.N) * HP * WP * Cw * 4 + 16);
   kern::pack_words(d.i(), static_cast<uint32_t*>(xwords.get()), cs.N, cs.C, cs.H, cs.W, cs.ph,
                    cs.pw, Cw, i16, static_cast<int32_t>(zps.at(0)), S());
-  const int rq = fused_requantize(i);
-  const Node* rqn = rq >= 0 ? steps[static_cast<size_t>(rq)].node : nullptr;
-  DevTensor y = out_like(rq >= 0 ? rq : i,
-                         rqn ? parse_dtype(rqn->attr<std::string>("out_dtype")) : acc);
+  const std::vector<int> chain = fused_chain(i);
+  DevTensor y = out_like(chain.empty() ? i : chain.back(), chain_dtype(chain, acc));
   kern::SimtConvSpec sp{};
   sp.x = static_cast<const uint32_t*>(xwords.get());
   sp.w = static_cast<const uint32_t*>(wwords.get());
@@ -706,10 +724,11 @@ bool Runner::exec_conv_int_simt(int i, const kern::ConvShape& cs, const DevTenso
   sp.OW = cs.OW;
   sp.i16 = i16;
   sp.u8 = u8;
-  sp.ie = int_epi(y, b, wsum.get(), trap_ptr(), acc, cs, zps, rqn);
+  sp.ie = int_epi(y, b, wsum.get(), trap_ptr(), acc, cs, zps);
+  fill_posts(sp.ie, chain);
   kern::conv_int_simt(sp, S());
   device::counters().simt_int_convs++;
-  finish_int(i, rq, y, cs, d, w, b, zps);
+  finish_int(i, chain, y, cs, d, w, b, zps);
   return true;
 }
 

@@ -575,16 +575,21 @@ __device__ __forceinline__ int32_t int_epi_value(const IntEpi& ie, int64_t acc, 
     if (ie.trap) atomicMin(ie.trap, static_cast<unsigned long long>(flat));
     v = v < ie.acc_min ? ie.acc_min : ie.acc_max;
   }
-  if (ie.rq) {
-    // fixed_point_rescale, round half away from zero
-    const int64_t p = (v - ie.in_zp) * ie.mult;
-    int64_t q = p;
-    if (ie.shift > 0) {
-      const int64_t nudge = int64_t{1} << (ie.shift - 1);
-      q = p >= 0 ? (p + nudge) >> ie.shift : -((-p + nudge) >> ie.shift);
+  for (int k = 0; k < ie.n_post; ++k) {
+    const IntEpi::Post& pp = ie.post[k];
+    if (pp.kind == kPostRelu) {
+      v = v > pp.out_zp ? v : pp.out_zp;  // relu int: max(x, zero_point)
+      continue;
     }
-    q += ie.out_zp;
-    v = q < ie.q_min ? ie.q_min : (q > ie.q_max ? ie.q_max : q);
+    // requantize: fixed_point_rescale, round half away from zero
+    const int64_t p = (v - pp.in_zp) * pp.mult;
+    int64_t q = p;
+    if (pp.shift > 0) {
+      const int64_t nudge = int64_t{1} << (pp.shift - 1);
+      q = p >= 0 ? (p + nudge) >> pp.shift : -((-p + nudge) >> pp.shift);
+    }
+    q += pp.out_zp;
+    v = q < pp.q_min ? pp.q_min : (q > pp.q_max ? pp.q_max : q);
   }
   return static_cast<int32_t>(v);
 }

@@ -189,12 +189,19 @@ struct IntEpi {
   const int32_t* wsum;  // sum_k w'[o][k]; may be null when zp0 == 0
   unsigned long long* trap;  // may be null (saturate)
   int64_t zp0, acc_min, acc_max;
-  int32_t rq;  // 1: fused requantize
-  int32_t shift;
-  int64_t mult, in_zp, out_zp, q_min, q_max;
+  // fused elementwise chain after the accumulator clamp (sole-consumer
+  // requantize / relu nodes, reference interpreter.cpp:326-336, :464-482)
+  struct Post {
+    int32_t kind;   // kPostRequantize or kPostRelu
+    int32_t shift;  // requantize
+    int64_t mult, in_zp, out_zp, q_min, q_max;  // requantize; relu: out_zp = zero point
+  };
+  Post post[3];
+  int32_t n_post;
   int32_t OHW;  // output pixels per image (1 for dense)
   int32_t a_unsigned;  // A codes are uint8 (tcgen05 unsigned A)
 };
+enum : int32_t { kPostRequantize = 1, kPostRelu = 2 };
 
 // kernels receive the stage's table block in global memory
 struct ProgArgs {

@@ -453,7 +453,7 @@ def overflow_dense(k: int = 256, value: int = 127, acc: str = "int16") -> Tuple[
 
 def int_conv_probe(n=2, c=16, h=12, w=12, o=24, k=3, stride=1, pad=1, dtype="int8",
                    zp0=0, zp1=0, acc="int32", requant=None, dense=False, seed=0,
-                   wlo=None, whi=None) -> Tuple[dict, bytes]:
+                   wlo=None, whi=None, relu_zp=None, requant2=None) -> Tuple[dict, bytes]:
     """Realized-graph integer conv2d/dense probe (SPEC.md realize output
     shapes): quantize(x) -> conv2d / dense(int weights, int32 bias, zero
     points, acc dtype) [-> requantize(multiplier, shift, zero points)].
@@ -484,6 +484,12 @@ def int_conv_probe(n=2, c=16, h=12, w=12, o=24, k=3, stride=1, pad=1, dtype="int
         y = gb.op("conv2d", [q, wt, b], strides=[stride, stride], padding=[pad, pad], **attrs)
     if requant is not None:
         mult, shift, in_zp, out_zp = requant
+        y = gb.op("requantize", [y], multiplier=mult, shift=shift, in_zero_point=in_zp,
+                  zero_point=out_zp, q_min=-128, q_max=127, out_dtype="int8")
+    if relu_zp is not None:  # relu int: max(x, zero_point)
+        y = gb.op("relu", [y], zero_point=relu_zp)
+    if requant2 is not None:
+        mult, shift, in_zp, out_zp = requant2
         y = gb.op("requantize", [y], multiplier=mult, shift=shift, in_zero_point=in_zp,
                   zero_point=out_zp, q_min=-128, q_max=127, out_dtype="int8")
     gb.output(y)

@@ -28,6 +28,11 @@ CASES = {
     "7x7_s2": (dict(k=7, stride=2, pad=3, c=3, o=16, h=20, w=20), "tc"),
     "5x5_c200": (dict(k=5, pad=2, c=200, o=130, h=9, w=9, zp0=5, requant=RQ), "tc"),
     "dense": (dict(dense=True, c=300, o=70, n=5, requant=RQ), "tc"),
+    # fused requantize -> relu -> requantize chains (realized-graph pattern)
+    "rq_relu": (dict(requant=RQ, relu_zp=-3), "tc"),
+    "rq_relu_rq": (dict(requant=RQ, relu_zp=2, requant2=(1 << 30, 31, 2, 5)), "tc"),
+    "relu_acc": (dict(relu_zp=0), "tc"),
+    "simt_rq_relu": (dict(acc="int16", requant=RQ, relu_zp=1), "simt"),
     "w_zp1_out_of_int8": (dict(zp1=-10, wlo=-128, whi=127), "generic"),
     # int16-accumulator backend ((i8, i8) -> i16) on CUDA cores
     "acc_int16_saturate": (dict(acc="int16", dtype="uint8", zp0=100), "simt"),
