@@ -58,7 +58,12 @@ std::vector<Tensor> run_single(const Graph& g, const FeedMap& feed, const SimBin
   // grow the allocator pool once for the run's activations (many growth
   // steps during the run stall the host for up to seconds)
   device::pool_reserve(static_cast<size_t>(plan.per_sample_bytes_peak()) * 2);
+  static const bool hprof = std::getenv("QUANTC_HOST_PROF") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+  const auto t0 = now();
   auto bufs = feed_inputs(g, feed);
+  const auto t1 = now();
   engine::RunSpec spec;
   spec.batch = 1;
   for (auto& b : bufs) spec.inputs.push_back(static_cast<const float*>(b.get()));
@@ -67,10 +72,15 @@ std::vector<Tensor> run_single(const Graph& g, const FeedMap& feed, const SimBin
   spec.mode = mode;
   for (const PortRef& o : g.outputs()) spec.keep.push_back(plan.step_of(o.node));
   auto vals = engine::run(plan, spec);
+  const auto t2 = now();
   std::vector<Tensor> outs;
   for (size_t k = 0; k < vals.size(); ++k) {
     if (!vals[k].buf) throw EvalError("graph output was never computed");
     outs.push_back(engine::download(vals[k], 1));
+  }
+  if (hprof) {
+    std::fprintf(stderr, "run_single ms: upload %.2f run(host) %.2f sync+download %.2f\n", ms(t0, t1),
+                 ms(t1, t2), ms(t2, now()));
   }
   return outs;
 }

@@ -1073,7 +1073,7 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
   // integer epilogue are per problem)
   const bool shape_kernel = sp.prog.shape != kShapeGeneric && sp.prog.shape != kShapeInt;
   a.groups = shape_kernel ? std::max(1, std::min(sp.groups, kMaxGroups)) : 1;
-  static TcGroupsT<kMaxGroups> grp;  // host staging (launches are serial per thread)
+  thread_local TcGroupsT<kMaxGroups> grp;  // host staging of the kernel parameter (per host thread)
   for (int g = 1; g < a.groups; ++g) {
     grp.gx[g - 1] = sp.xg[g - 1];
     grp.w_l1[g - 1] = sp.w_l1g[g - 1];
@@ -1082,7 +1082,7 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
     grp.epi[g - 1] = sp.epig[g - 1];
   }
   auto x_of = [&](int g) { return g == 0 ? sp.x : sp.xg[g - 1]; };
-  static TcMapsT<kMaxGroups> maps;  // host staging of the kernel parameter
+  thread_local TcMapsT<kMaxGroups> maps;  // host staging of the kernel parameter (per host thread)
   // A: direct 2-D map over the code rows (a valid dummy when gathering);
   // im2col TMA replaces the cp.async gather where the geometry allows: 128-
   // channel K blocks (SWIZZLE_128B) or, for 64-channel layers, 64-byte K
