@@ -619,15 +619,15 @@ void Runner::fill_posts(kern::IntEpi& ie, const std::vector<int>& chain) const {
     p = kern::IntEpi::Post{};
     if (n.op == OpKind::kRelu) {
       p.kind = kern::kPostRelu;
-      p.out_zp = n.attr_or<int64_t>("zero_point", 0);
+      p.out_zp = static_cast<int32_t>(n.attr_or<int64_t>("zero_point", 0));
     } else {
       p.kind = kern::kPostRequantize;
       p.mult = n.attr<int64_t>("multiplier");
       p.shift = n.attr<int>("shift");
-      p.in_zp = n.attr_or<int64_t>("in_zero_point", 0);
-      p.out_zp = n.attr_or<int64_t>("zero_point", 0);
-      p.q_min = n.attr<int64_t>("q_min");
-      p.q_max = n.attr<int64_t>("q_max");
+      p.in_zp = static_cast<int32_t>(n.attr_or<int64_t>("in_zero_point", 0));
+      p.out_zp = static_cast<int32_t>(n.attr_or<int64_t>("zero_point", 0));
+      p.q_min = static_cast<int32_t>(n.attr<int64_t>("q_min"));
+      p.q_max = static_cast<int32_t>(n.attr<int64_t>("q_max"));
     }
   }
 }

@@ -194,7 +194,8 @@ struct IntEpi {
   struct Post {
     int32_t kind;   // kPostRequantize or kPostRelu
     int32_t shift;  // requantize
-    int64_t mult, in_zp, out_zp, q_min, q_max;  // requantize; relu: out_zp = zero point
+    int64_t mult;   // requantize
+    int32_t in_zp, out_zp, q_min, q_max;  // requantize; relu: out_zp = zero point
   };
   Post post[3];
   int32_t n_post;
