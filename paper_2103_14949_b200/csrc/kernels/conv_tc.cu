@@ -466,7 +466,9 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
             // register pair and the eight copies do not serialise on a shared one
             const int8_t* src = gsrc + (ok ? rowoff + e[2 * j] : int64_t{0});
             const uint32_t dst = dst_row + ((j ^ (p & 7)) << 4);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+            // L1-allocating: neighbouring output rows re-read the same input
+            // pixels (KH*KW taps per pixel)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
                          "r"(ok ? 16u : 0u)
                          : "memory");
           }
