@@ -46,6 +46,15 @@ void* aux_stream(int i);  // i-th auxiliary compute stream (created on first use
 bool pin_host(const void* p, size_t bytes);
 void unpin_host(const void* p);
 bool host_pinned(const void* p, size_t bytes);
+
+// A contiguous page-locked copy of a C-ABI dataset's input samples (sample s
+// at [s * bytes_per, (s + 1) * bytes_per)): one DMA per upload instead of one
+// per sample.  alloc_pinned returns nullptr when it cannot (no device, cap).
+void* alloc_pinned(size_t bytes);
+void free_pinned(void* p);
+void set_dataset_mirror(const void* dataset, const void* pinned, size_t bytes_per, int64_t n);
+void clear_dataset_mirror(const void* dataset);
+bool dataset_mirror(const void* dataset, const void** pinned, size_t* bytes_per, int64_t* n);
 void synchronize();
 size_t memory_budget_bytes();  // per-batch activation budget
 // make sure the engine stream's allocator pool holds at least `bytes` (one

@@ -452,9 +452,16 @@ int qc_dataset_create(const float* data, int64_t n_samples, const int64_t* sampl
     std::vector<int64_t> sh(sample_shape, sample_shape + ndim);
     int64_t per = shape_numel(sh);
 #ifdef QUANTC_B200
-    // B200: the samples' storage is page-locked for the dataset's lifetime,
-    // so predictions DMA straight from it (device.hpp pin_host)
-    auto ds = std::shared_ptr<Dataset>(new Dataset, [](Dataset* p) {
+    // B200: a contiguous page-locked mirror of the samples (one DMA per
+    // upload), else the samples' own storage page-locked (device.hpp)
+    const size_t total_bytes = static_cast<size_t>(n_samples) * static_cast<size_t>(per) * 4;
+    void* mirror = device::alloc_pinned(total_bytes);
+    if (mirror) std::memcpy(mirror, data, total_bytes);
+    auto ds = std::shared_ptr<Dataset>(new Dataset, [mirror](Dataset* p) {
+      if (mirror) {
+        device::clear_dataset_mirror(p);
+        device::free_pinned(mirror);
+      }
       for (const Sample& s : *p) {
         for (const Tensor& t : s.inputs) {
           if (t.dtype().is_float() && t.numel() > 0) device::unpin_host(t.floats().data());
@@ -474,9 +481,13 @@ int qc_dataset_create(const float* data, int64_t n_samples, const int64_t* sampl
       ds->push_back(std::move(s));
     }
 #ifdef QUANTC_B200
-    for (const Sample& s : *ds) {
-      const Tensor& t = s.inputs[0];
-      if (t.numel() > 0) device::pin_host(t.floats().data(), static_cast<size_t>(t.numel()) * 4);
+    if (mirror) {
+      device::set_dataset_mirror(ds.get(), mirror, static_cast<size_t>(per) * 4, n_samples);
+    } else {
+      for (const Sample& s : *ds) {
+        const Tensor& t = s.inputs[0];
+        if (t.numel() > 0) device::pin_host(t.floats().data(), static_cast<size_t>(t.numel()) * 4);
+      }
     }
 #endif
     auto h = std::make_unique<qc_dataset>();

@@ -119,6 +119,20 @@ DeviceDataset::DeviceDataset(const Graph& g, const Dataset& ds, int64_t first, i
       cudaStreamWaitEvent(us, alloc_done, 0);
       cudaEventDestroy(alloc_done);
     }
+    const void* mirror = nullptr;
+    size_t mirror_bytes = 0;
+    int64_t mirror_n = 0;
+    if (n_in == 1 && per * count > 0 && device::dataset_mirror(&ds, &mirror, &mirror_bytes, &mirror_n) &&
+        mirror_bytes == static_cast<size_t>(per) * 4 && first + count <= mirror_n) {
+      // the dataset's contiguous page-locked mirror: one DMA
+      const cudaError_t e = cudaMemcpyAsync(
+          buf.get(), static_cast<const uint8_t*>(mirror) + static_cast<size_t>(first) * mirror_bytes,
+          static_cast<size_t>(count) * mirror_bytes, cudaMemcpyHostToDevice, us);
+      if (e != cudaSuccess) throw DeviceError(std::string("dataset upload: ") + cudaGetErrorString(e));
+      bufs_.push_back(buf);
+      per_.push_back(per);
+      continue;
+    }
     bool pinned = per * count > 0;
     for (int64_t s = 0; s < count && pinned; ++s) {
       pinned = device::host_pinned(ds[static_cast<size_t>(first + s)].inputs[k].floats().data(),

@@ -135,6 +135,66 @@ bool host_pinned(const void* p, size_t bytes) {
   return a + bytes <= it->first + it->second;
 }
 
+namespace {
+struct Mirror {
+  const void* pinned;
+  size_t bytes_per;
+  int64_t n;
+};
+std::mutex& mirror_mu() {
+  static std::mutex* m = new std::mutex;
+  return *m;
+}
+std::map<const void*, Mirror>& mirrors() {
+  static auto* m = new std::map<const void*, Mirror>;
+  return *m;
+}
+}  // namespace
+
+void* alloc_pinned(size_t bytes) {
+  static const size_t cap = [] {
+    const char* e = std::getenv("QUANTC_PIN_MAX_MB");
+    return (e ? static_cast<size_t>(std::max(0, std::atoi(e))) : size_t{16384}) << 20;
+  }();
+  if (bytes == 0 || bytes > cap) return nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  ctx();
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void free_pinned(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+void set_dataset_mirror(const void* dataset, const void* pinned, size_t bytes_per, int64_t n) {
+  std::lock_guard<std::mutex> lk(mirror_mu());
+  mirrors()[dataset] = Mirror{pinned, bytes_per, n};
+}
+
+void clear_dataset_mirror(const void* dataset) {
+  std::lock_guard<std::mutex> lk(mirror_mu());
+  mirrors().erase(dataset);
+}
+
+bool dataset_mirror(const void* dataset, const void** pinned, size_t* bytes_per, int64_t* n) {
+  std::lock_guard<std::mutex> lk(mirror_mu());
+  auto it = mirrors().find(dataset);
+  if (it == mirrors().end()) return false;
+  *pinned = it->second.pinned;
+  *bytes_per = it->second.bytes_per;
+  *n = it->second.n;
+  return true;
+}
+
 void* stream() { return ctx().stream; }
 void* copy_stream() { return ctx().copy_stream; }
 
