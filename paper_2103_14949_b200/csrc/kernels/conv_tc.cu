@@ -637,7 +637,7 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
             scale_g = gr.scale[grp - 1];
           }
         }
-        const EpiConsts& e = *ep;
+        const EpiConsts e = *ep;  // per-tile copy: loop-invariant constants stay in registers
         const bool small = (small_mask >> grp) & 1u;
         const float* btg = btab + grp * btab_n;
 #pragma unroll 1
