@@ -1124,7 +1124,9 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
   }
   // a wide tile whose slot sets cannot be double-buffered: halve it when the
   // narrower one can (per-tile store drains / residual loads then overlap)
-  if (BN == 256 && !dbuf_fits(a, 256, sp.prog.shape != 0) && dbuf_fits(a, 128, sp.prog.shape != 0)) {
+  static const bool keep_wide = std::getenv("QUANTC_KEEP_WIDE_TILES") != nullptr;
+  if (!keep_wide && BN == 256 && !dbuf_fits(a, 256, sp.prog.shape != 0) &&
+      dbuf_fits(a, 128, sp.prog.shape != 0)) {
     BN = 128;
   }
   const int swz = BN >= 128 ? 128 : 64;
