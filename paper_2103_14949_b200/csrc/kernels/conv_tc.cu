@@ -297,11 +297,25 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
   const int tiles_g = args.m_tiles * args.n_tiles;  // tiles of one group
   const int n_tiles_total = tiles_g * args.groups;
   // persistent tile t -> (group, row and column origin)
+  // (no integer division: the group by comparison, the row tile by a
+  // multiply-high with a host-free reciprocal and an exact correction)
+  const uint32_t nt = static_cast<uint32_t>(args.n_tiles);
+  // ~2^32 / n_tiles (n_tiles == 1: the quotient is lt itself)
+  const uint32_t nt_rcp = nt > 1 ? 0xFFFFFFFFu / nt + 1u : 0u;
   auto tile_at = [&](int t, int& grp, int& m0, int& n0) {
-    grp = NG > 1 ? t / tiles_g : 0;
-    const int lt = t - grp * tiles_g;
-    m0 = (lt / args.n_tiles) * BM;
-    n0 = (lt % args.n_tiles) * BN;
+    uint32_t lt = static_cast<uint32_t>(t);
+    grp = 0;
+    if constexpr (NG > 1) {
+      while (grp + 1 < args.groups && lt >= static_cast<uint32_t>(tiles_g)) {
+        lt -= static_cast<uint32_t>(tiles_g);
+        ++grp;
+      }
+    }
+    uint32_t q = nt > 1 ? __umulhi(lt, nt_rcp) : lt;
+    if (q * nt > lt) --q;
+    if ((q + 1u) * nt <= lt) ++q;
+    m0 = static_cast<int>(q) * BM;
+    n0 = static_cast<int>(lt - q * nt) * BN;
   };
 
   if (threadIdx.x == 0) {
