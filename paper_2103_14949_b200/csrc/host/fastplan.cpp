@@ -1634,7 +1634,11 @@ void FastPlan::predict_group(int batch, const std::vector<const float*>& inputs,
       launch_gemm(si, head);
     }
   }
-  for (int g = 0; g < G; ++g) finish(r[g]);
+  // one argmax launch for the group's outputs (finish() per binding otherwise)
+  std::vector<const float*> outs(static_cast<size_t>(G));
+  for (int g = 0; g < G; ++g) outs[g] = static_cast<const float*>(buf(r[g], out_val_));
+  kern::argmax_rows_multi(outs.data(), preds.data(), G, batch, out_per_sample_, ST());
+  device::counters().fused_batches += G;
 }
 
 }  // namespace quantc::fast

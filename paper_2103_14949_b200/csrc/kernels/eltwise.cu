@@ -123,6 +123,59 @@ __global__ void __launch_bounds__(256) argmax_kernel(const float* __restrict__ x
   }
 }
 
+// argmax of group blockIdx.y's rows (grouped candidate evaluation)
+struct RowsPack {
+  const float* x[4];
+  int64_t* out[4];
+};
+__global__ void __launch_bounds__(256) argmax_multi_kernel(RowsPack p, int64_t cols) {
+  pdl_trigger();
+  pdl_wait();
+  const float* row = p.x[blockIdx.y] + static_cast<int64_t>(blockIdx.x) * cols;
+  float bv = -FLT_MAX;
+  int64_t bi = -1;
+  for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
+    const float v = row[c];
+    if (bi < 0 || v > bv) {
+      bv = v;
+      bi = c;
+    }
+  }
+  __shared__ float sv[256];
+  __shared__ int64_t si[256];
+  sv[threadIdx.x] = bv;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  // first maximum in column order (strict >, lowest index on ties), like argmax_kernel
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      const float v2 = sv[threadIdx.x + w];
+      const int64_t i2 = si[threadIdx.x + w];
+      if (i2 >= 0 && (si[threadIdx.x] < 0 || v2 > sv[threadIdx.x] ||
+                      (v2 == sv[threadIdx.x] && i2 < si[threadIdx.x]))) {
+        sv[threadIdx.x] = v2;
+        si[threadIdx.x] = i2;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) p.out[blockIdx.y][blockIdx.x] = si[0];
+}
+
+// counts[g] += #{i : a[g * n + i] == b[i]} for group g = blockIdx.y
+__global__ void count_equal_multi_kernel(const int64_t* a, const int64_t* b, int n,
+                                         unsigned long long* counts) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t* ag = a + static_cast<int64_t>(blockIdx.y) * n;
+  unsigned int mine = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    mine += ag[i] == b[i];
+  }
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(counts + blockIdx.y, static_cast<unsigned long long>(mine));
+}
+
 __global__ void count_equal_kernel(const int64_t* a, const int64_t* b, int n,
                                    unsigned long long* count) {
   pdl_trigger();
@@ -174,6 +227,26 @@ void gap_f32(const float* x, float* y, int NC, int HW, cudaStream_t s) {
 void argmax_rows(const float* x, int rows, int64_t cols, int64_t* out, cudaStream_t s) {
   if (rows <= 0) return;
   launch_pdl(argmax_kernel, dim3(rows), dim3(256), 0, s, x, cols, out);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+void argmax_rows_multi(const float* const* xs, int64_t* const* outs, int groups, int rows,
+                       int64_t cols, cudaStream_t s) {
+  if (rows <= 0 || groups <= 0 || groups > 4) return;
+  RowsPack p{};
+  for (int g = 0; g < groups; ++g) {
+    p.x[g] = xs[g];
+    p.out[g] = outs[g];
+  }
+  launch_pdl(argmax_multi_kernel, dim3(rows, groups), dim3(256), 0, s, p, cols);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+void count_equal_multi(const int64_t* a, const int64_t* b, int n, int groups,
+                       unsigned long long* counts, cudaStream_t s) {
+  if (n <= 0 || groups <= 0) return;
+  launch_pdl(count_equal_multi_kernel, dim3(grid_for(n, 256, 64), groups), dim3(256), 0, s, a, b,
+             n, counts);
   QC_CUDA_CHECK_LAUNCH();
 }
 

@@ -62,6 +62,12 @@ void maxpool_f32(const float* x, float* y, int N, int C, int H, int W, int OH, i
                  int kw, int sh, int sw, int ph, int pw, cudaStream_t s);
 void gap_f32(const float* x, float* y, int NC, int HW, cudaStream_t s);
 void argmax_rows(const float* x, int rows, int64_t cols, int64_t* out, cudaStream_t s);
+// grouped candidate evaluation: argmax of `groups` (<= 4) row blocks in one
+// launch, and counts[g] += #{i : a[g*n + i] == b[i]}
+void argmax_rows_multi(const float* const* xs, int64_t* const* outs, int groups, int rows,
+                       int64_t cols, cudaStream_t s);
+void count_equal_multi(const int64_t* a, const int64_t* b, int n, int groups,
+                       unsigned long long* counts, cudaStream_t s);
 void count_equal(const int64_t* a, const int64_t* b, int n, unsigned long long* count,
                  cudaStream_t s);
 
