@@ -1596,6 +1596,25 @@ void FastPlan::predict_group(int batch, const std::vector<const float*>& inputs,
   static const bool no_group = std::getenv("QUANTC_NO_GROUPED") != nullptr;
   std::vector<kern::TcConvSpec> sp(static_cast<size_t>(G));
   for (size_t si = 0; si < stages_.size(); ++si) {
+    if (stages_[si]->kind == Stage::kInput && G > 1) {
+      // space-to-depth input of all bindings in one launch (one read of the images)
+      const Stage& st = *stages_[si];
+      const Val* sv = nullptr;
+      for (int vid : st.buf_vals) {
+        if (vals_[static_cast<size_t>(vid)]->s2d) sv = vals_[static_cast<size_t>(vid)].get();
+      }
+      if (sv && st.code.size() == 1 && st.code[0].op == kern::kPSqStore8 && sv->s2d_C <= 4) {
+        std::vector<FSq> ps(static_cast<size_t>(G));
+        std::vector<int8_t*> outs(static_cast<size_t>(G));
+        for (int g = 0; g < G; ++g) {
+          ps[g] = r[g].tabs[si].sq[st.code[0].a];
+          outs[g] = static_cast<int8_t*>(buf(r[g], st.buf_vals[0]));
+        }
+        kern::stage_input_s2d_multi(r[0].inputs.at(static_cast<size_t>(st.input_k)), batch * st.n0,
+                                    sv->s2d_C, sv->s2d_H, sv->s2d_W, ps.data(), outs.data(), G, ST());
+        continue;
+      }
+    }
     if (stages_[si]->kind != Stage::kGemm) {
       for (int g = 0; g < G; ++g) run_stage(r[g], si);
       continue;

@@ -194,6 +194,10 @@ void weight_codes_v2(const float* w, int8_t* codes, int O, int C, int taps, int 
 // [N, ceil(H/2), ceil(W/2), 16], channel ((h%2)*2 + w%2)*C + c (C <= 4)
 void stage_input_s2d(const float* x, int N, int C, int H, int W, const FSq& p, int8_t* out,
                      cudaStream_t s);
+// the same images under up to four bindings (grouped evaluation): one read,
+// one space-to-depth code image per binding
+void stage_input_s2d_multi(const float* x, int N, int C, int H, int W, const FSq* ps,
+                           int8_t* const* outs, int groups, cudaStream_t s);
 // weight codes [O][Kpad] of the space-to-depth form of a stride-2 KHxKW conv
 // (KH2 x KW2 taps of 16 channels; original tap = 2*ka + dy - dh, 2*kb + dx - dw)
 void weight_codes_s2d(const float* w, int8_t* codes, int O, int C, int KH, int KW, int KH2,

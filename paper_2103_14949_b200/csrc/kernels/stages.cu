@@ -268,6 +268,68 @@ __global__ void input_s2d_kernel(const float* __restrict__ x, int N, int C, int 
                   static_cast<int>(word[3]));
   }
 }
+// the same images quantized under up to four bindings (grouped candidate
+// evaluation): each pixel is read once and written once per binding
+struct S2dMulti {
+  FSq p[4];
+  int8_t* out[4];
+};
+__global__ void input_s2d_multi_kernel(const float* __restrict__ x, int N, int C, int H, int W,
+                                       int H2, int W2, S2dMulti m, int groups) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t total = static_cast<int64_t>(N) * H2 * W2;
+  const bool pair = (W & 1) == 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int w2 = static_cast<int>(i % W2);
+    const int64_t t = i / W2;
+    const int h2 = static_cast<int>(t % H2);
+    const int64_t n = t / H2;
+    float v[4][4] = {};  // [c][dy*2 + dx], C <= 4 (fully unrolled: registers)
+    bool ok[4] = {false, false, false, false};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (c >= C) break;
+      const float* plane = x + (n * C + c) * H * W;
+#pragma unroll
+      for (int dy = 0; dy < 2; ++dy) {
+        const int h = 2 * h2 + dy;
+        ok[dy * 2] = h < H;
+        ok[dy * 2 + 1] = h < H && 2 * w2 + 1 < W;
+        if (h >= H) continue;
+        if (pair) {
+          const float2 v2 = __ldg(reinterpret_cast<const float2*>(plane + h * W + 2 * w2));
+          v[c][dy * 2] = v2.x;
+          v[c][dy * 2 + 1] = v2.y;
+        } else {
+          v[c][dy * 2] = plane[h * W + 2 * w2];
+          v[c][dy * 2 + 1] = 2 * w2 + 1 < W ? plane[h * W + 2 * w2 + 1] : 0.0f;
+        }
+      }
+    }
+    for (int g = 0; g < groups; ++g) {
+      uint32_t word[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (c >= C) break;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (!ok[k]) continue;
+          const float q = __fsub_rn(fsq_code(v[c][k], m.p[g]), m.p[g].zp);
+          const int b = k * C + c;
+          word[b >> 2] |= static_cast<uint32_t>(static_cast<uint8_t>(static_cast<int8_t>(
+                              __float2int_rn(q))))
+                          << (8 * (b & 3));
+        }
+      }
+      *reinterpret_cast<int4*>(m.out[g] + i * 16) =
+          make_int4(static_cast<int>(word[0]), static_cast<int>(word[1]), static_cast<int>(word[2]),
+                    static_cast<int>(word[3]));
+    }
+  }
+}
+
 
 // weight codes of the space-to-depth conv: k = tap*16 + ch, tap = ka*KW2 + kb,
 // ch = (dy*2 + dx)*C + c  <->  original tap (2*ka + dy - dh, 2*kb + dx - dw)
@@ -456,6 +518,21 @@ void stage_input_s2d(const float* x, int N, int C, int H, int W, const FSq& p, i
   if (total <= 0) return;
   launch_pdl(input_s2d_kernel, dim3(static_cast<unsigned>((total + 255) / 256)), dim3(256), 0, s, x,
              N, C, H, W, H2, W2, p, out);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+void stage_input_s2d_multi(const float* x, int N, int C, int H, int W, const FSq* ps,
+                           int8_t* const* outs, int groups, cudaStream_t s) {
+  const int H2 = (H + 1) / 2, W2 = (W + 1) / 2;
+  const int64_t total = static_cast<int64_t>(N) * H2 * W2;
+  if (total <= 0 || groups <= 0 || groups > 4 || C > 4) return;
+  S2dMulti m{};
+  for (int g = 0; g < groups; ++g) {
+    m.p[g] = ps[g];
+    m.out[g] = outs[g];
+  }
+  launch_pdl(input_s2d_multi_kernel, dim3(static_cast<unsigned>((total + 255) / 256)), dim3(256), 0,
+             s, x, N, C, H, W, H2, W2, m, groups);
   QC_CUDA_CHECK_LAUNCH();
 }
 
