@@ -31,6 +31,8 @@
 #include "quantc/topology.hpp"
 #ifdef QUANTC_B200
 #include "quantc/device.hpp"
+#include "quantc/serialize.hpp"
+#include "quantc_files.h"
 #include "quantc_cuda.h"
 #endif
 
@@ -357,6 +359,39 @@ int qc_edge_order(const qc_graph* g, int64_t* out, size_t cap, size_t* n_edges) 
     if (n_edges) *n_edges = n4 / 4;
   });
 }
+
+// ---- files (quantc_files.h; B200 library only: the reference declares
+// serialize.hpp without implementing it) ----------------------------------
+#ifdef QUANTC_B200
+
+int qc_graph_save(const qc_graph* g, const char* json_path) {
+  return run([&] { save_graph(*g->g, json_path); });
+}
+
+int qc_graph_load(const char* json_path, qc_graph** out) {
+  return run([&] { *out = new qc_graph{std::make_shared<Graph>(load_graph(json_path))}; });
+}
+
+int qc_stats_save(const qc_stats* s, const char* path) {
+  return run([&] { save_stats(s->s, path); });
+}
+
+int qc_stats_load(const char* path, qc_stats** out) {
+  return run([&] {
+    auto h = std::make_unique<qc_stats>();
+    h->s = load_stats(path);
+    *out = h.release();
+  });
+}
+
+int qc_fingerprint_graph(const qc_graph* g, uint64_t* out) {
+  return run([&] { *out = fingerprint_graph(*g->g); });
+}
+
+int qc_fnv1a64(const void* data, size_t size, uint64_t seed, uint64_t* out) {
+  return run([&] { *out = fnv1a64(data, size, seed); });
+}
+#endif  // QUANTC_B200
 
 // ---- hwspec ---------------------------------------------------------------
 

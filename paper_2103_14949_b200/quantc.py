@@ -246,6 +246,33 @@ class Quantc:
                                                C.byref(h)))
         return Graph(self, h)
 
+    def _bind(self, name, res, args):
+        """Bind an entry point the reference build may not export (the
+        serialize.hpp files are B200-library only)."""
+        fn = getattr(self.lib, name)
+        fn.restype, fn.argtypes = res, args
+        return fn
+
+    # -- files (serialize.hpp) ------------------------------------------
+    def load_graph(self, path) -> "Graph":
+        h = C.c_void_p()
+        fn = self._bind("qc_graph_load", C.c_int, [C.c_char_p, C.POINTER(_P)])
+        self.check(fn(str(path).encode(), C.byref(h)))
+        return Graph(self, h)
+
+    def load_stats(self, path) -> "CalibrationStats":
+        h = C.c_void_p()
+        fn = self._bind("qc_stats_load", C.c_int, [C.c_char_p, C.POINTER(_P)])
+        self.check(fn(str(path).encode(), C.byref(h)))
+        return CalibrationStats(self, h)
+
+    def fnv1a64(self, data: bytes, seed: int = 1469598103934665603) -> int:
+        out = C.c_uint64()
+        fn = self._bind("qc_fnv1a64", C.c_int, [C.c_char_p, _SZ, C.c_uint64,
+                                                 C.POINTER(C.c_uint64)])
+        self.check(fn(data, len(data), seed, C.byref(out)))
+        return out.value
+
     def parse_spec(self, text) -> "HardwareSpec":
         if isinstance(text, dict):
             text = json.dumps(text)
@@ -535,6 +562,17 @@ class Graph(_Handle):
         self.q.check(fn(self.h, buf, n.value, C.byref(n)))
         return buf.raw[: n.value]
 
+    def save(self, path):
+        """Graph file + '<stem>.bin' sidecar (serialize.hpp save_graph)."""
+        fn = self.q._bind("qc_graph_save", C.c_int, [_P, C.c_char_p])
+        self.q.check(fn(self.h, str(path).encode()))
+
+    def fingerprint(self) -> int:
+        out = C.c_uint64()
+        fn = self.q._bind("qc_fingerprint_graph", C.c_int, [_P, C.POINTER(C.c_uint64)])
+        self.q.check(fn(self.h, C.byref(out)))
+        return out.value
+
     def copy_to(self, q: "Quantc") -> "Graph":
         """The same graph inside another library exporting this ABI (JSON +
         blob round trip), e.g. a realized graph handed to the reference."""
@@ -638,6 +676,11 @@ class CalibrationStats(_Handle):
 
     def per_edge(self) -> Dict[int, dict]:
         return {k: self.get(k) for k in self.edges()}
+
+    def save(self, path):
+        """Stats file (serialize.hpp save_stats)."""
+        fn = self.q._bind("qc_stats_save", C.c_int, [_P, C.c_char_p])
+        self.q.check(fn(self.h, str(path).encode()))
 
     def estimate_thresholds(self, method="quantile", quantile=0.99, kl_bits=8,
                             pow2=False) -> Dict[int, float]:
