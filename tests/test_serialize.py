@@ -118,3 +118,21 @@ def test_load_errors_are_io_errors(b200, tmp_path):
     (tmp_path / "m.bin").write_bytes(b"\0" * 8)  # truncated sidecar
     with pytest.raises(Q.QuantcError):
         b200.load_graph(tmp_path / "m.json")
+
+
+def test_cpp_dataset_strategy_trace_round_trip(tmp_path):
+    """The C++-only files (dataset manifest, strategy, trace): a small program
+    built against include/quantc/serialize.hpp and the B200 library."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    pkg = os.path.join(root, "paper_2103_14949_b200")
+    vendor = os.path.join(pkg, "csrc", "build", "vendor")
+    exe = tmp_path / "roundtrip"
+    subprocess.run(["g++", "-std=c++20", "-O1", f"-I{root}/include", f"-I{vendor}",
+                    os.path.join(root, "tests", "cpp", "serialize_roundtrip.cpp"),
+                    f"-L{pkg}", "-lquantc_b200", f"-Wl,-rpath,{pkg}", "-o", str(exe)],
+                   check=True, capture_output=True)
+    r = subprocess.run([str(exe), str(tmp_path)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert "ok" in r.stdout
