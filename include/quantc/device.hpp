@@ -91,11 +91,15 @@ void profile_read(double* gemm_ms, int64_t* gemm_launches, double* gemm_ops,
 // exact extrema of the listed canonical edges over this shard; pass 2
 // histograms against the GLOBAL absmax (after the extrema all-reduce).
 // collect_stats == pass1 + absmax + pass2 on one shard.
+// shard_key != 0 (e.g. the C-ABI dataset handle's uid) lets pass 2 on the
+// same graph, key and edges reuse the activations pass 1 kept resident; 0
+// recomputes the forward in pass 2.  (quantc/distributed.hpp's collect_stats
+// runs both passes and the merges in one call.)
 void collect_extrema(const Graph& g, const std::vector<Sample>& shard, const std::vector<int>& edges,
-                     std::vector<double>* mins, std::vector<double>* maxs);
+                     std::vector<double>* mins, std::vector<double>* maxs, uint64_t shard_key = 0);
 void collect_histograms(const Graph& g, const std::vector<Sample>& shard,
                         const std::vector<int>& edges, const std::vector<double>& absmax, int bins,
-                        std::vector<int64_t>* counts /* edges x bins */);
+                        std::vector<int64_t>* counts /* edges x bins */, uint64_t shard_key = 0);
 
 // predict_top1's fp32 score rows (first graph output, samples x per-sample
 // numel) under the active engine mode: the fused int8 engine in auto/fast

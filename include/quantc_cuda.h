@@ -96,6 +96,13 @@ int qc_collect_histograms(const qc_graph* g, const qc_dataset* d, const int* edg
  * qc_evaluator_strategy) into an integer graph for qc_eval_int. */
 int qc_realize(const qc_graph* sim_g, const char* strategy_json, const qc_spec* spec,
                qc_graph** out);
+/* realize.hpp helpers: fixed-point requantize parameters,
+ * storage dtype (candidates as "int8,int16"; writes the dtype name), and the
+ * integer clip bounds of rewrite_clip. */
+int qc_requantize_params(double s_in, double s_out, int32_t* multiplier, int* shift);
+int qc_choose_storage_dtype(int bit, const char* candidates_csv, int sign, char* out, size_t cap);
+int qc_rewrite_clip(double min_f, double max_f, double s_out, int64_t zero_point,
+                    const char* storage, int64_t* q_min, int64_t* q_max);
 /* fp32 score rows of predict_top1 (samples x per-sample numel) under the
  * active engine mode (B200 extension; quantc/device.hpp predict_scores). */
 int qc_predict_scores(const qc_graph* g, const qc_dataset* d, const int64_t* bind_nodes,
@@ -111,6 +118,46 @@ int qcu_counters(int64_t* steps, int64_t* tcgen05_gemms, int64_t* f64_convs,
 /* realized-graph integer conv/dense layers run on the CUDA-core backend
  * (int16 codes / int16 accumulator; kernels/conv_simt.cu) since load */
 int qcu_simt_int_convs(int64_t* n);
+
+/* ---- distributed hot path (quantc/comm.hpp, quantc/distributed.hpp) ------
+ * One process per GPU.  A communicator is NCCL (libnccl.so.2 bound at run
+ * time; the 128-byte unique id comes from one rank and is shared out of band)
+ * or host callbacks over the caller's own transport (e.g. torch.distributed
+ * gloo).  Every rank must make the same calls in the same order. */
+typedef struct qc_comm qc_comm;
+typedef int (*qc_comm_sum_i64_fn)(int64_t* data, size_t n, void* user);
+typedef int (*qc_comm_f64_fn)(double* data, size_t n, int op /* 0 min, 1 max */, void* user);
+typedef int (*qc_comm_gather_f64_fn)(const double* send, size_t n, double* recv, void* user);
+int qc_comm_local(qc_comm** out);
+int qc_comm_nccl_unique_id(char id[128]);
+int qc_comm_nccl(int rank, int world, const char id[128], qc_comm** out);
+int qc_comm_callbacks(int rank, int world, qc_comm_sum_i64_fn sum_i64, qc_comm_f64_fn minmax_f64,
+                      qc_comm_gather_f64_fn gather_f64, void* user, qc_comm** out);
+void qc_comm_free(qc_comm* c);
+/* collect_stats over every rank's shard `d` (all-reduced extrema, then
+ * histograms; EdgeStats.sample_count is the global count). */
+int qc_collect_stats_dist(const qc_graph* g, const qc_dataset* d, qc_comm* comm, int bins,
+                          const int* edges, size_t n_edges, qc_stats** out);
+/* CandidateEvaluator::scores (B200 extension): fp32 output rows of each
+ * candidate's forward, [n_cands x N x per_sample], `group` candidates per
+ * grouped launch (0: default). */
+int qc_evaluator_scores(const qc_evaluator* e, const int* cands, size_t n_cands, size_t n_slots,
+                        int group, float* out, size_t cap, size_t* n_out, int64_t* per_sample);
+/* The batched / speculative searches (search.hpp *_batched; results and
+ * traces identical to qc_search).  Loss source: `fn` (a batch callback) when
+ * non-NULL, else the evaluator: mode QC_LOSS_LOCAL (this process only),
+ * QC_LOSS_SAMPLES (ev holds this rank's calibration shard; counts
+ * all-reduced over comm) or QC_LOSS_CANDIDATES (ev holds the full set; each
+ * batch split over ranks, losses all-gathered).  spec_stats (optional):
+ * batches, evaluated, committed. */
+typedef int (*qc_batch_loss_fn)(const int* cands, size_t n_cands, size_t n_slots, void* user,
+                                double* losses);
+enum { QC_LOSS_LOCAL = 0, QC_LOSS_SAMPLES = 1, QC_LOSS_CANDIDATES = 2 };
+int qc_search_batched(int method, const int* edges, const int* lo, const int* hi, size_t n_slots,
+                      qc_batch_loss_fn fn, void* user, const qc_evaluator* ev, qc_comm* comm,
+                      int loss_mode, const qc_search_params* p, int width, int* best,
+                      double* best_loss, int64_t* evaluations, char** trace_json,
+                      int64_t* spec_stats);
 
 #ifdef __cplusplus
 }

@@ -26,6 +26,7 @@
 #include "dataset.hpp"
 #include "engine.hpp"
 #include "quantc/device.hpp"
+#include "quantc/distributed.hpp"
 
 namespace quantc {
 
@@ -250,64 +251,28 @@ struct ShardPasses {
   }
 };
 
-// Pass-1 -> pass-2 handoff of the sharded calibration (the two C-ABI calls
-// collect_extrema / collect_histograms on one shard, between which the
-// caller all-reduces the extrema): pass 1 keeps the targets' activations
-// resident when they fit the memory budget, exactly like collect_stats'
-// single-call cache, and the next collect_histograms on the same graph,
-// shard and edges consumes them instead of re-running the forward.
-struct Handoff {
-  uint64_t graph_uid = 0;
-  const Dataset* shard = nullptr;
-  size_t shard_size = 0;
-  const void* first_sample = nullptr;
-  std::vector<int> edges;
+// Activations pass 1 keeps resident for pass 2 (when the whole shard's
+// target activations fit the memory budget), exactly like collect_stats'
+// single-call cache: pass 2 then reads them instead of re-running the forward.
+struct PassCache {
   std::vector<int> edge_slot;
   int n_slots = 0;
   std::vector<std::vector<std::pair<int, engine::DevTensor>>> batches;  // (slot, value)
   std::vector<int> batch_size;
 };
-std::mutex g_handoff_mu;
-std::unique_ptr<Handoff> g_handoff;
 
-const void* first_sample_ptr(const Dataset& ds) {
-  if (ds.empty() || ds[0].inputs.empty() || ds[0].inputs[0].numel() == 0) return nullptr;
-  return ds[0].inputs[0].dtype().is_float() ? static_cast<const void*>(ds[0].inputs[0].floats().data())
-                                           : static_cast<const void*>(ds[0].inputs[0].ints().data());
-}
-
-}  // namespace
-
-void collect_extrema(const Graph& g, const Dataset& shard, const std::vector<int>& edges,
-                     std::vector<double>* mins, std::vector<double>* maxs) {
-  if (shard.empty()) throw CalibrationError("calibration dataset is empty");
-  static const bool hprof = std::getenv("QUANTC_HOST_PROF") != nullptr;
-  const auto t0 = std::chrono::steady_clock::now();
-  ShardPasses sp(g, shard, edges);
-  if (hprof) {
-    device::synchronize();
-    std::fprintf(stderr, "collect_extrema: plan lease + upload %.1f ms\n",
-                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
-  }
+// Pass 1 over one shard: exact per-edge extrema (calibration.cpp:62-91).
+std::unique_ptr<PassCache> pass_extrema(ShardPasses& sp, bool keep, std::vector<double>* mins,
+                                        std::vector<double>* maxs) {
   auto keys = engine::device_alloc(static_cast<size_t>(sp.n_slots) * 16 + 16);
   auto* k64 = static_cast<unsigned long long*>(keys.get());
   kern::minmax_init(k64, sp.n_slots, S());
-  {
-    std::lock_guard<std::mutex> lk(g_handoff_mu);
-    g_handoff.reset();  // a new pass 1 supersedes any unconsumed handoff
-  }
-  std::unique_ptr<Handoff> h;
-  if (sp.resident_bytes() <= static_cast<int64_t>(device::memory_budget_bytes())) {
+  std::unique_ptr<PassCache> h;
+  if (keep && sp.resident_bytes() <= static_cast<int64_t>(device::memory_budget_bytes())) {
     // grow the stream-ordered pool once for the retained activations (plus a
     // batch's transient working set) instead of in many small mappings
-    // during the forward
     device::pool_reserve(static_cast<size_t>(sp.resident_bytes()) * 5 / 4);
-    h = std::make_unique<Handoff>();
-    h->graph_uid = g.uid();
-    h->shard = &shard;
-    h->shard_size = shard.size();
-    h->first_sample = first_sample_ptr(shard);
-    h->edges = edges;
+    h = std::make_unique<PassCache>();
     h->edge_slot = sp.edge_slot;
     h->n_slots = sp.n_slots;
   }
@@ -322,10 +287,6 @@ void collect_extrema(const Graph& g, const Dataset& shard, const std::vector<int
       h->batches[static_cast<size_t>(bi)].push_back({slot, v});
     }
   });
-  if (h) {
-    std::lock_guard<std::mutex> lk(g_handoff_mu);
-    g_handoff = std::move(h);
-  }
   std::vector<double> mm(static_cast<size_t>(sp.n_slots) * 2);
   auto dmm = engine::device_alloc(mm.size() * 8 + 16);
   kern::minmax_decode(k64, static_cast<double*>(dmm.get()), sp.n_slots, S());
@@ -337,31 +298,20 @@ void collect_extrema(const Graph& g, const Dataset& shard, const std::vector<int
     mins->push_back(mm[2 * static_cast<size_t>(s)]);
     maxs->push_back(mm[2 * static_cast<size_t>(s) + 1]);
   }
+  return h;
 }
 
-void collect_histograms(const Graph& g, const Dataset& shard, const std::vector<int>& edges,
-                        const std::vector<double>& absmax, int bins,
-                        std::vector<int64_t>* counts) {
-  if (shard.empty()) throw CalibrationError("calibration dataset is empty");
-  if (bins < 2) throw CalibrationError("histogram needs at least 2 bins");
-  if (absmax.size() != edges.size()) throw std::invalid_argument("absmax per edge required");
-  std::unique_ptr<Handoff> h;
-  {
-    std::lock_guard<std::mutex> lk(g_handoff_mu);
-    if (g_handoff && g_handoff->graph_uid == g.uid() && g_handoff->shard == &shard &&
-        g_handoff->shard_size == shard.size() && g_handoff->first_sample == first_sample_ptr(shard) &&
-        g_handoff->edges == edges) {
-      h = std::move(g_handoff);
-    }
-    g_handoff.reset();
-  }
-  std::unique_ptr<ShardPasses> spp;
-  if (!h) spp = std::make_unique<ShardPasses>(g, shard, edges);
-  const int n_slots = h ? h->n_slots : spp->n_slots;
-  const std::vector<int> edge_slot = h ? h->edge_slot : spp->edge_slot;
+// Pass 2 over one shard: histograms against the given (global) absmax per
+// edge (calibration.cpp:93-113).  From the pass-1 cache when there is one,
+// else by a fresh forward of `sp`.  Constant edges are counted once and
+// scaled by the shard's sample count N.
+void pass_histograms(ShardPasses* sp, PassCache* cache, const std::vector<int>& edges,
+                     const std::vector<double>& absmax, int bins, int64_t N,
+                     std::vector<int64_t>* counts) {
+  const int n_slots = cache ? cache->n_slots : sp->n_slots;
+  const std::vector<int>& edge_slot = cache ? cache->edge_slot : sp->edge_slot;
   std::vector<double> slot_absmax(static_cast<size_t>(n_slots), 0.0);
   for (size_t t = 0; t < edges.size(); ++t) slot_absmax[static_cast<size_t>(edge_slot[t])] = absmax[t];
-  const int64_t N = static_cast<int64_t>(shard.size());
   auto dc = engine::device_alloc(static_cast<size_t>(n_slots) * bins * 8 + 16);
   ok(cudaMemsetAsync(dc.get(), 0, static_cast<size_t>(n_slots) * bins * 8, S()));
   auto* c64 = static_cast<unsigned long long*>(dc.get());
@@ -375,22 +325,135 @@ void collect_histograms(const Graph& g, const Dataset& shard, const std::vector<
                                  static_cast<unsigned long long>(N), S());
     }
   };
-  if (h) {
-    for (size_t bi = 0; bi < h->batches.size(); ++bi) {
-      for (auto& [slot, v] : h->batches[bi]) hist(slot, v, h->batch_size[bi], static_cast<int64_t>(bi));
+  if (cache) {
+    for (size_t bi = 0; bi < cache->batches.size(); ++bi) {
+      for (auto& [slot, v] : cache->batches[bi]) {
+        hist(slot, v, cache->batch_size[bi], static_cast<int64_t>(bi));
+      }
     }
   } else {
-    spp->forward(hist);
+    sp->forward(hist);
   }
   std::vector<int64_t> hc(static_cast<size_t>(n_slots) * bins);
   ok(cudaMemcpyAsync(hc.data(), dc.get(), hc.size() * 8, cudaMemcpyDeviceToHost, S()));
   device::synchronize();
-  h.reset();
   counts->clear();
   for (int s : edge_slot) {
     counts->insert(counts->end(), hc.begin() + static_cast<int64_t>(s) * bins,
                    hc.begin() + static_cast<int64_t>(s + 1) * bins);
   }
+}
+
+// Pass-1 -> pass-2 handoff between the two sharded C-ABI calls
+// (qc_collect_extrema / qc_collect_histograms, between which the caller
+// all-reduces the extrema).  Keyed on the graph's uid and a caller-supplied
+// shard key (the C-ABI dataset handle's uid): never on addresses, which the
+// allocator can reuse.  Key 0 disables the handoff (pass 2 recomputes).
+struct Handoff {
+  uint64_t graph_uid = 0;
+  uint64_t shard_key = 0;
+  std::vector<int> edges;
+  std::unique_ptr<PassCache> cache;
+};
+std::mutex g_handoff_mu;
+std::unique_ptr<Handoff> g_handoff;
+
+}  // namespace
+
+void collect_extrema(const Graph& g, const Dataset& shard, const std::vector<int>& edges,
+                     std::vector<double>* mins, std::vector<double>* maxs, uint64_t shard_key) {
+  if (shard.empty()) throw CalibrationError("calibration dataset is empty");
+  ShardPasses sp(g, shard, edges);
+  {
+    std::lock_guard<std::mutex> lk(g_handoff_mu);
+    g_handoff.reset();  // a new pass 1 supersedes any unconsumed handoff
+  }
+  auto cache = pass_extrema(sp, shard_key != 0, mins, maxs);
+  if (cache) {
+    auto h = std::make_unique<Handoff>();
+    h->graph_uid = g.uid();
+    h->shard_key = shard_key;
+    h->edges = edges;
+    h->cache = std::move(cache);
+    std::lock_guard<std::mutex> lk(g_handoff_mu);
+    g_handoff = std::move(h);
+  }
+}
+
+void collect_histograms(const Graph& g, const Dataset& shard, const std::vector<int>& edges,
+                        const std::vector<double>& absmax, int bins,
+                        std::vector<int64_t>* counts, uint64_t shard_key) {
+  if (shard.empty()) throw CalibrationError("calibration dataset is empty");
+  if (bins < 2) throw CalibrationError("histogram needs at least 2 bins");
+  if (absmax.size() != edges.size()) throw std::invalid_argument("absmax per edge required");
+  std::unique_ptr<Handoff> h;
+  {
+    std::lock_guard<std::mutex> lk(g_handoff_mu);
+    if (shard_key != 0 && g_handoff && g_handoff->graph_uid == g.uid() &&
+        g_handoff->shard_key == shard_key && g_handoff->edges == edges) {
+      h = std::move(g_handoff);
+    }
+    g_handoff.reset();
+  }
+  std::unique_ptr<ShardPasses> sp;
+  if (!h) sp = std::make_unique<ShardPasses>(g, shard, edges);
+  pass_histograms(sp.get(), h ? h->cache.get() : nullptr, edges, absmax, bins,
+                  static_cast<int64_t>(shard.size()), counts);
+}
+
+// Distributed collect_stats (quantc/distributed.hpp): pass 1 on this rank's
+// shard -> all-reduce MIN / MAX -> absmax -> pass 2 against the global absmax
+// -> all-reduce SUM.  Every merge is exact, so the result equals
+// collect_stats over the concatenated shards.  An empty shard contributes the
+// identities (+inf / -inf, zero counts).
+CalibrationStats collect_stats(const Graph& g, const Dataset& shard, Communicator& comm, int bins,
+                               const std::vector<int>& edge_indices) {
+  if (bins < 2) throw CalibrationError("histogram needs at least 2 bins");
+  const size_t n_edges = edge_order(g).size();
+  std::vector<int> targets = edge_indices;
+  if (targets.empty()) {
+    for (size_t k = 0; k < n_edges; ++k) targets.push_back(static_cast<int>(k));
+  }
+  for (int k : targets) {
+    if (k < 0 || k >= static_cast<int>(n_edges)) {
+      throw CalibrationError("edge index " + std::to_string(k) + " out of range");
+    }
+  }
+  int64_t n_total = static_cast<int64_t>(shard.size());
+  comm.allreduce_sum(&n_total, 1);
+  if (n_total == 0) throw CalibrationError("calibration dataset is empty");
+  const size_t T = targets.size();
+  std::vector<double> lo(T, std::numeric_limits<double>::infinity());
+  std::vector<double> hi(T, -std::numeric_limits<double>::infinity());
+  std::unique_ptr<ShardPasses> sp;
+  std::unique_ptr<PassCache> cache;
+  if (!shard.empty()) {
+    sp = std::make_unique<ShardPasses>(g, shard, targets);
+    cache = pass_extrema(*sp, true, &lo, &hi);
+  }
+  comm.allreduce_min(lo.data(), T);
+  comm.allreduce_max(hi.data(), T);
+  std::vector<double> absmax(T);
+  for (size_t t = 0; t < T; ++t) absmax[t] = std::max(std::fabs(lo[t]), std::fabs(hi[t]));
+  std::vector<int64_t> counts(T * static_cast<size_t>(bins), 0);
+  if (!shard.empty()) {
+    pass_histograms(sp.get(), cache.get(), targets, absmax, bins,
+                    static_cast<int64_t>(shard.size()), &counts);
+  }
+  cache.reset();
+  comm.allreduce_sum(counts.data(), counts.size());
+  CalibrationStats stats;
+  for (size_t t = 0; t < T; ++t) {
+    EdgeStats e;
+    e.min = lo[t];
+    e.max = hi[t];
+    e.absmax = absmax[t];
+    e.sample_count = n_total;
+    e.counts.assign(counts.begin() + static_cast<int64_t>(t) * bins,
+                    counts.begin() + static_cast<int64_t>(t + 1) * bins);
+    stats.per_edge[targets[t]] = std::move(e);
+  }
+  return stats;
 }
 
 double threshold_max(const EdgeStats& stats) {

@@ -9,6 +9,7 @@
 // point in include/quantc_capi.h.
 #include "quantc_capi.h"
 
+#include <atomic>
 #include <cstdlib>
 #include <functional>
 #include <map>
@@ -31,6 +32,7 @@
 #include "quantc/topology.hpp"
 #ifdef QUANTC_B200
 #include "quantc/device.hpp"
+#include "quantc/distributed.hpp"
 #include "quantc/serialize.hpp"
 #include "quantc_files.h"
 #include "quantc_cuda.h"
@@ -49,10 +51,22 @@ struct qc_topology {
 };
 struct qc_dataset {
   std::shared_ptr<Dataset> d;
+  // identity of this handle for the pass-1 -> pass-2 handoff (never reused,
+  // unlike addresses)
+  uint64_t uid = next_dataset_uid();
+  static uint64_t next_dataset_uid() {
+    static std::atomic<uint64_t> n{0};
+    return ++n;
+  }
 };
 struct qc_stats {
   CalibrationStats s;
 };
+#ifdef QUANTC_B200
+struct qc_comm {
+  std::unique_ptr<Communicator> c;
+};
+#endif
 struct qc_evaluator {
   // CandidateEvaluator borrows graph/spec/dataset (reference search.hpp:130-132);
   // the handle keeps them alive.
@@ -831,6 +845,38 @@ int qc_evaluator_strategy(const qc_evaluator* e, const int* cand, size_t n_slots
 }
 
 #ifdef QUANTC_B200
+int qc_requantize_params(double s_in, double s_out, int32_t* multiplier, int* shift) {
+  return run([&] {
+    const RequantParams r = requantize_params(s_in, s_out);
+    *multiplier = r.multiplier;
+    *shift = r.shift;
+  });
+}
+
+int qc_choose_storage_dtype(int bit, const char* candidates_csv, int sign, char* out,
+                            size_t cap) {
+  return run([&] {
+    std::vector<DType> cands;
+    std::string all(candidates_csv), tok;
+    std::stringstream ss(all);
+    while (std::getline(ss, tok, ',')) {
+      if (!tok.empty()) cands.push_back(parse_dtype(tok));
+    }
+    const std::string name = choose_storage_dtype(bit, cands, sign).name();
+    if (name.size() + 1 > cap) throw BufferTooSmall();
+    std::memcpy(out, name.c_str(), name.size() + 1);
+  });
+}
+
+int qc_rewrite_clip(double min_f, double max_f, double s_out, int64_t zero_point,
+                    const char* storage, int64_t* q_min, int64_t* q_max) {
+  return run([&] {
+    const auto [lo, hi] = rewrite_clip(min_f, max_f, s_out, zero_point, parse_dtype(storage));
+    *q_min = lo;
+    *q_max = hi;
+  });
+}
+
 int qc_realize(const qc_graph* sim_g, const char* strategy_json, const qc_spec* spec,
                qc_graph** out) {
   return run([&] {
@@ -855,7 +901,7 @@ int qc_collect_extrema(const qc_graph* g, const qc_dataset* d, const int* edges,
                        double* mins, double* maxs) {
   return run([&] {
     std::vector<double> lo, hi;
-    collect_extrema(*g->g, *d->d, std::vector<int>(edges, edges + n), &lo, &hi);
+    collect_extrema(*g->g, *d->d, std::vector<int>(edges, edges + n), &lo, &hi, d->uid);
     std::copy(lo.begin(), lo.end(), mins);
     std::copy(hi.begin(), hi.end(), maxs);
   });
@@ -866,7 +912,7 @@ int qc_collect_histograms(const qc_graph* g, const qc_dataset* d, const int* edg
   return run([&] {
     std::vector<int64_t> c;
     collect_histograms(*g->g, *d->d, std::vector<int>(edges, edges + n),
-                       std::vector<double>(absmax, absmax + n), bins, &c);
+                       std::vector<double>(absmax, absmax + n), bins, &c, d->uid);
     std::copy(c.begin(), c.end(), counts);
   });
 }
@@ -877,6 +923,131 @@ int qc_predict_scores(const qc_graph* g, const qc_dataset* d, const int64_t* bin
   return run([&] {
     SimBinding b = make_binding(bind_nodes, bind_params, n_bind);
     emit(predict_scores(*g->g, *d->d, n_bind ? &b : nullptr, per_sample), out, cap, n_out);
+  });
+}
+
+int qc_evaluator_scores(const qc_evaluator* e, const int* cands, size_t n_cands, size_t n_slots,
+                        int group, float* out, size_t cap, size_t* n_out, int64_t* per_sample) {
+  return run([&] {
+    std::vector<Candidate> cs;
+    for (size_t i = 0; i < n_cands; ++i) {
+      cs.emplace_back(cands + i * n_slots, cands + (i + 1) * n_slots);
+    }
+    emit(e->ev->scores(std::span<const Candidate>(cs.data(), cs.size()), group, per_sample), out,
+         cap, n_out);
+  });
+}
+
+int qc_comm_local(qc_comm** out) {
+  return run([&] { *out = new qc_comm{make_local_communicator()}; });
+}
+
+int qc_comm_nccl_unique_id(char id[128]) {
+  return run([&] {
+    const NcclId u = nccl_unique_id();
+    std::memcpy(id, u.data(), u.size());
+  });
+}
+
+int qc_comm_nccl(int rank, int world, const char id[128], qc_comm** out) {
+  return run([&] {
+    NcclId u;
+    std::memcpy(u.data(), id, u.size());
+    *out = new qc_comm{make_nccl_communicator(rank, world, u)};
+  });
+}
+
+int qc_comm_callbacks(int rank, int world, qc_comm_sum_i64_fn sum_i64, qc_comm_f64_fn minmax_f64,
+                      qc_comm_gather_f64_fn gather_f64, void* user, qc_comm** out) {
+  return run([&] {
+    CommHooks h;
+    h.rank = rank;
+    h.size = world;
+    h.user = user;
+    h.allreduce_sum_i64 = sum_i64;
+    h.allreduce_f64 = minmax_f64;
+    h.allgather_f64 = gather_f64;
+    *out = new qc_comm{make_callback_communicator(h)};
+  });
+}
+
+void qc_comm_free(qc_comm* c) { delete c; }
+
+int qc_collect_stats_dist(const qc_graph* g, const qc_dataset* d, qc_comm* comm, int bins,
+                          const int* edges, size_t n_edges, qc_stats** out) {
+  return run([&] {
+    auto h = std::make_unique<qc_stats>();
+    h->s = collect_stats(*g->g, *d->d, *comm->c, bins,
+                         std::vector<int>(edges, edges + n_edges));
+    *out = h.release();
+  });
+}
+
+int qc_search_batched(int method, const int* edges, const int* lo, const int* hi, size_t n_slots,
+                      qc_batch_loss_fn fn, void* user, const qc_evaluator* ev, qc_comm* comm,
+                      int loss_mode, const qc_search_params* p, int width, int* best,
+                      double* best_loss, int64_t* evaluations, char** trace_json,
+                      int64_t* spec_stats) {
+  return run([&] {
+    SearchSpace space;
+    for (size_t i = 0; i < n_slots; ++i) space.ranges.push_back(BitRange{edges[i], lo[i], hi[i]});
+    BatchLossFn losses;
+    if (fn) {
+      losses = [fn, user, n_slots](std::span<const Candidate> cs) {
+        std::vector<int> flat;
+        flat.reserve(cs.size() * n_slots);
+        for (const Candidate& c : cs) flat.insert(flat.end(), c.begin(), c.end());
+        std::vector<double> v(cs.size());
+        if (fn(flat.data(), cs.size(), n_slots, user, v.data()) != 0) {
+          throw SearchError("loss callback failed");
+        }
+        return v;
+      };
+      if (loss_mode == QC_LOSS_CANDIDATES) {
+        if (!comm) throw std::invalid_argument("sharded losses need a communicator");
+        losses = shard_candidates(std::move(losses), *comm->c);
+      } else if (loss_mode != QC_LOSS_LOCAL) {
+        throw std::invalid_argument("a batch callback supports local or candidate sharding");
+      }
+    } else if (ev) {
+      const CandidateEvaluator& E = *ev->ev;
+      if (loss_mode == QC_LOSS_SAMPLES || loss_mode == QC_LOSS_CANDIDATES) {
+        if (!comm) throw std::invalid_argument("sharded losses need a communicator");
+        losses = loss_mode == QC_LOSS_SAMPLES ? sample_sharded_losses(E, *comm->c)
+                                              : candidate_sharded_losses(E, *comm->c);
+      } else {
+        losses = E.batch_loss();
+      }
+    } else {
+      throw std::invalid_argument("qc_search_batched needs a loss callback or an evaluator");
+    }
+    SpeculationStats st;
+    SearchResult r;
+    switch (method) {
+      case QC_SEARCH_GREEDY:
+        r = greedy_search_batched(space, losses, p->rounds, p->tol, width, &st);
+        break;
+      case QC_SEARCH_ANNEAL:
+        r = anneal_search_batched(space, losses, p->steps, p->t0, p->decay, p->seed, width, &st);
+        break;
+      case QC_SEARCH_RANDOM:
+        r = random_search_batched(space, losses, p->n, p->seed, width, &st);
+        break;
+      case QC_SEARCH_EXHAUSTIVE:
+        r = exhaustive_search_batched(space, losses, p->cap, width, &st);
+        break;
+      default:
+        throw std::invalid_argument("unknown search method");
+    }
+    for (size_t i = 0; i < r.best.size(); ++i) best[i] = r.best[i];
+    *best_loss = r.best_loss;
+    *evaluations = r.evaluations;
+    if (trace_json) *trace_json = dup_string(trace_to_json(r));
+    if (spec_stats) {
+      spec_stats[0] = st.batches;
+      spec_stats[1] = st.evaluated;
+      spec_stats[2] = st.committed;
+    }
   });
 }
 

@@ -309,7 +309,8 @@ std::shared_ptr<void> predict_streamed(const engine::Plan& plan, const Graph& g,
 }
 
 std::shared_ptr<void> predict_device_group(const engine::Plan& plan, const DeviceDataset& dd,
-                                           const std::vector<const SimBinding*>& bindings) {
+                                           const std::vector<const SimBinding*>& bindings,
+                                           std::shared_ptr<void>* scores, int64_t* per_sample) {
   const int G = static_cast<int>(bindings.size());
   if (G < 2 || device::profile_enabled()) return nullptr;
   for (const SimBinding* b : bindings) {
@@ -318,6 +319,11 @@ std::shared_ptr<void> predict_device_group(const engine::Plan& plan, const Devic
   const int64_t n = dd.size();
   auto preds = engine::device_alloc(static_cast<size_t>(std::max<int64_t>(1, G * n)) * 8);
   auto* p = static_cast<int64_t*>(preds.get());
+  const int64_t per = plan.fused->out_per_sample();
+  if (scores) {
+    *scores = engine::device_alloc(static_cast<size_t>(std::max<int64_t>(1, G * n * per)) * 4);
+    *per_sample = per;
+  }
   const int fb = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, n), 256));
   for (int64_t first = 0; first < n; first += fb) {
     const int b = static_cast<int>(std::min<int64_t>(fb, n - first));
@@ -325,7 +331,13 @@ std::shared_ptr<void> predict_device_group(const engine::Plan& plan, const Devic
     for (size_t k = 0; k < dd.num_inputs(); ++k) ins.push_back(dd.input(k, first));
     std::vector<int64_t*> outs;
     for (int g = 0; g < G; ++g) outs.push_back(p + g * n + first);
-    plan.fused->predict_group(b, ins, bindings, outs);
+    std::vector<float*> souts;
+    if (scores) {
+      for (int g = 0; g < G; ++g) {
+        souts.push_back(static_cast<float*>(scores->get()) + (g * n + first) * per);
+      }
+    }
+    plan.fused->predict_group(b, ins, bindings, outs, scores ? &souts : nullptr);
   }
   return preds;
 }

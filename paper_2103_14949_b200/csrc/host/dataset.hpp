@@ -54,7 +54,10 @@ std::shared_ptr<void> predict_device(const engine::Plan& plan, const DeviceDatas
 // every compatible GEMM stage runs as one grouped tcgen05 launch.  Returns
 // [G x N] predictions (binding g's rows at g*N), or nullptr when the grouped
 // path does not apply.
+// scores (optional): also returns the output rows, [G x N x per_sample] fp32.
 std::shared_ptr<void> predict_device_group(const engine::Plan& plan, const DeviceDataset& dd,
-                                           const std::vector<const SimBinding*>& bindings);
+                                           const std::vector<const SimBinding*>& bindings,
+                                           std::shared_ptr<void>* scores = nullptr,
+                                           int64_t* per_sample = nullptr);
 
 }  // namespace quantc::gpu

@@ -1580,7 +1580,8 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
 // outputs, so results equal separate predict() calls.
 void FastPlan::predict_group(int batch, const std::vector<const float*>& inputs,
                              const std::vector<const SimBinding*>& bindings,
-                             const std::vector<int64_t*>& preds) {
+                             const std::vector<int64_t*>& preds,
+                             const std::vector<float*>* scores) {
   const int G = static_cast<int>(bindings.size());
   if (G < 1 || G > kern::kMaxGroups) throw std::logic_error("predict_group: 1..kMaxGroups bindings");
   if (wcache_.size() > 4 * stages_.size() * static_cast<size_t>(G)) wcache_.clear();
@@ -1657,6 +1658,13 @@ void FastPlan::predict_group(int batch, const std::vector<const float*>& inputs,
   std::vector<const float*> outs(static_cast<size_t>(G));
   for (int g = 0; g < G; ++g) outs[g] = static_cast<const float*>(buf(r[g], out_val_));
   kern::argmax_rows_multi(outs.data(), preds.data(), G, batch, out_per_sample_, ST());
+  if (scores) {
+    for (int g = 0; g < G; ++g) {
+      if (!(*scores)[g]) continue;
+      ok_cuda(cudaMemcpyAsync((*scores)[g], outs[g], static_cast<size_t>(batch) * out_per_sample_ * 4,
+                              cudaMemcpyDeviceToDevice, ST()));
+    }
+  }
   device::counters().fused_batches += G;
 }
 

@@ -41,7 +41,8 @@ class FastPlan {
   // run as one grouped tcgen05 launch (fastplan.cpp)
   void predict_group(int batch, const std::vector<const float*>& inputs,
                      const std::vector<const SimBinding*>& bindings,
-                     const std::vector<int64_t*>& preds);
+                     const std::vector<int64_t*>& preds,
+                     const std::vector<float*>* scores = nullptr);
   int64_t out_per_sample() const { return out_per_sample_; }
   // stream this instance enqueues on (nullptr: the engine stream); every
   // buffer, table upload and launch of the instance is ordered on it

@@ -110,6 +110,12 @@ class SearchParams(C.Structure):
 
 LOSS_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_int), C.c_size_t, C.c_void_p,
                       C.POINTER(C.c_double))
+BATCH_LOSS_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_int), C.c_size_t, C.c_size_t, C.c_void_p,
+                            C.POINTER(C.c_double))
+COMM_SUM_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_int64), C.c_size_t, C.c_void_p)
+COMM_F64_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_size_t, C.c_int, C.c_void_p)
+COMM_GATHER_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_size_t,
+                             C.POINTER(C.c_double), C.c_void_p)
 
 _P = C.c_void_p
 _SZ = C.c_size_t
@@ -471,6 +477,29 @@ class Quantc:
         self.check(fn(sim_g.h, doc, spec.h, C.byref(h)))
         return Graph(self, h)
 
+    def requantize_params(self, s_in: float, s_out: float):
+        m, sh = C.c_int32(), C.c_int()
+        fn = self._bind("qc_requantize_params", C.c_int,
+                        [C.c_double, C.c_double, C.POINTER(C.c_int32), C.POINTER(C.c_int)])
+        self.check(fn(s_in, s_out, C.byref(m), C.byref(sh)))
+        return m.value, sh.value
+
+    def choose_storage_dtype(self, bit: int, candidates: Sequence[str], sign: int = 1) -> str:
+        buf = C.create_string_buffer(32)
+        fn = self._bind("qc_choose_storage_dtype", C.c_int,
+                        [C.c_int, C.c_char_p, C.c_int, C.c_char_p, C.c_size_t])
+        self.check(fn(bit, ",".join(candidates).encode(), sign, buf, 32))
+        return buf.value.decode()
+
+    def rewrite_clip(self, min_f, max_f, s_out, zero_point, storage="int8"):
+        lo, hi = C.c_int64(), C.c_int64()
+        fn = self._bind("qc_rewrite_clip", C.c_int,
+                        [C.c_double, C.c_double, C.c_double, C.c_int64, C.c_char_p,
+                         C.POINTER(C.c_int64), C.POINTER(C.c_int64)])
+        self.check(fn(min_f, max_f, s_out, zero_point, storage.encode(), C.byref(lo),
+                      C.byref(hi)))
+        return lo.value, hi.value
+
     # -- search (search.hpp) --------------------------------------------
     def evaluator(self, sim_g, spec, topo, thresholds: Dict[int, float], stats, calib,
                   min_bit=4, workers=0) -> "CandidateEvaluator":
@@ -517,6 +546,138 @@ class Quantc:
         self.check(rc)
         trace = json.loads(self._take_string(tr))
         return SearchResult(best[:n].tolist(), bl.value, ne.value, trace)
+
+    def search_batched(self, method: str, space: "SearchSpace",
+                       losses: Optional[Callable[[List[List[int]]], Sequence[float]]] = None,
+                       evaluator: Optional["CandidateEvaluator"] = None,
+                       comm: Optional["Comm"] = None, mode: str = "local", width: int = 4,
+                       **kw) -> "SearchResult":
+        """search.hpp *_batched (B200 extension): the speculative batched
+        searches.  Results and traces equal search(); `losses` is a batch
+        callable, else the evaluator is used with mode "local", "samples"
+        (counts all-reduced over comm) or "candidates" (batches split over
+        comm's ranks).  Returns a SearchResult with .speculation =
+        (batches, evaluated, committed)."""
+        code = {"greedy": 0, "anneal": 1, "random": 2, "exhaustive": 3}[method]
+        lmode = {"local": 0, "samples": 1, "candidates": 2}[mode]
+        p = SearchParams(kw.get("rounds", 1), kw.get("tol", 0.0), kw.get("steps", 1),
+                         kw.get("t0", 0.1), kw.get("decay", 0.995), kw.get("seed", 0),
+                         kw.get("n", 1), kw.get("cap", 100000))
+        e, ep = _arr(space.edges or [0], C.c_int)
+        lo, lop = _arr(space.lo or [0], C.c_int)
+        hi, hip = _arr(space.hi or [0], C.c_int)
+        n = len(space.edges)
+        errors: List[BaseException] = []
+
+        def _cb(cands, nc, ns, user, out):
+            try:
+                a = np.ctypeslib.as_array(cands, shape=(nc * ns,)).reshape(nc, ns) if nc * ns \
+                    else np.zeros((nc, ns), np.int32)
+                v = [float(x) for x in losses(a.tolist())]
+                if len(v) != nc:
+                    raise ValueError("batch loss returned the wrong count")
+                for i, x in enumerate(v):
+                    out[i] = x
+                return 0
+            except BaseException as ex:  # surfaced after the call
+                errors.append(ex)
+                return 1
+
+        fn = self._bind("qc_search_batched", C.c_int,
+                        [C.c_int, _PI, _PI, _PI, _SZ, BATCH_LOSS_FN, _P, _P, _P, C.c_int,
+                         C.POINTER(SearchParams), C.c_int, _PI, _PD, _PI64, _PSTR, _PI64])
+        cb = BATCH_LOSS_FN(_cb) if losses is not None else BATCH_LOSS_FN()
+        best = np.zeros(max(n, 1), np.int32)
+        bl = C.c_double()
+        ne = C.c_int64()
+        tr = C.c_void_p()
+        st = np.zeros(3, np.int64)
+        rc = fn(code, ep, lop, hip, n, cb, None,
+                evaluator.h if evaluator is not None else None,
+                comm.h if comm is not None else None, lmode, C.byref(p), width,
+                best.ctypes.data_as(_PI), C.byref(bl), C.byref(ne), C.byref(tr),
+                st.ctypes.data_as(_PI64))
+        if errors:
+            raise errors[0]
+        self.check(rc)
+        trace = json.loads(self._take_string(tr))
+        r = SearchResult(best[:n].tolist(), bl.value, ne.value, trace)
+        r.speculation = tuple(int(x) for x in st)
+        return r
+
+    # -- communicators (comm.hpp; B200 extension) -------------------------
+    def comm_local(self) -> "Comm":
+        h = C.c_void_p()
+        self.check(self._bind("qc_comm_local", C.c_int, [C.POINTER(_P)])(C.byref(h)))
+        return Comm(self, h)
+
+    def nccl_unique_id(self) -> bytes:
+        buf = C.create_string_buffer(128)
+        self.check(self._bind("qc_comm_nccl_unique_id", C.c_int, [C.c_char_p])(buf))
+        return buf.raw
+
+    def comm_nccl(self, rank: int, world: int, uid: bytes) -> "Comm":
+        h = C.c_void_p()
+        fn = self._bind("qc_comm_nccl", C.c_int, [C.c_int, C.c_int, C.c_char_p, C.POINTER(_P)])
+        self.check(fn(rank, world, C.create_string_buffer(uid, 128), C.byref(h)))
+        return Comm(self, h)
+
+    def comm_torch(self, group=None) -> "Comm":
+        """A communicator whose collectives are torch.distributed calls on
+        `group` (any backend; gloo in the CPU tests)."""
+        import torch
+        import torch.distributed as dist
+        dev = (torch.device("cuda", torch.cuda.current_device())
+               if dist.get_backend(group) == "nccl" else torch.device("cpu"))
+        world = dist.get_world_size(group)
+
+        def sum_i64(data, n, user):
+            try:
+                t = torch.from_numpy(np.ctypeslib.as_array(data, shape=(n,)).copy()).to(dev)
+                dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+                np.ctypeslib.as_array(data, shape=(n,))[:] = t.cpu().numpy()
+                return 0
+            except BaseException:
+                return 1
+
+        def minmax(data, n, op, user):
+            try:
+                t = torch.from_numpy(np.ctypeslib.as_array(data, shape=(n,)).copy()).to(dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MIN if op == 0 else dist.ReduceOp.MAX,
+                                group=group)
+                np.ctypeslib.as_array(data, shape=(n,))[:] = t.cpu().numpy()
+                return 0
+            except BaseException:
+                return 1
+
+        def gather(send, n, recv, user):
+            try:
+                t = torch.from_numpy(np.ctypeslib.as_array(send, shape=(n,)).copy()).to(dev)
+                outs = [torch.empty_like(t) for _ in range(world)]
+                dist.all_gather(outs, t, group=group)
+                np.ctypeslib.as_array(recv, shape=(n * world,))[:] = \
+                    torch.cat(outs).cpu().numpy()
+                return 0
+            except BaseException:
+                return 1
+
+        cbs = (COMM_SUM_FN(sum_i64), COMM_F64_FN(minmax), COMM_GATHER_FN(gather))
+        fn = self._bind("qc_comm_callbacks", C.c_int,
+                        [C.c_int, C.c_int, COMM_SUM_FN, COMM_F64_FN, COMM_GATHER_FN, _P,
+                         C.POINTER(_P)])
+        h = C.c_void_p()
+        self.check(fn(dist.get_rank(group), world, *cbs, None, C.byref(h)))
+        return Comm(self, h, keep=cbs)
+
+    def collect_stats_dist(self, g: "Graph", shard: "Dataset", comm: "Comm", bins=2048,
+                           edges=()) -> "CalibrationStats":
+        """distributed.hpp collect_stats: this rank's shard, merged over comm."""
+        e, ep = _arr(list(edges) or [0], C.c_int)
+        h = C.c_void_p()
+        fn = self._bind("qc_collect_stats_dist", C.c_int,
+                        [_P, _P, _P, C.c_int, _PI, _SZ, C.POINTER(_P)])
+        self.check(fn(g.h, shard.h, comm.h, bins, ep, len(edges), C.byref(h)))
+        return CalibrationStats(self, h)
 
     def space_size(self, space: "SearchSpace") -> int:
         lo, lop = _arr(space.lo or [0], C.c_int)
@@ -718,6 +879,16 @@ class SearchResult:
     trace: dict
 
 
+class Comm(_Handle):
+    """A quantc::Communicator (comm.hpp)."""
+    _free = "qc_comm_free"
+
+    def __init__(self, q, h, keep=()):
+        q._bind("qc_comm_free", None, [_P])
+        super().__init__(q, h)
+        self._keep = keep
+
+
 class CandidateEvaluator(_Handle):
     _free = "qc_evaluator_free"
 
@@ -760,6 +931,27 @@ class CandidateEvaluator(_Handle):
         self.q.check(self.q.lib.qc_evaluator_losses(self.h, a.ctypes.data_as(_PI), a.shape[0],
                                                     a.shape[1], out.ctypes.data_as(_PD)))
         return out
+
+    def scores(self, cands, group: int = 0) -> np.ndarray:
+        """fp32 output rows of each candidate's forward over the calibration
+        set, [n_cands, N, per_sample] (B200 extension), `group` candidates per
+        grouped launch (0: the default)."""
+        a = np.ascontiguousarray(np.asarray(cands, dtype=np.int32))
+        fn = self.q._bind("qc_evaluator_scores", C.c_int,
+                          [_P, _PI, _SZ, _SZ, C.c_int, _PF, _SZ, _PSZ, _PI64])
+        n = len(self.reference_predictions())
+        cap = 1 << 16
+        while True:
+            out = np.zeros(cap, np.float32)
+            k = C.c_size_t()
+            per = C.c_int64()
+            rc = fn(self.h, a.ctypes.data_as(_PI), a.shape[0], a.shape[1], group,
+                    out.ctypes.data_as(_PF), cap, C.byref(k), C.byref(per))
+            if rc == 10 and k.value > cap:
+                cap = k.value
+                continue
+            self.q.check(rc)
+            return out[:k.value].reshape(a.shape[0], n, per.value)
 
     def strategy_for(self, cand) -> dict:
         c, cp = _arr(cand, C.c_int)

@@ -13,6 +13,11 @@ from paper_2103_14949_b200 import quantc as Q
 pytestmark = pytest.mark.gpu
 
 RQ = (1 << 30, 41, 7, -3)  # multiplier 2^30, shift 41, in_zp 7, out_zp -3
+# general (non power-of-two) fixed-point multipliers, as requantize_params
+# produces them for arbitrary scale ratios (SPEC.md realize module)
+RQG = (1518500250, 41, 7, -3)        # ~ sqrt(1/2) * 2^31
+RQG2 = (1900000001, 42, -5, 4)
+RQG_MAX = (2147483647, 44, 1, -1)    # the largest multiplier
 
 # case -> (probe config, backend that must run it: tc = tcgen05 kernel,
 # simt = CUDA-core backend, generic = the int64 reference-order kernel)
@@ -34,6 +39,13 @@ CASES = {
     "relu_acc": (dict(relu_zp=0), "tc"),
     "simt_rq_relu": (dict(acc="int16", requant=RQ, relu_zp=1), "simt"),
     "w_zp1_out_of_int8": (dict(zp1=-10, wlo=-128, whi=127), "generic"),
+    # general multipliers: fused epilogue (tcgen05 / CUDA cores) and chains
+    "3x3_rqg": (dict(requant=RQG), "tc"),
+    "3x3_zp_rqg2": (dict(zp0=-4, zp1=1, requant=RQG2), "tc"),
+    "dense_rqg_max": (dict(dense=True, c=300, o=70, n=5, requant=RQG_MAX), "tc"),
+    "rqg_relu_rqg": (dict(requant=RQG, relu_zp=2, requant2=(1610612737, 32, 2, 5)), "tc"),
+    "simt_rqg": (dict(acc="int16", requant=(1234567891, 39, 0, 0)), "simt"),
+    "i16_rqg": (dict(dtype="int16", requant=(1300000007, 52, 0, 1)), "simt"),
     # int16-accumulator backend ((i8, i8) -> i16) on CUDA cores
     "acc_int16_saturate": (dict(acc="int16", dtype="uint8", zp0=100), "simt"),
     "acc_int16_rq": (dict(acc="int16", zp0=-3, zp1=2, requant=RQ, c=40, o=70), "simt"),
@@ -115,6 +127,55 @@ def test_realized_model_eval_int_bit_exact(b200, ref, name, spec_name):
     model = F.small_cnn() if name == "small_cnn" else F.resnet(18, image=32, classes=10,
                                                                  width=8)
     R, data = _realized(ref, b200, model, spec_name, 3)
+    Rr = R.copy_to(ref)
+    for x in data:
+        yr, dtr = ref.eval_int(Rr, x)
+        yb, dtb = b200.eval_int(R, x)
+        assert dtb == dtr
+        np.testing.assert_array_equal(yb, yr)
+
+
+def test_standalone_requantize_general_multipliers(cuda_lib, port, b200):
+    """qcu_requantize (kernels/intops.cu) with multipliers from
+    requantize_params of random ratios vs the restatement of
+    fixed_point_rescale (reference interpreter.cpp:32-37, :464-482)."""
+    import torch
+    rng = np.random.default_rng(17)
+    x = rng.integers(-(1 << 31), (1 << 31) - 1, 1 << 16, dtype=np.int64).astype(np.int32)
+    x[:8] = [0, 1, -1, (1 << 31) - 1, -(1 << 31), 12345, -12345, 7]
+    for trial in range(24):
+        ratio = float(np.exp2(rng.uniform(-24, 2)))
+        mult, shift = b200.requantize_params(ratio, 1.0)
+        assert mult != 1 << 30 or ratio == 2.0 ** round(np.log2(ratio))
+        in_zp, out_zp = int(rng.integers(-20, 20)), int(rng.integers(-20, 20))
+        qmin, qmax = (-128, 127) if trial % 2 else (-32768, 32767)
+        y = cuda_lib.requantize(torch.from_numpy(x).cuda(), mult, shift, in_zp, out_zp, qmin,
+                                qmax).cpu().numpy()
+        np.testing.assert_array_equal(y, port.requantize(x, mult, shift, in_zp, out_zp, qmin,
+                                                         qmax))
+
+
+@pytest.mark.parametrize("name", ["small_cnn", "resnet18"])
+def test_realized_general_thresholds_eval_int_bit_exact(b200, ref, name):
+    """Realized graphs under NON-power-of-two thresholds (the reference's
+    default, calibration.hpp:71-76): realize() emits general fixed-point
+    multipliers, and the B200 eval_int equals the reference's eval_int."""
+    model = F.small_cnn() if name == "small_cnn" else F.resnet(18, image=32, classes=10,
+                                                                 width=8)
+    data = model.data(3)
+    g = ref.graph(model.doc, model.blob)
+    spec = ref.parse_spec(F.spec_fixture("int8_int32"))
+    topo = ref.generate_topology(g, spec)
+    sim = ref.insert_simulated_quantize(g, topo)
+    ds = ref.dataset(data)
+    st = ref.collect_stats(g, ds, 2048, ref.simulated_edge_indices(g, topo))
+    thr = st.estimate_thresholds("quantile", quantile=0.99, pow2=False)
+    ev = ref.evaluator(sim, spec, topo, thr, st, ds)
+    strat = ev.strategy_for(ev.space().all_hi())
+    R = b200.realize(sim.copy_to(b200), strat, b200.parse_spec(F.spec_fixture("int8_int32")))
+    mults = [nd["attrs"]["multiplier"] for nd in R.to_json()["nodes"]
+             if nd["op"] == "requantize"]
+    assert any(m != 1 << 30 for m in mults), "no general multiplier was emitted"
     Rr = R.copy_to(ref)
     for x in data:
         yr, dtr = ref.eval_int(Rr, x)
