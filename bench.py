@@ -130,31 +130,36 @@ def candidates(space, n, seed=0):
     return out
 
 
+def random_candidates(space, n, seed=1):
+    """Search-realistic candidates: every slot drawn independently (every
+    layer's weight codes change between candidates, unlike the probes)."""
+    rng = np.random.default_rng(seed)
+    return [[int(rng.integers(lo, hi + 1)) for lo, hi in zip(space.lo, space.hi)]
+            for _ in range(n)]
+
+
+def cpu_reference_preds(model, data, threads, binding):
+    """The reference CPU implementation (oracle/_ref, compiled from the
+    reference sources) on this host: predict_top1 of the sim-quant graph under
+    one candidate binding (the body of CandidateEvaluator::loss, reference
+    search.cpp:421-428) over `data` with `threads` workers.  Returns
+    (predictions, seconds)."""
+    ref = Q.load(REF_LIB)
+    g = ref.graph(model.doc, model.blob)
+    spec = ref.parse_spec(F.spec_fixture("int8_int32"))
+    sim = ref.insert_simulated_quantize(g, ref.generate_topology(g, spec))
+    ds = ref.dataset(data)
+    t0 = time.perf_counter()
+    preds = ref.predict_top1(sim, ds, threads, binding)
+    return preds, time.perf_counter() - t0
+
+
 def _ref_binding(ref, model, threads):
     """Reference-only setup: calibrate on one image, bind one candidate."""
     one = model.data(1, seed=11)
     g, spec, topo, sim, ds, st, thr = build_pipeline(ref, model, one)
     ev = ref.evaluator(sim, spec, topo, thr, st, ds, 4, threads)
     return sim, ev, ev.space()
-
-
-def cpu_reference_rate(model, sample, threads, binding):
-    """The reference CPU implementation (oracle/_ref, compiled from the
-    reference sources) timed on this host: predict_top1 of the sim-quant graph
-    under one candidate binding (the body of CandidateEvaluator::loss,
-    reference search.cpp:421-428) over `sample` images with `threads`
-    workers.  The binding is the bit-identical one computed by the B200
-    library (tests/test_gpu_parity.py) so no reference calibration pass is
-    needed to time this leg."""
-    ref = Q.load(REF_LIB)
-    g = ref.graph(model.doc, model.blob)
-    spec = ref.parse_spec(F.spec_fixture("int8_int32"))
-    sim = ref.insert_simulated_quantize(g, ref.generate_topology(g, spec))
-    ds = ref.dataset(model.data(sample, seed=11))
-    t0 = time.perf_counter()
-    ref.predict_top1(sim, ds, threads, binding)
-    dt = time.perf_counter() - t0
-    return sample / dt, dt
 
 
 def run_reference(args):
@@ -208,6 +213,79 @@ def run_reference(args):
     return 0
 
 
+def traffic_probe(args):
+    """Child of the traffic measurement: set up the bench pipeline, then run
+    ONE grouped losses call over 4 candidates (the timed step's unit) between
+    cudaProfilerStart/Stop, so ncu captures exactly that step's launches."""
+    import torch
+    from paper_2103_14949_b200 import cuda_ops
+    b = Q.load_b200()
+    cuda_ops.load()
+    model = F.resnet(50)
+    data = model.data(args.batch, seed=9)
+    g, spec, topo, sim, ds, st, thr = build_pipeline(b, model, data)
+    ev = b.evaluator(sim, spec, topo, thr, st, ds)
+    cands = candidates(ev.space(), 8)
+    ev.losses(cands[:4])  # warm: plan, weight-code cache, arenas
+    torch.cuda.synchronize()
+    torch.cuda.cudart().cudaProfilerStart()
+    ev.losses(cands[4:8])
+    torch.cuda.synchronize()
+    torch.cuda.cudart().cudaProfilerStop()
+    return 0
+
+
+def measure_traffic(args, timeout=420):
+    """DRAM bytes of the dominant kernel, measured in this run: ncu on a child
+    that replays one grouped step (dram__bytes_read.sum + dram__bytes_write.sum
+    and gpu__time_duration.sum per tc_conv_kernel launch).  None when ncu is
+    unavailable or fails."""
+    ncu = "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None
+    cmd = [ncu, "--profile-from-start", "off", "--clock-control", "none", "--csv",
+           "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+           "-k", "regex:tc_conv_kernel", sys.executable, os.path.abspath(__file__),
+           "--traffic-probe", "--batch", str(args.batch)]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout).stdout
+    except Exception:
+        return None
+    import csv
+    import io
+    rows = [r for r in csv.reader(io.StringIO(out)) if len(r) > 10]
+    if not rows:
+        return None
+    hdr = rows[0]
+    try:
+        i_id, i_name, i_val = hdr.index("ID"), hdr.index("Metric Name"), hdr.index("Metric Value")
+        i_unit = hdr.index("Metric Unit")
+    except ValueError:
+        return None
+    per = {}
+    for r in rows[1:]:
+        v = float(r[i_val].replace(",", ""))
+        unit = r[i_unit]
+        if r[i_name].startswith("dram__bytes"):
+            v *= {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+        else:
+            v *= {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1}.get(unit, 1)
+        per.setdefault(r[i_id], {})[r[i_name]] = v
+    launches = [d for d in per.values() if "gpu__time_duration.sum" in d]
+    if not launches:
+        return None
+    dram = [d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
+            for d in launches]
+    return {"launches": len(launches), "dram_bytes_per_launch": sum(dram) / len(dram),
+            "ncu_time_s_sum": sum(d["gpu__time_duration.sum"] for d in launches),
+            "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over one "
+                      "grouped 4-candidate step of this bench (child process, this run)"}
+
+
+def _events(torch):
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -219,23 +297,27 @@ def main():
     ap.add_argument("--engine", default="auto", choices=["auto", "fast", "exact"])
     ap.add_argument("--no-realized", action="store_true",
                     help="skip the realized-int8 eval_int leg")
+    ap.add_argument("--no-search", action="store_true", help="skip the search legs")
+    ap.add_argument("--no-traffic", action="store_true", help="skip the ncu traffic child")
+    ap.add_argument("--traffic-probe", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--calib-images", type=int, default=128,
                     help="C4 leg: calibration images per GPU (1024 at 8 GPUs)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.traffic_probe:
+        return traffic_probe(args)
 
     import torch
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
     local = _env_int("LOCAL_RANK", 0)
     dist = None
-    if world > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
     os.environ.setdefault("QUANTC_DEVICE", str(local))
     torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
 
     from paper_2103_14949_b200 import cuda_ops
     b = Q.load_b200()
@@ -248,67 +330,83 @@ def main():
     L.qcu_profile_enable.argtypes = [C.c_int]
     L.qcu_profile_read.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                    C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    stream = torch.cuda.ExternalStream(L.qcu_engine_stream())
+
+    # the library's own communicator (comm.hpp): NCCL over NVLink, one rank
+    # per GPU; the unique id travels over torch.distributed
+    if world > 1:
+        uid = [b.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = b.comm_nccl(rank, world, uid[0])
+    else:
+        comm = b.comm_local()
+
+    def max_over_ranks(ms):
+        if dist is None:
+            return ms
+        t = torch.tensor([ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
 
     model = F.resnet(50)
     B = args.batch
     # weak scaling: rank r owns calibration images [r*B, (r+1)*B)
     data_all = model.data(B * world, seed=9)
     data = np.ascontiguousarray(data_all[rank * B:(rank + 1) * B])
-    g, spec, topo, sim, ds, st, thr = build_pipeline(b, model, data)
-    stream = torch.cuda.ExternalStream(L.qcu_engine_stream())
+    g = b.graph(model.doc, model.blob)
+    spec = b.parse_spec(F.spec_fixture("int8_int32"))
+    topo = b.generate_topology(g, spec)
+    sim = b.insert_simulated_quantize(g, topo)
+    edges = b.simulated_edge_indices(g, topo)
+
     # ---- C4 leg (runs first, on a fresh allocator pool): ResNet-50 KL
-    # calibration, images sharded over ranks,
-    # extrema and int64 histograms all-reduced (parallel.sharded_collect_stats),
-    # KL thresholds for every edge; device-timed on the engine stream, max
-    # over ranks
+    # calibration, images sharded over ranks, distributed collect_stats
+    # (extrema MIN/MAX and int64 histograms SUM all-reduced over the
+    # library communicator), KL thresholds for every edge; device-timed on
+    # the engine stream, max over ranks
     calib = None
     if args.calib_images > 0:
-        from paper_2103_14949_b200 import parallel as P
         cn = args.calib_images
         cal = np.ascontiguousarray(model.data(cn * world, seed=17)[rank * cn:(rank + 1) * cn])
         cal_ds = b.dataset(cal)
-        cal_local = P.B200Local(b, g, cal_ds)
-        cal_edges = b.simulated_edge_indices(g, topo)
-        # one untimed pass over the same shard (allocator pool growth, plan
-        # upload), like the main leg's warm-up steps
-        P.sharded_collect_stats(cal_edges, cn * world, 2048, cal_local.extrema,
-                                cal_local.histograms)
-        if dist is not None:
-            dist.barrier()
-        torch.cuda.synchronize()
-        # three timed passes (the stream-ordered allocator reaches its steady
-        # state after a pass or two); report the median
+        b.collect_stats_dist(g, cal_ds, comm, 2048, edges)  # untimed warm pass
         runs = []
         for _ in range(3):
-            if dist is not None:
-                dist.barrier()
-            torch.cuda.synchronize()
-            c0 = torch.cuda.Event(enable_timing=True)
-            c1 = torch.cuda.Event(enable_timing=True)
+            barrier()
+            c0, c1 = _events(torch)
             c2 = torch.cuda.Event(enable_timing=True)
             c0.record(stream)
-            per_edge = P.sharded_collect_stats(cal_edges, cn * world, 2048, cal_local.extrema,
-                                               cal_local.histograms)
+            cst = b.collect_stats_dist(g, cal_ds, comm, 2048, edges)
             c1.record(stream)
-            cal_thr = P.stats_handle(b, per_edge).estimate_thresholds("kl", kl_bits=8)
+            cal_thr = cst.estimate_thresholds("kl", kl_bits=8)
             c2.record(stream)
             torch.cuda.synchronize()
-            cms, kms = c0.elapsed_time(c1), c1.elapsed_time(c2)
-            if dist is not None:
-                t = torch.tensor([cms, kms], device=f"cuda:{local}")
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                cms, kms = float(t[0]), float(t[1])
+            cms, kms = max_over_ranks(c0.elapsed_time(c1)), max_over_ranks(c1.elapsed_time(c2))
             runs.append((cms + kms, cms, kms))
         runs.sort()
         _, cms, kms = runs[1]
         calib = {"workload": "resnet50 KL calibration (BASELINE config C4)",
-                 "images": cn * world, "images_per_gpu": cn, "edges": len(cal_edges),
+                 "images": cn * world, "images_per_gpu": cn, "edges": len(edges),
                  "bins": 2048, "collect_stats_ms": cms, "kl_thresholds_ms": kms,
                  "images_per_s": cn * world / ((cms + kms) / 1e3),
                  "passes_ms": [round(r[0], 1) for r in runs], "reported": "median of 3 passes",
                  "thresholds": len(cal_thr),
-                 "merge": "all_reduce MIN/MAX extrema + SUM int64 histograms" if world > 1
+                 "merge": ("NCCL all_reduce MIN/MAX extrema + SUM int64 histograms "
+                           "(quantc::collect_stats over a Communicator)") if world > 1
                  else "single GPU"}
+        del cal_ds
+
+    # ---- main leg: thresholds from the MERGED statistics of all ranks'
+    # shards (every rank binds identical strategies); each rank's evaluator
+    # holds its own shard; per-candidate agreement counts all-reduced
+    ds = b.dataset(data)
+    st = b.collect_stats_dist(g, ds, comm, 2048, edges)
+    thr = st.estimate_thresholds("quantile", quantile=0.999, pow2=True)
     ev = b.evaluator(sim, spec, topo, thr, st, ds)
     sp = ev.space()
     cands = candidates(sp, args.warmup + args.steps)
@@ -330,8 +428,8 @@ def main():
     def steps_batched(cs):
         """K candidate evaluations through one CandidateEvaluator::losses(span)
         call (qc_evaluator_agreement over the batch; per-rank counts, one
-        all-reduce of the K counts): the search's batch API, with host-side
-        binding and launch work of candidate i+1 overlapping candidate i."""
+        all-reduce of the K counts): the search's batch API, evaluated four
+        at a time through grouped tcgen05 launches."""
         a = np.ascontiguousarray(np.asarray(cs, np.int32))
         out = np.zeros(len(cs), np.int64)
         b.check(L.qc_evaluator_agreement(ev.h, a.ctypes.data_as(C.POINTER(C.c_int)), a.shape[0],
@@ -345,59 +443,96 @@ def main():
     for i in range(args.warmup):
         step(cands[i])
     steps_batched(cands[:args.warmup])
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize()
+    barrier()
     launches0 = ops.counters()["steps"]
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
+    e0, e1 = _events(torch)
     with ClockSampler(local) as clk:
         e0.record(stream)
-        losses_timed = steps_batched(cands[args.warmup:args.warmup + args.steps])
+        steps_batched(cands[args.warmup:args.warmup + args.steps])
         e1.record(stream)
         torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     launches = ops.counters()["steps"] - launches0
-    ms = e0.elapsed_time(e1)
-    if dist is not None:
-        t = torch.tensor([ms], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(e0.elapsed_time(e1))
     ms_step = ms / args.steps
     imgs_per_s = B * world * args.steps / (ms / 1e3)
 
     # ---- the same candidates, one C-ABI call (and all-reduce) per candidate
     pc_steps = min(args.steps, 10)
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize()
-    p0 = torch.cuda.Event(enable_timing=True)
-    p1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    p0, p1 = _events(torch)
     p0.record(stream)
     for i in range(pc_steps):
         step(cands[args.warmup + i])
     p1.record(stream)
     torch.cuda.synchronize()
-    pc_ms = p0.elapsed_time(p1)
-    if dist is not None:
-        t = torch.tensor([pc_ms], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        pc_ms = float(t.item())
+    pc_ms = max_over_ranks(p0.elapsed_time(p1))
     per_call = {"ms_per_step": pc_ms / pc_steps,
                 "images_per_s": B * world * pc_steps / (pc_ms / 1e3), "steps": pc_steps,
                 "api": "qc_evaluator_agreement with one candidate per call (CandidateEvaluator::loss)"}
 
-    # ---- GEMM roofline pass (separate: per-launch events perturb the step)
-    prof_steps = max(2, min(5, args.steps))
+    # ---- random candidates (every layer's weight codes change per candidate)
+    rc_n = min(args.steps, 40)
+    rcands = random_candidates(sp, rc_n + 4)
+    steps_batched(rcands[:4])
+    barrier()
+    q0, q1 = _events(torch)
+    q0.record(stream)
+    steps_batched(rcands[4:])
+    q1.record(stream)
+    torch.cuda.synchronize()
+    rc_ms = max_over_ranks(q0.elapsed_time(q1))
+    random_leg = {"ms_per_step": rc_ms / rc_n, "images_per_s": B * world * rc_n / (rc_ms / 1e3),
+                  "steps": rc_n, "candidates": "every slot drawn uniformly (seed 1)"}
+
+    # ---- roofline pass: the SAME grouped losses call as the timed step, with
+    # per-launch CUDA events around every tc_conv_kernel launch (events cost
+    # the programmatic-dependent-launch overlap, so this pass is separate)
+    prof_n = min(args.steps, 20)
     L.qcu_profile_enable(1)
     gms, gl, gops, gbytes = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
     L.qcu_profile_read(C.byref(gms), C.byref(gl), C.byref(gops), C.byref(gbytes))  # drain
-    for i in range(prof_steps):
-        step(cands[args.warmup + (i % args.steps)])
+    r0, r1 = _events(torch)
+    r0.record(stream)
+    steps_batched(cands[args.warmup:args.warmup + prof_n])
+    r1.record(stream)
     torch.cuda.synchronize()
     L.qcu_profile_read(C.byref(gms), C.byref(gl), C.byref(gops), C.byref(gbytes))
     L.qcu_profile_enable(0)
+    prof_step_ms = r0.elapsed_time(r1)
+
+    # ---- search legs (BASELINE metric: search candidates/s at 1/2/4/8 GPUs):
+    # REAL searches on ResNet-50 over a fixed calibration set of B images held
+    # by every rank; candidate batches sharded over ranks (candidate-sharded
+    # losses, one all-gather per batch), speculative width 4 per rank
+    search = None
+    if not args.no_search:
+        fixed = np.ascontiguousarray(data_all[:B])
+        fds = b.dataset(fixed)
+        fst = b.collect_stats_dist(g, fds, b.comm_local(), 2048, edges)
+        fthr = fst.estimate_thresholds("quantile", quantile=0.999, pow2=True)
+        fev = b.evaluator(sim, spec, topo, fthr, fst, fds)
+        fev.losses(candidates(fev.space(), 4))  # warm
+        search = {"calibration_images": B, "sharding": "candidates over ranks" if world > 1
+                  else "single GPU", "width_per_rank": 4}
+        for method, kw in (("greedy", dict(rounds=1, tol=0.02)),
+                           ("random", dict(n=64 * world, seed=7))):
+            barrier()
+            s0, s1 = _events(torch)
+            s0.record(stream)
+            res = b.search_batched(method, fev.space(), evaluator=fev, comm=comm,
+                                   mode="candidates", width=4 * world, **kw)
+            s1.record(stream)
+            torch.cuda.synchronize()
+            sms = max_over_ranks(s0.elapsed_time(s1))
+            batches, evaluated, committed = res.speculation
+            search[method] = {
+                "params": kw, "ms": sms, "evaluations": res.evaluations,
+                "candidates_per_s": res.evaluations / (sms / 1e3),
+                "evaluated_per_s": evaluated / (sms / 1e3), "evaluated": evaluated,
+                "batches": batches, "best_loss": res.best_loss}
+        del fev, fds
 
     # ---- realized int8 leg: the all_hi strategy
     # lowered by realize() on the same network declared with a batched input;
@@ -415,8 +550,7 @@ def main():
         b.eval_int(R, xin)  # warm: plan, packed weights, allocator pool
         c_after = ops.counters()["tcgen05_gemms"]
         torch.cuda.synchronize()
-        r0 = torch.cuda.Event(enable_timing=True)
-        r1 = torch.cuda.Event(enable_timing=True)
+        r0, r1 = _events(torch)
         r0.record(stream)
         reps = 3
         for _ in range(reps):
@@ -433,9 +567,6 @@ def main():
 
     # ---- e2e: public C-ABI call with HOST buffers: predict_top1 of the sim
     # graph under a candidate binding (uploads images + plan, downloads preds)
-    # The first call compiles the plan and uploads the weights (cold); later
-    # calls on the same graph reuse the resident plan (engine plan cache), so
-    # a step moves the images in and the predictions out.
     e2e_steps = max(3, min(10, args.steps))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -445,18 +576,14 @@ def main():
     for i in range(e2e_steps):
         b.predict_top1(sim, ds, 0, ev.bind(cands[(i + 1) % len(cands)]))
     e2e_dt = (time.perf_counter() - t0) / e2e_steps
-    if dist is not None:
-        t = torch.tensor([e2e_dt], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_dt = float(t.item())
+    e2e_dt = max_over_ranks(e2e_dt * 1e3) / 1e3
     h2d = data.nbytes
     d2h = 8 * B
 
-
     # ---- roofline of the dominant kernel: tc_conv_kernel, the fused tcgen05
-    # implicit-GEMM conv + sq/add epilogue (every conv/dense launch of a step).
-    # HBM-bound framing: algorithmic bytes (each input / weight / output /
-    # residual once) / launch time; the tensor-core fraction rides along.
+    # implicit-GEMM conv + sq/add epilogue (every conv/dense launch of a
+    # step).  Tensor-bound framing (the north star's target): algorithmic
+    # int8 ops (2 x MACs, each group's problem counted) / launch time.
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
@@ -468,12 +595,10 @@ def main():
     gsec = gms.value / 1e3
     tops = (gops.value / gsec) / 1e12 if gsec > 0 else 0.0
     gbs = (gbytes.value / gsec) / 1e9 if gsec > 0 else 0.0
+    nl = max(1, gl.value)
     traffic = None
-    try:
-        prof = json.load(open(os.path.join(REPO, "profiles", "ncu_summary.json")))
-        traffic = prof.get("tc_conv_dram_bytes_per_launch")
-    except Exception:
-        pass
+    if rank == 0 and world == 1 and not args.no_traffic:
+        traffic = measure_traffic(args)
 
     line = {
         "metric": METRIC, "value": imgs_per_s, "unit": "images/s", "n_gpus": world,
@@ -483,47 +608,61 @@ def main():
         "config": {"workload": "resnet50 int8_int32 sim-quant candidate evaluation",
                    "model": "resnet50", "image": 224, "global_batch": B * world,
                    "per_gpu_batch": B, "parallelism": f"dp{world} (calibration shards)",
-                   "thresholds": "quantile 0.999, pow2 (tcgen05 path bit-exact)",
+                   "thresholds": "quantile 0.999, pow2, from the merged statistics of all "
+                                 "ranks (tcgen05 path bit-exact)",
                    "engine": args.engine, "l2": "inputs 38.5 MB/GPU + activations > L2",
                    "step_api": "CandidateEvaluator::losses over the K timed candidates in one "
                                "qc_evaluator_agreement call (see per_call for one call each)"},
-        "candidates_per_s": world * args.steps / (ms / 1e3) / world * 1.0,
+        "candidates_per_s": args.steps / (ms / 1e3),
         "e2e": {"value": B * world / e2e_dt, "unit": "images/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "api": "qc_predict_top1(sim_graph, host dataset, binding) per step, new binding each; the dataset (qc_dataset_create) holds its samples page-locked, so each step DMAs them straight from host memory",
                 "cold_first_call_s": cold_s,
                 "weights_bytes_uploaded_once": len(model.blob)},
         "per_call": per_call,
+        "random_candidates": random_leg,
+        "search": search,
         "calibration": calib,
         "realized_int8": realized,
         "gpu_launches": int(launches),
-        "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": gbs / hbm_peak if hbm_peak else None,
-                     "traffic": traffic,
+        "roofline": {"bound": "tensor", "achieved": tops, "peak": int8_peak, "unit": "TFLOP/s",
+                     "frac": tops / int8_peak if int8_peak else None,
+                     "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
                      "kernel": "tc_conv_kernel (fused tcgen05 kind::i8 implicit-GEMM conv + "
-                               "sq/add epilogue), all launches of a step",
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
-                     "algorithmic_bytes_per_launch": gbytes.value / max(1, gl.value),
-                     "avg_launch_us": 1e3 * gms.value / max(1, gl.value),
-                     "tensor": {"achieved": tops, "peak": int8_peak, "unit": "TOPS",
-                                "frac": tops / int8_peak if int8_peak else None,
-                                "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (burst)"},
-                     # the profiling pass runs one candidate per call: its
-                     # share is of the per_call step (grouped steps interleave
-                     # four candidates' launches)
-                     "kernel_share_of_step": (gms.value / prof_steps / per_call["ms_per_step"])
-                     if per_call["ms_per_step"] > 0 else None,
-                     "launches_per_step": int(gl.value) // prof_steps},
+                               "sq/add epilogue), every launch of the grouped timed step",
+                     "ops_unit": "int8 ops (2 x MAC), counted as FLOP",
+                     "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (dense int8 = 2x bf16)",
+                     "algorithmic_ops_per_launch": gops.value / nl,
+                     "algorithmic_bytes_per_launch": gbytes.value / nl,
+                     "avg_launch_us": 1e3 * gms.value / nl,
+                     "launches_per_step": gl.value / prof_n,
+                     "kernel_share_of_step": gms.value / prof_step_ms if prof_step_ms else None,
+                     "profiled_step_ms": prof_step_ms / prof_n,
+                     "profiled_vs_timed_step": (prof_step_ms / prof_n) / ms_step,
+                     "hbm": {"achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
+                             "frac": gbs / hbm_peak if hbm_peak else None,
+                             "bytes": "algorithmic (inputs, weights, bias, outputs, residual once)"},
+                     "traffic_source": traffic["source"] if traffic else None,
+                     "traffic_launches": traffic["launches"] if traffic else None},
         "clocks": clk.summary(),
     }
-    line["candidates_per_s"] = args.steps / (ms / 1e3)
     if rank == 0 and world == 1 and not args.no_cpu_baseline and os.path.exists(REF_LIB):
+        # the reference on the box's host cores, on the bench's own first
+        # images under candidate 0's binding; its predictions must equal the
+        # B200's for the same images and binding (parity of the timed path)
         threads = os.cpu_count() or 1
         sample = min(max(threads, 2), 16)
-        rate, dt = cpu_reference_rate(model, sample, threads, ev.bind(cands[0]))
-        line["cpu_baseline"] = {"value": rate, "unit": "images/s", "cores": threads,
+        bnd = ev.bind(cands[0])
+        sub = np.ascontiguousarray(data[:sample])
+        ref_preds, dt = cpu_reference_preds(model, sub, threads, bnd)
+        b200_preds = b.predict_top1(sim, b.dataset(sub), 0, bnd)
+        if not np.array_equal(ref_preds, b200_preds):
+            raise SystemExit(f"PARITY FAILURE: reference predictions {ref_preds.tolist()} != "
+                             f"B200 {b200_preds.tolist()} on the bench's images")
+        line["cpu_baseline"] = {"value": sample / dt, "unit": "images/s", "cores": threads,
                                 "kind": "reference",
-                                "sample": f"{sample} images x 1 candidate ({dt:.1f} s)"}
+                                "sample": f"{sample} bench images x 1 candidate ({dt:.1f} s); "
+                                          "predictions checked equal to the B200's"}
     if rank == 0:
         print(json.dumps(line))
     if dist is not None:

@@ -312,7 +312,7 @@ std::shared_ptr<void> predict_device_group(const engine::Plan& plan, const Devic
                                            const std::vector<const SimBinding*>& bindings,
                                            std::shared_ptr<void>* scores, int64_t* per_sample) {
   const int G = static_cast<int>(bindings.size());
-  if (G < 2 || device::profile_enabled()) return nullptr;
+  if (G < 2) return nullptr;
   for (const SimBinding* b : bindings) {
     if (!fused_ready(plan, b, false, true)) return nullptr;
   }

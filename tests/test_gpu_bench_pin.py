@@ -61,7 +61,7 @@ def pinned(b200, ref):
 
     def one(job):
         ci, i = job
-        return ref.eval_fp32(r["sim"], data[i:i + 1], bindings[ci])
+        return ref.eval_fp32(r["sim"], data[i], bindings[ci])
 
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 8) as ex:
         outs = list(ex.map(one, jobs))
