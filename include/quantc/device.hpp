@@ -105,6 +105,11 @@ void collect_histograms(const Graph& g, const std::vector<Sample>& shard,
 // numel) under the active engine mode: the fused int8 engine in auto/fast
 // mode when eligible, the FP64 exact engine otherwise.  Lets tests compare
 // engines bit for bit below the argmax.
+// Why the fused int8 engine does or does not run this graph under this
+// binding in the active engine mode: "" when it runs, else the reason
+// (the plan compiler's or the binding's).  Diagnostics for tests / users.
+std::string fused_status(const Graph& g, const SimBinding* binding);
+
 std::vector<float> predict_scores(const Graph& g, const std::vector<Sample>& dataset,
                                   const SimBinding* binding, int64_t* per_sample);
 

@@ -138,6 +138,10 @@ void qc_comm_free(qc_comm* c);
  * histograms; EdgeStats.sample_count is the global count). */
 int qc_collect_stats_dist(const qc_graph* g, const qc_dataset* d, qc_comm* comm, int bins,
                           const int* edges, size_t n_edges, qc_stats** out);
+/* Why the fused int8 engine does ("") or does not run graph g under the
+ * binding in the active engine mode (quantc/device.hpp fused_status). */
+int qc_fused_status(const qc_graph* g, const int64_t* bind_nodes, const qc_qparams* bind_params,
+                    size_t n_bind, char** why);
 /* CandidateEvaluator::scores (B200 extension): fp32 output rows of each
  * candidate's forward, [n_cands x N x per_sample], `group` candidates per
  * grouped launch (0: default). */

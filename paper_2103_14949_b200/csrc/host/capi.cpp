@@ -926,6 +926,14 @@ int qc_predict_scores(const qc_graph* g, const qc_dataset* d, const int64_t* bin
   });
 }
 
+int qc_fused_status(const qc_graph* g, const int64_t* bind_nodes, const qc_qparams* bind_params,
+                    size_t n_bind, char** why) {
+  return run([&] {
+    SimBinding b = make_binding(bind_nodes, bind_params, n_bind);
+    *why = dup_string(fused_status(*g->g, n_bind ? &b : nullptr));
+  });
+}
+
 int qc_evaluator_scores(const qc_evaluator* e, const int* cands, size_t n_cands, size_t n_slots,
                         int group, float* out, size_t cap, size_t* n_out, int64_t* per_sample) {
   return run([&] {

@@ -410,3 +410,23 @@ std::shared_ptr<void> predict_device(const engine::Plan& plan, const DeviceDatas
 }
 
 }  // namespace quantc::gpu
+
+namespace quantc {
+std::string fused_status(const Graph& g, const SimBinding* binding) {
+  const engine::PlanLease lease = engine::lease_plan(g);
+  const engine::Plan& plan = lease.plan();
+  const auto mode = device::engine_mode();
+  if (mode == device::EngineMode::kExact) return "engine mode is exact";
+  if (!kern::gemm_s8_tcgen05_available()) return "tcgen05 unavailable on this device";
+  if (!plan.fused_tried) {
+    plan.fused_tried = true;
+    plan.fused = std::make_shared<fast::FastPlan>(plan);
+  }
+  if (!plan.fused->ok()) return "plan: " + plan.fused->why_not();
+  std::string why;
+  if (!plan.fused->eligible(binding, mode == device::EngineMode::kAuto, &why)) {
+    return "binding: " + why;
+  }
+  return "";
+}
+}  // namespace quantc

@@ -369,7 +369,6 @@ struct Builder {
 
   // consumer x of the register value u
   void handle(int u, int x, int port) {
-    (void)u;
     const Node& nx = node(x);
     switch (nx.op) {
       case OpKind::kSimulatedQuantize: {
@@ -394,6 +393,12 @@ struct Builder {
             handle(x, y, cy[0].second);
             return;
           case OpKind::kAdd: {
+            if (nx.attr_or<bool>("boundary", false)) {
+              // a boundary sq is always a passthrough (fp32 out): fp32 add
+              op(kern::kPSq, sq_slot(x));
+              handle(x, y, cy[0].second);
+              return;
+            }
             const auto& yin = plan.steps()[static_cast<size_t>(y)].in;
             const int other = yin[static_cast<size_t>(1 - cy[0].second)];
             auto it = val_of.find(other);
@@ -447,6 +452,31 @@ struct Builder {
         emit(x);
         flat_hw = 1;
         flat_cs = 0;
+        return;
+      }
+      case OpKind::kGlobalAvgPool2d:
+        // an fp32 value pooled by a GAP stage (which reads it from rows)
+        store_f32(u, false);
+        return;
+      case OpKind::kAdd: {
+        // fp32 add (an add the spec does not quantize, e.g. arm_vmlal_like's
+        // residuals): float + float like the reference (interpreter.cpp
+        // add).  The first operand to arrive is materialised as fp32 rows;
+        // the program of the second reads it and carries on with the sum.
+        if (flat_hw != 1) {
+          fail("add after flatten");
+          return;
+        }
+        const auto& xin = plan.steps()[static_cast<size_t>(x)].in;
+        const int other = xin[static_cast<size_t>(1 - port)];
+        auto it = val_of.find(other);
+        if (it != val_of.end()) {
+          op(kern::kPAdd, 0, it->second);
+          absorbed.insert(x);
+          emit(x);
+        } else {
+          store_f32(u, false);
+        }
         return;
       }
       default:

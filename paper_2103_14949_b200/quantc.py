@@ -445,6 +445,16 @@ class Quantc:
         return self._vec(self.lib.qc_predict_top1, (g.h, d.h, workers, idp, params, nb),
                          C.c_int64, first_cap=max(1, d.n))
 
+    def fused_status(self, g: "Graph", binding=None) -> str:
+        """'' when the fused int8 tcgen05 engine runs g under `binding`, else
+        the reason (B200 extension)."""
+        ids, params, nb, idp = self._binding(binding)
+        s = C.c_void_p()
+        fn = self._bind("qc_fused_status", C.c_int,
+                        [_P, _PI64, C.POINTER(QParams), _SZ, _PSTR])
+        self.check(fn(g.h, idp, params, nb, C.byref(s)))
+        return self._take_string(s)
+
     def predict_scores(self, g: "Graph", d: "Dataset", binding=None) -> np.ndarray:
         """B200 extension (quantc/device.hpp): the fp32 output rows behind
         predict_top1 under the active engine mode, shape [samples, per]."""

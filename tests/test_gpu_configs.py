@@ -96,6 +96,8 @@ def test_c3_int16_accumulation_on_fused_engine(b200, ref, cuda_lib, c3_i16acc):
     # the bound signature really is (i8, i8) -> i16 with an int16 accumulator clamp
     bnd = r["ev"].bind(cands[0])
     assert any(p.acc_dtype == F_I16 for p in bnd.values())
+    why = b200.fused_status(a["sim"], a["ev"].bind(cands[0]))
+    assert why == "", why
     f0 = cuda_lib.counters()["fused_batches"]
     la = a["ev"].losses(cands)
     assert cuda_lib.counters()["fused_batches"] - f0 >= len(cands), "fused engine not used"
@@ -146,3 +148,31 @@ def test_c5_inception_search_identical(b200, ref, c5, method, kw):
     rr = ref.search(method, r["ev"].space(), evaluator=r["ev"], **kw)
     assert (ra.best, ra.best_loss, ra.evaluations) == (rr.best, rr.best_loss, rr.evaluations)
     assert ra.trace == rr.trace
+
+
+@pytest.fixture(scope="module")
+def c5_pow2(b200, ref):
+    m = F.inception_v3(modules=1, image=29, width=4)
+    data = m.data(6)
+    return _pipe(b200, m, data, "int8_int32", min_bit=4, pow2=True), \
+        _pipe(ref, m, data, "int8_int32", min_bit=4, pow2=True)
+
+
+def test_c5_inception_pow2_on_fused_engine(b200, ref, cuda_lib, c5_pow2):
+    """C5 with power-of-two thresholds: the whole search evaluation runs on
+    the fused tcgen05 engine and equals the reference."""
+    a, r = c5_pow2
+    _same_stats(a, r)
+    sp = r["ev"].space()
+    rng = np.random.default_rng(9)
+    cands = [sp.all_hi(), sp.all_lo()] + [
+        [int(rng.integers(lo, hi + 1)) for lo, hi in zip(sp.lo, sp.hi)] for _ in range(6)]
+    why = b200.fused_status(a["sim"], a["ev"].bind(cands[0]))
+    assert why == "", why
+    f0 = cuda_lib.counters()["fused_batches"]
+    np.testing.assert_array_equal(a["ev"].losses(cands), r["ev"].losses(cands))
+    assert cuda_lib.counters()["fused_batches"] - f0 >= len(cands)
+    ra = b200.search_batched("random", a["ev"].space(), evaluator=a["ev"], n=12, seed=5)
+    rr = ref.search("random", r["ev"].space(), evaluator=r["ev"], n=12, seed=5)
+    assert (ra.best, ra.best_loss, ra.evaluations, ra.trace) == \
+        (rr.best, rr.best_loss, rr.evaluations, rr.trace)
