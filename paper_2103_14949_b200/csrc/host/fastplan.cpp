@@ -1415,6 +1415,7 @@ void FastPlan::gemm_spec(Run& r, size_t si, kern::TcConvSpec& sp) {
     ok_cuda(cudaMemsetAsync(l1, 0, sizeof(int), ST()));
     kern::weight_l1_max(static_cast<const int8_t*>(codes.get()), st.O, st.Kpad, l1, ST());
     it = wcache_.emplace(ck, codes).first;
+    wcache_bytes_ += cbytes + 16;
   }
   r.keep.push_back(it->second);  // a cache clear must not free codes this run uses
   sp = kern::TcConvSpec{};
@@ -1576,6 +1577,23 @@ void FastPlan::finish(Run& r) {
   device::counters().fused_batches++;
 }
 
+// Weight codes depend only on (stage, weight sq parameters): for a search
+// that is (layer, bit-width), a handful of variants per layer.  They are
+// kept resident up to QUANTC_WCACHE_MB (default 4096 MB of HBM), so after the
+// first visit of each bit-width no candidate re-quantizes its weights
+// (ResNet-50: 25.5 MB of codes per variant set).  Over budget the cache is
+// dropped (stream-ordered frees: in-flight launches keep their codes).
+void FastPlan::trim_weight_cache() {
+  static const size_t budget = [] {
+    const char* e = std::getenv("QUANTC_WCACHE_MB");
+    return static_cast<size_t>(e ? std::max(1, std::atoi(e)) : 4096) << 20;
+  }();
+  if (wcache_bytes_ > budget) {
+    wcache_.clear();
+    wcache_bytes_ = 0;
+  }
+}
+
 void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
                        const SimBinding* binding, int64_t* d_preds, float* d_scores) {
   static const bool hprof = std::getenv("QUANTC_HOST_PROF") != nullptr;
@@ -1583,7 +1601,7 @@ void FastPlan::predict(int batch, const std::vector<const float*>& inputs,
   // weight codes are cached per (stage, weight sq parameters); a long search
   // visits many weight bit-widths, so keep roughly the last few bindings
   // (freed stream-ordered: in-flight launches keep their codes)
-  if (wcache_.size() > 4 * stages_.size()) wcache_.clear();
+  trim_weight_cache();
   Run r;
   r.group = 0;
   r.batch = batch;
@@ -1614,7 +1632,7 @@ void FastPlan::predict_group(int batch, const std::vector<const float*>& inputs,
                              const std::vector<float*>* scores) {
   const int G = static_cast<int>(bindings.size());
   if (G < 1 || G > kern::kMaxGroups) throw std::logic_error("predict_group: 1..kMaxGroups bindings");
-  if (wcache_.size() > 4 * stages_.size() * static_cast<size_t>(G)) wcache_.clear();
+  trim_weight_cache();
   std::vector<Run> r(static_cast<size_t>(G));
   for (int g = 0; g < G; ++g) {
     r[g].group = g;

@@ -74,6 +74,8 @@ class FastPlan {
   Arena arenas_[kern::kMaxGroups];
   // weight code cache: (stage, FSq bytes) -> codes
   std::map<std::pair<int, std::string>, std::shared_ptr<void>> wcache_;
+  size_t wcache_bytes_ = 0;
+  void trim_weight_cache();
 
   struct Run;
   void compile();
