@@ -65,6 +65,12 @@ int qcu_requantize(const int32_t* x, int32_t* y, int64_t n, int64_t multiplier, 
 int qcu_gemm_s8(const int8_t* A, const int8_t* B, int M, int N, int K, double scale,
                 const float* bias, float* y, int OHW, void* stream);
 
+/* per-row argmax of x [rows][cols] with the reference argmax_class
+ * semantics (interpreter.cpp:533-541: first maximum, strict '>', NaN never
+ * taken, NaN at index 0 wins); grouped > 0 runs the grouped-candidate kernel
+ * over that many equal row groups */
+int qcu_argmax_rows(const float* x, int rows, int64_t cols, int grouped, int64_t* out,
+                    void* stream);
 int qcu_synchronize(void* stream);
 const char* qcu_last_error(void);
 /* 1 when the tcgen05 path can run on the current device */

@@ -1,4 +1,5 @@
 // cuda_capi.cpp — include/quantc_cuda.h: the C-ABI over the sm_100a kernels.
+#include <algorithm>
 #include "quantc_cuda.h"
 
 #include <cuda_runtime.h>
@@ -137,6 +138,27 @@ int qcu_requantize(const int32_t* x, int32_t* y, int64_t n, int64_t multiplier, 
                    int64_t in_zp, int64_t out_zp, int64_t qmin, int64_t qmax, void* stream) {
   return wrap([&] {
     kern::requantize_int(x, y, n, multiplier, shift, in_zp, out_zp, qmin, qmax, st(stream));
+  });
+}
+
+int qcu_argmax_rows(const float* x, int rows, int64_t cols, int grouped, int64_t* out,
+                    void* stream) {
+  return wrap([&] {
+    if (grouped) {
+      // the grouped-candidate kernel: rows split into up to 4 equal groups
+      const int g = std::min(grouped, 4);
+      if (rows % g) throw std::invalid_argument("rows not divisible by the group count");
+      const int per = rows / g;
+      const float* xs[4];
+      int64_t* outs[4];
+      for (int i = 0; i < g; ++i) {
+        xs[i] = x + static_cast<int64_t>(i) * per * cols;
+        outs[i] = out + static_cast<int64_t>(i) * per;
+      }
+      kern::argmax_rows_multi(xs, outs, g, per, cols, st(stream));
+    } else {
+      kern::argmax_rows(x, rows, cols, out, st(stream));
+    }
   });
 }
 

@@ -109,7 +109,9 @@ Tensor ref_tensor(const Json& ref, SidecarCache& sc) {
     return decode_tensor(sc.get(ref.at("file").get<std::string>()), ref.at("offset").get<int64_t>(),
                          parse_dtype(ref.at("dtype").get<std::string>()),
                          ref.at("shape").get<std::vector<int64_t>>(), ref.dump());
-  } catch (const Json::exception& e) {
+  } catch (const IoError&) {
+    throw;
+  } catch (const std::exception& e) {
     throw IoError(std::string("bad tensor ref: ") + e.what());
   }
 }
@@ -137,7 +139,10 @@ Json graph_to_json(const Graph& g, const std::string& sidecar, std::string* side
   Json nodes = Json::array();
   for (const Node& n : g.nodes()) {
     Json jn = {{"id", n.id}, {"op", op_name(n.op)}, {"attrs", n.attrs}};
-    if (n.payload.has_value()) jn["payload"] = tensor_ref(*n.payload, sidecar, out);
+    if (!jn["attrs"].is_object()) jn["attrs"] = Json::object();
+    // SPEC.md graph module: the sidecar ref {file, offset, dtype, shape}
+    // lives in the constant's attrs
+    if (n.payload.has_value()) jn["attrs"]["payload"] = tensor_ref(*n.payload, sidecar, out);
     nodes.push_back(std::move(jn));
   }
   Json edges = Json::array();
@@ -158,7 +163,18 @@ Graph graph_from_json(const Json& doc, const fs::path& dir) {
       n.id = jn.at("id").get<NodeId>();
       n.op = parse_op(jn.at("op").get<std::string>());
       if (jn.contains("attrs") && jn.at("attrs").is_object()) n.attrs = jn.at("attrs");
-      if (jn.contains("payload")) n.payload = ref_tensor(jn.at("payload"), sc);
+      // the payload ref: attrs.payload (SPEC form), the ref keys directly in
+      // attrs, or a node-level "payload" (files written by round-1 builds)
+      if (n.attrs.is_object() && n.attrs.contains("payload")) {
+        n.payload = ref_tensor(n.attrs.at("payload"), sc);
+        n.attrs.erase("payload");
+      } else if (n.attrs.is_object() && n.attrs.contains("file") && n.attrs.contains("offset") &&
+                 n.attrs.contains("dtype") && n.attrs.contains("shape")) {
+        n.payload = ref_tensor(n.attrs, sc);
+        for (const char* k : {"file", "offset", "dtype", "shape"}) n.attrs.erase(k);
+      } else if (jn.contains("payload")) {
+        n.payload = ref_tensor(jn.at("payload"), sc);
+      }
       nodes.push_back(std::move(n));
     }
     std::vector<Edge> edges;
@@ -172,7 +188,9 @@ Graph graph_from_json(const Json& doc, const fs::path& dir) {
     }
     return Graph(std::move(nodes), std::move(edges), doc.at("inputs").get<std::vector<NodeId>>(),
                  std::move(outputs));
-  } catch (const Json::exception& e) {
+  } catch (const IoError&) {
+    throw;
+  } catch (const std::exception& e) {
     throw IoError(std::string("malformed graph document: ") + e.what());
   }
 }
@@ -214,11 +232,17 @@ Dataset load_dataset(const fs::path& manifest_path) {
   if (!arr.is_array()) throw IoError("dataset manifest must be a JSON array");
   SidecarCache sc{manifest_path.parent_path(), {}};
   Dataset ds;
-  for (const Json& js : arr) {
-    Sample s;
-    for (const Json& ref : js.at("inputs")) s.inputs.push_back(ref_tensor(ref, sc));
-    if (js.contains("label") && !js.at("label").is_null()) s.label = js.at("label").get<int64_t>();
-    ds.push_back(std::move(s));
+  try {
+    for (const Json& js : arr) {
+      Sample s;
+      for (const Json& ref : js.at("inputs")) s.inputs.push_back(ref_tensor(ref, sc));
+      if (js.contains("label") && !js.at("label").is_null()) s.label = js.at("label").get<int64_t>();
+      ds.push_back(std::move(s));
+    }
+  } catch (const IoError&) {
+    throw;
+  } catch (const std::exception& e) {
+    throw IoError(manifest_path.string() + ": malformed dataset manifest: " + e.what());
   }
   return ds;
 }
@@ -240,6 +264,7 @@ void save_stats(const CalibrationStats& stats, const fs::path& path) {
 CalibrationStats load_stats(const fs::path& path) {
   const Json doc = parse_json(path);
   CalibrationStats st;
+  if (!doc.is_object()) throw IoError(path.string() + ": stats file must be a JSON object");
   try {
     st.dataset_fingerprint = std::stoull(doc.value("dataset_fingerprint", std::string("0")));
     st.graph_fingerprint = std::stoull(doc.value("graph_fingerprint", std::string("0")));
@@ -255,8 +280,10 @@ CalibrationStats load_stats(const fs::path& path) {
       }
       st.per_edge[std::stoi(key)] = std::move(e);
     }
-  } catch (const Json::exception& e) {
-    throw IoError(std::string("malformed stats file: ") + e.what());
+  } catch (const IoError&) {
+    throw;
+  } catch (const std::exception& e) {
+    throw IoError(path.string() + ": malformed stats file: " + e.what());
   }
   return st;
 }
@@ -274,8 +301,11 @@ void save_strategy(const Strategy& strategy, const Json& meta, const fs::path& p
 Strategy load_strategy(const fs::path& path) {
   const Json doc = parse_json(path);
   Strategy s;
+  if (!doc.is_object() || !doc.contains("edges") || !doc.at("edges").is_object()) {
+    throw IoError(path.string() + ": a strategy file is an object with an \"edges\" object");
+  }
   try {
-    const Json& edges = doc.contains("edges") ? doc.at("edges") : doc;
+    const Json& edges = doc.at("edges");
     for (const auto& [key, j] : edges.items()) {
       EdgeDecision d;
       d.bit = j.at("bit").get<int>();
@@ -285,8 +315,10 @@ Strategy load_strategy(const fs::path& path) {
       d.zero_point = j.at("zero_point").get<int64_t>();
       s.edges[std::stoi(key)] = d;
     }
-  } catch (const Json::exception& e) {
-    throw IoError(std::string("malformed strategy file: ") + e.what());
+  } catch (const IoError&) {
+    throw;
+  } catch (const std::exception& e) {
+    throw IoError(path.string() + ": malformed strategy file: " + e.what());
   }
   return s;
 }

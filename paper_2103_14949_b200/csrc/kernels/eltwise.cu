@@ -89,11 +89,15 @@ __global__ void __launch_bounds__(256) argmax_kernel(const float* __restrict__ x
   pdl_trigger();
   pdl_wait();
   const float* row = x + static_cast<int64_t>(blockIdx.x) * cols;
+  // reference argmax_class (interpreter.cpp:533-541): best = 0, then strict
+  // '>' in index order — the first maximum over the non-NaN scores, except
+  // that a NaN at index 0 is never replaced (result 0).  NaNs are skipped
+  // here and index 0's NaN is applied at the end.
   float bv = -FLT_MAX;
   int64_t bi = -1;
   for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
     const float v = row[c];
-    if (bi < 0 || v > bv) {
+    if (v == v && (bi < 0 || v > bv)) {
       bv = v;
       bi = c;
     }
@@ -119,7 +123,8 @@ __global__ void __launch_bounds__(256) argmax_kernel(const float* __restrict__ x
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int w2 = 1; w2 < static_cast<int>(blockDim.x >> 5); ++w2) take(sv[w2], si[w2], bv, bi);
-    out[blockIdx.x] = bi < 0 ? 0 : bi;
+    const float r0 = row[0];
+    out[blockIdx.x] = (bi < 0 || r0 != r0) ? 0 : bi;
   }
 }
 
@@ -136,7 +141,7 @@ __global__ void __launch_bounds__(256) argmax_multi_kernel(RowsPack p, int64_t c
   int64_t bi = -1;
   for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
     const float v = row[c];
-    if (bi < 0 || v > bv) {
+    if (v == v && (bi < 0 || v > bv)) {  // NaN semantics: argmax_kernel
       bv = v;
       bi = c;
     }
@@ -159,7 +164,10 @@ __global__ void __launch_bounds__(256) argmax_multi_kernel(RowsPack p, int64_t c
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) p.out[blockIdx.y][blockIdx.x] = si[0];
+  if (threadIdx.x == 0) {
+    const float r0 = row[0];
+    p.out[blockIdx.y][blockIdx.x] = (si[0] < 0 || r0 != r0) ? 0 : si[0];
+  }
 }
 
 // counts[g] += #{i : a[g * n + i] == b[i]} for group g = blockIdx.y

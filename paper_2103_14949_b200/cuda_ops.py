@@ -28,6 +28,7 @@ class CudaOps:
                                      C.c_int64, C.c_int64, C.c_int64, _P]
         L.qcu_gemm_s8.argtypes = [_P, _P, C.c_int, C.c_int, C.c_int, C.c_double, _P, _P, C.c_int,
                                   _P]
+        L.qcu_argmax_rows.argtypes = [_P, C.c_int, C.c_int64, C.c_int, _P, _P]
         L.qcu_synchronize.argtypes = [_P]
         L.qcu_set_engine_mode.argtypes = [C.c_int]
         L.qcu_counters.argtypes = [C.POINTER(C.c_int64)] * 4
@@ -100,6 +101,12 @@ class CudaOps:
         self._ok(self.lib.qcu_requantize(self._p(x), self._p(y), x.numel(), mult, shift, in_zp,
                                          out_zp, qmin, qmax, self._s()))
         return y
+
+    def argmax_rows(self, x, grouped=0):
+        out = torch.empty(x.shape[0], dtype=torch.int64, device=x.device)
+        self._ok(self.lib.qcu_argmax_rows(self._p(x), x.shape[0], x.shape[1], grouped,
+                                          self._p(out), self._s()))
+        return out
 
     def gemm_s8(self, A, B, scale=1.0, bias=None, ohw=1):
         M, K = A.shape

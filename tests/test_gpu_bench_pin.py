@@ -69,6 +69,20 @@ def pinned(b200, ref):
     return dict(a=a, r=r, model=model, data=data, cands=cands, ref_scores=ref_scores)
 
 
+def test_collect_stats_bit_exact_at_224(pinned):
+    """collect_stats over the 8 bench images at 224x224 (all 191 simulated
+    edges): min / max / absmax / sample_count and all 2048 int64 counts equal
+    the reference's (calibration.cpp:37-115)."""
+    a, r = pinned["a"], pinned["r"]
+    assert a["st"].edges() == r["st"].edges()
+    assert len(r["st"].edges()) == 191
+    for k in r["st"].edges():
+        ea, er = a["st"].get(k), r["st"].get(k)
+        assert (ea["min"], ea["max"], ea["absmax"], ea["sample_count"]) == \
+            (er["min"], er["max"], er["absmax"], er["sample_count"]), k
+        np.testing.assert_array_equal(ea["counts"], er["counts"], err_msg=f"edge {k}")
+
+
 def test_thresholds_and_refs_identical(pinned):
     a, r = pinned["a"], pinned["r"]
     assert a["thr"] == r["thr"]

@@ -305,3 +305,35 @@ def test_candidate_pairs_grouped_equal_single_calls(b200, cuda_lib, name):
     batched = ev.losses(cands).tolist()
     single = [ev.loss(c) for c in cands]
     assert batched == single
+
+
+def _argmax_class(row):
+    """Restatement of the reference argmax_class (interpreter.cpp:533-541)."""
+    best = 0
+    for i in range(1, len(row)):
+        if row[i] > row[best]:
+            best = i
+    return best
+
+
+@pytest.mark.parametrize("grouped", [0, 4])
+def test_argmax_nan_and_ties_match_reference(cuda_lib, grouped):
+    """NaN scores are never taken (except a NaN at index 0, which wins),
+    ties keep the lowest index, +0 / -0 compare equal — per row, through the
+    single and the grouped-candidate argmax kernels."""
+    rng = np.random.default_rng(41)
+    rows, cols = 64, 1000
+    x = rng.standard_normal((rows, cols)).astype(np.float32)
+    x[0, :] = np.nan                         # all NaN -> 0
+    x[1, 0] = np.nan                         # NaN at 0 -> 0
+    x[2, 5] = np.nan; x[2, 6] = 50.0         # NaN before the max
+    x[3, :] = 1.0                            # all ties -> 0
+    x[4, 700] = 9.0; x[4, 3] = 9.0           # tie -> lowest index
+    x[5, :] = -np.inf; x[5, 900] = np.nan    # -inf everywhere -> 0
+    x[6, :] = 0.0; x[6, 0] = -0.0; x[6, 17] = 0.0
+    x[7, 1:] = np.nan                        # only index 0 is a number
+    x[8, 999] = np.inf; x[8, 998] = np.nan
+    x[9::7, rng.integers(0, cols, 8)] = np.nan  # scattered NaNs
+    got = cuda_lib.argmax_rows(torch.from_numpy(x).cuda(), grouped=grouped).cpu().numpy()
+    exp = np.array([_argmax_class(list(r)) for r in x])
+    np.testing.assert_array_equal(got, exp)

@@ -5,6 +5,7 @@ evaluation of the same graph.  Host code only; runs on CPU."""
 import json
 
 import numpy as np
+import pytest
 
 from paper_2103_14949_b200 import fixtures as F
 
@@ -37,7 +38,8 @@ def test_graph_file_round_trip(b200, ref, tmp_path):
     g.save(path)
     assert (tmp_path / "model.bin").exists()
     doc = json.loads(path.read_text())
-    refs = [n["payload"] for n in doc["nodes"] if "payload" in n]
+    # SPEC.md graph module: the sidecar ref lives in the constant's attrs
+    refs = [n["attrs"]["payload"] for n in doc["nodes"] if "payload" in n.get("attrs", {})]
     assert refs and all(set(r) == {"file", "offset", "dtype", "shape"} for r in refs)
     assert all(r["file"] == "model.bin" for r in refs)
     g2 = b200.load_graph(path)
@@ -66,7 +68,7 @@ def test_realized_graph_file_round_trip(b200, ref, tmp_path):
     g = b200.graph(doc, blob)
     g.save(tmp_path / "int.json")
     d = json.loads((tmp_path / "int.json").read_text())
-    dts = {n["payload"]["dtype"] for n in d["nodes"] if "payload" in n}
+    dts = {n["attrs"]["payload"]["dtype"] for n in d["nodes"] if "payload" in n["attrs"]}
     assert dts & {"int8", "int32"}, dts
     g2 = b200.load_graph(tmp_path / "int.json")
     assert g2.to_json() == g.to_json() and g2.blob() == g.blob()
@@ -136,3 +138,44 @@ def test_cpp_dataset_strategy_trace_round_trip(tmp_path):
     r = subprocess.run([str(exe), str(tmp_path)], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     assert "ok" in r.stdout
+
+
+def test_graph_file_spec_forms_load(b200, tmp_path):
+    """A graph file written to SPEC.md by another tool loads: the ref as
+    attrs.payload, the ref keys directly in attrs, or (round-1 files) a
+    node-level payload — all give the same graph."""
+    model = F.small_cnn()
+    g = b200.graph(model.doc, model.blob)
+    g.save(tmp_path / "m.json")
+    doc = json.loads((tmp_path / "m.json").read_text())
+    flat = json.loads(json.dumps(doc))
+    legacy = json.loads(json.dumps(doc))
+    for a, b in zip(flat["nodes"], legacy["nodes"]):
+        if "payload" in a.get("attrs", {}):
+            ref = a["attrs"].pop("payload")
+            a["attrs"].update(ref)
+            b["payload"] = b["attrs"].pop("payload")
+    for name, d in (("flat", flat), ("legacy", legacy)):
+        (tmp_path / f"{name}.json").write_text(json.dumps(d))
+        (tmp_path / f"{name}.bin").write_bytes((tmp_path / "m.bin").read_bytes())
+        for n in d["nodes"]:
+            for r in ([n["attrs"]] if "file" in n.get("attrs", {}) else []) + \
+                     ([n["payload"]] if "payload" in n else []):
+                r["file"] = f"{name}.bin"
+        (tmp_path / f"{name}.json").write_text(json.dumps(d))
+        g2 = b200.load_graph(tmp_path / f"{name}.json")
+        assert g2.to_json() == g.to_json(), name
+        assert g2.blob() == g.blob(), name
+
+
+def test_malformed_files_raise_io_error(b200, tmp_path):
+    from paper_2103_14949_b200 import quantc as Q
+    bad_stats = tmp_path / "s.json"
+    bad_stats.write_text('{"per_edge": {"x": {"min": 0, "max": 1, "absmax": 1, '
+                         '"counts": [1], "samples": 1}}}')
+    with pytest.raises(Q.QuantcError) as e:
+        b200.load_stats(bad_stats)
+    assert "malformed stats" in str(e.value)
+    bad_stats.write_text('[1, 2]')
+    with pytest.raises(Q.QuantcError):
+        b200.load_stats(bad_stats)
