@@ -1322,17 +1322,27 @@ void FastPlan::prepare(Run& r) {
       auto same = [](const kern::EpiSq& a, const kern::EpiSq& b) {
         return a.flags == b.flags && a.lo == b.lo && a.hi == b.hi;
       };
-      if (sh == kern::kShapeSqStore && e.q[0].flags == kern::kEpiNonneg && identity(e.q[1]) &&
-          fold_saturating(kern::kShapeSqStoreId, st.bias_absmin, e)) {
-        sh = kern::kShapeSqStoreId;
+      // integer shapes first (no float conversion at all), else the
+      // saturating float forms
+      static const bool no_int = std::getenv("QUANTC_NO_INT_EPI") != nullptr;
+      if (sh == kern::kShapeSqStore && e.q[0].flags == kern::kEpiNonneg && identity(e.q[1])) {
+        if (!no_int && fold_integer(si, kern::kShapeSqStoreInt, sxw_of[si], r.acc_bound[si], e, r.keep)) {
+          sh = kern::kShapeSqStoreInt;
+        } else if (fold_saturating(kern::kShapeSqStoreId, st.bias_absmin, e)) {
+          sh = kern::kShapeSqStoreId;
+        }
       } else if (sh == kern::kShapeAddFork && e.q[0].flags == 0 &&
                  e.q[1].flags == kern::kEpiNonneg && identity(e.q[2]) && identity(e.q[3]) &&
-                 same(e.q[2], e.q[3]) && fold_saturating(kern::kShapeAddForkId, st.bias_absmin, e)) {
-        sh = kern::kShapeAddForkId;
+                 same(e.q[2], e.q[3])) {
+        if (!no_int && fold_integer(si, kern::kShapeAddForkInt, sxw_of[si], r.acc_bound[si], e, r.keep)) {
+          sh = kern::kShapeAddForkInt;
+        } else if (fold_saturating(kern::kShapeAddForkId, st.bias_absmin, e)) {
+          sh = kern::kShapeAddForkId;
+        }
       }
     }
     shape_of[si] = sh;
-    if (!no_alias && (sh == kern::kShapeAddFork || sh == kern::kShapeAddForkId) &&
+    if (!no_alias && (sh == kern::kShapeAddFork || sh == kern::kShapeAddForkId || sh == kern::kShapeAddForkInt) &&
         st.n_out == 2 && std::memcmp(&e.q[2], &e.q[3], sizeof(kern::EpiSq)) == 0) {
       const Val& v0 = *vals_[static_cast<size_t>(st.out_vals[0])];
       const Val& v1 = *vals_[static_cast<size_t>(st.out_vals[1])];
@@ -1381,6 +1391,266 @@ void FastPlan::prepare(Run& r) {
   ok_cuda(cudaMemcpyAsync(ar.tables.get(), tabs.data(), tabs.size() * sizeof(kern::StageTables),
                           cudaMemcpyHostToDevice, ST()));
   r.d_tabs = static_cast<const kern::StageTables*>(ar.tables.get());
+}
+
+// Integer form of shapes 6/7 (fused.h EpiConsts i_*, fused.cuh run_int_epi).
+// Every scale is a power of two.  The code sq0 makes of a conv output is a
+// monotone step function of the channel's int32 accumulator a:
+//   f(a) = clamp(round(RN24(a*s + b[n]) / s0), lo0, hi0)
+// (reference interpreter.cpp:196-236: double sum, + bias, one rounding to
+// float; then simulate.cpp:64-78).  The kernel evaluates
+//   g(a) = clamp((a*m0 + C[n]) >> r0, lo0, hi0)
+// With s/s0 = 2^-r0 (r0 >= 1) g steps at a = k*2^r0 - C[n], C[n] = 2^(r0-1) -
+// ceil(-b/s); f steps there too unless the float rounding moves a boundary
+// (bias within half an ulp of a step) or a half-way tie is reachable, so both
+// sides of every step of every channel are checked with the reference
+// arithmetic (a monotone integer step function is pinned by its steps).  With
+// s/s0 = 2^L >= 1, g(a) = clamp(a*2^L + C[n]) is checked over its whole
+// unclamped range.  Any failing channel leaves the stage on the float shape.
+// Shape 7's add and sq1 act on codes: r0*s0 + c*s_res is an exact float when
+// the bound below holds, so round((r0*s0 + c*s_res)/s1) is the integer
+// half-away rounding of r0*2^a + c*2^b by 2^g (non-negative codes: +2^(g-1),
+// then an arithmetic shift; negative sums saturate to 0 in the byte pack).
+bool FastPlan::fold_integer(size_t si, int shape, double sxw, double acc_bound, kern::EpiConsts& e,
+                            std::vector<std::shared_ptr<void>>& keep) {
+  const Stage& st = *stages_[si];
+  const double M = kern::kMagic;
+  auto code_range = [](const kern::EpiSq& q, double& lo, double& hi) {
+    lo = std::nearbyint(static_cast<double>(q.lo) + 0.5);
+    hi = std::nearbyint(static_cast<double>(q.hi) - 0.5);
+  };
+  auto store_clamp = [&](const kern::EpiSq& q, double& lo, double& hi) {
+    if (q.flags & kern::kEpiNoClamp) return;
+    lo = std::max(lo, static_cast<double>(q.lo) - M);
+    hi = std::min(hi, static_cast<double>(q.hi) - M);
+  };
+  auto log2_exact = [](double v, int& out) {
+    int ex = 0;
+    if (!(v > 0.0) || std::frexp(v, &ex) != 0.5) return false;
+    out = ex - 1;
+    return true;
+  };
+  const bool addfork = shape == kern::kShapeAddForkInt;
+  double lo0, hi0;
+  code_range(e.q[0], lo0, hi0);
+  if (!addfork) {
+    store_clamp(e.q[1], lo0, hi0);
+    if (lo0 != 0.0 || hi0 < 0.0 || hi0 > 255.0) return false;
+  } else if (lo0 < -32768.0 || hi0 > 32767.0 || lo0 > hi0) {
+    return false;
+  }
+  const double inv0 = static_cast<double>(e.inv0);
+  int ek = 0;
+  if (!log2_exact(static_cast<double>(e.q[0].k), ek) || sxw * inv0 != static_cast<double>(e.q[0].k) ||
+      ek > 20 || ek < -30) {
+    return false;
+  }
+  const int m0 = ek >= 0 ? (1 << ek) : 1;
+  const int r0 = ek >= 0 ? 0 : -ek;
+  // the kernel shifts by multiply-high, which needs a shift >= 2: scale the
+  // accumulator side by 2^sc0 (exact) where sq0's shift is shorter
+  const int sc0 = r0 < 2 ? 2 - r0 : 0;
+  // shape 7: add + sq1 constants
+  double lo1 = 0.0, hi1 = 0.0;
+  int k0 = 0, kr = 0, h1 = 0, r1 = 0;
+  if (addfork) {
+    code_range(e.q[1], lo1, hi1);
+    store_clamp(e.q[2], lo1, hi1);
+    int d0 = 0, dr = 0;
+    if (lo1 != 0.0 || hi1 < 0.0 || hi1 > 255.0 || !log2_exact(static_cast<double>(e.q[1].k), d0) ||
+        !log2_exact(static_cast<double>(e.ka), dr)) {
+      return false;
+    }
+    const int mm = std::min(d0, dr);
+    const double p0 = std::max(std::fabs(lo0), std::fabs(hi0));
+    // the reference's float add r0*s0 + c*s_res must be exact (|sum| < 2^24 units)
+    if (d0 - mm > 20 || dr - mm > 20 || p0 * std::ldexp(1.0, d0 - mm) + 128.0 * std::ldexp(1.0, dr - mm) >= 0x1p24) {
+      return false;
+    }
+    if (mm >= 0) {
+      if (d0 > 20 || dr > 20 || p0 * std::ldexp(1.0, d0) + 128.0 * std::ldexp(1.0, dr) >= 0x1p30) return false;
+      k0 = 1 << d0;
+      kr = 1 << dr;
+    } else {
+      if (-mm > 30) return false;
+      k0 = 1 << (d0 - mm);
+      kr = 1 << (dr - mm);
+      r1 = -mm;
+      h1 = 1 << (r1 - 1);
+    }
+  }
+  // the folded-bias table, cached per (stage, sq0 grid, code range)
+  struct Key {
+    int shape, ek;
+    double sxw, inv0, lo0, hi0;
+  } key{shape, ek, sxw, inv0, lo0, hi0};
+  std::string ks(reinterpret_cast<const char*>(&key), sizeof(key));
+  auto ck = std::make_pair(static_cast<int>(si), ks);
+  auto it = ctab_cache_.find(ck);
+  static const bool dbg = std::getenv("QUANTC_DEBUG_INT") != nullptr;
+  if (it == ctab_cache_.end()) {
+    std::shared_ptr<void> dev;  // null: some channel is irregular
+    const int O = st.O;
+    const int nmask = (O + 511) / 512;  // one bit per 16-channel chunk
+    // device layout: C[O], Tp[O], Tn[O], chunk mask words (kern::IntTable)
+    std::vector<int32_t> tab(static_cast<size_t>(3 * O + nmask), 0);
+    int32_t* C = tab.data();
+    int32_t* Tp = C + O;
+    int32_t* Tn = Tp + O;
+    uint32_t* mask = reinterpret_cast<uint32_t*>(Tn + O);
+    std::span<const float> bias;
+    if (st.bias_const >= 0) bias = plan_.steps()[static_cast<size_t>(st.bias_const)].node->payload->floats();
+    bool ok = O <= 8192;
+    std::string why;
+    int64_t cmax = 0;
+    const int64_t lo = static_cast<int64_t>(lo0), hi = static_cast<int64_t>(hi0);
+    for (int n = 0; n < O && ok; ++n) {
+      const float b = bias.empty() ? 0.0f : bias[static_cast<size_t>(n)];
+      // the reference's code of accumulator a (double sum + bias, one rounding
+      // to float, then round half away on sq0's grid)
+      auto f = [&](int64_t a) {
+        const float v = static_cast<float>(static_cast<double>(a) * sxw + static_cast<double>(b));
+        const double q = std::round(static_cast<double>(v) * inv0);
+        return static_cast<int64_t>(std::min(std::max(q, lo0), hi0));
+      };
+      int64_t c = 0, tp = std::numeric_limits<int32_t>::max(), tn = std::numeric_limits<int32_t>::min();
+      if (r0 > 0) {
+        const int64_t N = int64_t{1} << r0;
+        const double phi = -static_cast<double>(b) / sxw;  // exact (sxw a power of two)
+        if (!(std::fabs(phi) < 0x1p40)) {
+          ok = false;
+          why = "bias/s out of range";
+          break;
+        }
+        c = N / 2 - static_cast<int64_t>(std::ceil(phi));
+        // Breakpoint k >= 1 sits at ceil((k - 1/2)N + phi - D) with D = N * 2^(p-24)
+        // the fp32 half-spacing below k - 1/2 (binade p) in accumulator units;
+        // k <= 0 at floor((k - 1/2)N + phi + D') + 1.  Both equal the regular
+        // (k - 1/2)N + ceil(phi) when frac(phi) lies strictly between the
+        // largest D and 1 - D' (or phi is an integer and no code is negative):
+        // then only the extreme breakpoints are spot-checked.
+        const double fr = phi - std::floor(phi);
+        auto dmax = [&](double cabs) {
+          return cabs < 0.5 ? 0.0 : std::ldexp(1.0, r0 + std::ilogb(cabs) - 24);
+        };
+        const double dp = hi >= 1 ? dmax(static_cast<double>(hi) - 0.5) : 0.0;
+        const double dn = lo < 0 ? dmax(-static_cast<double>(lo) - 0.5) : 0.0;
+        const bool regular = dp < 0.25 && dn < 0.25 &&
+                             ((fr == 0.0 && lo >= 0) || (fr > 2.0 * dp && 1.0 - fr > 2.0 * dn));
+        if (regular) {
+          for (int64_t k : {lo + 1, hi}) {
+            if (k <= lo || k > hi) continue;
+            const int64_t A = k * N - c;
+            if (f(A) != k || f(A - 1) != k - 1) {
+              ok = false;
+              why = "regular breakpoint check failed";
+            }
+          }
+          cmax = std::max(cmax, c < 0 ? -c : c);
+          C[n] = static_cast<int32_t>(c * (int64_t{1} << sc0));
+          Tp[n] = std::numeric_limits<int32_t>::max();
+          Tn[n] = std::numeric_limits<int32_t>::min();
+          continue;
+        }
+        // exact breakpoints A_k (first a with f(a) >= k) next to the regular
+        // ones k*N - c: the float rounding of the conv value moves them by at
+        // most one, down for the large positive codes (bias just above a grid
+        // point) and up for the large negative ones (or all negative codes
+        // when half-way ties are reachable)
+        int64_t kp = hi + 1, kn = lo;  // shifted ranges [kp, hi] (-1), (lo, kn] (+1)
+        int64_t prev_shift = -2;
+        for (int64_t k = lo + 1; k <= hi && ok; ++k) {
+          int64_t a = k * N - c;
+          int guard = 0;
+          while (f(a - 1) >= k && guard++ < 4) --a;
+          while (f(a) < k && guard++ < 8) ++a;
+          const int64_t d = a - (k * N - c);
+          if (guard >= 8 || d < -1 || d > 1 || f(a) != k || f(a - 1) != k - 1) {
+            ok = false;
+            why = "breakpoint moved by more than one";
+            break;
+          }
+          // the shift pattern must be +1... 0... -1 (monotone in k)
+          if (d > prev_shift && prev_shift != -2) {
+            ok = false;
+            why = "non-monotone breakpoint shifts";
+            break;
+          }
+          prev_shift = d;
+          if (d == 1) kn = k;
+          if (d == -1 && kp > hi) kp = k;
+        }
+        if (!ok) break;
+        if (kp <= hi) tp = kp * N - c - 1;   // a >= Tp: one step earlier
+        if (kn > lo) tn = kn * N - c + 1;    // a <  Tn: one step later
+        if (kp <= hi || kn > lo) mask[n / 512] |= 1u << ((n / 16) % 32);
+        // the folded formula reproduces every breakpoint
+        auto g = [&](int64_t a) {
+          const int64_t x = a + c + (a >= tp ? 1 : 0) - (a < tn ? 1 : 0);
+          return std::min(std::max(x >> r0, lo), hi);
+        };
+        for (int64_t k = lo + 1; k <= hi && ok; ++k) {
+          const int64_t a = k * N - c + (k >= kp ? -1 : 0) + (k <= kn ? 1 : 0);
+          ok = g(a) == k && g(a - 1) == k - 1;
+        }
+        if (!ok) why = "folded formula mismatch";
+      } else {
+        c = static_cast<int64_t>(std::round(static_cast<double>(b) * inv0));
+        const int64_t alo = static_cast<int64_t>(std::floor((lo0 - static_cast<double>(c)) / m0)) - 1;
+        const int64_t ahi = static_cast<int64_t>(std::ceil((hi0 - static_cast<double>(c)) / m0)) + 1;
+        for (int64_t a = alo; a <= ahi && ok; ++a) {
+          ok = f(a) == std::min(std::max(a * m0 + c, lo), hi);
+        }
+        if (!ok) why = "coarse grid mismatch";
+      }
+      cmax = std::max(cmax, c < 0 ? -c : c);
+      C[n] = static_cast<int32_t>(c * (int64_t{1} << sc0));
+      Tp[n] = static_cast<int32_t>(std::min<int64_t>(tp, std::numeric_limits<int32_t>::max()));
+      Tn[n] = static_cast<int32_t>(std::max<int64_t>(tn, std::numeric_limits<int32_t>::min()));
+    }
+    if (ok) {
+      dev = engine::device_alloc_on(ST(), tab.size() * sizeof(int32_t));
+      // pageable source: staged before the call returns
+      ok_cuda(cudaMemcpyAsync(dev.get(), tab.data(), tab.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
+                              ST()));
+    }
+    if (dbg) {
+      int corr = 0;
+      for (int w = 0; w < nmask; ++w) corr += __builtin_popcount(mask[w]);
+      std::fprintf(stderr, "fold_integer stage %zu shape %d r0 %d m0 %d [%g, %g]: %s (%d chunks corrected)\n", si,
+                   shape, r0, m0, lo0, hi0, ok ? "ok" : why.c_str(), corr);
+    }
+    it = ctab_cache_.emplace(ck, std::make_pair(dev, cmax)).first;
+  }
+  // no int32 overflow of (a*m0 + C) * 2^sc0 for any accumulator this run can reach
+  if (!it->second.first ||
+      (acc_bound * m0 + static_cast<double>(it->second.second) + 1.0) * std::ldexp(1.0, sc0) >= 0x1p31) {
+    return false;
+  }
+  // shape 7: the second shift likewise made >= 2
+  if (addfork && r1 < 2) {
+    const int sc1 = 2 - r1;
+    k0 <<= sc1;
+    kr <<= sc1;
+    h1 <<= sc1;
+    r1 = 2;
+  }
+  if (addfork && std::max(std::fabs(lo0), std::fabs(hi0)) * k0 + 128.0 * kr + h1 >= 0x1p31) return false;
+  keep.push_back(it->second.first);
+  e.ctab = static_cast<const int32_t*>(it->second.first.get());
+  e.i_m0 = m0 << sc0;
+  e.i_r0 = r0 + sc0;
+  e.i_cs = 1 << sc0;
+  e.i_mh0 = static_cast<int32_t>(int64_t{1} << (32 - (r0 + sc0)));
+  e.i_lo0 = static_cast<int32_t>(lo0);
+  e.i_hi0 = static_cast<int32_t>(hi0);
+  e.i_k0 = k0;
+  e.i_kr = kr;
+  e.i_h1 = h1;
+  e.i_r1 = r1;
+  e.i_mh1 = addfork ? static_cast<int32_t>(int64_t{1} << (32 - r1)) : 0;
+  e.i_hi1 = static_cast<int32_t>(hi1);
+  return true;
 }
 
 void* FastPlan::buf(const Run& r, int vid) const {

@@ -76,6 +76,12 @@ class FastPlan {
   std::map<std::pair<int, std::string>, std::shared_ptr<void>> wcache_;
   size_t wcache_bytes_ = 0;
   void trim_weight_cache();
+  // integer-epilogue folds (fold_integer): per (stage, sq0 grid) the device
+  // table of folded biases, or null when some channel's breakpoints are
+  // irregular (the float shape then runs)
+  std::map<std::pair<int, std::string>, std::pair<std::shared_ptr<void>, int64_t>> ctab_cache_;
+  bool fold_integer(size_t si, int shape, double sxw, double acc_bound, kern::EpiConsts& e,
+                    std::vector<std::shared_ptr<void>>& keep);
 
   struct Run;
   void compile();

@@ -267,12 +267,28 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
   int2* ktab = reinterpret_cast<int2*>(tabs + 1);
   // shape kernels: bias pre-scaled into sq0's grid, btab[n] = bias[n] / s0
   float* btab = reinterpret_cast<float*>(ktab + (args.gather == 1 ? args.K / 16 : 0));
+  // integer shapes: per group 16 words of chunk-correction bits after the tables
+  uint32_t* cmask = reinterpret_cast<uint32_t*>(btab + args.n_tiles * BN * args.groups);
   if (args.prog.tables) load_tables(tabs, args.prog.tables);
   const int btab_n = args.n_tiles * BN;  // per group
   if (SHAPE != kShapeGeneric && SHAPE != kShapeInt) {
     for (int i = threadIdx.x; i < args.groups * btab_n; i += blockDim.x) {
       const int grp = i / btab_n;
       const int n = i - grp * btab_n;
+      if constexpr (shape_is_int_fold(SHAPE)) {
+        // integer shapes: the host-verified folded bias ctab[n] (int32)
+        const int32_t* ct = args.epi.ctab;
+        if constexpr (NG > 1) {
+          if (grp) ct = gr.epi[grp - 1].ctab;
+        }
+        reinterpret_cast<int32_t*>(btab)[i] = n < args.N ? __ldg(ct + n) : 0;
+        // the chunk-correction mask (16 words per group) after the tables
+        if (n < 16) {
+          const int nmask = (args.N + 511) / 512;
+          cmask[grp * 16 + n] = n < nmask ? static_cast<uint32_t>(__ldg(ct + 3 * args.N + n)) : 0u;
+        }
+        continue;
+      }
       float inv0 = args.epi.inv0;
       if constexpr (NG > 1) {
         if (grp) inv0 = gr.epi[grp - 1].inv0;
@@ -638,6 +654,34 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
             ie.y[flat] = int_epi_value(ie, static_cast<int32_t>(d[j]), o, flat);
           }
         }
+      } else if constexpr (shape_is_int_fold(SHAPE)) {
+        // integer shapes 10/11: the chain on the int32 accumulators (fused.cuh run_int_epi)
+        const EpiConsts* ep = &args.epi;
+        if constexpr (NG > 1) {
+          if (grp) ep = &gr.epi[grp - 1];
+        }
+        const EpiConsts e = *ep;
+        const int32_t* ctg = reinterpret_cast<const int32_t*>(btab) + grp * btab_n;
+        const uint32_t* cmg = cmask + grp * 16;
+        const int32_t* tpg = e.ctab + args.N;  // Tp[O], Tn[O] (global)
+#pragma unroll 1
+        for (int c = part; c < NCHUNK; c += PARTS) {
+          const int c0 = c * EW;
+          uint32_t d[EW];
+          tmem_ld<EW>(tbase + c0, d);
+          tmem_wait(d);
+          const int n = n0 + c0;
+          if (n < args.N) {
+            // warp-uniform: every lane of the warp works on the same channels
+            uint32_t cm;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cm) : "r"(su32(cmg + (n >> 9))));
+            if ((cm >> ((n >> 4) & 31)) & 1u) {
+              run_int_epi<SHAPE, true>(d, ctg + n, e, io, c0, tpg + n, args.N);
+            } else {
+              run_int_epi<SHAPE, false>(d, ctg + n, e, io, c0, tpg + n, args.N);
+            }
+          }
+        }
       } else if constexpr (SHAPE != kShapeGeneric) {
         // straight-line shapes: host-checked preconditions (classify_shape)
         // — O % 16 == 0, all I/O through slots (rows >= M and columns >= O
@@ -942,7 +986,7 @@ int smem_fixed(const TcArgs& a, int bn, int sets, bool shape) {
   return 1024 + sets * (a.n_out + a.has_res) * BM * bn + (2 * MAX_STAGES + 10) * 8 + 16 +
          static_cast<int>(sizeof(StageTables)) + 64 +
          (a.gather == 1 ? a.K / 16 * static_cast<int>(sizeof(int2)) : 0) +
-         (shape ? ((a.N + bn - 1) / bn) * bn * 4 * a.groups : 0);
+         (shape ? ((a.N + bn - 1) / bn) * bn * 4 * a.groups + 64 * a.groups : 0);
 }
 
 // pipeline depth that fits next to `fixed` bytes (capped by what the K loop uses)
@@ -1047,6 +1091,12 @@ void launch_bn(const TcMapsT<kMaxGroups>* maps, const TcGroupsT<kMaxGroups>* grp
       break;
     case kShapeSqF32:
       launch_tc<BN, kShapeSqF32>(maps, grp, a, s);
+      break;
+    case kShapeSqStoreInt:
+      launch_tc<BN, kShapeSqStoreInt>(maps, grp, a, s);
+      break;
+    case kShapeAddForkInt:
+      launch_tc<BN, kShapeAddForkInt>(maps, grp, a, s);
       break;
     case kShapeInt:
       launch_tc<BN, kShapeInt>(maps, grp, a, s);

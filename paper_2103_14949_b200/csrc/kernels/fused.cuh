@@ -480,6 +480,86 @@ __device__ __forceinline__ void run_shape_epi(float (&x)[16], const EpiConsts& e
   }
 }
 
+// ---- integer shapes 10/11 (fused.h EpiConsts i_*) ------------------------------
+// four int32 codes -> four bytes, each saturated to [0, 255] (I2IP): the low
+// side of a non-negative code clamp comes for free
+__device__ __forceinline__ uint32_t pack_sat_u8(int32_t v0, int32_t v1, int32_t v2, int32_t v3) {
+  uint32_t hi, r;
+  asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(hi) : "r"(v3), "r"(v2), "r"(0));
+  asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(v1), "r"(v0), "r"(hi));
+  return r;
+}
+
+// byte K of w as a sign-extended int32 (PRMT sign-replicate selector)
+template <int K>
+__device__ __forceinline__ int32_t sbyte(uint32_t w) {
+  return static_cast<int32_t>(prmt_imm<K | ((8 | K) * 0x1110u)>(w, 0u));
+}
+
+// d: the 16 int32 accumulators of this thread's chunk; ct: the channels'
+// folded bias (shared memory, 16-byte aligned).  Host preconditions
+// (fastplan fold_integer): sq0 non-negative (shape 10) or signed (shape 11)
+// with every breakpoint of every channel verified, sq1 non-negative and the
+// add exact in fp32, identity stores.
+// CORR: some channel of the chunk has breakpoints moved by the float
+// rounding of the conv value (fastplan fold_integer): tp[j] / tp[O + j] are
+// its thresholds (global, read-only): a >= Tp counts one step early, a < Tn
+// one step late
+template <int SHAPE, bool CORR>
+__device__ __forceinline__ void run_int_epi(const uint32_t (&d)[16], const int32_t* ct,
+                                            const EpiConsts& e, const TileIo& io, int cl,
+                                            const int32_t* tp, int O) {
+  int32_t r[16];
+#pragma unroll
+  for (int j = 0; j < 16; j += 4) {
+    const int4 c4 = lds128(static_cast<uint32_t>(__cvta_generic_to_shared(ct + j)));
+    int32_t cc[4] = {c4.x, c4.y, c4.z, c4.w};
+    if constexpr (CORR) {
+      const int4 p4 = __ldg(reinterpret_cast<const int4*>(tp + j));
+      const int4 n4 = __ldg(reinterpret_cast<const int4*>(tp + O + j));
+      const int32_t pp[4] = {p4.x, p4.y, p4.z, p4.w};
+      const int32_t nn[4] = {n4.x, n4.y, n4.z, n4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int32_t a = static_cast<int32_t>(d[j + i]);
+        cc[i] += ((a >= pp[i] ? 1 : 0) - (a < nn[i] ? 1 : 0)) * e.i_cs;
+      }
+    }
+    // (a multiply-high on the FMA pipe instead of the shift measured slower:
+    // 1180 vs 1073 us for the step's add-forks)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      r[j + i] = (static_cast<int32_t>(d[j + i]) * e.i_m0 + cc[i]) >> e.i_r0;
+    }
+  }
+  if constexpr (SHAPE == kShapeSqStoreInt) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) r[j] = min(r[j], e.i_hi0);
+  } else {
+    const int4 raw = lds128(tile_addr(io, e.slot_res, cl));
+    const uint32_t w[4] = {static_cast<uint32_t>(raw.x), static_cast<uint32_t>(raw.y),
+                           static_cast<uint32_t>(raw.z), static_cast<uint32_t>(raw.w)};
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int32_t c0 = min(max(r[j], e.i_lo0), e.i_hi0);
+      int32_t c;
+      switch (j & 3) {
+        case 0: c = sbyte<0>(w[j >> 2]); break;
+        case 1: c = sbyte<1>(w[j >> 2]); break;
+        case 2: c = sbyte<2>(w[j >> 2]); break;
+        default: c = sbyte<3>(w[j >> 2]); break;
+      }
+      r[j] = min((c0 * e.i_k0 + c * e.i_kr + e.i_h1) >> e.i_r1, e.i_hi1);
+    }
+  }
+  const int4 packed = make_int4(static_cast<int>(pack_sat_u8(r[0], r[1], r[2], r[3])),
+                                static_cast<int>(pack_sat_u8(r[4], r[5], r[6], r[7])),
+                                static_cast<int>(pack_sat_u8(r[8], r[9], r[10], r[11])),
+                                static_cast<int>(pack_sat_u8(r[12], r[13], r[14], r[15])));
+  sts128(tile_addr(io, e.slot_out[0], cl), packed);
+  if (SHAPE == kShapeAddForkInt && e.slot_out[1] >= 0) sts128(tile_addr(io, e.slot_out[1], cl), packed);
+}
+
 // DEPTH: number of PUSH slots the program may use (host-checked)
 template <int W, int DEPTH>
 __device__ __forceinline__ void run_prog(float (&v)[W], int64_t m, int n0, int nvalid,

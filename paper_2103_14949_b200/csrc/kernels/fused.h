@@ -154,6 +154,21 @@ struct EpiConsts {
   float sat_half[2];  // 0.5 / P_i
   float sat_p[2];     // P_i
   float sat_top[2];   // highest code (r-domain) or M + highest code (T-domain)
+  // integer shapes 10/11 (fastplan fold_integer): the whole chain on the
+  // int32 accumulator, no float conversion.
+  //   r0 = clamp((acc * i_m0 + ctab[n]) >> i_r0, i_lo0, i_hi0)        (sq0)
+  //   y  = clamp((r0 * i_k0 + c * i_kr + i_h1) >> i_r1, 0, i_hi1)     (add + sq1, shape 11)
+  // ctab[n] is the channel's bias folded into sq0's grid; the host verified
+  // every code breakpoint of every channel against the reference arithmetic.
+  // Table layout (int32): C[O], Tp[O], Tn[O], then one bit per 16-channel
+  // chunk (ceil(O/512) words) marking chunks with a channel whose breakpoints
+  // the fp32 rounding of the conv value moved by one: there
+  //   r0 = clamp((acc*i_m0 + C[n] + (acc >= Tp[n]) - (acc < Tn[n])) >> i_r0, ..)
+  const int32_t* ctab;
+  int32_t i_m0, i_r0, i_lo0, i_hi0;
+  int32_t i_k0, i_kr, i_h1, i_r1, i_hi1;
+  int32_t i_cs;          // one breakpoint correction in the (scaled) C domain
+  int32_t i_mh0, i_mh1;  // 2^(32 - i_r0), 2^(32 - i_r1) (multiply-high form; unused)
 };
 
 // Straight-line epilogues for the program shapes that dominate CNN graphs
@@ -174,9 +189,16 @@ struct EpiConsts {
 //      chunk's columns past O are masked)
 //   8: integer conv/dense of a realized graph (IntEpi): exact int64 epilogue,
 //      accumulator-dtype clamp / trap, optional fused requantize, int32 NCHW out
+//  10: shape 6 on the integer accumulator (EpiConsts i_*): sq0 as one
+//      multiply-add, one shift and a saturating byte pack
+//  11: shape 7 on the integer accumulator: sq0, the residual add and sq1 as
+//      exact integer arithmetic on codes (every scale is a power of two)
 enum : int { kShapeGeneric = 0, kShapeStore = 1, kShapeSqStore = 2, kShapeAddFork = 3,
              kShapeAdd = 4, kShapeAddF32 = 5, kShapeSqStoreId = 6, kShapeAddForkId = 7,
-             kShapeInt = 8, kShapeSqF32 = 9 };
+             kShapeInt = 8, kShapeSqF32 = 9, kShapeSqStoreInt = 10, kShapeAddForkInt = 11 };
+QC_HD constexpr bool shape_is_int_fold(int s) {
+  return s == kShapeSqStoreInt || s == kShapeAddForkInt;
+}
 
 // Integer epilogue (reference interpreter.cpp:238-309 then :464-482):
 //   v = acc - zp0 * wsum[o] + bias[o]          (acc = sum_k x'*w', w' = w - zp1)
