@@ -286,6 +286,63 @@ def _events(torch):
     return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
 
+def config_legs(b, torch, stream, batch):
+    """The other BASELINE configs as bounded side legs (device-timed on the
+    engine stream; one GPU).  Each: calibrate on its images, bind, then time a
+    losses() call over a few candidates.
+
+    C2  ResNet-18 @224, batch 64, int8_int32, pow2 thresholds -> fused tcgen05 path
+    C3  MobileNetV2 (width 1.0) @224, arm_vmlal_like, native depthwise convs
+        (conv2d groups) -> exact FP64 engine (grouped convs are not fused)
+    C5  Inception-v3-style @299 (native concat / avg_pool2d), int8_int32
+        -> exact FP64 engine
+    R50 under the reference's DEFAULT thresholds (quantile 0.99, pow2 off,
+        calibration.hpp:71-76) -> the exact FP64 engine (the fused int8 engine
+        is bit-exact only under power-of-two scales)"""
+    legs = {}
+    plans = [
+        ("c2_resnet18", F.resnet(18), "int8_int32", batch, True, 0.999, 20),
+        ("c3_mobilenet_v2", F.mobilenet_v2(image=224, width=1.0, classes=1000, native=True),
+         "arm_vmlal_like", 16, True, 0.999, 4),
+        ("c5_inception_v3", F.inception_v3(image=299, width=16, modules=2, head="gap", native=True),
+         "int8_int32", 8, True, 0.999, 4),
+        ("r50_default_thresholds", F.resnet(50), "int8_int32", 16, False, 0.99, 4),
+    ]
+    for name, model, spec_name, n, pow2, qtl, k in plans:
+        try:
+            data = model.data(n, seed=9)
+            g = b.graph(model.doc, model.blob)
+            spec = b.parse_spec(F.spec_fixture(spec_name))
+            topo = b.generate_topology(g, spec)
+            sim = b.insert_simulated_quantize(g, topo)
+            ds = b.dataset(data)
+            st = b.collect_stats(g, ds, 2048, b.simulated_edge_indices(g, topo))
+            thr = st.estimate_thresholds("quantile", quantile=qtl, pow2=pow2)
+            ev = b.evaluator(sim, spec, topo, thr, st, ds, min_bit=4 if spec_name != "arm_vmlal_like" else 8)
+            sp = ev.space()
+            cands = candidates(sp, k + 1)
+            why = b.fused_status(sim, ev.bind(cands[0]))
+            engine = "fused int8 tcgen05" if not why else f"exact FP64 engine ({why[:120]})"
+            ev.losses(cands[:1])
+            torch.cuda.synchronize()
+            e0, e1 = _events(torch)
+            e0.record(stream)
+            ev.losses(cands[1:])
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / k
+            legs[name] = {"images": n, "image": data.shape[-1], "spec": spec_name,
+                          "thresholds": f"quantile {qtl}, pow2 {'on' if pow2 else 'off'}",
+                          "ms_per_candidate": ms, "images_per_s": n / (ms / 1e3),
+                          "candidates_per_s": 1e3 / ms, "candidates": k,
+                          "gmac_per_image": model.macs_per_sample() / 1e9,
+                          "engine": engine}
+            del ev, ds, st, sim
+        except Exception as e:  # a side leg never sinks the headline line
+            legs[name] = {"error": str(e)[:300]}
+    return legs
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -299,6 +356,7 @@ def main():
                     help="skip the realized-int8 eval_int leg")
     ap.add_argument("--no-search", action="store_true", help="skip the search legs")
     ap.add_argument("--no-traffic", action="store_true", help="skip the ncu traffic child")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C2/C3/C5 side legs")
     ap.add_argument("--traffic-probe", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--calib-images", type=int, default=128,
                     help="C4 leg: calibration images per GPU (1024 at 8 GPUs)")
@@ -565,6 +623,10 @@ def main():
                                 "layers (the reference Tensor semantics)"}
         del R, simb, gbatch, mb
 
+    configs = None
+    if not args.no_configs and world == 1:
+        configs = config_legs(b, torch, stream, B)
+
     # ---- e2e: public C-ABI call with HOST buffers: predict_top1 of the sim
     # graph under a candidate binding (uploads images + plan, downloads preds)
     e2e_steps = max(3, min(10, args.steps))
@@ -624,6 +686,7 @@ def main():
         "search": search,
         "calibration": calib,
         "realized_int8": realized,
+        "configs": configs,
         "gpu_launches": int(launches),
         "roofline": {"bound": "tensor", "achieved": tops, "peak": int8_peak, "unit": "TFLOP/s",
                      "frac": tops / int8_peak if int8_peak else None,

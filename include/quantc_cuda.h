@@ -50,6 +50,20 @@ int qcu_conv2d_f64acc(const float* x, const float* w, const float* bias, float* 
                       int H, int W, int O, int KH, int KW, int sh, int sw, int ph, int pw,
                       void* stream);
 
+/* Op-set extension (no reference counterpart — the
+ * semantics are those of the exact rewrites the reference does run,
+ * fixtures.py / tests/test_rewrites.py):
+ *   qcu_conv2d_grouped_f64acc  conv2d with `groups` (weight [O][C/G][KH][KW]),
+ *                              the interpreter.cpp:210-236 double accumulator
+ *                              over the group's channels
+ *   qcu_avg_pool2d_f32         double sum of x * fl32(1/(KH*KW)) over in-bounds
+ *                              taps (count_include_pad), one rounding */
+int qcu_conv2d_grouped_f64acc(const float* x, const float* w, const float* bias, float* y, int N,
+                              int C, int H, int W, int O, int KH, int KW, int sh, int sw, int ph,
+                              int pw, int groups, void* stream);
+int qcu_avg_pool2d_f32(const float* x, float* y, int N, int C, int H, int W, int KH, int KW,
+                       int sh, int sw, int ph, int pw, void* stream);
+
 /* int32-storage operands; acc_dtype QC_I16/QC_I32; trap != 0 reports the
  * lowest overflowing flat index through *overflow_flat (-1 if none). */
 int qcu_conv2d_int(const int32_t* x, const int32_t* w, const int32_t* bias, int32_t* y, int N,

@@ -117,27 +117,66 @@ int orc_kl_best_index(const int64_t* counts, int bins, int target_bit, double* b
   return best_i;
 }
 
-/* interpreter.cpp:218-234 */
-void orc_conv2d_f64acc(const float* x, const float* w, const float* bias, float* y, int N,
-                       int C, int H, int W, int O, int KH, int KW, int sh, int sw, int ph,
-                       int pw) {
+/* interpreter.cpp:218-234, generalised to groups (op-set extension: output
+ * channel o reads the C/G input channels of group o / (O/G); weight
+ * [O][C/G][KH][KW]).  groups == 1 is the reference loop verbatim. */
+void orc_conv2d_grouped_f64acc(const float* x, const float* w, const float* bias, float* y,
+                               int N, int C, int H, int W, int O, int KH, int KW, int sh, int sw,
+                               int ph, int pw, int groups) {
   int OH = (H + 2 * ph - KH) / sh + 1, OW = (W + 2 * pw - KW) / sw + 1;
+  int Cg = C / groups, Og = O / groups;
   for (int64_t n = 0; n < N; ++n)
     for (int64_t o = 0; o < O; ++o)
       for (int64_t oh = 0; oh < OH; ++oh)
         for (int64_t ow = 0; ow < OW; ++ow) {
           double acc = 0.0;
-          for (int64_t c = 0; c < C; ++c)
+          int64_t cb = (o / Og) * Cg;
+          for (int64_t c = 0; c < Cg; ++c)
             for (int64_t kh = 0; kh < KH; ++kh)
               for (int64_t kw = 0; kw < KW; ++kw) {
                 int64_t ih = oh * sh - ph + kh, iw = ow * sw - pw + kw;
                 if (ih < 0 || ih >= H || iw < 0 || iw >= W) continue;
-                acc += (double)x[((n * C + c) * H + ih) * W + iw] *
-                       (double)w[((o * C + c) * KH + kh) * KW + kw];
+                acc += (double)x[((n * C + cb + c) * H + ih) * W + iw] *
+                       (double)w[((o * Cg + c) * KH + kh) * KW + kw];
               }
           if (bias) acc += (double)bias[o];
           y[((n * O + o) * OH + oh) * OW + ow] = (float)acc;
         }
+}
+
+void orc_conv2d_f64acc(const float* x, const float* w, const float* bias, float* y, int N,
+                       int C, int H, int W, int O, int KH, int KW, int sh, int sw, int ph,
+                       int pw) {
+  orc_conv2d_grouped_f64acc(x, w, bias, y, N, C, H, W, O, KH, KW, sh, sw, ph, pw, 1);
+}
+
+/* avg_pool2d (op-set extension): the reference conv2d loop on the constant
+ * depthwise rewrite — double sum over in-bounds taps of x * fl32(1/(KH*KW)) */
+void orc_avg_pool2d(const float* x, float* y, int N, int C, int H, int W, int KH, int KW, int sh,
+                    int sw, int ph, int pw) {
+  int OH = (H + 2 * ph - KH) / sh + 1, OW = (W + 2 * pw - KW) / sw + 1;
+  double wk = (double)(float)(1.0 / ((double)KH * KW));
+  for (int64_t nc = 0; nc < (int64_t)N * C; ++nc)
+    for (int64_t oh = 0; oh < OH; ++oh)
+      for (int64_t ow = 0; ow < OW; ++ow) {
+        double acc = 0.0;
+        for (int64_t kh = 0; kh < KH; ++kh)
+          for (int64_t kw = 0; kw < KW; ++kw) {
+            int64_t ih = oh * sh - ph + kh, iw = ow * sw - pw + kw;
+            if (ih < 0 || ih >= H || iw < 0 || iw >= W) continue;
+            acc += (double)x[(nc * H + ih) * W + iw] * wk;
+          }
+        y[(nc * OH + oh) * OW + ow] = (float)acc;
+      }
+}
+
+/* interpreter.cpp global_avg_pool2d: sequential double sum / (double)(H*W) */
+void orc_global_avg_pool2d(const float* x, float* y, int NC, int HW) {
+  for (int64_t i = 0; i < NC; ++i) {
+    double acc = 0.0;
+    for (int64_t k = 0; k < HW; ++k) acc += (double)x[i * HW + k];
+    y[i] = (float)(acc / (double)HW);
+  }
 }
 
 /* interpreter.cpp:244-263 */

@@ -27,6 +27,12 @@ double orc_threshold_quantile(const int64_t* counts, int bins, double absmax, do
 int orc_kl_best_index(const int64_t* counts, int bins, int target_bit, double* best_kl);
 
 /* interpreter.cpp:210-236 (dense = conv with H=W=KH=KW=1) */
+void orc_conv2d_grouped_f64acc(const float* x, const float* w, const float* bias, float* y,
+                               int N, int C, int H, int W, int O, int KH, int KW, int sh, int sw,
+                               int ph, int pw, int groups);
+void orc_avg_pool2d(const float* x, float* y, int N, int C, int H, int W, int KH, int KW, int sh,
+                    int sw, int ph, int pw);
+void orc_global_avg_pool2d(const float* x, float* y, int NC, int HW);
 void orc_conv2d_f64acc(const float* x, const float* w, const float* bias, float* y, int N,
                        int C, int H, int W, int O, int KH, int KW, int sh, int sw, int ph,
                        int pw);

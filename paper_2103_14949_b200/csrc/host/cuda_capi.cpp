@@ -109,6 +109,27 @@ int qcu_conv2d_f64acc(const float* x, const float* w, const float* bias, float* 
   });
 }
 
+int qcu_conv2d_grouped_f64acc(const float* x, const float* w, const float* bias, float* y, int N,
+                              int C, int H, int W, int O, int KH, int KW, int sh, int sw, int ph,
+                              int pw, int groups, void* stream) {
+  return wrap([&] {
+    if (groups < 1 || C % groups != 0 || O % groups != 0) {
+      throw std::invalid_argument("qcu_conv2d_grouped_f64acc: groups must divide C and O");
+    }
+    kern::ConvShape cs = shape(N, C, H, W, O, KH, KW, sh, sw, ph, pw);
+    cs.G = groups;
+    kern::conv2d_f64acc(x, w, bias, y, cs, st(stream));
+  });
+}
+
+int qcu_avg_pool2d_f32(const float* x, float* y, int N, int C, int H, int W, int KH, int KW,
+                       int sh, int sw, int ph, int pw, void* stream) {
+  return wrap([&] {
+    const int OH = (H + 2 * ph - KH) / sh + 1, OW = (W + 2 * pw - KW) / sw + 1;
+    kern::avgpool_f32(x, y, N, C, H, W, OH, OW, KH, KW, sh, sw, ph, pw, st(stream));
+  });
+}
+
 int qcu_conv2d_int(const int32_t* x, const int32_t* w, const int32_t* bias, int32_t* y, int N,
                    int C, int H, int W, int O, int KH, int KW, int sh, int sw, int ph, int pw,
                    int64_t zp0, int64_t zp1, int acc_dtype, int trap, int64_t* overflow_flat,

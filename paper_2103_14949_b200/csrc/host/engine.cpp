@@ -61,7 +61,9 @@ std::vector<int64_t> infer_shape(const Node& n, const std::vector<const std::vec
       return n.payload->shape();
     case OpKind::kConv2d: {
       const auto &d = need(0), &w = need(1);
-      if (d.size() != 4 || w.size() != 4 || d[1] != w[1]) {
+      const int64_t groups = n.attr_or<int64_t>("groups", 1);
+      if (d.size() != 4 || w.size() != 4 || groups < 1 || w[0] % groups != 0 ||
+          d[1] != w[1] * groups) {
         throw EvalError("conv2d shape mismatch at node " + std::to_string(n.id));
       }
       Attr2 st = pair_attr(n, "strides", {1, 1}), pd = pair_attr(n, "padding", {0, 0});
@@ -89,6 +91,24 @@ std::vector<int64_t> infer_shape(const Node& n, const std::vector<const std::vec
     case OpKind::kGlobalAvgPool2d: {
       const auto& d = need(0);
       return {d[0], d[1], 1, 1};
+    }
+    case OpKind::kAvgPool2d: {
+      const auto& d = need(0);
+      auto k = n.attr<std::vector<int64_t>>("pool_size");
+      Attr2 st = pair_attr(n, "strides", {static_cast<int>(k[0]), static_cast<int>(k[1])});
+      Attr2 pd = pair_attr(n, "padding", {0, 0});
+      return {d[0], d[1], (d[2] + 2 * pd.a - k[0]) / st.a + 1, (d[3] + 2 * pd.b - k[1]) / st.b + 1};
+    }
+    case OpKind::kConcat: {
+      std::vector<int64_t> out = need(0);
+      for (size_t i = 1; i < in.size(); ++i) {
+        const auto& d = need(i);
+        if (d.size() != 4 || out.size() != 4 || d[0] != out[0] || d[2] != out[2] || d[3] != out[3]) {
+          throw EvalError("concat operand shapes differ at node " + std::to_string(n.id));
+        }
+        out[1] += d[1];
+      }
+      return out;
     }
     case OpKind::kFlatten: {
       const auto& d = need(0);
@@ -417,6 +437,7 @@ struct Runner {
     for (size_t i = 0; i < steps.size(); ++i) {
       const auto& st = steps[i];
       if (st.node->op != OpKind::kConv2d && st.node->op != OpKind::kDense) continue;
+      if (st.node->attr_or<int64_t>("groups", 1) != 1) continue;  // grouped: FP64 / int64 kernels
       if (st.in.size() < 2 || st.in[0] < 0 || st.in[1] < 0) continue;
       const int d = st.in[0], w = st.in[1];
       const auto &sd = steps[static_cast<size_t>(d)], &sw = steps[static_cast<size_t>(w)];
@@ -859,6 +880,7 @@ void Runner::exec_conv(int i, bool dense) {
     cs.sw = strd.b;
     cs.ph = pad.a;
     cs.pw = pad.b;
+    cs.G = static_cast<int>(n.attr_or<int64_t>("groups", 1));
   }
   if (d.dtype.is_float()) {
     if (!w.dtype.is_float() || (b && !b->dtype.is_float())) {
@@ -873,8 +895,9 @@ void Runner::exec_conv(int i, bool dense) {
   }
   DType acc = acc_dtype_of(n);
   auto zps = n.attr_or<std::vector<int64_t>>("in_zero_points", {0, 0});
-  if (exec_conv_int_tc(i, dense, cs, d, w, b, acc, zps)) return;
-  if (exec_conv_int_simt(i, cs, d, w, b, acc, zps)) return;
+  // grouped integer convs run on the exact int64 kernel
+  if (kern::conv_groups(cs) == 1 && exec_conv_int_tc(i, dense, cs, d, w, b, acc, zps)) return;
+  if (kern::conv_groups(cs) == 1 && exec_conv_int_simt(i, cs, d, w, b, acc, zps)) return;
   DevTensor y = out_like(i, acc);
   unsigned long long* trap = trap_ptr();
   kern::conv2d_int(d.i(), w.i(), b ? b->i() : nullptr, y.i(), cs, zps[0], zps[1],
@@ -1021,6 +1044,54 @@ void Runner::exec(int i) {
       DevTensor a = in(i, 0);
       a.shape = plan.shape(i);
       vals[static_cast<size_t>(i)] = a;
+      return;
+    }
+    case OpKind::kAvgPool2d: {
+      const DevTensor& x = in(i, 0);
+      if (!x.dtype.is_float()) {
+        throw EvalError("integer avg_pool2d is not supported (node " + std::to_string(n.id) + ")");
+      }
+      const auto& xs = plan.shape(st.in[0]);
+      const auto& os = plan.shape(i);
+      auto k = n.attr<std::vector<int64_t>>("pool_size");
+      Attr2 strd = pair_attr(n, "strides", {static_cast<int>(k[0]), static_cast<int>(k[1])});
+      Attr2 pad = pair_attr(n, "padding", {0, 0});
+      DevTensor y = out_like(i, f32);
+      kern::avgpool_f32(x.f(), y.f(), static_cast<int>(xs[0] * N(st.in[0])), static_cast<int>(xs[1]),
+                        static_cast<int>(xs[2]), static_cast<int>(xs[3]), static_cast<int>(os[2]),
+                        static_cast<int>(os[3]), static_cast<int>(k[0]), static_cast<int>(k[1]),
+                        strd.a, strd.b, pad.a, pad.b, S());
+      vals[static_cast<size_t>(i)] = y;
+      return;
+    }
+    case OpKind::kConcat: {
+      // every operand is [n, c_i, H, W] per sample: copy each into its channel
+      // range of the [n, sum c_i, H, W] output (batched operands only; an
+      // unbatched operand broadcasts over the batch)
+      const DevTensor& x0 = in(i, 0);
+      DevTensor y = out_like(i, x0.dtype);
+      const auto& os = plan.shape(i);
+      const int64_t hw = os[2] * os[3];
+      const int64_t outer = os[1] * hw;
+      const int rows = static_cast<int>(os[0] * N(i));
+      int64_t off = 0;
+      for (size_t p = 0; p < st.in.size(); ++p) {
+        const DevTensor& x = in(i, static_cast<int>(p));
+        if (x.dtype.is_float() != x0.dtype.is_float()) {
+          throw EvalError("concat mixes float and integer operands at node " + std::to_string(n.id));
+        }
+        const int64_t inner = plan.shape(st.in[p])[1] * hw;
+        if (plan.batched(st.in[p]) || N(i) == 1) {
+          kern::concat_words(x.buf.get(), y.buf.get(), rows, inner, outer, off, S());
+        } else {
+          for (int r = 0; r < rows; ++r) {
+            kern::concat_words(x.buf.get(), static_cast<uint32_t*>(y.buf.get()) + r * outer, 1,
+                               inner, outer, off, S());
+          }
+        }
+        off += inner;
+      }
+      vals[static_cast<size_t>(i)] = y;
       return;
     }
     case OpKind::kSimulatedQuantize:

@@ -253,6 +253,10 @@ struct Builder {
     bool zero = false;
     switch (ny.op) {
       case OpKind::kConv2d: {
+        if (ny.attr_or<int64_t>("groups", 1) != 1) {
+          fail("grouped conv2d runs on the exact engine");
+          return false;
+        }
         if (port != 0) {
           fail("conv2d weight is not a constant");
           return false;
@@ -863,6 +867,10 @@ void FastPlan::compile() {
       }
       case OpKind::kConv2d:
       case OpKind::kDense: {
+        if (n.attr_or<int64_t>("groups", 1) != 1) {
+          fail("grouped conv2d runs on the exact engine");
+          continue;
+        }
         st->kind = Stage::kGemm;
         st->dense = n.op == OpKind::kDense;
         const auto& in = steps[i].in;

@@ -14,6 +14,17 @@
 // owning a TM x TN register tile (rows ty+16i, cols tx+16j: conflict-free
 // shared-memory reads), BK = 8, double-buffered shared memory with register
 // prefetch of the next im2col/weight slice.  K is never split (order!).
+//
+// Grouped convs (op-set extension): grid.z = group; the
+// GEMM runs over the group's C/G input channels and O/G output channels.
+// Depthwise-like layers (O/G < 16, where a 16-wide channel tile would idle)
+// take the direct kernel: one thread per output, the same (c, kh, kw) DFMA
+// chain.  Both are what the reference computes on the block-diagonal dense
+// rewrite of the layer (fixtures.py _depthwise; tests/test_rewrites.py): the
+// off-group zero weights add signed zeros to an accumulator that is never
+// -0.0, so skipping them leaves every partial sum unchanged.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace quantc::kern {
@@ -36,10 +47,14 @@ __global__ void __launch_bounds__(256) conv_f64_kernel(const float* __restrict__
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
   const int64_t M = static_cast<int64_t>(cs.N) * cs.OH * cs.OW;
-  const int K = cs.C * cs.KH * cs.KW;
+  const int G = conv_groups(cs);
+  const int Cg = cs.C / G, Og = cs.O / G;
+  const int grp = blockIdx.z;
+  const int K = Cg * cs.KH * cs.KW;
   const int khw = cs.KH * cs.KW;
   const int64_t m0 = static_cast<int64_t>(blockIdx.x) * BM;
-  const int n0 = blockIdx.y * BN;
+  const int n0 = blockIdx.y * BN;  // within the group
+  w += static_cast<int64_t>(grp) * Og * K;
 
   // A loader: thread owns pixel column am = tid % BM and rows ak + (256/BM)*r
   const int am = tid % BM;
@@ -55,7 +70,7 @@ __global__ void __launch_bounds__(256) conv_f64_kernel(const float* __restrict__
     ih0 = (rem / cs.OW) * cs.sh - cs.ph;
     iw0 = (rem % cs.OW) * cs.sw - cs.pw;
   }
-  const float* ximg = x + static_cast<int64_t>(img) * cs.C * cs.H * cs.W;
+  const float* ximg = x + (static_cast<int64_t>(img) * cs.C + static_cast<int64_t>(grp) * Cg) * cs.H * cs.W;
 
   auto load_a = [&](int k0, double (&ra)[A_PER]) {
 #pragma unroll
@@ -83,7 +98,7 @@ __global__ void __launch_bounds__(256) conv_f64_kernel(const float* __restrict__
       const int bk = e % BK, bn = e / BK;
       const int k = k0 + bk, o = n0 + bn;
       double v = 0.0;
-      if (bn < BN && k < K && o < cs.O) v = static_cast<double>(__ldg(w + static_cast<int64_t>(o) * K + k));
+      if (bn < BN && k < K && o < Og) v = static_cast<double>(__ldg(w + static_cast<int64_t>(o) * K + k));
       rb[r] = v;
     }
   };
@@ -140,8 +155,9 @@ __global__ void __launch_bounds__(256) conv_f64_kernel(const float* __restrict__
     const int64_t im = m / ohw, pix = m % ohw;
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
-      const int o = n0 + tx + 16 * j;
-      if (o >= cs.O) continue;
+      const int ol = n0 + tx + 16 * j;
+      if (ol >= Og) continue;
+      const int o = grp * Og + ol;
       double v = acc[i][j];
       if (bias) v = __dadd_rn(v, static_cast<double>(__ldg(bias + o)));
       y[(im * cs.O + o) * ohw + pix] = __double2float_rn(v);
@@ -149,12 +165,52 @@ __global__ void __launch_bounds__(256) conv_f64_kernel(const float* __restrict__
   }
 }
 
+// direct grouped conv: one thread per output element (n, o, oh, ow), NCHW
+// order (consecutive threads: consecutive ow, coalesced input rows)
+__global__ void __launch_bounds__(256) conv_f64_direct_kernel(const float* __restrict__ x,
+                                                              const float* __restrict__ w,
+                                                              const float* __restrict__ bias,
+                                                              float* __restrict__ y, ConvShape cs) {
+  const int G = conv_groups(cs);
+  const int Cg = cs.C / G, Og = cs.O / G;
+  const int64_t ohw = static_cast<int64_t>(cs.OH) * cs.OW;
+  const int64_t total = static_cast<int64_t>(cs.N) * cs.O * ohw;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t pix = i % ohw;
+    const int64_t no = i / ohw;
+    const int o = static_cast<int>(no % cs.O);
+    const int64_t n = no / cs.O;
+    const int oh = static_cast<int>(pix / cs.OW), ow = static_cast<int>(pix % cs.OW);
+    const int c0 = (o / Og) * Cg;
+    const float* wo = w + static_cast<int64_t>(o) * Cg * cs.KH * cs.KW;
+    double acc = 0.0;
+    for (int c = 0; c < Cg; ++c) {
+      const float* xc = x + ((n * cs.C + c0 + c) * cs.H) * cs.W;
+      for (int kh = 0; kh < cs.KH; ++kh) {
+        const int ih = oh * cs.sh - cs.ph + kh;
+        if (ih < 0 || ih >= cs.H) continue;
+        for (int kw = 0; kw < cs.KW; ++kw) {
+          const int iw = ow * cs.sw - cs.pw + kw;
+          if (iw < 0 || iw >= cs.W) continue;
+          acc = __fma_rn(static_cast<double>(__ldg(xc + static_cast<int64_t>(ih) * cs.W + iw)),
+                         static_cast<double>(__ldg(wo + (c * cs.KH + kh) * cs.KW + kw)), acc);
+        }
+      }
+    }
+    if (bias) acc = __dadd_rn(acc, static_cast<double>(__ldg(bias + o)));
+    y[i] = __double2float_rn(acc);
+  }
+}
+
 template <int TM, int TN>
 void launch(const float* x, const float* w, const float* bias, float* y, const ConvShape& cs,
             cudaStream_t s) {
   const int64_t M = static_cast<int64_t>(cs.N) * cs.OH * cs.OW;
+  const int Og = cs.O / conv_groups(cs);
   dim3 grid(static_cast<unsigned>((M + 16 * TM - 1) / (16 * TM)),
-            static_cast<unsigned>((cs.O + 16 * TN - 1) / (16 * TN)));
+            static_cast<unsigned>((Og + 16 * TN - 1) / (16 * TN)),
+            static_cast<unsigned>(conv_groups(cs)));
   conv_f64_kernel<TM, TN><<<grid, 256, 0, s>>>(x, w, bias, y, cs);
   QC_CUDA_CHECK_LAUNCH();
 }
@@ -165,17 +221,26 @@ void conv2d_f64acc(const float* x, const float* w, const float* bias, float* y,
                    const ConvShape& cs, cudaStream_t s) {
   const int64_t M = static_cast<int64_t>(cs.N) * cs.OH * cs.OW;
   if (M <= 0 || cs.O <= 0) return;
+  const int G = conv_groups(cs);
+  const int Og = cs.O / G;
+  if (G > 1 && Og < 16) {
+    const int64_t total = M * cs.O;
+    conv_f64_direct_kernel<<<static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16)),
+                             256, 0, s>>>(x, w, bias, y, cs);
+    QC_CUDA_CHECK_LAUNCH();
+    return;
+  }
   // Pick the channel tile; shrink the pixel tile when the grid would not fill
   // the 148 SMs.
-  if (cs.O <= 16) {
+  if (Og <= 16) {
     launch<8, 1>(x, w, bias, y, cs, s);
-  } else if (cs.O <= 32) {
+  } else if (Og <= 32) {
     launch<8, 2>(x, w, bias, y, cs, s);
-  } else if (cs.O <= 64) {
+  } else if (Og <= 64) {
     launch<8, 4>(x, w, bias, y, cs, s);
-  } else if ((M + 127) / 128 * ((cs.O + 127) / 128) >= 148) {
+  } else if ((M + 127) / 128 * ((Og + 127) / 128) * G >= 148) {
     launch<8, 8>(x, w, bias, y, cs, s);
-  } else if ((M + 63) / 64 * ((cs.O + 127) / 128) >= 148) {
+  } else if ((M + 63) / 64 * ((Og + 127) / 128) * G >= 148) {
     launch<4, 8>(x, w, bias, y, cs, s);
   } else {
     launch<2, 8>(x, w, bias, y, cs, s);

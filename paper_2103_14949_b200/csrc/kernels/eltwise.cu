@@ -6,6 +6,14 @@
 //   maxpool  best = lowest; best = (best < v) ? v : best over in-bounds taps
 //   gap    sequential double sum / (double)(H*W), rounded to float
 //   argmax strict '>' scan == first index of the maximum (non-NaN data)
+// Op-set extension (the reference op set has neither):
+//   avg_pool2d  sequential double sum over the in-bounds taps (kh, kw) of
+//               (double)x * (double)(float)(1/(KH*KW)), rounded to float once
+//               — bit-identical to the reference conv2d on the constant
+//               depthwise rewrite (fixtures.py _avg_pool, test_rewrites.py);
+//               the divisor counts padded taps (count_include_pad)
+//   concat      channel concatenation of NCHW tensors (32-bit words: fp32 or
+//               the int32 storage of integer tensors)
 #include <cfloat>
 
 #include "common.cuh"
@@ -66,6 +74,52 @@ __global__ void maxpool_kernel(const float* __restrict__ x, float* __restrict__ 
 
 // one warp per (n, c): lanes stage the plane through registers, lane 0 sums
 // in the reference order
+__global__ void avgpool_kernel(const float* __restrict__ x, float* __restrict__ y, int N, int C,
+                               int H, int W, int OH, int OW, int kh, int kw, int sh, int sw,
+                               int ph, int pw, double wk) {
+  const int64_t total = static_cast<int64_t>(N) * C * OH * OW;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int ow = static_cast<int>(i % OW);
+    const int oh = static_cast<int>((i / OW) % OH);
+    const int64_t nc = i / (static_cast<int64_t>(OW) * OH);
+    const float* xp = x + nc * H * W;
+    double acc = 0.0;
+    for (int a = 0; a < kh; ++a) {
+      const int ih = oh * sh - ph + a;
+      if (ih < 0 || ih >= H) continue;
+      for (int b = 0; b < kw; ++b) {
+        const int iw = ow * sw - pw + b;
+        if (iw < 0 || iw >= W) continue;
+        acc = __fma_rn(static_cast<double>(__ldg(xp + static_cast<int64_t>(ih) * W + iw)), wk, acc);
+      }
+    }
+    y[i] = __double2float_rn(acc);
+  }
+}
+
+// one input of a channel concat: rows = N, each `inner` words of x landing at
+// word offset `off` of a `outer`-word output row
+__global__ void concat_kernel(const uint32_t* __restrict__ x, uint32_t* __restrict__ y, int N,
+                              int64_t inner, int64_t outer, int64_t off) {
+  const int64_t total = static_cast<int64_t>(N) * inner;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t n = i / inner, r = i - n * inner;
+    y[n * outer + off + r] = __ldg(x + i);
+  }
+}
+
+__global__ void concat_v4_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, int N,
+                                 int64_t inner, int64_t outer, int64_t off) {
+  const int64_t total = static_cast<int64_t>(N) * inner;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t n = i / inner, r = i - n * inner;
+    y[n * outer + off + r] = __ldg(x + i);
+  }
+}
+
 __global__ void gap_kernel(const float* __restrict__ x, float* __restrict__ y, int NC, int HW) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -223,6 +277,32 @@ void maxpool_f32(const float* x, float* y, int N, int C, int H, int W, int OH, i
   if (total <= 0) return;
   maxpool_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, y, N, C, H, W, OH, OW, kh, kw, sh, sw,
                                                       ph, pw);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+void avgpool_f32(const float* x, float* y, int N, int C, int H, int W, int OH, int OW, int kh,
+                 int kw, int sh, int sw, int ph, int pw, cudaStream_t s) {
+  const int64_t total = static_cast<int64_t>(N) * C * OH * OW;
+  if (total <= 0) return;
+  const double wk = static_cast<double>(static_cast<float>(1.0 / (static_cast<double>(kh) * kw)));
+  avgpool_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, y, N, C, H, W, OH, OW, kh, kw, sh, sw,
+                                                      ph, pw, wk);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+void concat_words(const void* x, void* y, int N, int64_t inner, int64_t outer, int64_t off,
+                  cudaStream_t s) {
+  const int64_t total = static_cast<int64_t>(N) * inner;
+  if (total <= 0) return;
+  const bool v4 = inner % 4 == 0 && outer % 4 == 0 && off % 4 == 0 &&
+                  reinterpret_cast<uintptr_t>(x) % 16 == 0 && reinterpret_cast<uintptr_t>(y) % 16 == 0;
+  if (v4) {
+    concat_v4_kernel<<<grid_for(total / 4, 256), 256, 0, s>>>(
+        static_cast<const uint4*>(x), static_cast<uint4*>(y), N, inner / 4, outer / 4, off / 4);
+  } else {
+    concat_kernel<<<grid_for(total, 256), 256, 0, s>>>(static_cast<const uint32_t*>(x),
+                                                       static_cast<uint32_t*>(y), N, inner, outer, off);
+  }
   QC_CUDA_CHECK_LAUNCH();
 }
 

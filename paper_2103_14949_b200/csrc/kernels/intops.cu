@@ -30,16 +30,20 @@ __device__ int64_t conv_acc(const int32_t* __restrict__ x, const int32_t* __rest
   const int oh = static_cast<int>((flat / cs.OW) % cs.OH);
   const int o = static_cast<int>((flat / (static_cast<int64_t>(cs.OW) * cs.OH)) % cs.O);
   const int64_t n = flat / (static_cast<int64_t>(cs.OW) * cs.OH * cs.O);
+  // grouped convs (op-set extension): output channel o reads the C/G input
+  // channels of its group; the weight is [O][C/G][KH][KW]
+  const int Cg = cs.C / conv_groups(cs);
+  const int cbase = (o / (cs.O / conv_groups(cs))) * Cg;
   int64_t acc = 0;
-  for (int c = 0; c < cs.C; ++c) {
+  for (int c = 0; c < Cg; ++c) {
     for (int kh = 0; kh < cs.KH; ++kh) {
       const int ih = oh * cs.sh - cs.ph + kh;
       if (ih < 0 || ih >= cs.H) continue;
       for (int kw = 0; kw < cs.KW; ++kw) {
         const int iw = ow * cs.sw - cs.pw + kw;
         if (iw < 0 || iw >= cs.W) continue;
-        const int64_t dv = x[((n * cs.C + c) * cs.H + ih) * cs.W + iw] - zp0;
-        const int64_t wv = w[((static_cast<int64_t>(o) * cs.C + c) * cs.KH + kh) * cs.KW + kw] - zp1;
+        const int64_t dv = x[((n * cs.C + cbase + c) * cs.H + ih) * cs.W + iw] - zp0;
+        const int64_t wv = w[((static_cast<int64_t>(o) * Cg + c) * cs.KH + kh) * cs.KW + kw] - zp1;
         acc += dv * wv;
       }
     }

@@ -49,7 +49,12 @@ void kl_sweep(const int64_t* counts, int n_edges, int bins, int target_bit, int*
 // ---- exact fp32 conv/dense with sequential FP64 accumulation (conv_f64.cu) --
 struct ConvShape {
   int N, C, H, W, O, KH, KW, OH, OW, sh, sw, ph, pw;
+  // groups (0 or 1: a dense conv).  C and O are the totals; the weight is
+  // [O][C/G][KH][KW] and output channel o reads input channels
+  // [(o / (O/G)) * C/G, ... + C/G).  Op-set extension.
+  int G;
 };
+__host__ __device__ inline int conv_groups(const ConvShape& cs) { return cs.G > 1 ? cs.G : 1; }
 void conv2d_f64acc(const float* x, const float* w, const float* bias, float* y,
                    const ConvShape& cs, cudaStream_t s);
 
@@ -60,6 +65,12 @@ void relu_f32(const float* x, float* y, int64_t n, cudaStream_t s);
 void clip_f32(const float* x, float* y, int64_t n, float lo, float hi, cudaStream_t s);
 void maxpool_f32(const float* x, float* y, int N, int C, int H, int W, int OH, int OW, int kh,
                  int kw, int sh, int sw, int ph, int pw, cudaStream_t s);
+// op-set extension: avg_pool2d (double sum of x * fl32(1/(kh*kw)), padded taps
+// skipped, count_include_pad divisor) and one input of a channel concat
+void avgpool_f32(const float* x, float* y, int N, int C, int H, int W, int OH, int OW, int kh,
+                 int kw, int sh, int sw, int ph, int pw, cudaStream_t s);
+void concat_words(const void* x, void* y, int N, int64_t inner, int64_t outer, int64_t off,
+                  cudaStream_t s);
 void gap_f32(const float* x, float* y, int NC, int HW, cudaStream_t s);
 void argmax_rows(const float* x, int rows, int64_t cols, int64_t* out, cudaStream_t s);
 // grouped candidate evaluation: argmax of `groups` (<= 4) row blocks in one

@@ -22,6 +22,8 @@ class CudaOps:
         L.qcu_histogram.argtypes = [_P, C.c_int64, C.c_double, C.c_int, _P, _P]
         L.qcu_kl_sweep.argtypes = [_P, C.c_int, C.c_int, C.c_int, _P, _P, _P]
         L.qcu_conv2d_f64acc.argtypes = [_P, _P, _P, _P] + [C.c_int] * 11 + [_P]
+        L.qcu_conv2d_grouped_f64acc.argtypes = [_P, _P, _P, _P] + [C.c_int] * 12 + [_P]
+        L.qcu_avg_pool2d_f32.argtypes = [_P, _P] + [C.c_int] * 10 + [_P]
         L.qcu_conv2d_int.argtypes = ([_P, _P, _P, _P] + [C.c_int] * 11 + [C.c_int64, C.c_int64]
                                      + [C.c_int, C.c_int, C.POINTER(C.c_int64), _P])
         L.qcu_requantize.argtypes = [_P, _P, C.c_int64, C.c_int64, C.c_int, C.c_int64,
@@ -81,6 +83,26 @@ class CudaOps:
         self._ok(self.lib.qcu_conv2d_f64acc(self._p(x), self._p(w), self._p(bias), self._p(y),
                                             N, Cc, H, W, O, KH, KW, stride[0], stride[1], pad[0],
                                             pad[1], self._s()))
+        return y
+
+    def conv2d_grouped_f64acc(self, x, w, bias, stride=(1, 1), pad=(0, 0), groups=1):
+        N, Cc, H, W = x.shape
+        O, _, KH, KW = w.shape
+        OH = (H + 2 * pad[0] - KH) // stride[0] + 1
+        OW = (W + 2 * pad[1] - KW) // stride[1] + 1
+        y = torch.empty((N, O, OH, OW), dtype=torch.float32, device=x.device)
+        self._ok(self.lib.qcu_conv2d_grouped_f64acc(self._p(x), self._p(w), self._p(bias),
+                                                    self._p(y), N, Cc, H, W, O, KH, KW, stride[0],
+                                                    stride[1], pad[0], pad[1], groups, self._s()))
+        return y
+
+    def avg_pool2d(self, x, k, stride, pad):
+        N, Cc, H, W = x.shape
+        OH = (H + 2 * pad[0] - k[0]) // stride[0] + 1
+        OW = (W + 2 * pad[1] - k[1]) // stride[1] + 1
+        y = torch.empty((N, Cc, OH, OW), dtype=torch.float32, device=x.device)
+        self._ok(self.lib.qcu_avg_pool2d_f32(self._p(x), self._p(y), N, Cc, H, W, k[0], k[1],
+                                             stride[0], stride[1], pad[0], pad[1], self._s()))
         return y
 
     def conv2d_int(self, x, w, bias, stride, pad, zp0, zp1, acc_dtype, trap=False):

@@ -121,7 +121,9 @@ class GraphBuilder:
             return (n, o, (h + 2 * p[0] - kh) // s[0] + 1, (w + 2 * p[1] - kw) // s[1] + 1)
         if op == "dense":
             return (ins[0][0], ins[1][0])
-        if op == "max_pool2d":
+        if op == "concat":
+            return (ins[0][0], sum(i[1] for i in ins), ins[0][2], ins[0][3])
+        if op in ("max_pool2d", "avg_pool2d"):
             n, c, h, w = ins[0]
             k = attrs["pool_size"]
             s = attrs.get("strides", k)
@@ -302,20 +304,32 @@ def resnet(depth: int = 50, seed: int = 42, image: int = 224, classes: int = 100
 #                         (count_include_pad semantics)
 #   relu6              -> clip(0, 6)
 
-def _depthwise(gb, wts, x, k, stride=1, pad=None, gain=1.0, bias=True):
+# native=True emits the op-set extension instead (conv2d groups=C,
+# avg_pool2d, concat: include/quantc/graph.hpp), with the same weights drawn
+# from the same RNG stream, so the native and rewritten graphs compute
+# bit-identical fp32 values (tests/test_gpu_native_ops.py).
+
+def _depthwise(gb, wts, x, k, stride=1, pad=None, gain=1.0, bias=True, native=False):
     c = gb.shapes[x][1]
     pad = k // 2 if pad is None else pad
-    w = np.zeros((c, c, k, k), np.float32)
     dw = wts.rng.standard_normal((c, k, k), dtype=np.float32) * np.float32(gain * np.sqrt(2.0 / (k * k)))
-    for i in range(c):
-        w[i, i] = dw[i]
+    if native:
+        w = dw.reshape(c, 1, k, k).copy()
+    else:
+        w = np.zeros((c, c, k, k), np.float32)
+        for i in range(c):
+            w[i, i] = dw[i]
     ins = [x, gb.constant(w)]
     if bias:
         ins.append(gb.constant(wts.bias(c)))
+    if native:
+        return gb.op("conv2d", ins, strides=[stride, stride], padding=[pad, pad], groups=c)
     return gb.op("conv2d", ins, strides=[stride, stride], padding=[pad, pad])
 
 
-def _avg_pool(gb, x, k=3, stride=1, pad=1):
+def _avg_pool(gb, x, k=3, stride=1, pad=1, native=False):
+    if native:
+        return gb.op("avg_pool2d", [x], pool_size=[k, k], strides=[stride, stride], padding=[pad, pad])
     c = gb.shapes[x][1]
     w = np.zeros((c, c, k, k), np.float32)
     for i in range(c):
@@ -323,7 +337,9 @@ def _avg_pool(gb, x, k=3, stride=1, pad=1):
     return gb.op("conv2d", [x, gb.constant(w)], strides=[stride, stride], padding=[pad, pad])
 
 
-def _concat(gb, xs):
+def _concat(gb, xs, native=False):
+    if native:
+        return gb.op("concat", list(xs), axis=1)
     total = sum(gb.shapes[x][1] for x in xs)
     out, off = None, 0
     for x in xs:
@@ -342,7 +358,7 @@ def _relu6(gb, x):
 
 
 def mobilenet_v2(seed: int = 11, image: int = 32, classes: int = 10, width: float = 0.25,
-                 blocks=None) -> Model:
+                 blocks=None, native: bool = False) -> Model:
     """BASELINE config C3: MobileNetV2 (inverted residuals, relu6, linear
     bottlenecks) with depthwise convs rewritten exactly (see above), for the
     arm_vmlal_like int16-accumulation spec.  `blocks` = (t, c, n, s) rows;
@@ -365,7 +381,7 @@ def mobilenet_v2(seed: int = 11, image: int = 32, classes: int = 10, width: floa
             y = h
             if t != 1:
                 y = _relu6(gb, _conv(gb, wts, y, in_c * t, 1))
-            y = _relu6(gb, _depthwise(gb, wts, y, 3, stride))
+            y = _relu6(gb, _depthwise(gb, wts, y, 3, stride, native=native))
             y = _conv(gb, wts, y, out_c, 1, gain=0.5)  # linear bottleneck
             h = gb.op("add", [h, y]) if (stride == 1 and in_c == out_c) else y
             in_c = out_c
@@ -376,11 +392,11 @@ def mobilenet_v2(seed: int = 11, image: int = 32, classes: int = 10, width: floa
                         gb.constant(wts.bias(classes))])
     gb.output(y)
     doc, blob = gb.build()
-    return Model("mobilenet_v2", doc, blob, [1, 3, image, image], gb)
+    return Model("mobilenet_v2" + ("_native" if native else ""), doc, blob, [1, 3, image, image], gb)
 
 
 def inception_v3(seed: int = 13, image: int = 35, classes: int = 10, width: int = 8,
-                 modules: int = 2, head: str = "flatten") -> Model:
+                 modules: int = 2, head: str = "flatten", native: bool = False) -> Model:
     """BASELINE config C5: an Inception-v3-style network (stem, Inception-A
     modules with 1x1 / 1x1-3x3 / 1x1-3x3-3x3 / avgpool-1x1 branches, a
     grid-reduction module, Inception-C-style 1x3/3x1 factorised branches) with
@@ -409,18 +425,18 @@ def inception_v3(seed: int = 13, image: int = 35, classes: int = 10, width: int 
         b1 = cbr(h, 4 * width, 1)
         b2 = cbr(cbr(h, 3 * width, 1), 4 * width, 3)
         b3 = cbr(cbr(cbr(h, 4 * width, 1), 6 * width, 3), 6 * width, 3)
-        b4 = cbr(_avg_pool(gb, h), 2 * width, 1)
-        h = _concat(gb, [b1, b2, b3, b4])
+        b4 = cbr(_avg_pool(gb, h, native=native), 2 * width, 1)
+        h = _concat(gb, [b1, b2, b3, b4], native=native)
     # grid reduction: 3x3 stride 2 | 1x1-3x3-3x3 stride 2 | max pool
     r1 = cbr(h, 8 * width, 3, stride=2, ph=0, pw=0)
     r2 = cbr(cbr(h, 4 * width, 1), 6 * width, 3, stride=2, ph=0, pw=0)
     r3 = gb.op("max_pool2d", [h], pool_size=[3, 3], strides=[2, 2], padding=[0, 0])
-    h = _concat(gb, [r1, r2, r3])
+    h = _concat(gb, [r1, r2, r3], native=native)
     # Inception-C-style: 1x1 | 1x1 -> (1x3, 3x1)
     c1 = cbr(h, 8 * width, 1)
     c2 = cbr(h, 6 * width, 1)
-    c2 = _concat(gb, [cbr(c2, 4 * width, 1, 3), cbr(c2, 4 * width, 3, 1)])
-    h = _concat(gb, [c1, c2])
+    c2 = _concat(gb, [cbr(c2, 4 * width, 1, 3), cbr(c2, 4 * width, 3, 1)], native=native)
+    h = _concat(gb, [c1, c2], native=native)
     if head == "gap":
         f = gb.op("flatten", [gb.op("global_avg_pool2d", [h])])
     else:
@@ -434,7 +450,7 @@ def inception_v3(seed: int = 13, image: int = 35, classes: int = 10, width: int 
                         gb.constant(wts.bias(classes))])
     gb.output(y)
     doc, blob = gb.build()
-    return Model("inception_v3", doc, blob, [1, 3, image, image], gb)
+    return Model("inception_v3" + ("_native" if native else ""), doc, blob, [1, 3, image, image], gb)
 
 
 def overflow_dense(k: int = 256, value: int = 127, acc: str = "int16") -> Tuple[dict, bytes]:

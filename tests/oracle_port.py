@@ -23,6 +23,9 @@ class Port:
         L.orc_kl_best_index.restype = C.c_int
         L.orc_kl_best_index.argtypes = [_I64, C.c_int, C.c_int, C.POINTER(C.c_double)]
         L.orc_conv2d_f64acc.argtypes = [_F, _F, _F, _F] + [C.c_int] * 11
+        L.orc_conv2d_grouped_f64acc.argtypes = [_F, _F, _F, _F] + [C.c_int] * 12
+        L.orc_avg_pool2d.argtypes = [_F, _F] + [C.c_int] * 10
+        L.orc_global_avg_pool2d.argtypes = [_F, _F, C.c_int, C.c_int]
         L.orc_conv2d_int.restype = C.c_int64
         L.orc_conv2d_int.argtypes = [_I32, _I32, _I32, _I32] + [C.c_int] * 11 + [C.c_int64] * 4
         L.orc_requantize.argtypes = [_I32, _I32, C.c_int64, C.c_int64, C.c_int, C.c_int64,
@@ -54,7 +57,7 @@ class Port:
         c = np.ascontiguousarray(counts, np.int64)
         return self.lib.orc_threshold_quantile(c.ctypes.data_as(_I64), len(c), absmax, q)
 
-    def conv2d(self, x, w, bias, stride=(1, 1), pad=(0, 0)):
+    def conv2d(self, x, w, bias, stride=(1, 1), pad=(0, 0), groups=1):
         x = np.ascontiguousarray(x, np.float32)
         w = np.ascontiguousarray(w, np.float32)
         N, Cc, H, W = x.shape
@@ -63,10 +66,27 @@ class Port:
         OW = (W + 2 * pad[1] - KW) // stride[1] + 1
         y = np.empty((N, O, OH, OW), np.float32)
         b = None if bias is None else np.ascontiguousarray(bias, np.float32)
-        self.lib.orc_conv2d_f64acc(x.ctypes.data_as(_F), w.ctypes.data_as(_F),
-                                   None if b is None else b.ctypes.data_as(_F),
-                                   y.ctypes.data_as(_F), N, Cc, H, W, O, KH, KW, stride[0],
-                                   stride[1], pad[0], pad[1])
+        self.lib.orc_conv2d_grouped_f64acc(x.ctypes.data_as(_F), w.ctypes.data_as(_F),
+                                           None if b is None else b.ctypes.data_as(_F),
+                                           y.ctypes.data_as(_F), N, Cc, H, W, O, KH, KW,
+                                           stride[0], stride[1], pad[0], pad[1], groups)
+        return y
+
+    def avg_pool2d(self, x, k, stride, pad):
+        x = np.ascontiguousarray(x, np.float32)
+        N, Cc, H, W = x.shape
+        OH = (H + 2 * pad[0] - k[0]) // stride[0] + 1
+        OW = (W + 2 * pad[1] - k[1]) // stride[1] + 1
+        y = np.empty((N, Cc, OH, OW), np.float32)
+        self.lib.orc_avg_pool2d(x.ctypes.data_as(_F), y.ctypes.data_as(_F), N, Cc, H, W, k[0], k[1],
+                                stride[0], stride[1], pad[0], pad[1])
+        return y
+
+    def global_avg_pool2d(self, x):
+        x = np.ascontiguousarray(x, np.float32)
+        N, Cc, H, W = x.shape
+        y = np.empty((N, Cc, 1, 1), np.float32)
+        self.lib.orc_global_avg_pool2d(x.ctypes.data_as(_F), y.ctypes.data_as(_F), N * Cc, H * W)
         return y
 
     def conv2d_int(self, x, w, bias, stride, pad, zp0, zp1, acc_min, acc_max):
