@@ -286,7 +286,7 @@ def _events(torch):
     return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
 
-def config_legs(b, torch, stream, batch):
+def config_legs(b, torch, stream, batch, engine="auto"):
     """The other BASELINE configs as bounded side legs (device-timed on the
     engine stream; one GPU).  Each: calibrate on its images, bind, then time a
     losses() call over a few candidates.
@@ -307,8 +307,14 @@ def config_legs(b, torch, stream, batch):
         ("c5_inception_v3", F.inception_v3(image=299, width=16, modules=2, head="gap", native=True),
          "int8_int32", 8, True, 0.999, 4),
         ("r50_default_thresholds", F.resnet(50), "int8_int32", 16, False, 0.99, 4),
+        # the same under engine `fast` (fused int8 engine with non-pow2 scales:
+        # within the tolerance stated and tested in tests/test_gpu_fast_mode.py)
+        ("r50_default_thresholds_fast", F.resnet(50), "int8_int32", batch, False, 0.99, 8),
     ]
+    from paper_2103_14949_b200 import cuda_ops
+    ops = cuda_ops.load()
     for name, model, spec_name, n, pow2, qtl, k in plans:
+        ops.set_engine_mode("fast" if name.endswith("_fast") else engine)
         try:
             data = model.data(n, seed=9)
             g = b.graph(model.doc, model.blob)
@@ -340,6 +346,7 @@ def config_legs(b, torch, stream, batch):
             del ev, ds, st, sim
         except Exception as e:  # a side leg never sinks the headline line
             legs[name] = {"error": str(e)[:300]}
+    ops.set_engine_mode(engine)
     return legs
 
 
@@ -625,7 +632,7 @@ def main():
 
     configs = None
     if not args.no_configs and world == 1:
-        configs = config_legs(b, torch, stream, B)
+        configs = config_legs(b, torch, stream, B, args.engine)
 
     # ---- e2e: public C-ABI call with HOST buffers: predict_top1 of the sim
     # graph under a candidate binding (uploads images + plan, downloads preds)

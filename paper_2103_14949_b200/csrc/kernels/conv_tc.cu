@@ -396,9 +396,22 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
           const int img = m0 / ohw, rem = m0 - img * ohw;
           const int oh = rem / g.OW, ow = rem - oh * g.OW;
           const int w0 = ow * g.sw - g.pw, h0 = oh * g.sh - g.ph;
+          // (c0, kw, kh) advance incrementally: this single thread feeds the
+          // whole CTA, and two integer divisions per K block made its
+          // dependent-instruction chain the pipeline's bottleneck on the
+          // 64-byte-block layers (3x3, 64 channels: ~500 cycles per block)
+          int c0 = 0, kw = 0, kh = 0;
           for (int kb = 0; kb < nk; ++kb) {
-            const int tap = (kb * args.bkb) / g.ld, c0 = kb * args.bkb - tap * g.ld;
-            const int kh = tap / g.KW, kw = tap - kh * g.KW;
+            if (kb) {
+              c0 += args.bkb;
+              if (c0 >= g.ld) {
+                c0 = 0;
+                if (++kw == g.KW) {
+                  kw = 0;
+                  ++kh;
+                }
+              }
+            }
             if (wrapped) bar_wait_sleep(&empty[s], ph ^ 1);
             bar_expect(&full[s], A_BYTES + B_BYTES);
             tma_im2col(ma, &full[s], sa + s * A_BYTES, c0, w0, h0, img,
@@ -457,10 +470,13 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
         uint64_t tapmask = 0;
         int64_t rowoff = 0;
         if (row < args.M) {
-          const int ohw = g.OH * g.OW;
-          const int img = static_cast<int>(row / ohw);
-          const int rem = static_cast<int>(row - static_cast<int64_t>(img) * ohw);
-          const int oh = rem / g.OW;
+          // 32-bit divisions (M < 2^31 host-checked): the per-tile row set-up
+          // sits on every producer thread's serial path
+          const uint32_t ohw = static_cast<uint32_t>(g.OH * g.OW);
+          const uint32_t r32 = static_cast<uint32_t>(row);
+          const int img = static_cast<int>(r32 / ohw);
+          const int rem = static_cast<int>(r32 - static_cast<uint32_t>(img) * ohw);
+          const int oh = static_cast<int>(static_cast<uint32_t>(rem) / static_cast<uint32_t>(g.OW));
           const int ih0 = oh * g.sh - g.ph;
           const int iw0 = (rem - oh * g.OW) * g.sw - g.pw;
           rowoff = ((static_cast<int64_t>(img) * g.H + ih0) * g.W + iw0) * g.ld;
@@ -994,7 +1010,14 @@ int fit_stages(const TcArgs& a, int bn, int fixed) {
   int stages = (SMEM_LIMIT - fixed) / (BM * a.bkb + bn * a.bkb);
   const int nk = a.K / a.bkb;
   stages = stages > MAX_STAGES ? MAX_STAGES : stages;
-  return stages > nk + 1 ? nk + 1 : stages;
+  // the ring spans tiles: a CTA with several tiles prefetches the next tile's
+  // K blocks while the current one drains, so the cap by the K loop applies
+  // only to single-tile CTAs
+  // (measured neutral on ResNet-50; opt-in QUANTC_STAGES_SPAN=1)
+  static const bool cap_nk = std::getenv("QUANTC_STAGES_SPAN") == nullptr;
+  const int64_t tiles = static_cast<int64_t>(a.m_tiles) * (a.N + bn - 1) / bn * a.groups;
+  if (cap_nk || tiles <= num_sms()) return stages > nk + 1 ? nk + 1 : stages;
+  return stages;
 }
 
 // double-buffered slot sets when they fit beside >= 2 pipeline stages
@@ -1185,6 +1208,20 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
     }();
     const int want = per_sm > 1 ? per_sm * num_sms() : num_sms() / 2;
     while (BN > 64 && a.m_tiles * ((sp.O + BN - 1) / BN) * a.groups < want) BN /= 2;
+    // wave quantisation of the persistent schedule: a CTA's time ~ its tile
+    // count x (BN + a per-tile fixed part ~ 64 columns' worth); a late-stage
+    // layer with 1.35 waves of 256-wide tiles (200 tiles on 148 SMs) runs
+    // 2.7 waves of 128-wide ones in 25% less time
+    // (measured: no gain on ResNet-50's late stages, where the halved tile
+    // doubles the A re-reads; opt-in QUANTC_WAVE_BN=1)
+    static const bool wave = std::getenv("QUANTC_WAVE_BN") != nullptr;
+    if (wave && BN == 256) {
+      auto cost = [&](int bn) {
+        const int64_t tiles = static_cast<int64_t>(a.m_tiles) * ((sp.O + bn - 1) / bn) * a.groups;
+        return ((tiles + num_sms() - 1) / num_sms()) * (bn + 64);
+      };
+      if (cost(128) < cost(256)) BN = 128;
+    }
   }
   // a wide tile whose slot sets cannot be double-buffered: halve it when the
   // narrower one can (per-tile store drains / residual loads then overlap)

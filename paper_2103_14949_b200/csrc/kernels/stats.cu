@@ -114,15 +114,30 @@ __device__ __forceinline__ int bin_of_fast(float v, float r_f, double absmax,
   return bin_of(v, absmax, bins_over_absmax, bins);
 }
 
+// Shared-memory privatised histogram.  Two contention relief measures for
+// activation edges (a relu edge puts ~half its elements into bin 0):
+//   * bin-0 hits (zeros and |v| < absmax/bins) are counted in a register and
+//     reduced per warp (one shared atomic per warp at the end);
+//   * `reps` replicated sub-histograms, warp w updating copy w % reps, merged
+//     once per CTA before the global atomics.
 __global__ void __launch_bounds__(512) hist_kernel(const float* __restrict__ x, int64_t n,
                                                    double absmax, double bins_over_absmax,
-                                                   int bins, unsigned long long* counts,
+                                                   int bins, int reps, unsigned long long* counts,
                                                    unsigned long long mult) {
   extern __shared__ unsigned int sh[];
-  for (int b = threadIdx.x; b < bins; b += blockDim.x) sh[b] = 0;
+  for (int b = threadIdx.x; b < bins * reps; b += blockDim.x) sh[b] = 0;
   __syncthreads();
+  unsigned int* hs = sh + ((threadIdx.x >> 5) % reps) * bins;
   const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  unsigned int zeros = 0;
+  auto put = [&](int b) {
+    if (b == 0) {
+      ++zeros;
+    } else {
+      atomicAdd(&hs[b], 1u);
+    }
+  };
   if (absmax > 0.0) {
     const float r_f = static_cast<float>(bins_over_absmax);
     if ((reinterpret_cast<uintptr_t>(x) & 15) == 0) {
@@ -130,28 +145,29 @@ __global__ void __launch_bounds__(512) hist_kernel(const float* __restrict__ x, 
       const float4* x4 = reinterpret_cast<const float4*>(x);
       for (int64_t i = tid; i < n4; i += stride) {
         float4 v = __ldg(x4 + i);
-        atomicAdd(&sh[bin_of_fast(v.x, r_f, absmax, bins_over_absmax, bins)], 1u);
-        atomicAdd(&sh[bin_of_fast(v.y, r_f, absmax, bins_over_absmax, bins)], 1u);
-        atomicAdd(&sh[bin_of_fast(v.z, r_f, absmax, bins_over_absmax, bins)], 1u);
-        atomicAdd(&sh[bin_of_fast(v.w, r_f, absmax, bins_over_absmax, bins)], 1u);
+        put(bin_of_fast(v.x, r_f, absmax, bins_over_absmax, bins));
+        put(bin_of_fast(v.y, r_f, absmax, bins_over_absmax, bins));
+        put(bin_of_fast(v.z, r_f, absmax, bins_over_absmax, bins));
+        put(bin_of_fast(v.w, r_f, absmax, bins_over_absmax, bins));
       }
       for (int64_t i = (n4 << 2) + tid; i < n; i += stride) {
-        atomicAdd(&sh[bin_of(x[i], absmax, bins_over_absmax, bins)], 1u);
+        put(bin_of(x[i], absmax, bins_over_absmax, bins));
       }
     } else {
-      for (int64_t i = tid; i < n; i += stride) {
-        atomicAdd(&sh[bin_of(x[i], absmax, bins_over_absmax, bins)], 1u);
-      }
+      for (int64_t i = tid; i < n; i += stride) put(bin_of(x[i], absmax, bins_over_absmax, bins));
     }
   } else {
     // absmax <= 0: every element lands in bin 0 (calibration.cpp:103)
-    int64_t mine = 0;
-    for (int64_t i = tid; i < n; i += stride) ++mine;
-    if (mine) atomicAdd(&sh[0], static_cast<unsigned int>(mine));
+    for (int64_t i = tid; i < n; i += stride) ++zeros;
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) zeros += __shfl_xor_sync(0xffffffffu, zeros, o);
+  if ((threadIdx.x & 31) == 0 && zeros) atomicAdd(&sh[0], zeros);
   __syncthreads();
   for (int b = threadIdx.x; b < bins; b += blockDim.x) {
-    if (sh[b]) atomicAdd(counts + b, static_cast<unsigned long long>(sh[b]) * mult);
+    unsigned long long c = 0;
+    for (int r = 0; r < reps; ++r) c += sh[r * bins + b];
+    if (c) atomicAdd(counts + b, c * mult);
   }
 }
 
@@ -179,8 +195,11 @@ void histogram_accumulate(const float* x, int64_t n, double absmax, int bins,
                           unsigned long long* counts, unsigned long long multiplier,
                           cudaStream_t s) {
   if (n <= 0) return;
-  const size_t smem = static_cast<size_t>(bins) * sizeof(unsigned int);
-  if (smem > 200 * 1024) throw std::runtime_error("histogram: too many bins for shared memory");
+  const size_t one = static_cast<size_t>(bins) * sizeof(unsigned int);
+  if (one > 200 * 1024) throw std::runtime_error("histogram: too many bins for shared memory");
+  int reps = 4;
+  while (reps > 1 && one * reps > 64 * 1024) reps >>= 1;
+  const size_t smem = one * reps;
   if (smem > 48 * 1024) {
     cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
@@ -188,7 +207,7 @@ void histogram_accumulate(const float* x, int64_t n, double absmax, int bins,
   // bins/absmax: with a power-of-two bin count this equals bins * RN(1/absmax)
   const double boa = absmax > 0.0 ? static_cast<double>(bins) / absmax : 0.0;
   const int grid = grid_for((n + 3) / 4, 512, 148 * 4);
-  hist_kernel<<<grid, 512, smem, s>>>(x, n, absmax, boa, bins, counts, multiplier);
+  hist_kernel<<<grid, 512, smem, s>>>(x, n, absmax, boa, bins, reps, counts, multiplier);
   QC_CUDA_CHECK_LAUNCH();
 }
 

@@ -44,6 +44,10 @@ out["minmax"] = {"s": t, "GB/s": 4 * n / t / 1e9, "frac": 4 * n / t / 1e9 / hbm}
 counts = torch.zeros(2048, dtype=torch.int64, device="cuda")
 t = timed(lambda: ops.histogram(x, 6.0, 2048, counts=counts))
 out["histogram_2048"] = {"s": t, "GB/s": 4 * n / t / 1e9, "frac": 4 * n / t / 1e9 / hbm}
+# a relu edge: half the elements are exact zeros (bin 0), the rest half-normal
+xr = torch.relu(x)
+t = timed(lambda: ops.histogram(xr, 6.0, 2048, counts=counts))
+out["histogram_2048_relu"] = {"s": t, "GB/s": 4 * n / t / 1e9, "frac": 4 * n / t / 1e9 / hbm}
 h = torch.randint(0, 1000, (191, 2048), dtype=torch.int64, device="cuda")
 t = timed(lambda: ops.kl_sweep(h, 8), reps=3)
 out["kl_sweep_191x2048"] = {"s": t, "edges_per_s": 191 / t}

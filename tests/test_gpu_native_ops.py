@@ -79,12 +79,16 @@ def test_native_pipeline_vs_graph_oracle(b200, port, which, spec_name):
     # statistics: min / max / absmax and the 2048-bin histogram of every edge
     _, vals = oracle_graph.GraphOracle(port, nat.doc, nat.blob).run(xs, values=True)
     order = g.edge_order()
+    consts = {n["id"] for n in nat.doc["nodes"] if n["op"] == "constant"}
     for k in edges:
-        v = vals[order[k][0]].astype(np.float64)
+        src = order[k][0]
+        v = vals[src].astype(np.float64)
         e = st.get(k)
         assert (e["min"], e["max"]) == (v.min(), v.max()), k
-        np.testing.assert_array_equal(e["counts"], port.histogram(vals[order[k][0]], e["absmax"], 2048),
-                                      err_msg=f"edge {k}")
+        # the reference histograms every edge once per sample
+        # (calibration.cpp:95-105): a constant's counts scale with N
+        want = port.histogram(vals[src], e["absmax"], 2048) * (len(xs) if src in consts else 1)
+        np.testing.assert_array_equal(e["counts"], want, err_msg=f"edge {k}")
     thr = st.estimate_thresholds("quantile", quantile=0.999, pow2=True)
     ev = b200.evaluator(sim, spec, topo, thr, st, ds, min_bit=8)
     sp = ev.space()
