@@ -72,20 +72,39 @@ __global__ void __launch_bounds__(256) conv_f64_kernel(const float* __restrict__
   }
   const float* ximg = x + (static_cast<int64_t>(img) * cs.C + static_cast<int64_t>(grp) * Cg) * cs.H * cs.W;
 
-  auto load_a = [&](int k0, double (&ra)[A_PER]) {
+  // this thread's A elements k = k0 + ak0 + r*AK_STEP as (c, kh, kw), walked
+  // incrementally by BK per tile (mixed radix KH*KW, KW with one carry each):
+  // no integer division in the K loop (it made the loader latency-bound)
+  int ac[A_PER], akh[A_PER], akw[A_PER];
+#pragma unroll
+  for (int r = 0; r < A_PER; ++r) {
+    const int k = ak0 + r * AK_STEP;
+    ac[r] = k / khw;
+    akh[r] = (k - ac[r] * khw) / cs.KW;
+    akw[r] = k - ac[r] * khw - akh[r] * cs.KW;
+  }
+  const int step_c = BK / khw, step_kh = (BK % khw) / cs.KW, step_kw = BK % cs.KW;
+  auto advance_a = [&]() {
 #pragma unroll
     for (int r = 0; r < A_PER; ++r) {
-      const int k = k0 + ak0 + r * AK_STEP;
+      akw[r] += step_kw;
+      int carry = akw[r] >= cs.KW;
+      akw[r] -= carry ? cs.KW : 0;
+      akh[r] += step_kh + carry;
+      carry = akh[r] >= cs.KH;
+      akh[r] -= carry ? cs.KH : 0;
+      ac[r] += step_c + carry;
+    }
+  };
+  const int64_t plane = static_cast<int64_t>(cs.H) * cs.W;
+  auto load_a = [&](double (&ra)[A_PER]) {
+#pragma unroll
+    for (int r = 0; r < A_PER; ++r) {
       double v = 0.0;
-      if (m_ok && k < K) {
-        const int c = k / khw;
-        const int rr = k - c * khw;
-        const int kh = rr / cs.KW;
-        const int kw = rr - kh * cs.KW;
-        const int ih = ih0 + kh, iw = iw0 + kw;
-        if (ih >= 0 && ih < cs.H && iw >= 0 && iw < cs.W) {
-          v = static_cast<double>(__ldg(ximg + (static_cast<int64_t>(c) * cs.H + ih) * cs.W + iw));
-        }
+      const int ih = ih0 + akh[r], iw = iw0 + akw[r];
+      if (m_ok && ac[r] < Cg && static_cast<unsigned>(ih) < static_cast<unsigned>(cs.H) &&
+          static_cast<unsigned>(iw) < static_cast<unsigned>(cs.W)) {
+        v = static_cast<double>(__ldg(ximg + ac[r] * plane + ih * cs.W + iw));
       }
       ra[r] = v;
     }
@@ -119,7 +138,8 @@ __global__ void __launch_bounds__(256) conv_f64_kernel(const float* __restrict__
     for (int j = 0; j < TN; ++j) acc[i][j] = 0.0;
 
   double ra[A_PER], rb[B_PER];
-  load_a(0, ra);
+  load_a(ra);
+  advance_a();
   load_b(0, rb);
   store(0, ra, rb);
   __syncthreads();
@@ -128,7 +148,8 @@ __global__ void __launch_bounds__(256) conv_f64_kernel(const float* __restrict__
   for (int t = 0; t < ntiles; ++t) {
     const int cur = t & 1;
     if (t + 1 < ntiles) {
-      load_a((t + 1) * BK, ra);
+      load_a(ra);
+      advance_a();
       load_b((t + 1) * BK, rb);
     }
 #pragma unroll

@@ -89,6 +89,7 @@ __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t phase) {
       : "memory");
 }
 __device__ __forceinline__ void bar_wait_sleep(uint64_t* b, uint32_t phase) { bar_wait(b, phase); }
+
 __device__ __forceinline__ void tma2d(const CUtensorMap* m, uint64_t* bar, void* dst, int c0,
                                       int c1) {
   asm volatile(
@@ -635,6 +636,8 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
       const int set = args.dbuf ? static_cast<int>(tl & 1) : 0;
       const uint32_t use = args.dbuf ? (tl >> 1) : tl;  // k-th use of this slot set
       TileIo io{su32(slots + set * SET_BYTES), r, static_cast<int>(SLOT_BYTES), SWZ};
+      // (one polling warp + a named barrier for the rest measured slower:
+      // the add-fork epilogue then pays a CTA barrier per tile)
       bar_wait(&tfull[acc], (tl / 2) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       // this set's previous TMA stores must have finished reading it

@@ -8,6 +8,9 @@
 //   (i*w, (i+1)*w], zeros in bin 0 (calibration.cpp:28-33).  Block-private
 //   shared-memory u32 histogram (B <= 8192 bins => <= 32 KB), flushed with one
 //   64-bit global atomic per non-empty bin.  4 B/element.
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace quantc::kern {
@@ -120,6 +123,7 @@ __device__ __forceinline__ int bin_of_fast(float v, float r_f, double absmax,
 //     reduced per warp (one shared atomic per warp at the end);
 //   * `reps` replicated sub-histograms, warp w updating copy w % reps, merged
 //     once per CTA before the global atomics.
+template <bool ZREG>
 __global__ void __launch_bounds__(512) hist_kernel(const float* __restrict__ x, int64_t n,
                                                    double absmax, double bins_over_absmax,
                                                    int bins, int reps, unsigned long long* counts,
@@ -132,7 +136,7 @@ __global__ void __launch_bounds__(512) hist_kernel(const float* __restrict__ x, 
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   unsigned int zeros = 0;
   auto put = [&](int b) {
-    if (b == 0) {
+    if (ZREG && b == 0) {
       ++zeros;
     } else {
       atomicAdd(&hs[b], 1u);
@@ -197,17 +201,25 @@ void histogram_accumulate(const float* x, int64_t n, double absmax, int bins,
   if (n <= 0) return;
   const size_t one = static_cast<size_t>(bins) * sizeof(unsigned int);
   if (one > 200 * 1024) throw std::runtime_error("histogram: too many bins for shared memory");
-  int reps = 4;
+  static const int reps0 = [] {
+    const char* e = std::getenv("QUANTC_HIST_REPS");
+    return e ? std::max(1, std::atoi(e)) : 4;
+  }();
+  int reps = reps0;
   while (reps > 1 && one * reps > 64 * 1024) reps >>= 1;
   const size_t smem = one * reps;
+  static const bool zreg = [] {
+    const char* e = std::getenv("QUANTC_HIST_ZREG");
+    return e ? std::atoi(e) != 0 : false;  // measured: the branch costs more than it saves
+  }();
+  auto kfn = zreg ? hist_kernel<true> : hist_kernel<false>;
   if (smem > 48 * 1024) {
-    cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   }
   // bins/absmax: with a power-of-two bin count this equals bins * RN(1/absmax)
   const double boa = absmax > 0.0 ? static_cast<double>(bins) / absmax : 0.0;
   const int grid = grid_for((n + 3) / 4, 512, 148 * 4);
-  hist_kernel<<<grid, 512, smem, s>>>(x, n, absmax, boa, bins, reps, counts, multiplier);
+  kfn<<<grid, 512, smem, s>>>(x, n, absmax, boa, bins, reps, counts, multiplier);
   QC_CUDA_CHECK_LAUNCH();
 }
 

@@ -977,7 +977,8 @@ class CandidateEvaluator(_Handle):
 
 # ---- library discovery -----------------------------------------------------
 _PKG = os.path.dirname(os.path.abspath(__file__))
-B200_LIB = os.path.join(_PKG, "libquantc_b200.so")
+# QUANTC_B200_LIB: an alternative build of the same library (A/B experiments)
+B200_LIB = os.environ.get("QUANTC_B200_LIB") or os.path.join(_PKG, "libquantc_b200.so")
 _loaded: Dict[str, Quantc] = {}
 
 

@@ -1,4 +1,4 @@
-"""HBM roofline evidence for the streaming kernels of the calibration path
+"""HBM roofline evidence (QUANTC_HIST_REPS: replicated histogram copies) for the streaming kernels of the calibration path
 (north star: "achieved HBM GB/s against the B200 peak for simulated-quantize
 and the histograms"): standalone sim-quant (8 B/elem), min/max pass (4 B/elem),
 histogram pass (4 B/elem) on 256 Mi fp32 elements (1 GiB, >> L2), CUDA-event
