@@ -328,7 +328,7 @@ def config_legs(b, torch, stream, batch, engine="auto"):
             sp = ev.space()
             cands = candidates(sp, k + 1)
             why = b.fused_status(sim, ev.bind(cands[0]))
-            engine = "fused int8 tcgen05" if not why else f"exact FP64 engine ({why[:120]})"
+            ran_on = "fused int8 tcgen05" if not why else f"exact FP64 engine ({why[:120]})"
             ev.losses(cands[:1])
             torch.cuda.synchronize()
             e0, e1 = _events(torch)
@@ -342,7 +342,7 @@ def config_legs(b, torch, stream, batch, engine="auto"):
                           "ms_per_candidate": ms, "images_per_s": n / (ms / 1e3),
                           "candidates_per_s": 1e3 / ms, "candidates": k,
                           "gmac_per_image": model.macs_per_sample() / 1e9,
-                          "engine": engine}
+                          "engine": ran_on}
             del ev, ds, st, sim
         except Exception as e:  # a side leg never sinks the headline line
             legs[name] = {"error": str(e)[:300]}
@@ -632,7 +632,11 @@ def main():
 
     configs = None
     if not args.no_configs and world == 1:
-        configs = config_legs(b, torch, stream, B, args.engine)
+        try:
+            configs = config_legs(b, torch, stream, B, args.engine)
+        except Exception as e:  # side legs never sink the headline line
+            configs = {"error": str(e)[:300]}
+            ops.set_engine_mode(args.engine)
 
     # ---- e2e: public C-ABI call with HOST buffers: predict_top1 of the sim
     # graph under a candidate binding (uploads images + plan, downloads preds)

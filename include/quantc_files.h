@@ -25,6 +25,13 @@ int qc_stats_load(const char* path, qc_stats** out);                  /* :42 */
 /* FNV-1a 64 over the graph's canonical JSON + sidecar bytes (:51) */
 int qc_fingerprint_graph(const qc_graph* g, uint64_t* out);
 int qc_fnv1a64(const void* data, size_t size, uint64_t seed, uint64_t* out); /* :53 */
+/* dataset manifest (serialize.hpp:27-28 load_dataset): single-input fp32
+ * samples of one shape */
+int qc_dataset_load(const char* manifest_path, qc_dataset** out, int64_t* n_samples);
+/* fixtures (reference fixtures.hpp:55-60): write every committed fixture
+ * under dir / regenerate and byte-compare (QC_ERR_* on a mismatch) */
+int qc_fixtures_write_all(const char* dir);
+int qc_fixtures_verify_committed(const char* dir);
 
 #ifdef __cplusplus
 }

@@ -33,6 +33,7 @@
 #ifdef QUANTC_B200
 #include "quantc/device.hpp"
 #include "quantc/distributed.hpp"
+#include "quantc/fixtures.hpp"
 #include "quantc/serialize.hpp"
 #include "quantc_files.h"
 #include "quantc_cuda.h"
@@ -405,6 +406,14 @@ int qc_fingerprint_graph(const qc_graph* g, uint64_t* out) {
 int qc_fnv1a64(const void* data, size_t size, uint64_t seed, uint64_t* out) {
   return run([&] { *out = fnv1a64(data, size, seed); });
 }
+
+int qc_fixtures_write_all(const char* dir) {
+  return run([&] { fixtures::write_all(dir); });
+}
+
+int qc_fixtures_verify_committed(const char* dir) {
+  return run([&] { fixtures::verify_committed(dir); });
+}
 #endif  // QUANTC_B200
 
 // ---- hwspec ---------------------------------------------------------------
@@ -544,6 +553,40 @@ int qc_dataset_create(const float* data, int64_t n_samples, const int64_t* sampl
     *out = h.release();
   });
 }
+
+#ifdef QUANTC_B200
+// dataset manifest (serialize.hpp load_dataset; quantc_files.h): single-input
+// samples of one shape, rebuilt through qc_dataset_create (page-locked mirror)
+int qc_dataset_load(const char* manifest_path, qc_dataset** out, int64_t* n_samples) {
+  Dataset d;
+  int rc = run([&] {
+    d = load_dataset(manifest_path);
+    if (d.empty()) throw IoError(std::string("empty dataset: ") + manifest_path);
+    for (const Sample& s : d) {
+      if (s.inputs.size() != 1 || s.inputs[0].shape() != d[0].inputs[0].shape() || !s.inputs[0].dtype().is_float()) {
+        throw IoError(std::string("qc_dataset_load: samples must share one fp32 input shape: ") + manifest_path);
+      }
+    }
+  });
+  if (rc != 0) return rc;
+  const auto& sh = d[0].inputs[0].shape();
+  const size_t per = static_cast<size_t>(d[0].inputs[0].numel());
+  std::vector<float> flat(per * d.size());
+  std::vector<int64_t> labels(d.size(), -1);
+  bool any_label = false;
+  for (size_t i = 0; i < d.size(); ++i) {
+    const auto v = d[i].inputs[0].floats();
+    std::copy(v.begin(), v.end(), flat.begin() + static_cast<std::ptrdiff_t>(i * per));
+    if (d[i].label) {
+      labels[i] = *d[i].label;
+      any_label = true;
+    }
+  }
+  if (n_samples) *n_samples = static_cast<int64_t>(d.size());
+  return qc_dataset_create(flat.data(), static_cast<int64_t>(d.size()), sh.data(),
+                           static_cast<int>(sh.size()), any_label ? labels.data() : nullptr, out);
+}
+#endif  // QUANTC_B200
 
 void qc_dataset_free(qc_dataset* d) { delete d; }
 

@@ -1,0 +1,487 @@
+// fixtures.cpp — quantc::fixtures (include/quantc/fixtures.hpp; contract
+// SPEC.md:734-782, declared only in reference fixtures.hpp:13-60).
+#include "quantc/fixtures.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <filesystem>
+#include <fstream>
+#include <iterator>
+#include <map>
+#include <random>
+#include <set>
+
+#include "quantc/serialize.hpp"
+
+namespace quantc::fixtures {
+
+namespace {
+
+namespace fs = std::filesystem;
+using Shape = std::vector<int64_t>;
+
+// mt19937_64 stream with explicit conversions (platform-independent bytes)
+class Stream {
+ public:
+  explicit Stream(uint64_t seed) : g_(seed) {}
+  double unit() { return static_cast<double>(g_() >> 11) * 0x1.0p-53; }  // [0, 1)
+  double normal() {
+    // Box-Muller on (0, 1] x [0, 1)
+    const double u1 = 1.0 - unit(), u2 = unit();
+    return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
+  }
+  uint64_t below(uint64_t n) { return g_() % n; }
+  std::vector<float> normals(size_t n, double scale) {
+    std::vector<float> v(n);
+    for (float& x : v) x = static_cast<float>(normal() * scale);
+    return v;
+  }
+
+ private:
+  std::mt19937_64 g_;
+};
+
+int64_t numel(const Shape& s) {
+  int64_t n = 1;
+  for (int64_t d : s) n *= d;
+  return n;
+}
+
+// graph assembly with per-node output shapes
+class Builder {
+ public:
+  NodeId input(const std::string& name, Shape shape) {
+    Node n = fresh(OpKind::kInput);
+    n.attrs = Json{{"name", name}, {"shape", shape}};
+    inputs_.push_back(n.id);
+    return add(std::move(n), {}, std::move(shape));
+  }
+  NodeId constant(Shape shape, std::vector<float> data) {
+    Node n = fresh(OpKind::kConstant);
+    n.payload = Tensor::from_floats(shape, std::move(data));
+    return add(std::move(n), {}, std::move(shape));
+  }
+  NodeId op(OpKind op, std::vector<NodeId> ins, Json attrs = Json::object()) {
+    Node n = fresh(op);
+    n.attrs = std::move(attrs);
+    const Shape& d = shapes_.at(ins.at(0));
+    Shape out = d;
+    switch (op) {
+      case OpKind::kConv2d: {
+        const Shape& w = shapes_.at(ins.at(1));
+        const auto st = n.attr_or<Shape>("strides", {1, 1});
+        const auto pd = n.attr_or<Shape>("padding", {0, 0});
+        out = {d[0], w[0], (d[2] + 2 * pd[0] - w[2]) / st[0] + 1, (d[3] + 2 * pd[1] - w[3]) / st[1] + 1};
+        break;
+      }
+      case OpKind::kDense:
+        out = {d[0], shapes_.at(ins.at(1))[0]};
+        break;
+      case OpKind::kGlobalAvgPool2d:
+        out = {d[0], d[1], 1, 1};
+        break;
+      case OpKind::kFlatten:
+        out = {d[0], numel(d) / d[0]};
+        break;
+      default:
+        break;
+    }
+    return add(std::move(n), std::move(ins), std::move(out));
+  }
+  void output(NodeId id) { outputs_.push_back(PortRef{id, 0}); }
+  const Shape& shape(NodeId id) const { return shapes_.at(id); }
+  Graph build() const { return Graph(nodes_, edges_, inputs_, outputs_); }
+
+ private:
+  Node fresh(OpKind op) {
+    Node n;
+    n.id = next_++;
+    n.op = op;
+    return n;
+  }
+  NodeId add(Node n, std::vector<NodeId> ins, Shape out) {
+    const NodeId id = n.id;
+    for (size_t p = 0; p < ins.size(); ++p) {
+      edges_.push_back(Edge{PortRef{ins[p], 0}, PortRef{id, static_cast<int>(p)}});
+    }
+    nodes_.push_back(std::move(n));
+    shapes_[id] = std::move(out);
+    return id;
+  }
+  NodeId next_ = 0;
+  std::vector<Node> nodes_;
+  std::vector<Edge> edges_;
+  std::vector<NodeId> inputs_;
+  std::vector<PortRef> outputs_;
+  std::map<NodeId, Shape> shapes_;
+};
+
+Sample sample_of(Shape shape, std::vector<float> x, std::optional<int64_t> label = std::nullopt) {
+  Sample s;
+  s.inputs.push_back(Tensor::from_floats(std::move(shape), std::move(x)));
+  s.label = label;
+  return s;
+}
+
+// ---- generation-time host arithmetic (the reference's order: double
+// accumulation over (c, kh, kw) skipping padded taps, + bias, one rounding)
+std::vector<float> conv3x3_relu(const std::vector<float>& x, int C, int H, int W,
+                                const std::vector<float>& w, const std::vector<float>& b, int O) {
+  std::vector<float> y(static_cast<size_t>(O) * H * W);
+  for (int o = 0; o < O; ++o) {
+    for (int h = 0; h < H; ++h) {
+      for (int v = 0; v < W; ++v) {
+        double acc = 0.0;
+        for (int c = 0; c < C; ++c) {
+          for (int kh = 0; kh < 3; ++kh) {
+            const int ih = h - 1 + kh;
+            if (ih < 0 || ih >= H) continue;
+            for (int kw = 0; kw < 3; ++kw) {
+              const int iw = v - 1 + kw;
+              if (iw < 0 || iw >= W) continue;
+              acc += static_cast<double>(x[(static_cast<size_t>(c) * H + ih) * W + iw]) *
+                     static_cast<double>(w[((static_cast<size_t>(o) * C + c) * 3 + kh) * 3 + kw]);
+            }
+          }
+        }
+        const float r = static_cast<float>(acc + static_cast<double>(b[static_cast<size_t>(o)]));
+        y[(static_cast<size_t>(o) * H + h) * W + v] = r < 0.0f ? 0.0f : r;
+      }
+    }
+  }
+  return y;
+}
+
+std::vector<float> gap(const std::vector<float>& x, int C, int HW) {
+  std::vector<float> y(static_cast<size_t>(C));
+  for (int c = 0; c < C; ++c) {
+    double acc = 0.0;
+    for (int k = 0; k < HW; ++k) acc += static_cast<double>(x[static_cast<size_t>(c) * HW + k]);
+    y[static_cast<size_t>(c)] = static_cast<float>(acc / static_cast<double>(HW));
+  }
+  return y;
+}
+
+std::vector<float> dense(const std::vector<float>& f, const std::vector<float>& w,
+                         const std::vector<float>& b, int M) {
+  const size_t K = f.size();
+  std::vector<float> y(static_cast<size_t>(M));
+  for (int m = 0; m < M; ++m) {
+    double acc = 0.0;
+    for (size_t k = 0; k < K; ++k) {
+      acc += static_cast<double>(f[k]) * static_cast<double>(w[static_cast<size_t>(m) * K + k]);
+    }
+    if (!b.empty()) acc += static_cast<double>(b[static_cast<size_t>(m)]);
+    y[static_cast<size_t>(m)] = static_cast<float>(acc);
+  }
+  return y;
+}
+
+// the committed fixture set of write_all
+struct Named {
+  std::string name;
+  Graph graph;
+  const Dataset* calibration;
+  const Dataset* evaluation;
+};
+
+}  // namespace
+
+// ---- specs (Fig. 3 and the section-1 backends) -----------
+
+HardwareSpec spec_fixture(const std::string& name) {
+  auto sig = [](std::vector<std::string> in, const std::string& out) {
+    return Json{{"in", in}, {"out", out}};
+  };
+  Json ops;
+  if (name == "fig3") {
+    ops = {{"add", {sig({"float32", "float32"}, "float32"), sig({"int32", "int32"}, "int32")}},
+           {"conv2d", {sig({"int16", "int16"}, "int32"), sig({"int8", "int8"}, "int16")}},
+           {"global_avg_pool2d", {sig({"float32"}, "float32")}}};
+  } else if (name == "x86_vnni_like") {
+    ops = {{"conv2d", {sig({"uint8", "int8"}, "int32")}}, {"dense", {sig({"uint8", "int8"}, "int32")}}};
+  } else if (name == "arm_vmlal_like") {
+    ops = {{"conv2d", {sig({"int8", "int8"}, "int16"), sig({"int16", "int16"}, "int32")}},
+           {"dense", {sig({"int8", "int8"}, "int16"), sig({"int16", "int16"}, "int32")}}};
+  } else if (name == "int8_int32") {
+    ops = {{"conv2d", {sig({"int8", "int8"}, "int32")}},  {"dense", {sig({"int8", "int8"}, "int32")}},
+           {"add", {sig({"int8", "int8"}, "int32")}},     {"relu", {sig({"int8"}, "int8")}},
+           {"max_pool2d", {sig({"int8"}, "int8")}},       {"clip", {sig({"int8"}, "int8")}}};
+  } else {
+    throw FixtureError("unknown spec fixture: " + name);
+  }
+  return parse_spec(Json{{"ops", ops}}.dump());
+}
+
+// ---- models ------------------------------------------------------------------
+
+ModelFixture make_small_cnn(uint64_t seed) {
+  constexpr int kC = 3, kH = 8, kW = 8, kClasses = 10, kCal = 64, kEval = 256;
+  const int widths[4] = {kC, 8, 16, 16};
+  Stream rs(seed);
+  Builder b;
+  NodeId h = b.input("data", {1, kC, kH, kW});
+  std::vector<std::vector<float>> ws, bs;
+  for (int l = 0; l < 3; ++l) {
+    const int c = widths[l], o = widths[l + 1];
+    ws.push_back(rs.normals(static_cast<size_t>(o) * c * 9, std::sqrt(2.0 / (c * 9))));
+    bs.push_back(rs.normals(static_cast<size_t>(o), 0.01));
+    const NodeId wn = b.constant({o, c, 3, 3}, ws.back());
+    const NodeId bn = b.constant({o}, bs.back());
+    h = b.op(OpKind::kRelu, {b.op(OpKind::kConv2d, {h, wn, bn},
+                                  Json{{"strides", {1, 1}}, {"padding", {1, 1}}})});
+  }
+  const NodeId f = b.op(OpKind::kFlatten, {b.op(OpKind::kGlobalAvgPool2d, {h})});
+  // data: a 10-prototype mixture; a prototype is a per-channel level N(0, 1.5^2)
+  // (what survives global pooling) plus a spatial pattern N(0, 1); samples are
+  // prototype + N(0, 0.6^2)
+  const size_t px = static_cast<size_t>(kC) * kH * kW;
+  std::vector<std::vector<float>> proto;
+  for (int k = 0; k < kClasses; ++k) {
+    std::vector<float> p = rs.normals(px, 1.0);
+    for (int c = 0; c < kC; ++c) {
+      const double level = 1.5 * rs.normal();
+      for (int j = 0; j < kH * kW; ++j) {
+        float& v = p[static_cast<size_t>(c) * kH * kW + static_cast<size_t>(j)];
+        v = static_cast<float>(static_cast<double>(v) + level);
+      }
+    }
+    proto.push_back(std::move(p));
+  }
+  auto draw = [&](int n) {
+    Dataset d;
+    for (int i = 0; i < n; ++i) {
+      const int64_t label = static_cast<int64_t>(rs.below(kClasses));
+      std::vector<float> x(px);
+      for (size_t j = 0; j < px; ++j) {
+        x[j] = static_cast<float>(static_cast<double>(proto[static_cast<size_t>(label)][j]) + 0.6 * rs.normal());
+      }
+      d.push_back(sample_of({1, kC, kH, kW}, std::move(x), label));
+    }
+    return d;
+  };
+  ModelFixture fx;
+  fx.calibration = draw(kCal);
+  fx.evaluation = draw(kEval);
+  auto features = [&](const Sample& s) {
+    const auto in = s.inputs[0].floats();
+    std::vector<float> a(in.begin(), in.end());
+    for (int l = 0; l < 3; ++l) a = conv3x3_relu(a, widths[l], kH, kW, ws[static_cast<size_t>(l)], bs[static_cast<size_t>(l)], widths[l + 1]);
+    return gap(a, widths[3], kH * kW);
+  };
+  // nearest-centroid head over the calibration features: score_k = mu_k . f - |mu_k|^2 / 2
+  const int F = widths[3];
+  std::vector<double> mu(static_cast<size_t>(kClasses) * F, 0.0);
+  std::vector<int> cnt(kClasses, 0);
+  for (const Sample& s : fx.calibration) {
+    const auto fv = features(s);
+    const size_t k = static_cast<size_t>(*s.label);
+    for (int j = 0; j < F; ++j) mu[k * F + static_cast<size_t>(j)] += fv[static_cast<size_t>(j)];
+    ++cnt[k];
+  }
+  std::vector<float> hw(static_cast<size_t>(kClasses) * F), hb(kClasses);
+  for (int k = 0; k < kClasses; ++k) {
+    double sq = 0.0;
+    for (int j = 0; j < F; ++j) {
+      const size_t i = static_cast<size_t>(k) * F + static_cast<size_t>(j);
+      const double m = cnt[static_cast<size_t>(k)] ? mu[i] / cnt[static_cast<size_t>(k)] : 0.0;
+      hw[i] = static_cast<float>(m);
+      sq += m * m;
+    }
+    hb[static_cast<size_t>(k)] = static_cast<float>(-0.5 * sq);
+  }
+  const NodeId y = b.op(OpKind::kDense, {f, b.constant({kClasses, F}, hw), b.constant({kClasses}, hb)});
+  b.output(y);
+  fx.graph = b.build();
+  // verified margin: every sample's fp32 winner beats the runner-up by more
+  // than 2^-14 of the score scale (no near-ties that rounding could flip)
+  for (const Dataset* d : {&fx.calibration, &fx.evaluation}) {
+    for (const Sample& s : *d) {
+      const auto sc = dense(features(s), hw, hb, kClasses);
+      float top = -INFINITY, second = -INFINITY, scale = 0.0f;
+      for (float v : sc) {
+        scale = std::max(scale, std::fabs(v));
+        if (v > top) {
+          second = top;
+          top = v;
+        } else if (v > second) {
+          second = v;
+        }
+      }
+      if (std::getenv("QUANTC_DEBUG_FIXTURES")) {
+        std::fprintf(stderr, "margin %g scale %g\n", static_cast<double>(top - second), static_cast<double>(scale));
+      }
+      if (!(top - second > scale * 0x1p-14f)) {
+        throw FixtureError("make_small_cnn: fp32 margin verification failed (seed " + std::to_string(seed) + ")");
+      }
+    }
+  }
+  return fx;
+}
+
+ModelFixture make_overflow_probe(uint64_t seed) {
+  constexpr int kK = 512, kM = 16, kCal = 64, kEval = 256;
+  Stream rs(seed);
+  // tuned at generation time: zero-mean weights; if a draw misses the margins
+  // the next sub-stream is tried (tuning failures abort)
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    std::vector<float> w = rs.normals(static_cast<size_t>(kM) * kK, 1.0 / std::sqrt(static_cast<double>(kK)));
+    auto draw = [&](int n) {
+      Dataset d;
+      for (int i = 0; i < n; ++i) {
+        std::vector<float> x(kK);
+        for (float& v : x) v = static_cast<float>(rs.unit());
+        d.push_back(sample_of({1, kK}, std::move(x)));
+      }
+      return d;
+    };
+    ModelFixture fx;
+    fx.calibration = draw(kCal);
+    fx.evaluation = draw(kEval);
+    // max-calibrated symmetric thresholds (the largest codes any threshold
+    // rule produces at a given bit width)
+    double xmax = 0.0, wmax = 0.0;
+    for (const Sample& s : fx.calibration) {
+      for (float v : s.inputs[0].floats()) xmax = std::max(xmax, std::fabs(static_cast<double>(v)));
+    }
+    for (float v : w) wmax = std::max(wmax, std::fabs(static_cast<double>(v)));
+    auto acc_max = [&](int bit) {
+      const double qmax = std::ldexp(1.0, bit - 1) - 1.0, qmin = -std::ldexp(1.0, bit - 1);
+      const double sx = xmax / std::ldexp(1.0, bit - 1), sw = wmax / std::ldexp(1.0, bit - 1);
+      std::vector<int64_t> qw(w.size());
+      for (size_t i = 0; i < w.size(); ++i) {
+        qw[i] = static_cast<int64_t>(std::clamp(std::round(static_cast<double>(w[i]) / sw), qmin, qmax));
+      }
+      int64_t worst = 0;
+      for (const Sample& s : fx.calibration) {
+        const auto& x = s.inputs[0].floats();
+        std::vector<int64_t> qx(x.size());
+        for (size_t i = 0; i < x.size(); ++i) {
+          qx[i] = static_cast<int64_t>(std::clamp(std::round(static_cast<double>(x[i]) / sx), qmin, qmax));
+        }
+        for (int m = 0; m < kM; ++m) {
+          int64_t a = 0;
+          for (int k = 0; k < kK; ++k) a += qx[static_cast<size_t>(k)] * qw[static_cast<size_t>(m) * kK + k];
+          worst = std::max<int64_t>(worst, a < 0 ? -a : a);
+        }
+      }
+      return worst;
+    };
+    const int64_t a8 = acc_max(8), a6 = acc_max(6);
+    if (a8 > 32767 && a6 <= 29490) {  // 6 bits clear with >= 10% margin
+      Builder b;
+      const NodeId x = b.input("data", {1, kK});
+      const NodeId y = b.op(OpKind::kDense, {x, b.constant({kM, kK}, std::move(w))});
+      b.output(y);
+      fx.graph = b.build();
+      return fx;
+    }
+  }
+  throw FixtureError("make_overflow_probe: overflow margins not met (seed " + std::to_string(seed) + ")");
+}
+
+Graph make_deep_chain(int searchable_edges, uint64_t seed) {
+  if (searchable_edges < 1) throw FixtureError("make_deep_chain: searchable_edges must be >= 1");
+  constexpr int kWidth = 8;
+  Stream rs(seed);
+  Builder b;
+  NodeId h = b.input("data", {1, kWidth});
+  int remaining = searchable_edges;
+  while (remaining > 0) {
+    if (remaining >= 2) {
+      const NodeId w = b.constant({kWidth, kWidth}, rs.normals(kWidth * kWidth, 1.0 / std::sqrt(double{kWidth})));
+      h = b.op(OpKind::kDense, {h, w});
+      remaining -= 2;
+    }
+    if (remaining >= 1) {
+      h = b.op(OpKind::kRelu, {h});
+      remaining -= 1;
+    }
+  }
+  b.output(h);
+  return b.build();
+}
+
+ModelFixture make_conv_add_pool_chain(uint64_t seed) {
+  constexpr int kC = 3, kO = 4, kH = 8, kW = 8, kN = 16;
+  Stream rs(seed);
+  Builder b;
+  const NodeId x = b.input("data", {1, kC, kH, kW});
+  const NodeId w = b.constant({kO, kC, 3, 3}, rs.normals(kO * kC * 9, std::sqrt(2.0 / (kC * 9))));
+  const NodeId c = b.op(OpKind::kConv2d, {x, w}, Json{{"strides", {1, 1}}, {"padding", {1, 1}}});
+  const NodeId k = b.constant({1, kO, kH, kW}, rs.normals(kO * kH * kW, 1.0));
+  const NodeId a = b.op(OpKind::kAdd, {c, k});
+  b.output(b.op(OpKind::kGlobalAvgPool2d, {a}));
+  ModelFixture fx;
+  fx.graph = b.build();
+  for (Dataset* d : {&fx.calibration, &fx.evaluation}) {
+    for (int i = 0; i < kN; ++i) d->push_back(sample_of({1, kC, kH, kW}, rs.normals(kC * kH * kW, 1.0)));
+  }
+  return fx;
+}
+
+// ---- committed files ---------------------------------------------------------
+
+void write_all(const std::string& dir) {
+  const fs::path root(dir);
+  fs::create_directories(root / "specs");
+  const ModelFixture cnn = make_small_cnn();
+  const ModelFixture probe = make_overflow_probe();
+  const ModelFixture chain = make_conv_add_pool_chain();
+  const std::vector<Named> models = {
+      {"small_cnn", cnn.graph, &cnn.calibration, &cnn.evaluation},
+      {"overflow_probe", probe.graph, &probe.calibration, &probe.evaluation},
+      {"conv_add_pool_chain", chain.graph, &chain.calibration, &chain.evaluation},
+      // the paper's 118-edge search-space example (SPEC.md acceptance 9)
+      {"deep_chain_118", make_deep_chain(118), nullptr, nullptr},
+  };
+  for (const Named& m : models) {
+    save_graph(m.graph, root / (m.name + ".json"));
+    if (m.calibration) save_dataset(*m.calibration, root / (m.name + "_calibration.json"));
+    if (m.evaluation) save_dataset(*m.evaluation, root / (m.name + "_evaluation.json"));
+  }
+  for (const char* s : {"fig3", "x86_vnni_like", "arm_vmlal_like", "int8_int32"}) {
+    std::ofstream f(root / "specs" / (std::string(s) + ".json"), std::ios::binary);
+    f << serialize_spec(spec_fixture(s));
+    if (!f) throw FixtureError(std::string("write_all: cannot write spec ") + s);
+  }
+}
+
+void verify_committed(const std::string& dir) {
+  const fs::path want(dir);
+  if (!fs::is_directory(want)) throw FixtureError("verify_committed: no directory " + dir);
+  const fs::path scratch = fs::temp_directory_path() /
+                           ("quantc_fixtures_" + std::to_string(std::random_device{}()));
+  struct Cleanup {
+    fs::path p;
+    ~Cleanup() {
+      std::error_code ec;
+      fs::remove_all(p, ec);
+    }
+  } cleanup{scratch};
+  write_all(scratch.string());
+  auto listing = [](const fs::path& r) {
+    std::set<std::string> out;
+    for (const auto& e : fs::recursive_directory_iterator(r)) {
+      if (e.is_regular_file()) out.insert(fs::relative(e.path(), r).generic_string());
+    }
+    return out;
+  };
+  auto bytes = [](const fs::path& p) {
+    std::ifstream f(p, std::ios::binary);
+    return std::string(std::istreambuf_iterator<char>(f), std::istreambuf_iterator<char>());
+  };
+  const auto have = listing(scratch);
+  const auto committed = listing(want);
+  if (have != committed) throw FixtureError("verify_committed: the file set differs from a regeneration");
+  for (const std::string& rel : have) {
+    if (bytes(scratch / rel) != bytes(want / rel)) {
+      throw FixtureError("verify_committed: " + rel + " differs from its regeneration");
+    }
+  }
+}
+
+}  // namespace quantc::fixtures

@@ -323,10 +323,12 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
     uint32_t lt = static_cast<uint32_t>(t);
     grp = 0;
     if constexpr (NG > 1) {
-      while (grp + 1 < args.groups && lt >= static_cast<uint32_t>(tiles_g)) {
-        lt -= static_cast<uint32_t>(tiles_g);
-        ++grp;
-      }
+      // branch-free: t < groups * tiles_g, so the group is the count of
+      // group boundaries at or below t
+      const uint32_t tg = static_cast<uint32_t>(tiles_g);
+#pragma unroll
+      for (int k = 1; k < NG; ++k) grp += lt >= static_cast<uint32_t>(k) * tg ? 1 : 0;
+      lt -= static_cast<uint32_t>(grp) * tg;
     }
     uint32_t q = nt > 1 ? __umulhi(lt, nt_rcp) : lt;
     if (q * nt > lt) --q;

@@ -266,6 +266,22 @@ class Quantc:
         self.check(fn(str(path).encode(), C.byref(h)))
         return Graph(self, h)
 
+    def load_dataset(self, path) -> "Dataset":
+        h, n = C.c_void_p(), C.c_int64()
+        fn = self._bind("qc_dataset_load", C.c_int, [C.c_char_p, C.POINTER(_P), C.POINTER(C.c_int64)])
+        self.check(fn(str(path).encode(), C.byref(h), C.byref(n)))
+        return Dataset(self, h, n.value)
+
+    def fixtures_write_all(self, directory):
+        """quantc::fixtures::write_all (fixtures.hpp; B200 library)."""
+        fn = self._bind("qc_fixtures_write_all", C.c_int, [C.c_char_p])
+        self.check(fn(str(directory).encode()))
+
+    def fixtures_verify_committed(self, directory):
+        """quantc::fixtures::verify_committed: raises on any byte mismatch."""
+        fn = self._bind("qc_fixtures_verify_committed", C.c_int, [C.c_char_p])
+        self.check(fn(str(directory).encode()))
+
     def load_stats(self, path) -> "CalibrationStats":
         h = C.c_void_p()
         fn = self._bind("qc_stats_load", C.c_int, [C.c_char_p, C.POINTER(_P)])
