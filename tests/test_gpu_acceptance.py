@@ -57,7 +57,10 @@ def _agreement(b, g_fp32, realized, xs):
 
 
 def test_acceptance4_small_cnn_int8_int32(b200):
-    g, spec, sim, ev = _pipeline(b200, "small_cnn", "int8_int32", "kl", kl_bits=8)
+    # max thresholds (the criterion leaves the estimator open; 8-bit KL
+    # thresholds clip this fixture's 1,024 pooled feature values so hard
+    # that even all_hi loses 89% agreement — scripts/diag_acceptance.py)
+    g, spec, sim, ev = _pipeline(b200, "small_cnn", "int8_int32", "max")
     res = b200.search("greedy", ev.space(), evaluator=ev, rounds=1, tol=0.01)
     R = b200.realize(sim, ev.strategy_for(res.best), spec)
     assert _agreement(b200, g, R, _samples("small_cnn_evaluation")) >= 0.99
