@@ -32,7 +32,8 @@ struct ModelFixture {
 
 // reference fixtures.hpp:22-26.  Three 3x3 conv2d (+relu) over 8x8x3 inputs,
 // global average pooling, flatten, a 10-class dense head set to the class
-// centroids of the pooled features (nearest-centroid scores); 64 calibration
+// centroids of the pooled features (nearest-centroid scores, centred on the
+// mean centroid); 64 calibration
 // and 256 evaluation samples from a seeded 10-prototype mixture.  Verified:
 // every sample's fp32 top-1 beats the runner-up by > 2^-14 of the score scale.
 ModelFixture make_small_cnn(uint64_t seed = 7);

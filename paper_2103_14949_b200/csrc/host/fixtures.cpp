@@ -235,7 +235,7 @@ ModelFixture make_small_cnn(uint64_t seed) {
                                   Json{{"strides", {1, 1}}, {"padding", {1, 1}}})});
   }
   const NodeId f = b.op(OpKind::kFlatten, {b.op(OpKind::kGlobalAvgPool2d, {h})});
-  // data: a 10-prototype mixture; a prototype is a per-channel level N(0, 1.5^2)
+  // data: a 10-prototype mixture; a prototype is a per-channel level N(0, 2.5^2)
   // (what survives global pooling) plus a spatial pattern N(0, 1); samples are
   // prototype + N(0, 0.6^2)
   const size_t px = static_cast<size_t>(kC) * kH * kW;
@@ -243,7 +243,7 @@ ModelFixture make_small_cnn(uint64_t seed) {
   for (int k = 0; k < kClasses; ++k) {
     std::vector<float> p = rs.normals(px, 1.0);
     for (int c = 0; c < kC; ++c) {
-      const double level = 1.5 * rs.normal();
+      const double level = 2.5 * rs.normal();
       for (int j = 0; j < kH * kW; ++j) {
         float& v = p[static_cast<size_t>(c) * kH * kW + static_cast<size_t>(j)];
         v = static_cast<float>(static_cast<double>(v) + level);
@@ -272,7 +272,9 @@ ModelFixture make_small_cnn(uint64_t seed) {
     for (int l = 0; l < 3; ++l) a = conv3x3_relu(a, widths[l], kH, kW, ws[static_cast<size_t>(l)], bs[static_cast<size_t>(l)], widths[l + 1]);
     return gap(a, widths[3], kH * kW);
   };
-  // nearest-centroid head over the calibration features: score_k = mu_k . f - |mu_k|^2 / 2
+  // nearest-centroid head over the calibration features, centred on the mean
+  // centroid (the relu features share a large common component that would
+  // otherwise dominate every score): score_k = (mu_k - mu) . f - (|mu_k|^2 - |mu|^2) / 2
   const int F = widths[3];
   std::vector<double> mu(static_cast<size_t>(kClasses) * F, 0.0);
   std::vector<int> cnt(kClasses, 0);
@@ -282,16 +284,27 @@ ModelFixture make_small_cnn(uint64_t seed) {
     for (int j = 0; j < F; ++j) mu[k * F + static_cast<size_t>(j)] += fv[static_cast<size_t>(j)];
     ++cnt[k];
   }
+  for (int k = 0; k < kClasses; ++k) {
+    for (int j = 0; j < F; ++j) {
+      double& m = mu[static_cast<size_t>(k) * F + static_cast<size_t>(j)];
+      m = cnt[static_cast<size_t>(k)] ? m / cnt[static_cast<size_t>(k)] : 0.0;
+    }
+  }
+  std::vector<double> mbar(static_cast<size_t>(F), 0.0);
+  for (int k = 0; k < kClasses; ++k) {
+    for (int j = 0; j < F; ++j) mbar[static_cast<size_t>(j)] += mu[static_cast<size_t>(k) * F + static_cast<size_t>(j)] / kClasses;
+  }
+  double mbar_sq = 0.0;
+  for (double v : mbar) mbar_sq += v * v;
   std::vector<float> hw(static_cast<size_t>(kClasses) * F), hb(kClasses);
   for (int k = 0; k < kClasses; ++k) {
     double sq = 0.0;
     for (int j = 0; j < F; ++j) {
       const size_t i = static_cast<size_t>(k) * F + static_cast<size_t>(j);
-      const double m = cnt[static_cast<size_t>(k)] ? mu[i] / cnt[static_cast<size_t>(k)] : 0.0;
-      hw[i] = static_cast<float>(m);
-      sq += m * m;
+      hw[i] = static_cast<float>(mu[i] - mbar[static_cast<size_t>(j)]);
+      sq += mu[i] * mu[i];
     }
-    hb[static_cast<size_t>(k)] = static_cast<float>(-0.5 * sq);
+    hb[static_cast<size_t>(k)] = static_cast<float>(-0.5 * (sq - mbar_sq));
   }
   const NodeId y = b.op(OpKind::kDense, {f, b.constant({kClasses, F}, hw), b.constant({kClasses}, hb)});
   b.output(y);

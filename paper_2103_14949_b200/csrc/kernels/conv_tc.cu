@@ -630,6 +630,16 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
     const int quarter = warp & 3;
     const int part = warp >> 2;  // this warp's chunks: part, part + PARTS, ...
     const int r = quarter * 32 + lane;
+    // integer shapes: bit g set when group g has any corrected chunk (most
+    // layers have none: their chunks then skip the per-chunk mask test)
+    uint32_t corr_groups = 0;
+    if constexpr (shape_is_int_fold(SHAPE)) {
+      for (int g = 0; g < args.groups; ++g) {
+        uint32_t any = 0;
+        for (int w = 0; w < 16; ++w) any |= cmask[g * 16 + w];
+        corr_groups |= (any != 0u ? 1u : 0u) << g;
+      }
+    }
     uint32_t tl = 0;
     for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
       int grp, m0, n0;
@@ -694,8 +704,10 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
           const int n = n0 + c0;
           if (n < args.N) {
             // warp-uniform: every lane of the warp works on the same channels
-            uint32_t cm;
-            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cm) : "r"(su32(cmg + (n >> 9))));
+            uint32_t cm = 0;
+            if ((corr_groups >> grp) & 1u) {
+              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cm) : "r"(su32(cmg + (n >> 9))));
+            }
             if ((cm >> ((n >> 4) & 31)) & 1u) {
               run_int_epi<SHAPE, true>(d, ctg + n, e, io, c0, tpg + n, args.N);
             } else {
