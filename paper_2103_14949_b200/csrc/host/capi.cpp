@@ -37,6 +37,7 @@
 #include "quantc/serialize.hpp"
 #include "quantc_files.h"
 #include "quantc_cuda.h"
+#include "engine.hpp"
 #endif
 
 using namespace quantc;
@@ -742,9 +743,15 @@ int qc_eval_fp32(const qc_graph* g, const float* input, const int64_t* shape, in
                  const int64_t* bind_nodes, const qc_qparams* bind_params, size_t n_bind,
                  float* out, size_t cap, size_t* n_out, int64_t* out_shape, int* out_ndim) {
   return run([&] {
-    FeedMap feed = single_feed(*g->g, input_tensor(input, shape, ndim));
     SimBinding b = make_binding(bind_nodes, bind_params, n_bind);
+#ifdef QUANTC_B200
+    // the caller's buffer is uploaded directly (no Tensor / FeedMap copies)
+    std::vector<Tensor> outs = engine::eval_fp32_host(*g->g, input, std::vector<int64_t>(shape, shape + ndim),
+                                                      n_bind ? &b : nullptr);
+#else
+    FeedMap feed = single_feed(*g->g, input_tensor(input, shape, ndim));
     std::vector<Tensor> outs = eval_fp32(*g->g, feed, n_bind ? &b : nullptr);
+#endif
     if (outs.empty()) throw EvalError("graph has no outputs");
     const Tensor& t = outs[0];
     if (out_ndim) *out_ndim = static_cast<int>(t.shape().size());
@@ -774,8 +781,13 @@ int qc_eval_fp32_values(const qc_graph* g, const float* input, const int64_t* sh
 int qc_eval_int(const qc_graph* g, const float* input, const int64_t* shape, int ndim,
                 int mode, int32_t* out, size_t cap, size_t* n_out, int* out_dtype) {
   return run([&] {
+#ifdef QUANTC_B200
+    auto outs = engine::eval_int_host(*g->g, input, std::vector<int64_t>(shape, shape + ndim),
+                                      mode ? OverflowMode::kTrap : OverflowMode::kSaturate);
+#else
     FeedMap feed = single_feed(*g->g, input_tensor(input, shape, ndim));
     auto outs = eval_int(*g->g, feed, mode ? OverflowMode::kTrap : OverflowMode::kSaturate);
+#endif
     if (outs.empty()) throw EvalError("graph has no outputs");
     const Tensor& t = outs[0];
     *out_dtype = code_of(t.dtype());

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <map>
 #include <cstdio>
 #include <cmath>
 #include <cstring>
@@ -1141,18 +1142,25 @@ void Runner::exec(int i) {
 }  // namespace
 
 std::vector<DevTensor> run(const Plan& plan, const RunSpec& spec) {
-  static const bool sprof = std::getenv("QUANTC_STEP_PROF") != nullptr;
+  // QUANTC_STEP_PROF=<ms>: report steps whose host-side work exceeds <ms>
+  // (default 5) and a per-op-kind host-time summary at the end
+  static const double sprof = [] {
+    const char* e = std::getenv("QUANTC_STEP_PROF");
+    if (!e) return -1.0;
+    const double v = std::atof(e);
+    return v > 0.0 ? v : 5.0;
+  }();
   Runner r(plan, spec);
   r.plan_fast();
   const int n = static_cast<int>(plan.steps().size());
+  std::map<std::string, std::pair<double, int>> by_op;
   for (int i = 0; i < n; ++i) {
-    if (!sprof) {
+    if (sprof < 0.0) {
       r.exec(i);
       if (spec.on_value) spec.on_value(i, r.vals[static_cast<size_t>(i)]);
       r.release_inputs(i);
       continue;
     }
-    // QUANTC_STEP_PROF: report steps whose host-side work exceeds 5 ms
     auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
     const auto t0 = std::chrono::steady_clock::now();
     r.exec(i);
@@ -1161,10 +1169,17 @@ std::vector<DevTensor> run(const Plan& plan, const RunSpec& spec) {
     const auto t2 = std::chrono::steady_clock::now();
     r.release_inputs(i);
     const auto t3 = std::chrono::steady_clock::now();
-    if (ms(t0, t3) > 5.0) {
-      std::fprintf(stderr, "  step %d op %s: exec %.1f hook %.1f release %.1f ms\n", i,
-                   op_name(plan.steps()[static_cast<size_t>(i)].node->op).c_str(), ms(t0, t1),
-                   ms(t1, t2), ms(t2, t3));
+    const std::string op = op_name(plan.steps()[static_cast<size_t>(i)].node->op);
+    by_op[op].first += ms(t0, t3);
+    by_op[op].second += 1;
+    if (ms(t0, t3) > sprof) {
+      std::fprintf(stderr, "  step %d op %s: exec %.2f hook %.2f release %.2f ms\n", i, op.c_str(),
+                   ms(t0, t1), ms(t1, t2), ms(t2, t3));
+    }
+  }
+  if (sprof >= 0.0) {
+    for (const auto& [op, v] : by_op) {
+      std::fprintf(stderr, "  host %-20s %8.2f ms over %d steps\n", op.c_str(), v.first, v.second);
     }
   }
   std::vector<DevTensor> out;

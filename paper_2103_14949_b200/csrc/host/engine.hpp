@@ -134,6 +134,12 @@ std::vector<DevTensor> run(const Plan& plan, const RunSpec& spec);
 
 // Host <-> device helpers
 DevTensor upload(const Tensor& t);
+// eval_fp32 / eval_int of a single-input graph on a caller-owned host buffer
+// (interpreter.cpp; the C-ABI's qc_eval_fp32 / qc_eval_int)
+std::vector<Tensor> eval_fp32_host(const Graph& g, const float* x, const std::vector<int64_t>& shape,
+                                   const SimBinding* binding);
+std::vector<Tensor> eval_int_host(const Graph& g, const float* x, const std::vector<int64_t>& shape,
+                                  OverflowMode mode);
 Tensor download(const DevTensor& d, int batch);
 
 }  // namespace quantc::engine
