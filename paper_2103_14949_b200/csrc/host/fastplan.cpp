@@ -1295,6 +1295,7 @@ void FastPlan::prepare(Run& r) {
   static const bool no_shapes = std::getenv("QUANTC_NO_SHAPES") != nullptr;
   static const bool no_special = std::getenv("QUANTC_NO_SPECIAL") != nullptr;
   static const bool no_alias = std::getenv("QUANTC_NO_FORK_ALIAS") != nullptr;
+  static const bool no_res_alias = std::getenv("QUANTC_NO_RES_ALIAS") != nullptr;
   auto& shape0 = r.shape0;
   auto& shape_of = r.shape_of;
   auto& epi_of = r.epi_of;
@@ -1361,7 +1362,10 @@ void FastPlan::prepare(Run& r) {
         // one output slot (0); the residual moves to slot 1 (= n_out)
         e.slot_out[0] = 0;
         e.slot_out[1] = -1;
-        if (e.slot_res >= 0) e.slot_res = 1;
+        // the integer add-fork reads its residual bytes and overwrites them
+        // with the output in one slot (TcConvSpec::res_alias): half the slot
+        // memory, so 256-wide tiles keep double-buffered sets
+        if (e.slot_res >= 0) e.slot_res = (sh == kern::kShapeAddForkInt && !no_res_alias) ? 0 : 1;
       }
     }
   }
@@ -1761,6 +1765,10 @@ void FastPlan::gemm_spec(Run& r, size_t si, kern::TcConvSpec& sp) {
     sp.res_ptr = buf(r, st.res_val);
     sp.res_cols = rv.C;
     sp.res_ld = rv.ld;
+    sp.res_alias = sp.prog.shape == kern::kShapeAddForkInt && sp.n_out == 1 && sp.epi.slot_res == 0 &&
+                           sp.epi.slot_out[0] == 0
+                       ? 1
+                       : 0;
   }
   sp.groups = 1;
 }
@@ -1960,7 +1968,8 @@ void FastPlan::predict_group(int batch, const std::vector<const float*>& inputs,
       for (int g = g0 + 1; g < G && !no_group && shape_kernel; ++g) {
         const kern::TcConvSpec& o = sp[g];
         if (launched[g] || o.prog.shape != sh || o.n_out != head.n_out ||
-            (o.res_ptr != nullptr) != (head.res_ptr != nullptr) || o.lda != head.lda) {
+            (o.res_ptr != nullptr) != (head.res_ptr != nullptr) || o.res_alias != head.res_alias ||
+            o.lda != head.lda) {
           continue;
         }
         launched[g] = 1;

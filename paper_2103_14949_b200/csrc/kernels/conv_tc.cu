@@ -163,6 +163,7 @@ struct TcArgs {
   int n_out;     // smem-staged code outputs (TMA store), 0..2
   int has_res;   // TMA-prefetched residual slot (index n_out)
   int dbuf;      // 1: two slot sets, alternating by tile (stores / prefetch overlap)
+  int res_alias; // residual prefetched into code-output slot 0 (TcConvSpec::res_alias)
   TcGeom g;
   const float* bias;
   double scale;
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
   uint8_t* sa = smem;
   uint8_t* sb = sa + stages * A_BYTES;
   uint8_t* slots = sb + stages * B_BYTES;  // 1024-aligned (stage sizes are multiples of 1 KB)
-  const int n_slots = args.n_out + args.has_res;
+  const int n_slots = args.n_out + args.has_res - args.res_alias;
   const uint32_t SET_BYTES = n_slots * SLOT_BYTES;  // one slot set
   uint64_t* full = reinterpret_cast<uint64_t*>(slots + (args.dbuf + 1) * SET_BYTES);
   uint64_t* empty = full + MAX_STAGES;
@@ -585,7 +586,7 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
         int grp, m0, n0;
         tile_at(t, grp, m0, n0);
         const CUtensorMap* mr = &maps.m[grp][4];
-        uint8_t* dst = slots + set * SET_BYTES + args.n_out * SLOT_BYTES;
+        uint8_t* dst = slots + set * SET_BYTES + (args.res_alias ? 0 : args.n_out) * SLOT_BYTES;
         bar_expect(&rfull[set], SLOT_BYTES);
         for (int blk = 0; blk < BN / SWZ; ++blk) {
           tma2d(mr, &rfull[set], dst + blk * (BM * SWZ), n0 + blk * SWZ, m0);
@@ -616,11 +617,17 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
           }
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
-        if (args.has_res) {
+        if (args.has_res && !args.res_alias) {
           const int t2 = t + nsets * static_cast<int>(gridDim.x);
           if (t2 < n_tiles_total) load_res(t2, set);
         }
         if (args.n_out > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        if (args.res_alias) {
+          // the residual shares the output slot: prefetch only after the
+          // stores have read it
+          const int t2 = t + nsets * static_cast<int>(gridDim.x);
+          if (t2 < n_tiles_total) load_res(t2, set);
+        }
         bar_arrive(&sfree[set]);
       }
       if (args.n_out > 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -1016,7 +1023,7 @@ int num_sms() {
 
 // shared memory of one CTA: everything but the pipeline stages
 int smem_fixed(const TcArgs& a, int bn, int sets, bool shape) {
-  return 1024 + sets * (a.n_out + a.has_res) * BM * bn + (2 * MAX_STAGES + 10) * 8 + 16 +
+  return 1024 + sets * (a.n_out + a.has_res - a.res_alias) * BM * bn + (2 * MAX_STAGES + 10) * 8 + 16 +
          static_cast<int>(sizeof(StageTables)) + 64 +
          (a.gather == 1 ? a.K / 16 * static_cast<int>(sizeof(int2)) : 0) +
          (shape ? ((a.N + bn - 1) / bn) * bn * 4 * a.groups + 64 * a.groups : 0);
@@ -1159,6 +1166,7 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
   a.gather = sp.gather ? 1 : 0;
   a.n_out = sp.n_out;
   a.has_res = sp.res_ptr != nullptr ? 1 : 0;
+  a.res_alias = a.has_res && sp.n_out == 1 && sp.res_alias ? 1 : 0;
   a.g = TcGeom{sp.x, sp.Nimg, sp.H, sp.W, sp.C, sp.ld, sp.KH, sp.KW, sp.sh, sp.sw,
                sp.ph, sp.pw, sp.OH, sp.OW};
   a.bias = sp.bias;

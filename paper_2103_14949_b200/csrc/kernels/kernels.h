@@ -154,6 +154,11 @@ struct TcConvSpec {
   const void* res_ptr;
   int res_cols;
   int64_t res_ld;
+  // 1: the add operand is prefetched into output slot 0 itself (no slot of
+  // its own: each epilogue thread reads its residual bytes, then overwrites
+  // them with its output codes); the store warp drains a set's stores before
+  // it prefetches the next residual into it
+  int res_alias;
   double acc_bound;  // host bound on |sum_k a*b| (K * max|qa| * max|qb|)
   // device bound on |sum_k a*b|: max_o sum_k |w_code[o][k]| (weight_l1_max),
   // times the input codes' max |q|; <= 2^24 lets the epilogue convert with I2F
