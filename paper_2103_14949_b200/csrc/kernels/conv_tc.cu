@@ -111,6 +111,32 @@ __device__ __forceinline__ void tma_im2col(const CUtensorMap* m, uint64_t* bar, 
       "h"(off_w), "h"(off_h)
       : "memory");
 }
+// tiled (non-im2col) TMA loads of rank 3 / 4; out-of-range coordinates
+// (negative included) read as zero
+__device__ __forceinline__ void tma3d(const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1,
+                                      int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma4d(const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1,
+                                      int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store3d(const CUtensorMap* m, const void* src, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(m)),
+      "r"(su32(src)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
 __device__ __forceinline__ void tma_store2d(const CUtensorMap* m, const void* src, int c0,
                                             int c1) {
   asm volatile(
@@ -130,6 +156,15 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
   return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>(1) << 16) |
          (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
          (static_cast<uint64_t>(2) << 61);
+}
+// K-major, no swizzle (canonical ((8,m),2):((16 B, SBO), LBO)): rows of a
+// core matrix 16 B apart, 8-row groups SBO apart, the two 16-byte K halves of
+// one K=32 MMA LBO apart.  The band producer points LBO at the NEXT PIXEL, so
+// one MMA reads two horizontally adjacent filter taps from the same smem rows.
+__device__ __forceinline__ uint64_t desc_none(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) |
+         (static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32) | (static_cast<uint64_t>(1) << 46);
 }
 __host__ __device__ constexpr uint32_t idesc(int m, int n) {
   return (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
@@ -157,7 +192,7 @@ struct TcGeom {
 
 struct TcArgs {
   int M, N, K;   // GEMM dims (K multiple of 128)
-  int gather;
+  int gather;    // 0 TMA rows, 1 cp.async gather, 2 im2col TMA, 3 row band (below)
   int stages;    // runtime pipeline depth (<= MAX_STAGES)
   int bkb;       // K-block bytes: 128 (SWIZZLE_128B tiles) or 64 (SWIZZLE_64B, 64-channel im2col)
   int n_out;     // smem-staged code outputs (TMA store), 0..2
@@ -180,6 +215,16 @@ struct TcArgs {
   // follow group g-1's in the persistent schedule.  Group 0 uses the fields
   // above, groups 1.. their TcGroupsT entries.
   int groups;
+  // gather == 3, the row band: one tile = one output row (n, oh) of OW <= 128
+  // pixels of a stride-1 conv over 16-byte pixels (the space-to-depth stem).
+  // The producer TMA-loads the KH input rows oh-ph.. as one box of band_cols
+  // = OW + KW - 1 pixels (zero outside the image), and the MMA reads tap
+  // (kh, kw) as the band shifted by kh rows and kw pixels: KH*KW/2 MMAs per
+  // tile from one ~7 KB load, no per-row gather.  B = [tap][o][16 B] (3-D
+  // map over the [O][Kpad] codes); outputs leave through a 3-D map whose
+  // width OW clips the tile's rows OW..127.
+  int band_cols;
+  int band_a_bytes;  // A stage of the band (covers the MMA's reads past the band's end)
 };
 
 // the tensor maps of NG groups: A, B, code outputs 0/1, residual
@@ -234,8 +279,10 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
     tc_conv_kernel(const __grid_constant__ TcMapsT<NG> maps, const TcArgs args,
                    const __grid_constant__ TcGroupsT<NG> gr) {
   constexpr int EW = 16;
-  const uint32_t A_BYTES = BM * args.bkb;
-  const uint32_t B_BYTES = BN * args.bkb;
+  const uint32_t A_BYTES = args.gather == 3 ? args.band_a_bytes : BM * args.bkb;
+  // row band: no B ring — every group's [tap][o][16 B] block stays resident
+  const uint32_t B_BYTES = args.gather == 3 ? 0u : BN * args.bkb;
+  const uint32_t WBLK = static_cast<uint32_t>(BN * args.g.KH * args.g.KW * 16);
   constexpr uint32_t SLOT_BYTES = BM * BN;
   constexpr int SWZ = BN >= 128 ? 128 : 64;
   constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
@@ -251,7 +298,7 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
                                              ~uintptr_t(1023));
   uint8_t* sa = smem;
   uint8_t* sb = sa + stages * A_BYTES;
-  uint8_t* slots = sb + stages * B_BYTES;  // 1024-aligned (stage sizes are multiples of 1 KB)
+  uint8_t* slots = sb + (args.gather == 3 ? args.groups * WBLK : stages * B_BYTES);  // 1024-aligned
   const int n_slots = args.n_out + args.has_res - args.res_alias;
   const uint32_t SET_BYTES = n_slots * SLOT_BYTES;  // one slot set
   uint64_t* full = reinterpret_cast<uint64_t*>(slots + (args.dbuf + 1) * SET_BYTES);
@@ -261,7 +308,8 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
   uint64_t* rfull = tempty + 2;   // [2] residual of a slot set landed
   uint64_t* sfull = rfull + 2;    // [2] epilogue warps wrote a slot set
   uint64_t* sfree = sfull + 2;    // [2] a slot set's stores drained (reusable)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfree + 2);
+  uint64_t* bres = sfree + 2;     // row band: the weight blocks landed (staging)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 2);
   StageTables* tabs = reinterpret_cast<StageTables*>(tmem_slot + 4);
   // gather K-chunk table: chunk q (16 bytes of K) = channel run c..c+15 of tap
   // (kh, kw); x = byte offset from the row's (ih0, iw0) pixel, y = tap index
@@ -352,6 +400,7 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
       bar_init(&sfull[a], EPI_WARPS);  // one arrival per epilogue warp
       bar_init(&sfree[a], 1);
     }
+    bar_init(&bres[0], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == MMA_WARP) {
@@ -368,6 +417,30 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
   // let the next kernel start its own, then wait for our predecessor's data
   pdl_trigger();
   pdl_wait();
+  if (args.gather == 3) {
+    // row band: stage each group's [O][Kpad] weight rows through the (still
+    // idle) A ring by TMA, then transpose them into the resident
+    // [tap][o][16 B] blocks the MMA's no-swizzle descriptors read
+    const int taps = args.g.KH * args.g.KW;
+    const uint32_t rows_bytes = static_cast<uint32_t>(BN * args.bkb);
+    if (threadIdx.x == 0) {
+      bar_expect(&bres[0], rows_bytes * args.groups);
+      for (int g = 0; g < args.groups; ++g) tma2d(&maps.m[g][1], &bres[0], sa + g * rows_bytes, 0, 0);
+    }
+    bar_wait(&bres[0], 0);
+    const int items = args.groups * BN * taps;
+    for (int i = threadIdx.x; i < items; i += blockDim.x) {
+      const int g = i / (BN * taps);
+      const int r = i - g * (BN * taps);
+      const int tap = r / BN, o = r - tap * BN;
+      const int4 v = lds128(su32(sa + g * rows_bytes + o * args.bkb + tap * 16));
+      sts128(su32(sb + g * WBLK + (tap * BN + o) * 16), v);
+    }
+    // generic-proxy smem writes -> tensor-core (async proxy) reads, and the
+    // staging reads done before the producer's TMA overwrites the ring
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+  }
   // |acc| <= L1(w) * max|x| <= 2^24: I2F is exact and the conversion pipe is idle
   const bool acc_small = args.w_l1 != nullptr &&
                          static_cast<int64_t>(__ldg(args.w_l1)) * args.x_absmax <= (1 << 24);
@@ -384,7 +457,34 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
   if (warp >= EPI_WARPS && warp < MMA_WARP) {
     // ================= producers =================
     const int p = threadIdx.x - EPI_WARPS * 32;  // 0..127 = tile row
-    if (args.gather == 2) {
+    if (args.gather == 3) {
+      // row band: per tile the KH input rows of output row (n, oh) and the
+      // whole [tap][o][16 B] weight block, one stage
+      if (p == 0) {
+        const TcGeom& g = args.g;
+        int s = 0;
+        uint32_t ph = 0;
+        bool wrapped = false;
+        // one box: KH input rows x band_cols pixels from pixel -pw, as 8-byte
+        // elements (whole rows per TMA request: boxes of 16-byte rows run at
+        // the TMA unit's per-row rate; 32 boxes of 256 bytes were issue-bound)
+        const uint32_t band_bytes = static_cast<uint32_t>(g.KH * args.band_cols * 16);
+        for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+          int grp, m0, n0;
+          tile_at(t, grp, m0, n0);
+          const int q = m0 / BM;  // output row index n*OH + oh
+          const int img = q / g.OH, oh = q - img * g.OH;
+          if (wrapped) bar_wait_sleep(&empty[s], ph ^ 1);
+          bar_expect(&full[s], band_bytes);
+          tma3d(&maps.m[grp][0], &full[s], sa + s * A_BYTES, -2 * g.pw, oh * g.sh - g.ph, img);
+          if (++s == stages) {
+            s = 0;
+            ph ^= 1;
+            wrapped = true;
+          }
+        }
+      }
+    } else if (args.gather == 2) {
       // im2col TMA: K block kb = channels [c0, c0+128) of tap (kh, kw)
       if (p == 0) {
         const TcGeom& g = args.g;
@@ -541,29 +641,33 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
       const uint32_t id = idesc(BM, BN) & ~(args.iepi.a_unsigned ? (1u << 7) : 0u);
       uint32_t tl = 0, ph = 0;
       int s = 0;
-      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
-        const uint32_t acc = tl & 1;
-        if (tl >= 2) bar_wait_sleep(&tempty[acc], ((tl / 2) - 1) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t d = tmem + acc * BN;
-        for (int kb = 0; kb < nk; ++kb) {
-          bar_wait_sleep(&full[s], ph);
-          // gathered A was written by cp.async (generic proxy): make it
-          // visible to the tensor core's async-proxy reads
-          if (args.gather == 1) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (args.gather == 3) {
+        // row band, one stage per tile.  Tap pair (kh, kw..kw+1): A = band
+        // row kh from pixel kw (LBO = one pixel), B = taps kh*4+kw..
+        // ([tap][o][16 B], LBO = one tap); 4x4 taps (host-checked): the eight
+        // descriptors are two base descriptors plus constant offsets
+        // (address field, >> 4)
+        const uint32_t row16 = static_cast<uint32_t>(args.band_cols);  // row pitch >> 4
+        for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
+          const uint32_t acc = tl & 1;
+          if (tl >= 2) bar_wait_sleep(&tempty[acc], ((tl / 2) - 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t ab = su32(sa + s * A_BYTES), bb = su32(sb + s * B_BYTES);
-          if (args.bkb == 128) {
+          const uint32_t d = tmem + acc * BN;
+          uint32_t wb = su32(sb);
+          if constexpr (NG > 1) {
+            int grp, m0, n0;
+            tile_at(t, grp, m0, n0);
+            wb += grp * WBLK;
+          }
+          bar_wait_sleep(&full[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t a0 = desc_none(su32(sa + s * A_BYTES), 16, 128);
+          const uint64_t b0 = desc_none(wb, BN * 16, 128);
 #pragma unroll
-            for (int k = 0; k < 128 / UMMA_K; ++k) {
-              mma(d, desc_sw128(ab + k * UMMA_K), desc_sw128(bb + k * UMMA_K), id,
-                  (kb | k) != 0 ? 1u : 0u);
-            }
-          } else {
+          for (int kh = 0; kh < 4; ++kh) {
 #pragma unroll
-            for (int k = 0; k < 64 / UMMA_K; ++k) {
-              mma(d, desc_sw(ab + k * UMMA_K, 64), desc_sw(bb + k * UMMA_K, 64), id,
-                  (kb | k) != 0 ? 1u : 0u);
+            for (int kw = 0; kw < 4; kw += 2) {
+              mma(d, a0 + (kh * row16 + kw), b0 + ((kh * 4 + kw) * BN), id, (kh | kw) != 0 ? 1u : 0u);
             }
           }
           commit(&empty[s]);
@@ -571,8 +675,42 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
             s = 0;
             ph ^= 1;
           }
+          commit(&tfull[acc]);
         }
-        commit(&tfull[acc]);
+      } else {
+        for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
+          const uint32_t acc = tl & 1;
+          if (tl >= 2) bar_wait_sleep(&tempty[acc], ((tl / 2) - 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t d = tmem + acc * BN;
+          for (int kb = 0; kb < nk; ++kb) {
+            bar_wait_sleep(&full[s], ph);
+            // gathered A was written by cp.async (generic proxy): make it
+            // visible to the tensor core's async-proxy reads
+            if (args.gather == 1) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t ab = su32(sa + s * A_BYTES), bb = su32(sb + s * B_BYTES);
+            if (args.bkb == 128) {
+#pragma unroll
+              for (int k = 0; k < 128 / UMMA_K; ++k) {
+                mma(d, desc_sw128(ab + k * UMMA_K), desc_sw128(bb + k * UMMA_K), id,
+                    (kb | k) != 0 ? 1u : 0u);
+              }
+            } else {
+#pragma unroll
+              for (int k = 0; k < 64 / UMMA_K; ++k) {
+                mma(d, desc_sw(ab + k * UMMA_K, 64), desc_sw(bb + k * UMMA_K, 64), id,
+                    (kb | k) != 0 ? 1u : 0u);
+              }
+            }
+            commit(&empty[s]);
+            if (++s == stages) {
+              s = 0;
+              ph ^= 1;
+            }
+          }
+          commit(&tfull[acc]);
+        }
       }
     }
   } else if (warp == STORE_WARP) {
@@ -610,6 +748,15 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
         uint8_t* base = slots + set * SET_BYTES;
         if (args.n_out > 0) {
           for (int blk = 0; blk < BN / SWZ; ++blk) {
+            if (args.gather == 3) {
+              // row band: output maps are [rows n*OH+oh][OW][cols]
+              const int q = m0 / BM;
+              tma_store3d(mo0, base + blk * (BM * SWZ), n0 + blk * SWZ, 0, q);
+              if (args.n_out > 1) {
+                tma_store3d(mo1, base + SLOT_BYTES + blk * (BM * SWZ), n0 + blk * SWZ, 0, q);
+              }
+              continue;
+            }
             tma_store2d(mo0, base + blk * (BM * SWZ), n0 + blk * SWZ, m0);
             if (args.n_out > 1) {
               tma_store2d(mo1, base + SLOT_BYTES + blk * (BM * SWZ), n0 + blk * SWZ, m0);
@@ -1011,6 +1158,49 @@ CUtensorMap bmap(const void* base, int64_t rows, int64_t cols, int64_t stride, i
   return m;
 }
 
+// tiled map of rank 3 or 4 over bytes (dims[0] innermost), cached like bmap
+CUtensorMap nd_map(const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+                   const cuuint32_t* box, int swz, int kind, int elem_bytes = 1) {
+  int64_t k[4] = {0, 0, 0, 0};
+  for (int i = 0; i < rank; ++i) k[i] = static_cast<int64_t>(dims[i]) << 20 | box[i];
+  const MapKey key{base, k[0], k[1], k[2], k[3],
+                   static_cast<int>(strides[0]), rank > 2 ? static_cast<int>(strides[1]) : 0,
+                   rank > 3 ? static_cast<int>(strides[2]) : 0, (kind * 16 + elem_bytes) * 1024 + swz};
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    auto it = map_cache().find(key);
+    if (it != map_cache().end()) return it->second;
+  }
+  CUtensorMap m;
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  const CUtensorMapSwizzle sw = swz == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : swz == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                            : CU_TENSOR_MAP_SWIZZLE_NONE;
+  const CUtensorMapDataType dt = elem_bytes == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT8;
+  if (encoder()(&m, dt, static_cast<cuuint32_t>(rank), const_cast<void*>(base),
+                dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+    throw std::runtime_error("cuTensorMapEncodeTiled failed (conv_tc rank-" + std::to_string(rank) + " map)");
+  }
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  if (map_cache().size() > 8192) map_cache().clear();
+  map_cache().emplace(key, m);
+  return m;
+}
+
+// the row-band producer (TcArgs::band_cols): a stride-1 conv over 16-byte
+// pixels whose output rows fit one tile, store-only epilogue shapes
+bool band_ok(const TcConvSpec& sp) {
+  static const bool off = std::getenv("QUANTC_NO_BAND") != nullptr;
+  const int sh = sp.prog.shape;
+  const bool store_only = sh == kShapeStore || sh == kShapeSqStore || sh == kShapeSqStoreId ||
+                          sh == kShapeSqStoreInt;
+  return !off && store_only && sp.gather && sp.ld == 16 && sp.C <= 16 && sp.sh == 1 && sp.sw == 1 &&
+         sp.KH == 4 && sp.KW == 4 && sp.OW <= BM && sp.OW + sp.KW - 1 <= 128 && sp.KH <= 16 &&
+         sp.KH * sp.KW * 16 <= sp.Kpad && sp.Kpad <= 256 && sp.O % 16 == 0 && sp.res_ptr == nullptr &&
+         sp.n_out >= 1 && sp.M == static_cast<int64_t>(sp.Nimg) * sp.OH * sp.OW;
+}
+
 int num_sms() {
   static int n = [] {
     int dev = 0, v = 148;
@@ -1023,15 +1213,19 @@ int num_sms() {
 
 // shared memory of one CTA: everything but the pipeline stages
 int smem_fixed(const TcArgs& a, int bn, int sets, bool shape) {
-  return 1024 + sets * (a.n_out + a.has_res - a.res_alias) * BM * bn + (2 * MAX_STAGES + 10) * 8 + 16 +
+  return 1024 + sets * (a.n_out + a.has_res - a.res_alias) * BM * bn + (2 * MAX_STAGES + 12) * 8 + 16 +
+         (a.gather == 3 ? a.groups * bn * a.g.KH * a.g.KW * 16 : 0) +
          static_cast<int>(sizeof(StageTables)) + 64 +
          (a.gather == 1 ? a.K / 16 * static_cast<int>(sizeof(int2)) : 0) +
          (shape ? ((a.N + bn - 1) / bn) * bn * 4 * a.groups + 64 * a.groups : 0);
 }
 
+int a_stage_bytes(const TcArgs& a) { return a.gather == 3 ? a.band_a_bytes : BM * a.bkb; }
+int b_stage_bytes(const TcArgs& a, int bn) { return a.gather == 3 ? 0 : bn * a.bkb; }
+
 // pipeline depth that fits next to `fixed` bytes (capped by what the K loop uses)
 int fit_stages(const TcArgs& a, int bn, int fixed) {
-  int stages = (SMEM_LIMIT - fixed) / (BM * a.bkb + bn * a.bkb);
+  int stages = (SMEM_LIMIT - fixed) / (a_stage_bytes(a) + b_stage_bytes(a, bn));
   const int nk = a.K / a.bkb;
   stages = stages > MAX_STAGES ? MAX_STAGES : stages;
   // the ring spans tiles: a CTA with several tiles prefetches the next tile's
@@ -1040,7 +1234,8 @@ int fit_stages(const TcArgs& a, int bn, int fixed) {
   // (measured neutral on ResNet-50; opt-in QUANTC_STAGES_SPAN=1)
   static const bool cap_nk = std::getenv("QUANTC_STAGES_SPAN") == nullptr;
   const int64_t tiles = static_cast<int64_t>(a.m_tiles) * (a.N + bn - 1) / bn * a.groups;
-  if (cap_nk || tiles <= num_sms()) return stages > nk + 1 ? nk + 1 : stages;
+  // (the row band loads one stage per tile: its ring always spans tiles)
+  if ((cap_nk && a.gather != 3) || tiles <= num_sms()) return stages > nk + 1 ? nk + 1 : stages;
   return stages;
 }
 
@@ -1080,13 +1275,17 @@ void launch_kernel(const TcMapsT<kMaxGroups>& all, const TcGroupsT<kMaxGroups>& 
 template <int BN, int SHAPE>
 void launch_tc(const TcMapsT<kMaxGroups>* maps, const TcGroupsT<kMaxGroups>* grp, TcArgs a,
                cudaStream_t s) {
-  const int stage_bytes = BM * a.bkb + BN * a.bkb;
+  const int stage_bytes = a_stage_bytes(a) + b_stage_bytes(a, BN);
   constexpr bool shape = SHAPE != kShapeGeneric && SHAPE != kShapeInt;  // btab in smem
   a.dbuf = dbuf_fits(a, BN, shape) ? 1 : 0;
   const int fixed = smem_fixed(a, BN, a.dbuf + 1, shape);
   int stages = fit_stages(a, BN, fixed);
   if (stages < 2) stages = 2;
   a.stages = stages;
+  if (a.gather == 3 && stages * a.band_a_bytes < a.groups * BN * a.bkb) {
+    // the weight rows are staged through the A ring before the band starts
+    throw std::runtime_error("conv_tc: row-band ring too small to stage the weights");
+  }
   const size_t smem = static_cast<size_t>(fixed) + static_cast<size_t>(stages) * stage_bytes;
   const int tiles = a.m_tiles * a.n_tiles * a.groups;
   const int grid = tiles < num_sms() ? tiles : num_sms();
@@ -1205,7 +1404,29 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
     maps.m[g][0] = bmap(x_of(g), sp.gather ? BM : sp.M, sp.gather ? BK : sp.Ktrue,
                         sp.gather ? BK : sp.lda, BK, BM, 128);
   }
-  if (im2col_ok(sp)) {
+  const bool band = band_ok(sp);
+  if (band) {
+    a.gather = 3;
+    a.bkb = sp.Kpad;
+    a.K = sp.Kpad;
+    a.m_tiles = sp.Nimg * sp.OH;
+    a.band_cols = sp.OW + sp.KW - 1;
+    // the last MMA rows read up to BM + KW - 1 pixels from the last band row
+    {
+      const int pitch = a.band_cols * 16;
+      a.band_a_bytes = ((sp.KH - 1) * pitch + (BM + sp.KW) * 16 + 1023) / 1024 * 1024;
+    }
+    for (int g = 0; g < a.groups; ++g) {
+      // the codes as [N][H][W*2] 8-byte elements (a 256-element box then
+      // spans a whole band row); one box = the KH rows of the band
+      const cuuint64_t dims[3] = {static_cast<cuuint64_t>(sp.W) * 2, static_cast<cuuint64_t>(sp.H),
+                                  static_cast<cuuint64_t>(sp.Nimg)};
+      const cuuint64_t str[2] = {static_cast<cuuint64_t>(sp.W) * 16,
+                                 static_cast<cuuint64_t>(sp.W) * sp.H * 16};
+      const cuuint32_t box[3] = {static_cast<cuuint32_t>(a.band_cols) * 2, static_cast<cuuint32_t>(sp.KH), 1};
+      maps.m[g][0] = nd_map(x_of(g), 3, dims, str, box, 0, 1, 8);
+    }
+  } else if (im2col_ok(sp)) {
     const int cbox = sp.ld % BK == 0 ? BK : 64;
     bool ok = true;
     for (int g = 0; g < a.groups && ok; ++g) {
@@ -1290,11 +1511,27 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
   }
   for (int g = 0; g < a.groups; ++g) {
     const int8_t* w = g == 0 ? sp.w : sp.wg[g - 1];
-    maps.m[g][1] = bmap(w, sp.O, sp.Kpad, sp.Kpad, a.bkb, BN, a.bkb);
+    if (band) {
+      // the whole [BN][Kpad] weight rows (staged, then transposed in smem)
+      maps.m[g][1] = bmap(w, sp.O, sp.Kpad, sp.Kpad, sp.Kpad, BN, 0);
+    } else {
+      maps.m[g][1] = bmap(w, sp.O, sp.Kpad, sp.Kpad, a.bkb, BN, a.bkb);
+    }
     for (int o = 0; o < 2; ++o) {
       void* out = g == 0 ? sp.out_ptr[o] : sp.out_ptrg[g - 1][o];
-      maps.m[g][2 + o] = o < sp.n_out ? bmap(out, sp.M, sp.out_cols[o], sp.out_ld[o], swz, BM, swz)
-                                      : maps.m[g][1];
+      if (o >= sp.n_out) {
+        maps.m[g][2 + o] = maps.m[g][1];
+      } else if (band) {
+        // [n*OH + oh][ow][cols]: the tile's rows >= OW fall outside and are clipped
+        const cuuint64_t dims[3] = {static_cast<cuuint64_t>(sp.out_cols[o]), static_cast<cuuint64_t>(sp.OW),
+                                    static_cast<cuuint64_t>(sp.Nimg) * sp.OH};
+        const cuuint64_t str[2] = {static_cast<cuuint64_t>(sp.out_ld[o]),
+                                   static_cast<cuuint64_t>(sp.out_ld[o]) * sp.OW};
+        const cuuint32_t box[3] = {static_cast<cuuint32_t>(swz), static_cast<cuuint32_t>(BM), 1};
+        maps.m[g][2 + o] = nd_map(out, 3, dims, str, box, swz, 3);
+      } else {
+        maps.m[g][2 + o] = bmap(out, sp.M, sp.out_cols[o], sp.out_ld[o], swz, BM, swz);
+      }
     }
     const void* res = g == 0 ? sp.res_ptr : sp.res_ptrg[g - 1];
     maps.m[g][4] = a.has_res ? bmap(res, sp.M, sp.res_cols, sp.res_ld, swz, BM, swz) : maps.m[g][1];

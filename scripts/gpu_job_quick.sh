@@ -10,3 +10,6 @@ timeout 600 python bench.py --no-realized --no-traffic --no-search --no-configs 
 if [ -n "$AB_ENV" ]; then
   env $AB_ENV timeout 600 python bench.py --no-realized --no-traffic --no-search --no-configs --no-cpu-baseline > gpurun_out/${TAG}_bench_ab.log 2> gpurun_out/${TAG}_bench_ab.err
 fi
+if [ -n "$AB_ENV" ] && [ -n "$AB_LAUNCHES" ]; then
+  env $AB_ENV GROUP=4 timeout 600 ncu $M --log-file gpurun_out/${TAG}_launches_ab.csv python scripts/profile_step.py > gpurun_out/${TAG}_ncu_ab.log 2>&1
+fi
