@@ -690,17 +690,21 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
             if (args.gather == 1) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t ab = su32(sa + s * A_BYTES), bb = su32(sb + s * B_BYTES);
+            // one descriptor per operand and stage; the k-th 32-byte K step
+            // adds k * 2 to the start-address field (addr >> 4): the single
+            // issuing thread is the bottleneck of the narrow layers, so no
+            // per-MMA descriptor rebuild
             if (args.bkb == 128) {
+              const uint64_t a0 = desc_sw128(ab), b0 = desc_sw128(bb);
 #pragma unroll
               for (int k = 0; k < 128 / UMMA_K; ++k) {
-                mma(d, desc_sw128(ab + k * UMMA_K), desc_sw128(bb + k * UMMA_K), id,
-                    (kb | k) != 0 ? 1u : 0u);
+                mma(d, a0 + 2 * k, b0 + 2 * k, id, (kb | k) != 0 ? 1u : 0u);
               }
             } else {
+              const uint64_t a0 = desc_sw(ab, 64), b0 = desc_sw(bb, 64);
 #pragma unroll
               for (int k = 0; k < 64 / UMMA_K; ++k) {
-                mma(d, desc_sw(ab + k * UMMA_K, 64), desc_sw(bb + k * UMMA_K, 64), id,
-                    (kb | k) != 0 ? 1u : 0u);
+                mma(d, a0 + 2 * k, b0 + 2 * k, id, (kb | k) != 0 ? 1u : 0u);
               }
             }
             commit(&empty[s]);
