@@ -822,11 +822,22 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
       const int64_t m = static_cast<int64_t>(m0) + r;
       const uint32_t tbase = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
       if constexpr (SHAPE == kShapeInt) {
-        // realized-graph integer conv/dense: exact int64 epilogue (IntEpi)
+        // realized-graph integer conv/dense: the exact int64 chain of
+        // int_epi_value (fused.cuh), restructured for throughput: per-tile
+        // scalars in registers, the bias / zero-point term once per chunk,
+        // each fused post op applied to the chunk's 16 values under one
+        // warp-uniform branch (no per-element dispatch, no local memory)
         const IntEpi& ie = args.iepi;
+        const int64_t zp0 = ie.zp0, amin = ie.acc_min, amax = ie.acc_max;
+        const int npost = ie.n_post;
+        const int32_t ohw = ie.OHW;
         const bool row_ok = m < args.M;
-        const int64_t img = row_ok ? m / ie.OHW : 0;
-        const int64_t hw = row_ok ? m - img * ie.OHW : 0;
+        int32_t img = 0, hw = 0;
+        if (row_ok) {
+          img = static_cast<int32_t>(static_cast<uint32_t>(m) / static_cast<uint32_t>(ohw));
+          hw = static_cast<int32_t>(m) - img * ohw;
+        }
+        const int64_t row_base = static_cast<int64_t>(img) * args.N * ohw + hw;
 #pragma unroll 1
         for (int c = part; c < NCHUNK; c += PARTS) {
           const int c0 = c * EW;
@@ -834,13 +845,49 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
           tmem_ld<EW>(tbase + c0, d);
           tmem_wait(d);
           const int n = n0 + c0;
-          if (!row_ok) continue;
-#pragma unroll 4
+          if (!row_ok || n >= args.N) continue;
+          int64_t v[EW];
+#pragma unroll
           for (int j = 0; j < EW; ++j) {
-            const int o = n + j;
-            if (o >= args.N) break;
-            const int64_t flat = (img * args.N + o) * ie.OHW + hw;
-            ie.y[flat] = int_epi_value(ie, static_cast<int32_t>(d[j]), o, flat);
+            const int o = n + j < args.N ? n + j : args.N - 1;
+            int64_t off = 0;
+            if (ie.wsum) off -= zp0 * static_cast<int64_t>(__ldg(ie.wsum + o));
+            if (ie.bias) off += __ldg(ie.bias + o);
+            v[j] = static_cast<int64_t>(static_cast<int32_t>(d[j])) + off;
+            if (v[j] < amin || v[j] > amax) {
+              if (ie.trap && n + j < args.N) {
+                atomicMin(ie.trap, static_cast<unsigned long long>(row_base + static_cast<int64_t>(n + j) * ohw));
+              }
+              v[j] = v[j] < amin ? amin : amax;
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            if (k >= npost) break;
+            const IntEpi::Post& pp = ie.post[k];
+            if (pp.kind == kPostRelu) {
+              const int64_t z = pp.out_zp;
+#pragma unroll
+              for (int j = 0; j < EW; ++j) v[j] = v[j] > z ? v[j] : z;
+            } else {
+              const int64_t mult = pp.mult, in_zp = pp.in_zp, out_zp = pp.out_zp;
+              const int64_t qmin = pp.q_min, qmax = pp.q_max;
+              const int sh = pp.shift;
+              const int64_t nudge = sh > 0 ? (int64_t{1} << (sh - 1)) : 0;
+#pragma unroll
+              for (int j = 0; j < EW; ++j) {
+                const int64_t pr = (v[j] - in_zp) * mult;
+                int64_t q = pr;
+                if (sh > 0) q = pr >= 0 ? (pr + nudge) >> sh : -((-pr + nudge) >> sh);
+                q += out_zp;
+                v[j] = q < qmin ? qmin : (q > qmax ? qmax : q);
+              }
+            }
+          }
+          int32_t* yc = ie.y + row_base + static_cast<int64_t>(n) * ohw;
+#pragma unroll
+          for (int j = 0; j < EW; ++j) {
+            if (n + j < args.N) yc[static_cast<int64_t>(j) * ohw] = static_cast<int32_t>(v[j]);
           }
         }
       } else if constexpr (shape_is_int_fold(SHAPE)) {
