@@ -406,7 +406,7 @@ struct Runner {
     return h == ~0ull ? -1 : static_cast<int64_t>(h);
   }
 
-  DType acc_dtype_of(const Node& n) {
+  DType acc_dtype_of(const Node& n) const {
     if (!n.has_attr("acc_dtype")) {
       throw EvalError("node " + std::to_string(n.id) + " (" + op_name(n.op) +
                       ") missing accumulator dtype annotation");
@@ -478,9 +478,9 @@ struct Runner {
   bool exec_conv_int_simt(int i, const kern::ConvShape& cs, const DevTensor& d,
                           const DevTensor& w, const DevTensor* b, DType acc,
                           const std::vector<int64_t>& zps);
-  std::vector<int> fused_chain(int i) const;
+  std::vector<int> fused_chain(int i, bool allow_add = false) const;
   DType chain_dtype(const std::vector<int>& chain, DType acc) const;
-  void fill_posts(kern::IntEpi& ie, const std::vector<int>& chain) const;
+  void fill_posts(kern::IntEpi& ie, int i, const std::vector<int>& chain) const;
   void finish_int(int i, const std::vector<int>& chain, const DevTensor& y, const kern::ConvShape& cs,
                   const DevTensor& d, const DevTensor& w, const DevTensor* b,
                   const std::vector<int64_t>& zps);
@@ -549,11 +549,38 @@ bool Runner::exec_conv_int_tc(int i, bool dense, const kern::ConvShape& cs, cons
   const bool pad_fill = zps.at(0) != 0 && (cs.ph != 0 || cs.pw != 0);
   const int pph = pad_fill ? cs.ph : 0, ppw = pad_fill ? cs.pw : 0;
   const int HP = cs.H + 2 * pph, WP = cs.W + 2 * ppw;
-  auto xcodes = device_alloc(static_cast<size_t>(cs.N) * HP * WP * ld + 64);
-  kern::pack_i32_nhwc(d.i(), static_cast<uint8_t*>(xcodes.get()), cs.N, cs.C, cs.H, cs.W, pph,
-                      ppw, ld, static_cast<int32_t>(zps.at(0)), S());
-  const std::vector<int> chain = fused_chain(i);
-  DevTensor y = out_like(chain.empty() ? i : chain.back(), chain_dtype(chain, acc));
+  std::shared_ptr<void> xcodes;
+  if (d.codes && d.codes_ld == ld && !pad_fill) {
+    xcodes = d.codes;  // the producer's epilogue already wrote them
+  } else {
+    xcodes = device_alloc(static_cast<size_t>(cs.N) * HP * WP * ld + 64);
+    kern::pack_i32_nhwc(d.i(), static_cast<uint8_t*>(xcodes.get()), cs.N, cs.C, cs.H, cs.W, pph,
+                        ppw, ld, static_cast<int32_t>(zps.at(0)), S());
+  }
+  const std::vector<int> chain = fused_chain(i, true);
+  const int last = chain.empty() ? i : chain.back();
+  const DType ydt = chain_dtype(chain, acc);
+  DevTensor y = out_like(last, ydt);
+  // side output of the final values' code bytes when an integer conv/dense
+  // consumes them (its input pack is then skipped)
+  int64_t code_rows = 0;
+  int code_ld = 0;
+  if (ydt.width() <= 8 && !keep[static_cast<size_t>(last)]) {
+    const auto& steps = plan.steps();
+    for (size_t j = static_cast<size_t>(last) + 1; j < steps.size(); ++j) {
+      const auto& sj = steps[j];
+      const OpKind op = sj.node->op;
+      if ((op == OpKind::kConv2d || op == OpKind::kDense) && !sj.in.empty() && sj.in[0] == last) {
+        code_rows = static_cast<int64_t>(cs.N) * cs.OH * cs.OW;
+        code_ld = (cs.O + 15) / 16 * 16;
+        break;
+      }
+    }
+  }
+  if (code_rows > 0 && !dense) {
+    y.codes = device_alloc(static_cast<size_t>(code_rows) * code_ld + 64);
+    y.codes_ld = code_ld;
+  }
   kern::TcConvSpec sp{};
   sp.x = static_cast<const int8_t*>(xcodes.get());
   sp.w = static_cast<const int8_t*>(wcodes.get());
@@ -587,7 +614,9 @@ bool Runner::exec_conv_int_tc(int i, bool dense, const kern::ConvShape& cs, cons
   ie.acc_max = acc.max_value();
   ie.OHW = cs.OH * cs.OW;
   ie.a_unsigned = d.dtype.is_signed() ? 0 : 1;
-  fill_posts(ie, chain);
+  ie.codes = static_cast<uint8_t*>(y.codes.get());
+  ie.codes_ld = y.codes_ld;
+  fill_posts(ie, i, chain);
   kern::tc_conv(sp, S());
   device::counters().tcgen05_gemms++;
   finish_int(i, chain, y, cs, d, w, b, zps);
@@ -597,12 +626,15 @@ bool Runner::exec_conv_int_tc(int i, bool dense, const kern::ConvShape& cs, cons
 // the sole-consumer chain after integer conv/dense step i that the
 // epilogue absorbs: up to three requantize / relu steps, each the only
 // consumer of the previous value and not a kept (output) value
-std::vector<int> Runner::fused_chain(int i) const {
+std::vector<int> Runner::fused_chain(int i, bool allow_add) const {
   std::vector<int> chain;
   if (!spec.integer_regime) return chain;
+  static const bool no_add = std::getenv("QUANTC_NO_INT_ADD_FUSION") != nullptr;
   const auto& steps = plan.steps();
   int cur = i;
-  while (chain.size() < 3) {
+  DType cur_dt = acc_dtype_of(*steps[static_cast<size_t>(i)].node);
+  bool added = false;
+  while (static_cast<int>(chain.size()) < kern::kMaxIntPosts) {
     if (steps[static_cast<size_t>(cur)].uses != 1 || keep[static_cast<size_t>(cur)]) break;
     int next = -1;
     for (size_t j = static_cast<size_t>(cur) + 1; j < steps.size(); ++j) {
@@ -615,10 +647,32 @@ std::vector<int> Runner::fused_chain(int i) const {
     if (next < 0) break;
     const auto& sn = steps[static_cast<size_t>(next)];
     const OpKind op = sn.node->op;
+    if (op == OpKind::kAdd && allow_add && !no_add && sn.in.size() == 2 && !added) {
+      // an integer add whose other operand is already computed (an earlier
+      // step), of the same batched shape, and whose accumulator provably
+      // cannot overflow given both operands' dtypes (no trap to report)
+      const int other = sn.in[0] == cur ? sn.in[1] : sn.in[0];
+      if (other < 0 || other >= i || sn.in[0] == sn.in[1]) break;
+      const DevTensor& ov = vals[static_cast<size_t>(other)];
+      if (!ov.buf || !ov.dtype.is_integer() || ov.batched != plan.batched(cur) ||
+          ov.per_numel() != shape_numel(plan.shape(cur))) {
+        break;
+      }
+      const DType add_acc = acc_dtype_of(*sn.node);
+      const int64_t lo = cur_dt.min_value() + ov.dtype.min_value();
+      const int64_t hi = cur_dt.max_value() + ov.dtype.max_value();
+      if (lo < add_acc.min_value() || hi > add_acc.max_value()) break;
+      chain.push_back(next);
+      cur = next;
+      cur_dt = add_acc;
+      added = true;  // one add per chain (the epilogue prefetches one operand)
+      continue;
+    }
     if (op != OpKind::kRequantize && op != OpKind::kRelu) break;
     if (sn.in.size() != 1) break;
     chain.push_back(next);
     cur = next;
+    if (op == OpKind::kRequantize) cur_dt = parse_dtype(sn.node->attr<std::string>("out_dtype"));
   }
   return chain;
 }
@@ -629,12 +683,14 @@ DType Runner::chain_dtype(const std::vector<int>& chain, DType acc) const {
   for (int j : chain) {
     const Node& n = *plan.steps()[static_cast<size_t>(j)].node;
     if (n.op == OpKind::kRequantize) dt = parse_dtype(n.attr<std::string>("out_dtype"));
+    if (n.op == OpKind::kAdd) dt = parse_dtype(n.attr<std::string>("acc_dtype"));
   }
   return dt;
 }
 
-void Runner::fill_posts(kern::IntEpi& ie, const std::vector<int>& chain) const {
+void Runner::fill_posts(kern::IntEpi& ie, int i, const std::vector<int>& chain) const {
   ie.n_post = 0;
+  int run = i;  // the step whose value the chain element consumes
   for (int j : chain) {
     const Node& n = *plan.steps()[static_cast<size_t>(j)].node;
     kern::IntEpi::Post& p = ie.post[ie.n_post++];
@@ -642,6 +698,12 @@ void Runner::fill_posts(kern::IntEpi& ie, const std::vector<int>& chain) const {
     if (n.op == OpKind::kRelu) {
       p.kind = kern::kPostRelu;
       p.out_zp = static_cast<int32_t>(n.attr_or<int64_t>("zero_point", 0));
+    } else if (n.op == OpKind::kAdd) {
+      // the operand that is not the chain's running value
+      const auto& in = plan.steps()[static_cast<size_t>(j)].in;
+      const int other = in[0] == run ? in[1] : in[0];
+      p.kind = kern::kPostAdd;
+      p.other = vals[static_cast<size_t>(other)].i();
     } else {
       p.kind = kern::kPostRequantize;
       p.mult = n.attr<int64_t>("multiplier");
@@ -651,6 +713,7 @@ void Runner::fill_posts(kern::IntEpi& ie, const std::vector<int>& chain) const {
       p.q_min = static_cast<int32_t>(n.attr<int64_t>("q_min"));
       p.q_max = static_cast<int32_t>(n.attr<int64_t>("q_max"));
     }
+    run = j;
   }
 }
 
@@ -747,7 +810,7 @@ bool Runner::exec_conv_int_simt(int i, const kern::ConvShape& cs, const DevTenso
   sp.i16 = i16;
   sp.u8 = u8;
   sp.ie = int_epi(y, b, wsum.get(), trap_ptr(), acc, cs, zps);
-  fill_posts(sp.ie, chain);
+  fill_posts(sp.ie, i, chain);
   kern::conv_int_simt(sp, S());
   device::counters().simt_int_convs++;
   finish_int(i, chain, y, cs, d, w, b, zps);

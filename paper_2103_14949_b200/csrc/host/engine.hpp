@@ -34,6 +34,11 @@ struct DevTensor {
   DType dtype = f32;          // float32 or integer (int32 storage)
   std::vector<int64_t> shape; // batched: per-sample shape; else full shape
   bool batched = false;
+  // integer values of <= 8 bits may also carry their NHWC code bytes
+  // [pixels][codes_ld] (written by the producing conv's epilogue): an integer
+  // conv consuming them without a zero-point border skips its pack pass
+  std::shared_ptr<void> codes;
+  int codes_ld = 0;
 
   int64_t per_numel() const { return shape_numel(shape); }
   int64_t numel(int batch) const { return batched ? per_numel() * batch : per_numel(); }

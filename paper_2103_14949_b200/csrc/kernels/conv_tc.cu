@@ -838,11 +838,31 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
           hw = static_cast<int32_t>(m) - img * ohw;
         }
         const int64_t row_base = static_cast<int64_t>(img) * args.N * ohw + hw;
+        // a fused add's operand (at most one per chain): loaded one chunk
+        // ahead, so its DRAM latency overlaps the previous chunk's math
+        const int32_t* addp = nullptr;
+#pragma unroll
+        for (int k = 0; k < kMaxIntPosts; ++k) {
+          if (k < npost && ie.post[k].kind == kPostAdd) addp = ie.post[k].other;
+        }
+        int32_t pre[EW];
+        auto load_other = [&](int cc) {
+          const int nn = n0 + cc * EW;
+#pragma unroll
+          for (int j = 0; j < EW; ++j) {
+            pre[j] = (row_ok && nn + j < args.N) ? __ldg(addp + row_base + static_cast<int64_t>(nn + j) * ohw) : 0;
+          }
+        };
+        if (addp) load_other(part);
 #pragma unroll 1
         for (int c = part; c < NCHUNK; c += PARTS) {
           const int c0 = c * EW;
           uint32_t d[EW];
           tmem_ld<EW>(tbase + c0, d);
+          int32_t cur[EW];
+#pragma unroll
+          for (int j = 0; j < EW; ++j) cur[j] = pre[j];
+          if (addp && c + PARTS < NCHUNK) load_other(c + PARTS);
           tmem_wait(d);
           const int n = n0 + c0;
           if (!row_ok || n >= args.N) continue;
@@ -862,13 +882,17 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
             }
           }
 #pragma unroll
-          for (int k = 0; k < 3; ++k) {
+          for (int k = 0; k < kMaxIntPosts; ++k) {
             if (k >= npost) break;
             const IntEpi::Post& pp = ie.post[k];
             if (pp.kind == kPostRelu) {
               const int64_t z = pp.out_zp;
 #pragma unroll
               for (int j = 0; j < EW; ++j) v[j] = v[j] > z ? v[j] : z;
+            } else if (pp.kind == kPostAdd) {
+              // the fused add's other operand (host-proven: no overflow)
+#pragma unroll
+              for (int j = 0; j < EW; ++j) v[j] += cur[j];
             } else {
               const int64_t mult = pp.mult, in_zp = pp.in_zp, out_zp = pp.out_zp;
               const int64_t qmin = pp.q_min, qmax = pp.q_max;
@@ -888,6 +912,16 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
 #pragma unroll
           for (int j = 0; j < EW; ++j) {
             if (n + j < args.N) yc[static_cast<int64_t>(j) * ohw] = static_cast<int32_t>(v[j]);
+          }
+          if (ie.codes) {
+            uint32_t w4[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int j = 0; j < EW; ++j) {
+              if (n + j < args.N) w4[j >> 2] |= (static_cast<uint32_t>(v[j]) & 0xFFu) << (8 * (j & 3));
+            }
+            *reinterpret_cast<int4*>(ie.codes + m * ie.codes_ld + n) =
+                make_int4(static_cast<int>(w4[0]), static_cast<int>(w4[1]), static_cast<int>(w4[2]),
+                          static_cast<int>(w4[3]));
           }
         }
       } else if constexpr (shape_is_int_fold(SHAPE)) {

@@ -661,6 +661,10 @@ __device__ __forceinline__ int32_t int_epi_value(const IntEpi& ie, int64_t acc, 
       v = v > pp.out_zp ? v : pp.out_zp;  // relu int: max(x, zero_point)
       continue;
     }
+    if (pp.kind == kPostAdd) {
+      v += __ldg(pp.other + flat);  // host-proven inside the add's accumulator range
+      continue;
+    }
     // requantize: fixed_point_rescale, round half away from zero
     const int64_t p = (v - pp.in_zp) * pp.mult;
     int64_t q = p;

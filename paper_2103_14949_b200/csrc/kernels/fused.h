@@ -205,6 +205,7 @@ QC_HD constexpr bool shape_is_int_fold(int s) {
 //   v outside [acc_min, acc_max] -> trap (lowest flat index) or saturate
 //   requantize (optional): q = clamp(rescale(v - in_zp) + out_zp, q_min, q_max)
 //   y[((img*O + o)*OH + oh)*OW + ow] = v or q   (int32, NCHW like Tensor)
+constexpr int kMaxIntPosts = 5;
 struct IntEpi {
   int32_t* y;
   const int32_t* bias;  // may be null
@@ -214,17 +215,23 @@ struct IntEpi {
   // fused elementwise chain after the accumulator clamp (sole-consumer
   // requantize / relu nodes, reference interpreter.cpp:326-336, :464-482)
   struct Post {
-    int32_t kind;   // kPostRequantize or kPostRelu
+    int32_t kind;   // kPostRequantize, kPostRelu or kPostAdd
     int32_t shift;  // requantize
     int64_t mult;   // requantize
     int32_t in_zp, out_zp, q_min, q_max;  // requantize; relu: out_zp = zero point
+    const int32_t* other;  // add: the other operand (same flat indexing as y)
   };
-  Post post[3];
+  Post post[kMaxIntPosts];
   int32_t n_post;
+  // optional side output: the final values' low bytes as NHWC codes
+  // [M][codes_ld] (channels >= O zero) — the next integer conv's packed
+  // input, so it skips its pack pass
+  uint8_t* codes;
+  int32_t codes_ld;
   int32_t OHW;  // output pixels per image (1 for dense)
   int32_t a_unsigned;  // A codes are uint8 (tcgen05 unsigned A)
 };
-enum : int32_t { kPostRequantize = 1, kPostRelu = 2 };
+enum : int32_t { kPostRequantize = 1, kPostRelu = 2, kPostAdd = 3 };
 
 // kernels receive the stage's table block in global memory
 struct ProgArgs {
