@@ -936,6 +936,14 @@ void FastPlan::compile() {
           st->gather = !(st->taps == 1 && st->sh == 1 && st->sw == 1 && st->ph == 0 &&
                          st->pw == 0 && dv.ld == st->C);
           st->ldk = st->gather ? static_cast<int>(dv.ld) : st->C;
+          // 64-channel stride-1 KxK convs: weight taps at a 128-byte stride
+          // (zero channels 64..127) so the conv runs on the 2-D band producer
+          // (conv_tc.cu TcArgs::b2_*), which reads 128-byte channel chunks
+          static const bool no_band2 = std::getenv("QUANTC_BAND2") == nullptr;  // opt-in, conv_tc.cu
+          if (!no_band2 && st->gather && dv.ld == 64 && st->C == 64 && st->taps > 1 && st->sh == 1 &&
+              st->sw == 1 && st->ph < st->KH && st->pw < st->KW && st->OW + st->KW - 1 <= 128 && !dv.s2d) {
+            st->ldk = 128;
+          }
           st->Ktrue = st->gather ? st->taps * st->ldk : st->C;
           // tiny-channel convs (e.g. the RGB stem, C=3 in 16-byte rows): pack
           // dense im2col rows k = tap*C + c first, then run the GEMM direct
@@ -1725,6 +1733,7 @@ void FastPlan::gemm_spec(Run& r, size_t si, kern::TcConvSpec& sp) {
   sp.W = st.W;
   sp.C = st.C;
   sp.ld = static_cast<int>(dv.ld);
+  sp.ldk = st.ldk;
   sp.KH = st.KH;
   sp.KW = st.KW;
   sp.sh = st.sh;

@@ -129,6 +129,14 @@ __device__ __forceinline__ void tma4d(const CUtensorMap* m, uint64_t* bar, void*
       "l"(reinterpret_cast<uint64_t>(m)), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
+__device__ __forceinline__ void tma_store4d(const CUtensorMap* m, const void* src, int c0, int c1,
+                                            int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(m)),
+      "r"(su32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
 __device__ __forceinline__ void tma_store3d(const CUtensorMap* m, const void* src, int c0, int c1,
                                             int c2) {
   asm volatile(
@@ -188,6 +196,7 @@ __device__ __forceinline__ void commit(uint64_t* b) {
 struct TcGeom {
   const int8_t* x;  // gather source: NHWC codes [N*H*W, ld]
   int N, H, W, C, ld, KH, KW, sh, sw, ph, pw, OH, OW;
+  int ldk;          // K stride of one tap in the weight rows (>= C; usually ld)
 };
 
 struct TcArgs {
@@ -225,6 +234,22 @@ struct TcArgs {
   // width OW clips the tile's rows OW..127.
   int band_cols;
   int band_a_bytes;  // A stage of the band (covers the MMA's reads past the band's end)
+  // gather == 4, the 2-D band of a stride-1 KxK conv over 128-byte channel
+  // chunks: one tile = R output rows of one image laid out at a pitch of P =
+  // 128 / R pixels (P >= OW + KW - 1; tile row q -> output (r0 + q / P,
+  // q % P)).  Per tile the producer TMA-loads the R + KH - 1 input rows from
+  // pixel -pw as one SW128 box per 128-byte channel chunk (zero outside the
+  // image); tap (kh, kw) of chunk c is that band shifted by kh*P + kw pixel
+  // rows (the SW128 swizzle is address-based: a descriptor may start at any
+  // 128-byte row — scripts/probes/umma_shift_probe.cu), so the 9 taps of a
+  // 3x3 conv read one load instead of nine im2col boxes.  B is the usual
+  // [O][Kpad] ring with K = tap * nchunk * 128 + chunk * 128 + c.
+  int b2_P, b2_R, b2_nchunk, b2_oh_tiles;
+  int b2_chunk_bytes;  // one channel chunk's band region
+  int b2_bytes;        // one band buffer (nchunk chunks), double-buffered
+  int b2_nbuf;         // band buffers in flight (2..4)
+  int b2_wres;         // 1: the group's whole [BN][Kpad] weight block stays resident
+                       // (reloaded when a CTA's tiles move to the next group)
 };
 
 // the tensor maps of NG groups: A, B, code outputs 0/1, residual
@@ -248,6 +273,12 @@ template <>
 struct TcGroupsT<1> {
   int unused;
 };
+
+// the grouped kernel's parameter block (maps + args + group operands) must
+// stay within the classic 4 KB kernel-parameter limit: past it the launch
+// fails with cudaErrorInvalidValue
+static_assert(sizeof(TcMapsT<kMaxGroups>) + sizeof(TcArgs) + sizeof(TcGroupsT<kMaxGroups>) <= 4096,
+              "tc_conv_kernel parameter block exceeds 4 KB");
 
 template <int W>
 __device__ __forceinline__ void tmem_ld(uint32_t addr, uint32_t (&d)[W]);
@@ -297,8 +328,11 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sa = smem;
-  uint8_t* sb = sa + stages * A_BYTES;
-  uint8_t* slots = sb + (args.gather == 3 ? args.groups * WBLK : stages * B_BYTES);  // 1024-aligned
+  // gather == 4: two band buffers, then the B ring (A_BYTES unused)
+  uint8_t* sb = sa + (args.gather == 4 ? args.b2_nbuf * args.b2_bytes : stages * A_BYTES);
+  uint8_t* slots = sb + (args.gather == 3 ? args.groups * WBLK
+                         : (args.gather == 4 && args.b2_wres) ? (args.K / args.bkb) * B_BYTES
+                                                               : stages * B_BYTES);  // 1024-aligned
   const int n_slots = args.n_out + args.has_res - args.res_alias;
   const uint32_t SET_BYTES = n_slots * SLOT_BYTES;  // one slot set
   uint64_t* full = reinterpret_cast<uint64_t*>(slots + (args.dbuf + 1) * SET_BYTES);
@@ -309,7 +343,11 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
   uint64_t* sfull = rfull + 2;    // [2] epilogue warps wrote a slot set
   uint64_t* sfree = sfull + 2;    // [2] a slot set's stores drained (reusable)
   uint64_t* bres = sfree + 2;     // row band: the weight blocks landed (staging)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 2);
+  uint64_t* bandf = bres + 2;     // [4] 2-D band buffer loaded
+  uint64_t* bande = bandf + 4;    // [4] 2-D band buffer consumed by the MMAs
+  uint64_t* wfull = bande + 4;    // resident weights landed (one phase per group switch)
+  uint64_t* wfree = wfull + 1;    // resident weights no longer read by the MMAs
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wfree + 1);
   StageTables* tabs = reinterpret_cast<StageTables*>(tmem_slot + 4);
   // gather K-chunk table: chunk q (16 bytes of K) = channel run c..c+15 of tap
   // (kh, kw); x = byte offset from the row's (ih0, iw0) pixel, y = tap index
@@ -350,7 +388,7 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
     const TcGeom& g = args.g;
     for (int q = threadIdx.x; q < args.K / 16; q += blockDim.x) {
       const int k = q * 16;
-      const int tap = k / g.ld, c = k - tap * g.ld;
+      const int tap = k / g.ldk, c = k - tap * g.ldk;
       const int kh = tap / g.KW, kw = tap - kh * g.KW;
       const bool ok = tap < g.KH * g.KW && c < g.C;
       ktab[q] = ok ? make_int2((kh * g.W + kw) * g.ld + c, tap) : make_int2(0, 63);
@@ -401,6 +439,12 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
       bar_init(&sfree[a], 1);
     }
     bar_init(&bres[0], 1);
+    for (int a = 0; a < 4; ++a) {
+      bar_init(&bandf[a], 1);
+      bar_init(&bande[a], 1);
+    }
+    bar_init(wfull, 1);
+    bar_init(wfree, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == MMA_WARP) {
@@ -457,7 +501,56 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
   if (warp >= EPI_WARPS && warp < MMA_WARP) {
     // ================= producers =================
     const int p = threadIdx.x - EPI_WARPS * 32;  // 0..127 = tile row
-    if (args.gather == 3) {
+    if (args.gather == 4) {
+      if (p == 0) {
+        const TcGeom& g = args.g;
+        const int R = args.b2_R, P = args.b2_P, nch = args.b2_nchunk;
+        const uint32_t band_tx = static_cast<uint32_t>((R + g.KH - 1) * P * 128 * nch);
+        int wgrp = -1;      // group whose weights are resident
+        uint32_t wph = 0;   // phase of the next wfull completion
+        int s = 0;
+        uint32_t ph = 0;
+        bool wrapped = false;
+        uint32_t tl = 0;
+        for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
+          int grp, m0, n0;
+          tile_at(t, grp, m0, n0);
+          const int q = m0 / BM;  // tile index in the group: img * oh_tiles + row tile
+          const int img = q / args.b2_oh_tiles, r0 = (q - img * args.b2_oh_tiles) * R;
+          const uint32_t nb = static_cast<uint32_t>(args.b2_nbuf);
+          const uint32_t b = tl % nb, use = tl / nb;
+          if (tl >= nb) bar_wait_sleep(&bande[b], (use - 1) & 1);
+          bar_expect(&bandf[b], band_tx);
+          uint8_t* band = sa + b * args.b2_bytes;
+          for (int c = 0; c < nch; ++c) {
+            tma4d(&maps.m[grp][0], &bandf[b], band + c * args.b2_chunk_bytes, c * 128, -g.pw,
+                  r0 - g.ph, img);
+          }
+          const CUtensorMap* mb = &maps.m[grp][1];
+          if (args.b2_wres) {
+            if (grp != wgrp) {
+              // the MMAs of the previous group's last tile must be done with it
+              if (wgrp >= 0) bar_wait_sleep(wfree, wph ^ 1);
+              bar_expect(wfull, B_BYTES * nk);
+              for (int kb = 0; kb < nk; ++kb) tma2d(mb, wfull, sb + kb * B_BYTES, kb * BK, n0);
+              wgrp = grp;
+              wph ^= 1;
+            }
+            continue;
+          }
+          for (int kb = 0; kb < nk; ++kb) {
+            if (wrapped) bar_wait_sleep(&empty[s], ph ^ 1);
+            bar_expect(&full[s], B_BYTES);
+            tma2d(mb, &full[s], sb + s * B_BYTES, kb * BK, n0);
+            if (++s == stages) {
+              s = 0;
+              ph ^= 1;
+              wrapped = true;
+            }
+          }
+        }
+      }
+    } else if (args.gather == 3) {
       // row band: per tile the KH input rows of output row (n, oh) and the
       // whole [tap][o][16 B] weight block, one stage
       if (p == 0) {
@@ -641,7 +734,61 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
       const uint32_t id = idesc(BM, BN) & ~(args.iepi.a_unsigned ? (1u << 7) : 0u);
       uint32_t tl = 0, ph = 0;
       int s = 0;
-      if (args.gather == 3) {
+      if (args.gather == 4) {
+        // 2-D band: K block kb = (tap, chunk); A = the tile's band shifted by
+        // kh*P + kw pixel rows in chunk c's region (SW128, 128-byte rows)
+        const int P = args.b2_P, nch = args.b2_nchunk, KW = args.g.KW;
+        int wgrp = -1;
+        uint32_t wph = 0;
+        for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
+          const uint32_t acc = tl & 1;
+          if (tl >= 2) bar_wait_sleep(&tempty[acc], ((tl / 2) - 1) & 1);
+          const uint32_t nb = static_cast<uint32_t>(args.b2_nbuf);
+          const uint32_t b = tl % nb;
+          bar_wait_sleep(&bandf[b], (tl / nb) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t d = tmem + acc * BN;
+          const uint32_t band = su32(sa + b * args.b2_bytes);
+          if (args.b2_wres) {
+            int grp, m0, n0;
+            tile_at(t, grp, m0, n0);
+            if (grp != wgrp) {
+              if (wgrp >= 0) commit(wfree);  // arrives when the old group's MMAs are done
+              bar_wait_sleep(wfull, wph);
+              asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+              wgrp = grp;
+              wph ^= 1;
+            }
+          }
+          int kh = 0, kw = 0, c = 0;
+          for (int kb = 0; kb < nk; ++kb) {
+            if (!args.b2_wres) bar_wait_sleep(&full[s], ph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint64_t a0 = desc_sw128(band + c * args.b2_chunk_bytes + (kh * P + kw) * 128);
+            const uint64_t b0 = desc_sw128(su32(sb + (args.b2_wres ? kb : s) * B_BYTES));
+#pragma unroll
+            for (int k = 0; k < 128 / UMMA_K; ++k) {
+              mma(d, a0 + 2 * k, b0 + 2 * k, id, (kb | k) != 0 ? 1u : 0u);
+            }
+            if (!args.b2_wres) {
+              commit(&empty[s]);
+              if (++s == stages) {
+                s = 0;
+                ph ^= 1;
+              }
+            }
+            if (++c == nch) {
+              c = 0;
+              if (++kw == KW) {
+                kw = 0;
+                ++kh;
+              }
+            }
+          }
+          commit(&bande[b]);
+          commit(&tfull[acc]);
+        }
+      } else if (args.gather == 3) {
         // row band, one stage per tile.  Tap pair (kh, kw..kw+1): A = band
         // row kh from pixel kw (LBO = one pixel), B = taps kh*4+kw..
         // ([tap][o][16 B], LBO = one tap); 4x4 taps (host-checked): the eight
@@ -752,6 +899,14 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
         uint8_t* base = slots + set * SET_BYTES;
         if (args.n_out > 0) {
           for (int blk = 0; blk < BN / SWZ; ++blk) {
+            if (args.gather == 4) {
+              // 2-D band: output maps are [N][OH][OW][cols], boxes {SWZ, P, R, 1}
+              const int q = m0 / BM;
+              const int img = q / args.b2_oh_tiles, r0 = (q - img * args.b2_oh_tiles) * args.b2_R;
+              tma_store4d(mo0, base + blk * (BM * SWZ), n0 + blk * SWZ, 0, r0, img);
+              if (args.n_out > 1) tma_store4d(mo1, base + SLOT_BYTES + blk * (BM * SWZ), n0 + blk * SWZ, 0, r0, img);
+              continue;
+            }
             if (args.gather == 3) {
               // row band: output maps are [rows n*OH+oh][OW][cols]
               const int q = m0 / BM;
@@ -1286,6 +1441,32 @@ bool band_ok(const TcConvSpec& sp) {
          sp.n_out >= 1 && sp.M == static_cast<int64_t>(sp.Nimg) * sp.OH * sp.OW;
 }
 
+// the 2-D band (TcArgs::b2_*): stride-1 KxK conv whose weight rows hold one
+// 128-byte chunk per (tap, chunk) (ldk a multiple of 128), store-only
+// epilogue shapes, no residual; returns the pixel pitch P (0: not eligible)
+int band2_pitch(const TcConvSpec& sp) {
+  // opt-in (QUANTC_BAND2=1): bit-exact, but measured slower than the im2col
+  // TMA path on ResNet-50's stage-1/2 3x3 layers (133 vs 100 us, 56 vs 46 us
+  // per 4-candidate launch) with resident weights and up to 4 bands in
+  // flight — neither the TMA, the tensor pipe (23%) nor the epilogue is
+  // saturated (profiles/r2_band2_ncu.md)
+  static const bool off = std::getenv("QUANTC_BAND2") == nullptr;
+  const int sh = sp.prog.shape;
+  const bool store_only = sh == kShapeStore || sh == kShapeSqStore || sh == kShapeSqStoreId ||
+                          sh == kShapeSqStoreInt;
+  const int ldk = sp.ldk > 0 ? sp.ldk : sp.ld;
+  if (off || !store_only || !sp.gather || sp.sh != 1 || sp.sw != 1 || ldk % 128 != 0 || ldk > 256 ||
+      sp.C > ldk || sp.res_ptr != nullptr || sp.n_out < 1 || sp.KH * sp.KW * ldk != sp.Kpad ||
+      sp.ph >= sp.KH || sp.pw >= sp.KW || sp.M != static_cast<int64_t>(sp.Nimg) * sp.OH * sp.OW) {
+    return 0;
+  }
+  int P = 8;
+  while (P < sp.OW + sp.KW - 1) P *= 2;
+  if (P > BM) return 0;
+  if (BM / P + sp.KH - 1 > 256) return 0;
+  return P;
+}
+
 int num_sms() {
   static int n = [] {
     int dev = 0, v = 148;
@@ -1298,18 +1479,20 @@ int num_sms() {
 
 // shared memory of one CTA: everything but the pipeline stages
 int smem_fixed(const TcArgs& a, int bn, int sets, bool shape) {
-  return 1024 + sets * (a.n_out + a.has_res - a.res_alias) * BM * bn + (2 * MAX_STAGES + 12) * 8 + 16 +
+  return 1024 + sets * (a.n_out + a.has_res - a.res_alias) * BM * bn + (2 * MAX_STAGES + 20) * 8 + 16 +
          (a.gather == 3 ? a.groups * bn * a.g.KH * a.g.KW * 16 : 0) +
+         (a.gather == 4 ? a.b2_nbuf * a.b2_bytes + (a.b2_wres ? bn * a.K : 0) : 0) +
          static_cast<int>(sizeof(StageTables)) + 64 +
          (a.gather == 1 ? a.K / 16 * static_cast<int>(sizeof(int2)) : 0) +
          (shape ? ((a.N + bn - 1) / bn) * bn * 4 * a.groups + 64 * a.groups : 0);
 }
 
-int a_stage_bytes(const TcArgs& a) { return a.gather == 3 ? a.band_a_bytes : BM * a.bkb; }
-int b_stage_bytes(const TcArgs& a, int bn) { return a.gather == 3 ? 0 : bn * a.bkb; }
+int a_stage_bytes(const TcArgs& a) { return a.gather == 3 ? a.band_a_bytes : a.gather == 4 ? 0 : BM * a.bkb; }
+int b_stage_bytes(const TcArgs& a, int bn) { return a.gather == 3 || (a.gather == 4 && a.b2_wres) ? 0 : bn * a.bkb; }
 
 // pipeline depth that fits next to `fixed` bytes (capped by what the K loop uses)
 int fit_stages(const TcArgs& a, int bn, int fixed) {
+  if (a_stage_bytes(a) + b_stage_bytes(a, bn) == 0) return 2;  // no ring (resident operands)
   int stages = (SMEM_LIMIT - fixed) / (a_stage_bytes(a) + b_stage_bytes(a, bn));
   const int nk = a.K / a.bkb;
   stages = stages > MAX_STAGES ? MAX_STAGES : stages;
@@ -1360,8 +1543,35 @@ void launch_kernel(const TcMapsT<kMaxGroups>& all, const TcGroupsT<kMaxGroups>& 
 template <int BN, int SHAPE>
 void launch_tc(const TcMapsT<kMaxGroups>* maps, const TcGroupsT<kMaxGroups>* grp, TcArgs a,
                cudaStream_t s) {
-  const int stage_bytes = a_stage_bytes(a) + b_stage_bytes(a, BN);
   constexpr bool shape = SHAPE != kShapeGeneric && SHAPE != kShapeInt;  // btab in smem
+  if (a.gather == 4) {
+    // the deepest band buffering (2..4 loads in flight: the band loads are
+    // latency-bound) that fits with resident weights and double-buffered
+    // slot sets; else with the B ring
+    static const bool no_wres = std::getenv("QUANTC_NO_WRES") != nullptr;
+    static const int max_nbuf = [] {
+      const char* e = std::getenv("QUANTC_BAND_BUFS");
+      return e ? std::max(2, std::min(4, std::atoi(e))) : 4;
+    }();
+    bool done = false;
+    for (int wres = no_wres ? 0 : 1; wres >= 0 && !done; --wres) {
+      for (int nb = max_nbuf; nb >= 2 && !done; --nb) {
+        TcArgs t = a;
+        t.b2_wres = wres;
+        t.b2_nbuf = nb;
+        const int ring = wres ? 0 : 2 * BN * a.bkb;
+        if (smem_fixed(t, BN, 2, shape) + ring + 1024 <= SMEM_LIMIT) {
+          a.b2_wres = wres;
+          a.b2_nbuf = nb;
+          done = true;
+        }
+      }
+    }
+    if (!done) {
+      a.b2_wres = 0;
+      a.b2_nbuf = 2;
+    }
+  }
   a.dbuf = dbuf_fits(a, BN, shape) ? 1 : 0;
   const int fixed = smem_fixed(a, BN, a.dbuf + 1, shape);
   int stages = fit_stages(a, BN, fixed);
@@ -1371,6 +1581,7 @@ void launch_tc(const TcMapsT<kMaxGroups>* maps, const TcGroupsT<kMaxGroups>* grp
     // the weight rows are staged through the A ring before the band starts
     throw std::runtime_error("conv_tc: row-band ring too small to stage the weights");
   }
+  const int stage_bytes = a_stage_bytes(a) + b_stage_bytes(a, BN);
   const size_t smem = static_cast<size_t>(fixed) + static_cast<size_t>(stages) * stage_bytes;
   const int tiles = a.m_tiles * a.n_tiles * a.groups;
   const int grid = tiles < num_sms() ? tiles : num_sms();
@@ -1451,8 +1662,9 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
   a.n_out = sp.n_out;
   a.has_res = sp.res_ptr != nullptr ? 1 : 0;
   a.res_alias = a.has_res && sp.n_out == 1 && sp.res_alias ? 1 : 0;
+  const int ldk = sp.ldk > 0 ? sp.ldk : sp.ld;
   a.g = TcGeom{sp.x, sp.Nimg, sp.H, sp.W, sp.C, sp.ld, sp.KH, sp.KW, sp.sh, sp.sw,
-               sp.ph, sp.pw, sp.OH, sp.OW};
+               sp.ph, sp.pw, sp.OH, sp.OW, ldk};
   a.bias = sp.bias;
   a.scale = sp.scale;
   {
@@ -1490,7 +1702,32 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
                         sp.gather ? BK : sp.lda, BK, BM, 128);
   }
   const bool band = band_ok(sp);
-  if (band) {
+  const int b2P = band2_pitch(sp);
+  const bool band2 = !band && b2P > 0;
+  if (band2) {
+    a.gather = 4;
+    a.bkb = BK;
+    a.K = sp.Kpad;
+    a.b2_P = b2P;
+    a.b2_R = BM / b2P;
+    a.b2_nchunk = ldk / BK;
+    a.b2_oh_tiles = (sp.OH + a.b2_R - 1) / a.b2_R;
+    a.m_tiles = sp.Nimg * a.b2_oh_tiles;
+    const int rows = (a.b2_R + sp.KH - 1) * b2P + sp.KW;  // rows the MMAs may touch
+    a.b2_chunk_bytes = (rows * 128 + 1023) / 1024 * 1024;
+    a.b2_bytes = a.b2_nchunk * a.b2_chunk_bytes;
+    for (int g = 0; g < a.groups; ++g) {
+      // NHWC codes as [N][H][W][C bytes]; one box = 128 channel bytes (past C
+      // read as zero) x P pixels from -pw x the band's input rows
+      const cuuint64_t dims[4] = {static_cast<cuuint64_t>(sp.C), static_cast<cuuint64_t>(sp.W),
+                                  static_cast<cuuint64_t>(sp.H), static_cast<cuuint64_t>(sp.Nimg)};
+      const cuuint64_t str[3] = {static_cast<cuuint64_t>(sp.ld), static_cast<cuuint64_t>(sp.W) * sp.ld,
+                                 static_cast<cuuint64_t>(sp.W) * sp.H * sp.ld};
+      const cuuint32_t box[4] = {128, static_cast<cuuint32_t>(b2P),
+                                 static_cast<cuuint32_t>(a.b2_R + sp.KH - 1), 1};
+      maps.m[g][0] = nd_map(x_of(g), 4, dims, str, box, 128, 4);
+    }
+  } else if (band) {
     a.gather = 3;
     a.bkb = sp.Kpad;
     a.K = sp.Kpad;
@@ -1511,7 +1748,7 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
       const cuuint32_t box[3] = {static_cast<cuuint32_t>(a.band_cols) * 2, static_cast<cuuint32_t>(sp.KH), 1};
       maps.m[g][0] = nd_map(x_of(g), 3, dims, str, box, 0, 1, 8);
     }
-  } else if (im2col_ok(sp)) {
+  } else if (ldk == sp.ld && im2col_ok(sp)) {
     const int cbox = sp.ld % BK == 0 ? BK : 64;
     bool ok = true;
     for (int g = 0; g < a.groups && ok; ++g) {
@@ -1606,6 +1843,16 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
       void* out = g == 0 ? sp.out_ptr[o] : sp.out_ptrg[g - 1][o];
       if (o >= sp.n_out) {
         maps.m[g][2 + o] = maps.m[g][1];
+      } else if (band2) {
+        // [N][OH][OW][cols]: tile rows past OW (pitch padding) or OH are clipped
+        const cuuint64_t dims[4] = {static_cast<cuuint64_t>(sp.out_cols[o]), static_cast<cuuint64_t>(sp.OW),
+                                    static_cast<cuuint64_t>(sp.OH), static_cast<cuuint64_t>(sp.Nimg)};
+        const cuuint64_t str[3] = {static_cast<cuuint64_t>(sp.out_ld[o]),
+                                   static_cast<cuuint64_t>(sp.out_ld[o]) * sp.OW,
+                                   static_cast<cuuint64_t>(sp.out_ld[o]) * sp.OW * sp.OH};
+        const cuuint32_t box[4] = {static_cast<cuuint32_t>(swz), static_cast<cuuint32_t>(b2P),
+                                   static_cast<cuuint32_t>(BM / b2P), 1};
+        maps.m[g][2 + o] = nd_map(out, 4, dims, str, box, swz, 5);
       } else if (band) {
         // [n*OH + oh][ow][cols]: the tile's rows >= OW fall outside and are clipped
         const cuuint64_t dims[3] = {static_cast<cuuint64_t>(sp.out_cols[o]), static_cast<cuuint64_t>(sp.OW),

@@ -205,7 +205,7 @@ QC_HD constexpr bool shape_is_int_fold(int s) {
 //   v outside [acc_min, acc_max] -> trap (lowest flat index) or saturate
 //   requantize (optional): q = clamp(rescale(v - in_zp) + out_zp, q_min, q_max)
 //   y[((img*O + o)*OH + oh)*OW + ow] = v or q   (int32, NCHW like Tensor)
-constexpr int kMaxIntPosts = 5;
+constexpr int kMaxIntPosts = 4;  // requantize, add, requantize, relu (kernel parameter block: <= 4 KB total)
 struct IntEpi {
   int32_t* y;
   const int32_t* bias;  // may be null

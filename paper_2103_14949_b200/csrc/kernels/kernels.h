@@ -142,6 +142,7 @@ struct TcConvSpec {
   int gather;        // 1: implicit im2col gather, 0: direct TMA rows
   int Ktrue, lda;    // direct: valid K bytes per row, row stride
   int Nimg, H, W, C, ld, KH, KW, sh, sw, ph, pw, OH, OW;  // gather geometry
+  int ldk;           // weight K stride of one tap (0: ld); 128 for 64-channel 2-D band convs
   const float* bias;
   double scale;      // s_x * s_w
   ProgArgs prog;
