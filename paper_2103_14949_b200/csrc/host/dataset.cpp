@@ -84,6 +84,25 @@ class Staging {
 };
 }  // namespace
 
+void staged_h2d(void* dst_dev, const void* src, size_t bytes, void* stream) {
+  const cudaStream_t us = stream ? static_cast<cudaStream_t>(stream) : S();
+  constexpr size_t kUnit = size_t{1} << 20;
+  const size_t units = bytes / kUnit, tail = bytes - units * kUnit;
+  const uint8_t* s8 = static_cast<const uint8_t*>(src);
+  uint8_t* d8 = static_cast<uint8_t*>(dst_dev);
+  if (units > 0) {
+    Staging& st = Staging::get();
+    std::lock_guard<std::mutex> lk(st.mu());
+    st.upload(d8, static_cast<int64_t>(units), kUnit,
+              [&](int64_t u, uint8_t* dst) { std::memcpy(dst, s8 + static_cast<size_t>(u) * kUnit, kUnit); },
+              us);
+  }
+  if (tail > 0 && cudaMemcpyAsync(d8 + units * kUnit, s8 + units * kUnit, tail, cudaMemcpyHostToDevice, us) !=
+                      cudaSuccess) {
+    throw DeviceError("staged upload failed");
+  }
+}
+
 DeviceDataset::DeviceDataset(const Graph& g, const Dataset& ds, int64_t first, int64_t count,
                              void* upload) {
   const cudaStream_t us = upload ? static_cast<cudaStream_t>(upload) : S();

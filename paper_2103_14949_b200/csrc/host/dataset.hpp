@@ -11,6 +11,11 @@
 
 namespace quantc::gpu {
 
+// host -> device copy through the reusable pinned staging chunks (packed by
+// host threads while the previous chunk's DMA runs): a pageable source of
+// tens of MB arrives at the staging rate instead of the pageable DMA rate
+void staged_h2d(void* dst_dev, const void* src, size_t bytes, void* stream = nullptr);
+
 class DeviceDataset {
  public:
   // Validates every sample against the graph inputs (reference

@@ -48,7 +48,10 @@ std::vector<std::shared_ptr<void>> upload_inputs(const Graph& g, const std::vect
     }
     const size_t bytes = static_cast<size_t>(shape_numel(shape)) * 4;
     auto buf = engine::device_alloc(bytes);
-    if (bytes) {
+    static const bool no_staging = std::getenv("QUANTC_NO_STAGED_INPUT") != nullptr;
+    if (bytes >= (size_t{4} << 20) && !no_staging && !device::host_pinned(in[k].data, bytes)) {
+      gpu::staged_h2d(buf.get(), in[k].data, bytes);  // pageable caller buffer, tens of MB
+    } else if (bytes) {
       if (cudaMemcpyAsync(buf.get(), in[k].data, bytes, cudaMemcpyHostToDevice, S()) != cudaSuccess) {
         throw DeviceError("input upload failed");
       }
