@@ -292,8 +292,9 @@ def config_legs(b, torch, stream, batch, engine="auto"):
     losses() call over a few candidates.
 
     C2  ResNet-18 @224, batch 64, int8_int32, pow2 thresholds -> fused tcgen05 path
-    C3  MobileNetV2 (width 1.0) @224, arm_vmlal_like, native depthwise convs
-        (conv2d groups) -> exact FP64 engine (grouped convs are not fused)
+    C3  MobileNetV2 (width 1.0) @224, arm_vmlal_like with 8-bit codes (the
+        (i8, i8) -> i16 accumulation signature), native depthwise convs
+        (conv2d groups) -> fused engine (depthwise as a CUDA-core stage)
     C5  Inception-v3-style @299 (native concat / avg_pool2d), int8_int32
         -> exact FP64 engine
     R50 under the reference's DEFAULT thresholds (quantile 0.99, pow2 off,
@@ -303,7 +304,7 @@ def config_legs(b, torch, stream, batch, engine="auto"):
     plans = [
         ("c2_resnet18", F.resnet(18), "int8_int32", batch, True, 0.999, 20),
         ("c3_mobilenet_v2", F.mobilenet_v2(image=224, width=1.0, classes=1000, native=True),
-         "arm_vmlal_like", 16, True, 0.999, 4),
+         "arm_vmlal_like", batch, True, 0.999, 8),
         ("c5_inception_v3", F.inception_v3(image=299, width=16, modules=2, head="gap", native=True),
          "int8_int32", 8, True, 0.999, 4),
         ("r50_default_thresholds", F.resnet(50), "int8_int32", 16, False, 0.99, 4),
@@ -327,6 +328,9 @@ def config_legs(b, torch, stream, batch, engine="auto"):
             ev = b.evaluator(sim, spec, topo, thr, st, ds, min_bit=4 if spec_name != "arm_vmlal_like" else 8)
             sp = ev.space()
             cands = candidates(sp, k + 1)
+            if spec_name == "arm_vmlal_like":
+                # 8-bit codes on every edge: the int8 x int8 -> int16 signature
+                cands = [[min(v, 8) for v in c] for c in cands]
             why = b.fused_status(sim, ev.bind(cands[0]))
             ran_on = "fused int8 tcgen05" if not why else f"exact FP64 engine ({why[:120]})"
             ev.losses(cands[:1])

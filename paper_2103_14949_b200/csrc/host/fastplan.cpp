@@ -69,7 +69,7 @@ struct FastPlan::Val {
 };
 
 struct FastPlan::Stage {
-  enum Kind { kInput, kGemm, kMaxpool, kGap } kind = kInput;
+  enum Kind { kInput, kGemm, kMaxpool, kGap, kDw } kind = kInput;
   int step = -1;
   int code_off = 0, code_len = 0;
   int in_val = -1;
@@ -211,6 +211,18 @@ struct Builder {
     }
     return out;
   }
+  // conv2d step with groups == C_in == O and weights [O, 1, KH, KW]
+  bool depthwise(int step) const {
+    const Node& n = node(step);
+    if (n.op != OpKind::kConv2d) return false;
+    const auto& st = plan.steps()[static_cast<size_t>(step)];
+    if (st.in.size() < 2 || st.in[0] < 0 || st.in[1] < 0) return false;
+    const auto& ds = plan.shape(st.in[0]);
+    const auto& ws = plan.shape(st.in[1]);
+    const int64_t groups = n.attr_or<int64_t>("groups", 1);
+    return ds.size() == 4 && ws.size() == 4 && groups > 1 && groups == ds[1] && ws[0] == groups &&
+           ws[1] == 1 && ws[2] * ws[3] <= 1024;
+  }
   bool is_output(int step) const {
     for (const PortRef& o : g().outputs()) {
       if (o.node == node(step).id) return true;
@@ -254,8 +266,14 @@ struct Builder {
     switch (ny.op) {
       case OpKind::kConv2d: {
         if (ny.attr_or<int64_t>("groups", 1) != 1) {
-          fail("grouped conv2d runs on the exact engine");
-          return false;
+          // depthwise (groups == C == O): CUDA-core stage over NHWC codes
+          if (!depthwise(y) || port != 0 || flat_hw != 1) {
+            fail("grouped conv2d (other than depthwise) runs on the exact engine");
+            return false;
+          }
+          ld = r16(C);
+          zero = ld != C;
+          break;
         }
         if (port != 0) {
           fail("conv2d weight is not a constant");
@@ -868,8 +886,65 @@ void FastPlan::compile() {
       case OpKind::kConv2d:
       case OpKind::kDense: {
         if (n.attr_or<int64_t>("groups", 1) != 1) {
-          fail("grouped conv2d runs on the exact engine");
-          continue;
+          if (!b.depthwise(step)) {
+            fail("grouped conv2d (other than depthwise) runs on the exact engine");
+            continue;
+          }
+          // depthwise: CUDA-core stage (kern::stage_dw_conv), the consumers'
+          // program like any producing stage
+          st->kind = Stage::kDw;
+          const auto& in = steps[i].in;
+          const Node& wsq = *steps[static_cast<size_t>(in[1])].node;
+          auto vit = val_of.find(in[0]);
+          if (steps[static_cast<size_t>(in[0])].node->op != OpKind::kSimulatedQuantize || vit == val_of.end() ||
+              vals_[static_cast<size_t>(vit->second)]->kind != 0) {
+            fail("depthwise data input is not an int8 simulated_quantize");
+            continue;
+          }
+          if (wsq.op != OpKind::kSimulatedQuantize ||
+              steps[static_cast<size_t>(steps[static_cast<size_t>(in[1])].in[0])].node->op != OpKind::kConstant) {
+            fail("depthwise weight is not a simulated-quantized constant");
+            continue;
+          }
+          st->in_val = vit->second;
+          st->w_sq = in[1];
+          st->w_const = steps[static_cast<size_t>(in[1])].in[0];
+          if (in.size() > 2 && in[2] >= 0) {
+            if (steps[static_cast<size_t>(in[2])].node->op != OpKind::kConstant ||
+                !steps[static_cast<size_t>(in[2])].node->payload->dtype().is_float()) {
+              fail("bias is not a float constant");
+              continue;
+            }
+            st->bias_const = in[2];
+            for (float bv : steps[static_cast<size_t>(in[2])].node->payload->floats()) {
+              st->bias_absmax = std::max(st->bias_absmax, std::fabs(static_cast<double>(bv)));
+            }
+          }
+          const auto& ds = plan_.shape(in[0]);
+          const auto& ws = plan_.shape(st->w_const);
+          Attr2 strd = pair_of(n, "strides", {1, 1}), pad = pair_of(n, "padding", {0, 0});
+          st->n0 = static_cast<int>(ds[0]);
+          st->C = static_cast<int>(ds[1]);
+          st->H = static_cast<int>(ds[2]);
+          st->W = static_cast<int>(ds[3]);
+          st->O = static_cast<int>(ws[0]);
+          st->KH = static_cast<int>(ws[2]);
+          st->KW = static_cast<int>(ws[3]);
+          st->sh = strd.a;
+          st->sw = strd.b;
+          st->ph = pad.a;
+          st->pw = pad.b;
+          st->OH = static_cast<int>(shp[2]);
+          st->OW = static_cast<int>(shp[3]);
+          st->taps = st->KH * st->KW;
+          st->ldk = (st->C + 15) / 16 * 16;  // weight codes [tap][ldk]
+          st->Ktrue = st->taps * st->ldk;
+          st->Kpad = st->Ktrue;
+          st->rows_out_ps = static_cast<int64_t>(st->n0) * st->OH * st->OW;
+          b.rows_ps = st->rows_out_ps;
+          b.C = st->O;
+          absorbed.insert(in[1]);
+          break;
         }
         st->kind = Stage::kGemm;
         st->dense = n.op == OpKind::kDense;
@@ -1122,7 +1197,7 @@ void FastPlan::compile() {
   }
   if (ok_ && out_val_ < 0) fail("graph output not reached");
   if (std::getenv("QUANTC_DUMP_PLAN")) {
-    static const char* kind[] = {"input", "gemm", "maxpool", "gap"};
+    static const char* kind[] = {"input", "gemm", "maxpool", "gap", "dw"};
     static const char* opn[] = {"end", "sq", "sq_store8", "relu", "clip", "add", "store_f32",
                                 "push", "pop"};
     for (const auto& st : stages_) {
@@ -1146,7 +1221,7 @@ bool FastPlan::eligible(const SimBinding* binding, bool exact, std::string* why)
     if (v->kind == 0) coded.insert(v->sq_step);
   }
   for (const auto& st : stages_) {
-    if (st->kind == Stage::kGemm) coded.insert(st->w_sq);
+    if (st->kind == Stage::kGemm || st->kind == Stage::kDw) coded.insert(st->w_sq);
   }
   auto check = [&](int step) -> bool {
     const QParams p = engine::qparams_of(*plan_.steps()[static_cast<size_t>(step)].node, binding);
@@ -1187,7 +1262,7 @@ bool FastPlan::eligible(const SimBinding* binding, bool exact, std::string* why)
     if (!check(step)) return false;
   }
   for (const auto& st : stages_) {
-    if (st->kind == Stage::kGemm && !check(st->w_sq)) return false;
+    if ((st->kind == Stage::kGemm || st->kind == Stage::kDw) && !check(st->w_sq)) return false;
   }
   return true;
 }
@@ -1250,11 +1325,13 @@ void FastPlan::prepare(Run& r) {
   acc_bound.assign(stages_.size(), 0.0);
   for (size_t si = 0; si < stages_.size(); ++si) {
     const Stage& st = *stages_[si];
-    if (st.kind != Stage::kGemm) continue;
+    if (st.kind != Stage::kGemm && st.kind != Stage::kDw) continue;
     wfsq[si] = make_fsq(engine::qparams_of(*plan_.steps()[static_cast<size_t>(st.w_sq)].node, binding));
     const Val& dv = *vals_[static_cast<size_t>(st.in_val)];
     const FSq& df = fsq[static_cast<size_t>(sq_index_.at(dv.sq_step))];
-    const double kreal = st.dense ? st.Ktrue : static_cast<double>(st.C) * st.KH * st.KW;
+    const double kreal = st.kind == Stage::kDw ? static_cast<double>(st.taps)
+                         : st.dense            ? st.Ktrue
+                                               : static_cast<double>(st.C) * st.KH * st.KW;
     acc_bound[si] = kreal * code_absmax(df) * code_absmax(wfsq[si]);
   }
   // one compact table block per stage (instructions + referenced params)
@@ -1284,7 +1361,7 @@ void FastPlan::prepare(Run& r) {
       t.clip[k] = make_float2(clip_lo_[static_cast<size_t>(c)], clip_hi_[static_cast<size_t>(c)]);
     }
     double v0 = std::numeric_limits<double>::infinity();
-    if (st.kind == Stage::kGemm) {
+    if (st.kind == Stage::kGemm || st.kind == Stage::kDw) {
       const Val& dv = *vals_[static_cast<size_t>(st.in_val)];
       const double sxw = static_cast<double>(scale_by_step.at(dv.sq_step)) *
                          static_cast<double>(wfsq[si].s);
@@ -1851,6 +1928,29 @@ void FastPlan::run_stage(Run& r, size_t si) {
       const Val& v = *vals_[static_cast<size_t>(st.in_val)];
       kern::stage_gap(static_cast<const float*>(buf(r, st.in_val)), v.ld, batch * st.n0, st.C,
                       st.HW, pa, ST());
+      break;
+    }
+    case Stage::kDw: {
+      // weight codes [tap][ldk] under this binding's weight sq (cached like
+      // the GEMM stages'), then one CUDA-core launch
+      const FSq wf = r.wfsq[si];
+      std::string key(reinterpret_cast<const char*>(&wf), sizeof(FSq));
+      auto ck = std::make_pair(static_cast<int>(si), key);
+      auto it = wcache_.find(ck);
+      if (it == wcache_.end()) {
+        const size_t cbytes = static_cast<size_t>(st.Kpad);
+        auto codes = engine::device_alloc_on(ST(), cbytes + 16);
+        kern::weight_codes_v2(plan_.constant(st.w_const).f(), static_cast<int8_t*>(codes.get()), 1, st.C,
+                              st.taps, st.ldk, st.Kpad, wf, ST());
+        it = wcache_.emplace(ck, codes).first;
+        wcache_bytes_ += cbytes + 16;
+      }
+      const Val& dv = *vals_[static_cast<size_t>(st.in_val)];
+      const float sxw = r.scale_by_step.at(dv.sq_step) * wf.s;  // pow2 x pow2: exact
+      kern::stage_dw_conv(static_cast<const int8_t*>(buf(r, st.in_val)), static_cast<int>(dv.ld),
+                          batch * st.n0, st.C, st.H, st.W, st.KH, st.KW, st.sh, st.sw, st.ph, st.pw,
+                          st.OH, st.OW, static_cast<const int8_t*>(it->second.get()), st.ldk,
+                          st.bias_const >= 0 ? plan_.constant(st.bias_const).f() : nullptr, sxw, pa, ST());
       break;
     }
     case Stage::kGemm: {

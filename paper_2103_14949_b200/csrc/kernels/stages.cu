@@ -92,6 +92,66 @@ __global__ void maxpool_codes_kernel(const int8_t* __restrict__ x, int ld, float
   }
 }
 
+// depthwise conv (groups == C == O) of int8 codes -> the stage program:
+// one thread per (output pixel, 16-channel group), int32 tap sums of
+// code x weight-code products, then v = RN24(acc * s_x*s_w + bias) — the
+// reference's double accumulation rounded to float, exact for power-of-two
+// scales (|acc| <= taps * 128 * 128 < 2^24 keeps acc * s an exact float and
+// the double rounding innocuous) — and the consumers' program.  Weight codes
+// are [tap][ldw] (16 channels per 16-byte load).
+__global__ void dw_conv_kernel(const int8_t* __restrict__ x, int ld, int N, int C, int H, int W,
+                               int KH, int KW, int sh, int sw, int ph, int pw, int OH, int OW,
+                               const int8_t* __restrict__ wc, int ldw, const float* __restrict__ bias,
+                               float scale, ProgArgs prog) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ StageTables T;
+  load_tables(&T, prog.tables);
+  __syncthreads();
+  const int groups = (C + 15) / 16;
+  const int64_t total = static_cast<int64_t>(N) * OH * OW * groups;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int grp = static_cast<int>(i % groups);
+    const int64_t m = i / groups;
+    const int ow = static_cast<int>(m % OW);
+    const int oh = static_cast<int>((m / OW) % OH);
+    const int64_t n = m / (static_cast<int64_t>(OW) * OH);
+    const int c0 = grp * 16;
+    const int nvalid = C - c0 < 16 ? C - c0 : 16;
+    int acc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = 0;
+    for (int a = 0; a < KH; ++a) {
+      const int ih = oh * sh - ph + a;
+      if (ih < 0 || ih >= H) continue;
+      for (int b = 0; b < KW; ++b) {
+        const int iw = ow * sw - pw + b;
+        if (iw < 0 || iw >= W) continue;
+        const int4 xr = __ldg(reinterpret_cast<const int4*>(x + ((n * H + ih) * W + iw) * ld + c0));
+        const int4 wr = __ldg(reinterpret_cast<const int4*>(wc + (a * KW + b) * ldw + c0));
+        const uint32_t xw[4] = {static_cast<uint32_t>(xr.x), static_cast<uint32_t>(xr.y),
+                                static_cast<uint32_t>(xr.z), static_cast<uint32_t>(xr.w)};
+        const uint32_t ww[4] = {static_cast<uint32_t>(wr.x), static_cast<uint32_t>(wr.y),
+                                static_cast<uint32_t>(wr.z), static_cast<uint32_t>(wr.w)};
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int xb = static_cast<int8_t>((xw[j >> 2] >> (8 * (j & 3))) & 0xFFu);
+          const int wb = static_cast<int8_t>((ww[j >> 2] >> (8 * (j & 3))) & 0xFFu);
+          acc[j] += xb * wb;
+        }
+      }
+    }
+    float v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float b = (bias && j < nvalid) ? __ldg(bias + c0 + j) : 0.0f;
+      v[j] = __fadd_rn(__fmul_rn(static_cast<float>(acc[j]), scale), b);
+    }
+    run_prog<16, 3>(v, m, c0, nvalid, T);
+  }
+}
+
 // one thread per (n, c): sequential double sum in h*W+w order (coalesced
 // across c), then the stage program on that one value
 __global__ void gap_rows_kernel(const float* __restrict__ x, int64_t ld, int N, int C, int HW,
@@ -559,6 +619,16 @@ void stage_maxpool(const int8_t* x, int ld, float scale, int N, int C, int H, in
   if (total <= 0) return;
   launch_pdl(maxpool_codes_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, x, ld, scale, N, C, H, W, OH, OW, kh,
                                                             kw, sh, sw, ph, pw, prog);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+void stage_dw_conv(const int8_t* x, int ld, int N, int C, int H, int W, int KH, int KW, int sh,
+                   int sw, int ph, int pw, int OH, int OW, const int8_t* wcodes, int ldw,
+                   const float* bias, float scale, const ProgArgs& prog, cudaStream_t s) {
+  const int64_t total = static_cast<int64_t>(N) * OH * OW * ((C + 15) / 16);
+  if (total <= 0) return;
+  launch_pdl(dw_conv_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, x, ld, N, C, H, W, KH, KW,
+             sh, sw, ph, pw, OH, OW, wcodes, ldw, bias, scale, prog);
   QC_CUDA_CHECK_LAUNCH();
 }
 

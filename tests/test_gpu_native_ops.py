@@ -106,3 +106,42 @@ def test_native_pipeline_vs_graph_oracle(b200, port, which, spec_name):
         got = b200.predict_scores(sim, ds, binding=bnd)
         assert got.reshape(scores.shape).tobytes() == scores.tobytes()
         assert loss == 1.0 - float(np.sum(want == refs)) / len(refs)
+
+
+@pytest.mark.parametrize("spec_name,min_bit", [("arm_vmlal_like", 4), ("int8_int32", 4)])
+def test_native_depthwise_on_fused_engine(b200, cuda_lib, spec_name, min_bit):
+    """C3 MobileNetV2 with native depthwise convs under power-of-two
+    thresholds runs on the fused engine (depthwise as a CUDA-core stage of
+    int8 codes, fastplan Stage::kDw) and reproduces the exact FP64 engine —
+    itself pinned to the reference on the rewritten graph — bit for bit:
+    fp32 score bytes and losses of mixed-bit candidates."""
+    _, nat = _pair("c3")
+    data = nat.data(6)
+    g = b200.graph(nat.doc, nat.blob)
+    spec = b200.parse_spec(F.spec_fixture(spec_name))
+    topo = b200.generate_topology(g, spec)
+    sim = b200.insert_simulated_quantize(g, topo)
+    ds = b200.dataset(data)
+    st = b200.collect_stats(g, ds, 2048, b200.simulated_edge_indices(g, topo))
+    thr = st.estimate_thresholds("quantile", quantile=0.999, pow2=True)
+    ev = b200.evaluator(sim, spec, topo, thr, st, ds, min_bit=min_bit)
+    sp = ev.space()
+    rng = np.random.default_rng(3)
+    # the fused engine materialises int8 codes: bit widths <= 8 (for
+    # arm_vmlal_like that binds the (i8, i8) -> i16 accumulation signature)
+    his = [min(hi, 8) for hi in sp.hi]
+    cands = [his, sp.all_lo()] + [
+        [int(rng.integers(lo, hi + 1)) for lo, hi in zip(sp.lo, his)] for _ in range(4)]
+    assert b200.fused_status(sim, ev.bind(cands[0])) == ""
+    cuda_lib.set_engine_mode("exact")
+    try:
+        exact = ev.losses(cands)
+        s_exact = [b200.predict_scores(sim, ds, ev.bind(c)) for c in cands[:3]]
+    finally:
+        cuda_lib.set_engine_mode("auto")
+    f0 = cuda_lib.counters()["fused_batches"]
+    fused = ev.losses(cands)
+    assert cuda_lib.counters()["fused_batches"] - f0 >= len(cands)
+    np.testing.assert_array_equal(exact, fused)
+    for c, se in zip(cands[:3], s_exact):
+        assert b200.predict_scores(sim, ds, ev.bind(c)).tobytes() == se.tobytes()
