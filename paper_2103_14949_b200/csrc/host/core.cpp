@@ -11,6 +11,7 @@
 #include <exception>
 #include <functional>
 #include <mutex>
+#include <numeric>
 #include <condition_variable>
 #include <stdexcept>
 #include <thread>
@@ -78,6 +79,9 @@ int max_bits(DType dtype) {
 }
 
 // ---- Tensor -----------------------------------------------------------------
+// Host-side value type of the drop-in API (device work never goes through
+// it: the engine keeps its own device buffers).  Error strings are the
+// reference's (tensor.cpp), which the errors-identical tests compare.
 
 int64_t shape_numel(const std::vector<int64_t>& shape) {
   int64_t n = 1;
@@ -89,28 +93,31 @@ int64_t shape_numel(const std::vector<int64_t>& shape) {
 }
 
 std::string shape_to_string(const std::vector<int64_t>& shape) {
-  std::string s = "(";
-  for (size_t i = 0; i < shape.size(); ++i) s += (i ? "," : "") + std::to_string(shape[i]);
-  return s + ")";
+  std::string s;
+  for (int64_t d : shape) s += (s.empty() ? "" : ",") + std::to_string(d);
+  return "(" + s + ")";
 }
 
-Tensor Tensor::zeros(DType dtype, std::vector<int64_t> shape) {
-  Tensor t;
-  t.dtype_ = dtype;
-  size_t n = static_cast<size_t>(shape_numel(shape));
-  t.shape_ = std::move(shape);
-  if (dtype.is_float()) {
-    t.f_.assign(n, 0.0f);
-  } else {
-    t.i_.assign(n, 0);
+namespace {
+// element count of `shape` must equal the payload length
+void check_length(const std::vector<int64_t>& shape, size_t len) {
+  if (shape_numel(shape) != static_cast<int64_t>(len)) {
+    throw std::invalid_argument("data length does not match shape " + shape_to_string(shape));
   }
-  return t;
+}
+[[noreturn]] void wrong_view(const char* view, const DType& d) {
+  throw std::logic_error(std::string(view) + " on " + d.name() + " tensor");
+}
+}  // namespace
+
+Tensor Tensor::zeros(DType dtype, std::vector<int64_t> shape) {
+  const size_t n = static_cast<size_t>(shape_numel(shape));
+  return dtype.is_float() ? from_floats(std::move(shape), std::vector<float>(n, 0.0f))
+                          : from_ints(dtype, std::move(shape), std::vector<int32_t>(n, 0));
 }
 
 Tensor Tensor::from_floats(std::vector<int64_t> shape, std::vector<float> data) {
-  if (shape_numel(shape) != static_cast<int64_t>(data.size())) {
-    throw std::invalid_argument("data length does not match shape " + shape_to_string(shape));
-  }
+  check_length(shape, data.size());
   Tensor t;
   t.dtype_ = f32;
   t.shape_ = std::move(shape);
@@ -120,9 +127,7 @@ Tensor Tensor::from_floats(std::vector<int64_t> shape, std::vector<float> data) 
 
 Tensor Tensor::from_ints(DType dtype, std::vector<int64_t> shape, std::vector<int32_t> data) {
   if (dtype.is_float()) throw std::invalid_argument("from_ints needs an integer dtype");
-  if (shape_numel(shape) != static_cast<int64_t>(data.size())) {
-    throw std::invalid_argument("data length does not match shape " + shape_to_string(shape));
-  }
+  check_length(shape, data.size());
   Tensor t;
   t.dtype_ = dtype;
   t.shape_ = std::move(shape);
@@ -133,50 +138,45 @@ Tensor Tensor::from_ints(DType dtype, std::vector<int64_t> shape, std::vector<in
 
 Tensor Tensor::scalar(float value) { return from_floats({1}, {value}); }
 
-int64_t Tensor::numel() const {
-  return static_cast<int64_t>(dtype_.is_float() ? f_.size() : i_.size());
-}
+int64_t Tensor::numel() const { return static_cast<int64_t>(dtype_.is_float() ? f_.size() : i_.size()); }
 
 std::span<const float> Tensor::floats() const {
-  if (!dtype_.is_float()) throw std::logic_error("floats() on " + dtype_.name() + " tensor");
+  if (!dtype_.is_float()) wrong_view("floats()", dtype_);
   return f_;
 }
 std::span<float> Tensor::floats() {
-  if (!dtype_.is_float()) throw std::logic_error("floats() on " + dtype_.name() + " tensor");
+  if (!dtype_.is_float()) wrong_view("floats()", dtype_);
   return f_;
 }
 std::span<const int32_t> Tensor::ints() const {
-  if (dtype_.is_float()) throw std::logic_error("ints() on float32 tensor");
+  if (dtype_.is_float()) wrong_view("ints()", dtype_);
   return i_;
 }
 std::span<int32_t> Tensor::ints() {
-  if (dtype_.is_float()) throw std::logic_error("ints() on float32 tensor");
+  if (dtype_.is_float()) wrong_view("ints()", dtype_);
   return i_;
 }
 
 bool Tensor::in_range() const {
-  if (dtype_.is_float()) return true;
-  const int64_t lo = dtype_.min_value(), hi = dtype_.max_value();
-  return std::all_of(i_.begin(), i_.end(), [&](int32_t v) { return v >= lo && v <= hi; });
+  if (dtype_.is_float() || i_.empty()) return true;
+  const auto [lo, hi] = std::minmax_element(i_.begin(), i_.end());
+  return *lo >= dtype_.min_value() && *hi <= dtype_.max_value();
 }
 
 float Tensor::max_abs() const {
-  float m = 0.0f;
-  if (dtype_.is_float()) {
-    for (float v : f_) m = std::max(m, std::fabs(v));
-  } else {
-    for (int32_t v : i_) m = std::max(m, std::fabs(static_cast<float>(v)));
-  }
-  return m;
+  // |v| of integers compared as floats, like the reference
+  auto fold = [](float m, float v) { return std::max(m, std::fabs(v)); };
+  if (dtype_.is_float()) return std::accumulate(f_.begin(), f_.end(), 0.0f, fold);
+  return std::accumulate(i_.begin(), i_.end(), 0.0f,
+                         [&](float m, int32_t v) { return fold(m, static_cast<float>(v)); });
 }
 
 bool Tensor::equals(const Tensor& other) const {
   if (dtype_ != other.dtype_ || shape_ != other.shape_) return false;
-  if (dtype_.is_float()) {
-    return f_.size() == other.f_.size() &&
-           std::memcmp(f_.data(), other.f_.data(), f_.size() * sizeof(float)) == 0;
-  }
-  return i_ == other.i_;
+  if (!dtype_.is_float()) return i_ == other.i_;
+  // bitwise (NaN payloads and signed zeros count)
+  return f_.size() == other.f_.size() &&
+         (f_.empty() || std::memcmp(f_.data(), other.f_.data(), f_.size() * sizeof(float)) == 0);
 }
 
 // ---- BigUInt ------------------------------------------------------------------
