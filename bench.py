@@ -296,7 +296,7 @@ def config_legs(b, torch, stream, batch, engine="auto"):
         (i8, i8) -> i16 accumulation signature), native depthwise convs
         (conv2d groups) -> fused engine (depthwise as a CUDA-core stage)
     C5  Inception-v3-style @299 (native concat / avg_pool2d), int8_int32
-        -> exact FP64 engine
+        -> fused engine (avg_pool2d and concat as fused stages)
     R50 under the reference's DEFAULT thresholds (quantile 0.99, pow2 off,
         calibration.hpp:71-76) -> the exact FP64 engine (the fused int8 engine
         is bit-exact only under power-of-two scales)"""

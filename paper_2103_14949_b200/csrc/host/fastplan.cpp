@@ -58,6 +58,10 @@ struct FastPlan::Val {
   int hw = 1, cs = 0;
   int64_t ld = 0;
   bool zero_fill = false;
+  // a column slice of another fp32 value (a concat input writing into the
+  // concat's buffer): no storage of its own, columns [col_off, col_off + C)
+  int alias_root = -1;
+  int64_t col_off = 0;
   // space-to-depth layout of a tiny-channel graph input feeding a stride-2
   // conv: pixel (h, w, c) of an [H, W, C] image lives at s2d pixel
   // (h/2, w/2), channel ((h%2)*2 + w%2)*C + c, 16-byte rows
@@ -69,7 +73,7 @@ struct FastPlan::Val {
 };
 
 struct FastPlan::Stage {
-  enum Kind { kInput, kGemm, kMaxpool, kGap, kDw } kind = kInput;
+  enum Kind { kInput, kGemm, kMaxpool, kGap, kDw, kAvg, kCat } kind = kInput;
   int step = -1;
   int code_off = 0, code_len = 0;
   int in_val = -1;
@@ -222,6 +226,61 @@ struct Builder {
     const int64_t groups = n.attr_or<int64_t>("groups", 1);
     return ds.size() == 4 && ws.size() == 4 && groups > 1 && groups == ds[1] && ws[0] == groups &&
            ws[1] == 1 && ws[2] * ws[3] <= 1024;
+  }
+  // concat step x feeding another concat (its sole consumer, not an output):
+  // that concat's step and the port x occupies, else -1
+  std::pair<int, int> concat_outer(int x) const {
+    const auto cs = consumers(x);
+    if (cs.size() == 1 && !is_output(x) && node(cs[0].first).op == OpKind::kConcat) return cs[0];
+    return {-1, -1};
+  }
+  // channel offset of input `port` of concat step x, within x
+  int64_t concat_port_off(int x, int port) const {
+    const auto& in = plan.steps()[static_cast<size_t>(x)].in;
+    int64_t off = 0;
+    for (int p = 0; p < port; ++p) off += plan.shape(in[static_cast<size_t>(p)])[1];
+    return off;
+  }
+  // the outermost concat's buffer (fp32, created when its first input lands)
+  // and the column slice of input `port` of concat x inside it
+  std::map<int, int>* concat_root_val = nullptr;
+  int concat_slice(int x, int port) {
+    int64_t off = concat_port_off(x, port);
+    int root = x;
+    for (auto o = concat_outer(root); o.first >= 0; o = concat_outer(root)) {
+      off += concat_port_off(o.first, o.second);
+      root = o.first;
+    }
+    const auto& rshape = plan.shape(root);
+    if (rshape.size() != 4) {
+      fail("concat of non-4-D values");
+      return -1;
+    }
+    const int C_total = static_cast<int>(rshape[1]);
+    auto it = concat_root_val->find(root);
+    if (it == concat_root_val->end()) {
+      const int keepC = C;
+      C = C_total;
+      const int v = make_val(root, -1, 1, C_total, 1, 0, false);
+      C = keepC;
+      it = concat_root_val->emplace(root, v).first;
+    }
+    const int rv = it->second;
+    if (vals[static_cast<size_t>(rv)]->rows_ps != rows_ps) {
+      fail("concat inputs with different row spaces");
+      return -1;
+    }
+    // (not registered in val_of: step x's own value is the concat, not a slice)
+    auto v = std::make_unique<FastPlan::Val>();
+    v->step = x;
+    v->kind = 1;
+    v->rows_ps = rows_ps;
+    v->C = C;
+    v->ld = C_total;
+    v->alias_root = rv;
+    v->col_off = off;
+    vals.push_back(std::move(v));
+    return static_cast<int>(vals.size()) - 1;
   }
   bool is_output(int step) const {
     for (const PortRef& o : g().outputs()) {
@@ -438,6 +497,17 @@ struct Builder {
             op(kern::kPSq, sq_slot(x));
             store_f32(x, false);
             return;
+          case OpKind::kConcat:
+            op(kern::kPSq, sq_slot(x));
+            handle(x, y, cy[0].second);
+            return;
+          case OpKind::kAvgPool2d:
+            // float-only op (its input edge is a passthrough in every
+            // binding Algorithm 1 allows): the sq's fp32 value, pooled by
+            // an avg stage with the exact engine's double arithmetic
+            op(kern::kPSq, sq_slot(x));
+            store_f32(x, false);
+            return;
           default:
             codes_for(x, y, cy[0].second);
             return;
@@ -480,6 +550,18 @@ struct Builder {
         // an fp32 value pooled by a GAP stage (which reads it from rows)
         store_f32(u, false);
         return;
+      case OpKind::kConcat: {
+        // channel placement: the value lands as fp32 in its column slice of
+        // the (outermost) concat buffer; the concat's stage runs its
+        // consumers over the whole buffer once every input has landed
+        if (flat_hw != 1) {
+          fail("concat after flatten");
+          return;
+        }
+        const int sv = concat_slice(x, port);
+        if (sv >= 0) op(kern::kPStoreF32, 0, sv);
+        return;
+      }
       case OpKind::kAdd: {
         // fp32 add (an add the spec does not quantize, e.g. arm_vmlal_like's
         // residuals): float + float like the reference (interpreter.cpp
@@ -717,7 +799,9 @@ bool make_epi(const kern::StageTables& t, int shape, double sxw, kern::EpiConsts
         e.f32_s = 1.0f;
         e.f32_off = 0.0f;
         const kern::ProgBuf& fb = t.buf[c[0].b];
-        if (fb.kind != 1 || fb.hw != 1) return false;
+        if (fb.kind != 1 || fb.hw != 1 || (reinterpret_cast<uintptr_t>(fb.ptr) & 15) != 0 || fb.ld % 4 != 0) {
+          return false;  // (concat column slices: the interpreter's scalar stores)
+        }
         e.f32_ptr = static_cast<float*>(fb.ptr);
         e.f32_ld = fb.ld;
         e.slot_out[0] = e.slot_out[1] = -1;
@@ -771,7 +855,9 @@ bool make_epi(const kern::StageTables& t, int shape, double sxw, kern::EpiConsts
       return false;
     }
     const kern::ProgBuf& fb = t.buf[out0];
-    if (fb.kind != 1 || fb.hw != 1) return false;
+    if (fb.kind != 1 || fb.hw != 1 || (reinterpret_cast<uintptr_t>(fb.ptr) & 15) != 0 || fb.ld % 4 != 0) {
+      return false;  // (concat column slices: the interpreter's scalar stores)
+    }
     e.f32_ptr = static_cast<float*>(fb.ptr);
     e.f32_ld = fb.ld;
   }
@@ -837,6 +923,8 @@ void FastPlan::compile() {
             [this](const std::string& w) { fail(w); }};
   b.out_val = &out_val_;
   b.out_per_sample = &out_per_sample_;
+  std::map<int, int> concat_root_val;
+  b.concat_root_val = &concat_root_val;
   const Graph& g = plan_.graph();
 
   for (size_t i = 0; i < steps.size() && ok_; ++i) {
@@ -1092,6 +1180,58 @@ void FastPlan::compile() {
         b.C = st->C;
         break;
       }
+      case OpKind::kAvgPool2d: {
+        // average of materialised fp32 rows (zero padding counted: the op's
+        // semantics are the constant depthwise conv it rewrites to)
+        st->kind = Stage::kAvg;
+        const int src = steps[i].in[0];
+        auto vit = val_of.find(src);
+        if (vit == val_of.end() || vals_[static_cast<size_t>(vit->second)]->kind != 1) {
+          fail("avg_pool2d input is not materialised fp32");
+          continue;
+        }
+        st->in_val = vit->second;
+        const auto& ds = plan_.shape(src);
+        auto k = n.attr<std::vector<int64_t>>("pool_size");
+        Attr2 strd = pair_of(n, "strides", {static_cast<int>(k[0]), static_cast<int>(k[1])});
+        Attr2 pad = pair_of(n, "padding", {0, 0});
+        st->n0 = static_cast<int>(ds[0]);
+        st->C = static_cast<int>(ds[1]);
+        st->H = static_cast<int>(ds[2]);
+        st->W = static_cast<int>(ds[3]);
+        st->OH = static_cast<int>(shp[2]);
+        st->OW = static_cast<int>(shp[3]);
+        st->pkh = static_cast<int>(k[0]);
+        st->pkw = static_cast<int>(k[1]);
+        st->sh = strd.a;
+        st->sw = strd.b;
+        st->ph = pad.a;
+        st->pw = pad.b;
+        b.rows_ps = static_cast<int64_t>(st->n0) * st->OH * st->OW;
+        b.C = st->C;
+        break;
+      }
+      case OpKind::kConcat: {
+        // a concat inside another concat has no stage: its inputs wrote
+        // straight into the outer buffer
+        if (b.concat_outer(step).first >= 0) continue;
+        auto cit = concat_root_val.find(step);
+        if (cit == concat_root_val.end()) {
+          fail("concat not reached by its inputs");
+          continue;
+        }
+        if (n.attr_or<int64_t>("axis", 1) != 1) {
+          fail("concat along an axis other than channels");
+          continue;
+        }
+        st->kind = Stage::kCat;
+        st->in_val = cit->second;
+        const Val& cv = *vals_[static_cast<size_t>(cit->second)];
+        st->C = cv.C;
+        b.rows_ps = cv.rows_ps;
+        b.C = cv.C;
+        break;
+      }
       case OpKind::kGlobalAvgPool2d: {
         st->kind = Stage::kGap;
         const int src = steps[i].in[0];
@@ -1197,7 +1337,7 @@ void FastPlan::compile() {
   }
   if (ok_ && out_val_ < 0) fail("graph output not reached");
   if (std::getenv("QUANTC_DUMP_PLAN")) {
-    static const char* kind[] = {"input", "gemm", "maxpool", "gap", "dw"};
+    static const char* kind[] = {"input", "gemm", "maxpool", "gap", "dw", "avg", "cat"};
     static const char* opn[] = {"end", "sq", "sq_store8", "relu", "clip", "add", "store_f32",
                                 "push", "pop"};
     for (const auto& st : stages_) {
@@ -1273,6 +1413,10 @@ void FastPlan::ensure_arena(int batch, int group) {
   if (ar.batch >= batch) return;
   ar.bufs.clear();
   for (const auto& v : vals_) {
+    if (v->alias_root >= 0) {
+      ar.bufs.push_back(nullptr);  // a column slice of its root's buffer
+      continue;
+    }
     const size_t bytes = static_cast<size_t>(v->bytes_ps()) * batch;
     auto buf = engine::device_alloc_on(ST(), bytes + 64);
     if (v->zero_fill) ok_cuda(cudaMemsetAsync(buf.get(), 0, bytes + 64, ST()));
@@ -1351,7 +1495,7 @@ void FastPlan::prepare(Run& r) {
       const Val& v = *vals_[static_cast<size_t>(vid)];
       // the value's own buffer (shape 5 folds it into f32_ptr); re-pointed
       // below once fork aliases are known
-      t.buf[k] = ProgBuf{arenas_[static_cast<size_t>(r.group)].bufs[static_cast<size_t>(vid)].get(),
+      t.buf[k] = ProgBuf{arena_ptr(r.group, vid),
                          v.ld, v.hw, v.cs, v.kind,
                          v.kind == 0 ? scale_by_step.at(v.sq_step) : 1.0f,
                          k < st.buf_slot.size() ? st.buf_slot[k] : -1, 0};
@@ -1751,8 +1895,16 @@ bool FastPlan::fold_integer(size_t si, int shape, double sxw, double acc_bound, 
 }
 
 void* FastPlan::buf(const Run& r, int vid) const {
+  const Val& v = *vals_[static_cast<size_t>(vid)];
+  if (v.alias_root >= 0) return static_cast<char*>(buf(r, v.alias_root)) + v.col_off * 4;
   const int root = r.alias.empty() ? vid : r.alias[static_cast<size_t>(vid)];
   return arenas_[static_cast<size_t>(r.group)].bufs[static_cast<size_t>(root)].get();
+}
+
+void* FastPlan::arena_ptr(int group, int vid) const {
+  const Val& v = *vals_[static_cast<size_t>(vid)];
+  if (v.alias_root >= 0) return static_cast<char*>(arena_ptr(group, v.alias_root)) + v.col_off * 4;
+  return arenas_[static_cast<size_t>(group)].bufs[static_cast<size_t>(vid)].get();
 }
 
 // weight codes of stage si under the run's binding (cached per FSq), and the
@@ -1928,6 +2080,20 @@ void FastPlan::run_stage(Run& r, size_t si) {
       const Val& v = *vals_[static_cast<size_t>(st.in_val)];
       kern::stage_gap(static_cast<const float*>(buf(r, st.in_val)), v.ld, batch * st.n0, st.C,
                       st.HW, pa, ST());
+      break;
+    }
+    case Stage::kAvg: {
+      const Val& v = *vals_[static_cast<size_t>(st.in_val)];
+      const double wk = static_cast<double>(static_cast<float>(1.0 / (st.pkh * st.pkw)));
+      kern::stage_avgpool_f32(static_cast<const float*>(buf(r, st.in_val)), static_cast<int>(v.ld),
+                              batch * st.n0, st.C, st.H, st.W, st.OH, st.OW, st.pkh, st.pkw, st.sh,
+                              st.sw, st.ph, st.pw, wk, pa, ST());
+      break;
+    }
+    case Stage::kCat: {
+      const Val& v = *vals_[static_cast<size_t>(st.in_val)];
+      const kern::ProgBuf src{buf(r, st.in_val), v.ld, 1, 0, 1, 1.0f, -1, 0};
+      kern::stage_ew(src, batch * v.rows_ps, v.C, pa, ST());
       break;
     }
     case Stage::kDw: {

@@ -89,6 +89,8 @@ class FastPlan {
   void ensure_arena(int batch, int group);
   void prepare(Run& r);
   void* buf(const Run& r, int vid) const;
+  // a value's device pointer in arena `group`, through concat column slices
+  void* arena_ptr(int group, int vid) const;
   void gemm_spec(Run& r, size_t si, kern::TcConvSpec& sp);
   void launch_gemm(size_t si, const kern::TcConvSpec& sp);
   void run_stage(Run& r, size_t si);

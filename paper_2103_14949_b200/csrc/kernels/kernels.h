@@ -233,6 +233,11 @@ void pack_i32_weights(const int32_t* w, int8_t* codes, int32_t* wsum, int* bad, 
 // graph input NCHW fp32 -> program over (m = n*H*W + hw, c)
 void stage_input(const float* x, int N, int C, int HW, const ProgArgs& prog, cudaStream_t s);
 // max_pool2d over NHWC codes (value = code * scale) -> program
+// average pool (zero padding counted) of fp32 NHWC rows with the stage
+// program (fused engine; the exact engine's double arithmetic, wk = fl32(1/(kh*kw)))
+void stage_avgpool_f32(const float* x, int ld, int N, int C, int H, int W, int OH, int OW, int kh,
+                       int kw, int sh, int sw, int ph, int pw, double wk, const ProgArgs& prog,
+                       cudaStream_t s);
 // depthwise conv (groups == C == O) of int8 codes with the stage program
 // (fused engine; weight codes [tap][ldw])
 void stage_dw_conv(const int8_t* x, int ld, int N, int C, int H, int W, int KH, int KW, int sh,

@@ -92,6 +92,53 @@ __global__ void maxpool_codes_kernel(const int8_t* __restrict__ x, int ld, float
   }
 }
 
+// average pool of fp32 NHWC rows -> the stage program.  The op is DEFINED
+// as the constant depthwise conv with weight wk = fl32(1/(kh*kw)) and zero
+// padding (fixtures.py _avg_pool); the reference's double accumulation
+// (x*wk exact in double, one rounding per tap) in (kh, kw) order, as the
+// exact engine's avgpool_kernel (eltwise.cu), then one rounding to float.
+__global__ void avgpool_f32_kernel(const float* __restrict__ x, int ld, int N, int C, int H, int W,
+                                   int OH, int OW, int kh, int kw, int sh, int sw, int ph, int pw,
+                                   double wk, ProgArgs prog) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ StageTables T;
+  load_tables(&T, prog.tables);
+  __syncthreads();
+  const int groups = (C + 15) / 16;
+  const int64_t total = static_cast<int64_t>(N) * OH * OW * groups;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int grp = static_cast<int>(i % groups);
+    const int64_t m = i / groups;
+    const int ow = static_cast<int>(m % OW);
+    const int oh = static_cast<int>((m / OW) % OH);
+    const int64_t n = m / (static_cast<int64_t>(OW) * OH);
+    const int c0 = grp * 16;
+    const int nvalid = C - c0 < 16 ? C - c0 : 16;
+    double acc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+    for (int a = 0; a < kh; ++a) {
+      const int ih = oh * sh - ph + a;
+      if (ih < 0 || ih >= H) continue;
+      for (int b = 0; b < kw; ++b) {
+        const int iw = ow * sw - pw + b;
+        if (iw < 0 || iw >= W) continue;
+        const float* src = x + ((n * H + ih) * W + iw) * ld + c0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if (j < nvalid) acc[j] = __fma_rn(static_cast<double>(__ldg(src + j)), wk, acc[j]);
+        }
+      }
+    }
+    float v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = __double2float_rn(acc[j]);
+    run_prog<16, 3>(v, m, c0, nvalid, T);
+  }
+}
+
 // depthwise conv (groups == C == O) of int8 codes -> the stage program:
 // one thread per (output pixel, 16-channel group), int32 tap sums of
 // code x weight-code products, then v = RN24(acc * s_x*s_w + bias) — the
@@ -619,6 +666,16 @@ void stage_maxpool(const int8_t* x, int ld, float scale, int N, int C, int H, in
   if (total <= 0) return;
   launch_pdl(maxpool_codes_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, x, ld, scale, N, C, H, W, OH, OW, kh,
                                                             kw, sh, sw, ph, pw, prog);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
+void stage_avgpool_f32(const float* x, int ld, int N, int C, int H, int W, int OH, int OW, int kh,
+                       int kw, int sh, int sw, int ph, int pw, double wk, const ProgArgs& prog,
+                       cudaStream_t s) {
+  const int64_t total = static_cast<int64_t>(N) * OH * OW * ((C + 15) / 16);
+  if (total <= 0) return;
+  launch_pdl(avgpool_f32_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, x, ld, N, C, H, W, OH, OW,
+             kh, kw, sh, sw, ph, pw, wk, prog);
   QC_CUDA_CHECK_LAUNCH();
 }
 

@@ -108,14 +108,17 @@ def test_native_pipeline_vs_graph_oracle(b200, port, which, spec_name):
         assert loss == 1.0 - float(np.sum(want == refs)) / len(refs)
 
 
-@pytest.mark.parametrize("spec_name,min_bit", [("arm_vmlal_like", 4), ("int8_int32", 4)])
-def test_native_depthwise_on_fused_engine(b200, cuda_lib, spec_name, min_bit):
-    """C3 MobileNetV2 with native depthwise convs under power-of-two
-    thresholds runs on the fused engine (depthwise as a CUDA-core stage of
-    int8 codes, fastplan Stage::kDw) and reproduces the exact FP64 engine —
-    itself pinned to the reference on the rewritten graph — bit for bit:
-    fp32 score bytes and losses of mixed-bit candidates."""
-    _, nat = _pair("c3")
+@pytest.mark.parametrize("which,spec_name,min_bit", [("c3", "arm_vmlal_like", 4), ("c3", "int8_int32", 4),
+                                                    ("c5", "int8_int32", 4)])
+def test_native_ops_on_fused_engine(b200, cuda_lib, which, spec_name, min_bit):
+    """Native graphs under power-of-two thresholds run on the fused engine —
+    C3 MobileNetV2's depthwise convs as a CUDA-core stage of int8 codes
+    (fastplan Stage::kDw), C5 Inception's avg_pool2d over codes (Stage::kAvg)
+    and concat as fp32 column placement plus one stage over the concatenated
+    value (Stage::kCat) — and reproduce the exact FP64 engine, itself pinned
+    to the reference on the rewritten graph, bit for bit: fp32 score bytes
+    and losses of mixed-bit candidates."""
+    _, nat = _pair(which)
     data = nat.data(6)
     g = b200.graph(nat.doc, nat.blob)
     spec = b200.parse_spec(F.spec_fixture(spec_name))
