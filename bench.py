@@ -347,6 +347,19 @@ def config_legs(b, torch, stream, batch, engine="auto"):
                           "candidates_per_s": 1e3 / ms, "candidates": k,
                           "gmac_per_image": model.macs_per_sample() / 1e9,
                           "engine": ran_on}
+            if name == "c5_inception_v3":
+                # C5 is a strategy-search config: a real random search over
+                # its calibration images (speculative batches of 4)
+                torch.cuda.synchronize()
+                s0, s1 = _events(torch)
+                s0.record(stream)
+                res = b.search_batched("random", sp, evaluator=ev, mode="local", width=4, n=32, seed=7)
+                s1.record(stream)
+                torch.cuda.synchronize()
+                sms = s0.elapsed_time(s1)
+                legs[name]["search"] = {"method": "random", "n": 32, "ms": sms,
+                                        "candidates_per_s": res.evaluations / (sms / 1e3),
+                                        "best_loss": res.best_loss}
             del ev, ds, st, sim
         except Exception as e:  # a side leg never sinks the headline line
             legs[name] = {"error": str(e)[:300]}
