@@ -550,6 +550,20 @@ struct Builder {
         // an fp32 value pooled by a GAP stage (which reads it from rows)
         store_f32(u, false);
         return;
+      case OpKind::kAvgPool2d: {
+        // an fp32 value pooled by an avg stage; a concat's value already is
+        // fp32 rows (the concat buffer the register was loaded from)
+        if (flat_hw != 1) {
+          fail("avg_pool2d after flatten");
+          return;
+        }
+        auto it = val_of.find(u);
+        if (it == val_of.end() || vals[static_cast<size_t>(it->second)]->kind != 1 ||
+            vals[static_cast<size_t>(it->second)]->C != C) {
+          store_f32(u, false);
+        }
+        return;
+      }
       case OpKind::kConcat: {
         // channel placement: the value lands as fp32 in its column slice of
         // the (outermost) concat buffer; the concat's stage runs its

@@ -48,6 +48,11 @@ def test_avg_pool_kernel_vs_port(cuda_lib, port, k, s, p):
 
 
 def _pair(which):
+    if which == "c5gap":
+        # the bench's C5 layout: two modules (module 2 pools the concat of
+        # module 1 directly) and a GAP head
+        return (F.inception_v3(modules=2, image=35, width=4, head="gap"),
+                F.inception_v3(modules=2, image=35, width=4, head="gap", native=True))
     if which == "c3":
         return F.mobilenet_v2(blocks=MNV2), F.mobilenet_v2(blocks=MNV2, native=True)
     return (F.inception_v3(modules=1, image=29, width=4),
@@ -109,7 +114,7 @@ def test_native_pipeline_vs_graph_oracle(b200, port, which, spec_name):
 
 
 @pytest.mark.parametrize("which,spec_name,min_bit", [("c3", "arm_vmlal_like", 4), ("c3", "int8_int32", 4),
-                                                    ("c5", "int8_int32", 4)])
+                                                    ("c5", "int8_int32", 4), ("c5gap", "int8_int32", 4)])
 def test_native_ops_on_fused_engine(b200, cuda_lib, which, spec_name, min_bit):
     """Native graphs under power-of-two thresholds run on the fused engine —
     C3 MobileNetV2's depthwise convs as a CUDA-core stage of int8 codes
