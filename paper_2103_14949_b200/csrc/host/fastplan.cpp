@@ -2118,18 +2118,25 @@ void FastPlan::run_stage(Run& r, size_t si) {
       auto ck = std::make_pair(static_cast<int>(si), key);
       auto it = wcache_.find(ck);
       if (it == wcache_.end()) {
+        // codes [tap][ldk], then the tap quads [ceil(taps/4)][ldk] words after them
         const size_t cbytes = static_cast<size_t>(st.Kpad);
-        auto codes = engine::device_alloc_on(ST(), cbytes + 16);
+        const size_t qoff = (cbytes + 15) / 16 * 16;
+        const size_t qbytes = static_cast<size_t>((st.taps + 3) / 4) * st.ldk * 4;
+        auto codes = engine::device_alloc_on(ST(), qoff + qbytes + 16);
         kern::weight_codes_v2(plan_.constant(st.w_const).f(), static_cast<int8_t*>(codes.get()), 1, st.C,
                               st.taps, st.ldk, st.Kpad, wf, ST());
+        kern::dw_weight_quads(static_cast<const int8_t*>(codes.get()), st.taps, st.ldk,
+                              reinterpret_cast<int32_t*>(static_cast<int8_t*>(codes.get()) + qoff), ST());
         it = wcache_.emplace(ck, codes).first;
-        wcache_bytes_ += cbytes + 16;
+        wcache_bytes_ += qoff + qbytes + 16;
       }
+      const size_t qoff = (static_cast<size_t>(st.Kpad) + 15) / 16 * 16;
       const Val& dv = *vals_[static_cast<size_t>(st.in_val)];
       const float sxw = r.scale_by_step.at(dv.sq_step) * wf.s;  // pow2 x pow2: exact
       kern::stage_dw_conv(static_cast<const int8_t*>(buf(r, st.in_val)), static_cast<int>(dv.ld),
                           batch * st.n0, st.C, st.H, st.W, st.KH, st.KW, st.sh, st.sw, st.ph, st.pw,
-                          st.OH, st.OW, static_cast<const int8_t*>(it->second.get()), st.ldk,
+                          st.OH, st.OW,
+                          reinterpret_cast<const int32_t*>(static_cast<const int8_t*>(it->second.get()) + qoff), st.ldk,
                           st.bias_const >= 0 ? plan_.constant(st.bias_const).f() : nullptr, sxw, pa, ST());
       break;
     }

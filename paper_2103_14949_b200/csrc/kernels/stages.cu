@@ -144,11 +144,11 @@ __global__ void avgpool_f32_kernel(const float* __restrict__ x, int ld, int N, i
 // code x weight-code products, then v = RN24(acc * s_x*s_w + bias) — the
 // reference's double accumulation rounded to float, exact for power-of-two
 // scales (|acc| <= taps * 128 * 128 < 2^24 keeps acc * s an exact float and
-// the double rounding innocuous) — and the consumers' program.  Weight codes
-// are [tap][ldw] (16 channels per 16-byte load).
+// the double rounding innocuous) — and the consumers' program.  Weights are
+// tap quads [ceil(taps/4)][ldw] of packed int8 codes (dw_weight_quads).
 __global__ void dw_conv_kernel(const int8_t* __restrict__ x, int ld, int N, int C, int H, int W,
                                int KH, int KW, int sh, int sw, int ph, int pw, int OH, int OW,
-                               const int8_t* __restrict__ wc, int ldw, const float* __restrict__ bias,
+                               const int32_t* __restrict__ wq, int ldw, const float* __restrict__ bias,
                                float scale, ProgArgs prog) {
   pdl_trigger();
   pdl_wait();
@@ -166,27 +166,48 @@ __global__ void dw_conv_kernel(const int8_t* __restrict__ x, int ld, int N, int 
     const int64_t n = m / (static_cast<int64_t>(OW) * OH);
     const int c0 = grp * 16;
     const int nvalid = C - c0 < 16 ? C - c0 : 16;
+    // taps in quads: per 4 channels, the four taps' input words are byte-
+    // transposed (8 PRMT) so each channel's 4 taps share one word, then one
+    // dp4a per channel against its pre-packed weight quad (wq: [quad][ldw]
+    // words, zero past the last tap) — 12 instructions per 16 products
     int acc[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) acc[j] = 0;
-    for (int a = 0; a < KH; ++a) {
-      const int ih = oh * sh - ph + a;
-      if (ih < 0 || ih >= H) continue;
-      for (int b = 0; b < KW; ++b) {
-        const int iw = ow * sw - pw + b;
-        if (iw < 0 || iw >= W) continue;
-        const int4 xr = __ldg(reinterpret_cast<const int4*>(x + ((n * H + ih) * W + iw) * ld + c0));
-        const int4 wr = __ldg(reinterpret_cast<const int4*>(wc + (a * KW + b) * ldw + c0));
-        const uint32_t xw[4] = {static_cast<uint32_t>(xr.x), static_cast<uint32_t>(xr.y),
-                                static_cast<uint32_t>(xr.z), static_cast<uint32_t>(xr.w)};
-        const uint32_t ww[4] = {static_cast<uint32_t>(wr.x), static_cast<uint32_t>(wr.y),
-                                static_cast<uint32_t>(wr.z), static_cast<uint32_t>(wr.w)};
+    const int taps = KH * KW;
+    int t = 0, a = 0, b = 0;
+    for (int q = 0; t < taps; ++q) {
+      uint32_t X[4][4];  // [tap in quad][channel word]
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int xb = static_cast<int8_t>((xw[j >> 2] >> (8 * (j & 3))) & 0xFFu);
-          const int wb = static_cast<int8_t>((ww[j >> 2] >> (8 * (j & 3))) & 0xFFu);
-          acc[j] += xb * wb;
+      for (int k = 0; k < 4; ++k) {
+        int4 xr = make_int4(0, 0, 0, 0);
+        if (t < taps) {
+          const int ih = oh * sh - ph + a, iw = ow * sw - pw + b;
+          if (ih >= 0 && ih < H && iw >= 0 && iw < W) {
+            xr = __ldg(reinterpret_cast<const int4*>(x + ((n * H + ih) * W + iw) * ld + c0));
+          }
+          ++t;
+          if (++b == KW) {
+            b = 0;
+            ++a;
+          }
         }
+        X[k][0] = static_cast<uint32_t>(xr.x);
+        X[k][1] = static_cast<uint32_t>(xr.y);
+        X[k][2] = static_cast<uint32_t>(xr.z);
+        X[k][3] = static_cast<uint32_t>(xr.w);
+      }
+      const int4* wp = reinterpret_cast<const int4*>(wq + static_cast<int64_t>(q) * ldw + c0);
+#pragma unroll
+      for (int g4 = 0; g4 < 4; ++g4) {
+        const int4 wr = __ldg(wp + g4);
+        const uint32_t t0 = __byte_perm(X[0][g4], X[1][g4], 0x5140);
+        const uint32_t t1 = __byte_perm(X[2][g4], X[3][g4], 0x5140);
+        const uint32_t t2 = __byte_perm(X[0][g4], X[1][g4], 0x7362);
+        const uint32_t t3 = __byte_perm(X[2][g4], X[3][g4], 0x7362);
+        acc[4 * g4 + 0] = __dp4a(static_cast<int>(__byte_perm(t0, t1, 0x5410)), wr.x, acc[4 * g4 + 0]);
+        acc[4 * g4 + 1] = __dp4a(static_cast<int>(__byte_perm(t0, t1, 0x7632)), wr.y, acc[4 * g4 + 1]);
+        acc[4 * g4 + 2] = __dp4a(static_cast<int>(__byte_perm(t2, t3, 0x5410)), wr.z, acc[4 * g4 + 2]);
+        acc[4 * g4 + 3] = __dp4a(static_cast<int>(__byte_perm(t2, t3, 0x7632)), wr.w, acc[4 * g4 + 3]);
       }
     }
     float v[16];
@@ -679,13 +700,39 @@ void stage_avgpool_f32(const float* x, int ld, int N, int C, int H, int W, int O
   QC_CUDA_CHECK_LAUNCH();
 }
 
+// [tap][ldw] int8 codes -> [quad][ldw] words of 4 consecutive taps' codes
+__global__ void dw_weight_quads_kernel(const int8_t* __restrict__ codes, int taps, int ldw,
+                                       int32_t* __restrict__ quads) {
+  pdl_trigger();
+  pdl_wait();
+  const int nq = (taps + 3) / 4;
+  const int64_t total = static_cast<int64_t>(nq) * ldw;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int q = static_cast<int>(i / ldw), c = static_cast<int>(i % ldw);
+    uint32_t w = 0;
+    for (int k = 0; k < 4; ++k) {
+      const int t = 4 * q + k;
+      if (t < taps) w |= static_cast<uint32_t>(static_cast<uint8_t>(codes[static_cast<int64_t>(t) * ldw + c])) << (8 * k);
+    }
+    quads[i] = static_cast<int32_t>(w);
+  }
+}
+
+void dw_weight_quads(const int8_t* codes, int taps, int ldw, int32_t* quads, cudaStream_t s) {
+  const int64_t total = static_cast<int64_t>((taps + 3) / 4) * ldw;
+  if (total <= 0) return;
+  launch_pdl(dw_weight_quads_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, codes, taps, ldw, quads);
+  QC_CUDA_CHECK_LAUNCH();
+}
+
 void stage_dw_conv(const int8_t* x, int ld, int N, int C, int H, int W, int KH, int KW, int sh,
-                   int sw, int ph, int pw, int OH, int OW, const int8_t* wcodes, int ldw,
+                   int sw, int ph, int pw, int OH, int OW, const int32_t* wquads, int ldw,
                    const float* bias, float scale, const ProgArgs& prog, cudaStream_t s) {
   const int64_t total = static_cast<int64_t>(N) * OH * OW * ((C + 15) / 16);
   if (total <= 0) return;
   launch_pdl(dw_conv_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, x, ld, N, C, H, W, KH, KW,
-             sh, sw, ph, pw, OH, OW, wcodes, ldw, bias, scale, prog);
+             sh, sw, ph, pw, OH, OW, wquads, ldw, bias, scale, prog);
   QC_CUDA_CHECK_LAUNCH();
 }
 
