@@ -113,6 +113,11 @@ double code_absmax(const FSq& f) {
                   std::fabs(static_cast<double>(f.qmax) - f.zp));
 }
 
+bool no_clip_fold() {
+  static const bool off = std::getenv("QUANTC_NO_CLIP_FOLD") != nullptr;
+  return off;
+}
+
 // Per-run table optimisation of one stage (observable results unchanged):
 //  * interval analysis of |v| along the program; an accumulator clamp that
 //    the bound proves can never fire is dropped (has_acc = 0);
@@ -147,6 +152,26 @@ void optimise_tables(kern::StageTables& t, double v0) {
           out.push_back(ins);
           ++pc;  // relu folded
           continue;
+        }
+        // sq -> clip(lo, hi) (e.g. relu6) folds into the code clamp when both
+        // bounds sit on the sq's grid: clip((q-zp)*s, lo, hi) ==
+        // (clamp(q, zp + lo/s, zp + hi/s) - zp)*s for integral lo/s, hi/s
+        const bool clip_next = pc + 1 < t.n_code && t.code[pc + 1].op == kern::kPClip;
+        if (ins.op == kern::kPSq && clip_next && !f.passthrough && !no_clip_fold()) {
+          const float2 c = t.clip[t.code[pc + 1].a];
+          const double ql = static_cast<double>(c.x) / f.s, qh = static_cast<double>(c.y) / f.s;
+          if (std::isfinite(ql) && std::isfinite(qh) && ql == std::floor(ql) && qh == std::floor(qh) &&
+              ql <= qh && std::fabs(ql) < 1e6 && std::fabs(qh) < 1e6) {
+            const float lo = static_cast<float>(f.zp + ql), hi = static_cast<float>(f.zp + qh);
+            f.qmin = std::min(std::max(f.qmin, lo), hi);
+            f.qmax = std::max(std::min(f.qmax, hi), lo);
+            f.q_lo = std::min(std::max(f.q_lo, lo), hi);
+            f.q_hi = std::min(std::max(f.q_hi, lo), hi);
+            b = std::min(b, std::max(std::fabs(static_cast<double>(c.x)), std::fabs(static_cast<double>(c.y))));
+            out.push_back(ins);
+            ++pc;  // clip folded
+            continue;
+          }
         }
         break;
       }
