@@ -617,6 +617,26 @@ bool Runner::exec_conv_int_tc(int i, bool dense, const kern::ConvShape& cs, cons
   ie.codes = static_cast<uint8_t*>(y.codes.get());
   ie.codes_ld = y.codes_ld;
   fill_posts(ie, i, chain);
+  {
+    static const bool off32 = std::getenv("QUANTC_NO_INT_FAST32") != nullptr;
+    bool f32ok = !off32;
+    for (int k = 0; k < ie.n_post; ++k) {
+      const kern::IntEpi::Post& p = ie.post[k];
+      if (p.kind == kern::kPostRequantize) {
+        f32ok = f32ok && p.mult == (1 << 30) && p.shift >= 30 && p.shift < 61 &&
+                std::abs(p.in_zp) < (1 << 16) && std::abs(p.out_zp) < (1 << 16);
+      } else if (p.kind == kern::kPostAdd) {
+        // the other operand of the add at chain position k
+        const int run = k == 0 ? i : chain[static_cast<size_t>(k - 1)];
+        const auto& in = plan.steps()[static_cast<size_t>(chain[static_cast<size_t>(k)])].in;
+        const int other = in[0] == run ? in[1] : in[0];
+        f32ok = f32ok && vals[static_cast<size_t>(other)].dtype.width() <= 16;
+      } else if (p.kind == kern::kPostRelu) {
+        f32ok = f32ok && std::abs(p.out_zp) < (1 << 16);
+      }
+    }
+    ie.fast32 = f32ok ? 1 : 0;
+  }
   kern::tc_conv(sp, S());
   device::counters().tcgen05_gemms++;
   finish_int(i, chain, y, cs, d, w, b, zps);
@@ -706,8 +726,13 @@ void Runner::fill_posts(kern::IntEpi& ie, int i, const std::vector<int>& chain) 
       p.other = vals[static_cast<size_t>(other)].i();
     } else {
       p.kind = kern::kPostRequantize;
-      p.mult = n.attr<int64_t>("multiplier");
-      p.shift = n.attr<int>("shift");
+      const int64_t mult = n.attr<int64_t>("multiplier");
+      const int shift = n.attr<int>("shift");
+      if (mult < INT32_MIN || mult > INT32_MAX || shift < -32768 || shift > 32767) {
+        throw EvalError("requantize multiplier/shift out of range at node " + std::to_string(n.id));
+      }
+      p.mult = static_cast<int32_t>(mult);
+      p.shift = static_cast<int16_t>(shift);
       p.in_zp = static_cast<int32_t>(n.attr_or<int64_t>("in_zero_point", 0));
       p.out_zp = static_cast<int32_t>(n.attr_or<int64_t>("zero_point", 0));
       p.q_min = static_cast<int32_t>(n.attr<int64_t>("q_min"));

@@ -1036,9 +1036,45 @@ __global__ void __launch_bounds__(Layout<EPIW>::THREADS, 1)
               v[j] = v[j] < amin ? amin : amax;
             }
           }
+          // 32-bit chain (host flag ie.fast32: every requantize is a pow2
+          // rounding right shift — multiplier 2^30, shift >= 30 — and every
+          // add operand is <= 16-bit) when this chunk's values are < 2^30:
+          // the same rounding as the int64 form below, in int32 registers
+          bool small = ie.fast32 != 0;
+#pragma unroll
+          for (int j = 0; j < EW; ++j) small = small && v[j] < (int64_t{1} << 30) && v[j] > -(int64_t{1} << 30);
+          if (small) {
+            int32_t w[EW];
+#pragma unroll
+            for (int j = 0; j < EW; ++j) w[j] = static_cast<int32_t>(v[j]);
+#pragma unroll
+            for (int k = 0; k < kMaxIntPosts; ++k) {
+              if (k >= npost) break;
+              const IntEpi::Post& pp = ie.post[k];
+              if (pp.kind == kPostRelu) {
+#pragma unroll
+                for (int j = 0; j < EW; ++j) w[j] = max(w[j], pp.out_zp);
+              } else if (pp.kind == kPostAdd) {
+#pragma unroll
+                for (int j = 0; j < EW; ++j) w[j] += cur[j];
+              } else {
+                // round half away from zero of t / 2^r: (t + 2^(r-1) - [t < 0]) >> r
+                const int r = pp.shift - 30;
+                const int32_t h = r > 0 ? (1 << (r - 1)) : 0;
+#pragma unroll
+                for (int j = 0; j < EW; ++j) {
+                  const int32_t t = w[j] - pp.in_zp;
+                  const int32_t q = r > 0 ? ((t + h - (t < 0 ? 1 : 0)) >> r) : t;
+                  w[j] = min(max(q + pp.out_zp, pp.q_min), pp.q_max);
+                }
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < EW; ++j) v[j] = w[j];
+          }
 #pragma unroll
           for (int k = 0; k < kMaxIntPosts; ++k) {
-            if (k >= npost) break;
+            if (small || k >= npost) break;
             const IntEpi::Post& pp = ie.post[k];
             if (pp.kind == kPostRelu) {
               const int64_t z = pp.out_zp;

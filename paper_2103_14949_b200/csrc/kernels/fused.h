@@ -205,7 +205,7 @@ QC_HD constexpr bool shape_is_int_fold(int s) {
 //   v outside [acc_min, acc_max] -> trap (lowest flat index) or saturate
 //   requantize (optional): q = clamp(rescale(v - in_zp) + out_zp, q_min, q_max)
 //   y[((img*O + o)*OH + oh)*OW + ow] = v or q   (int32, NCHW like Tensor)
-constexpr int kMaxIntPosts = 4;  // requantize, add, requantize, relu (kernel parameter block: <= 4 KB total)
+constexpr int kMaxIntPosts = 5;  // e.g. requantize, add, requantize, relu, requantize (parameter block <= 4 KB)
 struct IntEpi {
   int32_t* y;
   const int32_t* bias;  // may be null
@@ -215,9 +215,9 @@ struct IntEpi {
   // fused elementwise chain after the accumulator clamp (sole-consumer
   // requantize / relu nodes, reference interpreter.cpp:326-336, :464-482)
   struct Post {
-    int32_t kind;   // kPostRequantize, kPostRelu or kPostAdd
-    int32_t shift;  // requantize
-    int64_t mult;   // requantize
+    int16_t kind;   // kPostRequantize, kPostRelu or kPostAdd
+    int16_t shift;  // requantize
+    int32_t mult;   // requantize (RequantParams::multiplier is int32)
     int32_t in_zp, out_zp, q_min, q_max;  // requantize; relu: out_zp = zero point
     const int32_t* other;  // add: the other operand (same flat indexing as y)
   };
@@ -228,6 +228,10 @@ struct IntEpi {
   // input, so it skips its pack pass
   uint8_t* codes;
   int32_t codes_ld;
+  // 1: every requantize post is multiplier 2^30 with shift >= 30 and every
+  // add operand's dtype is <= 16 bits — chunks whose values are < 2^30 run
+  // the chain in int32 (kShapeInt epilogue)
+  int32_t fast32;
   int32_t OHW;  // output pixels per image (1 for dense)
   int32_t a_unsigned;  // A codes are uint8 (tcgen05 unsigned A)
 };
