@@ -254,11 +254,27 @@ __global__ void maxpool_stores_kernel(const int8_t* __restrict__ x, int ld, int 
   const int64_t total = static_cast<int64_t>(N) * OH * OW * groups;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int grp = static_cast<int>(i % groups);
-    const int64_t m = i / groups;
-    const int ow = static_cast<int>(m % OW);
-    const int oh = static_cast<int>((m / OW) % OH);
-    const int64_t n = m / (static_cast<int64_t>(OW) * OH);
+    // 32-bit index decomposition when the space fits (64-bit divisions are
+    // ~100 instructions each: four of them per item dominated this kernel)
+    int grp, ow, oh;
+    int64_t m, n;
+    if (total <= 0xFFFFFFFFll) {
+      const uint32_t ii = static_cast<uint32_t>(i);
+      const uint32_t mm = ii / static_cast<uint32_t>(groups);
+      grp = static_cast<int>(ii - mm * static_cast<uint32_t>(groups));
+      const uint32_t t = mm / static_cast<uint32_t>(OW);
+      ow = static_cast<int>(mm - t * static_cast<uint32_t>(OW));
+      const uint32_t nn = t / static_cast<uint32_t>(OH);
+      oh = static_cast<int>(t - nn * static_cast<uint32_t>(OH));
+      m = mm;
+      n = nn;
+    } else {
+      grp = static_cast<int>(i % groups);
+      m = i / groups;
+      ow = static_cast<int>(m % OW);
+      oh = static_cast<int>((m / OW) % OH);
+      n = m / (static_cast<int64_t>(OW) * OH);
+    }
     uint32_t best[4] = {0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u};
     if constexpr (K3) {
       // 3x3 window: the nine (masked) 16-byte loads are issued together
@@ -357,10 +373,21 @@ __global__ void input_s2d_kernel(const float* __restrict__ x, int N, int C, int 
   const int64_t total = static_cast<int64_t>(N) * H2 * W2;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int w2 = static_cast<int>(i % W2);
-    const int64_t t = i / W2;
-    const int h2 = static_cast<int>(t % H2);
-    const int64_t n = t / H2;
+    int w2, h2;
+    int64_t n;
+    if (total <= 0xFFFFFFFFll) {  // 32-bit decomposition (see maxpool_stores_kernel)
+      const uint32_t ii = static_cast<uint32_t>(i);
+      const uint32_t t = ii / static_cast<uint32_t>(W2);
+      w2 = static_cast<int>(ii - t * static_cast<uint32_t>(W2));
+      const uint32_t nn = t / static_cast<uint32_t>(H2);
+      h2 = static_cast<int>(t - nn * static_cast<uint32_t>(H2));
+      n = nn;
+    } else {
+      w2 = static_cast<int>(i % W2);
+      const int64_t t = i / W2;
+      h2 = static_cast<int>(t % H2);
+      n = t / H2;
+    }
     uint32_t word[4] = {0, 0, 0, 0};
     const bool pair = (W & 1) == 0;  // the two pixels of a row are one 8-byte load
     for (int c = 0; c < C; ++c) {
@@ -410,10 +437,21 @@ __global__ void input_s2d_multi_kernel(const float* __restrict__ x, int N, int C
   const bool pair = (W & 1) == 0;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int w2 = static_cast<int>(i % W2);
-    const int64_t t = i / W2;
-    const int h2 = static_cast<int>(t % H2);
-    const int64_t n = t / H2;
+    int w2, h2;
+    int64_t n;
+    if (total <= 0xFFFFFFFFll) {  // 32-bit decomposition (see maxpool_stores_kernel)
+      const uint32_t ii = static_cast<uint32_t>(i);
+      const uint32_t t = ii / static_cast<uint32_t>(W2);
+      w2 = static_cast<int>(ii - t * static_cast<uint32_t>(W2));
+      const uint32_t nn = t / static_cast<uint32_t>(H2);
+      h2 = static_cast<int>(t - nn * static_cast<uint32_t>(H2));
+      n = nn;
+    } else {
+      w2 = static_cast<int>(i % W2);
+      const int64_t t = i / W2;
+      h2 = static_cast<int>(t % H2);
+      n = t / H2;
+    }
     float v[4][4] = {};  // [c][dy*2 + dx], C <= 4 (fully unrolled: registers)
     bool ok[4] = {false, false, false, false};
 #pragma unroll
