@@ -113,6 +113,11 @@ double code_absmax(const FSq& f) {
                   std::fabs(static_cast<double>(f.qmax) - f.zp));
 }
 
+bool no_acc_shape() {
+  static const bool off = std::getenv("QUANTC_NO_ACC_SHAPE") != nullptr;
+  return off;
+}
+
 bool no_clip_fold() {
   static const bool off = std::getenv("QUANTC_NO_CLIP_FOLD") != nullptr;
   return off;
@@ -144,6 +149,15 @@ void optimise_tables(kern::StageTables& t, double v0) {
         if (!f.passthrough) b = code_absmax(f) * static_cast<double>(f.s);
         // a passthrough sq without a live accumulator clamp is the identity
         if (ins.op == kern::kPSq && f.passthrough && !f.has_acc) continue;
+        // a passthrough accumulator clamp followed by a clip whose bounds lie
+        // inside the saturation range is absorbed by the clip (v < lo_up <= a
+        // gives clip(lo_rn) = a = clip(v); symmetric above): e.g. MobileNetV2's
+        // int16 accumulator sq before relu6
+        if (ins.op == kern::kPSq && f.passthrough && f.has_acc && !no_clip_fold() && pc + 1 < t.n_code &&
+            t.code[pc + 1].op == kern::kPClip) {
+          const float2 c = t.clip[t.code[pc + 1].a];
+          if (f.lo_up <= c.x && f.lo_rn <= c.x && f.hi_dn >= c.y && f.hi_rn >= c.y) continue;
+        }
         const bool relu_next = pc + 1 < t.n_code && t.code[pc + 1].op == kern::kPRelu;
         if (ins.op == kern::kPSq && relu_next && !f.passthrough) {
           f.qmin = std::max(f.qmin, f.zp);
@@ -178,6 +192,21 @@ void optimise_tables(kern::StageTables& t, double v0) {
       case kern::kPClip: {
         const float2 c = t.clip[ins.a];
         b = std::min(b, std::max(std::fabs(static_cast<double>(c.x)), std::fabs(static_cast<double>(c.y))));
+        // clip(a, b) -> sq folds into the sq's code clamp when a/s and b/s
+        // are integers: round is monotonic and both bounds are grid points
+        if (pc + 1 < t.n_code && !no_clip_fold() &&
+            (t.code[pc + 1].op == kern::kPSq || t.code[pc + 1].op == kern::kPSqStore8)) {
+          FSq& f = t.sq[t.code[pc + 1].a];
+          const double ql = static_cast<double>(c.x) / f.s, qh = static_cast<double>(c.y) / f.s;
+          if (!f.passthrough && !f.has_acc && std::isfinite(ql) && std::isfinite(qh) &&
+              ql == std::floor(ql) && qh == std::floor(qh) && ql <= qh && std::fabs(ql) < 1e6 &&
+              std::fabs(qh) < 1e6) {
+            const float lo = static_cast<float>(f.zp + ql), hi = static_cast<float>(f.zp + qh);
+            f.qmin = std::min(std::max(f.qmin, lo), hi);
+            f.qmax = std::max(std::min(f.qmax, hi), lo);
+            continue;  // clip folded into the next sq
+          }
+        }
         break;
       }
       case kern::kPAdd: {
@@ -677,12 +706,23 @@ FSq make_fsq(const QParams& p) {
 // O % 16 == 0 (whole 16-column chunks).  Anything else runs the interpreter.
 int classify_shape(const kern::StageTables& t, int O) {
   std::vector<uint8_t> ops;
+  bool acc0 = false;  // the conv output's sq carries a live accumulator clamp
+  bool pt0 = false;   // ... as a passthrough (a float edge's accumulator simulation)
   for (int i = 0; i < t.n_code; ++i) {
     const kern::ProgInstr& in = t.code[i];
     ops.push_back(in.op);
     if (in.op == kern::kPSq || in.op == kern::kPSqStore8) {
       const kern::FSq& f = t.sq[in.a];
-      if (f.zp != 0.0f || f.has_acc || f.passthrough) return 0;
+      if (f.zp != 0.0f) return 0;
+      if (f.passthrough) {
+        if (i != 0 || in.op != kern::kPSq || !f.has_acc || no_acc_shape()) return 0;
+        pt0 = acc0 = true;
+        continue;
+      }
+      if (f.has_acc) {
+        if (i != 0 || no_acc_shape()) return 0;
+        acc0 = true;
+      }
     }
     if ((in.op == kern::kPSqStore8 || in.op == kern::kPAdd) &&
         (t.buf[in.b].slot < 0 || t.buf[in.b].kind != 0)) {
@@ -696,6 +736,13 @@ int classify_shape(const kern::StageTables& t, int O) {
     return kern::kShapeSqF32;
   }
   if (O % 16 != 0) return 0;
+  if (acc0) {
+    // [passthrough acc sq, sq_store8]: the clamp overrides the store's code
+    if (pt0) return ops == V{kern::kPSq, kern::kPSqStore8} ? kern::kShapeStoreAcc : 0;
+    if (ops == V{kern::kPSq, kern::kPSqStore8}) return kern::kShapeSqStoreAcc;
+    if (ops == V{kern::kPSqStore8}) return kern::kShapeStoreAcc;
+    return 0;
+  }
   if (ops == V{kern::kPSqStore8}) return 1;
   if (ops == V{kern::kPSq, kern::kPSqStore8}) return 2;
   if (ops == V{kern::kPSq, kern::kPAdd, kern::kPSq, kern::kPPush, kern::kPSqStore8, kern::kPPop,
@@ -811,7 +858,14 @@ bool make_epi(const kern::StageTables& t, int shape, double sxw, kern::EpiConsts
   int res = -1, out0 = -1, out1 = -1;
   switch (shape) {
     case 1: qs = {c[0].a}; out0 = static_cast<int>(c[0].b); break;
-    case 2: qs = {c[0].a, c[1].a}; out0 = static_cast<int>(c[1].b); break;
+    case kern::kShapeStoreAcc: {
+      const int k = t.n_code == 2 ? 1 : 0;  // [pt acc sq, sq_store8] or [sq_store8 with acc]
+      qs = {c[k].a};
+      out0 = static_cast<int>(c[k].b);
+      break;
+    }
+    case 2:
+    case kern::kShapeSqStoreAcc: qs = {c[0].a, c[1].a}; out0 = static_cast<int>(c[1].b); break;
     case 3:
       qs = {c[0].a, c[2].a, c[4].a, c[6].a};
       res = static_cast<int>(c[1].b);
@@ -902,6 +956,30 @@ bool make_epi(const kern::StageTables& t, int shape, double sxw, kern::EpiConsts
   }
   e.slot_out[0] = out0 >= 0 && shape != 5 && shape != kern::kShapeSqF32 ? t.buf[out0].slot : -1;
   e.slot_out[1] = out1 >= 0 ? t.buf[out1].slot : -1;
+  if (shape == kern::kShapeSqStoreAcc || shape == kern::kShapeStoreAcc) {
+    // sq0's accumulator clamp on x0 = v / s0 (power-of-two scaling: exact),
+    // saturation codes in the domain epi_round leaves x0 in (T: M + code)
+    const kern::FSq& f0 = t.sq[qs[0]];  // the grid sq x0 is in
+    const bool pt = shape == kern::kShapeStoreAcc && t.n_code == 2;
+    const kern::FSq& fa = pt ? t.sq[c[0].a] : f0;  // the accumulator clamp
+    float alo = 0.0f, ahi = 0.0f;
+    if (!exact_float(static_cast<double>(fa.lo_up) / f0.s, alo) ||
+        !exact_float(static_cast<double>(fa.hi_dn) / f0.s, ahi)) {
+      return false;
+    }
+    double clo = f0.q_lo, chi = f0.q_hi;
+    if (pt) {
+      // the store sq's code of the saturated value (round half away, clamp)
+      clo = std::clamp(std::round(static_cast<double>(fa.lo_rn) / f0.s) + f0.zp, static_cast<double>(f0.qmin),
+                       static_cast<double>(f0.qmax));
+      chi = std::clamp(std::round(static_cast<double>(fa.hi_rn) / f0.s) + f0.zp, static_cast<double>(f0.qmin),
+                       static_cast<double>(f0.qmax));
+    }
+    const double base = (e.q[0].flags & kEpiNonneg) ? kern::kMagic : 0.0;
+    e.q[3].lo = alo;
+    e.q[3].hi = ahi;
+    if (!exact_float(base + clo, e.q[3].k) || !exact_float(base + chi, e.q[3].off)) return false;
+  }
   return true;
 }
 

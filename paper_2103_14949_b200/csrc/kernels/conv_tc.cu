@@ -1470,7 +1470,7 @@ bool band_ok(const TcConvSpec& sp) {
   static const bool off = std::getenv("QUANTC_NO_BAND") != nullptr;
   const int sh = sp.prog.shape;
   const bool store_only = sh == kShapeStore || sh == kShapeSqStore || sh == kShapeSqStoreId ||
-                          sh == kShapeSqStoreInt;
+                          sh == kShapeSqStoreInt || sh == kShapeSqStoreAcc || sh == kShapeStoreAcc;
   return !off && store_only && sp.gather && sp.ld == 16 && sp.C <= 16 && sp.sh == 1 && sp.sw == 1 &&
          sp.KH == 4 && sp.KW == 4 && sp.OW <= BM && sp.OW + sp.KW - 1 <= 128 && sp.KH <= 16 &&
          sp.KH * sp.KW * 16 <= sp.Kpad && sp.Kpad <= 256 && sp.O % 16 == 0 && sp.res_ptr == nullptr &&
@@ -1651,6 +1651,12 @@ void launch_bn(const TcMapsT<kMaxGroups>* maps, const TcGroupsT<kMaxGroups>* grp
       break;
     case kShapeSqStore:
       launch_tc<BN, kShapeSqStore>(maps, grp, a, s);
+      break;
+    case kShapeSqStoreAcc:
+      launch_tc<BN, kShapeSqStoreAcc>(maps, grp, a, s);
+      break;
+    case kShapeStoreAcc:
+      launch_tc<BN, kShapeStoreAcc>(maps, grp, a, s);
       break;
     case kShapeAddFork:
       launch_tc<BN, kShapeAddFork>(maps, grp, a, s);

@@ -404,6 +404,26 @@ __device__ __forceinline__ void run_shape_epi(float (&x)[16], const EpiConsts& e
     if (e.slot_out[1] >= 0) sts128(tile_addr(io, e.slot_out[1], cl), packed);
     return;
   }
+  if constexpr (SHAPE == kShapeSqStoreAcc || SHAPE == kShapeStoreAcc) {
+    // sq0 with a live accumulator clamp: the reference saturates on the
+    // conv value (fsq_code: v < lo_up -> q_lo, v > hi_dn -> q_hi), i.e. on
+    // x0 against the bounds scaled into sq0's grid
+    float raw[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) raw[j] = x[j];
+    epi_round(x, e.q[0]);
+    const float alo = e.q[3].lo, ahi = e.q[3].hi, clo = e.q[3].k, chi = e.q[3].off;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) x[j] = raw[j] < alo ? clo : (raw[j] > ahi ? chi : x[j]);
+    if constexpr (SHAPE == kShapeStoreAcc) {
+      epi_store(x, e.q[0], io, e.slot_out[0], cl);
+      return;
+    }
+    float y0[16];
+    epi_next(x, y0, e.q[1]);
+    epi_store(y0, e.q[1], io, e.slot_out[0], cl);
+    return;
+  }
   epi_round(x, e.q[0]);
   if constexpr (SHAPE == kShapeSqF32) {
     // fp32 value of the code: v = fma(R, s, off) (T-domain offset folded)

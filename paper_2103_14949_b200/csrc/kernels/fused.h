@@ -195,7 +195,11 @@ struct EpiConsts {
 //      exact integer arithmetic on codes (every scale is a power of two)
 enum : int { kShapeGeneric = 0, kShapeStore = 1, kShapeSqStore = 2, kShapeAddFork = 3,
              kShapeAdd = 4, kShapeAddF32 = 5, kShapeSqStoreId = 6, kShapeAddForkId = 7,
-             kShapeInt = 8, kShapeSqF32 = 9, kShapeSqStoreInt = 10, kShapeAddForkInt = 11 };
+             kShapeInt = 8, kShapeSqF32 = 9, kShapeSqStoreInt = 10, kShapeAddForkInt = 11,
+             kShapeSqStoreAcc = 12, kShapeStoreAcc = 13 };
+//  12: shape 2 whose sq0 carries a live accumulator clamp (e.g. the
+//      arm_vmlal_like int16 sums): x0 outside the host-scaled bounds q[3].lo /
+//      q[3].hi takes the saturation codes q[3].k / q[3].off
 QC_HD constexpr bool shape_is_int_fold(int s) {
   return s == kShapeSqStoreInt || s == kShapeAddForkInt;
 }
