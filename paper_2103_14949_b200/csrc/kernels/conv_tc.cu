@@ -1693,6 +1693,25 @@ void launch_bn(const TcMapsT<kMaxGroups>* maps, const TcGroupsT<kMaxGroups>* grp
 
 }  // namespace
 
+// The kernel instances of each tile width live in their own translation unit
+// (the Makefile compiles this file three more times with QC_TC_BN_ONLY=64 /
+// 128 / 256), so nvcc builds them in parallel; the dispatch below calls them.
+void tc_launch_bn64(const TcMapsT<kMaxGroups>* maps, const TcGroupsT<kMaxGroups>* grp, const TcArgs& a,
+                    cudaStream_t s);
+void tc_launch_bn128(const TcMapsT<kMaxGroups>* maps, const TcGroupsT<kMaxGroups>* grp, const TcArgs& a,
+                     cudaStream_t s);
+void tc_launch_bn256(const TcMapsT<kMaxGroups>* maps, const TcGroupsT<kMaxGroups>* grp, const TcArgs& a,
+                     cudaStream_t s);
+
+#if defined(QC_TC_BN_ONLY)
+#define QC_TC_ENTRY2(bn) tc_launch_bn##bn
+#define QC_TC_ENTRY(bn) QC_TC_ENTRY2(bn)
+void QC_TC_ENTRY(QC_TC_BN_ONLY)(const TcMapsT<kMaxGroups>* maps, const TcGroupsT<kMaxGroups>* grp,
+                                const TcArgs& a, cudaStream_t s) {
+  launch_bn<QC_TC_BN_ONLY>(maps, grp, a, s);
+}
+#else
+
 int tc_conv_bn(int O) { return O <= 64 ? 64 : (O <= 128 ? 128 : 256); }
 
 void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
@@ -1915,12 +1934,14 @@ void tc_conv(const TcConvSpec& sp, cudaStream_t s) {
   }
   const TcMapsT<kMaxGroups>* mp = &maps;
   if (BN == 64) {
-    launch_bn<64>(mp, &grp, a, s);
+    tc_launch_bn64(mp, &grp, a, s);
   } else if (BN == 128) {
-    launch_bn<128>(mp, &grp, a, s);
+    tc_launch_bn128(mp, &grp, a, s);
   } else {
-    launch_bn<256>(mp, &grp, a, s);
+    tc_launch_bn256(mp, &grp, a, s);
   }
 }
+
+#endif  // QC_TC_BN_ONLY
 
 }  // namespace quantc::kern
