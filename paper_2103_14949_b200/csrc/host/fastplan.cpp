@@ -2236,11 +2236,32 @@ void FastPlan::run_stage(Run& r, size_t si) {
       const size_t qoff = (static_cast<size_t>(st.Kpad) + 15) / 16 * 16;
       const Val& dv = *vals_[static_cast<size_t>(st.in_val)];
       const float sxw = r.scale_by_step.at(dv.sq_step) * wf.s;  // pow2 x pow2: exact
+      // [passthrough accumulator sq,] sq_store8 into plain code rows: inline
+      kern::DwFast fast{};
+      {
+        static const bool no_fast = std::getenv("QUANTC_NO_DW_FAST") != nullptr;
+        const kern::StageTables& t = r.tabs[si];
+        const int k = t.n_code - 1;
+        if (!no_fast && (t.n_code == 1 || t.n_code == 2) && t.code[k].op == kern::kPSqStore8 &&
+            t.buf[t.code[k].b].kind == 0 && t.buf[t.code[k].b].hw == 1) {
+          bool ok = true;
+          if (t.n_code == 2) {
+            const FSq& fa = t.sq[t.code[0].a];
+            ok = t.code[0].op == kern::kPSq && fa.passthrough;
+            fast.fa = fa;
+          }
+          if (ok) {
+            fast.n = t.n_code;
+            fast.fs = t.sq[t.code[k].a];
+            fast.buf = t.buf[t.code[k].b];
+          }
+        }
+      }
       kern::stage_dw_conv(static_cast<const int8_t*>(buf(r, st.in_val)), static_cast<int>(dv.ld),
                           batch * st.n0, st.C, st.H, st.W, st.KH, st.KW, st.sh, st.sw, st.ph, st.pw,
                           st.OH, st.OW,
                           reinterpret_cast<const int32_t*>(static_cast<const int8_t*>(it->second.get()) + qoff), st.ldk,
-                          st.bias_const >= 0 ? plan_.constant(st.bias_const).f() : nullptr, sxw, pa, ST());
+                          st.bias_const >= 0 ? plan_.constant(st.bias_const).f() : nullptr, sxw, pa, fast, ST());
       break;
     }
     case Stage::kGemm: {

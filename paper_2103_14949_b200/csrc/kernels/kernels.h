@@ -240,9 +240,18 @@ void stage_avgpool_f32(const float* x, int ld, int N, int C, int H, int W, int O
                        cudaStream_t s);
 // depthwise conv (groups == C == O) of int8 codes with the stage program
 // (fused engine; weights as tap quads [ceil(taps/4)][ldw] from dw_weight_quads)
+// n > 0: the stage program is [passthrough accumulator sq fa (n == 2),]
+// sq_store8 fs -> buf, run without the table interpreter
+struct DwFast {
+  int32_t n;
+  int32_t pad_;
+  FSq fa, fs;
+  ProgBuf buf;
+};
 void stage_dw_conv(const int8_t* x, int ld, int N, int C, int H, int W, int KH, int KW, int sh,
                    int sw, int ph, int pw, int OH, int OW, const int32_t* wquads, int ldw,
-                   const float* bias, float scale, const ProgArgs& prog, cudaStream_t s);
+                   const float* bias, float scale, const ProgArgs& prog, const DwFast& fast,
+                   cudaStream_t s);
 void dw_weight_quads(const int8_t* codes, int taps, int ldw, int32_t* quads, cudaStream_t s);
 void stage_maxpool(const int8_t* x, int ld, float scale, int N, int C, int H, int W, int OH,
                    int OW, int kh, int kw, int sh, int sw, int ph, int pw, const ProgArgs& prog,

@@ -146,15 +146,20 @@ __global__ void avgpool_f32_kernel(const float* __restrict__ x, int ld, int N, i
 // scales (|acc| <= taps * 128 * 128 < 2^24 keeps acc * s an exact float and
 // the double rounding innocuous) — and the consumers' program.  Weights are
 // tap quads [ceil(taps/4)][ldw] of packed int8 codes (dw_weight_quads).
-__global__ void dw_conv_kernel(const int8_t* __restrict__ x, int ld, int N, int C, int H, int W,
+// FAST: the inline [accumulator sq,] sq_store8 program only (no table
+// interpreter: ~60 instead of ~166 registers, so 4x the resident warps)
+template <bool FAST>
+__global__ void __launch_bounds__(256) dw_conv_kernel(const int8_t* __restrict__ x, int ld, int N, int C, int H, int W,
                                int KH, int KW, int sh, int sw, int ph, int pw, int OH, int OW,
                                const int32_t* __restrict__ wq, int ldw, const float* __restrict__ bias,
-                               float scale, ProgArgs prog) {
+                               float scale, ProgArgs prog, DwFast fast) {
   pdl_trigger();
   pdl_wait();
   __shared__ StageTables T;
-  load_tables(&T, prog.tables);
-  __syncthreads();
+  if constexpr (!FAST) {
+    load_tables(&T, prog.tables);
+    __syncthreads();
+  }
   const int groups = (C + 15) / 16;
   const int64_t total = static_cast<int64_t>(N) * OH * OW * groups;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -216,7 +221,16 @@ __global__ void dw_conv_kernel(const int8_t* __restrict__ x, int ld, int N, int 
       const float b = (bias && j < nvalid) ? __ldg(bias + c0 + j) : 0.0f;
       v[j] = __fadd_rn(__fmul_rn(static_cast<float>(acc[j]), scale), b);
     }
-    run_prog<16, 3>(v, m, c0, nvalid, T);
+    if constexpr (FAST) {
+      // the program [passthrough accumulator sq,] sq_store8 without the
+      // interpreter: the same device functions run_prog calls for them
+      if (fast.n == 2) sq_values<16>(v, fast.fa);
+      float q[16];
+      sq_codes<16>(v, q, fast.fs);
+      store_codes<16>(fast.buf, m, c0, nvalid, q, nullptr, 0);
+    } else {
+      run_prog<16, 3>(v, m, c0, nvalid, T);
+    }
   }
 }
 
@@ -766,11 +780,17 @@ void dw_weight_quads(const int8_t* codes, int taps, int ldw, int32_t* quads, cud
 
 void stage_dw_conv(const int8_t* x, int ld, int N, int C, int H, int W, int KH, int KW, int sh,
                    int sw, int ph, int pw, int OH, int OW, const int32_t* wquads, int ldw,
-                   const float* bias, float scale, const ProgArgs& prog, cudaStream_t s) {
+                   const float* bias, float scale, const ProgArgs& prog, const DwFast& fast,
+                   cudaStream_t s) {
   const int64_t total = static_cast<int64_t>(N) * OH * OW * ((C + 15) / 16);
   if (total <= 0) return;
-  launch_pdl(dw_conv_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, x, ld, N, C, H, W, KH, KW,
-             sh, sw, ph, pw, OH, OW, wquads, ldw, bias, scale, prog);
+  if (fast.n > 0) {
+    launch_pdl(dw_conv_kernel<true>, dim3(grid_for(total, 256)), dim3(256), 0, s, x, ld, N, C, H, W, KH, KW,
+               sh, sw, ph, pw, OH, OW, wquads, ldw, bias, scale, prog, fast);
+  } else {
+    launch_pdl(dw_conv_kernel<false>, dim3(grid_for(total, 256)), dim3(256), 0, s, x, ld, N, C, H, W, KH, KW,
+               sh, sw, ph, pw, OH, OW, wquads, ldw, bias, scale, prog, fast);
+  }
   QC_CUDA_CHECK_LAUNCH();
 }
 
