@@ -113,6 +113,27 @@ double code_absmax(const FSq& f) {
                   std::fabs(static_cast<double>(f.qmax) - f.zp));
 }
 
+// a CUDA-core stage whose program is [passthrough accumulator sq,] sq_store8
+// into plain code rows runs it inline (kern::DwFast) instead of through the
+// table interpreter (whose registers cut the kernel's occupancy ~3x)
+kern::DwFast inline_store_program(const kern::StageTables& t) {
+  static const bool off = std::getenv("QUANTC_NO_DW_FAST") != nullptr;
+  kern::DwFast fast{};
+  const int k = t.n_code - 1;
+  if (off || (t.n_code != 1 && t.n_code != 2) || t.code[k].op != kern::kPSqStore8 ||
+      t.buf[t.code[k].b].kind != 0 || t.buf[t.code[k].b].hw != 1) {
+    return fast;
+  }
+  if (t.n_code == 2) {
+    if (t.code[0].op != kern::kPSq || !t.sq[t.code[0].a].passthrough) return fast;
+    fast.fa = t.sq[t.code[0].a];
+  }
+  fast.n = t.n_code;
+  fast.fs = t.sq[t.code[k].a];
+  fast.buf = t.buf[t.code[k].b];
+  return fast;
+}
+
 bool no_acc_shape() {
   static const bool off = std::getenv("QUANTC_NO_ACC_SHAPE") != nullptr;
   return off;
@@ -2204,7 +2225,7 @@ void FastPlan::run_stage(Run& r, size_t si) {
       const double wk = static_cast<double>(static_cast<float>(1.0 / (st.pkh * st.pkw)));
       kern::stage_avgpool_f32(static_cast<const float*>(buf(r, st.in_val)), static_cast<int>(v.ld),
                               batch * st.n0, st.C, st.H, st.W, st.OH, st.OW, st.pkh, st.pkw, st.sh,
-                              st.sw, st.ph, st.pw, wk, pa, ST());
+                              st.sw, st.ph, st.pw, wk, pa, inline_store_program(r.tabs[si]), ST());
       break;
     }
     case Stage::kCat: {
@@ -2237,26 +2258,7 @@ void FastPlan::run_stage(Run& r, size_t si) {
       const Val& dv = *vals_[static_cast<size_t>(st.in_val)];
       const float sxw = r.scale_by_step.at(dv.sq_step) * wf.s;  // pow2 x pow2: exact
       // [passthrough accumulator sq,] sq_store8 into plain code rows: inline
-      kern::DwFast fast{};
-      {
-        static const bool no_fast = std::getenv("QUANTC_NO_DW_FAST") != nullptr;
-        const kern::StageTables& t = r.tabs[si];
-        const int k = t.n_code - 1;
-        if (!no_fast && (t.n_code == 1 || t.n_code == 2) && t.code[k].op == kern::kPSqStore8 &&
-            t.buf[t.code[k].b].kind == 0 && t.buf[t.code[k].b].hw == 1) {
-          bool ok = true;
-          if (t.n_code == 2) {
-            const FSq& fa = t.sq[t.code[0].a];
-            ok = t.code[0].op == kern::kPSq && fa.passthrough;
-            fast.fa = fa;
-          }
-          if (ok) {
-            fast.n = t.n_code;
-            fast.fs = t.sq[t.code[k].a];
-            fast.buf = t.buf[t.code[k].b];
-          }
-        }
-      }
+      const kern::DwFast fast = inline_store_program(r.tabs[si]);
       kern::stage_dw_conv(static_cast<const int8_t*>(buf(r, st.in_val)), static_cast<int>(dv.ld),
                           batch * st.n0, st.C, st.H, st.W, st.KH, st.KW, st.sh, st.sw, st.ph, st.pw,
                           st.OH, st.OW,

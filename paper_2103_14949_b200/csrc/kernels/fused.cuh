@@ -205,6 +205,17 @@ __device__ __forceinline__ void load_values(const ProgBuf& b, int64_t m, int n0,
     }
   } else {
     const float* src = static_cast<const float*>(b.ptr) + buf_off(b, m, n0);
+    if (W % 4 == 0 && nvalid == W && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+#pragma unroll
+      for (int i = 0; i < W / 4; ++i) {
+        const float4 f = *reinterpret_cast<const float4*>(src + 4 * i);
+        o[4 * i] = f.x;
+        o[4 * i + 1] = f.y;
+        o[4 * i + 2] = f.z;
+        o[4 * i + 3] = f.w;
+      }
+      return;
+    }
 #pragma unroll
     for (int j = 0; j < W; ++j) o[j] = j < nvalid ? src[j] : 0.0f;
   }

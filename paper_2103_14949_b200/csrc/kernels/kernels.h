@@ -235,9 +235,10 @@ void stage_input(const float* x, int N, int C, int HW, const ProgArgs& prog, cud
 // max_pool2d over NHWC codes (value = code * scale) -> program
 // average pool (zero padding counted) of fp32 NHWC rows with the stage
 // program (fused engine; the exact engine's double arithmetic, wk = fl32(1/(kh*kw)))
+struct DwFast;
 void stage_avgpool_f32(const float* x, int ld, int N, int C, int H, int W, int OH, int OW, int kh,
                        int kw, int sh, int sw, int ph, int pw, double wk, const ProgArgs& prog,
-                       cudaStream_t s);
+                       const DwFast& fast, cudaStream_t s);
 // depthwise conv (groups == C == O) of int8 codes with the stage program
 // (fused engine; weights as tap quads [ceil(taps/4)][ldw] from dw_weight_quads)
 // n > 0: the stage program is [passthrough accumulator sq fa (n == 2),]

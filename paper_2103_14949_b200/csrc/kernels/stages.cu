@@ -97,14 +97,18 @@ __global__ void maxpool_codes_kernel(const int8_t* __restrict__ x, int ld, float
 // padding (fixtures.py _avg_pool); the reference's double accumulation
 // (x*wk exact in double, one rounding per tap) in (kh, kw) order, as the
 // exact engine's avgpool_kernel (eltwise.cu), then one rounding to float.
-__global__ void avgpool_f32_kernel(const float* __restrict__ x, int ld, int N, int C, int H, int W,
+template <bool FAST>
+__global__ void __launch_bounds__(256) avgpool_f32_kernel(const float* __restrict__ x, int ld, int N, int C, int H, int W,
                                    int OH, int OW, int kh, int kw, int sh, int sw, int ph, int pw,
-                                   double wk, ProgArgs prog) {
+                                   double wk, ProgArgs prog, DwFast fast) {
   pdl_trigger();
   pdl_wait();
   __shared__ StageTables T;
-  load_tables(&T, prog.tables);
-  __syncthreads();
+  if constexpr (!FAST) {
+    load_tables(&T, prog.tables);
+    __syncthreads();
+  }
+  const bool vec = (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
   const int groups = (C + 15) / 16;
   const int64_t total = static_cast<int64_t>(N) * OH * OW * groups;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -126,16 +130,34 @@ __global__ void avgpool_f32_kernel(const float* __restrict__ x, int ld, int N, i
         const int iw = ow * sw - pw + b;
         if (iw < 0 || iw >= W) continue;
         const float* src = x + ((n * H + ih) * W + iw) * ld + c0;
+        if (vec && nvalid == 16) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          if (j < nvalid) acc[j] = __fma_rn(static_cast<double>(__ldg(src + j)), wk, acc[j]);
+          for (int q = 0; q < 4; ++q) {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(src) + q);
+            acc[4 * q + 0] = __fma_rn(static_cast<double>(f.x), wk, acc[4 * q + 0]);
+            acc[4 * q + 1] = __fma_rn(static_cast<double>(f.y), wk, acc[4 * q + 1]);
+            acc[4 * q + 2] = __fma_rn(static_cast<double>(f.z), wk, acc[4 * q + 2]);
+            acc[4 * q + 3] = __fma_rn(static_cast<double>(f.w), wk, acc[4 * q + 3]);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (j < nvalid) acc[j] = __fma_rn(static_cast<double>(__ldg(src + j)), wk, acc[j]);
+          }
         }
       }
     }
     float v[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = __double2float_rn(acc[j]);
-    run_prog<16, 3>(v, m, c0, nvalid, T);
+    if constexpr (FAST) {
+      if (fast.n == 2) sq_values<16>(v, fast.fa);
+      float q[16];
+      sq_codes<16>(v, q, fast.fs);
+      store_codes<16>(fast.buf, m, c0, nvalid, q, nullptr, 0);
+    } else {
+      run_prog<16, 3>(v, m, c0, nvalid, T);
+    }
   }
 }
 
@@ -744,11 +766,16 @@ void stage_maxpool(const int8_t* x, int ld, float scale, int N, int C, int H, in
 
 void stage_avgpool_f32(const float* x, int ld, int N, int C, int H, int W, int OH, int OW, int kh,
                        int kw, int sh, int sw, int ph, int pw, double wk, const ProgArgs& prog,
-                       cudaStream_t s) {
+                       const DwFast& fast, cudaStream_t s) {
   const int64_t total = static_cast<int64_t>(N) * OH * OW * ((C + 15) / 16);
   if (total <= 0) return;
-  launch_pdl(avgpool_f32_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, x, ld, N, C, H, W, OH, OW,
-             kh, kw, sh, sw, ph, pw, wk, prog);
+  if (fast.n > 0) {
+    launch_pdl(avgpool_f32_kernel<true>, dim3(grid_for(total, 256)), dim3(256), 0, s, x, ld, N, C, H, W, OH,
+               OW, kh, kw, sh, sw, ph, pw, wk, prog, fast);
+  } else {
+    launch_pdl(avgpool_f32_kernel<false>, dim3(grid_for(total, 256)), dim3(256), 0, s, x, ld, N, C, H, W,
+               OH, OW, kh, kw, sh, sw, ph, pw, wk, prog, fast);
+  }
   QC_CUDA_CHECK_LAUNCH();
 }
 
