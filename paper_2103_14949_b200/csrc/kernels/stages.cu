@@ -39,7 +39,8 @@ __global__ void input_kernel(const float* __restrict__ x, int N, int C, int HW, 
   }
 }
 
-__global__ void maxpool_codes_kernel(const int8_t* __restrict__ x, int ld, float scale, int N,
+template <int DEPTH>
+__global__ void __launch_bounds__(256) maxpool_codes_kernel(const int8_t* __restrict__ x, int ld, float scale, int N,
                                      int C, int H, int W, int OH, int OW, int kh, int kw, int sh,
                                      int sw, int ph, int pw, ProgArgs prog) {
   pdl_trigger();
@@ -88,7 +89,7 @@ __global__ void maxpool_codes_kernel(const int8_t* __restrict__ x, int ld, float
     for (int j = 0; j < 16; ++j) {
       v[j] = any ? __fmul_rn(static_cast<float>(best[j]), scale) : -FLT_MAX;
     }
-    run_prog<16, 3>(v, m, c0, nvalid, T);
+    run_prog<16, DEPTH>(v, m, c0, nvalid, T);
   }
 }
 
@@ -361,7 +362,10 @@ __global__ void maxpool_stores_kernel(const int8_t* __restrict__ x, int ld, int 
   }
 }
 
-__global__ void ew_kernel(ProgBuf src, int64_t M, int C, ProgArgs prog) {
+// DEPTH: the program's push depth (prog.depth); a shallow program needs
+// fewer stack registers, so more warps stay resident
+template <int DEPTH>
+__global__ void __launch_bounds__(256) ew_kernel(ProgBuf src, int64_t M, int C, ProgArgs prog) {
   pdl_trigger();
   pdl_wait();
   __shared__ StageTables T;
@@ -377,7 +381,7 @@ __global__ void ew_kernel(ProgBuf src, int64_t M, int C, ProgArgs prog) {
     const int nvalid = C - c0 < 16 ? C - c0 : 16;
     float v[16];
     load_values<16>(src, m, c0, nvalid, v);
-    run_prog<16, 3>(v, m, c0, nvalid, T);
+    run_prog<16, DEPTH>(v, m, c0, nvalid, T);
   }
 }
 
@@ -759,8 +763,13 @@ void stage_maxpool(const int8_t* x, int ld, float scale, int N, int C, int H, in
                    cudaStream_t s) {
   const int64_t total = static_cast<int64_t>(N) * OH * OW * ((C + 15) / 16);
   if (total <= 0) return;
-  launch_pdl(maxpool_codes_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, x, ld, scale, N, C, H, W, OH, OW, kh,
-                                                            kw, sh, sw, ph, pw, prog);
+  if (prog.depth <= 1) {
+    launch_pdl(maxpool_codes_kernel<1>, dim3(grid_for(total, 256)), dim3(256), 0, s, x, ld, scale, N, C, H, W, OH,
+               OW, kh, kw, sh, sw, ph, pw, prog);
+  } else {
+    launch_pdl(maxpool_codes_kernel<3>, dim3(grid_for(total, 256)), dim3(256), 0, s, x, ld, scale, N, C, H, W, OH,
+               OW, kh, kw, sh, sw, ph, pw, prog);
+  }
   QC_CUDA_CHECK_LAUNCH();
 }
 
@@ -851,7 +860,13 @@ void stage_maxpool_stores(const int8_t* x, int ld, int N, int C, int H, int W, i
 void stage_ew(const ProgBuf& src, int64_t M, int C, const ProgArgs& prog, cudaStream_t s) {
   const int64_t total = M * ((C + 15) / 16);
   if (total <= 0) return;
-  launch_pdl(ew_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, src, M, C, prog);
+  if (prog.depth <= 1) {
+    launch_pdl(ew_kernel<1>, dim3(grid_for(total, 256)), dim3(256), 0, s, src, M, C, prog);
+  } else if (prog.depth == 2) {
+    launch_pdl(ew_kernel<2>, dim3(grid_for(total, 256)), dim3(256), 0, s, src, M, C, prog);
+  } else {
+    launch_pdl(ew_kernel<3>, dim3(grid_for(total, 256)), dim3(256), 0, s, src, M, C, prog);
+  }
   QC_CUDA_CHECK_LAUNCH();
 }
 
